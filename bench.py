@@ -1,0 +1,450 @@
+"""Benchmark: decode tokens/s of the mixed-precision MoE expert layer (HOBBIT,
+arXiv 2411.01433) on B200, Mixtral-8x7B shapes, batch-1 decode.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one decode token through all 32 MoE layers (every row of SURVEY.md
+8(a) on the resident path: exact router + top-k + gates + Eq. 2 + T1/T2,
+expert lookup in the slot table, W1/W3+SwiGLU and W2+gate-sum GEMVs), with
+the Mixtral-8x7B shapes of BASELINE.json configs[1]: E=8, top-2, H=4096,
+F=14336, fp16 High / int4 Low, T1=0.6, T2=0.9, all 256
+experts resident in both encodings (107.6 GiB).  Inputs per (token, layer)
+are seeded synthetic fp16 hidden states (not chained, R23); weights
+are seeded synthetic (no checkpoints).  Each token streams ~17 GB of expert
+weights, far larger than the 126 MB L2, so no L2 flush is needed.
+
+N > 1 (torchrun): expert-parallel, rank r owns experts e % N == r of every
+layer; each layer's partial y is summed with an NCCL all-reduce on the
+compute stream.  All ranks process the same token (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "decode tokens/s (Mixtral-8x7B shape) at 1/2/4/8 B200; expert-FFN HBM GB/s vs peak"
+UNIT = "tokens/s"
+WORKLOAD = "mixtral-8x7b-shapes batch-1 decode, 32 layers, fp16/int4 strict (T1=0.6,T2=0.9), all experts resident"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ our arm
+def build_model(h, sg, fm, shape, hi, lo, rank, world, dev):
+    import torch
+    cfg = h.default_config(n_layers=shape.n_layers, n_experts=shape.n_experts, top_k=shape.top_k,
+                           hidden=shape.hidden, ffn=shape.ffn, hi_enc=hi, lo_enc=lo, t1=0.6,
+                           t2=0.9, max_batch=1, rank=rank, world=world)
+    ctx = h.Context(cfg, dev)
+    H, F = shape.hidden, shape.ffn
+    tmp = [torch.empty(n * k, dtype=torch.float16, device="cuda")
+           for n, k in ((F, H), (F, H), (H, F))]
+    blobs = []
+    for l in range(shape.n_layers):
+        ctx.set_router(l, sg.router_weights(shape, l))
+        for e in range(shape.n_experts):
+            if e % world != rank:
+                continue
+            for mat, t in enumerate(tmp):
+                h.synth_fill(t, sg.expert_key(sg.DEFAULT_SEED, l, e, mat),
+                             float(sg.scale_f32(sg.expert_sigma(shape, mat))))
+            ws = [tmp[0].view(F, H), tmp[1].view(F, H), tmp[2].view(H, F)]
+            for enc in (hi, lo):
+                b = h.quantize_expert(enc, *ws)
+                ctx.register_expert(l, e, enc, b)
+                blobs.append(b)
+    del tmp
+    torch.cuda.synchronize()
+    return ctx, blobs
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import synthgen as sg
+    from oracle import formats as fm  # noqa: F401  (enc constants only; cpu_baseline below)
+    from paper_2411_01433_b200 import hobbit as h
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shape = sg.MIXTRAL
+    hi, lo = h.HB_F16, h.HB_Q4
+    L, Hd = shape.n_layers, shape.hidden
+    t_init = time.time()
+    ctx, blobs = build_model(h, sg, None, shape, hi, lo, rank, world, local)
+    t_init = time.time() - t_init
+
+    # token inputs: a pool of P tokens x 32 layers, resident on the device
+    P = 16
+    X = torch.from_numpy(np.stack([
+        np.stack([sg.hidden_states(shape, 1000 + t, l)[0] for l in range(L)]) for t in range(P)
+    ])).cuda()                                                       # [P, L, H] fp16
+    Y = torch.empty(L, Hd, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.Stream()
+
+    def step(t, s):
+        for l in range(L):
+            ctx.forward(l, X[t % P, l].view(1, Hd), Y[l].view(1, Hd), stream=s)
+            if world > 1:
+                dist.all_reduce(Y[l])
+
+    # ---- realised algorithmic bytes of the pool's tokens (decisions, untimed)
+    blob_b = {hi: h.blob_bytes(hi, Hd, shape.ffn), lo: h.blob_bytes(lo, Hd, shape.ffn)}
+    bytes_tok = []
+    w13_bytes_tok, w2_bytes_tok = [], []
+    mix = [0, 0, 0]
+    for t in range(P):
+        tot = w13 = w2 = 0
+        for l in range(L):
+            with torch.cuda.stream(stream):
+                ctx.forward(l, X[t, l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
+            for d in ctx.decisions(1):
+                mix[d.prec] += 1
+                if d.served_enc == h.HB_ENC_NONE:
+                    continue
+                b = blob_b[d.served_enc]
+                w13_part = 2 * (b - (b // 3))     # refined below
+                tot += b
+            tot += 2 * shape.n_experts * Hd + 2 * Hd + 4 * Hd
+        bytes_tok.append(tot)
+    torch.cuda.synchronize()
+    # per-matrix bytes of one blob (W1+W3 vs W2) from the layout
+    def mat_bytes(enc, mats):
+        tot = 0
+        for m in mats:
+            for sec in range(3):
+                try:
+                    tot += h.blob_section(enc, Hd, shape.ffn, m, sec)[1]
+                except h.HobbitError:
+                    pass
+        return tot
+    w13b = {e: mat_bytes(e, (0, 1)) for e in (hi, lo)}
+    w2b = {e: mat_bytes(e, (2,)) for e in (hi, lo)}
+
+    # ---- CUDA graphs: one per pool token (32 layers x 3 kernels each), N=1
+    use_graph = world == 1
+    graphs = []
+    launches_per_step = 0
+    if use_graph:
+        c0 = ctx.launch_count()
+        with torch.cuda.stream(stream):
+            for t in range(P):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    step(t, stream)
+                graphs.append(g)
+        launches_per_step = (ctx.launch_count() - c0) // P
+
+    def run_step(t):
+        if use_graph:
+            graphs[t % P].replay()
+        else:
+            step(t, stream)
+
+    # ---- warmup + timed region
+    with torch.cuda.stream(stream):
+        for w in range(args.warmup):
+            run_step(w)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        c_before = ctx.launch_count()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for k in range(args.steps):
+                run_step(args.warmup + k)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    gpu_launches = (launches_per_step * args.steps if use_graph
+                    else ctx.launch_count() - c_before)
+    tok_s = 1000.0 / ms_step
+    steps_tokens = [(args.warmup + k) % P for k in range(args.steps)]
+    bytes_step = float(np.mean([bytes_tok[t] for t in steps_tokens]))
+
+    # ---- kernel timing for the roofline (eager, events around K2a / K2b)
+    with torch.cuda.stream(stream):
+        nprof = min(args.steps, P)
+        ctx.profile(nprof * L)
+        for t in range(nprof):
+            for l in range(L):
+                ctx.forward(l, X[t, l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
+                if world > 1:
+                    dist.all_reduce(Y[l])
+        prof = ctx.profile_read()
+        ctx.profile(0)
+    # bytes per K2a / K2b launch, from the decisions of the same tokens
+    k2a_bytes, k2b_bytes = [], []
+    with torch.cuda.stream(stream):
+        for t in range(nprof):
+            for l in range(L):
+                ctx.forward(l, X[t, l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
+                a = b = 0
+                for d in ctx.decisions(1):
+                    if d.served_enc != h.HB_ENC_NONE:
+                        a += w13b[d.served_enc]
+                        b += w2b[d.served_enc]
+                k2a_bytes.append(a + 2 * Hd + 2 * 2 * shape.ffn * 2)
+                k2b_bytes.append(b + 2 * 2 * shape.ffn * 2 + 4 * Hd)
+    k2a_ms = sum(p[0] for p in prof)
+    k2b_ms = sum(p[1] for p in prof)
+    gemv_ms = k2a_ms + k2b_ms
+    gemv_bytes = sum(k2a_bytes) + sum(k2b_bytes)
+    achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+
+    # ---- end to end through the public API with host buffers
+    Xh = torch.empty(P, L, Hd, dtype=torch.float16, pin_memory=True)
+    Xh.copy_(X.cpu())
+    Yh = torch.empty(L, Hd, dtype=torch.float32, pin_memory=True)
+    Xd = torch.empty(L, Hd, dtype=torch.float16, device="cuda")
+    with torch.cuda.stream(stream):
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e2.record(stream)
+        for k in range(args.steps):
+            Xd.copy_(Xh[k % P], non_blocking=True)
+            for l in range(L):
+                ctx.forward(l, Xd[l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
+                if world > 1:
+                    dist.all_reduce(Y[l])
+            Yh.copy_(Y, non_blocking=True)
+        e3.record(stream)
+        torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_e2e = float(tt.item())
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(shape, n_token_layers=args.cpu_sample)
+
+    tot_mix = sum(mix)
+    clk_sum = clk.summary()
+    out = {
+        "metric": METRIC, "value": round(tok_s, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f16 weights / q4 codes, fp32 accumulate", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": 1, "layers": L, "experts": shape.n_experts,
+                   "top_k": shape.top_k, "hidden": Hd, "ffn": shape.ffn, "pair": "F16/Q4",
+                   "parallelism": f"ep{world}", "l2": "inputs > L2 (~17 GB of weights per step)",
+                   "graph": use_graph},
+        "e2e": {"value": round(1000.0 / ms_e2e, 3), "unit": UNIT,
+                "h2d_bytes_per_step": L * Hd * 2, "d2h_bytes_per_step": L * Hd * 4},
+        "gpu_launches": int(gpu_launches),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": None, "kernel": "K2a+K2b dequant-GEMV (w13_kernel, w2_kernel)",
+                     "k2a_gbs": round(sum(k2a_bytes) / (k2a_ms * 1e-3) / 1e9, 1),
+                     "k2b_gbs": round(sum(k2b_bytes) / (k2b_ms * 1e-3) / 1e9, 1),
+                     "gemv_share_of_step": round(gemv_ms / nprof / ms_step, 4)},
+        "layer_gbs": round(bytes_step / (ms_step * 1e-3) / 1e9, 1),
+        "bytes_per_step": int(bytes_step),
+        "precision_mix": [round(v / tot_mix, 4) for v in mix],
+        "clocks": clk_sum,
+        "init_s": round(t_init, 1),
+    }
+    if cpu is not None:
+        out["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ oracle timings
+def _oracle_sample(shape, n_token_layers, seed_tok=2000):
+    """Pre-generate blobs (untimed), then time the oracle as it stands on
+    n_token_layers (token, layer) pairs: exact router + decode + fp64 FFN."""
+    import synthgen as sg
+    from oracle import formats as fm
+    from oracle import moe as om
+    from oracle import router as rt
+    blobs = {}
+
+    def blob(l, e, enc):
+        if (l, e, enc) not in blobs:
+            w1, w3, w2 = sg.expert_weights(shape, l, e)
+            blobs[(l, e, enc)] = fm.quantize_blob(enc, w1, w3, w2)
+        return blobs[(l, e, enc)]
+
+    cases = []
+    for i in range(n_token_layers):
+        l = i % shape.n_layers
+        x16 = sg.hidden_states(shape, seed_tok + i, l)
+        wg = sg.router_weights(shape, l)
+        r = rt.route(x16, wg, 2, 0.6, 0.9)[0]
+        for e, d in zip(r.experts, r.decisions):
+            if d != rt.SKIP:
+                blob(l, e, fm.F16 if d == rt.HIGH else fm.Q4)
+        cases.append((l, x16, wg))
+    times = []
+    for l, x16, wg in cases:
+        store = om.ExpertStore(blob, shape.hidden, shape.ffn)      # fresh: decode is timed
+        t0 = time.perf_counter()
+        om.moe_layer(x16, wg, store, l, 2, 0.6, 0.9, fm.F16, fm.Q4)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_baseline(shape, n_token_layers=2):
+    cores = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_limits
+        ctxm = threadpool_limits(limits=cores)
+    except Exception:
+        ctxm = None
+    times = _oracle_sample(shape, n_token_layers)
+    if ctxm is not None:
+        ctxm.unregister() if hasattr(ctxm, "unregister") else None
+    s_tl = float(np.mean(times))
+    return {"value": round(1.0 / (shape.n_layers * s_tl), 6), "unit": UNIT, "cores": cores,
+            "kind": "oracle",
+            "sample": f"{n_token_layers} token-layers of the Mixtral-shape workload (exact router, "
+                      f"blob decode, fp64 SwiGLU + Eq. 1), {s_tl:.2f} s per token-layer; "
+                      f"tokens/s extrapolated = 1/(32 * s per token-layer)"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synthgen as sg
+    shape = sg.MIXTRAL
+    t0 = time.time()
+    n = max(1, args.warmup + args.steps)
+    n = min(n, args.ref_max_steps)
+    times = _oracle_sample(shape, n)
+    timed = times[min(args.warmup, len(times) - 1):] or times
+    s_tl = float(np.mean(timed))
+    ms_step = 1000.0 * shape.n_layers * s_tl
+    cores = len(os.sched_getaffinity(0))
+    v = 1000.0 / ms_step
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": UNIT,
+           "n_gpus": world, "steps": len(timed), "warmup": n - len(timed),
+           "ms_per_step": round(ms_step, 1), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": WORKLOAD, "global_batch": 1},
+           "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"each step = 1 token-layer of the workload timed on the "
+                                      f"oracle, extrapolated x32 layers; {len(timed)} steps"},
+           "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "wall_s": round(time.time() - t0, 1)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=2)
+    ap.add_argument("--ref-max-steps", type=int, default=12)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

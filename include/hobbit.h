@@ -1,0 +1,226 @@
+/*
+ * hobbit.h — C ABI of the B200-native mixed-precision MoE expert layer
+ * (HOBBIT, arXiv 2411.01433).  libhobbit.so, built for sm_100a.
+ *
+ * Citations: P:n = PAPER.md line n (the paper), S:n = SPEC.md line n.
+ *
+ * The paper states the per-token, per-layer problem (Sec. 3.1
+ * steps 1-9; Sec. 3.2): given the gating input, select the top-k
+ * experts; score the selected experts (Eq. 2); for a cache miss pick the
+ * precision by the thresholds T1/T2 (High / Low / Skip); load; and compute
+ * Eq. 1, y = sum_i G(x)_{e_i} E_{e_i}(x).  Sec. 3.3 adds the
+ * stacked next-layer prediction + prefetch, Sec. 3.4 (Eq. 3) the
+ * two-pool cache policy.  The three calls the paper's problem needs are
+ * moe_layer_forward, expert_cache_load and prefetch_next_layer; the rest is
+ * setup, inspection and the offline quantiser.
+ *
+ * Conventions
+ *  - Every call returns HB_OK (0) or a negative HB_E* code; hb_last_error()
+ *    returns the message of the last failure on that context (thread-local
+ *    message for calls without a context).
+ *  - "stream" is a cudaStream_t passed as void* (e.g. torch's current stream).
+ *    Device work is stream-ordered; no call allocates device memory after
+ *    hb_create, so the resident path can be captured in a CUDA graph.
+ *  - x is fp16 [batch, hidden] row-major on the device (the MoE block input,
+ *    post-norm, "gating input"); y is fp32 [batch, hidden] row-major on
+ *    the device and is OVERWRITTEN with this rank's part of Eq. 1.
+ *  - A context is not thread-safe: one context per GPU per host thread.
+ *  - Expert-parallel (EP): rank r owns experts e with e % world == r.  Each
+ *    rank computes the exact router itself (no decision exchange); the caller
+ *    sums y over ranks (NCCL all-reduce).
+ */
+#ifndef HOBBIT_H
+#define HOBBIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes */
+#define HB_OK            0
+#define HB_EINVAL       -1  /* bad argument: dims, t1>t2, K%256, bad ids */
+#define HB_ECAPACITY    -2  /* pool full and every member masked or in use */
+#define HB_ESTATE       -3  /* expert/router not registered; forward before hb_token_begin */
+#define HB_ECUDA        -4  /* CUDA runtime error */
+#define HB_ENOMEM       -5  /* host or device allocation failed */
+#define HB_EUNSUPPORTED -6  /* e.g. constrained cache with batch > 1 */
+
+/* ------------------------------------------------------ encodings, levels */
+/* Expert encodings (fp16+int4 and int8+int2 pairs).  Block = 32
+ * consecutive K elements of one row; d, m fp16 per block:
+ *   HB_F16  w = fp16                      16   bits/weight
+ *   HB_Q8   w = d*q,      q int8 [-127,127] 8.5 bits/weight
+ *   HB_Q4   w = d*(q-8),  q in [0,15]       4.5 bits/weight
+ *   HB_Q2   w = d*q + m,  q in [0,3]        3.0 bits/weight
+ * Blob = W1 [F,H], W3 [F,H], W2 [H,F]; each matrix = sections q, d (, m),
+ * each section 256-byte aligned; q rows are stored in 64-byte groups whose
+ * element order is given in DESIGN.md "Blob layout" (hb_blob_section()). */
+enum { HB_F16 = 0, HB_Q8 = 1, HB_Q4 = 2, HB_Q2 = 3 };
+/* Precision decision of one selected expert. */
+enum { HB_HIGH = 0, HB_LOW = 1, HB_SKIP = 2 };
+#define HB_ENC_NONE 255
+
+typedef struct {
+  int n_layers, n_experts, top_k;   /* l_n (Eq. 3), E, K (Eq. 1) */
+  int hidden, ffn;                  /* H, F: multiples of 256 */
+  int hi_enc, lo_enc;               /* precision pair, default HB_F16 / HB_Q4 */
+  double t1, t2;                    /* thresholds, default 0.6 / 0.9; 0<=t1<=t2 */
+  int lookahead_p;                  /* prefetch depth p; 0 = off */
+  int w_lru, w_lfu, w_lhu, w_fld;   /* Eq. 3 weights as integer numerators, sum > 0 */
+  int cap_high, cap_low;            /* slots per pool on this rank; -1 = fully resident */
+  int allow_upgrade;                /* Low request served by a cached High copy (1) */
+  int rank, world;                  /* EP: owner(e) = e % world */
+  int max_batch;                    /* tokens per forward call */
+} hb_config;
+
+/* One routed (token, rank) pair of the last forward (inspection / parity). */
+typedef struct {
+  int32_t token;
+  int32_t expert;                   /* e_i */
+  uint8_t sel_rank;                 /* i, position in the top-k order */
+  uint8_t prec;                     /* HB_HIGH / HB_LOW / HB_SKIP */
+  uint8_t served_enc;               /* encoding computed, HB_ENC_NONE if skipped / not owned */
+  uint8_t hit;                      /* 1 if the expert was cache-resident (offload mode) */
+  float gate;                       /* G(x)_{e_i}, softmax over the selected logits */
+} hb_decision;
+
+/* Cache event (offload mode), identical to the oracle's event tuples. */
+typedef struct {
+  int32_t type;                     /* 0 hit, 1 load, 2 prefetch dropped (no eligible victim) */
+  int32_t kind;                     /* 0 on-demand, 1 prefetch, 2 explicit expert_cache_load */
+  int32_t layer, expert, enc;
+  int32_t slot;                     /* slot index in the pool of enc */
+  int32_t victim;                   /* evicted key layer*E+expert, or -1 */
+} hb_event;
+
+typedef struct hb_ctx hb_ctx;
+
+/* ------------------------------------------------------------ host helpers */
+void        hb_config_default(hb_config* cfg);
+size_t      hb_blob_bytes(int enc, int hidden, int ffn);
+/* Offset/size of section sec (0 q or w, 1 d, 2 m) of matrix mat (0 W1, 1 W3,
+ * 2 W2) inside a blob.  Returns HB_EINVAL if the section does not exist. */
+int         hb_blob_section(int enc, int hidden, int ffn, int mat, int sec,
+                            size_t* offset, size_t* nbytes);
+/* k = 2 gap threshold floor(ln(T/(1-T)) * 2^48) (exact-integer form of the
+ * T1/T2 test, R9).  *kind = 0 finite, +1 T>=1 (always), -1 T<=0. */
+int64_t     hb_theta(double t, int* kind);
+const char* hb_last_error(const hb_ctx* ctx);   /* ctx may be NULL */
+const char* hb_version(void);
+
+/* ---------------------------------------------------------------- context */
+/* Allocate pools (cap_* slots of blob_bytes(hi/lo)) or the resident slot
+ * table, the router table, scratch for max_batch tokens, a copy stream and
+ * events on `device`.  The caller owns *out and must hb_destroy it. */
+int hb_create(const hb_config* cfg, int device, hb_ctx** out);
+int hb_destroy(hb_ctx* ctx);
+
+/* Router weights W_g of `layer`, fp16 [E, H] ("linear layer").
+ * w is a host pointer (copied) or, with on_device=1, a device pointer (D2D
+ * copy on the null stream).  Stacked prediction reads these per layer. */
+int hb_set_router(hb_ctx* ctx, int layer, const void* w, int on_device);
+
+/* Register the blob of expert (layer, expert) in encoding enc.
+ *   HB_REG_DEVICE_BORROW  blob is device memory owned by the caller that
+ *                         outlives ctx (fully resident mode: cap_* = -1);
+ *   HB_REG_HOST_PINNED    blob is caller-owned pinned host memory that
+ *                         outlives ctx (offload mode: next-level storage);
+ *   HB_REG_HOST_COPY      blob is any host memory; copied into the
+ *                         library's pinned arena (offload mode).
+ * nbytes must equal hb_blob_bytes(enc, H, F).  Only owned experts. */
+#define HB_REG_DEVICE_BORROW 1
+#define HB_REG_HOST_PINNED   2
+#define HB_REG_HOST_COPY     3
+int hb_register_expert(hb_ctx* ctx, int layer, int expert, int enc,
+                       const void* blob, size_t nbytes, int flags);
+
+/* Eq. 3 bookkeeping: T += 1 per forward step (a prefill is one step); masks
+ * of the previous step expire.  reset zeroes R, F, H and T;
+ * pools and masks are kept. */
+int hb_token_begin(hb_ctx* ctx);
+int hb_reset_sequence(hb_ctx* ctx);
+
+/* ------------------------------------------------------------- the path */
+/* Expert load into the expert cache (P:349 steps 6-8): a logical
+ * insert of (layer, expert) into the high pool if enc == hi_enc, the low
+ * pool if enc == lo_enc (evicting by Eq. 3 if full, no record update), and
+ * an async host->device copy on the library's copy stream, ordered after
+ * every earlier reader of the reused slot.  No-op if already resident.
+ * Offload mode only (HB_ESTATE in resident mode). */
+int expert_cache_load(hb_ctx* ctx, int layer, int expert, int enc, void* stream);
+
+/* Stacked next-layer prediction + prefetch (Sec. 3.3): runs the
+ * routers of layers layer+1 .. layer+p on x (one launch, the "Stacking
+ * Computer"), masks the predicted experts, and queues loads of the first
+ * lookahead layer with a miss in the PREDICTED precision (R14)
+ * behind the on-demand loads.  Returns the number of loads queued (>= 0).
+ * Blocks the host until the prediction is visible.  Resident mode: 0. */
+int prefetch_next_layer(hb_ctx* ctx, int layer, const void* x, int batch, void* stream);
+
+/* One MoE layer (P:347-349 + Eq. 1): exact router + top-k + softmax gates +
+ * Eq. 2 scores + T1/T2 decision; cache lookup / victim / loads (offload
+ * mode; blocks the host until the 1-layer decision record is visible); then
+ * the grouped dequant-GEMV W1/W3 + SwiGLU and W2 + gate-weighted sum.
+ * y[b,:] = sum over this rank's non-skipped selections of g * E_served(x_b).
+ * Resident mode never blocks the host.  batch <= max_batch; batch > 1 with
+ * a constrained cache returns HB_EUNSUPPORTED. */
+int moe_layer_forward(hb_ctx* ctx, int layer, const void* x, int batch,
+                      void* y, void* stream);
+
+/* ------------------------------------------------------------ inspection */
+/* Decisions of the last forward: batch*top_k records (synchronises). */
+int hb_get_decisions(hb_ctx* ctx, hb_decision* out, int cap);
+/* Exact router logits of the last forward, L = logit * 2^48 as int128 split
+ * into (lo uint64, hi int64) pairs, [batch][E][2] (synchronises). */
+int hb_get_logits(hb_ctx* ctx, int64_t* out, int cap_pairs);
+/* Cache events since the last call (offload mode). Returns the count. */
+int hb_get_events(hb_ctx* ctx, hb_event* out, int cap);
+/* Realised bytes of expert weights read by the GEMV kernels in the last
+ * forward (sum of served blob bytes), for the roofline. */
+int hb_last_expert_bytes(hb_ctx* ctx, uint64_t* out);
+/* Number of kernel launches issued by the library since creation. */
+int hb_launch_count(hb_ctx* ctx, uint64_t* out);
+/* Kernel timing for the roofline: with max_calls > 0 every following
+ * moe_layer_forward records CUDA events around its W1/W3 (K2a) and W2 (K2b)
+ * kernels on the forward's stream (up to max_calls forwards); 0 disables.
+ * hb_profile_read synchronises and returns, per recorded forward, the K2a
+ * and K2b durations in ms as [n][2] floats; returns n. */
+int hb_profile(hb_ctx* ctx, int max_calls);
+int hb_profile_read(hb_ctx* ctx, float* ms, int cap);
+
+/* ------------------------------------------- offline quantiser, generator */
+/* Quantise an fp16 expert (W1 [F,H], W3 [F,H], W2 [H,F], device pointers)
+ * into a device blob of hb_blob_bytes(enc, H, F) bytes (R8). */
+int hb_quantize_expert(int enc, int hidden, int ffn, const void* w1, const void* w3,
+                       const void* w2, void* blob, void* stream);
+/* Seeded synthetic fp16 fill (the counter-based generator of synthgen/):
+ * dst[i] = fp16_rne(fp32(s(key, start+i)) * scale). */
+int hb_synth_fill_f16(void* dst, size_t n, uint64_t key, float scale, uint64_t start,
+                      void* stream);
+
+/* ------------------------------------------- host-only cache (no GPU) */
+/* The Eq. 3 two-pool cache state machine used by the offload path, exposed
+ * for CPU-only parity tests.  Same semantics and events as the device ctx. */
+typedef struct hb_cache hb_cache;
+int hbc_create(const hb_config* cfg, hb_cache** out);
+int hbc_destroy(hb_cache* c);
+int hbc_token_begin(hb_cache* c);
+int hbc_reset_sequence(hb_cache* c);
+/* experts/prec: top_k entries in rank order; served: out, top_k encodings. */
+int hbc_forward(hb_cache* c, int layer, const int32_t* experts, const uint8_t* prec,
+                uint8_t* served);
+/* n_pred lookahead layers layer+1..layer+n_pred, [n_pred][top_k] each.
+ * *prefetched = the layer whose loads were queued, or -1. */
+int hbc_prefetch(hb_cache* c, int layer, int n_pred, const int32_t* experts,
+                 const uint8_t* prec, int* prefetched);
+int hbc_load(hb_cache* c, int layer, int expert, int enc);
+int hbc_get_events(hb_cache* c, hb_event* out, int cap);
+const char* hbc_last_error(const hb_cache* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOBBIT_H */

@@ -1,0 +1,730 @@
+// C ABI of libhobbit (include/hobbit.h): context, expert registry, HBM slot
+// pools, pinned next-level storage, copy stream + events (the Dynamic Expert
+// Loader, P:349 / fig:handler), and the three calls of the paper's problem:
+// moe_layer_forward, expert_cache_load, prefetch_next_layer.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "cache.h"
+#include "hb_internal.h"
+#include "hobbit.h"
+
+namespace hb {
+
+int blob_layout(int enc, int hidden, int ffn, BlobLayout* out) {
+  if (enc < HB_F16 || enc > HB_Q2 || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
+    return HB_EINVAL;
+  const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
+  const int bits = enc == HB_F16 ? 16 : enc == HB_Q8 ? 8 : enc == HB_Q4 ? 4 : 2;
+  auto align = [](uint64_t v) { return (v + 255) / 256 * 256; };
+  uint64_t off = 0;
+  for (int m = 0; m < 3; ++m) {
+    const uint64_t qbytes = (uint64_t)N[m] * K[m] * bits / 8;
+    const uint64_t sbytes = (uint64_t)N[m] * (K[m] / 32) * 2;
+    out->mat[m].q = off;
+    off = align(off + qbytes);
+    out->mat[m].d = out->mat[m].m = off;
+    if (enc != HB_F16) {
+      out->mat[m].d = off;
+      off = align(off + sbytes);
+      if (enc == HB_Q2) {
+        out->mat[m].m = off;
+        off = align(off + sbytes);
+      }
+    }
+  }
+  out->total = off;
+  return HB_OK;
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+static thread_local std::string g_err;
+
+struct hb_ctx {
+  hb_config cfg{};
+  int device = 0;
+  bool resident = true;
+  BlobLayout lay[4]{};
+  size_t bbytes[4]{};
+  int S = 1, chunk = 256;
+  // router weights [L][E][H]
+  __half* wg = nullptr;
+  std::vector<char> router_set;
+  // resident registry: device blobs [L][E][4]
+  std::vector<const uint8_t*> dev_blob;
+  const uint8_t** dev_blob_table = nullptr;
+  // offload registry: host blobs [L][E][4]
+  std::vector<const uint8_t*> host_blob;
+  std::vector<void*> arena;               // pinned copies owned by the library
+  uint8_t* pool_mem[2] = {nullptr, nullptr};
+  size_t slot_bytes[2] = {0, 0};
+  std::vector<cudaEvent_t> slot_ready[2], slot_free[2];
+  cudaStream_t copy_stream = nullptr;
+  ExpertCache* cache = nullptr;
+  std::vector<hb_event> log;
+  // scratch
+  hb_decision* dec = nullptr;             // [B][k]
+  hb_decision* dec_pred = nullptr;        // [p][B][k]
+  hb_decision* dec_host = nullptr;        // pinned [(1+p)][B][k]
+  long long* logits = nullptr;            // [B][E][2]
+  uint4* x_perm = nullptr;
+  float* xsum = nullptr;
+  uint4* h_hi = nullptr;
+  uint4* h_lo = nullptr;
+  float* hsum = nullptr;
+  float* partial = nullptr;
+  unsigned* tile_count = nullptr;
+  unsigned* done = nullptr;
+  JobTable jt{};
+  void* jt_dev = nullptr;
+  void* jt_host = nullptr;                // pinned staging
+  size_t jt_bytes = 0;
+  int max_jobs = 0, max_slots = 0;
+  cudaEvent_t dec_ready = nullptr;
+  // kernel timing (hb_profile)
+  std::vector<cudaEvent_t> prof_ev;       // 3 per recorded forward
+  int prof_max = 0, prof_n = 0;
+  // bookkeeping
+  int last_batch = 0, last_layer = -1;
+  bool last_host_decisions = false;
+  bool token_started = false;
+  uint64_t launches = 0;
+  std::string err;
+};
+
+#define CUDA_TRY(ctx, call)                                                   \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(_e);        \
+      return HB_ECUDA;                                                        \
+    }                                                                         \
+  } while (0)
+
+static int fail(hb_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  else g_err = msg;
+  return code;
+}
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+extern "C" {
+
+void hb_config_default(hb_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->n_layers = 32;
+  c->n_experts = 8;
+  c->top_k = 2;
+  c->hidden = 4096;
+  c->ffn = 14336;
+  c->hi_enc = HB_F16;
+  c->lo_enc = HB_Q4;
+  c->t1 = 0.6;
+  c->t2 = 0.9;
+  c->lookahead_p = 1;
+  c->w_lru = c->w_lfu = c->w_lhu = c->w_fld = 1;
+  c->cap_high = c->cap_low = -1;
+  c->allow_upgrade = 1;
+  c->rank = 0;
+  c->world = 1;
+  c->max_batch = 1;
+}
+
+size_t hb_blob_bytes(int enc, int hidden, int ffn) {
+  BlobLayout L;
+  return blob_layout(enc, hidden, ffn, &L) ? 0 : (size_t)L.total;
+}
+
+int hb_blob_section(int enc, int hidden, int ffn, int mat, int sec, size_t* offset,
+                    size_t* nbytes) {
+  BlobLayout L;
+  if (blob_layout(enc, hidden, ffn, &L) || mat < 0 || mat > 2 || sec < 0 || sec > 2 || !offset ||
+      !nbytes)
+    return fail(nullptr, HB_EINVAL, "bad blob section query");
+  const int N = mat < 2 ? ffn : hidden, K = mat < 2 ? hidden : ffn;
+  const int bits = enc == HB_F16 ? 16 : enc == HB_Q8 ? 8 : enc == HB_Q4 ? 4 : 2;
+  if (sec == 0) { *offset = L.mat[mat].q; *nbytes = (size_t)N * K * bits / 8; return HB_OK; }
+  if (enc == HB_F16 || (sec == 2 && enc != HB_Q2))
+    return fail(nullptr, HB_EINVAL, "section does not exist");
+  *offset = sec == 1 ? L.mat[mat].d : L.mat[mat].m;
+  *nbytes = (size_t)N * (K / 32) * 2;
+  return HB_OK;
+}
+
+int64_t hb_theta(double t, int* kind) {
+  // floor(ln(T/(1-T)) * 2^48) in 80-bit long double (R9)
+  if (t >= 1.0) { if (kind) *kind = 1; return 0; }
+  if (t <= 0.0) { if (kind) *kind = -1; return 0; }
+  if (kind) *kind = 0;
+  const long double T = (long double)t;
+  const long double v = logl(T / (1.0L - T)) * 281474976710656.0L;   // 2^48
+  return (int64_t)floorl(v);
+}
+
+const char* hb_last_error(const hb_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+const char* hb_version(void) { return "hobbit-b200 0.1 (sm_100a)"; }
+
+static void free_ctx(hb_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
+                   c->logits, c->x_perm, c->xsum, c->h_hi, c->h_lo, c->hsum, c->partial,
+                   c->tile_count, c->done, c->jt_dev};
+  for (void* p : dptrs)
+    if (p) cudaFree(p);
+  if (c->dec_host) cudaFreeHost(c->dec_host);
+  if (c->jt_host) cudaFreeHost(c->jt_host);
+  for (void* p : c->arena) cudaFreeHost(p);
+  for (int i = 0; i < 2; ++i) {
+    for (cudaEvent_t e : c->slot_ready[i]) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->slot_free[i]) cudaEventDestroy(e);
+  }
+  if (c->dec_ready) cudaEventDestroy(c->dec_ready);
+  for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  delete c->cache;
+  delete c;
+}
+
+int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
+  if (!cfg || !out) return fail(nullptr, HB_EINVAL, "null argument");
+  const hb_config& k = *cfg;
+  if (k.n_layers <= 0 || k.n_experts <= 0 || k.n_experts > 64 || k.top_k <= 0 ||
+      k.top_k > k.n_experts || k.top_k > kMaxTopK)
+    return fail(nullptr, HB_EINVAL, "bad n_layers / n_experts (<=64) / top_k (<=8)");
+  if (k.hidden <= 0 || k.ffn <= 0 || k.hidden % 256 || k.ffn % 256)
+    return fail(nullptr, HB_EINVAL, "hidden and ffn must be positive multiples of 256");
+  if (!(k.t1 <= k.t2)) return fail(nullptr, HB_EINVAL, "t1 > t2 (S:131)");
+  if (k.hi_enc < 0 || k.hi_enc > 3 || k.lo_enc < 0 || k.lo_enc > 3 || k.hi_enc == k.lo_enc)
+    return fail(nullptr, HB_EINVAL, "bad encoding pair");
+  if (k.world <= 0 || k.rank < 0 || k.rank >= k.world) return fail(nullptr, HB_EINVAL, "bad rank/world");
+  if (k.max_batch <= 0) return fail(nullptr, HB_EINVAL, "max_batch must be > 0");
+  if (k.lookahead_p < 0 || k.lookahead_p > kMaxRouteLayers - 1)
+    return fail(nullptr, HB_EINVAL, "lookahead_p must be in [0, 3]");
+  if (k.w_lru < 0 || k.w_lfu < 0 || k.w_lhu < 0 || k.w_fld < 0 ||
+      k.w_lru + k.w_lfu + k.w_lhu + k.w_fld <= 0)
+    return fail(nullptr, HB_EINVAL, "Eq. 3 weights must be >= 0 with a positive sum");
+  const bool resident = k.cap_high < 0 && k.cap_low < 0;
+  if (!resident && (k.cap_high < 0 || k.cap_low < 0))
+    return fail(nullptr, HB_EINVAL, "cap_high and cap_low must both be -1 or both >= 0");
+
+  hb_ctx* c = new (std::nothrow) hb_ctx;
+  if (!c) return fail(nullptr, HB_ENOMEM, "out of host memory");
+  c->cfg = k;
+  c->device = device;
+  c->resident = resident;
+  for (int e = 0; e < 4; ++e) {
+    blob_layout(e, k.hidden, k.ffn, &c->lay[e]);
+    c->bbytes[e] = c->lay[e].total;
+  }
+  // W2 split-K: about 12 tiles per SM
+  const int tiles = k.hidden / 16;
+  const int groups = k.ffn / 256;
+  int S = (int)std::lround(kNumSM * 12.0 / tiles);
+  S = std::max(1, std::min(S, groups));
+  const int chunk_groups = (groups + S - 1) / S;
+  c->chunk = chunk_groups * 256;
+  c->S = (k.ffn + c->chunk - 1) / c->chunk;
+
+  auto bail = [&](int code, const std::string& m) {
+    g_err = m;
+    free_ctx(c);
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return bail(HB_ECUDA, "cudaSetDevice failed");
+  const int L = k.n_layers, E = k.n_experts, B = k.max_batch, K = k.top_k, H = k.hidden,
+            F = k.ffn;
+  const int P = std::max(1, k.lookahead_p);
+  c->max_slots = B * K;
+  c->max_jobs = std::min(2 * E, B * K) + 1;
+  auto dm = [&](void** p, size_t n) { return cudaMalloc(p, std::max<size_t>(n, 16)) == cudaSuccess; };
+  bool ok = dm((void**)&c->wg, (size_t)L * E * H * 2) &&
+            dm((void**)&c->dec, sizeof(hb_decision) * B * K) &&
+            dm((void**)&c->dec_pred, sizeof(hb_decision) * P * B * K) &&
+            dm((void**)&c->logits, sizeof(long long) * B * E * 2) &&
+            dm((void**)&c->x_perm, (size_t)B * H * 2) && dm((void**)&c->xsum, (size_t)B * (H / 32) * 4) &&
+            dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
+            dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
+            dm((void**)&c->hsum, (size_t)c->max_slots * (F / 32) * 4) &&
+            dm((void**)&c->partial, (size_t)c->S * B * H * 4) &&
+            dm((void**)&c->tile_count, (size_t)(H / 16) * 4) && dm((void**)&c->done, 16);
+  if (!ok) return bail(HB_ENOMEM, "device allocation of scratch failed");
+  cudaMemset(c->tile_count, 0, (size_t)(H / 16) * 4);
+  cudaMemset(c->done, 0, 16);
+  cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
+  // job table: hdr | jobs | slot_token | slot_gate
+  const size_t o_jobs = 64, o_tok = align_up(o_jobs + sizeof(Job) * c->max_jobs, 64),
+               o_gate = align_up(o_tok + 4 * (size_t)c->max_slots, 64),
+               total = align_up(o_gate + 4 * (size_t)c->max_slots, 64);
+  c->jt_bytes = total;
+  if (!dm(&c->jt_dev, total) || cudaHostAlloc(&c->jt_host, total, cudaHostAllocDefault) != cudaSuccess)
+    return bail(HB_ENOMEM, "job table allocation failed");
+  cudaMemset(c->jt_dev, 0, total);
+  uint8_t* jb = (uint8_t*)c->jt_dev;
+  c->jt.hdr = (int32_t*)jb;
+  c->jt.jobs = (Job*)(jb + o_jobs);
+  c->jt.slot_token = (int32_t*)(jb + o_tok);
+  c->jt.slot_gate = (float*)(jb + o_gate);
+  if (cudaHostAlloc((void**)&c->dec_host, sizeof(hb_decision) * (1 + P) * B * K,
+                    cudaHostAllocDefault) != cudaSuccess)
+    return bail(HB_ENOMEM, "pinned decision buffer allocation failed");
+  if (cudaEventCreateWithFlags(&c->dec_ready, cudaEventDisableTiming) != cudaSuccess)
+    return bail(HB_ECUDA, "event creation failed");
+  c->router_set.assign(L, 0);
+  if (resident) {
+    c->dev_blob.assign((size_t)L * E * 4, nullptr);
+    if (!dm((void**)&c->dev_blob_table, sizeof(void*) * (size_t)L * E * 4))
+      return bail(HB_ENOMEM, "blob table allocation failed");
+    cudaMemset(c->dev_blob_table, 0, sizeof(void*) * (size_t)L * E * 4);
+  } else {
+    c->host_blob.assign((size_t)L * E * 4, nullptr);
+    const int cap[2] = {k.cap_high, k.cap_low};
+    const int enc[2] = {k.hi_enc, k.lo_enc};
+    for (int p = 0; p < 2; ++p) {
+      c->slot_bytes[p] = align_up(c->bbytes[enc[p]], 4096);
+      if (cap[p] > 0 && !dm((void**)&c->pool_mem[p], c->slot_bytes[p] * cap[p]))
+        return bail(HB_ENOMEM, "expert pool allocation failed");
+      c->slot_ready[p].resize(cap[p]);
+      c->slot_free[p].resize(cap[p]);
+      for (int s = 0; s < cap[p]; ++s) {
+        cudaEventCreateWithFlags(&c->slot_ready[p][s], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&c->slot_free[p][s], cudaEventDisableTiming);
+      }
+    }
+    if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(HB_ECUDA, "copy stream creation failed");
+    const int w[4] = {k.w_lru, k.w_lfu, k.w_lhu, k.w_fld};
+    c->cache = new (std::nothrow) ExpertCache(L, E, K, k.cap_high, k.cap_low, w, k.hi_enc,
+                                              k.lo_enc, k.allow_upgrade != 0, k.rank, k.world);
+    if (!c->cache) return bail(HB_ENOMEM, "cache allocation failed");
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(HB_ECUDA, "device sync failed");
+  *out = c;
+  return HB_OK;
+}
+
+int hb_destroy(hb_ctx* c) {
+  if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  free_ctx(c);
+  return HB_OK;
+}
+
+int hb_set_router(hb_ctx* c, int layer, const void* w, int on_device) {
+  if (!c || !w) return fail(c, HB_EINVAL, "null argument");
+  if (layer < 0 || layer >= c->cfg.n_layers) return fail(c, HB_EINVAL, "bad layer");
+  const size_t n = (size_t)c->cfg.n_experts * c->cfg.hidden * 2;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpy((uint8_t*)c->wg + (size_t)layer * n, w, n,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  c->router_set[layer] = 1;
+  return HB_OK;
+}
+
+int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* blob,
+                       size_t nbytes, int flags) {
+  if (!c || !blob) return fail(c, HB_EINVAL, "null argument");
+  const hb_config& k = c->cfg;
+  if (layer < 0 || layer >= k.n_layers || expert < 0 || expert >= k.n_experts)
+    return fail(c, HB_EINVAL, "bad layer / expert");
+  if (enc != k.hi_enc && enc != k.lo_enc) return fail(c, HB_EINVAL, "encoding is neither hi_enc nor lo_enc");
+  if (nbytes != c->bbytes[enc]) return fail(c, HB_EINVAL, "blob size != hb_blob_bytes(enc, H, F)");
+  if (expert % k.world != k.rank) return fail(c, HB_EINVAL, "expert not owned by this rank");
+  const size_t idx = ((size_t)layer * k.n_experts + expert) * 4 + enc;
+  if (c->resident) {
+    if (flags != HB_REG_DEVICE_BORROW) return fail(c, HB_EINVAL, "resident mode takes device blobs");
+    c->dev_blob[idx] = (const uint8_t*)blob;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpy(c->dev_blob_table + idx, &c->dev_blob[idx], sizeof(void*),
+                           cudaMemcpyHostToDevice));
+    return HB_OK;
+  }
+  if (flags == HB_REG_HOST_PINNED) {
+    c->host_blob[idx] = (const uint8_t*)blob;
+  } else if (flags == HB_REG_HOST_COPY) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, nbytes, cudaHostAllocDefault) != cudaSuccess)
+      return fail(c, HB_ENOMEM, "pinned arena allocation failed");
+    std::memcpy(p, blob, nbytes);
+    c->arena.push_back(p);
+    c->host_blob[idx] = (const uint8_t*)p;
+  } else {
+    return fail(c, HB_EINVAL, "offload mode takes host blobs");
+  }
+  return HB_OK;
+}
+
+int hb_token_begin(hb_ctx* c) {
+  if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  if (c->cache) c->cache->token_begin();
+  c->token_started = true;
+  return HB_OK;
+}
+
+int hb_reset_sequence(hb_ctx* c) {
+  if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  if (c->cache) c->cache->reset_sequence();
+  return HB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- internals
+static RouterParams router_params(hb_ctx* c, const void* x, int batch) {
+  const hb_config& k = c->cfg;
+  RouterParams p{};
+  p.x = (const __half*)x;
+  p.B = batch;
+  p.E = k.n_experts;
+  p.H = k.hidden;
+  p.k = k.top_k;
+  p.theta1 = hb_theta(k.t1, &p.th1_kind);
+  p.theta2 = hb_theta(k.t2, &p.th2_kind);
+  p.t1 = k.t1;
+  p.t2 = k.t2;
+  p.rank = k.rank;
+  p.world = k.world;
+  p.hi_enc = k.hi_enc;
+  p.lo_enc = k.lo_enc;
+  p.jt = c->jt;
+  p.done = c->done;
+  return p;
+}
+
+static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
+  const hb_config& k = c->cfg;
+  GemvParams g{};
+  g.jt = c->jt;
+  for (int e = 0; e < 4; ++e) g.lay[e] = c->lay[e];
+  g.H = k.hidden;
+  g.F = k.ffn;
+  g.B = batch;
+  g.x_perm = c->x_perm;
+  g.xsum = c->xsum;
+  g.h_hi = c->h_hi;
+  g.h_lo = c->h_lo;
+  g.hsum = c->hsum;
+  g.partial = c->partial;
+  g.partial_n = (long long)c->S * batch * k.hidden;
+  g.S = c->S;
+  g.chunk = c->chunk;
+  g.y = (float*)y;
+  g.tile_count = c->tile_count;
+  return g;
+}
+
+// K2a + K2b, bracketed by timing events when hb_profile is on
+static void launch_gemv(hb_ctx* c, const GemvParams& gp, int nt, cudaStream_t s) {
+  cudaEvent_t* ev = nullptr;
+  if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
+  if (ev) cudaEventRecord(ev[0], s);
+  launch_w13(gp, nt, s);
+  if (ev) cudaEventRecord(ev[1], s);
+  launch_w2(gp, nt, s);
+  if (ev) cudaEventRecord(ev[2], s);
+  c->launches += 2;
+}
+
+static const __half* router_of(hb_ctx* c, int layer) {
+  return c->wg + (size_t)layer * c->cfg.n_experts * c->cfg.hidden;
+}
+
+// queue the host->device copies of the load events [from, end) of the cache log
+static int issue_loads(hb_ctx* c, size_t from) {
+  std::vector<hb_event>& ev = c->cache->events;
+  for (size_t i = from; i < ev.size(); ++i) {
+    const hb_event& e = ev[i];
+    if (e.type != 1) continue;
+    const int pool = c->cache->pool_of_enc(e.enc);
+    const size_t idx = ((size_t)e.layer * c->cfg.n_experts + e.expert) * 4 + e.enc;
+    const uint8_t* src = c->host_blob[idx];
+    if (!src) return fail(c, HB_ESTATE, "expert blob not registered for a load");
+    uint8_t* dst = c->pool_mem[pool] + (size_t)e.slot * c->slot_bytes[pool];
+    // WAR: every earlier reader of this slot must be done before it is overwritten
+    CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[pool][e.slot], 0));
+    CUDA_TRY(c, cudaMemcpyAsync(dst, src, c->bbytes[e.enc], cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_TRY(c, cudaEventRecord(c->slot_ready[pool][e.slot], c->copy_stream));
+  }
+  return HB_OK;
+}
+
+static void drain_events(hb_ctx* c) {
+  std::vector<hb_event>& ev = c->cache->events;
+  c->log.insert(c->log.end(), ev.begin(), ev.end());
+  ev.clear();
+}
+
+extern "C" {
+
+int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, void* stream) {
+  if (!c || !x || !y) return fail(c, HB_EINVAL, "null argument");
+  const hb_config& k = c->cfg;
+  if (layer < 0 || layer >= k.n_layers) return fail(c, HB_EINVAL, "bad layer");
+  if (batch <= 0 || batch > k.max_batch) return fail(c, HB_EINVAL, "batch must be in [1, max_batch]");
+  if (!c->router_set[layer]) return fail(c, HB_ESTATE, "router of this layer not set");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  RouterParams rp = router_params(c, x, batch);
+  rp.wg[0] = router_of(c, layer);
+  rp.n_route = 1;
+  rp.dec = c->dec;
+  rp.logits = c->logits;
+  rp.x_perm = c->x_perm;
+  rp.xsum = c->xsum;
+  rp.zero_buf = c->hsum;
+  rp.zero_n = (long long)batch * k.top_k * (k.ffn / 32);
+  const int rgrid = std::min(batch, kNumSM);
+  const int nt = batch <= 1 ? 1 : 2;
+  c->last_batch = batch;
+  c->last_layer = layer;
+
+  if (c->resident) {
+    rp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
+    launch_router(rp, rgrid, s);
+    c->launches += 1;
+    GemvParams gp = gemv_params(c, batch, y);
+    launch_gemv(c, gp, nt, s);
+    c->last_host_decisions = false;
+    CUDA_TRY(c, cudaGetLastError());
+    return HB_OK;
+  }
+
+  // ---- offload mode: decisions to the host, cache state machine, loads ----
+  if (batch != 1) return fail(c, HB_EUNSUPPORTED, "constrained cache supports batch 1 decode (v1)");
+  if (!c->token_started) return fail(c, HB_ESTATE, "forward before hb_token_begin");
+  rp.blob_table = nullptr;
+  launch_router(rp, rgrid, s);
+  c->launches += 1;
+  const int K = k.top_k;
+  CUDA_TRY(c, cudaMemcpyAsync(c->dec_host, c->dec, sizeof(hb_decision) * K, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaEventRecord(c->dec_ready, s));
+  CUDA_TRY(c, cudaEventSynchronize(c->dec_ready));
+  int32_t ex[kMaxTopK];
+  uint8_t pr[kMaxTopK], served[kMaxTopK], hit[kMaxTopK];
+  int pool[kMaxTopK], slot[kMaxTopK];
+  for (int i = 0; i < K; ++i) {
+    ex[i] = c->dec_host[i].expert;
+    pr[i] = c->dec_host[i].prec;
+  }
+  const size_t ev0 = c->cache->events.size();
+  int rc = c->cache->forward(layer, ex, pr, served, pool, slot, hit);
+  if (rc) {
+    drain_events(c);
+    return fail(c, rc, c->cache->err);
+  }
+  rc = issue_loads(c, ev0);
+  drain_events(c);
+  if (rc) return rc;
+  // job table on the host: one job per non-skipped owned selection
+  uint8_t* jh = (uint8_t*)c->jt_host;
+  int32_t* hdr = (int32_t*)jh;
+  Job* jobs = (Job*)(jh + ((uint8_t*)c->jt.jobs - (uint8_t*)c->jt_dev));
+  int32_t* stok = (int32_t*)(jh + ((uint8_t*)c->jt.slot_token - (uint8_t*)c->jt_dev));
+  float* sgate = (float*)(jh + ((uint8_t*)c->jt.slot_gate - (uint8_t*)c->jt_dev));
+  int nj = 0;
+  for (int i = 0; i < K; ++i) {
+    c->dec_host[i].served_enc = served[i];
+    c->dec_host[i].hit = hit[i];
+    if (served[i] == HB_ENC_NONE) continue;
+    Job j;
+    j.blob = c->pool_mem[pool[i]] + (size_t)slot[i] * c->slot_bytes[pool[i]];
+    j.enc = served[i];
+    j.expert = ex[i];
+    j.n_tok = 1;
+    j.slot_off = nj;
+    jobs[nj] = j;
+    stok[nj] = 0;
+    sgate[nj] = c->dec_host[i].gate;
+    ++nj;
+  }
+  hdr[0] = nj;
+  hdr[1] = nj;
+  CUDA_TRY(c, cudaMemcpyAsync(c->jt_dev, c->jt_host, c->jt_bytes, cudaMemcpyHostToDevice, s));
+  for (int i = 0; i < K; ++i)
+    if (served[i] != HB_ENC_NONE)
+      CUDA_TRY(c, cudaStreamWaitEvent(s, c->slot_ready[pool[i]][slot[i]], 0));
+  GemvParams gp = gemv_params(c, batch, y);
+  launch_gemv(c, gp, nt, s);
+  for (int i = 0; i < K; ++i)
+    if (served[i] != HB_ENC_NONE)
+      CUDA_TRY(c, cudaEventRecord(c->slot_free[pool[i]][slot[i]], s));
+  c->last_host_decisions = true;
+  CUDA_TRY(c, cudaGetLastError());
+  return HB_OK;
+}
+
+int expert_cache_load(hb_ctx* c, int layer, int expert, int enc, void* stream) {
+  (void)stream;
+  if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  if (c->resident) return fail(c, HB_ESTATE, "expert_cache_load needs a constrained cache");
+  const hb_config& k = c->cfg;
+  if (layer < 0 || layer >= k.n_layers || expert < 0 || expert >= k.n_experts)
+    return fail(c, HB_EINVAL, "bad layer / expert");
+  if (expert % k.world != k.rank) return fail(c, HB_EINVAL, "expert not owned by this rank");
+  const size_t ev0 = c->cache->events.size();
+  bool queued = false;
+  int rc = c->cache->load(layer, expert, enc, &queued);
+  if (rc) return fail(c, rc, c->cache->err);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  rc = issue_loads(c, ev0);
+  drain_events(c);
+  return rc;
+}
+
+int prefetch_next_layer(hb_ctx* c, int layer, const void* x, int batch, void* stream) {
+  if (!c || !x) return fail(c, HB_EINVAL, "null argument");
+  const hb_config& k = c->cfg;
+  if (layer < 0 || layer >= k.n_layers) return fail(c, HB_EINVAL, "bad layer");
+  if (c->resident) return 0;
+  if (batch != 1) return fail(c, HB_EUNSUPPORTED, "prefetch supports batch 1 decode (v1)");
+  const int n = std::min(k.lookahead_p, k.n_layers - 1 - layer);
+  if (n <= 0) {
+    int pl;
+    c->cache->prefetch(layer, 0, nullptr, nullptr, &pl);   // still expires masks
+    return 0;
+  }
+  for (int j = 0; j < n; ++j)
+    if (!c->router_set[layer + 1 + j]) return fail(c, HB_ESTATE, "router of a lookahead layer not set");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  RouterParams rp = router_params(c, x, batch);
+  rp.n_route = n;
+  for (int j = 0; j < n; ++j) rp.wg[j] = router_of(c, layer + 1 + j);   // Stacking Computer
+  rp.dec = c->dec_pred;
+  rp.blob_table = nullptr;
+  launch_router(rp, 1, s);
+  c->launches += 1;
+  const int K = k.top_k;
+  hb_decision* hd = c->dec_host + K;                 // after the forward's record
+  CUDA_TRY(c, cudaMemcpyAsync(hd, c->dec_pred, sizeof(hb_decision) * n * K, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaEventRecord(c->dec_ready, s));
+  CUDA_TRY(c, cudaEventSynchronize(c->dec_ready));
+  std::vector<int32_t> ex(n * K);
+  std::vector<uint8_t> pr(n * K);
+  for (int i = 0; i < n * K; ++i) {
+    ex[i] = hd[i].expert;
+    pr[i] = hd[i].prec;
+  }
+  const size_t ev0 = c->cache->events.size();
+  int pl = -1;
+  int rc = c->cache->prefetch(layer, n, ex.data(), pr.data(), &pl);
+  if (rc) return fail(c, rc, c->cache->err);
+  int queued = 0;
+  for (size_t i = ev0; i < c->cache->events.size(); ++i) queued += c->cache->events[i].type == 1;
+  rc = issue_loads(c, ev0);
+  drain_events(c);
+  return rc ? rc : queued;
+}
+
+int hb_get_decisions(hb_ctx* c, hb_decision* out, int cap) {
+  if (!c || (cap > 0 && !out)) return fail(c, HB_EINVAL, "null argument");
+  const int n = std::min(cap, c->last_batch * c->cfg.top_k);
+  if (n <= 0) return 0;
+  if (c->last_host_decisions) {
+    std::memcpy(out, c->dec_host, sizeof(hb_decision) * n);
+  } else {
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    CUDA_TRY(c, cudaMemcpy(out, c->dec, sizeof(hb_decision) * n, cudaMemcpyDeviceToHost));
+  }
+  return n;
+}
+
+int hb_get_logits(hb_ctx* c, int64_t* out, int cap_pairs) {
+  if (!c || (cap_pairs > 0 && !out)) return fail(c, HB_EINVAL, "null argument");
+  const int n = std::min(cap_pairs, c->last_batch * c->cfg.n_experts);
+  if (n <= 0) return 0;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  CUDA_TRY(c, cudaMemcpy(out, c->logits, sizeof(long long) * 2 * n, cudaMemcpyDeviceToHost));
+  return n;
+}
+
+int hb_get_events(hb_ctx* c, hb_event* out, int cap) {
+  if (!c || (cap > 0 && !out)) return fail(c, HB_EINVAL, "null argument");
+  const int n = std::min<int>(cap, (int)c->log.size());
+  for (int i = 0; i < n; ++i) out[i] = c->log[i];
+  c->log.erase(c->log.begin(), c->log.begin() + n);
+  return n;
+}
+
+int hb_last_expert_bytes(hb_ctx* c, uint64_t* out) {
+  if (!c || !out) return fail(c, HB_EINVAL, "null argument");
+  std::vector<hb_decision> d(c->last_batch * c->cfg.top_k);
+  int n = hb_get_decisions(c, d.data(), (int)d.size());
+  if (n < 0) return n;
+  // one stream of each served (expert, enc) per forward
+  std::vector<char> seen((size_t)c->cfg.n_experts * 4, 0);
+  uint64_t tot = 0;
+  for (int i = 0; i < n; ++i) {
+    if (d[i].served_enc == HB_ENC_NONE) continue;
+    const size_t key = (size_t)d[i].expert * 4 + d[i].served_enc;
+    if (seen[key]) continue;
+    seen[key] = 1;
+    tot += c->bbytes[d[i].served_enc];
+  }
+  *out = tot;
+  return HB_OK;
+}
+
+int hb_launch_count(hb_ctx* c, uint64_t* out) {
+  if (!c || !out) return fail(c, HB_EINVAL, "null argument");
+  *out = c->launches;
+  return HB_OK;
+}
+
+int hb_profile(hb_ctx* c, int max_calls) {
+  if (!c || max_calls < 0) return fail(c, HB_EINVAL, "bad argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  while ((int)c->prof_ev.size() < 3 * max_calls) {
+    cudaEvent_t e;
+    CUDA_TRY(c, cudaEventCreate(&e));
+    c->prof_ev.push_back(e);
+  }
+  c->prof_max = max_calls;
+  c->prof_n = 0;
+  return HB_OK;
+}
+
+int hb_profile_read(hb_ctx* c, float* ms, int cap) {
+  if (!c || (cap > 0 && !ms)) return fail(c, HB_EINVAL, "bad argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int n = std::min(cap, c->prof_n);
+  for (int i = 0; i < n; ++i) {
+    CUDA_TRY(c, cudaEventSynchronize(c->prof_ev[3 * i + 2]));
+    CUDA_TRY(c, cudaEventElapsedTime(&ms[2 * i], c->prof_ev[3 * i], c->prof_ev[3 * i + 1]));
+    CUDA_TRY(c, cudaEventElapsedTime(&ms[2 * i + 1], c->prof_ev[3 * i + 1], c->prof_ev[3 * i + 2]));
+  }
+  return n;
+}
+
+int hb_quantize_expert(int enc, int hidden, int ffn, const void* w1, const void* w3, const void* w2,
+                       void* blob, void* stream) {
+  if (!w1 || !w3 || !w2 || !blob) return fail(nullptr, HB_EINVAL, "null argument");
+  int rc = launch_quantize_expert(enc, hidden, ffn, (const __half*)w1, (const __half*)w3,
+                                  (const __half*)w2, (uint8_t*)blob, (cudaStream_t)stream);
+  if (rc) return fail(nullptr, rc, "quantize failed (bad dims/enc or CUDA error)");
+  return HB_OK;
+}
+
+int hb_synth_fill_f16(void* dst, size_t n, uint64_t key, float scale, uint64_t start, void* stream) {
+  if (!dst) return fail(nullptr, HB_EINVAL, "null argument");
+  launch_synth((__half*)dst, n, key, scale, start, (cudaStream_t)stream);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(nullptr, HB_ECUDA, cudaGetErrorString(e));
+  return HB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hobbit.h"
+
+namespace hb {
+
+constexpr int kMaxTopK = 8;
+constexpr int kMaxRouteLayers = 4;      // 1 + max lookahead p handled per launch
+constexpr int kNumSM = 148;             // B200
+constexpr int kGemvWarps = 16;          // warps per GEMV CTA (one CTA per SM)
+constexpr int kRouterThreads = 256;
+
+// Byte offsets of the sections of one matrix inside an expert blob.
+struct MatLayout {
+  uint64_t q;        // codes (or the fp16 matrix for F16)
+  uint64_t d;        // fp16 scales [N][K/32]
+  uint64_t m;        // fp16 mins   [N][K/32] (Q2 only)
+};
+struct BlobLayout {
+  MatLayout mat[3];  // W1 [F,H], W3 [F,H], W2 [H,F]
+  uint64_t total;
+};
+int blob_layout(int enc, int hidden, int ffn, BlobLayout* out);   // host
+
+// One (expert, served encoding) group of a layer on this rank: the GEMV
+// kernels stream its blob once for all of its token slots.
+struct Job {
+  const uint8_t* blob;
+  int32_t enc;
+  int32_t expert;
+  int32_t n_tok;       // token slots of this job
+  int32_t slot_off;    // first slot in slot_token / slot_gate / h
+};
+
+// Device job table of one forward: [hdr | jobs | slot_token | slot_gate]
+struct JobTable {
+  int32_t* hdr;        // [0] n_jobs, [1] n_slots
+  Job* jobs;           // max_jobs
+  int32_t* slot_token; // max_slots
+  float* slot_gate;    // max_slots
+};
+
+struct RouterParams {
+  const __half* x;                     // [B, H]
+  const __half* wg[kMaxRouteLayers];   // router of each routed layer
+  int n_route;                         // routed layers in this launch
+  int B, E, H, k;
+  int64_t theta1, theta2;              // k = 2 exact gap test
+  int th1_kind, th2_kind;              // 0 finite, +1 always true, -1 never
+  double t1, t2;                       // k > 2 fp64 test
+  int rank, world;
+  hb_decision* dec;                    // [n_route][B][k]
+  long long* logits;                   // [B][E][2] for route 0, or null
+  uint4* x_perm;                       // [B][H/8] pair-permuted x, or null
+  float* xsum;                         // [B][H/32], or null
+  float* zero_buf;                     // zeroed by the router grid (h block sums)
+  long long zero_n;
+  // resident job building (blob_table != null): last CTA builds the table
+  const uint8_t* const* blob_table;    // [E][4] device blob of (expert, enc) for this layer
+  int hi_enc, lo_enc;
+  JobTable jt;
+  unsigned* done;                      // grid completion counter (self-resetting)
+};
+
+struct GemvParams {
+  JobTable jt;
+  BlobLayout lay[4];
+  int H, F, B;
+  const uint4* x_perm;                 // [B][H/8]
+  const float* xsum;                   // [B][H/32]
+  uint4* h_hi;                         // [slots][F/8]  pair-permuted fp16 hi part of h
+  uint4* h_lo;                         // [slots][F/8]  fp16 residual h - hi
+  float* hsum;                         // [slots][F/32] block sums of h (zeroed by router)
+  float* partial;                      // [S][B][H]
+  long long partial_n;
+  int S, chunk;                        // W2 split-K: S chunks of `chunk` elements of F
+  float* y;                            // [B][H]
+  unsigned* tile_count;                // [H/16] (self-resetting)
+};
+
+void launch_router(const RouterParams& p, int grid, cudaStream_t s);
+void launch_w13(const GemvParams& p, int nt, cudaStream_t s);
+void launch_w2(const GemvParams& p, int nt, cudaStream_t s);
+int launch_quantize_expert(int enc, int hidden, int ffn, const __half* w1, const __half* w3,
+                           const __half* w2, uint8_t* blob, cudaStream_t s);
+void launch_synth(__half* dst, size_t n, uint64_t key, float scale, uint64_t start,
+                  cudaStream_t s);
+
+}  // namespace hb

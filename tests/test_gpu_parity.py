@@ -1,0 +1,301 @@
+"""GPU parity: the CUDA path through the C-ABI vs the fp64 / exact oracle.
+
+Bar: decisions, logits, quantised bytes, generator
+output and cache events bit-exact; y within max relative error 2e-3
+(north_star) normwise per token, fp32 accumulation vs the fp64 oracle on
+identical quantised weights.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synthgen as sg  # noqa: E402
+from oracle import cache as oc  # noqa: E402
+from oracle import formats as fm  # noqa: E402
+from oracle import moe as om  # noqa: E402
+from oracle import router as rt  # noqa: E402
+from tests.gpu_util import TOL, OracleStore, gpu_blobs, rel_err  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2411_01433_b200 import hobbit  # noqa: F401  (fails loudly if not built)
+    torch.cuda.set_device(0)
+
+
+def H():
+    from paper_2411_01433_b200 import hobbit
+    return hobbit
+
+
+# ------------------------------------------------------------ generator
+@pytest.mark.parametrize("n,sigma,start", [(1 << 20, 1.0, 0), (12345, 0.0156, 777), (4096, 1.5 / 64, 3)])
+def test_synth_kernel_bit_exact(n, sigma, start):
+    key = sg.stream_key(1433, 9, n)
+    t = torch.empty(n, dtype=torch.float16, device="cuda")
+    H().synth_fill(t, key, float(sg.scale_f32(sigma)), start)
+    ref = sg.fill_f16(key, n, sigma, start)
+    assert np.array_equal(t.cpu().numpy().view(np.uint16), ref.view(np.uint16))
+
+
+# ------------------------------------------------------------ quantiser
+@pytest.mark.parametrize("enc", [fm.F16, fm.Q8, fm.Q4, fm.Q2])
+@pytest.mark.parametrize("shape", [sg.TINY, sg.MoEShape("phi-slice", 1, 1, 2, 4096, 6400, 1.8)],
+                         ids=["tiny", "phi"])
+def test_quantiser_bytes_bit_exact(enc, shape):
+    blob = gpu_blobs(shape, 0, [0], [enc])[(0, enc)].cpu().numpy()
+    w1, w3, w2 = sg.expert_weights(shape, 0, 0)
+    ref = fm.quantize_blob(enc, w1, w3, w2)
+    assert blob.shape == ref.shape
+    bad = np.nonzero(blob != ref)[0]
+    assert bad.size == 0, f"{bad.size} bytes differ, first at {bad[:8]}"
+
+
+# ------------------------------------------------------------ helpers
+def _ctx(shape, hi, lo, t1=0.6, t2=0.9, max_batch=1, **kw):
+    h = H()
+    cfg = h.default_config(n_layers=shape.n_layers, n_experts=shape.n_experts,
+                           top_k=shape.top_k, hidden=shape.hidden, ffn=shape.ffn,
+                           hi_enc=hi, lo_enc=lo, t1=t1, t2=t2, max_batch=max_batch, **kw)
+    return h.Context(cfg)
+
+
+def _resident(shape, layers, hi, lo, **kw):
+    ctx = _ctx(shape, hi, lo, **kw)
+    world = kw.get("world", 1)
+    rank = kw.get("rank", 0)
+    for l in layers:
+        ctx.set_router(l, sg.router_weights(shape, l))
+        owned = [e for e in range(shape.n_experts) if e % world == rank]
+        for (e, enc), b in gpu_blobs(shape, l, owned, [hi, lo]).items():
+            ctx.register_expert(l, e, enc, b)
+    return ctx
+
+
+def _run(ctx, layer, x16):
+    x = torch.from_numpy(x16).cuda()
+    y = torch.empty(x.shape[0], x.shape[1], dtype=torch.float32, device="cuda")
+    ctx.forward(layer, x, y)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def _check_routes(ctx, routes, B, k):
+    dec = ctx.decisions(B)
+    for b, r in enumerate(routes):
+        for i in range(k):
+            d = dec[b * k + i]
+            assert d.token == b and d.sel_rank == i
+            assert d.expert == r.experts[i], (b, i)
+            assert d.prec == r.decisions[i], (b, i)
+            assert abs(d.gate - r.gates[i]) <= 1e-6 * max(1.0, abs(r.gates[i]))
+
+
+# ------------------------------------------------------------ router
+@pytest.mark.parametrize("shape,B", [(sg.TINY, 16), (sg.MIXTRAL, 3), (sg.PHI, 2)],
+                         ids=["tiny", "mixtral", "phi"])
+def test_router_exact_logits_and_decisions(shape, B):
+    sh = sg.MoEShape(shape.name, 1, shape.n_experts, shape.top_k, shape.hidden, 512,
+                     shape.sigma_router)
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=B)
+    for t in range(3):
+        x16 = sg.hidden_states(sh, t, 0, batch=B)
+        _run(ctx, 0, x16)
+        L = rt.exact_logits(x16, sg.router_weights(sh, 0))
+        assert ctx.logits(B) == L
+        routes = [rt.route_token(row, sh.top_k, 0.6, 0.9) for row in L]
+        _check_routes(ctx, routes, B, sh.top_k)
+
+
+# ------------------------------------------------------------ full layer
+PAIRS = [(fm.F16, fm.Q4), (fm.F16, fm.Q2), (fm.Q8, fm.Q2), (fm.Q8, fm.Q4)]
+
+
+@pytest.mark.parametrize("pair", PAIRS, ids=lambda p: f"{fm.ENC_NAMES[p[0]]}-{fm.ENC_NAMES[p[1]]}")
+@pytest.mark.parametrize("B", [1, 5, 16])
+def test_layer_parity_tiny(pair, B):
+    sh = sg.TINY
+    hi, lo = pair
+    ctx = _resident(sh, [0, 1], hi, lo, max_batch=16)
+    store = OracleStore(sh)
+    for t in range(2):
+        for l in range(sh.n_layers):
+            x16 = sg.hidden_states(sh, 10 + t, l, batch=B)
+            y = _run(ctx, l, x16)
+            ref, routes = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9, hi, lo)
+            _check_routes(ctx, routes, B, 2)
+            for b in range(B):
+                nw, el = rel_err(y[b], ref[b])
+                assert nw <= TOL, (b, nw, el)
+                assert nw <= 1e-4, (b, nw)       # expected ~1e-6 with exact codes
+
+
+@pytest.mark.parametrize("t1,t2", [(1.0, 1.0), (0.0, 0.0), (0.5, 0.5), (0.6, 0.6)])
+def test_layer_threshold_edges(t1, t2):
+    sh = sg.TINY
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, t1=t1, t2=t2, max_batch=16)
+    store = OracleStore(sh)
+    x16 = sg.hidden_states(sh, 3, 0, batch=16)
+    y = _run(ctx, 0, x16)
+    ref, routes = om.moe_layer(x16, sg.router_weights(sh, 0), store, 0, 2, t1, t2, fm.F16, fm.Q4)
+    _check_routes(ctx, routes, 16, 2)
+    for b in range(16):
+        assert rel_err(y[b], ref[b])[0] <= TOL
+
+
+def test_zero_input_gives_zero():
+    sh = sg.TINY
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=2)
+    y = _run(ctx, 0, np.zeros((2, sh.hidden), np.float16))
+    assert np.all(y == 0)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_partition_on_one_gpu(world):
+    """O11: per-rank contexts (same GPU) sum to the 1-rank output, identical decisions."""
+    sh = sg.TINY
+    x16 = sg.hidden_states(sh, 7, 1, batch=4)
+    full = _run(_resident(sh, [1], fm.F16, fm.Q4, max_batch=4), 1, x16)
+    parts = []
+    for r in range(world):
+        ctx = _resident(sh, [1], fm.F16, fm.Q4, max_batch=4, rank=r, world=world)
+        parts.append(_run(ctx, 1, x16))
+        d = ctx.decisions(4)
+        assert all((v.served_enc == 255) == (v.prec == rt.SKIP or v.expert % world != r) for v in d)
+    np.testing.assert_allclose(np.sum(parts, axis=0), full, rtol=1e-5, atol=1e-6)
+
+
+def test_cuda_graph_capture_replays_identically():
+    sh = sg.TINY
+    ctx = _resident(sh, [0, 1], fm.F16, fm.Q4, max_batch=1)
+    x = torch.from_numpy(sg.hidden_states(sh, 1, 0)).cuda()
+    y = torch.zeros(1, sh.hidden, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx.forward(0, x, y)
+        ctx.forward(1, x, y)
+    torch.cuda.synchronize()
+    ref = y.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ctx.forward(0, x, y)
+        ctx.forward(1, x, y)
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+
+
+# ------------------------------------------------------------ full size
+@pytest.mark.parametrize("shape,pair,tokens", [
+    (sg.MIXTRAL, (fm.F16, fm.Q4), 3), (sg.MIXTRAL, (fm.F16, fm.Q2), 2),
+    (sg.MIXTRAL, (fm.Q8, fm.Q2), 2), (sg.PHI, (fm.F16, fm.Q4), 3)],
+    ids=["mixtral-f16q4", "mixtral-f16q2", "mixtral-q8q2", "phi-f16q4"])
+def test_layer_parity_full_size(shape, pair, tokens):
+    """BASELINE.json full shapes, batch-1 decode, the launch configuration the
+    bench times (one layer; all E experts of that layer resident)."""
+    hi, lo = pair
+    layer = 5
+    sh1 = sg.MoEShape(shape.name, shape.n_layers, shape.n_experts, 2, shape.hidden, shape.ffn,
+                      shape.sigma_router)
+    ctx = _resident(sh1, [layer], hi, lo)
+    store = OracleStore(sh1)
+    wg = sg.router_weights(sh1, layer)
+    for t in range(tokens):
+        x16 = sg.hidden_states(sh1, 100 + t, layer)
+        y = _run(ctx, layer, x16)
+        ref, routes = om.moe_layer(x16, wg, store, layer, 2, 0.6, 0.9, hi, lo)
+        _check_routes(ctx, routes, 1, 2)
+        nw, el = rel_err(y[0], ref[0])
+        assert nw <= TOL, (nw, el)
+
+
+# ------------------------------------------------------------ offload path
+def _offload_ctx(sh, ch, cl, p, w=(1, 1, 1, 1)):
+    ctx = _ctx(sh, fm.F16, fm.Q4, max_batch=1, cap_high=ch, cap_low=cl, lookahead_p=p,
+               w_lru=w[0], w_lfu=w[1], w_lhu=w[2], w_fld=w[3])
+    store = OracleStore(sh)
+    for l in range(sh.n_layers):
+        ctx.set_router(l, sg.router_weights(sh, l))
+        # the library's own quantised blobs, staged in host memory (next-level storage)
+        for (e, enc), b in gpu_blobs(sh, l, range(sh.n_experts), [fm.F16, fm.Q4]).items():
+            ctx.register_expert(l, e, enc, b.cpu().numpy())           # HB_REG_HOST_COPY
+    return ctx, store
+
+
+@pytest.mark.parametrize("p", [0, 1, 2])
+def test_offload_cache_events_and_outputs(p):
+    """Constrained cache (C4 on the tiny shape): cache events bit-exact with
+    O9/O10 and y equal to the oracle computed with the served encodings."""
+    sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
+    ch, cl = 6, 6
+    ctx, store = _offload_ctx(sh, ch, cl, p)
+    ref_cache = oc.ExpertCache(sh.n_layers, sh.n_experts, ch, cl, (1, 1, 1, 1), fm.F16, fm.Q4)
+    xs = sg.correlated_states(sh, 12, 0.999, 0.5)
+    for t in range(12):
+        ctx.token_begin()
+        ref_cache.token_begin()
+        for l in range(sh.n_layers):
+            x16 = xs[t, l][None, :]
+            y = _run(ctx, l, x16)
+            route = rt.route(x16, sg.router_weights(sh, l), 2, 0.6, 0.9)[0]
+            served = ref_cache.forward(l, route)
+            ref, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9,
+                                  fm.F16, fm.Q4, served=[served])
+            assert rel_err(y[0], ref[0])[0] <= TOL
+            d = ctx.decisions(1)
+            assert [v.served_enc if v.served_enc != 255 else None for v in d] == served
+            if p > 0:
+                ctx.prefetch(l, torch.from_numpy(x16).cuda())
+                pred = {l + j: rt.route(x16, sg.router_weights(sh, l + j), 2, 0.6, 0.9)[0]
+                        for j in range(1, p + 1) if l + j < sh.n_layers}
+                ref_cache.prefetch(l, pred)
+    torch.cuda.synchronize()
+    assert ctx.events() == ref_cache.events
+
+
+def test_offload_explicit_load_and_reset():
+    sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
+    ctx, store = _offload_ctx(sh, 5, 5, 0)
+    ref_cache = oc.ExpertCache(4, 8, 5, 5, (1, 1, 1, 1), fm.F16, fm.Q4)
+    for l, e, enc in [(0, 1, fm.F16), (0, 2, fm.Q4), (1, 3, fm.F16), (0, 1, fm.F16)]:
+        ctx.load(l, e, enc)
+        ref_cache.load(l, e, enc)
+    for seq in range(2):
+        ctx.reset_sequence()
+        ref_cache.reset_sequence()
+        for t in range(4):
+            ctx.token_begin()
+            ref_cache.token_begin()
+            for l in range(4):
+                x16 = sg.hidden_states(sh, 50 + 10 * seq + t, l)
+                y = _run(ctx, l, x16)
+                route = rt.route(x16, sg.router_weights(sh, l), 2, 0.6, 0.9)[0]
+                served = ref_cache.forward(l, route)
+                ref, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9,
+                                      fm.F16, fm.Q4, served=[served])
+                assert rel_err(y[0], ref[0])[0] <= TOL
+    assert ctx.events() == ref_cache.events
+
+
+def test_errors_are_loud():
+    h = H()
+    sh = sg.TINY
+    ctx = _ctx(sh, fm.F16, fm.Q4, max_batch=2)
+    x = torch.zeros(3, sh.hidden, dtype=torch.float16, device="cuda")
+    y = torch.zeros(3, sh.hidden, dtype=torch.float32, device="cuda")
+    with pytest.raises(h.HobbitError):          # router not set
+        ctx.forward(0, x[:1], y[:1])
+    ctx.set_router(0, sg.router_weights(sh, 0))
+    with pytest.raises(h.HobbitError):          # batch > max_batch
+        ctx.forward(0, x, y)
+    with pytest.raises(h.HobbitError):          # wrong blob size
+        ctx.register_expert(0, 0, fm.F16, torch.zeros(10, dtype=torch.uint8, device="cuda"))
+    off = _ctx(sh, fm.F16, fm.Q4, max_batch=1, cap_high=4, cap_low=4)
+    off.set_router(0, sg.router_weights(sh, 0))
+    with pytest.raises(h.HobbitError):          # forward before token_begin
+        off.forward(0, x[:1], y[:1])
