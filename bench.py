@@ -171,21 +171,18 @@ def run_ours(args):
 
     # ---- realised algorithmic bytes of the pool's tokens (decisions, untimed)
     blob_b = {hi: h.blob_bytes(hi, Hd, shape.ffn), lo: h.blob_bytes(lo, Hd, shape.ffn)}
+    # SURVEY 8(d) unit: served blob bytes + router W_g + x + y + h (write + read)
     bytes_tok = []
-    w13_bytes_tok, w2_bytes_tok = [], []
     mix = [0, 0, 0]
     for t in range(P):
-        tot = w13 = w2 = 0
+        tot = 0
         for l in range(L):
             with torch.cuda.stream(stream):
                 ctx.forward(l, X[t, l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
             for d in ctx.decisions(1):
                 mix[d.prec] += 1
-                if d.served_enc == h.HB_ENC_NONE:
-                    continue
-                b = blob_b[d.served_enc]
-                w13_part = 2 * (b - (b // 3))     # refined below
-                tot += b
+                if d.served_enc != h.HB_ENC_NONE:
+                    tot += blob_b[d.served_enc] + 2 * 4 * shape.ffn
             tot += 2 * shape.n_experts * Hd + 2 * Hd + 4 * Hd
         bytes_tok.append(tot)
     torch.cuda.synchronize()
@@ -223,21 +220,29 @@ def run_ours(args):
             step(t, stream)
 
     # ---- warmup + timed region
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream), ClockSampler(local) as clk:
         for w in range(args.warmup):
             run_step(w)
+        # keep the GPU busy (untimed) until the clock sampler is producing samples
+        t_wait = time.time()
+        while not clk.lines and time.time() - t_wait < 5.0:
+            for w in range(8):
+                run_step(w)
+            torch.cuda.synchronize()
+        n_pre = len(clk.lines)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         c_before = ctx.launch_count()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clk:
-            e0.record(stream)
-            for k in range(args.steps):
-                run_step(args.warmup + k)
-            e1.record(stream)
-            torch.cuda.synchronize()
+        e0.record(stream)
+        for k in range(args.steps):
+            run_step(args.warmup + k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        time.sleep(0.15)
+        clk.lines = clk.lines[max(0, n_pre - 1):]   # samples from the timed region on
         if world > 1:
             dist.barrier()
     ms = e0.elapsed_time(e1)

@@ -77,6 +77,7 @@ struct hb_ctx {
   hb_decision* dec_pred = nullptr;        // [p][B][k]
   hb_decision* dec_host = nullptr;        // pinned [(1+p)][B][k]
   long long* logits = nullptr;            // [B][E][2]
+  long long* lbuf = nullptr;              // [P][B][E][2] router scratch
   uint4* x_perm = nullptr;
   float* xsum = nullptr;
   uint4* h_hi = nullptr;
@@ -181,7 +182,7 @@ static void free_ctx(hb_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
-                   c->logits, c->x_perm, c->xsum, c->h_hi, c->h_lo, c->hsum, c->partial,
+                   c->logits, c->lbuf, c->x_perm, c->xsum, c->h_hi, c->h_lo, c->hsum, c->partial,
                    c->tile_count, c->done, c->jt_dev};
   for (void* p : dptrs)
     if (p) cudaFree(p);
@@ -255,6 +256,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
             dm((void**)&c->dec, sizeof(hb_decision) * B * K) &&
             dm((void**)&c->dec_pred, sizeof(hb_decision) * P * B * K) &&
             dm((void**)&c->logits, sizeof(long long) * B * E * 2) &&
+            dm((void**)&c->lbuf, sizeof(long long) * P * B * E * 2) &&
             dm((void**)&c->x_perm, (size_t)B * H * 2) && dm((void**)&c->xsum, (size_t)B * (H / 32) * 4) &&
             dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
@@ -400,6 +402,7 @@ static RouterParams router_params(hb_ctx* c, const void* x, int batch) {
   p.lo_enc = k.lo_enc;
   p.jt = c->jt;
   p.done = c->done;
+  p.lbuf = c->lbuf;
   return p;
 }
 
@@ -485,14 +488,13 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   rp.xsum = c->xsum;
   rp.zero_buf = c->hsum;
   rp.zero_n = (long long)batch * k.top_k * (k.ffn / 32);
-  const int rgrid = std::min(batch, kNumSM);
   const int nt = batch <= 1 ? 1 : 2;
   c->last_batch = batch;
   c->last_layer = layer;
 
   if (c->resident) {
     rp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
-    launch_router(rp, rgrid, s);
+    launch_router(rp, s);
     c->launches += 1;
     GemvParams gp = gemv_params(c, batch, y);
     launch_gemv(c, gp, nt, s);
@@ -505,7 +507,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   if (batch != 1) return fail(c, HB_EUNSUPPORTED, "constrained cache supports batch 1 decode (v1)");
   if (!c->token_started) return fail(c, HB_ESTATE, "forward before hb_token_begin");
   rp.blob_table = nullptr;
-  launch_router(rp, rgrid, s);
+  launch_router(rp, s);
   c->launches += 1;
   const int K = k.top_k;
   CUDA_TRY(c, cudaMemcpyAsync(c->dec_host, c->dec, sizeof(hb_decision) * K, cudaMemcpyDeviceToHost, s));
@@ -604,7 +606,7 @@ int prefetch_next_layer(hb_ctx* c, int layer, const void* x, int batch, void* st
   for (int j = 0; j < n; ++j) rp.wg[j] = router_of(c, layer + 1 + j);   // Stacking Computer
   rp.dec = c->dec_pred;
   rp.blob_table = nullptr;
-  launch_router(rp, 1, s);
+  launch_router(rp, s);
   c->launches += 1;
   const int K = k.top_k;
   hb_decision* hd = c->dec_host + K;                 // after the forward's record

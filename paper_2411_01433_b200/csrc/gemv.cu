@@ -124,7 +124,13 @@ template <> struct Enc<HB_Q4>  { static constexpr int BPG = 4, EPG = 128, SB = 8
 template <> struct Enc<HB_Q2>  { static constexpr int BPG = 8, EPG = 256, SB = 32; };
 
 constexpr int kWarpSmem = 12 * 1024;                    // per-warp cp.async ring
-constexpr int kGemvSmem = kGemvWarps * kWarpSmem;       // 192 KB per CTA
+constexpr int kXStage = 24 * 1024;                      // CTA-shared copy of x / h chunk
+constexpr int kGemvSmem = kGemvWarps * kWarpSmem + kXStage;   // 216 KB per CTA
+
+// B-operand load: a generic 16-byte load (the source is either the CTA's
+// shared-memory stage of x / h or, when it does not fit, global memory).
+__device__ __forceinline__ uint4 ldx(const uint4* p) { return *p; }
+__device__ __forceinline__ float ldxf(const float* p) { return *p; }
 
 // Dequantise block `blk` of the lane's 16-byte share into P0..P3, the fp16
 // pairs (w[8t+c], w[8t+c+4]) with the codes' exact integer values (scale
@@ -251,13 +257,13 @@ __device__ __forceinline__ void mainloop(uint32_t wsm, const MatPtr (&M)[NMAT], 
       uint4 xb[NT], xl[NT];
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
-        xb[n] = __ldg(X.b[n] + gblk * 4 + t);
-        if constexpr (SPLIT) xl[n] = __ldg(X.blo[n] + gblk * 4 + t);
+        xb[n] = ldx(X.b[n] + gblk * 4 + t);
+        if constexpr (SPLIT) xl[n] = ldx(X.blo[n] + gblk * 4 + t);
       }
       float s0[NT], s1[NT];
       if constexpr (ENC == HB_Q2) {
 #pragma unroll
-        for (int n = 0; n < NT; ++n) { s0[n] = __ldg(X.s0[n] + gblk); s1[n] = __ldg(X.s1[n] + gblk); }
+        for (int n = 0; n < NT; ++n) { s0[n] = ldxf(X.s0[n] + gblk); s1[n] = ldxf(X.s1[n] + gblk); }
       }
 #pragma unroll
       for (int m = 0; m < NMAT; ++m) {
@@ -323,9 +329,17 @@ __device__ __forceinline__ int item_for(int it) {
   return blockIdx.x + gridDim.x * (warp + kGemvWarps * it);
 }
 
+extern __shared__ __align__(128) uint8_t gemv_smem[];
+
 __device__ __forceinline__ uint32_t warp_smem() {
-  extern __shared__ __align__(128) uint8_t gemv_smem[];
   return smem_u32(gemv_smem) + (threadIdx.x >> 5) * kWarpSmem;
+}
+// the CTA-shared stage of the B operand (after the warps' rings)
+__device__ __forceinline__ uint8_t* x_stage() { return gemv_smem + kGemvWarps * kWarpSmem; }
+
+// CTA-wide copy of n16 16-byte words (global -> shared)
+__device__ __forceinline__ void stage_copy(uint4* dst, const uint4* src, int n16) {
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldcg(src + i);
 }
 
 template <int ENC>
@@ -340,7 +354,8 @@ __device__ __forceinline__ MatPtr mat_ptr(const GemvParams& p, const Job& j, int
 
 // ------------------------------------------------------------------ K2a
 template <int ENC, int NT>
-__device__ __forceinline__ void w13_tile(const GemvParams& p, const Job& j, int row0) {
+__device__ __forceinline__ void w13_tile(const GemvParams& p, const Job& j, int row0,
+                                         const uint4* xp, const float* xs) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const MatPtr M[2] = {mat_ptr<ENC>(p, j, 0), mat_ptr<ENC>(p, j, 1)};
   const int ngrp = p.H / Enc<ENC>::EPG;
@@ -351,9 +366,9 @@ __device__ __forceinline__ void w13_tile(const GemvParams& p, const Job& j, int 
       const int sb = j.slot_off + min(t0 + 8 * n + g, j.n_tok - 1);
       const int s0 = j.slot_off + min(t0 + 8 * n + 2 * t, j.n_tok - 1);
       const int s1 = j.slot_off + min(t0 + 8 * n + 2 * t + 1, j.n_tok - 1);
-      X.b[n] = p.x_perm + (size_t)p.jt.slot_token[sb] * (p.H / 8);
-      X.s0[n] = p.xsum + (size_t)p.jt.slot_token[s0] * (p.H / 32);
-      X.s1[n] = p.xsum + (size_t)p.jt.slot_token[s1] * (p.H / 32);
+      X.b[n] = xp + (size_t)p.jt.slot_token[sb] * (p.H / 8);
+      X.s0[n] = xs + (size_t)p.jt.slot_token[s0] * (p.H / 32);
+      X.s1[n] = xs + (size_t)p.jt.slot_token[s1] * (p.H / 32);
     }
     float acc[2][NT][4];
 #pragma unroll
@@ -412,24 +427,46 @@ w13_kernel(const __grid_constant__ GemvParams p) {
   const int n_jobs = p.jt.hdr[0];
   const int tiles = p.F / 16;
   const int n_items = n_jobs * tiles;
+  if (blockIdx.x >= n_items) return;
+  // stage x (pair-permuted) and its block sums in shared memory when they fit
+  const uint4* xp = p.x_perm;
+  const float* xs = p.xsum;
+  const int nx16 = p.B * (p.H / 8), ns16 = p.B * (p.H / 32) / 4;
+  if ((nx16 + ns16) * 16 <= kXStage) {
+    uint4* st = reinterpret_cast<uint4*>(x_stage());
+    stage_copy(st, p.x_perm, nx16);
+    stage_copy(st + nx16, reinterpret_cast<const uint4*>(p.xsum), ns16);
+    __syncthreads();
+    xp = st;
+    xs = reinterpret_cast<const float*>(st + nx16);
+  }
   for (int it = 0;; ++it) {
     const int item = item_for(it);
     if (item >= n_items) break;
     const Job j = p.jt.jobs[item / tiles];
     const int row0 = (item % tiles) * 16;
     switch (j.enc) {
-      case HB_F16: w13_tile<HB_F16, NT>(p, j, row0); break;
-      case HB_Q8: w13_tile<HB_Q8, NT>(p, j, row0); break;
-      case HB_Q4: w13_tile<HB_Q4, NT>(p, j, row0); break;
-      default: w13_tile<HB_Q2, NT>(p, j, row0); break;
+      case HB_F16: w13_tile<HB_F16, NT>(p, j, row0, xp, xs); break;
+      case HB_Q8: w13_tile<HB_Q8, NT>(p, j, row0, xp, xs); break;
+      case HB_Q4: w13_tile<HB_Q4, NT>(p, j, row0, xp, xs); break;
+      default: w13_tile<HB_Q2, NT>(p, j, row0, xp, xs); break;
     }
   }
 }
 
 // ------------------------------------------------------------------ K2b
+// B-operand view of h for one W2 chunk: element k of slot s is at
+// hi[s*stride + k/8 ...] (stride in uint4), sums at sum[s*sstride + k/32].
+struct HView {
+  const uint4* hi;
+  const uint4* lo;
+  const float* sum;
+  size_t stride, sstride;
+};
+
 template <int ENC, int NT>
 __device__ __forceinline__ void w2_chunk(const GemvParams& p, const Job& j, int row0, int kbeg,
-                                         int kend, int s) {
+                                         int kend, int s, const HView& hv) {
   constexpr int EPG = Enc<ENC>::EPG;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const MatPtr M[1] = {mat_ptr<ENC>(p, j, 2)};
@@ -440,10 +477,10 @@ __device__ __forceinline__ void w2_chunk(const GemvParams& p, const Job& j, int 
       const int sb = j.slot_off + min(t0 + 8 * n + g, j.n_tok - 1);
       const int s0 = j.slot_off + min(t0 + 8 * n + 2 * t, j.n_tok - 1);
       const int s1 = j.slot_off + min(t0 + 8 * n + 2 * t + 1, j.n_tok - 1);
-      X.b[n] = p.h_hi + (size_t)sb * (p.F / 8);
-      X.blo[n] = p.h_lo + (size_t)sb * (p.F / 8);
-      X.s0[n] = p.hsum + (size_t)s0 * (p.F / 32);
-      X.s1[n] = p.hsum + (size_t)s1 * (p.F / 32);
+      X.b[n] = hv.hi + (size_t)sb * hv.stride;
+      X.blo[n] = hv.lo + (size_t)sb * hv.stride;
+      X.s0[n] = hv.sum + (size_t)s0 * hv.sstride;
+      X.s1[n] = hv.sum + (size_t)s1 * hv.sstride;
     }
     float acc[1][NT][4];
 #pragma unroll
@@ -471,23 +508,49 @@ __device__ __forceinline__ void w2_chunk(const GemvParams& p, const Job& j, int 
 template <int NT>
 __global__ void __launch_bounds__(kGemvWarps * 32, 1)
 w2_kernel(const __grid_constant__ GemvParams p) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n_jobs = p.jt.hdr[0];
+  const int n_slots = p.jt.hdr[1];
   const int tiles = p.H / 16;
-  const int n_items = tiles * p.S;
+  // every CTA works on ONE split-K chunk s (so its warps share the h chunk);
+  // the row tiles of chunk s are dealt over the CTAs with blockIdx % S == s
+  const int s = blockIdx.x % p.S;
+  const int nS = (gridDim.x - s + p.S - 1) / p.S;
+  const int cidx = blockIdx.x / p.S;
+  const int kbeg = s * p.chunk, kend = min(p.F, kbeg + p.chunk);
+  if (cidx >= tiles) return;
+  // stage the chunk of h (hi, lo, block sums) of every slot when it fits
+  HView hv{p.h_hi, p.h_lo, p.hsum, (size_t)p.F / 8, (size_t)p.F / 32};
+  const int clen = kend - kbeg;
+  const int nh16 = n_slots * (clen / 8), ns16 = n_slots * (clen / 32) / 4;
+  if (n_jobs > 0 && (2 * nh16 + ns16) * 16 <= kXStage) {
+    uint4* st = reinterpret_cast<uint4*>(x_stage());
+    for (int sl = 0; sl < n_slots; ++sl) {
+      stage_copy(st + sl * (clen / 8), p.h_hi + (size_t)sl * (p.F / 8) + kbeg / 8, clen / 8);
+      stage_copy(st + nh16 + sl * (clen / 8), p.h_lo + (size_t)sl * (p.F / 8) + kbeg / 8, clen / 8);
+      stage_copy(st + 2 * nh16 + sl * (clen / 32) / 4,
+                 reinterpret_cast<const uint4*>(p.hsum + (size_t)sl * (p.F / 32) + kbeg / 32),
+                 (clen / 32) / 4);
+    }
+    __syncthreads();
+    // views indexed by global k: shift the bases back by the chunk start
+    hv.hi = st - kbeg / 8;
+    hv.lo = st + nh16 - kbeg / 8;
+    hv.sum = reinterpret_cast<const float*>(st + 2 * nh16) - kbeg / 32;
+    hv.stride = clen / 8;
+    hv.sstride = clen / 32;
+  }
   for (int it = 0;; ++it) {
-    const int item = item_for(it);
-    if (item >= n_items) break;
-    const int tile = item / p.S, s = item % p.S;
+    const int tile = cidx + nS * (warp + kGemvWarps * it);
+    if (tile >= tiles) break;
     const int row0 = tile * 16;
-    const int kbeg = s * p.chunk, kend = min(p.F, kbeg + p.chunk);
     for (int jj = 0; jj < n_jobs; ++jj) {
       const Job j = p.jt.jobs[jj];
       switch (j.enc) {
-        case HB_F16: w2_chunk<HB_F16, NT>(p, j, row0, kbeg, kend, s); break;
-        case HB_Q8: w2_chunk<HB_Q8, NT>(p, j, row0, kbeg, kend, s); break;
-        case HB_Q4: w2_chunk<HB_Q4, NT>(p, j, row0, kbeg, kend, s); break;
-        default: w2_chunk<HB_Q2, NT>(p, j, row0, kbeg, kend, s); break;
+        case HB_F16: w2_chunk<HB_F16, NT>(p, j, row0, kbeg, kend, s, hv); break;
+        case HB_Q8: w2_chunk<HB_Q8, NT>(p, j, row0, kbeg, kend, s, hv); break;
+        case HB_Q4: w2_chunk<HB_Q4, NT>(p, j, row0, kbeg, kend, s, hv); break;
+        default: w2_chunk<HB_Q2, NT>(p, j, row0, kbeg, kend, s, hv); break;
       }
     }
     // the last chunk of this row tile reduces the S partials in order -> y

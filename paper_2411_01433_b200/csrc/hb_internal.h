@@ -13,7 +13,7 @@ constexpr int kMaxTopK = 8;
 constexpr int kMaxRouteLayers = 4;      // 1 + max lookahead p handled per launch
 constexpr int kNumSM = 148;             // B200
 constexpr int kGemvWarps = 16;          // warps per GEMV CTA (one CTA per SM)
-constexpr int kRouterThreads = 256;
+constexpr int kRouterThreads = 128;
 
 // Byte offsets of the sections of one matrix inside an expert blob.
 struct MatLayout {
@@ -55,7 +55,8 @@ struct RouterParams {
   double t1, t2;                       // k > 2 fp64 test
   int rank, world;
   hb_decision* dec;                    // [n_route][B][k]
-  long long* logits;                   // [B][E][2] for route 0, or null
+  long long* lbuf;                     // [n_route][B][E][2] exact logits (scratch)
+  long long* logits;                   // [B][E][2] copy for route 0, or null
   uint4* x_perm;                       // [B][H/8] pair-permuted x, or null
   float* xsum;                         // [B][H/32], or null
   float* zero_buf;                     // zeroed by the router grid (h block sums)
@@ -83,7 +84,7 @@ struct GemvParams {
   unsigned* tile_count;                // [H/16] (self-resetting)
 };
 
-void launch_router(const RouterParams& p, int grid, cudaStream_t s);
+void launch_router(const RouterParams& p, cudaStream_t s);
 void launch_w13(const GemvParams& p, int nt, cudaStream_t s);
 void launch_w2(const GemvParams& p, int nt, cudaStream_t s);
 int launch_quantize_expert(int enc, int hidden, int ffn, const __half* w1, const __half* w3,
