@@ -38,6 +38,9 @@ UNIT = "tokens/s"
 WORKLOAD = "mixtral-8x7b-shapes batch-1 decode, 32 layers, fp16/int4 strict (T1=0.6,T2=0.9), all experts resident"
 
 
+PAIRS = {"f16q4": (0, 2), "f16q2": (0, 3), "q8q2": (1, 3), "q8q4": (1, 2)}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -148,8 +151,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    shape = sg.MIXTRAL
-    hi, lo = h.HB_F16, h.HB_Q4
+    shape = {"mixtral": sg.MIXTRAL, "phi": sg.PHI}[args.model]
+    hi, lo = PAIRS[args.pair]
     L, Hd = shape.n_layers, shape.hidden
     t_init = time.time()
     ctx, blobs = build_model(h, sg, None, shape, hi, lo, rank, world, local)
@@ -325,8 +328,10 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f16 weights / q4 codes, fp32 accumulate", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": 1, "layers": L, "experts": shape.n_experts,
-                   "top_k": shape.top_k, "hidden": Hd, "ffn": shape.ffn, "pair": "F16/Q4",
+        "config": {"workload": WORKLOAD if (args.model, args.pair) == ("mixtral", "f16q4")
+                   else f"DIAGNOSTIC {shape.name} pair {args.pair} (not the headline workload)",
+                   "global_batch": 1, "layers": L, "experts": shape.n_experts,
+                   "top_k": shape.top_k, "hidden": Hd, "ffn": shape.ffn, "pair": args.pair,
                    "parallelism": f"ep{world}", "l2": "inputs > L2 (~17 GB of weights per step)",
                    "graph": use_graph},
         "e2e": {"value": round(1000.0 / ms_e2e, 3), "unit": UNIT,
@@ -444,6 +449,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2)
     ap.add_argument("--ref-max-steps", type=int, default=12)
+    ap.add_argument("--model", choices=["mixtral", "phi"], default="mixtral",
+                    help="diagnostics only: the headline is mixtral")
+    ap.add_argument("--pair", choices=sorted(PAIRS), default="f16q4",
+                    help="diagnostics only: the headline is f16q4")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -56,7 +56,6 @@ struct hb_ctx {
   bool resident = true;
   BlobLayout lay[4]{};
   size_t bbytes[4]{};
-  int S = 1, chunk = 256;
   // router weights [L][E][H]
   __half* wg = nullptr;
   std::vector<char> router_set;
@@ -83,8 +82,11 @@ struct hb_ctx {
   uint4* h_hi = nullptr;
   uint4* h_lo = nullptr;
   float* hsum = nullptr;
-  float* partial = nullptr;
-  unsigned* tile_count = nullptr;
+  float* part = nullptr;                  // stream-K pieces
+  float* ob = nullptr;                    // per-slot W2 outputs
+  unsigned* cnt13 = nullptr;              // piece / job counters (self-resetting)
+  unsigned* cnt2 = nullptr;
+  unsigned* cnty = nullptr;
   unsigned* done = nullptr;
   JobTable jt{};
   void* jt_dev = nullptr;
@@ -182,8 +184,8 @@ static void free_ctx(hb_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
-                   c->logits, c->lbuf, c->x_perm, c->xsum, c->h_hi, c->h_lo, c->hsum, c->partial,
-                   c->tile_count, c->done, c->jt_dev};
+                   c->logits, c->lbuf, c->x_perm, c->xsum, c->h_hi, c->h_lo, c->hsum, c->part,
+                   c->ob, c->cnt13, c->cnt2, c->cnty, c->done, c->jt_dev};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
@@ -231,15 +233,6 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     blob_layout(e, k.hidden, k.ffn, &c->lay[e]);
     c->bbytes[e] = c->lay[e].total;
   }
-  // W2 split-K: about 12 tiles per SM
-  const int tiles = k.hidden / 16;
-  const int groups = k.ffn / 256;
-  int S = (int)std::lround(kNumSM * 12.0 / tiles);
-  S = std::max(1, std::min(S, groups));
-  const int chunk_groups = (groups + S - 1) / S;
-  c->chunk = chunk_groups * 256;
-  c->S = (k.ffn + c->chunk - 1) / c->chunk;
-
   auto bail = [&](int code, const std::string& m) {
     g_err = m;
     free_ctx(c);
@@ -251,6 +244,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   const int P = std::max(1, k.lookahead_p);
   c->max_slots = B * K;
   c->max_jobs = std::min(2 * E, B * K) + 1;
+  const int max_vjobs = c->max_jobs + (c->max_slots + kVSlots - 1) / kVSlots + 1;
   auto dm = [&](void** p, size_t n) { return cudaMalloc(p, std::max<size_t>(n, 16)) == cudaSuccess; };
   bool ok = dm((void**)&c->wg, (size_t)L * E * H * 2) &&
             dm((void**)&c->dec, sizeof(hb_decision) * B * K) &&
@@ -261,16 +255,22 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
             dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->hsum, (size_t)c->max_slots * (F / 32) * 4) &&
-            dm((void**)&c->partial, (size_t)c->S * B * H * 4) &&
-            dm((void**)&c->tile_count, (size_t)(H / 16) * 4) && dm((void**)&c->done, 16);
+            dm((void**)&c->part, sizeof(float) * kGemvTotalWarps * 2 * 32 * kPartFloats) &&
+            dm((void**)&c->ob, (size_t)c->max_slots * H * 4) &&
+            dm((void**)&c->cnt13, sizeof(unsigned) * max_vjobs * (F / 16)) &&
+            dm((void**)&c->cnt2, sizeof(unsigned) * max_vjobs * (H / 16)) &&
+            dm((void**)&c->cnty, sizeof(unsigned) * (H / 16)) && dm((void**)&c->done, 16);
   if (!ok) return bail(HB_ENOMEM, "device allocation of scratch failed");
-  cudaMemset(c->tile_count, 0, (size_t)(H / 16) * 4);
+  cudaMemset(c->cnt13, 0, sizeof(unsigned) * max_vjobs * (F / 16));
+  cudaMemset(c->cnt2, 0, sizeof(unsigned) * max_vjobs * (H / 16));
+  cudaMemset(c->cnty, 0, sizeof(unsigned) * (H / 16));
   cudaMemset(c->done, 0, 16);
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
-  // job table: hdr | jobs | slot_token | slot_gate
+  // job table: hdr | jobs | slot_token | slot_gate | tok_slots
   const size_t o_jobs = 64, o_tok = align_up(o_jobs + sizeof(Job) * c->max_jobs, 64),
                o_gate = align_up(o_tok + 4 * (size_t)c->max_slots, 64),
-               total = align_up(o_gate + 4 * (size_t)c->max_slots, 64);
+               o_ts = align_up(o_gate + 4 * (size_t)c->max_slots, 64),
+               total = align_up(o_ts + 4 * (size_t)c->max_slots, 64);
   c->jt_bytes = total;
   if (!dm(&c->jt_dev, total) || cudaHostAlloc(&c->jt_host, total, cudaHostAllocDefault) != cudaSuccess)
     return bail(HB_ENOMEM, "job table allocation failed");
@@ -280,6 +280,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   c->jt.jobs = (Job*)(jb + o_jobs);
   c->jt.slot_token = (int32_t*)(jb + o_tok);
   c->jt.slot_gate = (float*)(jb + o_gate);
+  c->jt.tok_slots = (int32_t*)(jb + o_ts);
   if (cudaHostAlloc((void**)&c->dec_host, sizeof(hb_decision) * (1 + P) * B * K,
                     cudaHostAllocDefault) != cudaSuccess)
     return bail(HB_ENOMEM, "pinned decision buffer allocation failed");
@@ -414,28 +415,29 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
   g.H = k.hidden;
   g.F = k.ffn;
   g.B = batch;
+  g.k = k.top_k;
   g.x_perm = c->x_perm;
   g.xsum = c->xsum;
   g.h_hi = c->h_hi;
   g.h_lo = c->h_lo;
   g.hsum = c->hsum;
-  g.partial = c->partial;
-  g.partial_n = (long long)c->S * batch * k.hidden;
-  g.S = c->S;
-  g.chunk = c->chunk;
+  g.part = c->part;
+  g.ob = c->ob;
+  g.cnt13 = c->cnt13;
+  g.cnt2 = c->cnt2;
+  g.cnty = c->cnty;
   g.y = (float*)y;
-  g.tile_count = c->tile_count;
   return g;
 }
 
 // K2a + K2b, bracketed by timing events when hb_profile is on
-static void launch_gemv(hb_ctx* c, const GemvParams& gp, int nt, cudaStream_t s) {
+static void launch_gemv(hb_ctx* c, const GemvParams& gp, cudaStream_t s) {
   cudaEvent_t* ev = nullptr;
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
   if (ev) cudaEventRecord(ev[0], s);
-  launch_w13(gp, nt, s);
+  launch_w13(gp, s);
   if (ev) cudaEventRecord(ev[1], s);
-  launch_w2(gp, nt, s);
+  launch_w2(gp, s);
   if (ev) cudaEventRecord(ev[2], s);
   c->launches += 2;
 }
@@ -488,7 +490,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   rp.xsum = c->xsum;
   rp.zero_buf = c->hsum;
   rp.zero_n = (long long)batch * k.top_k * (k.ffn / 32);
-  const int nt = batch <= 1 ? 1 : 2;
+
   c->last_batch = batch;
   c->last_layer = layer;
 
@@ -497,7 +499,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
     launch_router(rp, s);
     c->launches += 1;
     GemvParams gp = gemv_params(c, batch, y);
-    launch_gemv(c, gp, nt, s);
+    launch_gemv(c, gp, s);
     c->last_host_decisions = false;
     CUDA_TRY(c, cudaGetLastError());
     return HB_OK;
@@ -535,10 +537,12 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   Job* jobs = (Job*)(jh + ((uint8_t*)c->jt.jobs - (uint8_t*)c->jt_dev));
   int32_t* stok = (int32_t*)(jh + ((uint8_t*)c->jt.slot_token - (uint8_t*)c->jt_dev));
   float* sgate = (float*)(jh + ((uint8_t*)c->jt.slot_gate - (uint8_t*)c->jt_dev));
+  int32_t* tslots = (int32_t*)(jh + ((uint8_t*)c->jt.tok_slots - (uint8_t*)c->jt_dev));
   int nj = 0;
   for (int i = 0; i < K; ++i) {
     c->dec_host[i].served_enc = served[i];
     c->dec_host[i].hit = hit[i];
+    tslots[i] = served[i] == HB_ENC_NONE ? -1 : nj;
     if (served[i] == HB_ENC_NONE) continue;
     Job j;
     j.blob = c->pool_mem[pool[i]] + (size_t)slot[i] * c->slot_bytes[pool[i]];
@@ -558,7 +562,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
     if (served[i] != HB_ENC_NONE)
       CUDA_TRY(c, cudaStreamWaitEvent(s, c->slot_ready[pool[i]][slot[i]], 0));
   GemvParams gp = gemv_params(c, batch, y);
-  launch_gemv(c, gp, nt, s);
+  launch_gemv(c, gp, s);
   for (int i = 0; i < K; ++i)
     if (served[i] != HB_ENC_NONE)
       CUDA_TRY(c, cudaEventRecord(c->slot_free[pool[i]][slot[i]], s));

@@ -7,25 +7,32 @@
 // (Eq. 1); a Low expert is computed from its low-precision version;
 // experts are SwiGLU FFNs (reading R10).  This is the B200 hot path: batch-1
 // decode streams 66-352 MB of expert weights per token-layer, so the kernels
-// are HBM-bound; their job is to keep ~6 MB of loads in flight while spending
-// ~2 or fewer thread-instructions per weight on dequantisation.
+// are HBM-bound; their job is to keep ~100 KB of loads in flight per SM on
+// every SM for the whole kernel while spending few instructions per weight.
 //
 // Structure:
-//  * persistent grid, one 512-thread CTA per SM; work items are 16-row tiles
-//    (K2a: of W1 and W3 together; K2b: of W2 x a split-K chunk of F), dealt
-//    round-robin over CTAs first so every SM gets the same number of tiles;
-//  * each warp streams its tile through a private multi-stage shared-memory
-//    ring with cp.async.cg (16 B per lane per row, L1 bypassed, L2
-//    evict-first), so ~96 KB per SM are in flight without holding registers;
-//    a "group" is 64 bytes of one row, and lane t's 16 bytes of it hold its
-//    share of every block of the group;
+//  * warp-level STREAM-K.  The work of a launch is a sequence of UNITS, one
+//    unit = one 64-byte group of the 16 rows of a row tile (of W1 and W3
+//    together for K2a), ordered (virtual job, tile, group).  Every unit moves
+//    the same number of weight bytes whatever the encoding, so giving each of
+//    the 148 x 16 warps an equal contiguous range of units balances HBM
+//    traffic to within one unit.  A warp streams its range as ONE pipeline
+//    (no drain at tile boundaries); a tile split between warps leaves
+//    "pieces" that the last-arriving warp adds up in warp order
+//    (deterministic), then applies the epilogue;
+//  * each warp owns a multi-stage shared-memory ring filled with cp.async:
+//    its 16 bytes of the two rows g, g+8 of each unit (L1 bypassed, L2
+//    evict-first), the block scales, and the B fragments (x or h, at most two
+//    token slots at batch 1);
 //  * the dot products run on the tensor cores as mma.sync.m16n8k16 with the
 //    weights as A (16 rows x 16 k) and up to 8 token slots as B: dequantised
 //    codes are EXACT in fp16 (q-8, q, int8 q), so every per-block partial sum
 //    is an fp32 sum of exact products; the block scale is applied in fp32
 //    after each 32-element block (acc += d*D_b (+ m*S_b for Q2));
 //  * x and h are stored "pair-permuted" (Q_c = (v[8t+c], v[8t+c+4])) so that
-//    the B fragment is one 16-byte load per block and lane;
+//    the B fragment is one 16-byte load per block and lane, and the blob
+//    layout puts lane t's share of every block of a group in bytes
+//    [16t, 16t+16);
 //  * K2b takes h as an fp16 hi/lo pair (h = hi + lo to ~2^-22) and issues two
 //    MMAs per k-step, so W2 sees h at ~fp32 precision.
 #include <cuda_fp16.h>
@@ -38,9 +45,12 @@ namespace hb {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
+__device__ __forceinline__ void cp_async16_ef(uint32_t dst, const void* src, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
                :: "r"(dst), "l"(src), "l"(pol));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src));
 }
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src));
@@ -66,6 +76,11 @@ __device__ __forceinline__ float lds_half(uint32_t a) {
   unsigned short v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
   return __half2float(__ushort_as_half(v));
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
 }
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
@@ -123,14 +138,27 @@ template <> struct Enc<HB_Q8>  { static constexpr int BPG = 2, EPG = 64,  SB = 4
 template <> struct Enc<HB_Q4>  { static constexpr int BPG = 4, EPG = 128, SB = 8;  };
 template <> struct Enc<HB_Q2>  { static constexpr int BPG = 8, EPG = 256, SB = 32; };
 
-constexpr int kWarpSmem = 12 * 1024;                    // per-warp cp.async ring
-constexpr int kXStage = 24 * 1024;                      // CTA-shared copy of x / h chunk
-constexpr int kGemvSmem = kGemvWarps * kWarpSmem + kXStage;   // 216 KB per CTA
+__host__ __device__ constexpr int epg_of(int enc) {
+  return enc == HB_F16 ? 32 : enc == HB_Q8 ? 64 : enc == HB_Q4 ? 128 : 256;
+}
 
-// B-operand load: a generic 16-byte load (the source is either the CTA's
-// shared-memory stage of x / h or, when it does not fit, global memory).
-__device__ __forceinline__ uint4 ldx(const uint4* p) { return *p; }
-__device__ __forceinline__ float ldxf(const float* p) { return *p; }
+constexpr int kWarpSmem = 13 * 1024;                    // per-warp cp.async ring
+constexpr int kGemvSmem = kGemvWarps * kWarpSmem;       // 208 KB per CTA
+constexpr int kXSlots = 2;                              // token slots staged in the ring
+
+// Ring stage layout of one unit: W codes | S scales | X B-fragments | Z block sums
+template <int ENC, int NMAT, bool SPLIT>
+struct Ring {
+  static constexpr int BPG = Enc<ENC>::BPG, SB = Enc<ENC>::SB;
+  static constexpr int XS = SPLIT ? 2 : 1;
+  static constexpr int W = NMAT * 1024;
+  static constexpr int S = NMAT * 16 * SB;
+  static constexpr int X = XS * kXSlots * BPG * 64;
+  static constexpr int Z = ENC == HB_Q2 ? kXSlots * BPG * 4 : 0;
+  static constexpr int STAGE = (W + S + X + Z + 127) / 128 * 128;
+  static constexpr int DEPTH = kWarpSmem / STAGE >= 16 ? 16 : kWarpSmem / STAGE;
+  static_assert(DEPTH >= 2, "ring too small");
+};
 
 // Dequantise block `blk` of the lane's 16-byte share into P0..P3, the fp16
 // pairs (w[8t+c], w[8t+c+4]) with the codes' exact integer values (scale
@@ -167,409 +195,396 @@ __device__ __forceinline__ void dequant(const uint4& v, int blk, uint32_t (&P)[4
   }
 }
 
-// One matrix of an expert blob.
-struct MatPtr {
-  const uint8_t* q;      // codes
-  const __half* d;       // scales [N][K/32]
-  const __half* m;       // mins   [N][K/32]
+// ---------------------------------------------------------- work space
+// Virtual job: one job's token slots [slot0, slot0 + nslot), nslot <= kVSlots.
+struct VJob {
+  const uint8_t* blob;
+  int enc;
+  int slot0;
+  int nslot;
 };
 
-// Token-slot sources of the B fragment (x or h) for NT 8-slot tiles.
-template <int NT, bool SPLIT>
-struct XSrc {
-  const uint4* b[NT];      // row of slot (tile*8 + g): pair-permuted, uint4 per (block, t)
-  const uint4* blo[NT];    // SPLIT: residual part
-  const float* s0[NT];     // block sums of slots tile*8 + 2t and +1 (Q2 only)
-  const float* s1[NT];
-};
-
-// Stream groups [g0, g1) of NMAT matrices (same rows, same K) against the
-// slots in X; accumulate acc[m][n][4] (rows g,g+8 x slots 2t,2t+1).
-// wsm: shared address of this warp's kWarpSmem-byte ring.
-template <int ENC, int NMAT, int NT, bool SPLIT>
-__device__ __forceinline__ void mainloop(uint32_t wsm, const MatPtr (&M)[NMAT], int K, int row0,
-                                         int g0, int g1, const XSrc<NT, SPLIT>& X,
-                                         float (&acc)[NMAT][NT][4]) {
-  constexpr int BPG = Enc<ENC>::BPG, SB = Enc<ENC>::SB;
-  constexpr int CODE = 16 * 64;                         // 16 rows x 64 B per matrix
-  constexpr int SCALE = 16 * SB;
-  constexpr int STAGE = NMAT * (CODE + SCALE);
-  constexpr int DEPTH = kWarpSmem / STAGE >= 8 ? 8 : kWarpSmem / STAGE;
-  static_assert(DEPTH >= 2, "ring too small");
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const size_t rowbytes = ENC == HB_F16 ? (size_t)K * 2 : ENC == HB_Q8 ? (size_t)K
-                        : ENC == HB_Q4 ? (size_t)K / 2 : (size_t)K / 4;
-  const int nb = K / 32;                                 // blocks (scales) per row
-  const uint64_t pol = evict_first_policy();
-  // producer: the lane copies rows g and g+8, bytes [16t, 16t+16) of each
-  // group (exactly the bytes it consumes); scales: one lane per (row, part).
-  const uint8_t* src[NMAT];
-#pragma unroll
-  for (int m = 0; m < NMAT; ++m) src[m] = M[m].q + (size_t)(row0 + g) * rowbytes + 16 * t;
-  const size_t src8 = 8 * rowbytes;
-  const int srow = lane & 15;                            // scale row of this lane
-  const bool sact = ENC == HB_Q2 ? true : lane < 16;
-  const __half* ssrc[NMAT];
-#pragma unroll
-  for (int m = 0; m < NMAT; ++m) {
-    const __half* base = (ENC == HB_Q2 && lane >= 16) ? M[m].m : M[m].d;
-    ssrc[m] = base + (size_t)(row0 + srow) * nb;
-  }
-
-  auto issue = [&](int grp) {
-    if (grp < g1) {
-      const uint32_t st = wsm + (grp % DEPTH) * STAGE;
-#pragma unroll
-      for (int m = 0; m < NMAT; ++m) {
-        const uint8_t* s = src[m] + (size_t)grp * 64;
-        cp_async16(st + m * CODE + g * 64 + 16 * t, s, pol);
-        cp_async16(st + m * CODE + (g + 8) * 64 + 16 * t, s + src8, pol);
-        if constexpr (SB > 0) {
-          const uint32_t sd = st + NMAT * CODE + m * SCALE;
-          if (sact) {
-            if constexpr (ENC == HB_Q8) cp_async4(sd + srow * SB, ssrc[m] + grp * BPG);
-            else if constexpr (ENC == HB_Q4) cp_async8(sd + srow * SB, ssrc[m] + grp * BPG);
-            else cp_async16(sd + srow * SB + (lane >> 4) * 16, ssrc[m] + grp * BPG, pol);
-          }
-        }
-      }
+__device__ __forceinline__ int n_vjobs(const GemvParams& p) {
+  const int nj = p.jt.hdr[0];
+  int nv = 0;
+  for (int j = 0; j < nj; ++j) nv += (p.jt.jobs[j].n_tok + kVSlots - 1) / kVSlots;
+  return nv;
+}
+__device__ __forceinline__ VJob get_vjob(const GemvParams& p, int v) {
+  const int nj = p.jt.hdr[0];
+  for (int j = 0; j < nj; ++j) {
+    const Job& J = p.jt.jobs[j];
+    const int np = (J.n_tok + kVSlots - 1) / kVSlots;
+    if (v < np) {
+      VJob r;
+      r.blob = J.blob;
+      r.enc = J.enc;
+      r.slot0 = J.slot_off + v * kVSlots;
+      r.nslot = min(kVSlots, J.n_tok - v * kVSlots);
+      return r;
     }
-    cp_commit();
-  };
-
-#pragma unroll
-  for (int s = 0; s < DEPTH - 1; ++s) issue(g0 + s);
-
-  for (int grp = g0; grp < g1; ++grp) {
-    __syncwarp();                                  // slot (grp-1)%DEPTH fully consumed
-    issue(grp + DEPTH - 1);
-    cp_wait<DEPTH - 1>();
-    __syncwarp();                                  // everyone's copies of grp visible
-    const uint32_t st = wsm + (grp % DEPTH) * STAGE;
-    uint4 w[NMAT][2];
-#pragma unroll
-    for (int m = 0; m < NMAT; ++m)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) w[m][h] = lds128(st + m * CODE + (g + 8 * h) * 64 + 16 * t);
-#pragma unroll
-    for (int blk = 0; blk < BPG; ++blk) {
-      const int gblk = grp * BPG + blk;            // block index along K
-      uint4 xb[NT], xl[NT];
-#pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        xb[n] = ldx(X.b[n] + gblk * 4 + t);
-        if constexpr (SPLIT) xl[n] = ldx(X.blo[n] + gblk * 4 + t);
-      }
-      float s0[NT], s1[NT];
-      if constexpr (ENC == HB_Q2) {
-#pragma unroll
-        for (int n = 0; n < NT; ++n) { s0[n] = ldxf(X.s0[n] + gblk); s1[n] = ldxf(X.s1[n] + gblk); }
-      }
-#pragma unroll
-      for (int m = 0; m < NMAT; ++m) {
-        uint32_t Pg[4], Ph[4];
-        dequant<ENC>(w[m][0], blk, Pg);
-        dequant<ENC>(w[m][1], blk, Ph);
-        float dg = 1.f, dh = 1.f, mg = 0.f, mh = 0.f;
-        if constexpr (SB > 0) {
-          const uint32_t sd = st + NMAT * CODE + m * SCALE;
-          dg = lds_half(sd + g * SB + 2 * blk);
-          dh = lds_half(sd + (g + 8) * SB + 2 * blk);
-          if constexpr (ENC == HB_Q2) {
-            mg = lds_half(sd + g * SB + 16 + 2 * blk);
-            mh = lds_half(sd + (g + 8) * SB + 16 + 2 * blk);
-          }
-        }
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          if constexpr (ENC == HB_F16) {
-            mma16816(acc[m][n], Pg[0], Ph[0], Pg[1], Ph[1], xb[n].x, xb[n].y);
-            mma16816(acc[m][n], Pg[2], Ph[2], Pg[3], Ph[3], xb[n].z, xb[n].w);
-            if constexpr (SPLIT) {
-              mma16816(acc[m][n], Pg[0], Ph[0], Pg[1], Ph[1], xl[n].x, xl[n].y);
-              mma16816(acc[m][n], Pg[2], Ph[2], Pg[3], Ph[3], xl[n].z, xl[n].w);
-            }
-          } else {
-            float D[4] = {0.f, 0.f, 0.f, 0.f};
-            mma16816(D, Pg[0], Ph[0], Pg[1], Ph[1], xb[n].x, xb[n].y);
-            mma16816(D, Pg[2], Ph[2], Pg[3], Ph[3], xb[n].z, xb[n].w);
-            if constexpr (SPLIT) {
-              mma16816(D, Pg[0], Ph[0], Pg[1], Ph[1], xl[n].x, xl[n].y);
-              mma16816(D, Pg[2], Ph[2], Pg[3], Ph[3], xl[n].z, xl[n].w);
-            }
-            acc[m][n][0] = fmaf(dg, D[0], acc[m][n][0]);
-            acc[m][n][1] = fmaf(dg, D[1], acc[m][n][1]);
-            acc[m][n][2] = fmaf(dh, D[2], acc[m][n][2]);
-            acc[m][n][3] = fmaf(dh, D[3], acc[m][n][3]);
-            if constexpr (ENC == HB_Q2) {               // + m_row * sum_block(x)
-              acc[m][n][0] = fmaf(mg, s0[n], acc[m][n][0]);
-              acc[m][n][1] = fmaf(mg, s1[n], acc[m][n][1]);
-              acc[m][n][2] = fmaf(mh, s0[n], acc[m][n][2]);
-              acc[m][n][3] = fmaf(mh, s1[n], acc[m][n][3]);
-            }
-          }
-        }
-      }
-    }
+    v -= np;
   }
-  cp_wait<0>();
-  __syncwarp();
+  return VJob{nullptr, 0, 0, 0};
 }
 
+// Warp ranges: warp w owns units [b(w), b(w+1)), b(w) = floor(w*U/NW).
+struct Space {
+  long long U;
+  int NW;
+  __device__ __forceinline__ long long b(int w) const { return (long long)w * U / NW; }
+  __device__ __forceinline__ int owner(long long u) const {
+    int w = (int)((u * NW) / U);
+    while (w + 1 < NW && b(w + 1) <= u) ++w;
+    while (w > 0 && b(w) > u) --w;
+    return w;
+  }
+};
+
+// ------------------------------------------------------------ epilogues
 // position of element f of a row in the pair-permuted layout (in halves)
 __device__ __forceinline__ int perm_pos(int f) {
   const int r8 = f & 31, t = r8 >> 3, r = r8 & 7;
   return (f & ~31) + 8 * t + 2 * (r & 3) + (r >> 2);
 }
 
-__device__ __forceinline__ int item_for(int it) {
-  // item index of iteration `it` of this warp: CTAs first, then warps, so that
-  // consecutive items land on different SMs.
-  const int warp = threadIdx.x >> 5;
-  return blockIdx.x + gridDim.x * (warp + kGemvWarps * it);
+// K2a: h = silu(a) * u for rows row0+g(+8), slots 2t, 2t+1 of the vjob
+__device__ void finalize13(const GemvParams& p, const VJob& vj, int row0, const float (&acc)[2][4]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  float hs[2] = {0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int sl = 2 * t + (i & 1);
+    const int f = row0 + g + 8 * (i >> 1);
+    const float a = acc[0][i], u = acc[1][i];
+    const float h = a / (1.f + expf(-a)) * u;
+    if (sl < vj.nslot) {
+      const int slot = vj.slot0 + sl;
+      const __half hh = __float2half_rn(h);
+      const __half hl = __float2half_rn(h - __half2float(hh));
+      reinterpret_cast<__half*>(p.h_hi)[(size_t)slot * p.F + perm_pos(f)] = hh;
+      reinterpret_cast<__half*>(p.h_lo)[(size_t)slot * p.F + perm_pos(f)] = hl;
+      hs[i & 1] += h;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {          // 16 rows of the tile, per slot
+    hs[0] += __shfl_xor_sync(0xffffffffu, hs[0], o);
+    hs[1] += __shfl_xor_sync(0xffffffffu, hs[1], o);
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      if (2 * t + c < vj.nslot)     // two tiles per 32-row block: fl(fl(0+a)+b) is order-free
+        atomicAdd(p.hsum + (size_t)(vj.slot0 + 2 * t + c) * (p.F / 32) + row0 / 32, hs[c]);
+  }
+}
+
+// K2b: o -> ob[slot][rows]; the last job of this H tile writes y (fixed order)
+__device__ void finalize2(const GemvParams& p, const VJob& vj, int tile, int nv,
+                          const float (&acc)[1][4]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int row0 = tile * 16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int sl = 2 * t + (i & 1);
+    if (sl < vj.nslot)
+      p.ob[(size_t)(vj.slot0 + sl) * p.H + row0 + g + 8 * (i >> 1)] = acc[0][i];
+  }
+  __syncwarp();
+  __threadfence();
+  unsigned prev = 0;
+  if (lane == 0) prev = atomicAdd(p.cnty + tile, 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != (unsigned)(nv - 1)) return;
+  __threadfence();
+  for (int e = lane; e < 16 * p.B; e += 32) {            // Eq. 1, ranks in order
+    const int tok = e >> 4, r = row0 + (e & 15);
+    float v = 0.f;
+    for (int i = 0; i < p.k; ++i) {
+      const int s = p.jt.tok_slots[tok * p.k + i];
+      if (s >= 0) v = fmaf(p.jt.slot_gate[s], __ldcg(p.ob + (size_t)s * p.H + r), v);
+    }
+    p.y[(size_t)tok * p.H + r] = v;
+  }
+  if (lane == 0) p.cnty[tile] = 0u;
+}
+
+// ------------------------------------------------------------ the run
+// Stream units [a, b) of virtual job v (unit l = tile * G + grp) through the
+// warp's ring.  W13: K2a (W1 and W3 rows, x); else K2b (W2 rows, h hi/lo).
+template <int ENC, bool W13, bool XR>
+__device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long long cum,
+                    long long a, long long b, const Space& sp, int gw, uint32_t ring) {
+  constexpr int NMAT = W13 ? 2 : 1;
+  constexpr bool SPLIT = !W13;
+  using R = Ring<ENC, NMAT, SPLIT>;
+  constexpr int BPG = R::BPG, SB = R::SB, XS = R::XS, DEPTH = R::DEPTH;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int K = W13 ? p.H : p.F;
+  const int G = K / Enc<ENC>::EPG;
+  const int nb = K / 32;
+  const size_t rowbytes = ENC == HB_F16 ? (size_t)K * 2 : ENC == HB_Q8 ? (size_t)K
+                        : ENC == HB_Q4 ? (size_t)K / 2 : (size_t)K / 4;
+  const uint64_t pol = evict_first_policy();
+  // matrices
+  const uint8_t* q0[NMAT];
+  const __half* d0[NMAT];
+  const __half* m0[NMAT];
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m) {
+    const MatLayout& L = p.lay[ENC].mat[W13 ? m : 2];
+    q0[m] = vj.blob + L.q + (size_t)g * rowbytes + 16 * t;        // row g of tile 0
+    d0[m] = reinterpret_cast<const __half*>(vj.blob + L.d);
+    m0[m] = reinterpret_cast<const __half*>(vj.blob + L.m);
+  }
+  const size_t q8 = 8 * rowbytes, qtile = 16 * rowbytes;
+  // B-operand sources per slot (x or h hi/lo) and block sums
+  const int ns = vj.nslot;
+  const uint4* xsrc[XS][kVSlots];
+  const float* zsrc[kVSlots];
+#pragma unroll
+  for (int s = 0; s < kVSlots; ++s) {
+    const int sl = vj.slot0 + min(s, ns - 1);
+    if constexpr (W13) {
+      const int tok = p.jt.slot_token[sl];
+      xsrc[0][s] = p.x_perm + (size_t)tok * (p.H / 8);
+      zsrc[s] = p.xsum + (size_t)tok * (p.H / 32);
+    } else {
+      xsrc[0][s] = p.h_hi + (size_t)sl * (p.F / 8);
+      xsrc[XS - 1][s] = p.h_lo + (size_t)sl * (p.F / 8);
+      zsrc[s] = p.hsum + (size_t)sl * (p.F / 32);
+    }
+  }
+  // producer state
+  long long pl = a;
+  int p_tile = (int)(a / G), p_grp = (int)(a % G);
+  int pslot = 0;
+  auto issue = [&]() {
+    if (pl < b) {
+      const uint32_t st = ring + pslot * R::STAGE;
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) {
+        const uint8_t* s = q0[m] + (size_t)p_tile * qtile + (size_t)p_grp * 64;
+        cp_async16_ef(st + m * 1024 + g * 64 + 16 * t, s, pol);
+        cp_async16_ef(st + m * 1024 + (g + 8) * 64 + 16 * t, s + q8, pol);
+        if constexpr (SB > 0) {
+          const uint32_t sd = st + R::W + m * 16 * SB;
+          const int srow = lane & 15;
+          const size_t so = (size_t)(p_tile * 16 + srow) * nb + p_grp * BPG;
+          if constexpr (ENC == HB_Q8) { if (lane < 16) cp_async4(sd + srow * SB, d0[m] + so); }
+          else if constexpr (ENC == HB_Q4) { if (lane < 16) cp_async8(sd + srow * SB, d0[m] + so); }
+          else cp_async16_ef(sd + srow * SB + (lane >> 4) * 16, (lane < 16 ? d0[m] : m0[m]) + so, pol);
+        }
+      }
+      if constexpr (XR) {
+        const uint32_t sx = st + R::W + R::S;
+        const int ncp = BPG * ns * XS * 4;
+        for (int c = lane; c < ncp; c += 32) {
+          const int tt = c & 3;
+          int r = c >> 2;
+          const int part = r % XS;
+          r /= XS;
+          const int sl = r % ns, blk = r / ns;
+          cp_async16(sx + ((part * kXSlots + sl) * BPG + blk) * 64 + tt * 16,
+                     xsrc[part][sl] + (size_t)(p_grp * BPG + blk) * 4 + tt);
+        }
+        if constexpr (ENC == HB_Q2) {
+          if (lane < ns * BPG) {
+            const int sl = lane / BPG, blk = lane % BPG;
+            cp_async4(sx + R::X + (sl * BPG + blk) * 4, zsrc[sl] + p_grp * BPG + blk);
+          }
+        }
+      }
+      ++pl;
+      if (++p_grp == G) { p_grp = 0; ++p_tile; }
+      if (++pslot == DEPTH) pslot = 0;
+    }
+    cp_commit();
+  };
+
+#pragma unroll 1
+  for (int s = 0; s < DEPTH - 1; ++s) issue();
+
+  float acc[NMAT][4];
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
+  int c_tile = (int)(a / G), c_grp = (int)(a % G), piece0 = c_grp;
+  int cslot = 0;
+  const int xg = min(g, ns - 1), z0 = min(2 * t, ns - 1), z1 = min(2 * t + 1, ns - 1);
+
+  for (long long l = a; l < b; ++l) {
+    __syncwarp();                                  // slot being refilled is consumed
+    issue();
+    cp_wait<DEPTH - 1>();
+    __syncwarp();                                  // everyone's copies of unit l visible
+    const uint32_t st = ring + cslot * R::STAGE;
+    if (++cslot == DEPTH) cslot = 0;
+    uint4 w[NMAT][2];
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+      w[m][0] = lds128(st + m * 1024 + g * 64 + 16 * t);
+      w[m][1] = lds128(st + m * 1024 + (g + 8) * 64 + 16 * t);
+    }
+#pragma unroll
+    for (int blk = 0; blk < BPG; ++blk) {
+      uint4 xb, xl;
+      float s0 = 0.f, s1 = 0.f;
+      if constexpr (XR) {
+        const uint32_t sx = st + R::W + R::S;
+        xb = lds128(sx + ((0 * kXSlots + xg) * BPG + blk) * 64 + t * 16);
+        if constexpr (SPLIT) xl = lds128(sx + ((1 * kXSlots + xg) * BPG + blk) * 64 + t * 16);
+        if constexpr (ENC == HB_Q2) {
+          s0 = lds_f32(sx + R::X + (z0 * BPG + blk) * 4);
+          s1 = lds_f32(sx + R::X + (z1 * BPG + blk) * 4);
+        }
+      } else {
+        const size_t gb = (size_t)(c_grp * BPG + blk);
+        xb = __ldg(xsrc[0][xg] + gb * 4 + t);
+        if constexpr (SPLIT) xl = __ldg(xsrc[XS - 1][xg] + gb * 4 + t);
+        if constexpr (ENC == HB_Q2) { s0 = __ldg(zsrc[z0] + gb); s1 = __ldg(zsrc[z1] + gb); }
+      }
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) {
+        uint32_t Pg[4], Ph[4];
+        dequant<ENC>(w[m][0], blk, Pg);
+        dequant<ENC>(w[m][1], blk, Ph);
+        if constexpr (ENC == HB_F16) {
+          mma16816(acc[m], Pg[0], Ph[0], Pg[1], Ph[1], xb.x, xb.y);
+          mma16816(acc[m], Pg[2], Ph[2], Pg[3], Ph[3], xb.z, xb.w);
+          if constexpr (SPLIT) {
+            mma16816(acc[m], Pg[0], Ph[0], Pg[1], Ph[1], xl.x, xl.y);
+            mma16816(acc[m], Pg[2], Ph[2], Pg[3], Ph[3], xl.z, xl.w);
+          }
+        } else {
+          const uint32_t sd = st + R::W + m * 16 * SB;
+          const float dg = lds_half(sd + g * SB + 2 * blk);
+          const float dh = lds_half(sd + (g + 8) * SB + 2 * blk);
+          float D[4] = {0.f, 0.f, 0.f, 0.f};
+          mma16816(D, Pg[0], Ph[0], Pg[1], Ph[1], xb.x, xb.y);
+          mma16816(D, Pg[2], Ph[2], Pg[3], Ph[3], xb.z, xb.w);
+          if constexpr (SPLIT) {
+            mma16816(D, Pg[0], Ph[0], Pg[1], Ph[1], xl.x, xl.y);
+            mma16816(D, Pg[2], Ph[2], Pg[3], Ph[3], xl.z, xl.w);
+          }
+          acc[m][0] = fmaf(dg, D[0], acc[m][0]);
+          acc[m][1] = fmaf(dg, D[1], acc[m][1]);
+          acc[m][2] = fmaf(dh, D[2], acc[m][2]);
+          acc[m][3] = fmaf(dh, D[3], acc[m][3]);
+          if constexpr (ENC == HB_Q2) {               // + m_row * sum_block(x)
+            const float mg = lds_half(sd + g * SB + 16 + 2 * blk);
+            const float mh = lds_half(sd + (g + 8) * SB + 16 + 2 * blk);
+            acc[m][0] = fmaf(mg, s0, acc[m][0]);
+            acc[m][1] = fmaf(mg, s1, acc[m][1]);
+            acc[m][2] = fmaf(mh, s0, acc[m][2]);
+            acc[m][3] = fmaf(mh, s1, acc[m][3]);
+          }
+        }
+      }
+    }
+    // ---- end of a tile piece?
+    if (c_grp == G - 1 || l == b - 1) {
+      const long long gu0 = cum + (long long)c_tile * G, gu1 = gu0 + G;
+      if (piece0 == 0 && c_grp == G - 1) {
+        if constexpr (W13) finalize13(p, vj, c_tile * 16, acc);
+        else finalize2(p, vj, c_tile, nv, acc);
+      } else {
+        // partial piece: store, count, the last piece's warp adds all in warp order
+        const int pslot_k = sp.b(gw) >= gu0 ? 0 : 1;
+        float* dst = p.part + (((size_t)gw * 2 + pslot_k) * 32 + lane) * kPartFloats;
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m)
+          *reinterpret_cast<float4*>(dst + 4 * m) = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
+        __syncwarp();
+        __threadfence();
+        const int wa = sp.owner(gu0), wb = sp.owner(gu1 - 1);
+        unsigned* cnt = (W13 ? p.cnt13 + (size_t)v * (p.F / 16) : p.cnt2 + (size_t)v * (p.H / 16)) + c_tile;
+        unsigned prev = 0;
+        if (lane == 0) prev = atomicAdd(cnt, 1u);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == (unsigned)(wb - wa)) {
+          __threadfence();
+          float sum[NMAT][4];
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) sum[m][i] = 0.f;
+          for (int w2 = wa; w2 <= wb; ++w2) {
+            const int ks = sp.b(w2) >= gu0 ? 0 : 1;
+            const float* src = p.part + (((size_t)w2 * 2 + ks) * 32 + lane) * kPartFloats;
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) {
+              const float4 q = __ldcg(reinterpret_cast<const float4*>(src + 4 * m));
+              sum[m][0] += q.x; sum[m][1] += q.y; sum[m][2] += q.z; sum[m][3] += q.w;
+            }
+          }
+          if (lane == 0) *cnt = 0u;
+          if constexpr (W13) finalize13(p, vj, c_tile * 16, sum);
+          else finalize2(p, vj, c_tile, nv, sum);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
+      piece0 = 0;
+    }
+    if (++c_grp == G) { c_grp = 0; ++c_tile; }
+  }
+  cp_wait<0>();
+  __syncwarp();
 }
 
 extern __shared__ __align__(128) uint8_t gemv_smem[];
 
-__device__ __forceinline__ uint32_t warp_smem() {
-  return smem_u32(gemv_smem) + (threadIdx.x >> 5) * kWarpSmem;
-}
-// the CTA-shared stage of the B operand (after the warps' rings)
-__device__ __forceinline__ uint8_t* x_stage() { return gemv_smem + kGemvWarps * kWarpSmem; }
-
-// CTA-wide copy of n16 16-byte words (global -> shared)
-__device__ __forceinline__ void stage_copy(uint4* dst, const uint4* src, int n16) {
-  for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldcg(src + i);
-}
-
-template <int ENC>
-__device__ __forceinline__ MatPtr mat_ptr(const GemvParams& p, const Job& j, int mat) {
-  const MatLayout& L = p.lay[ENC].mat[mat];
-  MatPtr r;
-  r.q = j.blob + L.q;
-  r.d = reinterpret_cast<const __half*>(j.blob + L.d);
-  r.m = reinterpret_cast<const __half*>(j.blob + L.m);
-  return r;
-}
-
-// ------------------------------------------------------------------ K2a
-template <int ENC, int NT>
-__device__ __forceinline__ void w13_tile(const GemvParams& p, const Job& j, int row0,
-                                         const uint4* xp, const float* xs) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const MatPtr M[2] = {mat_ptr<ENC>(p, j, 0), mat_ptr<ENC>(p, j, 1)};
-  const int ngrp = p.H / Enc<ENC>::EPG;
-  for (int t0 = 0; t0 < j.n_tok; t0 += 8 * NT) {
-    XSrc<NT, false> X;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const int sb = j.slot_off + min(t0 + 8 * n + g, j.n_tok - 1);
-      const int s0 = j.slot_off + min(t0 + 8 * n + 2 * t, j.n_tok - 1);
-      const int s1 = j.slot_off + min(t0 + 8 * n + 2 * t + 1, j.n_tok - 1);
-      X.b[n] = xp + (size_t)p.jt.slot_token[sb] * (p.H / 8);
-      X.s0[n] = xs + (size_t)p.jt.slot_token[s0] * (p.H / 32);
-      X.s1[n] = xs + (size_t)p.jt.slot_token[s1] * (p.H / 32);
-    }
-    float acc[2][NT][4];
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int n = 0; n < NT; ++n)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[m][n][i] = 0.f;
-    mainloop<ENC, 2, NT, false>(warp_smem(), M, p.H, row0, 0, ngrp, X, acc);
-    // epilogue: h = silu(a) * u, stored as pair-permuted fp16 hi + lo; block sums
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      float hs[2] = {0.f, 0.f};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int slot_rel = t0 + 8 * n + 2 * t + (i & 1);
-        const int f = row0 + g + 8 * (i >> 1);
-        const float a = acc[0][n][i], u = acc[1][n][i];
-        const float h = a / (1.f + expf(-a)) * u;
-        if (slot_rel < j.n_tok) {
-          const int slot = j.slot_off + slot_rel;
-          const __half hh = __float2half_rn(h);
-          const __half hl = __float2half_rn(h - __half2float(hh));
-          __half* hi = reinterpret_cast<__half*>(p.h_hi) + (size_t)slot * p.F;
-          __half* lo = reinterpret_cast<__half*>(p.h_lo) + (size_t)slot * p.F;
-          hi[perm_pos(f)] = hh;
-          lo[perm_pos(f)] = hl;
-          hs[i & 1] += h;
-        }
-      }
-      // reduce the 16 rows of this tile (lanes with equal t) -> 2 slots per t
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        hs[0] += __shfl_xor_sync(0xffffffffu, hs[0], o);
-        hs[1] += __shfl_xor_sync(0xffffffffu, hs[1], o);
-      }
-      if (g == 0) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int slot_rel = t0 + 8 * n + 2 * t + c;
-          if (slot_rel < j.n_tok)
-            atomicAdd(p.hsum + (size_t)(j.slot_off + slot_rel) * (p.F / 32) + row0 / 32, hs[c]);
-        }
-      }
-    }
-  }
-}
-
-template <int NT>
+template <bool W13>
 __global__ void __launch_bounds__(kGemvWarps * 32, 1)
-w13_kernel(const __grid_constant__ GemvParams p) {
-  // zero the W2 split-K partials (consumed by the next kernel)
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.partial_n;
-       i += (long long)gridDim.x * blockDim.x)
-    p.partial[i] = 0.f;
-  const int n_jobs = p.jt.hdr[0];
-  const int tiles = p.F / 16;
-  const int n_items = n_jobs * tiles;
-  if (blockIdx.x >= n_items) return;
-  // stage x (pair-permuted) and its block sums in shared memory when they fit
-  const uint4* xp = p.x_perm;
-  const float* xs = p.xsum;
-  const int nx16 = p.B * (p.H / 8), ns16 = p.B * (p.H / 32) / 4;
-  if ((nx16 + ns16) * 16 <= kXStage) {
-    uint4* st = reinterpret_cast<uint4*>(x_stage());
-    stage_copy(st, p.x_perm, nx16);
-    stage_copy(st + nx16, reinterpret_cast<const uint4*>(p.xsum), ns16);
-    __syncthreads();
-    xp = st;
-    xs = reinterpret_cast<const float*>(st + nx16);
+gemv_kernel(const __grid_constant__ GemvParams p) {
+  const int warp = threadIdx.x >> 5;
+  const int nv = n_vjobs(p);
+  if (!W13 && nv == 0) {                                     // nothing owned: y = 0
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)p.B * p.H;
+         i += (long long)gridDim.x * blockDim.x)
+      p.y[i] = 0.f;
+    return;
   }
-  for (int it = 0;; ++it) {
-    const int item = item_for(it);
-    if (item >= n_items) break;
-    const Job j = p.jt.jobs[item / tiles];
-    const int row0 = (item % tiles) * 16;
-    switch (j.enc) {
-      case HB_F16: w13_tile<HB_F16, NT>(p, j, row0, xp, xs); break;
-      case HB_Q8: w13_tile<HB_Q8, NT>(p, j, row0, xp, xs); break;
-      case HB_Q4: w13_tile<HB_Q4, NT>(p, j, row0, xp, xs); break;
-      default: w13_tile<HB_Q2, NT>(p, j, row0, xp, xs); break;
-    }
+  const int T = W13 ? p.F / 16 : p.H / 16;
+  const int K = W13 ? p.H : p.F;
+  long long U = 0;
+  for (int v = 0; v < nv; ++v) U += (long long)T * (K / epg_of(get_vjob(p, v).enc));
+  Space sp{U, (int)(gridDim.x * kGemvWarps)};
+  const int gw = blockIdx.x * kGemvWarps + warp;
+  const long long u0 = sp.b(gw), u1 = sp.b(gw + 1);
+  if (u0 >= u1) return;
+  const uint32_t ring = smem_u32(gemv_smem) + warp * kWarpSmem;
+  long long cum = 0;
+  int v = 0;
+  for (; v < nv; ++v) {                                       // vjob containing u0
+    const long long Uv = (long long)T * (K / epg_of(get_vjob(p, v).enc));
+    if (u0 < cum + Uv) break;
+    cum += Uv;
   }
-}
-
-// ------------------------------------------------------------------ K2b
-// B-operand view of h for one W2 chunk: element k of slot s is at
-// hi[s*stride + k/8 ...] (stride in uint4), sums at sum[s*sstride + k/32].
-struct HView {
-  const uint4* hi;
-  const uint4* lo;
-  const float* sum;
-  size_t stride, sstride;
-};
-
-template <int ENC, int NT>
-__device__ __forceinline__ void w2_chunk(const GemvParams& p, const Job& j, int row0, int kbeg,
-                                         int kend, int s, const HView& hv) {
-  constexpr int EPG = Enc<ENC>::EPG;
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const MatPtr M[1] = {mat_ptr<ENC>(p, j, 2)};
-  for (int t0 = 0; t0 < j.n_tok; t0 += 8 * NT) {
-    XSrc<NT, true> X;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const int sb = j.slot_off + min(t0 + 8 * n + g, j.n_tok - 1);
-      const int s0 = j.slot_off + min(t0 + 8 * n + 2 * t, j.n_tok - 1);
-      const int s1 = j.slot_off + min(t0 + 8 * n + 2 * t + 1, j.n_tok - 1);
-      X.b[n] = hv.hi + (size_t)sb * hv.stride;
-      X.blo[n] = hv.lo + (size_t)sb * hv.stride;
-      X.s0[n] = hv.sum + (size_t)s0 * hv.sstride;
-      X.s1[n] = hv.sum + (size_t)s1 * hv.sstride;
+  long long u = u0;
+  while (u < u1 && v < nv) {
+    const VJob vj = get_vjob(p, v);
+    const long long Uv = (long long)T * (K / epg_of(vj.enc));
+    const long long a = u - cum, b = min(u1, cum + Uv) - cum;
+    const bool xr = vj.nslot <= kXSlots;
+    switch (vj.enc * 2 + (xr ? 1 : 0)) {
+      case 2 * HB_F16 + 1: run<HB_F16, W13, true>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
+      case 2 * HB_F16 + 0: run<HB_F16, W13, false>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
+      case 2 * HB_Q8 + 1: run<HB_Q8, W13, true>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
+      case 2 * HB_Q8 + 0: run<HB_Q8, W13, false>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
+      case 2 * HB_Q4 + 1: run<HB_Q4, W13, true>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
+      case 2 * HB_Q4 + 0: run<HB_Q4, W13, false>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
+      case 2 * HB_Q2 + 1: run<HB_Q2, W13, true>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
+      default: run<HB_Q2, W13, false>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
     }
-    float acc[1][NT][4];
-#pragma unroll
-    for (int n = 0; n < NT; ++n)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[0][n][i] = 0.f;
-    mainloop<ENC, 1, NT, true>(warp_smem(), M, p.F, row0, kbeg / EPG, kend / EPG, X, acc);
-    // partial[s][token][row] += gate * o   (this warp owns (s, row tile))
-#pragma unroll
-    for (int n = 0; n < NT; ++n)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int slot_rel = t0 + 8 * n + 2 * t + (i & 1);
-        if (slot_rel < j.n_tok) {
-          const int slot = j.slot_off + slot_rel;
-          const int tok = p.jt.slot_token[slot];
-          const float gate = p.jt.slot_gate[slot];
-          float* dst = p.partial + ((size_t)s * p.B + tok) * p.H + row0 + g + 8 * (i >> 1);
-          *dst = fmaf(gate, acc[0][n][i], *dst);
-        }
-      }
-  }
-}
-
-template <int NT>
-__global__ void __launch_bounds__(kGemvWarps * 32, 1)
-w2_kernel(const __grid_constant__ GemvParams p) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n_jobs = p.jt.hdr[0];
-  const int n_slots = p.jt.hdr[1];
-  const int tiles = p.H / 16;
-  // every CTA works on ONE split-K chunk s (so its warps share the h chunk);
-  // the row tiles of chunk s are dealt over the CTAs with blockIdx % S == s
-  const int s = blockIdx.x % p.S;
-  const int nS = (gridDim.x - s + p.S - 1) / p.S;
-  const int cidx = blockIdx.x / p.S;
-  const int kbeg = s * p.chunk, kend = min(p.F, kbeg + p.chunk);
-  if (cidx >= tiles) return;
-  // stage the chunk of h (hi, lo, block sums) of every slot when it fits
-  HView hv{p.h_hi, p.h_lo, p.hsum, (size_t)p.F / 8, (size_t)p.F / 32};
-  const int clen = kend - kbeg;
-  const int nh16 = n_slots * (clen / 8), ns16 = n_slots * (clen / 32) / 4;
-  if (n_jobs > 0 && (2 * nh16 + ns16) * 16 <= kXStage) {
-    uint4* st = reinterpret_cast<uint4*>(x_stage());
-    for (int sl = 0; sl < n_slots; ++sl) {
-      stage_copy(st + sl * (clen / 8), p.h_hi + (size_t)sl * (p.F / 8) + kbeg / 8, clen / 8);
-      stage_copy(st + nh16 + sl * (clen / 8), p.h_lo + (size_t)sl * (p.F / 8) + kbeg / 8, clen / 8);
-      stage_copy(st + 2 * nh16 + sl * (clen / 32) / 4,
-                 reinterpret_cast<const uint4*>(p.hsum + (size_t)sl * (p.F / 32) + kbeg / 32),
-                 (clen / 32) / 4);
-    }
-    __syncthreads();
-    // views indexed by global k: shift the bases back by the chunk start
-    hv.hi = st - kbeg / 8;
-    hv.lo = st + nh16 - kbeg / 8;
-    hv.sum = reinterpret_cast<const float*>(st + 2 * nh16) - kbeg / 32;
-    hv.stride = clen / 8;
-    hv.sstride = clen / 32;
-  }
-  for (int it = 0;; ++it) {
-    const int tile = cidx + nS * (warp + kGemvWarps * it);
-    if (tile >= tiles) break;
-    const int row0 = tile * 16;
-    for (int jj = 0; jj < n_jobs; ++jj) {
-      const Job j = p.jt.jobs[jj];
-      switch (j.enc) {
-        case HB_F16: w2_chunk<HB_F16, NT>(p, j, row0, kbeg, kend, s, hv); break;
-        case HB_Q8: w2_chunk<HB_Q8, NT>(p, j, row0, kbeg, kend, s, hv); break;
-        case HB_Q4: w2_chunk<HB_Q4, NT>(p, j, row0, kbeg, kend, s, hv); break;
-        default: w2_chunk<HB_Q2, NT>(p, j, row0, kbeg, kend, s, hv); break;
-      }
-    }
-    // the last chunk of this row tile reduces the S partials in order -> y
-    __syncwarp();
-    __threadfence();
-    unsigned prev = 0;
-    if (lane == 0) prev = atomicAdd(p.tile_count + tile, 1u);
-    prev = __shfl_sync(0xffffffffu, prev, 0);
-    if (prev == (unsigned)(p.S - 1)) {
-      __threadfence();
-      for (int e = lane; e < 16 * p.B; e += 32) {
-        const int tok = e >> 4, r = row0 + (e & 15);
-        float v = 0.f;
-        for (int ss = 0; ss < p.S; ++ss)
-          v += __ldcg(p.partial + ((size_t)ss * p.B + tok) * p.H + r);
-        p.y[(size_t)tok * p.H + r] = v;
-      }
-      if (lane == 0) p.tile_count[tile] = 0u;
-    }
+    u = cum + b;
+    cum += Uv;
+    ++v;
   }
 }
 
@@ -581,25 +596,15 @@ static void set_smem(Kern kernel, bool& done) {
   }
 }
 
-void launch_w13(const GemvParams& p, int nt, cudaStream_t s) {
-  static bool d1 = false, d2 = false;
-  if (nt <= 1) {
-    set_smem(w13_kernel<1>, d1);
-    w13_kernel<1><<<kNumSM, kGemvWarps * 32, kGemvSmem, s>>>(p);
-  } else {
-    set_smem(w13_kernel<2>, d2);
-    w13_kernel<2><<<kNumSM, kGemvWarps * 32, kGemvSmem, s>>>(p);
-  }
+void launch_w13(const GemvParams& p, cudaStream_t s) {
+  static bool d = false;
+  set_smem(gemv_kernel<true>, d);
+  gemv_kernel<true><<<kGemvCTAs, kGemvWarps * 32, kGemvSmem, s>>>(p);
 }
-void launch_w2(const GemvParams& p, int nt, cudaStream_t s) {
-  static bool d1 = false, d2 = false;
-  if (nt <= 1) {
-    set_smem(w2_kernel<1>, d1);
-    w2_kernel<1><<<kNumSM, kGemvWarps * 32, kGemvSmem, s>>>(p);
-  } else {
-    set_smem(w2_kernel<2>, d2);
-    w2_kernel<2><<<kNumSM, kGemvWarps * 32, kGemvSmem, s>>>(p);
-  }
+void launch_w2(const GemvParams& p, cudaStream_t s) {
+  static bool d = false;
+  set_smem(gemv_kernel<false>, d);
+  gemv_kernel<false><<<kGemvCTAs, kGemvWarps * 32, kGemvSmem, s>>>(p);
 }
 
 }  // namespace hb

@@ -43,6 +43,7 @@ struct JobTable {
   Job* jobs;           // max_jobs
   int32_t* slot_token; // max_slots
   float* slot_gate;    // max_slots
+  int32_t* tok_slots;  // [max_batch][top_k] slot of each (token, rank) or -1, rank order
 };
 
 struct RouterParams {
@@ -71,22 +72,27 @@ struct RouterParams {
 struct GemvParams {
   JobTable jt;
   BlobLayout lay[4];
-  int H, F, B;
+  int H, F, B, k;
   const uint4* x_perm;                 // [B][H/8]
   const float* xsum;                   // [B][H/32]
   uint4* h_hi;                         // [slots][F/8]  pair-permuted fp16 hi part of h
   uint4* h_lo;                         // [slots][F/8]  fp16 residual h - hi
   float* hsum;                         // [slots][F/32] block sums of h (zeroed by router)
-  float* partial;                      // [S][B][H]
-  long long partial_n;
-  int S, chunk;                        // W2 split-K: S chunks of `chunk` elements of F
+  float* part;                         // stream-K pieces [warps][2][32 lanes][8]
+  float* ob;                           // [slots][H] per-slot W2 outputs
+  unsigned* cnt13;                     // [max_vjobs][F/16] piece counters (self-resetting)
+  unsigned* cnt2;                      // [max_vjobs][H/16]
+  unsigned* cnty;                      // [H/16] job counters of the y combine
   float* y;                            // [B][H]
-  unsigned* tile_count;                // [H/16] (self-resetting)
 };
 
 void launch_router(const RouterParams& p, cudaStream_t s);
-void launch_w13(const GemvParams& p, int nt, cudaStream_t s);
-void launch_w2(const GemvParams& p, int nt, cudaStream_t s);
+void launch_w13(const GemvParams& p, cudaStream_t s);
+void launch_w2(const GemvParams& p, cudaStream_t s);
+constexpr int kVSlots = 8;             // token slots per virtual job (one mma N tile)
+constexpr int kGemvCTAs = kNumSM;      // persistent grid: one CTA per SM
+constexpr int kGemvTotalWarps = kGemvCTAs * kGemvWarps;
+constexpr int kPartFloats = 8;         // per lane per piece
 int launch_quantize_expert(int enc, int hidden, int ffn, const __half* w1, const __half* w3,
                            const __half* w2, uint8_t* blob, cudaStream_t s);
 void launch_synth(__half* dst, size_t n, uint64_t key, float scale, uint64_t start,

@@ -159,11 +159,13 @@ __device__ void build_jobs(const RouterParams& p) {
   for (int i = 0; i < nsel; ++i) {           // slots in token order
     const int4 raw = __ldcg(reinterpret_cast<const int4*>(p.dec) + i);
     hb_decision d = *reinterpret_cast<const hb_decision*>(&raw);
+    p.jt.tok_slots[i] = -1;
     if (d.prec == HB_SKIP || d.expert % p.world != p.rank) continue;
     const int key = d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1);
     const int slot = p.jt.jobs[jobid[key]].slot_off + fill[key]++;
     p.jt.slot_token[slot] = d.token;
     p.jt.slot_gate[slot] = d.gate;
+    p.jt.tok_slots[i] = slot;
     d.served_enc = (uint8_t)((key & 1) ? p.lo_enc : p.hi_enc);
     d.hit = 1;
     p.dec[i] = d;
