@@ -55,9 +55,10 @@ extern "C" {
  *   HB_Q8   w = d*q,      q int8 [-127,127] 8.5 bits/weight
  *   HB_Q4   w = d*(q-8),  q in [0,15]       4.5 bits/weight
  *   HB_Q2   w = d*q + m,  q in [0,3]        3.0 bits/weight
- * Blob = W1 [F,H], W3 [F,H], W2 [H,F]; each matrix = sections q, d (, m),
- * each section 256-byte aligned; q rows are stored in 64-byte groups whose
- * element order is given in DESIGN.md "Blob layout" (hb_blob_section()). */
+ * Blob = W1 [F,H], W3 [F,H], W2 [H,F]; each matrix = a code section and a
+ * scale section (d, and m for Q2), each 256-byte aligned.  Codes are stored
+ * tile-major: 16 rows x one 64-byte group of K = one contiguous 1 KB "unit";
+ * exact element order in DESIGN.md "Blob layout" (hb_blob_section()). */
 enum { HB_F16 = 0, HB_Q8 = 1, HB_Q4 = 2, HB_Q2 = 3 };
 /* Precision decision of one selected expert. */
 enum { HB_HIGH = 0, HB_LOW = 1, HB_SKIP = 2 };
@@ -101,8 +102,9 @@ typedef struct hb_ctx hb_ctx;
 /* ------------------------------------------------------------ host helpers */
 void        hb_config_default(hb_config* cfg);
 size_t      hb_blob_bytes(int enc, int hidden, int ffn);
-/* Offset/size of section sec (0 q or w, 1 d, 2 m) of matrix mat (0 W1, 1 W3,
- * 2 W2) inside a blob.  Returns HB_EINVAL if the section does not exist. */
+/* Offset/size of section sec (0 codes / fp16 values, 1 scales) of matrix mat
+ * (0 W1, 1 W3, 2 W2) inside a blob.  HB_EINVAL if the section does not exist
+ * (F16 has no scale section). */
 int         hb_blob_section(int enc, int hidden, int ffn, int mat, int sec,
                             size_t* offset, size_t* nbytes);
 /* k = 2 gap threshold floor(ln(T/(1-T)) * 2^48) (exact-integer form of the

@@ -15,22 +15,34 @@ Encodings (block = 32 consecutive elements along K of one row):
     Q2   w = d * q + m      q in [0, 3]                    (3.0 bits/weight)
 d, m fp16, one per block.  Every value is an exact dyadic rational in fp64.
 
-Blob of one expert = W1 [F,H], W3 [F,H], W2 [H,F] in that order, each row-major
-[N,K] quantised along K; each matrix = sections (q, d[, m]); every section
-starts on a 256-byte boundary of the blob.  d and m sections are [N, K/32]
-fp16 row-major.  The q section is row-major with K*b/8 bytes per row; inside a
-row the codes are stored in 64-byte GROUPS, and element k of the row is at
+Blob of one expert = W1 [F,H], W3 [F,H], W2 [H,F] in that order, each [N,K]
+quantised along K (N, K multiples of 256).  Each matrix = a CODE section and
+(quantised encodings) a SCALE section, each starting on a 256-byte boundary
+of the blob.
 
-    Q8 : group k//64 , byte 16*t + 8*j + r               (whole byte, int8)
-         j = (k%64)//32 , t = (k%32)//8 , r = k%8
-    Q4 : group k//128, byte 16*t + 4*j + r//2, bits 4*(r%2)..+3
-         j = (k%128)//32, t = (k%32)//8 , r = k%8
-    Q2 : group k//256, byte 16*t + 4*(j//2) + 2*(r//4) + (j%2), bits 2*(r%4)..+1
-         j = (k%256)//32, t = (k%32)//8 , r = k%8
+Layout.  Rows come in TILES of 16 rows; along K a
+row is cut into GROUPS of EPG elements that occupy 64 bytes (EPG = 32 F16,
+64 Q8, 128 Q4, 256 Q2; G = K/EPG groups per row).  A UNIT = (tile, group) =
+the 16 rows' 64-byte pieces of that group, stored contiguously (1 KB), units
+in (tile, group) order:
 
-(byte offsets relative to the group start = row start + 64*group).  The
-formulas ARE the definition; tests/golden/formats_*.txt pin them with bytes
-worked out by hand.  (Why this order: DESIGN.md "Blob layout".)
+    code byte of element (n, k) = 1024*(G*tile + grp) + 64*r + o(k % EPG)
+        tile = n // 16, r = n % 16, grp = k // EPG
+
+with the within-group offset o (t = (k%32)//8, q = k%8, j = block in group):
+    F16: o = 2*(k%32)                  (the group's 32 fp16 values in order)
+    Q8 : byte 16*t + 8*j + q                                (whole byte, int8)
+    Q4 : byte 16*t + 4*j + q//2, bits 4*(q%2)..+3
+    Q2 : byte 16*t + 4*(j//2) + 2*(q//4) + (j%2), bits 2*(q%4)..+1
+
+Scales: one SB-byte record per (unit, row) -- SB = 2*BPG (d of the BPG blocks
+of the group, fp16) and, for Q2, another 2*BPG bytes of m:
+
+    scale record of (n, grp) at 16*SB*(G*tile + grp) + SB*r
+        d of block j at +2*j,  m of block j at +2*BPG + 2*j   (Q2)
+
+The formulas ARE the definition; tests/golden/formats_*.txt pin them with
+bytes worked out by hand.
 """
 from __future__ import annotations
 
@@ -39,7 +51,9 @@ import numpy as np
 F16, Q8, Q4, Q2 = 0, 1, 2, 3
 ENC_NAMES = {F16: "F16", Q8: "Q8", Q4: "Q4", Q2: "Q2"}
 QBITS = {F16: 16, Q8: 8, Q4: 4, Q2: 2}
+EPG = {F16: 32, Q8: 64, Q4: 128, Q2: 256}      # elements per 64-byte group
 BLOCK = 32
+TILE = 16
 SECTION_ALIGN = 256
 
 
@@ -47,15 +61,23 @@ def _align(n: int) -> int:
     return (n + SECTION_ALIGN - 1) // SECTION_ALIGN * SECTION_ALIGN
 
 
+def bpg(enc: int) -> int:
+    """Blocks per group."""
+    return EPG[enc] // BLOCK
+
+
+def scale_record_bytes(enc: int) -> int:
+    """SB: bytes of scales per (unit, row)."""
+    if enc == F16:
+        return 0
+    return 2 * bpg(enc) * (2 if enc == Q2 else 1)
+
+
 def matrix_sections(enc: int, n: int, k: int):
     """[(name, nbytes)] of one [n,k] matrix in encoding enc."""
     if enc == F16:
         return [("w", n * k * 2)]
-    nb = n * (k // BLOCK) * 2
-    q = [("q", n * k * QBITS[enc] // 8), ("d", nb)]
-    if enc == Q2:
-        q.append(("m", nb))
-    return q
+    return [("q", n * k * QBITS[enc] // 8), ("s", n * (k // EPG[enc]) * scale_record_bytes(enc))]
 
 
 def expert_matrix_shapes(hidden: int, ffn: int):
@@ -81,55 +103,81 @@ def blob_bytes(enc: int, hidden: int, ffn: int) -> int:
 
 # ------------------------------------------------------------ code locations
 
-def code_location(enc: int, k):
-    """(byte offset within the row, bit shift) of element k (int or array)."""
+def within_group(enc: int, k):
+    """(byte offset inside the row's 64-byte group piece, bit shift) of element k."""
     k = np.asarray(k, dtype=np.int64)
-    t = (k % 32) // 8
-    r = k % 8
+    e = k % EPG[enc]
+    t = (e % 32) // 8
+    q = e % 8
+    j = e // 32
+    if enc == F16:
+        return 2 * e, np.zeros_like(k)
     if enc == Q8:
-        g, j = k // 64, (k % 64) // 32
-        return 64 * g + 16 * t + 8 * j + r, np.zeros_like(k)
+        return 16 * t + 8 * j + q, np.zeros_like(k)
     if enc == Q4:
-        g, j = k // 128, (k % 128) // 32
-        return 64 * g + 16 * t + 4 * j + r // 2, 4 * (r % 2)
+        return 16 * t + 4 * j + q // 2, 4 * (q % 2)
     if enc == Q2:
-        g, j = k // 256, (k % 256) // 32
-        return 64 * g + 16 * t + 4 * (j // 2) + 2 * (r // 4) + (j % 2), 2 * (r % 4)
-    raise ValueError(f"no packed codes for encoding {enc}")
+        return 16 * t + 4 * (j // 2) + 2 * (q // 4) + (j % 2), 2 * (q % 4)
+    raise ValueError(enc)
 
 
-def row_group(enc: int) -> int:
-    """K must be a multiple of this for encoding enc."""
-    return {F16: 32, Q8: 64, Q4: 128, Q2: 256}[enc]
+def code_offset(enc: int, n, k, K: int):
+    """(byte offset in the code section, bit shift) of element (n, k)."""
+    n = np.asarray(n, dtype=np.int64)
+    k = np.asarray(k, dtype=np.int64)
+    G = K // EPG[enc]
+    tile, r = n // TILE, n % TILE
+    grp = k // EPG[enc]
+    o, shift = within_group(enc, k)
+    return 1024 * (G * tile + grp) + 64 * r + o, shift
+
+
+def scale_offset(enc: int, n, blk, K: int, which: str = "d"):
+    """Byte offset in the scale section of d (or m) of block blk of row n."""
+    n = np.asarray(n, dtype=np.int64)
+    blk = np.asarray(blk, dtype=np.int64)
+    G = K // EPG[enc]
+    b = bpg(enc)
+    tile, r = n // TILE, n % TILE
+    grp, j = blk // b, blk % b
+    rec = 16 * scale_record_bytes(enc) * (G * tile + grp) + scale_record_bytes(enc) * r
+    return rec + 2 * j + (2 * b if which == "m" else 0)
 
 
 # ------------------------------------------------------------------- decode
 
-def _f16(buf: np.ndarray, off: int, count: int) -> np.ndarray:
-    return buf[off:off + 2 * count].view(np.float16)
-
-
 def decode_matrix(enc: int, blob: np.ndarray, sections: dict, n: int, k: int) -> np.ndarray:
     """O1: the exact fp64 matrix [n,k] stored in `blob` (uint8) at `sections`."""
     blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    N = np.arange(n)[:, None]
+    Kx = np.arange(k)[None, :]
     if enc == F16:
-        off, _ = sections["w"]
-        return _f16(blob, off, n * k).astype(np.float64).reshape(n, k)
+        off, nb = sections["w"]
+        sec = blob[off:off + nb]
+        pos, _ = code_offset(enc, N, Kx, k)
+        lo = sec[pos].astype(np.uint16)
+        hi = sec[pos + 1].astype(np.uint16)
+        return (lo | (hi << 8)).view(np.float16).astype(np.float64)
     qoff, qbytes = sections["q"]
-    rows = blob[qoff:qoff + qbytes].reshape(n, -1)
-    byte, shift = code_location(enc, np.arange(k))
-    raw = (rows[:, byte].astype(np.int64) >> shift[None, :]) & ((1 << QBITS[enc]) - 1)
-    doff, _ = sections["d"]
-    d = _f16(blob, doff, n * (k // BLOCK)).astype(np.float64).reshape(n, k // BLOCK)
-    d_el = np.repeat(d, BLOCK, axis=1)
+    qsec = blob[qoff:qoff + qbytes]
+    pos, shift = code_offset(enc, N, Kx, k)
+    raw = (qsec[pos].astype(np.int64) >> shift) & ((1 << QBITS[enc]) - 1)
+    soff, sbytes = sections["s"]
+    ssec = blob[soff:soff + sbytes]
+
+    def f16_at(p):
+        return (ssec[p].astype(np.uint16) | (ssec[p + 1].astype(np.uint16) << 8)).view(
+            np.float16).astype(np.float64)
+
+    blk = Kx // BLOCK
+    d = f16_at(scale_offset(enc, N, blk, k, "d"))
     if enc == Q8:
         q = np.where(raw >= 128, raw - 256, raw)            # two's complement int8
-        return d_el * q
+        return d * q
     if enc == Q4:
-        return d_el * (raw - 8)
-    moff, _ = sections["m"]
-    m = _f16(blob, moff, n * (k // BLOCK)).astype(np.float64).reshape(n, k // BLOCK)
-    return d_el * raw + np.repeat(m, BLOCK, axis=1)
+        return d * (raw - 8)
+    m = f16_at(scale_offset(enc, N, blk, k, "m"))
+    return d * raw + m
 
 
 def decode_blob(enc: int, blob: np.ndarray, hidden: int, ffn: int):
@@ -189,14 +237,42 @@ def quantize_codes(enc: int, w16: np.ndarray):
 
 
 def pack_codes(enc: int, codes: np.ndarray) -> np.ndarray:
-    """Place codes [n,k] at their code_location; returns uint8 [n, k*b/8]."""
+    """Place codes [n,k] at their code_offset; returns the code section (uint8)."""
     n, k = codes.shape
-    out = np.zeros((n, k * QBITS[enc] // 8), dtype=np.uint8)
-    byte, shift = code_location(enc, np.arange(k))
+    out = np.zeros(n * k * QBITS[enc] // 8, dtype=np.uint8)
+    pos, shift = code_offset(enc, np.arange(n)[:, None], np.arange(k)[None, :], k)
     mask = (1 << QBITS[enc]) - 1
     for s in np.unique(shift):                       # one shift class at a time:
-        sel = np.nonzero(shift == s)[0]              # no byte repeats inside it
-        out[:, byte[sel]] |= ((codes[:, sel] & mask) << s).astype(np.uint8)
+        sel = shift[0] == s                          # no byte repeats inside it
+        out[pos[:, sel].ravel()] |= ((codes[:, sel] & mask) << s).astype(np.uint8).ravel()
+    return out
+
+
+def pack_scales(enc: int, d16: np.ndarray, m16) -> np.ndarray:
+    """Scale section (uint8) from d [n, k/32] (and m) fp16."""
+    n, nb = d16.shape
+    k = nb * BLOCK
+    out = np.zeros(n * (k // EPG[enc]) * scale_record_bytes(enc), dtype=np.uint8)
+    N = np.arange(n)[:, None]
+    Bk = np.arange(nb)[None, :]
+    for arr, which in ((d16, "d"), (m16, "m")):
+        if arr is None:
+            continue
+        p = scale_offset(enc, N, Bk, k, which)
+        bits = arr.view(np.uint16).astype(np.uint16)
+        out[p.ravel()] = (bits & 0xFF).astype(np.uint8).ravel()
+        out[(p + 1).ravel()] = (bits >> 8).astype(np.uint8).ravel()
+    return out
+
+
+def pack_f16(w16: np.ndarray) -> np.ndarray:
+    """F16 code section: the fp16 values at their code_offset."""
+    n, k = w16.shape
+    out = np.zeros(n * k * 2, dtype=np.uint8)
+    pos, _ = code_offset(F16, np.arange(n)[:, None], np.arange(k)[None, :], k)
+    bits = np.ascontiguousarray(w16, dtype=np.float16).view(np.uint16)
+    out[pos.ravel()] = (bits & 0xFF).astype(np.uint8).ravel()
+    out[(pos + 1).ravel()] = (bits >> 8).astype(np.uint8).ravel()
     return out
 
 
@@ -209,14 +285,11 @@ def quantize_blob(enc: int, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray) -> n
         sec = lay[mat]
         if enc == F16:
             off, nb = sec["w"]
-            blob[off:off + nb] = np.ascontiguousarray(w, dtype=np.float16).view(np.uint8).ravel()
+            blob[off:off + nb] = pack_f16(w)
             continue
         codes, d16, m16 = quantize_codes(enc, w)
         off, nb = sec["q"]
-        blob[off:off + nb] = pack_codes(enc, codes).ravel()
-        off, nb = sec["d"]
-        blob[off:off + nb] = d16.view(np.uint8).ravel()
-        if m16 is not None:
-            off, nb = sec["m"]
-            blob[off:off + nb] = m16.view(np.uint8).ravel()
+        blob[off:off + nb] = pack_codes(enc, codes)
+        off, nb = sec["s"]
+        blob[off:off + nb] = pack_scales(enc, d16, m16)
     return blob

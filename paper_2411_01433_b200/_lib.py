@@ -13,7 +13,8 @@ import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "libhobbit.so")
+# HOBBIT_LIB: an alternative in-tree build (kernel-variant experiments only)
+LIB_PATH = os.environ.get("HOBBIT_LIB") or os.path.join(PKG, "libhobbit.so")
 HEADER = os.path.join(ROOT, "include", "hobbit.h")
 
 HB_OK, HB_EINVAL, HB_ECAPACITY, HB_ESTATE, HB_ECUDA, HB_ENOMEM, HB_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6

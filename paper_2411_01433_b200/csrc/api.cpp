@@ -21,24 +21,19 @@ namespace hb {
 int blob_layout(int enc, int hidden, int ffn, BlobLayout* out) {
   if (enc < HB_F16 || enc > HB_Q2 || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
     return HB_EINVAL;
+  // code section + one scale section per matrix (tile-major units, DESIGN.md
+  // "Blob layout"); every section 256-byte aligned
   const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
   const int bits = enc == HB_F16 ? 16 : enc == HB_Q8 ? 8 : enc == HB_Q4 ? 4 : 2;
   auto align = [](uint64_t v) { return (v + 255) / 256 * 256; };
   uint64_t off = 0;
   for (int m = 0; m < 3; ++m) {
     const uint64_t qbytes = (uint64_t)N[m] * K[m] * bits / 8;
-    const uint64_t sbytes = (uint64_t)N[m] * (K[m] / 32) * 2;
+    const uint64_t sbytes = (uint64_t)N[m] * (K[m] / 32) * 2 * (enc == HB_Q2 ? 2 : 1);
     out->mat[m].q = off;
     off = align(off + qbytes);
-    out->mat[m].d = out->mat[m].m = off;
-    if (enc != HB_F16) {
-      out->mat[m].d = off;
-      off = align(off + sbytes);
-      if (enc == HB_Q2) {
-        out->mat[m].m = off;
-        off = align(off + sbytes);
-      }
-    }
+    out->mat[m].s = off;
+    if (enc != HB_F16) off = align(off + sbytes);
   }
   out->total = off;
   return HB_OK;
@@ -159,10 +154,9 @@ int hb_blob_section(int enc, int hidden, int ffn, int mat, int sec, size_t* offs
   const int N = mat < 2 ? ffn : hidden, K = mat < 2 ? hidden : ffn;
   const int bits = enc == HB_F16 ? 16 : enc == HB_Q8 ? 8 : enc == HB_Q4 ? 4 : 2;
   if (sec == 0) { *offset = L.mat[mat].q; *nbytes = (size_t)N * K * bits / 8; return HB_OK; }
-  if (enc == HB_F16 || (sec == 2 && enc != HB_Q2))
-    return fail(nullptr, HB_EINVAL, "section does not exist");
-  *offset = sec == 1 ? L.mat[mat].d : L.mat[mat].m;
-  *nbytes = (size_t)N * (K / 32) * 2;
+  if (enc == HB_F16 || sec == 2) return fail(nullptr, HB_EINVAL, "section does not exist");
+  *offset = L.mat[mat].s;
+  *nbytes = (size_t)N * (K / 32) * 2 * (enc == HB_Q2 ? 2 : 1);
   return HB_OK;
 }
 

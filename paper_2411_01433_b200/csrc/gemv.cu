@@ -142,7 +142,7 @@ __host__ __device__ constexpr int epg_of(int enc) {
   return enc == HB_F16 ? 32 : enc == HB_Q8 ? 64 : enc == HB_Q4 ? 128 : 256;
 }
 
-constexpr int kWarpSmem = 13 * 1024;                    // per-warp cp.async ring
+constexpr int kWarpSmem = HB_WARP_SMEM_KB * 1024;       // per-warp cp.async ring
 constexpr int kGemvSmem = kGemvWarps * kWarpSmem;       // 208 KB per CTA
 constexpr int kXSlots = 2;                              // token slots staged in the ring
 
@@ -280,9 +280,8 @@ __device__ void finalize13(const GemvParams& p, const VJob& vj, int row0, const 
   }
 }
 
-// K2b: o -> ob[slot][rows]; the last job of this H tile writes y (fixed order)
-__device__ void finalize2(const GemvParams& p, const VJob& vj, int tile, int nv,
-                          const float (&acc)[1][4]) {
+// K2b: o -> ob[slot][rows] of a finished (job, H tile)
+__device__ void store_ob(const GemvParams& p, const VJob& vj, int tile, const float (&acc)[1][4]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int row0 = tile * 16;
 #pragma unroll
@@ -291,8 +290,13 @@ __device__ void finalize2(const GemvParams& p, const VJob& vj, int tile, int nv,
     if (sl < vj.nslot)
       p.ob[(size_t)(vj.slot0 + sl) * p.H + row0 + g + 8 * (i >> 1)] = acc[0][i];
   }
-  __syncwarp();
-  __threadfence();
+}
+
+// after a fence: count this job as done for H tile `tile`; the last job of the
+// tile writes y = Eq. 1 in fixed (token, rank) order
+__device__ void publish_y(const GemvParams& p, int tile, int nv) {
+  const int lane = threadIdx.x & 31;
+  const int row0 = tile * 16;
   unsigned prev = 0;
   if (lane == 0) prev = atomicAdd(p.cnty + tile, 1u);
   prev = __shfl_sync(0xffffffffu, prev, 0);
@@ -309,6 +313,12 @@ __device__ void finalize2(const GemvParams& p, const VJob& vj, int tile, int nv,
   }
   if (lane == 0) p.cnty[tile] = 0u;
 }
+
+struct Pend {
+  int tile;
+  int kind;          // 0 partial piece stored in part[], 1 finished W2 tile (ob stored)
+};
+constexpr int kMaxPend = 4;
 
 // ------------------------------------------------------------ the run
 // Stream units [a, b) of virtual job v (unit l = tile * G + grp) through the
@@ -328,76 +338,86 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
                         : ENC == HB_Q4 ? (size_t)K / 2 : (size_t)K / 4;
   const uint64_t pol = evict_first_policy();
   // matrices
-  const uint8_t* q0[NMAT];
-  const __half* d0[NMAT];
-  const __half* m0[NMAT];
+  // tile-major blobs: unit l (tile l/G, group l%G) = 1 KB of codes at q + 1024*l,
+  // its 16 scale records at s + 16*SB*l -- a warp's range is one contiguous span
+  const uint8_t* qp[NMAT];
+  const uint8_t* sp_[NMAT];
 #pragma unroll
   for (int m = 0; m < NMAT; ++m) {
     const MatLayout& L = p.lay[ENC].mat[W13 ? m : 2];
-    q0[m] = vj.blob + L.q + (size_t)g * rowbytes + 16 * t;        // row g of tile 0
-    d0[m] = reinterpret_cast<const __half*>(vj.blob + L.d);
-    m0[m] = reinterpret_cast<const __half*>(vj.blob + L.m);
+    qp[m] = vj.blob + L.q + (size_t)a * 1024 + 16 * lane;
+    sp_[m] = vj.blob + L.s + (size_t)a * 16 * SB + 16 * lane;
   }
-  const size_t q8 = 8 * rowbytes, qtile = 16 * rowbytes;
-  // B-operand sources per slot (x or h hi/lo) and block sums
+  (void)rowbytes;
+  (void)nb;
+  const bool s_act = lane < SB;               // 16*SB bytes of scales per unit = SB lanes x 16 B
   const int ns = vj.nslot;
-  const uint4* xsrc[XS][kVSlots];
-  const float* zsrc[kVSlots];
-#pragma unroll
-  for (int s = 0; s < kVSlots; ++s) {
+  // B-operand source of slot s (x or h hi/lo) and of its block sums
+  auto xsrc_of = [&](int part, int s) -> const uint4* {
     const int sl = vj.slot0 + min(s, ns - 1);
-    if constexpr (W13) {
-      const int tok = p.jt.slot_token[sl];
-      xsrc[0][s] = p.x_perm + (size_t)tok * (p.H / 8);
-      zsrc[s] = p.xsum + (size_t)tok * (p.H / 32);
-    } else {
-      xsrc[0][s] = p.h_hi + (size_t)sl * (p.F / 8);
-      xsrc[XS - 1][s] = p.h_lo + (size_t)sl * (p.F / 8);
-      zsrc[s] = p.hsum + (size_t)sl * (p.F / 32);
+    if constexpr (W13) return p.x_perm + (size_t)p.jt.slot_token[sl] * (p.H / 8);
+    else return (part ? p.h_lo : p.h_hi) + (size_t)sl * (p.F / 8);
+  };
+  auto zsrc_of = [&](int s) -> const float* {
+    const int sl = vj.slot0 + min(s, ns - 1);
+    if constexpr (W13) return p.xsum + (size_t)p.jt.slot_token[sl] * (p.H / 32);
+    else return p.hsum + (size_t)sl * (p.F / 32);
+  };
+
+  // ---- producer state
+  int p_grp = (int)(a % G);
+  // B fragments: copy descriptors of this lane (fixed per run), source offset + grp*BPG*4
+  constexpr int NCP = (BPG * kXSlots * XS * 4 + 31) / 32;
+  const uint4* xc_src[NCP];
+  uint32_t xc_dst[NCP];
+  bool xc_on[NCP];
+  const float* zc_src = nullptr;
+  uint32_t zc_dst = 0;
+  if constexpr (XR) {
+    const int ncp = BPG * ns * XS * 4;
+#pragma unroll
+    for (int i = 0; i < NCP; ++i) {
+      const int c = lane + 32 * i;
+      xc_on[i] = c < ncp;
+      const int tt = c & 3;
+      int r = c >> 2;
+      const int part = r % XS;
+      r /= XS;
+      const int sl = r % ns, blk = r / ns;
+      xc_src[i] = xc_on[i] ? xsrc_of(part, sl) + blk * 4 + tt : nullptr;
+      xc_dst[i] = R::W + R::S + ((part * kXSlots + sl) * BPG + blk) * 64 + tt * 16;
+    }
+    if constexpr (ENC == HB_Q2) {
+      if (lane < ns * BPG) {
+        zc_src = zsrc_of(lane / BPG) + (lane % BPG);
+        zc_dst = R::W + R::S + R::X + ((lane / BPG) * BPG + (lane % BPG)) * 4;
+      }
     }
   }
-  // producer state
   long long pl = a;
-  int p_tile = (int)(a / G), p_grp = (int)(a % G);
   int pslot = 0;
   auto issue = [&]() {
     if (pl < b) {
       const uint32_t st = ring + pslot * R::STAGE;
 #pragma unroll
-      for (int m = 0; m < NMAT; ++m) {
-        const uint8_t* s = q0[m] + (size_t)p_tile * qtile + (size_t)p_grp * 64;
-        cp_async16_ef(st + m * 1024 + g * 64 + 16 * t, s, pol);
-        cp_async16_ef(st + m * 1024 + (g + 8) * 64 + 16 * t, s + q8, pol);
-        if constexpr (SB > 0) {
-          const uint32_t sd = st + R::W + m * 16 * SB;
-          const int srow = lane & 15;
-          const size_t so = (size_t)(p_tile * 16 + srow) * nb + p_grp * BPG;
-          if constexpr (ENC == HB_Q8) { if (lane < 16) cp_async4(sd + srow * SB, d0[m] + so); }
-          else if constexpr (ENC == HB_Q4) { if (lane < 16) cp_async8(sd + srow * SB, d0[m] + so); }
-          else cp_async16_ef(sd + srow * SB + (lane >> 4) * 16, (lane < 16 ? d0[m] : m0[m]) + so, pol);
-        }
+      for (int m = 0; m < NMAT; ++m) {                 // 2 x 512 contiguous bytes
+        cp_async16_ef(st + m * 1024 + 16 * lane, qp[m], pol);
+        cp_async16_ef(st + m * 1024 + 512 + 16 * lane, qp[m] + 512, pol);
+        if constexpr (SB > 0)
+          if (s_act) cp_async16_ef(st + R::W + m * 16 * SB + 16 * lane, sp_[m], pol);
       }
       if constexpr (XR) {
-        const uint32_t sx = st + R::W + R::S;
-        const int ncp = BPG * ns * XS * 4;
-        for (int c = lane; c < ncp; c += 32) {
-          const int tt = c & 3;
-          int r = c >> 2;
-          const int part = r % XS;
-          r /= XS;
-          const int sl = r % ns, blk = r / ns;
-          cp_async16(sx + ((part * kXSlots + sl) * BPG + blk) * 64 + tt * 16,
-                     xsrc[part][sl] + (size_t)(p_grp * BPG + blk) * 4 + tt);
-        }
-        if constexpr (ENC == HB_Q2) {
-          if (lane < ns * BPG) {
-            const int sl = lane / BPG, blk = lane % BPG;
-            cp_async4(sx + R::X + (sl * BPG + blk) * 4, zsrc[sl] + p_grp * BPG + blk);
-          }
-        }
+        const size_t xo = (size_t)p_grp * BPG * 4;
+#pragma unroll
+        for (int i = 0; i < NCP; ++i)
+          if (xc_on[i]) cp_async16(st + xc_dst[i], xc_src[i] + xo);
+        if constexpr (ENC == HB_Q2)
+          if (zc_src) cp_async4(st + zc_dst, zc_src + p_grp * BPG);
       }
       ++pl;
-      if (++p_grp == G) { p_grp = 0; ++p_tile; }
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) { qp[m] += 1024; sp_[m] += 16 * SB; }
+      if (++p_grp == G) p_grp = 0;
       if (++pslot == DEPTH) pslot = 0;
     }
     cp_commit();
@@ -414,6 +434,60 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
   int c_tile = (int)(a / G), c_grp = (int)(a % G), piece0 = c_grp;
   int cslot = 0;
   const int xg = min(g, ns - 1), z0 = min(2 * t, ns - 1), z1 = min(2 * t + 1, ns - 1);
+  // deferred publications: partial pieces (kind 0) and finished W2 tiles (kind 1)
+  Pend pend[kMaxPend];
+  int npend = 0;
+  auto publish = [&](const Pend* pd, int n) {
+    if (n == 0) return;
+    __syncwarp();
+    __threadfence();
+    int ytile[kMaxPend];
+    int ny = 0;
+    for (int i = 0; i < n; ++i) {
+      const int tile = pd[i].tile;
+      if (pd[i].kind == 1) { ytile[ny++] = tile; continue; }
+      const long long gu0 = cum + (long long)tile * G, gu1 = gu0 + G;
+      const int wa = sp.owner(gu0), wb = sp.owner(gu1 - 1);
+      unsigned* cnt = (W13 ? p.cnt13 + (size_t)v * (p.F / 16) : p.cnt2 + (size_t)v * (p.H / 16)) + tile;
+      unsigned prev = 0;
+      if (lane == 0) prev = atomicAdd(cnt, 1u);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev != (unsigned)(wb - wa)) continue;
+      // last piece of the tile: add all pieces in warp order (deterministic)
+      __threadfence();
+      float sum[NMAT][4];
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sum[m][q] = 0.f;
+      for (int w2 = wa; w2 <= wb; ++w2) {
+        const int ks = sp.b(w2) >= gu0 ? 0 : 1;
+        const float* src = p.part + (((size_t)w2 * 2 + ks) * 32 + lane) * kPartFloats;
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m) {
+          const float4 q = __ldcg(reinterpret_cast<const float4*>(src + 4 * m));
+          sum[m][0] += q.x; sum[m][1] += q.y; sum[m][2] += q.z; sum[m][3] += q.w;
+        }
+      }
+      if (lane == 0) *cnt = 0u;
+      if constexpr (W13) {
+        finalize13(p, vj, tile * 16, sum);
+      } else {
+        store_ob(p, vj, tile, sum);
+        ytile[ny++] = tile;
+      }
+    }
+    if (ny) {
+      __syncwarp();
+      __threadfence();
+      for (int i = 0; i < ny; ++i) publish_y(p, ytile[i], nv);
+    }
+  };
+  // global B-operand sources (only when the slots do not fit the ring)
+  const uint4* gx0 = XR ? nullptr : xsrc_of(0, xg);
+  const uint4* gx1 = XR ? nullptr : xsrc_of(XS - 1, xg);
+  const float* gz0 = XR ? nullptr : zsrc_of(z0);
+  const float* gz1 = XR ? nullptr : zsrc_of(z1);
 
   for (long long l = a; l < b; ++l) {
     __syncwarp();                                  // slot being refilled is consumed
@@ -442,9 +516,9 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
         }
       } else {
         const size_t gb = (size_t)(c_grp * BPG + blk);
-        xb = __ldg(xsrc[0][xg] + gb * 4 + t);
-        if constexpr (SPLIT) xl = __ldg(xsrc[XS - 1][xg] + gb * 4 + t);
-        if constexpr (ENC == HB_Q2) { s0 = __ldg(zsrc[z0] + gb); s1 = __ldg(zsrc[z1] + gb); }
+        xb = __ldg(gx0 + gb * 4 + t);
+        if constexpr (SPLIT) xl = __ldg(gx1 + gb * 4 + t);
+        if constexpr (ENC == HB_Q2) { s0 = __ldg(gz0 + gb); s1 = __ldg(gz1 + gb); }
       }
 #pragma unroll
       for (int m = 0; m < NMAT; ++m) {
@@ -484,46 +558,30 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
         }
       }
     }
-    // ---- end of a tile piece?
+    // ---- end of a tile piece?  (anything that needs a fence is deferred to the
+    // end of the run, so the cp.async pipeline never drains mid-stream)
     if (c_grp == G - 1 || l == b - 1) {
-      const long long gu0 = cum + (long long)c_tile * G, gu1 = gu0 + G;
+      if (npend == kMaxPend) {                 // cannot happen at production sizes
+        cp_wait<0>();
+        publish(pend, npend);
+        npend = 0;
+      }
       if (piece0 == 0 && c_grp == G - 1) {
-        if constexpr (W13) finalize13(p, vj, c_tile * 16, acc);
-        else finalize2(p, vj, c_tile, nv, acc);
+        if constexpr (W13) {
+          finalize13(p, vj, c_tile * 16, acc);
+        } else {
+          store_ob(p, vj, c_tile, acc);
+          pend[npend++] = Pend{c_tile, 1};
+        }
       } else {
-        // partial piece: store, count, the last piece's warp adds all in warp order
+        // partial piece: store it; counting / combining happens in publish()
+        const long long gu0 = cum + (long long)c_tile * G;
         const int pslot_k = sp.b(gw) >= gu0 ? 0 : 1;
         float* dst = p.part + (((size_t)gw * 2 + pslot_k) * 32 + lane) * kPartFloats;
 #pragma unroll
         for (int m = 0; m < NMAT; ++m)
           *reinterpret_cast<float4*>(dst + 4 * m) = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
-        __syncwarp();
-        __threadfence();
-        const int wa = sp.owner(gu0), wb = sp.owner(gu1 - 1);
-        unsigned* cnt = (W13 ? p.cnt13 + (size_t)v * (p.F / 16) : p.cnt2 + (size_t)v * (p.H / 16)) + c_tile;
-        unsigned prev = 0;
-        if (lane == 0) prev = atomicAdd(cnt, 1u);
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev == (unsigned)(wb - wa)) {
-          __threadfence();
-          float sum[NMAT][4];
-#pragma unroll
-          for (int m = 0; m < NMAT; ++m)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) sum[m][i] = 0.f;
-          for (int w2 = wa; w2 <= wb; ++w2) {
-            const int ks = sp.b(w2) >= gu0 ? 0 : 1;
-            const float* src = p.part + (((size_t)w2 * 2 + ks) * 32 + lane) * kPartFloats;
-#pragma unroll
-            for (int m = 0; m < NMAT; ++m) {
-              const float4 q = __ldcg(reinterpret_cast<const float4*>(src + 4 * m));
-              sum[m][0] += q.x; sum[m][1] += q.y; sum[m][2] += q.z; sum[m][3] += q.w;
-            }
-          }
-          if (lane == 0) *cnt = 0u;
-          if constexpr (W13) finalize13(p, vj, c_tile * 16, sum);
-          else finalize2(p, vj, c_tile, nv, sum);
-        }
+        pend[npend++] = Pend{c_tile, 0};
       }
 #pragma unroll
       for (int m = 0; m < NMAT; ++m)
@@ -535,6 +593,7 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
   }
   cp_wait<0>();
   __syncwarp();
+  publish(pend, npend);
 }
 
 extern __shared__ __align__(128) uint8_t gemv_smem[];
@@ -554,10 +613,14 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   const int K = W13 ? p.H : p.F;
   long long U = 0;
   for (int v = 0; v < nv; ++v) U += (long long)T * (K / epg_of(get_vjob(p, v).enc));
-  Space sp{U, (int)(gridDim.x * kGemvWarps)};
-  const int gw = blockIdx.x * kGemvWarps + warp;
+  // at most U warps take part, so every participating warp owns >= 1 unit
+  Space sp{U, (int)min((long long)gridDim.x * kGemvWarps, U)};
+  // warp ranges are dealt SM-interleaved: consecutive ranges (same job, same
+  // encoding) land on different SMs, so every SM gets the same mix of
+  // fp16 (HBM-heavy) and low-bit (ALU-heavy) units
+  const int gw = warp * gridDim.x + blockIdx.x;
+  if (gw >= sp.NW) return;
   const long long u0 = sp.b(gw), u1 = sp.b(gw + 1);
-  if (u0 >= u1) return;
   const uint32_t ring = smem_u32(gemv_smem) + warp * kWarpSmem;
   long long cum = 0;
   int v = 0;

@@ -12,14 +12,21 @@ namespace hb {
 constexpr int kMaxTopK = 8;
 constexpr int kMaxRouteLayers = 4;      // 1 + max lookahead p handled per launch
 constexpr int kNumSM = 148;             // B200
-constexpr int kGemvWarps = 16;          // warps per GEMV CTA (one CTA per SM)
+#ifndef HB_GEMV_WARPS
+#define HB_GEMV_WARPS 16
+#endif
+#ifndef HB_WARP_SMEM_KB
+#define HB_WARP_SMEM_KB 13
+#endif
+constexpr int kGemvWarps = HB_GEMV_WARPS;   // warps per GEMV CTA (one CTA per SM)
 constexpr int kRouterThreads = 128;
 
 // Byte offsets of the sections of one matrix inside an expert blob.
+// Tile-major layout: unit (tile of 16 rows, 64-byte group) = 1 KB of codes at
+// q + 1024*unit, and 16 scale records of SB bytes at s + 16*SB*unit.
 struct MatLayout {
-  uint64_t q;        // codes (or the fp16 matrix for F16)
-  uint64_t d;        // fp16 scales [N][K/32]
-  uint64_t m;        // fp16 mins   [N][K/32] (Q2 only)
+  uint64_t q;        // code section (the permuted fp16 values for F16)
+  uint64_t s;        // scale section: per (unit, row) d[BPG] (+ m[BPG] for Q2)
 };
 struct BlobLayout {
   MatLayout mat[3];  // W1 [F,H], W3 [F,H], W2 [H,F]

@@ -17,16 +17,33 @@ namespace hb {
 
 __device__ __forceinline__ float f16(const __half* p, size_t i) { return __half2float(p[i]); }
 
-// one thread per (row, 64-byte group); writes the group's 16 words + scales
+// F16 "codes": the fp16 values permuted into tile-major units
+__global__ void f16_tile_kernel(const __half* __restrict__ w, int n, int k, uint8_t* __restrict__ q) {
+  const int groups = k / 32;
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)n * groups) return;
+  const int row = (int)(gid / groups), grp = (int)(gid % groups);
+  const uint4* src = reinterpret_cast<const uint4*>(w + (size_t)row * k + (size_t)grp * 32);
+  const size_t unit = (size_t)(row / 16) * groups + grp;
+  uint4* dst = reinterpret_cast<uint4*>(q + unit * 1024 + (row % 16) * 64);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dst[i] = src[i];
+}
+
+// one thread per (row, 64-byte group); writes the row's 64 bytes of the unit
+// (tile-major layout) and its scale record
 template <int ENC>
 __global__ void quant_kernel(const __half* __restrict__ w, int n, int k, uint8_t* __restrict__ q,
-                             __half* __restrict__ dsec, __half* __restrict__ msec) {
+                             uint8_t* __restrict__ ssec) {
   constexpr int EPG = ENC == HB_Q8 ? 64 : ENC == HB_Q4 ? 128 : 256;
   constexpr int BPG = EPG / 32;
+  constexpr int SB = 2 * BPG * (ENC == HB_Q2 ? 2 : 1);
   const int groups = k / EPG;
   const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (gid >= (long long)n * groups) return;
   const int row = (int)(gid / groups), grp = (int)(gid % groups);
+  const size_t unit = (size_t)(row / 16) * groups + grp;
+  __half* rec = reinterpret_cast<__half*>(ssec + (unit * 16 + row % 16) * SB);
   const __half* src = w + (size_t)row * k + (size_t)grp * EPG;
   uint32_t words[16];
 #pragma unroll
@@ -48,7 +65,7 @@ __global__ void quant_kernel(const __half* __restrict__ w, int n, int k, uint8_t
         r = fminf(fmaxf(r, -127.f), 127.f);
         code[i] = (int)r;
       }
-      dsec[(size_t)row * (k / 32) + grp * BPG + j] = d16;
+      rec[j] = d16;
     } else if (ENC == HB_Q4) {
       float m = 0.f;                                  // signed value of max |x|, first on ties
       for (int i = 0; i < 32; ++i) {
@@ -64,7 +81,7 @@ __global__ void quant_kernel(const __half* __restrict__ w, int n, int k, uint8_t
         r = fminf(fmaxf(r, 0.f), 15.f);
         code[i] = (int)r;
       }
-      dsec[(size_t)row * (k / 32) + grp * BPG + j] = d16;
+      rec[j] = d16;
     } else {
       float mn = f16(x, 0), mx = f16(x, 0);
       for (int i = 1; i < 32; ++i) {
@@ -82,8 +99,8 @@ __global__ void quant_kernel(const __half* __restrict__ w, int n, int k, uint8_t
         r = fminf(fmaxf(r, 0.f), 3.f);
         code[i] = (int)r;
       }
-      dsec[(size_t)row * (k / 32) + grp * BPG + j] = d16;
-      msec[(size_t)row * (k / 32) + grp * BPG + j] = m16;
+      rec[j] = d16;
+      rec[BPG + j] = m16;
     }
     (void)dval;
     (void)mval;
@@ -103,8 +120,7 @@ __global__ void quant_kernel(const __half* __restrict__ w, int n, int k, uint8_t
         }
       }
   }
-  const size_t rowbytes = (size_t)k * (ENC == HB_Q8 ? 8 : ENC == HB_Q4 ? 4 : 2) / 8;
-  uint4* dst = reinterpret_cast<uint4*>(q + (size_t)row * rowbytes + (size_t)grp * 64);
+  uint4* dst = reinterpret_cast<uint4*>(q + unit * 1024 + (row % 16) * 64);
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     dst[i] = make_uint4(words[4 * i], words[4 * i + 1], words[4 * i + 2], words[4 * i + 3]);
@@ -119,20 +135,19 @@ int launch_quantize_expert(int enc, int hidden, int ffn, const __half* w1, const
   const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
   for (int m = 0; m < 3; ++m) {
     if (enc == HB_F16) {
-      if (cudaMemcpyAsync(blob + L.mat[m].q, src[m], (size_t)N[m] * K[m] * 2,
-                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-        return HB_ECUDA;
+      const long long threads = (long long)N[m] * (K[m] / 32);
+      f16_tile_kernel<<<(int)((threads + 127) / 128), 128, 0, s>>>(src[m], N[m], K[m],
+                                                                     blob + L.mat[m].q);
       continue;
     }
     const int epg = enc == HB_Q8 ? 64 : enc == HB_Q4 ? 128 : 256;
     const long long threads = (long long)N[m] * (K[m] / epg);
     const int grid = (int)((threads + 127) / 128);
     uint8_t* q = blob + L.mat[m].q;
-    __half* d = reinterpret_cast<__half*>(blob + L.mat[m].d);
-    __half* mn = reinterpret_cast<__half*>(blob + L.mat[m].m);
-    if (enc == HB_Q8) quant_kernel<HB_Q8><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, d, mn);
-    else if (enc == HB_Q4) quant_kernel<HB_Q4><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, d, mn);
-    else quant_kernel<HB_Q2><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, d, mn);
+    uint8_t* sc = blob + L.mat[m].s;
+    if (enc == HB_Q8) quant_kernel<HB_Q8><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, sc);
+    else if (enc == HB_Q4) quant_kernel<HB_Q4><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, sc);
+    else quant_kernel<HB_Q2><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, sc);
   }
   return cudaGetLastError() == cudaSuccess ? HB_OK : HB_ECUDA;
 }

@@ -32,7 +32,7 @@ def test_blob_layout_matches_oracle(enc, hf):
     assert blob_bytes(enc, H, F) == fm.blob_bytes(enc, H, F)
     lay, _ = fm.blob_layout(enc, H, F)
     for mat in range(3):
-        for sec, name in enumerate(["q", "d", "m"]):
+        for sec, name in enumerate(["q", "s", "none"]):
             key = "w" if (enc == fm.F16 and name == "q") else name
             if key not in lay[mat]:
                 with pytest.raises(L.HobbitError):

@@ -42,20 +42,21 @@ def _load_fixture(name):
 
 @pytest.mark.parametrize("name", ["formats_q4.txt", "formats_q2.txt", "formats_q8.txt"])
 def test_decode_hand_worked(name):
+    # one 16-row tile, one group (K = EPG): row 0's 64 bytes are the first 64
+    # bytes of the code section and its scale record the first SB bytes of the
+    # scale section (d of each block, then m for Q2); other rows are defaults
     spec = _load_fixture(name)
     enc, K = spec["enc"], spec["K"]
-    q = np.full(K * fm.QBITS[enc] // 8, spec["default"], dtype=np.uint8)
+    assert K == fm.EPG[enc]
+    q = np.full(16 * 64, spec["default"], dtype=np.uint8)
     for off, v in spec["bytes"].items():
         q[off] = v
-    d = np.array(spec["scales"], dtype=np.uint16)
-    buf = [q.tobytes(), d.tobytes()]
-    secs = {"q": (0, q.size), "d": (q.size, 2 * d.size)}
-    if spec["mins"] is not None:
-        m = np.array(spec["mins"], dtype=np.uint16)
-        secs["m"] = (q.size + 2 * d.size, 2 * m.size)
-        buf.append(m.tobytes())
-    blob = np.frombuffer(b"".join(buf), dtype=np.uint8)
-    w = fm.decode_matrix(enc, blob, secs, 1, K)[0]
+    rec = spec["scales"] + (spec["mins"] or [])
+    s = np.zeros(16 * fm.scale_record_bytes(enc) // 2, dtype=np.uint16)
+    s[:len(rec)] = rec
+    blob = np.concatenate([q, s.view(np.uint8)])
+    secs = {"q": (0, q.size), "s": (q.size, s.nbytes)}
+    w = fm.decode_matrix(enc, blob, secs, 16, K)[0]
     for k, v in spec["expect"].items():
         assert w[k] == v, (name, k, w[k], v)
     if enc == fm.Q4:      # every unlisted element has the default code 8 -> 0
@@ -68,19 +69,36 @@ def test_fp16_values():
     assert list(v.astype(np.float64)) == [0.5, 0.25, -0.375, 2.0 ** -6, 1.0]
 
 
-@pytest.mark.parametrize("enc", [fm.Q8, fm.Q4, fm.Q2])
-def test_code_location_is_a_bijection(enc):
-    """Every bit of a 2-group row is written by exactly one element."""
-    K = 2 * fm.row_group(enc)
+@pytest.mark.parametrize("enc", [fm.F16, fm.Q8, fm.Q4, fm.Q2])
+def test_code_offset_is_a_bijection(enc):
+    """Every bit of a 2-tile x 2-group code section is written by exactly one
+    element, and every scale byte by exactly one (row, block, d/m)."""
+    N, K = 32, 2 * fm.EPG[enc]
     b = fm.QBITS[enc]
-    byte, shift = fm.code_location(enc, np.arange(K))
-    bits = set()
-    for k in range(K):
-        for i in range(b):
-            bit = int(byte[k]) * 8 + int(shift[k]) + i
-            assert bit not in bits
-            bits.add(bit)
-    assert bits == set(range(K * b))
+    n, k = np.meshgrid(np.arange(N), np.arange(K), indexing="ij")
+    pos, shift = fm.code_offset(enc, n, k, K)
+    bits = (pos * 8 + shift)[..., None] + np.arange(b)
+    assert np.array_equal(np.sort(bits.ravel()), np.arange(N * K * b))
+    if enc == fm.F16:
+        return
+    nb, blk = np.meshgrid(np.arange(N), np.arange(K // 32), indexing="ij")
+    offs = [fm.scale_offset(enc, nb, blk, K, "d")]
+    if enc == fm.Q2:
+        offs.append(fm.scale_offset(enc, nb, blk, K, "m"))
+    allb = np.concatenate([(o[..., None] + np.arange(2)).ravel() for o in offs])
+    assert np.array_equal(np.sort(allb), np.arange(N * (K // fm.EPG[enc]) * fm.scale_record_bytes(enc)))
+
+
+def test_unit_is_contiguous():
+    """A unit (16 rows x one group) occupies one contiguous 1 KB of the code section."""
+    for enc in (fm.F16, fm.Q8, fm.Q4, fm.Q2):
+        K = 4 * fm.EPG[enc]
+        n, k = np.meshgrid(np.arange(16, 32), np.arange(2 * fm.EPG[enc], 3 * fm.EPG[enc]),
+                           indexing="ij")
+        pos, _ = fm.code_offset(enc, n, k, K)
+        unit = 1 * 4 + 2                      # tile 1, group 2
+        last = pos.max() + (1 if enc == fm.F16 else 0)    # fp16: 2-byte elements
+        assert pos.min() == 1024 * unit and last == 1024 * unit + 1023
 
 
 def test_quantiser_q4_worked_example():
@@ -109,16 +127,17 @@ def test_quantiser_roundtrip_bound(enc):
     rng = np.random.default_rng(7)
     n, k = 64, 512
     w = (rng.standard_normal((n, k)) * 0.02).astype(np.float16)
-    sec = dict(zip(["q", "d", "m"], [None] * 3))
     codes, d16, m16 = fm.quantize_codes(enc, w)
     q = fm.pack_codes(enc, codes)
-    parts = [q.ravel(), d16.view(np.uint8).ravel()]
-    sec = {"q": (0, q.size), "d": (q.size, d16.size * 2)}
-    if m16 is not None:
-        sec["m"] = (q.size + d16.size * 2, m16.size * 2)
-        parts.append(m16.view(np.uint8).ravel())
-    blob = np.concatenate(parts)
+    s = fm.pack_scales(enc, d16, m16)
+    blob = np.concatenate([q, s])
+    sec = {"q": (0, q.size), "s": (q.size, s.size)}
     deq = fm.decode_matrix(enc, blob, sec, n, k)
+    # and the decode reproduces the codes' own dequantisation element-wise
+    dd = np.repeat(d16.astype(np.float64), 32, axis=1)
+    own = {fm.Q8: dd * codes, fm.Q4: dd * (codes - 8),
+           fm.Q2: dd * codes + (np.repeat(m16.astype(np.float64), 32, axis=1) if m16 is not None else 0)}[enc]
+    assert np.array_equal(deq, own)
     d = np.abs(np.repeat(d16.astype(np.float64), 32, axis=1))
     err = np.abs(deq - w.astype(np.float64))
     # scale rounding: d carries a relative error <= 2^-11, which can move the
