@@ -142,21 +142,31 @@ __host__ __device__ constexpr int epg_of(int enc) {
   return enc == HB_F16 ? 32 : enc == HB_Q8 ? 64 : enc == HB_Q4 ? 128 : 256;
 }
 
-constexpr int kWarpSmem = HB_WARP_SMEM_KB * 1024;       // per-warp cp.async ring
-constexpr int kGemvSmem = kGemvWarps * kWarpSmem;       // 208 KB per CTA
-constexpr int kXSlots = 2;                              // token slots staged in the ring
+// Shared memory of a GEMV CTA: kGemvWarps private cp.async rings (weights +
+// scales) followed by ONE CTA-wide stage of the B operand (x for K2a, h hi/lo
+// for K2b, and their block sums), loaded once per CTA.  Reading B from a
+// CTA copy instead of per unit from L2 avoids hammering the same few L2 lines
+// from every warp of the GPU (measured: it capped the kernels at ~4.5 TB/s).
+template <bool W13> struct KCfg;
+template <> struct KCfg<true> {        // K2a: x is small (8 KB per token at H=4096)
+  static constexpr int RING = 12 * 1024;
+  static constexpr int XSTAGE = 32 * 1024;
+};
+template <> struct KCfg<false> {       // K2b: h of two slots is 118 KB at F=14336
+  static constexpr int RING = 6656;
+  static constexpr int XSTAGE = 120 * 1024;
+};
+template <bool W13>
+constexpr int gemv_smem_bytes() { return kGemvWarps * KCfg<W13>::RING + KCfg<W13>::XSTAGE; }
 
-// Ring stage layout of one unit: W codes | S scales | X B-fragments | Z block sums
-template <int ENC, int NMAT, bool SPLIT>
+// Ring stage layout of one unit: W codes | S scales
+template <int ENC, int NMAT, int RINGB>
 struct Ring {
   static constexpr int BPG = Enc<ENC>::BPG, SB = Enc<ENC>::SB;
-  static constexpr int XS = SPLIT ? 2 : 1;
   static constexpr int W = NMAT * 1024;
   static constexpr int S = NMAT * 16 * SB;
-  static constexpr int X = XS * kXSlots * BPG * 64;
-  static constexpr int Z = ENC == HB_Q2 ? kXSlots * BPG * 4 : 0;
-  static constexpr int STAGE = (W + S + X + Z + 127) / 128 * 128;
-  static constexpr int DEPTH = kWarpSmem / STAGE >= 16 ? 16 : kWarpSmem / STAGE;
+  static constexpr int STAGE = (W + S + 127) / 128 * 128;
+  static constexpr int DEPTH = RINGB / STAGE >= 16 ? 16 : RINGB / STAGE;
   static_assert(DEPTH >= 2, "ring too small");
 };
 
@@ -323,13 +333,18 @@ constexpr int kMaxPend = 4;
 // ------------------------------------------------------------ the run
 // Stream units [a, b) of virtual job v (unit l = tile * G + grp) through the
 // warp's ring.  W13: K2a (W1 and W3 rows, x); else K2b (W2 rows, h hi/lo).
+// XR: the B operand of every slot is in the CTA stage at shared address xst
+// (W13: x_perm [B][H/8] uint4 | xsum [B][H/32]; W2: h_hi [S][F/8] | h_lo
+// [S][F/8] | hsum [S][F/32]); otherwise it is read from global memory.
 template <int ENC, bool W13, bool XR>
 __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long long cum,
-                    long long a, long long b, const Space& sp, int gw, uint32_t ring) {
+                    long long a, long long b, const Space& sp, int gw, uint32_t ring,
+                    uint32_t xst, int nrows_x) {
   constexpr int NMAT = W13 ? 2 : 1;
   constexpr bool SPLIT = !W13;
-  using R = Ring<ENC, NMAT, SPLIT>;
-  constexpr int BPG = R::BPG, SB = R::SB, XS = R::XS, DEPTH = R::DEPTH;
+  constexpr int XS = SPLIT ? 2 : 1;
+  using R = Ring<ENC, NMAT, KCfg<W13>::RING>;
+  constexpr int BPG = R::BPG, SB = R::SB, DEPTH = R::DEPTH;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int K = W13 ? p.H : p.F;
   const int G = K / Enc<ENC>::EPG;
@@ -364,36 +379,7 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
     else return p.hsum + (size_t)sl * (p.F / 32);
   };
 
-  // ---- producer state
-  int p_grp = (int)(a % G);
-  // B fragments: copy descriptors of this lane (fixed per run), source offset + grp*BPG*4
-  constexpr int NCP = (BPG * kXSlots * XS * 4 + 31) / 32;
-  const uint4* xc_src[NCP];
-  uint32_t xc_dst[NCP];
-  bool xc_on[NCP];
-  const float* zc_src = nullptr;
-  uint32_t zc_dst = 0;
-  if constexpr (XR) {
-    const int ncp = BPG * ns * XS * 4;
-#pragma unroll
-    for (int i = 0; i < NCP; ++i) {
-      const int c = lane + 32 * i;
-      xc_on[i] = c < ncp;
-      const int tt = c & 3;
-      int r = c >> 2;
-      const int part = r % XS;
-      r /= XS;
-      const int sl = r % ns, blk = r / ns;
-      xc_src[i] = xc_on[i] ? xsrc_of(part, sl) + blk * 4 + tt : nullptr;
-      xc_dst[i] = R::W + R::S + ((part * kXSlots + sl) * BPG + blk) * 64 + tt * 16;
-    }
-    if constexpr (ENC == HB_Q2) {
-      if (lane < ns * BPG) {
-        zc_src = zsrc_of(lane / BPG) + (lane % BPG);
-        zc_dst = R::W + R::S + R::X + ((lane / BPG) * BPG + (lane % BPG)) * 4;
-      }
-    }
-  }
+  // ---- producer: weights + scales only (B operand is in the CTA stage)
   long long pl = a;
   int pslot = 0;
   auto issue = [&]() {
@@ -406,18 +392,9 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
         if constexpr (SB > 0)
           if (s_act) cp_async16_ef(st + R::W + m * 16 * SB + 16 * lane, sp_[m], pol);
       }
-      if constexpr (XR) {
-        const size_t xo = (size_t)p_grp * BPG * 4;
-#pragma unroll
-        for (int i = 0; i < NCP; ++i)
-          if (xc_on[i]) cp_async16(st + xc_dst[i], xc_src[i] + xo);
-        if constexpr (ENC == HB_Q2)
-          if (zc_src) cp_async4(st + zc_dst, zc_src + p_grp * BPG);
-      }
       ++pl;
 #pragma unroll
       for (int m = 0; m < NMAT; ++m) { qp[m] += 1024; sp_[m] += 16 * SB; }
-      if (++p_grp == G) p_grp = 0;
       if (++pslot == DEPTH) pslot = 0;
     }
     cp_commit();
@@ -483,11 +460,21 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
       for (int i = 0; i < ny; ++i) publish_y(p, ytile[i], nv);
     }
   };
-  // global B-operand sources (only when the slots do not fit the ring)
+  // B-operand sources: rows (token for x, slot for h) of the lane's fragment slots
+  auto row_of = [&](int s) -> int {
+    const int sl = vj.slot0 + min(s, ns - 1);
+    return W13 ? p.jt.slot_token[sl] : sl;
+  };
   const uint4* gx0 = XR ? nullptr : xsrc_of(0, xg);
   const uint4* gx1 = XR ? nullptr : xsrc_of(XS - 1, xg);
   const float* gz0 = XR ? nullptr : zsrc_of(z0);
   const float* gz1 = XR ? nullptr : zsrc_of(z1);
+  // stage addresses (XR): part p of row r at xst + (p*nrows + r)*K*2, sums after
+  const uint32_t sxb = xst + (uint32_t)row_of(xg) * K * 2 + t * 16;
+  const uint32_t sxl = sxb + (uint32_t)nrows_x * K * 2;
+  const uint32_t szb = xst + (uint32_t)XS * nrows_x * K * 2;
+  const uint32_t sz0 = szb + (uint32_t)row_of(z0) * (K / 32) * 4;
+  const uint32_t sz1 = szb + (uint32_t)row_of(z1) * (K / 32) * 4;
 
   for (long long l = a; l < b; ++l) {
     __syncwarp();                                  // slot being refilled is consumed
@@ -507,12 +494,12 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
       uint4 xb, xl;
       float s0 = 0.f, s1 = 0.f;
       if constexpr (XR) {
-        const uint32_t sx = st + R::W + R::S;
-        xb = lds128(sx + ((0 * kXSlots + xg) * BPG + blk) * 64 + t * 16);
-        if constexpr (SPLIT) xl = lds128(sx + ((1 * kXSlots + xg) * BPG + blk) * 64 + t * 16);
+        const uint32_t gb = (uint32_t)(c_grp * BPG + blk);
+        xb = lds128(sxb + gb * 64);
+        if constexpr (SPLIT) xl = lds128(sxl + gb * 64);
         if constexpr (ENC == HB_Q2) {
-          s0 = lds_f32(sx + R::X + (z0 * BPG + blk) * 4);
-          s1 = lds_f32(sx + R::X + (z1 * BPG + blk) * 4);
+          s0 = lds_f32(sz0 + gb * 4);
+          s1 = lds_f32(sz1 + gb * 4);
         }
       } else {
         const size_t gb = (size_t)(c_grp * BPG + blk);
@@ -611,6 +598,24 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   }
   const int T = W13 ? p.F / 16 : p.H / 16;
   const int K = W13 ? p.H : p.F;
+  constexpr int XS = W13 ? 1 : 2;
+  // ---- CTA stage of the B operand (all rows: tokens for x, slots for h)
+  const uint32_t xst = smem_u32(gemv_smem) + kGemvWarps * KCfg<W13>::RING;
+  const int nrows = W13 ? p.B : p.jt.hdr[1];
+  const size_t stage_bytes = (size_t)nrows * (XS * K * 2 + (K / 32) * 4);
+  const bool xr = stage_bytes <= (size_t)KCfg<W13>::XSTAGE;
+  if (xr) {
+    uint4* dst = reinterpret_cast<uint4*>(gemv_smem + kGemvWarps * KCfg<W13>::RING);
+    const int n16 = nrows * (K / 8);                          // one part, all rows
+    const uint4* src0 = W13 ? p.x_perm : p.h_hi;
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldcg(src0 + i);
+    if (!W13)
+      for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[n16 + i] = __ldcg(p.h_lo + i);
+    const uint4* zs = reinterpret_cast<const uint4*>(W13 ? p.xsum : p.hsum);
+    const int nz16 = nrows * (K / 32) / 4;
+    for (int i = threadIdx.x; i < nz16; i += blockDim.x) dst[XS * n16 + i] = __ldcg(zs + i);
+  }
+  __syncthreads();
   long long U = 0;
   for (int v = 0; v < nv; ++v) U += (long long)T * (K / epg_of(get_vjob(p, v).enc));
   // at most U warps take part, so every participating warp owns >= 1 unit
@@ -621,7 +626,7 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   const int gw = warp * gridDim.x + blockIdx.x;
   if (gw >= sp.NW) return;
   const long long u0 = sp.b(gw), u1 = sp.b(gw + 1);
-  const uint32_t ring = smem_u32(gemv_smem) + warp * kWarpSmem;
+  const uint32_t ring = smem_u32(gemv_smem) + warp * KCfg<W13>::RING;
   long long cum = 0;
   int v = 0;
   for (; v < nv; ++v) {                                       // vjob containing u0
@@ -634,17 +639,18 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
     const VJob vj = get_vjob(p, v);
     const long long Uv = (long long)T * (K / epg_of(vj.enc));
     const long long a = u - cum, b = min(u1, cum + Uv) - cum;
-    const bool xr = vj.nslot <= kXSlots;
+#define HB_RUN(E, X) run<E, W13, X>(p, vj, v, nv, cum, a, b, sp, gw, ring, xst, nrows)
     switch (vj.enc * 2 + (xr ? 1 : 0)) {
-      case 2 * HB_F16 + 1: run<HB_F16, W13, true>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
-      case 2 * HB_F16 + 0: run<HB_F16, W13, false>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
-      case 2 * HB_Q8 + 1: run<HB_Q8, W13, true>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
-      case 2 * HB_Q8 + 0: run<HB_Q8, W13, false>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
-      case 2 * HB_Q4 + 1: run<HB_Q4, W13, true>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
-      case 2 * HB_Q4 + 0: run<HB_Q4, W13, false>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
-      case 2 * HB_Q2 + 1: run<HB_Q2, W13, true>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
-      default: run<HB_Q2, W13, false>(p, vj, v, nv, cum, a, b, sp, gw, ring); break;
+      case 2 * HB_F16 + 1: HB_RUN(HB_F16, true); break;
+      case 2 * HB_F16 + 0: HB_RUN(HB_F16, false); break;
+      case 2 * HB_Q8 + 1: HB_RUN(HB_Q8, true); break;
+      case 2 * HB_Q8 + 0: HB_RUN(HB_Q8, false); break;
+      case 2 * HB_Q4 + 1: HB_RUN(HB_Q4, true); break;
+      case 2 * HB_Q4 + 0: HB_RUN(HB_Q4, false); break;
+      case 2 * HB_Q2 + 1: HB_RUN(HB_Q2, true); break;
+      default: HB_RUN(HB_Q2, false); break;
     }
+#undef HB_RUN
     u = cum + b;
     cum += Uv;
     ++v;
@@ -652,22 +658,24 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
 }
 
 template <typename Kern>
-static void set_smem(Kern kernel, bool& done) {
+static void set_smem(Kern kernel, int bytes, bool& done) {
   if (!done) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmem);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     done = true;
   }
 }
 
 void launch_w13(const GemvParams& p, cudaStream_t s) {
   static bool d = false;
-  set_smem(gemv_kernel<true>, d);
-  gemv_kernel<true><<<kGemvCTAs, kGemvWarps * 32, kGemvSmem, s>>>(p);
+  constexpr int smem = gemv_smem_bytes<true>();
+  set_smem(gemv_kernel<true>, smem, d);
+  gemv_kernel<true><<<kGemvCTAs, kGemvWarps * 32, smem, s>>>(p);
 }
 void launch_w2(const GemvParams& p, cudaStream_t s) {
   static bool d = false;
-  set_smem(gemv_kernel<false>, d);
-  gemv_kernel<false><<<kGemvCTAs, kGemvWarps * 32, kGemvSmem, s>>>(p);
+  constexpr int smem = gemv_smem_bytes<false>();
+  set_smem(gemv_kernel<false>, smem, d);
+  gemv_kernel<false><<<kGemvCTAs, kGemvWarps * 32, smem, s>>>(p);
 }
 
 }  // namespace hb
