@@ -50,6 +50,27 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic():
+    """DRAM bytes (read + write) of one K2a + one K2b launch from the newest committed
+    `ncu --set full` summary under profiles/ (tools/ncu_summary.py), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as f:
+            ks = json.load(f)["kernels"]
+        tot = {}
+        for k in ks:
+            if "gemv_kernel" in k["kernel"]:
+                tot.setdefault(k["kernel"], k["dram_read"] + k.get("dram_write", 0.0))
+        if len(tot) != 2:
+            return None, None
+        return int(sum(tot.values())), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 # ------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -290,6 +311,7 @@ def run_ours(args):
     gemv_bytes = sum(k2a_bytes) + sum(k2b_bytes)
     achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
+    traffic, traffic_src = ncu_traffic()
 
     # ---- end to end through the public API with host buffers
     Xh = torch.empty(P, L, Hd, dtype=torch.float16, pin_memory=True)
@@ -339,7 +361,9 @@ def run_ours(args):
         "gpu_launches": int(gpu_launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": None, "kernel": "K2a+K2b dequant-GEMV (w13_kernel, w2_kernel)",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "alg_bytes_per_launch_pair": int(gemv_bytes / (nprof * L)),
+                     "kernel": "K2a+K2b dequant-GEMV (gemv_kernel<1>, gemv_kernel<0>)",
                      "k2a_gbs": round(sum(k2a_bytes) / (k2a_ms * 1e-3) / 1e9, 1),
                      "k2b_gbs": round(sum(k2b_bytes) / (k2b_ms * 1e-3) / 1e9, 1),
                      "gemv_share_of_step": round(gemv_ms / nprof / ms_step, 4)},

@@ -42,6 +42,20 @@
 namespace hb {
 
 // ------------------------------------------------------------ primitives
+#ifdef HB_DBG_TIMELINE
+// diagnostic build only: per-warp %globaltimer stamps of the last K2a / K2b launch
+// [kernel][warp][0 entry, 1 stage done, 2 stream loop done, 3 publish done]
+__device__ unsigned long long g_tl[2][kGemvCTAs * kGemvWarps][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define HB_TL(W13, gw, i) do { if ((threadIdx.x & 31) == 0) g_tl[(W13) ? 0 : 1][gw][i] = gtimer(); } while (0)
+#else
+#define HB_TL(W13, gw, i) do { } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -489,6 +503,10 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
       w[m][0] = lds128(st + m * 1024 + g * 64 + 16 * t);
       w[m][1] = lds128(st + m * 1024 + (g + 8) * 64 + 16 * t);
     }
+#ifdef HB_DBG_NOCOMPUTE
+    acc[0][0] += __uint_as_float((w[0][0].x ^ w[0][1].y) & 0x3F800000u);
+    if (false)
+#endif
 #pragma unroll
     for (int blk = 0; blk < BPG; ++blk) {
       uint4 xb, xl;
@@ -547,7 +565,11 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
     }
     // ---- end of a tile piece?  (anything that needs a fence is deferred to the
     // end of the run, so the cp.async pipeline never drains mid-stream)
+#ifdef HB_DBG_NOEPI
+    if (false) {
+#else
     if (c_grp == G - 1 || l == b - 1) {
+#endif
       if (npend == kMaxPend) {                 // cannot happen at production sizes
         cp_wait<0>();
         publish(pend, npend);
@@ -580,7 +602,9 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
   }
   cp_wait<0>();
   __syncwarp();
+  HB_TL(W13, gw, 2);
   publish(pend, npend);
+  HB_TL(W13, gw, 3);
 }
 
 extern __shared__ __align__(128) uint8_t gemv_smem[];
@@ -589,6 +613,9 @@ template <bool W13>
 __global__ void __launch_bounds__(kGemvWarps * 32, 1)
 gemv_kernel(const __grid_constant__ GemvParams p) {
   const int warp = threadIdx.x >> 5;
+#ifdef HB_DBG_TIMELINE
+  HB_TL(W13, warp * gridDim.x + blockIdx.x, 0);
+#endif
   const int nv = n_vjobs(p);
   if (!W13 && nv == 0) {                                     // nothing owned: y = 0
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)p.B * p.H;
@@ -616,6 +643,7 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
     for (int i = threadIdx.x; i < nz16; i += blockDim.x) dst[XS * n16 + i] = __ldcg(zs + i);
   }
   __syncthreads();
+  HB_TL(W13, warp * gridDim.x + blockIdx.x, 1);
   long long U = 0;
   for (int v = 0; v < nv; ++v) U += (long long)T * (K / epg_of(get_vjob(p, v).enc));
   // at most U warps take part, so every participating warp owns >= 1 unit
@@ -679,3 +707,10 @@ void launch_w2(const GemvParams& p, cudaStream_t s) {
 }
 
 }  // namespace hb
+
+#ifdef HB_DBG_TIMELINE
+extern "C" int hb_debug_timeline(void* host, int which) {
+  return (int)cudaMemcpyFromSymbol(host, hb::g_tl, sizeof(hb::g_tl[0]),
+                                   (size_t)which * sizeof(hb::g_tl[0]));
+}
+#endif

@@ -111,6 +111,132 @@ __global__ void k_bulk(const uint8_t* buf, size_t units, int warps_per_cta, unsi
   if (acc == 0x12345678u) atomicAdd(out, 1ull);
 }
 
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t lop_magic(uint32_t a) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "n"(MASK), "n"(0x64006400));
+  return r;
+}
+
+// The K2a consumer emulated on the same stream: 2 matrices per 2 KB unit.
+// MODE 0: F16 (PRMT + 2 chained HMMA per matrix); 1: F16 with a fresh D per
+// unit (chain broken); 2: Q4 (4 blocks: LOP3 dequant + 2 HMMA + 4 FFMA each).
+template <int DEPTH, int MODE>
+__global__ void k_mma(const uint8_t* buf, size_t units, int warps_per_cta, unsigned long long* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = warp * gridDim.x + blockIdx.x, nw = gridDim.x * warps_per_cta;
+  const size_t u0 = (units / 2) * gw / nw * 2, u1 = (units / 2) * (gw + 1) / nw * 2;
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem) + warp * DEPTH * 2048;
+  float acc[2][4] = {};
+  const uint32_t xb0 = 0x3c003c00u, xb1 = 0x3c003c00u;
+  size_t pu = u0;
+  auto issue = [&]() {
+    if (pu < u1) {
+      const uint32_t st = ring + ((pu - u0) / 2 % DEPTH) * 2048;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        cp16(st + m * 1024 + 16 * lane, buf + (pu + m) * 1024 + 16 * lane);
+        cp16(st + m * 1024 + 512 + 16 * lane, buf + (pu + m) * 1024 + 512 + 16 * lane);
+      }
+      pu += 2;
+    }
+    commit();
+  };
+  for (int s = 0; s < DEPTH - 1; ++s) issue();
+  const int g = lane >> 2, t = lane & 3;
+  for (size_t u = u0; u < u1; u += 2) {
+    __syncwarp();
+    issue();
+    waitg<DEPTH - 1>();
+    __syncwarp();
+    const uint32_t st = ring + ((u - u0) / 2 % DEPTH) * 2048;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const uint4 a = lds128(st + m * 1024 + g * 64 + 16 * t);
+      const uint4 b = lds128(st + m * 1024 + (g + 8) * 64 + 16 * t);
+      if (MODE <= 1) {
+        float D[4] = {0.f, 0.f, 0.f, 0.f};
+        float (&tgt)[4] = MODE == 0 ? acc[m] : D;
+        mma16816(tgt, prmt(a.x, a.z, 0x5410), prmt(b.x, b.z, 0x5410), prmt(a.x, a.z, 0x7632),
+                 prmt(b.x, b.z, 0x7632), xb0, xb1);
+        mma16816(tgt, prmt(a.y, a.w, 0x5410), prmt(b.y, b.w, 0x5410), prmt(a.y, a.w, 0x7632),
+                 prmt(b.y, b.w, 0x7632), xb0, xb1);
+        if (MODE == 1)
+          for (int i = 0; i < 4; ++i) acc[m][i] += D[i];
+      } else {
+        const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int blk = 0; blk < 4; ++blk) {
+          const uint32_t w = wa[blk], w8 = w >> 8, v = wb[blk], v8 = v >> 8;
+          float D[4] = {0.f, 0.f, 0.f, 0.f};
+          mma16816(D, lop_magic<0x000F000Fu>(w), lop_magic<0x000F000Fu>(v),
+                   lop_magic<0x00F000F0u>(w), lop_magic<0x00F000F0u>(v), xb0, xb1);
+          mma16816(D, lop_magic<0x000F000Fu>(w8), lop_magic<0x000F000Fu>(v8),
+                   lop_magic<0x00F000F0u>(w8), lop_magic<0x00F000F0u>(v8), xb0, xb1);
+          const float d = 0.5f + blk;
+          for (int i = 0; i < 4; ++i) acc[m][i] = fmaf(d, D[i], acc[m][i]);
+        }
+      }
+    }
+  }
+  float s = 0.f;
+  for (int m = 0; m < 2; ++m)
+    for (int i = 0; i < 4; ++i) s += acc[m][i];
+  if (s == 1234.5f) atomicAdd(out, 1ull);
+}
+
+// NS separate streams per warp (matrix m of unit u at buf + m*span + u*1024),
+// like K2a's W1 / W3 code sections (+ scale sections) far apart in a blob
+template <int DEPTH, int NS>
+__global__ void k_streams(const uint8_t* buf, size_t units, int warps_per_cta, unsigned long long* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = warp * gridDim.x + blockIdx.x, nw = gridDim.x * warps_per_cta;
+  const size_t span = units / NS;                     // units per stream region
+  const size_t u0 = span * gw / nw, u1 = span * (gw + 1) / nw;
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem) + warp * DEPTH * NS * 1024;
+  uint32_t acc = 0;
+  size_t pu = u0;
+  auto issue = [&]() {
+    if (pu < u1) {
+      const uint32_t st = ring + ((pu - u0) % DEPTH) * NS * 1024;
+#pragma unroll
+      for (int m = 0; m < NS; ++m) {
+        const uint8_t* src = buf + ((size_t)m * span + pu) * 1024;
+        cp16(st + m * 1024 + 16 * lane, src + 16 * lane);
+        cp16(st + m * 1024 + 512 + 16 * lane, src + 512 + 16 * lane);
+      }
+      ++pu;
+    }
+    commit();
+  };
+  for (int s = 0; s < DEPTH - 1; ++s) issue();
+  for (size_t u = u0; u < u1; ++u) {
+    __syncwarp();
+    issue();
+    waitg<DEPTH - 1>();
+    const uint32_t st = ring + ((u - u0) % DEPTH) * NS * 1024;
+#pragma unroll
+    for (int m = 0; m < NS; ++m) {
+      uint4 a = lds128(st + m * 1024 + 16 * lane), b = lds128(st + m * 1024 + 512 + 16 * lane);
+      acc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w;
+    }
+  }
+  if (acc == 0x12345678u) atomicAdd(out, 1ull);
+}
+
 template <int UNROLL>
 __global__ void k_ldg(const uint8_t* buf, size_t units, int warps_per_cta, unsigned long long* out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -156,6 +282,37 @@ int main() {
   CK(cudaMemset(buf, 1, bytes));
   const size_t units = bytes / 1024;
   const int ctas = 148;
+  if (getenv("STREAMS")) {               // separate streams per warp
+    for (size_t mb : {4096, 300}) {
+      const size_t u = mb * 1024;
+      printf("streams=1 W=16 D=4 %5zu MB %7.0f GB/s\n", mb, run(k_streams<4, 1>, ctas, 16, 16 * 4 * 1024, buf, u, out));
+      printf("streams=2 W=16 D=4 %5zu MB %7.0f GB/s\n", mb, run(k_streams<4, 2>, ctas, 16, 16 * 4 * 2048, buf, u, out));
+      printf("streams=2 W=16 D=6 %5zu MB %7.0f GB/s\n", mb, run(k_streams<6, 2>, ctas, 16, 16 * 6 * 2048, buf, u, out));
+      printf("streams=2 W=8  D=6 %5zu MB %7.0f GB/s\n", mb, run(k_streams<6, 2>, ctas, 8, 8 * 6 * 2048, buf, u, out));
+      printf("streams=4 W=16 D=3 %5zu MB %7.0f GB/s\n", mb, run(k_streams<3, 4>, ctas, 16, 16 * 3 * 4096, buf, u, out));
+      printf("streams=4 W=8  D=4 %5zu MB %7.0f GB/s\n", mb, run(k_streams<4, 4>, ctas, 8, 8 * 4 * 4096, buf, u, out));
+    }
+    return 0;
+  }
+  if (getenv("SIZE_SWEEP")) {            // fixed per-launch cost: bytes per launch sweep
+    for (size_t mb : {4096, 1024, 300, 150, 66, 33}) {
+      const size_t u = mb * 1024;
+      printf("cp.async W=16 D=4 %5zu MB/launch %7.0f GB/s\n", mb, run(k_cpasync<4>, ctas, 16, 16 * 4 * 1024, buf, u, out));
+      printf("mma Q4   W=12 D=4 %5zu MB/launch %7.0f GB/s\n", mb, run(k_mma<4, 2>, ctas, 12, 12 * 4 * 2048, buf, u, out));
+    }
+    return 0;
+  }
+  if (getenv("MMA_ONLY")) {
+    for (int w : {8, 12, 16}) {
+      printf("mma F16 chain   W=%2d D=4 %7.0f GB/s\n", w, run(k_mma<4, 0>, ctas, w, w * 4 * 2048, buf, units, out));
+      printf("mma F16 chain   W=%2d D=6 %7.0f GB/s\n", w, run(k_mma<6, 0>, ctas, w, w * 6 * 2048, buf, units, out));
+      printf("mma F16 fresh   W=%2d D=4 %7.0f GB/s\n", w, run(k_mma<4, 1>, ctas, w, w * 4 * 2048, buf, units, out));
+      printf("mma F16 fresh   W=%2d D=6 %7.0f GB/s\n", w, run(k_mma<6, 1>, ctas, w, w * 6 * 2048, buf, units, out));
+      printf("mma Q4          W=%2d D=4 %7.0f GB/s\n", w, run(k_mma<4, 2>, ctas, w, w * 4 * 2048, buf, units, out));
+      printf("mma Q4          W=%2d D=6 %7.0f GB/s\n", w, run(k_mma<6, 2>, ctas, w, w * 6 * 2048, buf, units, out));
+    }
+    return 0;
+  }
   for (int w : {8, 12, 16}) {
     printf("cp.async W=%2d D=4  %7.0f GB/s\n", w, run(k_cpasync<4>, ctas, w, w * 4 * 1024, buf, units, out));
     printf("cp.async W=%2d D=8  %7.0f GB/s\n", w, run(k_cpasync<8>, ctas, w, w * 8 * 1024, buf, units, out));
