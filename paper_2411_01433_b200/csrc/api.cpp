@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -74,20 +75,19 @@ struct hb_ctx {
   long long* lbuf = nullptr;              // [P][B][E][2] router scratch
   uint4* x_perm = nullptr;
   float* xsum = nullptr;
-  uint4* h_hi = nullptr;
+  float* au = nullptr;                    // [slots][2][F] K2a sums
+  uint4* h_hi = nullptr;                  // h in global memory (large batches only)
   uint4* h_lo = nullptr;
   float* hsum = nullptr;
-  float* part = nullptr;                  // stream-K pieces
-  float* ob = nullptr;                    // per-slot W2 outputs
-  unsigned* cnt13 = nullptr;              // piece / job counters (self-resetting)
-  unsigned* cnt2 = nullptr;
-  unsigned* cnty = nullptr;
+  bool force_h_global = false;            // HB_FORCE_H_GLOBAL=1 (tests of that path)
   unsigned* done = nullptr;
   JobTable jt{};
   void* jt_dev = nullptr;
   void* jt_host = nullptr;                // pinned staging
   size_t jt_bytes = 0;
-  int max_jobs = 0, max_slots = 0;
+  int max_jobs = 0, max_slots = 0, max_vjobs = 0;
+  float static_frac = 0.6f;               // GEMV work feed (HB_STATIC_FRAC, HB_CHUNK)
+  int chunk = 8;
   cudaEvent_t dec_ready = nullptr;
   // kernel timing (hb_profile)
   std::vector<cudaEvent_t> prof_ev;       // 3 per recorded forward
@@ -178,8 +178,8 @@ static void free_ctx(hb_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
-                   c->logits, c->lbuf, c->x_perm, c->xsum, c->h_hi, c->h_lo, c->hsum, c->part,
-                   c->ob, c->cnt13, c->cnt2, c->cnty, c->done, c->jt_dev};
+                   c->logits, c->lbuf, c->x_perm, c->xsum, c->au, c->h_hi, c->h_lo,
+                   c->hsum, c->done, c->jt_dev};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
@@ -238,7 +238,11 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   const int P = std::max(1, k.lookahead_p);
   c->max_slots = B * K;
   c->max_jobs = std::min(2 * E, B * K) + 1;
-  const int max_vjobs = c->max_jobs + (c->max_slots + kVSlots - 1) / kVSlots + 1;
+  c->max_vjobs = c->max_jobs + (c->max_slots + kVSlots - 1) / kVSlots;
+  if (c->max_vjobs + 1 > kMaxVJobs)
+    return bail(HB_EUNSUPPORTED, "max_batch * top_k too large for one forward's job table");
+  if ((long long)c->max_vjobs * (F / 16) * (H / 32) >= (1LL << 31))
+    return bail(HB_EUNSUPPORTED, "GEMV unit space of one forward exceeds 2^31 units");
   auto dm = [&](void** p, size_t n) { return cudaMalloc(p, std::max<size_t>(n, 16)) == cudaSuccess; };
   bool ok = dm((void**)&c->wg, (size_t)L * E * H * 2) &&
             dm((void**)&c->dec, sizeof(hb_decision) * B * K) &&
@@ -246,25 +250,30 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
             dm((void**)&c->logits, sizeof(long long) * B * E * 2) &&
             dm((void**)&c->lbuf, sizeof(long long) * P * B * E * 2) &&
             dm((void**)&c->x_perm, (size_t)B * H * 2) && dm((void**)&c->xsum, (size_t)B * (H / 32) * 4) &&
+            dm((void**)&c->au, (size_t)c->max_slots * 2 * F * 4) &&
             dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->hsum, (size_t)c->max_slots * (F / 32) * 4) &&
-            dm((void**)&c->part, sizeof(float) * kGemvTotalWarps * 2 * 32 * kPartFloats) &&
-            dm((void**)&c->ob, (size_t)c->max_slots * H * 4) &&
-            dm((void**)&c->cnt13, sizeof(unsigned) * max_vjobs * (F / 16)) &&
-            dm((void**)&c->cnt2, sizeof(unsigned) * max_vjobs * (H / 16)) &&
-            dm((void**)&c->cnty, sizeof(unsigned) * (H / 16)) && dm((void**)&c->done, 16);
+            dm((void**)&c->done, 16);
   if (!ok) return bail(HB_ENOMEM, "device allocation of scratch failed");
-  cudaMemset(c->cnt13, 0, sizeof(unsigned) * max_vjobs * (F / 16));
-  cudaMemset(c->cnt2, 0, sizeof(unsigned) * max_vjobs * (H / 16));
-  cudaMemset(c->cnty, 0, sizeof(unsigned) * (H / 16));
+  {
+    const char* fh = std::getenv("HB_FORCE_H_GLOBAL");
+    c->force_h_global = fh && fh[0] == '1';
+    const char* sf = std::getenv("HB_STATIC_FRAC");
+    if (sf) c->static_frac = std::min(1.0f, std::max(0.0f, (float)std::atof(sf)));
+    const char* ch = std::getenv("HB_CHUNK");
+    if (ch) c->chunk = std::max(1, std::atoi(ch));
+  }
   cudaMemset(c->done, 0, 16);
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
   // job table: hdr | jobs | slot_token | slot_gate | tok_slots
   const size_t o_jobs = 64, o_tok = align_up(o_jobs + sizeof(Job) * c->max_jobs, 64),
                o_gate = align_up(o_tok + 4 * (size_t)c->max_slots, 64),
                o_ts = align_up(o_gate + 4 * (size_t)c->max_slots, 64),
-               total = align_up(o_ts + 4 * (size_t)c->max_slots, 64);
+               o_vj = align_up(o_ts + 4 * (size_t)c->max_slots, 64),
+               o_c13 = align_up(o_vj + sizeof(VJobD) * (c->max_vjobs + 1), 64),
+               o_c2 = align_up(o_c13 + 8 * (size_t)(c->max_vjobs + 1), 64),
+               total = align_up(o_c2 + 8 * (size_t)(c->max_vjobs + 1), 64);
   c->jt_bytes = total;
   if (!dm(&c->jt_dev, total) || cudaHostAlloc(&c->jt_host, total, cudaHostAllocDefault) != cudaSuccess)
     return bail(HB_ENOMEM, "job table allocation failed");
@@ -275,6 +284,9 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   c->jt.slot_token = (int32_t*)(jb + o_tok);
   c->jt.slot_gate = (float*)(jb + o_gate);
   c->jt.tok_slots = (int32_t*)(jb + o_ts);
+  c->jt.vjobs = (VJobD*)(jb + o_vj);
+  c->jt.vcum13 = (long long*)(jb + o_c13);
+  c->jt.vcum2 = (long long*)(jb + o_c2);
   if (cudaHostAlloc((void**)&c->dec_host, sizeof(hb_decision) * (1 + P) * B * K,
                     cudaHostAllocDefault) != cudaSuccess)
     return bail(HB_ENOMEM, "pinned decision buffer allocation failed");
@@ -386,6 +398,7 @@ static RouterParams router_params(hb_ctx* c, const void* x, int batch) {
   p.B = batch;
   p.E = k.n_experts;
   p.H = k.hidden;
+  p.F = k.ffn;
   p.k = k.top_k;
   p.theta1 = hb_theta(k.t1, &p.th1_kind);
   p.theta2 = hb_theta(k.t2, &p.th2_kind);
@@ -412,15 +425,19 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
   g.k = k.top_k;
   g.x_perm = c->x_perm;
   g.xsum = c->xsum;
+  g.au = c->au;
   g.h_hi = c->h_hi;
   g.h_lo = c->h_lo;
   g.hsum = c->hsum;
-  g.part = c->part;
-  g.ob = c->ob;
-  g.cnt13 = c->cnt13;
-  g.cnt2 = c->cnt2;
-  g.cnty = c->cnty;
+  // K2b builds h in each CTA's shared memory when every possible slot fits
+  const size_t slot_bytes = (size_t)k.ffn * 2 * 2 + (size_t)(k.ffn / 32) * 4;
+  g.h_global = c->force_h_global ||
+               (size_t)batch * k.top_k * slot_bytes > (size_t)w2_stage_capacity();
   g.y = (float*)y;
+  g.ctr = c->done + 1;
+  g.max_vjobs = c->max_vjobs;
+  g.static_frac = c->static_frac;
+  g.chunk = c->chunk;
   return g;
 }
 
@@ -430,6 +447,10 @@ static void launch_gemv(hb_ctx* c, const GemvParams& gp, cudaStream_t s) {
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
   if (ev) cudaEventRecord(ev[0], s);
   launch_w13(gp, s);
+  if (gp.h_global) {
+    launch_hfin(gp, c->last_batch * c->cfg.top_k, s);
+    c->launches += 1;
+  }
   if (ev) cudaEventRecord(ev[1], s);
   launch_w2(gp, s);
   if (ev) cudaEventRecord(ev[2], s);
@@ -482,8 +503,10 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   rp.logits = c->logits;
   rp.x_perm = c->x_perm;
   rp.xsum = c->xsum;
-  rp.zero_buf = c->hsum;
-  rp.zero_n = (long long)batch * k.top_k * (k.ffn / 32);
+  rp.zero_buf[0] = c->au;
+  rp.zero_n[0] = (long long)batch * k.top_k * 2 * k.ffn;
+  rp.zero_buf[1] = (float*)y;
+  rp.zero_n[1] = (long long)batch * k.hidden;
 
   c->last_batch = batch;
   c->last_layer = layer;
@@ -551,6 +574,10 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   }
   hdr[0] = nj;
   hdr[1] = nj;
+  hdr[2] = build_vjobs(jobs, nj, k.hidden, k.ffn,
+                       (VJobD*)(jh + ((uint8_t*)c->jt.vjobs - (uint8_t*)c->jt_dev)),
+                       (long long*)(jh + ((uint8_t*)c->jt.vcum13 - (uint8_t*)c->jt_dev)),
+                       (long long*)(jh + ((uint8_t*)c->jt.vcum2 - (uint8_t*)c->jt_dev)));
   CUDA_TRY(c, cudaMemcpyAsync(c->jt_dev, c->jt_host, c->jt_bytes, cudaMemcpyHostToDevice, s));
   for (int i = 0; i < K; ++i)
     if (served[i] != HB_ENC_NONE)

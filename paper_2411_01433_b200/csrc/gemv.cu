@@ -1,14 +1,14 @@
 // K2a / K2b: grouped mixed-precision dequant-GEMV of the selected experts.
 //
-//   K2a  h = silu(W1 x) * (W3 x)          per job (expert, served encoding)
-//   K2b  y = sum_jobs gate * (W2 h)        Eq. 1, Skip = no job
+//   K2a  a = W1 x, u = W3 x               per job (expert, served encoding)
+//   K2b  h = silu(a) * u;  y = sum_jobs gate * (W2 h)     Eq. 1
 //
 // Paper: the layer output is the gate-weighted sum of the selected experts
 // (Eq. 1); a Low expert is computed from its low-precision version;
 // experts are SwiGLU FFNs (reading R10).  This is the B200 hot path: batch-1
 // decode streams 66-352 MB of expert weights per token-layer, so the kernels
-// are HBM-bound; their job is to keep ~100 KB of loads in flight per SM on
-// every SM for the whole kernel while spending few instructions per weight.
+// are HBM-bound; their job is to keep ~100-200 KB of loads in flight per SM
+// on every SM for the whole kernel while spending few instructions per weight.
 //
 // Structure:
 //  * warp-level STREAM-K.  The work of a launch is a sequence of UNITS, one
@@ -17,13 +17,19 @@
 //    the same number of weight bytes whatever the encoding, so giving each of
 //    the 148 x 16 warps an equal contiguous range of units balances HBM
 //    traffic to within one unit.  A warp streams its range as ONE pipeline
-//    (no drain at tile boundaries); a tile split between warps leaves
-//    "pieces" that the last-arriving warp adds up in warp order
-//    (deterministic), then applies the epilogue;
-//  * each warp owns a multi-stage shared-memory ring filled with cp.async:
-//    its 16 bytes of the two rows g, g+8 of each unit (L1 bypassed, L2
-//    evict-first), the block scales, and the B fragments (x or h, at most two
-//    token slots at batch 1);
+//    (no drain at tile boundaries); at the end of each tile piece it adds its
+//    partial sums into the output with fire-and-forget fp32 reductions
+//    (red.global.add): K2a into a/u [slot][2][F], K2b (times the gate) into y.
+//    No counters, fences or combine passes; the summation order of the <= 3
+//    pieces of a row varies from run to run (reading R24);
+//  * each warp owns a multi-stage shared-memory ring filled with cp.async
+//    (L1 bypassed, L2 evict-first): per unit the 1 KB of codes of each matrix
+//    and the 16 rows' block scales;
+//  * the B operand (x for K2a; h = silu(a) * u as an fp16 hi/lo pair for
+//    K2b, plus block sums for Q2) lives in ONE CTA-wide shared-memory stage,
+//    built by all warps of the CTA right after they issued their first ring
+//    loads (so the build overlaps the first HBM round trip) and published
+//    through an mbarrier;
 //  * the dot products run on the tensor cores as mma.sync.m16n8k16 with the
 //    weights as A (16 rows x 16 k) and up to 8 token slots as B: dequantised
 //    codes are EXACT in fp16 (q-8, q, int8 q), so every per-block partial sum
@@ -158,17 +164,17 @@ __host__ __device__ constexpr int epg_of(int enc) {
 
 // Shared memory of a GEMV CTA: kGemvWarps private cp.async rings (weights +
 // scales) followed by ONE CTA-wide stage of the B operand (x for K2a, h hi/lo
-// for K2b, and their block sums), loaded once per CTA.  Reading B from a
-// CTA copy instead of per unit from L2 avoids hammering the same few L2 lines
-// from every warp of the GPU (measured: it capped the kernels at ~4.5 TB/s).
+// for K2b, and their block sums), built once per CTA, so the hot loop reads
+// its B fragments with one shared-memory load per block instead of an L2
+// round trip (K2b also computes h = silu(a) * u only here, not per unit).
 template <bool W13> struct KCfg;
 template <> struct KCfg<true> {        // K2a: x is small (8 KB per token at H=4096)
-  static constexpr int RING = 12 * 1024;
-  static constexpr int XSTAGE = 32 * 1024;
+  static constexpr int RING = 16 * 12 * 1024 / kGemvWarps / 128 * 128;
+  static constexpr int XSTAGE = 28 * 1024;  // 3 tokens at H = 4096
 };
 template <> struct KCfg<false> {       // K2b: h of two slots is 118 KB at F=14336
-  static constexpr int RING = 6656;
-  static constexpr int XSTAGE = 120 * 1024;
+  static constexpr int RING = 16 * 6656 / kGemvWarps / 128 * 128;
+  static constexpr int XSTAGE = 116 * 1024; // 2 slots at F = 14336 (118272 B)
 };
 template <bool W13>
 constexpr int gemv_smem_bytes() { return kGemvWarps * KCfg<W13>::RING + KCfg<W13>::XSTAGE; }
@@ -219,7 +225,114 @@ __device__ __forceinline__ void dequant(const uint4& v, int blk, uint32_t (&P)[4
   }
 }
 
-// ---------------------------------------------------------- work space
+// ------------------------------------------------------------ B operand of K2b
+// h of slot s, block j (32 consecutive rows of F) from the K2a sums:
+// h = silu(a) * u (reading R10), split into fp16 hi + lo (hi = rn(h),
+// lo = rn(h - hi)) and pair-permuted; returns the fp32 block sum (Q2 term).
+__device__ __forceinline__ float h_block(const float* au, int F, int s, int j, uint4 (&hi)[4],
+                                         uint4 (&lo)[4]) {
+  const float4* pa = reinterpret_cast<const float4*>(au + (size_t)s * 2 * F + (size_t)j * 32);
+  const float4* pu = reinterpret_cast<const float4*>(au + (size_t)s * 2 * F + F + (size_t)j * 32);
+  float h[32];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 va = __ldcg(pa + q), vu = __ldcg(pu + q);
+    h[4 * q + 0] = va.x; h[4 * q + 1] = va.y; h[4 * q + 2] = va.z; h[4 * q + 3] = va.w;
+    const float uu[4] = {vu.x, vu.y, vu.z, vu.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float a = h[4 * q + i];
+      h[4 * q + i] = a / (1.f + expf(-a)) * uu[i];
+    }
+  }
+  float hs = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) hs += h[i];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    uint32_t wh[4], wl[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float e0 = h[8 * t + c], e1 = h[8 * t + c + 4];
+      const __half h0 = __float2half_rn(e0), h1 = __float2half_rn(e1);
+      const __half l0 = __float2half_rn(e0 - __half2float(h0));
+      const __half l1 = __float2half_rn(e1 - __half2float(h1));
+      wh[c] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+      wl[c] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+    }
+    hi[t] = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+    lo[t] = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+  }
+  return hs;
+}
+
+// ------------------------------------------------------------ CTA stage
+// Shared-memory layout of the B operand (nrows = tokens for K2a, slots for K2b):
+//   part 0 (x / h hi) [nrows][K/8] uint4 | part 1 (h lo, K2b) | sums [nrows][K/32] f32
+// Warp `w` of the CTA builds its share (items w, w + kGemvWarps, ...).
+template <bool W13>
+__device__ void stage_share(const GemvParams& p, int w, uint8_t* st, int nrows) {
+  const int lane = threadIdx.x & 31;
+  if constexpr (W13) {
+    const int K = p.H;
+    const int n16 = nrows * (K / 8);
+    uint4* dst = reinterpret_cast<uint4*>(st);
+    for (int i = w * 32 + lane; i < n16; i += kGemvWarps * 32) dst[i] = __ldcg(p.x_perm + i);
+    const int nz = nrows * (K / 32);
+    float* zd = reinterpret_cast<float*>(st + (size_t)n16 * 16);
+    for (int i = w * 32 + lane; i < nz; i += kGemvWarps * 32) zd[i] = __ldcg(p.xsum + i);
+  } else {
+    const int K = p.F, nb = K / 32;
+    uint4* dhi = reinterpret_cast<uint4*>(st);
+    uint4* dlo = dhi + (size_t)nrows * (K / 8);
+    float* zd = reinterpret_cast<float*>(dlo + (size_t)nrows * (K / 8));
+    for (int i = w * 32 + lane; i < nrows * nb; i += kGemvWarps * 32) {
+      const int s = i / nb, j = i - s * nb;
+      uint4 hi[4], lo[4];
+      const float hs = h_block(p.au, K, s, j, hi, lo);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        dhi[(size_t)s * (K / 8) + j * 4 + t] = hi[t];
+        dlo[(size_t)s * (K / 8) + j * 4 + t] = lo[t];
+      }
+      zd[i] = hs;
+    }
+  }
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+
+// Stage hand-off of one launch: every thread of the CTA arrives once (after its
+// share of the build); readers wait for phase 0.
+struct Stage {
+  uint8_t* ptr;      // generic pointer of the stage
+  uint32_t xst;      // its shared address
+  uint32_t bar;      // mbarrier (count = blockDim.x)
+  int nrows;
+  bool on;           // B operand read from the stage (else from global memory)
+};
+
+template <bool W13>
+__device__ __forceinline__ void stage_build_and_wait(const GemvParams& p, const Stage& S) {
+  stage_share<W13>(p, threadIdx.x >> 5, S.ptr, S.nrows);
+  mbar_arrive(S.bar);
+  mbar_wait(S.bar, 0);
+}
+
+// ---------------------------------------------------------- work feed
 // Virtual job: one job's token slots [slot0, slot0 + nslot), nslot <= kVSlots.
 struct VJob {
   const uint8_t* blob;
@@ -228,132 +341,66 @@ struct VJob {
   int nslot;
 };
 
-__device__ __forceinline__ int n_vjobs(const GemvParams& p) {
-  const int nj = p.jt.hdr[0];
-  int nv = 0;
-  for (int j = 0; j < nj; ++j) nv += (p.jt.jobs[j].n_tok + kVSlots - 1) / kVSlots;
-  return nv;
-}
-__device__ __forceinline__ VJob get_vjob(const GemvParams& p, int v) {
-  const int nj = p.jt.hdr[0];
-  for (int j = 0; j < nj; ++j) {
-    const Job& J = p.jt.jobs[j];
-    const int np = (J.n_tok + kVSlots - 1) / kVSlots;
-    if (v < np) {
-      VJob r;
-      r.blob = J.blob;
-      r.enc = J.enc;
-      r.slot0 = J.slot_off + v * kVSlots;
-      r.nslot = min(kVSlots, J.n_tok - v * kVSlots);
-      return r;
-    }
-    v -= np;
-  }
-  return VJob{nullptr, 0, 0, 0};
-}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
-// Warp ranges: warp w owns units [b(w), b(w+1)), b(w) = floor(w*U/NW).
-struct Space {
-  long long U;
-  int NW;
-  __device__ __forceinline__ long long b(int w) const { return (long long)w * U / NW; }
-  __device__ __forceinline__ int owner(long long u) const {
-    int w = (int)((u * NW) / U);
-    while (w + 1 < NW && b(w + 1) <= u) ++w;
-    while (w > 0 && b(w) > u) --w;
-    return w;
+// The units of a launch (ordered vjob, tile, group; vjob v owns
+// [cum[v], cum[v+1])) are dealt in two phases: the first S = static_frac * U
+// units as equal contiguous warp ranges (dealt SM-interleaved), the rest as
+// chunks of `chunk` units from a global counter.  SMs do not all get the same
+// share of HBM bandwidth (measured: per-SM stream times differ by up to 30%,
+// in GPC-sized groups), so warps on slow SMs simply take fewer chunks.  The
+// next chunk index is fetched one chunk ahead, so the atomic's latency is
+// hidden behind the current chunk's loads.
+struct FeedConst {         // per launch, in shared memory (CTA-wide constants)
+  int S, U;                // static units, all units (< 2^31: checked by the host)
+  int nch;                 // dynamic chunks
+  int chunk;
+  int nwarps;              // warps taking part (each fetches until it sees >= nch)
+  unsigned* ctr;
+};
+struct Feed {
+  int a, b;                // pending segment [a, b) (global units); empty when a >= b
+  unsigned pre;            // lane 0: the prefetched chunk index
+  bool done;
+  const FeedConst* k;
+  __device__ __forceinline__ void prefetch() {
+    if ((threadIdx.x & 31) == 0) pre = atomicAdd(k->ctr, 1u);
+  }
+  // next chunk into [a, b); false when the launch's work is exhausted
+  __device__ __forceinline__ bool refill() {
+    if (done) return false;
+    const int c = (int)__shfl_sync(0xffffffffu, pre, 0);
+    if (c >= k->nch) {
+      // every warp receives exactly one index >= nch; the warp that receives
+      // the last one hands the counter back zeroed for the next launch
+      if ((threadIdx.x & 31) == 0 && c == k->nch + k->nwarps - 1) *k->ctr = 0u;
+      done = true;
+      return false;
+    }
+    a = k->S + c * k->chunk;
+    b = min(a + k->chunk, k->U);
+    prefetch();
+    return true;
   }
 };
-
-// ------------------------------------------------------------ epilogues
-// position of element f of a row in the pair-permuted layout (in halves)
-__device__ __forceinline__ int perm_pos(int f) {
-  const int r8 = f & 31, t = r8 >> 3, r = r8 & 7;
-  return (f & ~31) + 8 * t + 2 * (r & 3) + (r >> 2);
-}
-
-// K2a: h = silu(a) * u for rows row0+g(+8), slots 2t, 2t+1 of the vjob
-__device__ void finalize13(const GemvParams& p, const VJob& vj, int row0, const float (&acc)[2][4]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  float hs[2] = {0.f, 0.f};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int sl = 2 * t + (i & 1);
-    const int f = row0 + g + 8 * (i >> 1);
-    const float a = acc[0][i], u = acc[1][i];
-    const float h = a / (1.f + expf(-a)) * u;
-    if (sl < vj.nslot) {
-      const int slot = vj.slot0 + sl;
-      const __half hh = __float2half_rn(h);
-      const __half hl = __float2half_rn(h - __half2float(hh));
-      reinterpret_cast<__half*>(p.h_hi)[(size_t)slot * p.F + perm_pos(f)] = hh;
-      reinterpret_cast<__half*>(p.h_lo)[(size_t)slot * p.F + perm_pos(f)] = hl;
-      hs[i & 1] += h;
-    }
-  }
-#pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {          // 16 rows of the tile, per slot
-    hs[0] += __shfl_xor_sync(0xffffffffu, hs[0], o);
-    hs[1] += __shfl_xor_sync(0xffffffffu, hs[1], o);
-  }
-  if (g == 0) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-      if (2 * t + c < vj.nslot)     // two tiles per 32-row block: fl(fl(0+a)+b) is order-free
-        atomicAdd(p.hsum + (size_t)(vj.slot0 + 2 * t + c) * (p.F / 32) + row0 / 32, hs[c]);
-  }
-}
-
-// K2b: o -> ob[slot][rows] of a finished (job, H tile)
-__device__ void store_ob(const GemvParams& p, const VJob& vj, int tile, const float (&acc)[1][4]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int row0 = tile * 16;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int sl = 2 * t + (i & 1);
-    if (sl < vj.nslot)
-      p.ob[(size_t)(vj.slot0 + sl) * p.H + row0 + g + 8 * (i >> 1)] = acc[0][i];
-  }
-}
-
-// after a fence: count this job as done for H tile `tile`; the last job of the
-// tile writes y = Eq. 1 in fixed (token, rank) order
-__device__ void publish_y(const GemvParams& p, int tile, int nv) {
-  const int lane = threadIdx.x & 31;
-  const int row0 = tile * 16;
-  unsigned prev = 0;
-  if (lane == 0) prev = atomicAdd(p.cnty + tile, 1u);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != (unsigned)(nv - 1)) return;
-  __threadfence();
-  for (int e = lane; e < 16 * p.B; e += 32) {            // Eq. 1, ranks in order
-    const int tok = e >> 4, r = row0 + (e & 15);
-    float v = 0.f;
-    for (int i = 0; i < p.k; ++i) {
-      const int s = p.jt.tok_slots[tok * p.k + i];
-      if (s >= 0) v = fmaf(p.jt.slot_gate[s], __ldcg(p.ob + (size_t)s * p.H + r), v);
-    }
-    p.y[(size_t)tok * p.H + r] = v;
-  }
-  if (lane == 0) p.cnty[tile] = 0u;
-}
-
-struct Pend {
-  int tile;
-  int kind;          // 0 partial piece stored in part[], 1 finished W2 tile (ob stored)
-};
-constexpr int kMaxPend = 4;
 
 // ------------------------------------------------------------ the run
-// Stream units [a, b) of virtual job v (unit l = tile * G + grp) through the
-// warp's ring.  W13: K2a (W1 and W3 rows, x); else K2b (W2 rows, h hi/lo).
-// XR: the B operand of every slot is in the CTA stage at shared address xst
-// (W13: x_perm [B][H/8] uint4 | xsum [B][H/32]; W2: h_hi [S][F/8] | h_lo
-// [S][F/8] | hsum [S][F/32]); otherwise it is read from global memory.
+// Stream the feed's segments that lie in virtual job vj (units [cum, cum+Uv),
+// unit l = tile * G + grp of the vjob) through the warp's ring as one
+// pipeline.  W13: K2a (W1 and W3 rows, x); else K2b (W2 rows, h hi/lo).  The
+// producer runs DEPTH-1 units ahead and records each unit's (tile, group,
+// end-of-piece) in `meta` next to its ring slot.  `first`: the warp's first
+// run of the launch, which builds its share of the CTA stage between issuing
+// the ring prologue and consuming the first unit.
+#ifdef HB_RUN_NOINLINE
+#define HB_RUN_ATTR __noinline__
+#else
+#define HB_RUN_ATTR
+#endif
 template <int ENC, bool W13, bool XR>
-__device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long long cum,
-                    long long a, long long b, const Space& sp, int gw, uint32_t ring,
-                    uint32_t xst, int nrows_x) {
+__device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, int Uv, Feed& fd,
+                    uint32_t ring, uint2* meta, const Stage& S, bool first) {
   constexpr int NMAT = W13 ? 2 : 1;
   constexpr bool SPLIT = !W13;
   constexpr int XS = SPLIT ? 2 : 1;
@@ -362,42 +409,37 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int K = W13 ? p.H : p.F;
   const int G = K / Enc<ENC>::EPG;
-  const int nb = K / 32;
-  const size_t rowbytes = ENC == HB_F16 ? (size_t)K * 2 : ENC == HB_Q8 ? (size_t)K
-                        : ENC == HB_Q4 ? (size_t)K / 2 : (size_t)K / 4;
   const uint64_t pol = evict_first_policy();
-  // matrices
   // tile-major blobs: unit l (tile l/G, group l%G) = 1 KB of codes at q + 1024*l,
-  // its 16 scale records at s + 16*SB*l -- a warp's range is one contiguous span
-  const uint8_t* qp[NMAT];
-  const uint8_t* sp_[NMAT];
-#pragma unroll
-  for (int m = 0; m < NMAT; ++m) {
-    const MatLayout& L = p.lay[ENC].mat[W13 ? m : 2];
-    qp[m] = vj.blob + L.q + (size_t)a * 1024 + 16 * lane;
-    sp_[m] = vj.blob + L.s + (size_t)a * 16 * SB + 16 * lane;
-  }
-  (void)rowbytes;
-  (void)nb;
+  // its 16 scale records at s + 16*SB*l -- a segment is one contiguous span
   const bool s_act = lane < SB;               // 16*SB bytes of scales per unit = SB lanes x 16 B
   const int ns = vj.nslot;
-  // B-operand source of slot s (x or h hi/lo) and of its block sums
-  auto xsrc_of = [&](int part, int s) -> const uint4* {
-    const int sl = vj.slot0 + min(s, ns - 1);
-    if constexpr (W13) return p.x_perm + (size_t)p.jt.slot_token[sl] * (p.H / 8);
-    else return (part ? p.h_lo : p.h_hi) + (size_t)sl * (p.F / 8);
-  };
-  auto zsrc_of = [&](int s) -> const float* {
-    const int sl = vj.slot0 + min(s, ns - 1);
-    if constexpr (W13) return p.xsum + (size_t)p.jt.slot_token[sl] * (p.H / 32);
-    else return p.hsum + (size_t)sl * (p.F / 32);
-  };
 
-  // ---- producer: weights + scales only (B operand is in the CTA stage)
-  long long pl = a;
-  int pslot = 0;
+  // ---- producer: weights + scales
+  int pl = 0, pe = 0;                          // vjob-local next unit / end of its segment
+  int ptile = 0, pgrp = 0, pslot = 0, iss = 0;
+  bool pactive = true;
+  const uint8_t* qp[NMAT];
+  const uint8_t* sp_[NMAT];
+  auto take = [&]() -> bool {                  // the feed's next segment, if it is in this vjob
+    if (fd.a >= fd.b && !fd.refill()) return false;
+    if (fd.a >= cum + Uv) return false;
+    pl = fd.a - cum;
+    pe = min(fd.b, cum + Uv) - cum;
+    fd.a = cum + pe;                           // a remainder past the vjob stays in the feed
+    ptile = pl / G;
+    pgrp = pl - ptile * G;
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+      const MatLayout& L = p.lay[ENC].mat[W13 ? m : 2];
+      qp[m] = vj.blob + L.q + (size_t)pl * 1024 + 16 * lane;
+      sp_[m] = vj.blob + L.s + (size_t)pl * 16 * SB + 16 * lane;
+    }
+    return true;
+  };
   auto issue = [&]() {
-    if (pl < b) {
+    if (pactive && pl == pe) pactive = take();
+    if (pactive) {
       const uint32_t st = ring + pslot * R::STAGE;
 #pragma unroll
       for (int m = 0; m < NMAT; ++m) {                 // 2 x 512 contiguous bytes
@@ -406,97 +448,90 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
         if constexpr (SB > 0)
           if (s_act) cp_async16_ef(st + R::W + m * 16 * SB + 16 * lane, sp_[m], pol);
       }
+      const bool flush = pgrp == G - 1 || pl + 1 == pe;   // last unit of a tile piece
+      if (lane == 0) meta[pslot] = make_uint2((uint32_t)ptile, (uint32_t)pgrp | (flush ? 0x80000000u : 0u));
       ++pl;
 #pragma unroll
       for (int m = 0; m < NMAT; ++m) { qp[m] += 1024; sp_[m] += 16 * SB; }
+      if (++pgrp == G) { pgrp = 0; ++ptile; }
       if (++pslot == DEPTH) pslot = 0;
+      ++iss;
     }
     cp_commit();
   };
 
+  // K2a: x is tiny and already in L2 -- stage it before the weight loads are
+  // queued (behind ~24 MB of ring prologues it would wait microseconds).
+  // K2b: the ring prologue (W2 is independent of K2a) goes out first, during
+  // K2a's tail; then wait for K2a and build h.
+  if (W13 && first && S.on) stage_build_and_wait<W13>(p, S);
 #pragma unroll 1
   for (int s = 0; s < DEPTH - 1; ++s) issue();
+  if (!W13 && first) {
+    pdl_wait();                                // h comes from K2a
+    if (S.on) stage_build_and_wait<W13>(p, S);
+  }
+  if (first) HB_TL(W13, (threadIdx.x >> 5) * gridDim.x + blockIdx.x, 2);
+
+  // ---- lane constants: B-operand rows, outputs of the lane's two slots
+  const int xg = min(g, ns - 1);
+  const int z0 = min(2 * t, ns - 1), z1 = min(2 * t + 1, ns - 1);
+  auto row_of = [&](int s) -> int {          // stage row: token (x) or slot (h)
+    const int sl = vj.slot0 + s;
+    return W13 ? p.jt.slot_token[sl] : sl;
+  };
+  const uint4* gx0 = nullptr;
+  const uint4* gx1 = nullptr;
+  const float* gz0 = nullptr;
+  const float* gz1 = nullptr;
+  if constexpr (!XR) {
+    if constexpr (W13) {
+      gx0 = gx1 = p.x_perm + (size_t)row_of(xg) * (K / 8);
+      gz0 = p.xsum + (size_t)row_of(z0) * (K / 32);
+      gz1 = p.xsum + (size_t)row_of(z1) * (K / 32);
+    } else {
+      gx0 = p.h_hi + (size_t)row_of(xg) * (K / 8);
+      gx1 = p.h_lo + (size_t)row_of(xg) * (K / 8);
+      gz0 = p.hsum + (size_t)row_of(z0) * (K / 32);
+      gz1 = p.hsum + (size_t)row_of(z1) * (K / 32);
+    }
+  }
+  const uint32_t sxb = S.xst + (uint32_t)row_of(xg) * K * 2 + t * 16;
+  const uint32_t sxl = sxb + (uint32_t)S.nrows * K * 2;
+  const uint32_t szb = S.xst + (uint32_t)XS * S.nrows * K * 2;
+  const uint32_t sz0 = szb + (uint32_t)row_of(z0) * (K / 32) * 4;
+  const uint32_t sz1 = szb + (uint32_t)row_of(z1) * (K / 32) * 4;
+  // output targets of the lane's slots 2t, 2t+1 (K2a: a/u rows; K2b: y rows, gate)
+  const bool v0 = 2 * t < ns, v1 = 2 * t + 1 < ns;
+  float* out0;
+  float* out1;
+  float gate0 = 0.f, gate1 = 0.f;
+  if constexpr (W13) {
+    out0 = p.au + (size_t)(vj.slot0 + z0) * 2 * p.F;
+    out1 = p.au + (size_t)(vj.slot0 + z1) * 2 * p.F;
+  } else {
+    out0 = p.y + (size_t)p.jt.slot_token[vj.slot0 + z0] * p.H;
+    out1 = p.y + (size_t)p.jt.slot_token[vj.slot0 + z1] * p.H;
+    gate0 = p.jt.slot_gate[vj.slot0 + z0];
+    gate1 = p.jt.slot_gate[vj.slot0 + z1];
+  }
 
   float acc[NMAT][4];
 #pragma unroll
   for (int m = 0; m < NMAT; ++m)
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
-  int c_tile = (int)(a / G), c_grp = (int)(a % G), piece0 = c_grp;
   int cslot = 0;
-  const int xg = min(g, ns - 1), z0 = min(2 * t, ns - 1), z1 = min(2 * t + 1, ns - 1);
-  // deferred publications: partial pieces (kind 0) and finished W2 tiles (kind 1)
-  Pend pend[kMaxPend];
-  int npend = 0;
-  auto publish = [&](const Pend* pd, int n) {
-    if (n == 0) return;
-    __syncwarp();
-    __threadfence();
-    int ytile[kMaxPend];
-    int ny = 0;
-    for (int i = 0; i < n; ++i) {
-      const int tile = pd[i].tile;
-      if (pd[i].kind == 1) { ytile[ny++] = tile; continue; }
-      const long long gu0 = cum + (long long)tile * G, gu1 = gu0 + G;
-      const int wa = sp.owner(gu0), wb = sp.owner(gu1 - 1);
-      unsigned* cnt = (W13 ? p.cnt13 + (size_t)v * (p.F / 16) : p.cnt2 + (size_t)v * (p.H / 16)) + tile;
-      unsigned prev = 0;
-      if (lane == 0) prev = atomicAdd(cnt, 1u);
-      prev = __shfl_sync(0xffffffffu, prev, 0);
-      if (prev != (unsigned)(wb - wa)) continue;
-      // last piece of the tile: add all pieces in warp order (deterministic)
-      __threadfence();
-      float sum[NMAT][4];
-#pragma unroll
-      for (int m = 0; m < NMAT; ++m)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sum[m][q] = 0.f;
-      for (int w2 = wa; w2 <= wb; ++w2) {
-        const int ks = sp.b(w2) >= gu0 ? 0 : 1;
-        const float* src = p.part + (((size_t)w2 * 2 + ks) * 32 + lane) * kPartFloats;
-#pragma unroll
-        for (int m = 0; m < NMAT; ++m) {
-          const float4 q = __ldcg(reinterpret_cast<const float4*>(src + 4 * m));
-          sum[m][0] += q.x; sum[m][1] += q.y; sum[m][2] += q.z; sum[m][3] += q.w;
-        }
-      }
-      if (lane == 0) *cnt = 0u;
-      if constexpr (W13) {
-        finalize13(p, vj, tile * 16, sum);
-      } else {
-        store_ob(p, vj, tile, sum);
-        ytile[ny++] = tile;
-      }
-    }
-    if (ny) {
-      __syncwarp();
-      __threadfence();
-      for (int i = 0; i < ny; ++i) publish_y(p, ytile[i], nv);
-    }
-  };
-  // B-operand sources: rows (token for x, slot for h) of the lane's fragment slots
-  auto row_of = [&](int s) -> int {
-    const int sl = vj.slot0 + min(s, ns - 1);
-    return W13 ? p.jt.slot_token[sl] : sl;
-  };
-  const uint4* gx0 = XR ? nullptr : xsrc_of(0, xg);
-  const uint4* gx1 = XR ? nullptr : xsrc_of(XS - 1, xg);
-  const float* gz0 = XR ? nullptr : zsrc_of(z0);
-  const float* gz1 = XR ? nullptr : zsrc_of(z1);
-  // stage addresses (XR): part p of row r at xst + (p*nrows + r)*K*2, sums after
-  const uint32_t sxb = xst + (uint32_t)row_of(xg) * K * 2 + t * 16;
-  const uint32_t sxl = sxb + (uint32_t)nrows_x * K * 2;
-  const uint32_t szb = xst + (uint32_t)XS * nrows_x * K * 2;
-  const uint32_t sz0 = szb + (uint32_t)row_of(z0) * (K / 32) * 4;
-  const uint32_t sz1 = szb + (uint32_t)row_of(z1) * (K / 32) * 4;
 
-  for (long long l = a; l < b; ++l) {
+  for (int con = 0; con < iss; ++con) {            // iss grows while the producer runs
     __syncwarp();                                  // slot being refilled is consumed
     issue();
     cp_wait<DEPTH - 1>();
-    __syncwarp();                                  // everyone's copies of unit l visible
+    __syncwarp();                                  // everyone's copies of unit con visible
+    const uint2 md = meta[cslot];
     const uint32_t st = ring + cslot * R::STAGE;
     if (++cslot == DEPTH) cslot = 0;
+    const int c_tile = (int)md.x, c_grp = (int)(md.y & 0x7FFFFFFFu);
     uint4 w[NMAT][2];
 #pragma unroll
     for (int m = 0; m < NMAT; ++m) {
@@ -563,48 +598,27 @@ __device__ void run(const GemvParams& p, const VJob& vj, int v, int nv, long lon
         }
       }
     }
-    // ---- end of a tile piece?  (anything that needs a fence is deferred to the
-    // end of the run, so the cp.async pipeline never drains mid-stream)
-#ifdef HB_DBG_NOEPI
-    if (false) {
-#else
-    if (c_grp == G - 1 || l == b - 1) {
-#endif
-      if (npend == kMaxPend) {                 // cannot happen at production sizes
-        cp_wait<0>();
-        publish(pend, npend);
-        npend = 0;
-      }
-      if (piece0 == 0 && c_grp == G - 1) {
-        if constexpr (W13) {
-          finalize13(p, vj, c_tile * 16, acc);
-        } else {
-          store_ob(p, vj, c_tile, acc);
-          pend[npend++] = Pend{c_tile, 1};
+    // ---- end of a tile piece: add it into the output (fire-and-forget)
+    if (md.y & 0x80000000u) {
+      const int r0 = c_tile * 16 + g;
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) {
+        const int off = W13 ? m * p.F + r0 : r0;
+        if (v0) {
+          atomicAdd(out0 + off, W13 ? acc[m][0] : gate0 * acc[m][0]);
+          atomicAdd(out0 + off + 8, W13 ? acc[m][2] : gate0 * acc[m][2]);
         }
-      } else {
-        // partial piece: store it; counting / combining happens in publish()
-        const long long gu0 = cum + (long long)c_tile * G;
-        const int pslot_k = sp.b(gw) >= gu0 ? 0 : 1;
-        float* dst = p.part + (((size_t)gw * 2 + pslot_k) * 32 + lane) * kPartFloats;
-#pragma unroll
-        for (int m = 0; m < NMAT; ++m)
-          *reinterpret_cast<float4*>(dst + 4 * m) = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
-        pend[npend++] = Pend{c_tile, 0};
-      }
-#pragma unroll
-      for (int m = 0; m < NMAT; ++m)
+        if (v1) {
+          atomicAdd(out1 + off, W13 ? acc[m][1] : gate1 * acc[m][1]);
+          atomicAdd(out1 + off + 8, W13 ? acc[m][3] : gate1 * acc[m][3]);
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
-      piece0 = 0;
+      }
     }
-    if (++c_grp == G) { c_grp = 0; ++c_tile; }
   }
   cp_wait<0>();
   __syncwarp();
-  HB_TL(W13, gw, 2);
-  publish(pend, npend);
-  HB_TL(W13, gw, 3);
 }
 
 extern __shared__ __align__(128) uint8_t gemv_smem[];
@@ -612,63 +626,68 @@ extern __shared__ __align__(128) uint8_t gemv_smem[];
 template <bool W13>
 __global__ void __launch_bounds__(kGemvWarps * 32, 1)
 gemv_kernel(const __grid_constant__ GemvParams p) {
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ int s_cum[kMaxVJobs + 1];
+  __shared__ uint2 s_meta[kGemvWarps][16];
+  __shared__ FeedConst s_fk;
   const int warp = threadIdx.x >> 5;
-#ifdef HB_DBG_TIMELINE
-  HB_TL(W13, warp * gridDim.x + blockIdx.x, 0);
-#endif
-  const int nv = n_vjobs(p);
-  if (!W13 && nv == 0) {                                     // nothing owned: y = 0
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)p.B * p.H;
-         i += (long long)gridDim.x * blockDim.x)
-      p.y[i] = 0.f;
-    return;
-  }
-  const int T = W13 ? p.F / 16 : p.H / 16;
-  const int K = W13 ? p.H : p.F;
+  const int gw = warp * gridDim.x + blockIdx.x;
+  HB_TL(W13, gw, 0);
+  // K2a needs the router's job table and x; K2b may read the table before
+  // waiting (K2a triggers its dependents only after its own wait, i.e. after
+  // the router completed) and waits for K2a's sums inside its first run
+  if constexpr (W13) pdl_wait();
+  pdl_trigger();
+  const long long* cum = W13 ? p.jt.vcum13 : p.jt.vcum2;
+  for (int i = threadIdx.x; i <= p.max_vjobs; i += blockDim.x) s_cum[i] = (int)__ldcg(cum + i);
+  const int nv = __ldcg(p.jt.hdr + 2);
+  const int nslots = __ldcg(p.jt.hdr + 1);
   constexpr int XS = W13 ? 1 : 2;
+  const int K = W13 ? p.H : p.F;
   // ---- CTA stage of the B operand (all rows: tokens for x, slots for h)
-  const uint32_t xst = smem_u32(gemv_smem) + kGemvWarps * KCfg<W13>::RING;
-  const int nrows = W13 ? p.B : p.jt.hdr[1];
-  const size_t stage_bytes = (size_t)nrows * (XS * K * 2 + (K / 32) * 4);
-  const bool xr = stage_bytes <= (size_t)KCfg<W13>::XSTAGE;
-  if (xr) {
-    uint4* dst = reinterpret_cast<uint4*>(gemv_smem + kGemvWarps * KCfg<W13>::RING);
-    const int n16 = nrows * (K / 8);                          // one part, all rows
-    const uint4* src0 = W13 ? p.x_perm : p.h_hi;
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldcg(src0 + i);
-    if (!W13)
-      for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[n16 + i] = __ldcg(p.h_lo + i);
-    const uint4* zs = reinterpret_cast<const uint4*>(W13 ? p.xsum : p.hsum);
-    const int nz16 = nrows * (K / 32) / 4;
-    for (int i = threadIdx.x; i < nz16; i += blockDim.x) dst[XS * n16 + i] = __ldcg(zs + i);
+  Stage S;
+  S.ptr = gemv_smem + kGemvWarps * KCfg<W13>::RING;
+  S.xst = smem_u32(S.ptr);
+  S.bar = smem_u32(&s_bar);
+  S.nrows = W13 ? p.B : nslots;
+  const size_t stage_bytes = (size_t)S.nrows * (XS * K * 2 + (K / 32) * 4);
+  S.on = W13 ? stage_bytes <= (size_t)KCfg<W13>::XSTAGE : !p.h_global;
+  if (threadIdx.x == 0) mbar_init(S.bar, blockDim.x);
+  __syncthreads();
+  if (nv == 0) return;                       // nothing owned: y stays zero (router)
+  if (threadIdx.x == 0) {
+    const int U = s_cum[nv];
+    s_fk.U = U;
+    s_fk.S = min(U, (int)((double)U * p.static_frac));
+    s_fk.chunk = p.chunk;
+    s_fk.nch = (U - s_fk.S + p.chunk - 1) / p.chunk;
+    s_fk.nwarps = gridDim.x * kGemvWarps;
+    s_fk.ctr = p.ctr + (W13 ? 0 : 1);
   }
   __syncthreads();
-  HB_TL(W13, warp * gridDim.x + blockIdx.x, 1);
-  long long U = 0;
-  for (int v = 0; v < nv; ++v) U += (long long)T * (K / epg_of(get_vjob(p, v).enc));
-  // at most U warps take part, so every participating warp owns >= 1 unit
-  Space sp{U, (int)min((long long)gridDim.x * kGemvWarps, U)};
-  // warp ranges are dealt SM-interleaved: consecutive ranges (same job, same
-  // encoding) land on different SMs, so every SM gets the same mix of
-  // fp16 (HBM-heavy) and low-bit (ALU-heavy) units
-  const int gw = warp * gridDim.x + blockIdx.x;
-  if (gw >= sp.NW) return;
-  const long long u0 = sp.b(gw), u1 = sp.b(gw + 1);
+  Feed fd;
+  fd.k = &s_fk;
+  fd.done = false;
+  // static ranges are dealt SM-interleaved (gw = warp * #CTAs + CTA):
+  // consecutive ranges (same job, same encoding) land on different SMs
+  fd.a = (int)((long long)s_fk.S * gw / s_fk.nwarps);
+  fd.b = (int)((long long)s_fk.S * (gw + 1) / s_fk.nwarps);
+  fd.prefetch();
   const uint32_t ring = smem_u32(gemv_smem) + warp * KCfg<W13>::RING;
-  long long cum = 0;
-  int v = 0;
-  for (; v < nv; ++v) {                                       // vjob containing u0
-    const long long Uv = (long long)T * (K / epg_of(get_vjob(p, v).enc));
-    if (u0 < cum + Uv) break;
-    cum += Uv;
-  }
-  long long u = u0;
-  while (u < u1 && v < nv) {
-    const VJob vj = get_vjob(p, v);
-    const long long Uv = (long long)T * (K / epg_of(vj.enc));
-    const long long a = u - cum, b = min(u1, cum + Uv) - cum;
-#define HB_RUN(E, X) run<E, W13, X>(p, vj, v, nv, cum, a, b, sp, gw, ring, xst, nrows)
-    switch (vj.enc * 2 + (xr ? 1 : 0)) {
+  uint2* meta = s_meta[warp];
+  bool first = true;
+  HB_TL(W13, gw, 1);
+  while (fd.a < fd.b || fd.refill()) {
+    int lo = 0, hi = nv - 1;                   // vjob containing unit fd.a
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_cum[mid] <= fd.a) lo = mid; else hi = mid - 1;
+    }
+    const VJobD d = p.jt.vjobs[lo];
+    const VJob vj{d.blob, d.enc, d.slot0, d.nslot};
+    const int cv = s_cum[lo], Uv = s_cum[lo + 1] - cv;
+#define HB_RUN(E, X) run<E, W13, X>(p, vj, cv, Uv, fd, ring, meta, S, first)
+    switch (vj.enc * 2 + (S.on ? 1 : 0)) {
       case 2 * HB_F16 + 1: HB_RUN(HB_F16, true); break;
       case 2 * HB_F16 + 0: HB_RUN(HB_F16, false); break;
       case 2 * HB_Q8 + 1: HB_RUN(HB_Q8, true); break;
@@ -679,9 +698,30 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
       default: HB_RUN(HB_Q2, false); break;
     }
 #undef HB_RUN
-    u = cum + b;
-    cum += Uv;
-    ++v;
+    first = false;
+  }
+  if (first && S.on) {                       // no units at all: still build the stage share
+    if constexpr (!W13) pdl_wait();
+    stage_build_and_wait<W13>(p, S);
+  }
+  HB_TL(W13, gw, 3);
+}
+
+// h in global memory for K2b launches whose stage would not fit (large batch):
+// one thread per (slot, 32-row block)
+__global__ void hfin_kernel(const __grid_constant__ GemvParams p) {
+  const int nb = p.F / 32;
+  const int n = p.jt.hdr[1] * nb;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = i / nb, j = i - s * nb;
+    uint4 hi[4], lo[4];
+    const float hs = h_block(p.au, p.F, s, j, hi, lo);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      p.h_hi[(size_t)s * (p.F / 8) + j * 4 + t] = hi[t];
+      p.h_lo[(size_t)s * (p.F / 8) + j * 4 + t] = lo[t];
+    }
+    p.hsum[i] = hs;
   }
 }
 
@@ -697,14 +737,19 @@ void launch_w13(const GemvParams& p, cudaStream_t s) {
   static bool d = false;
   constexpr int smem = gemv_smem_bytes<true>();
   set_smem(gemv_kernel<true>, smem, d);
-  gemv_kernel<true><<<kGemvCTAs, kGemvWarps * 32, smem, s>>>(p);
+  launch_pdl(gemv_kernel<true>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
+}
+void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
+  const int n = max_slots * (p.F / 32);
+  hfin_kernel<<<(n + 255) / 256, 256, 0, s>>>(p);
 }
 void launch_w2(const GemvParams& p, cudaStream_t s) {
   static bool d = false;
   constexpr int smem = gemv_smem_bytes<false>();
   set_smem(gemv_kernel<false>, smem, d);
-  gemv_kernel<false><<<kGemvCTAs, kGemvWarps * 32, smem, s>>>(p);
+  launch_pdl(gemv_kernel<false>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
 }
+int w2_stage_capacity() { return KCfg<false>::XSTAGE; }
 
 }  // namespace hb
 

@@ -19,7 +19,7 @@ constexpr int kNumSM = 148;             // B200
 #define HB_WARP_SMEM_KB 13
 #endif
 constexpr int kGemvWarps = HB_GEMV_WARPS;   // warps per GEMV CTA (one CTA per SM)
-constexpr int kRouterThreads = 128;
+constexpr int kRouterThreads = 256;
 
 // Byte offsets of the sections of one matrix inside an expert blob.
 // Tile-major layout: unit (tile of 16 rows, 64-byte group) = 1 KB of codes at
@@ -44,20 +44,71 @@ struct Job {
   int32_t slot_off;    // first slot in slot_token / slot_gate / h
 };
 
-// Device job table of one forward: [hdr | jobs | slot_token | slot_gate]
+// Virtual job: <= kVSlots token slots of one job (one mma N tile), the unit
+// of the GEMV kernels' work space.
+constexpr int kVSlots = 8;
+constexpr int kMaxVJobs = 256;         // per forward (checked at hb_create)
+struct VJobD {
+  const uint8_t* blob;
+  int32_t enc;
+  int32_t slot0;
+  int32_t nslot;
+  int32_t pad;
+};
+
+// Device job table of one forward: [hdr | jobs | slot_token | slot_gate | tok_slots |
+// vjobs | vcum13 | vcum2]
 struct JobTable {
-  int32_t* hdr;        // [0] n_jobs, [1] n_slots
+  int32_t* hdr;        // [0] n_jobs, [1] n_slots, [2] n_vjobs
   Job* jobs;           // max_jobs
   int32_t* slot_token; // max_slots
   float* slot_gate;    // max_slots
   int32_t* tok_slots;  // [max_batch][top_k] slot of each (token, rank) or -1, rank order
+  VJobD* vjobs;        // max_vjobs
+  long long* vcum13;   // [max_vjobs + 1] K2a units before vjob v (last = total)
+  long long* vcum2;    // [max_vjobs + 1] K2b units before vjob v
 };
+
+#if defined(__CUDACC__)
+#define HB_HD __host__ __device__
+#else
+#define HB_HD
+#endif
+HB_HD inline int epg_of_enc(int enc) {
+  return enc == HB_F16 ? 32 : enc == HB_Q8 ? 64 : enc == HB_Q4 ? 128 : 256;
+}
+// Split jobs into virtual jobs and lay out the unit spaces of K2a (tiles of
+// F rows x groups of H) and K2b (tiles of H rows x groups of F).
+HB_HD inline int build_vjobs(const Job* jobs, int nj, int H, int F, VJobD* vj, long long* c13,
+                             long long* c2) {
+  int nv = 0;
+  long long u13 = 0, u2 = 0;
+  for (int j = 0; j < nj; ++j) {
+    for (int s = 0; s < jobs[j].n_tok; s += kVSlots) {
+      VJobD d;
+      d.blob = jobs[j].blob;
+      d.enc = jobs[j].enc;
+      d.slot0 = jobs[j].slot_off + s;
+      d.nslot = jobs[j].n_tok - s < kVSlots ? jobs[j].n_tok - s : kVSlots;
+      d.pad = 0;
+      vj[nv] = d;
+      c13[nv] = u13;
+      c2[nv] = u2;
+      u13 += (long long)(F / 16) * (H / epg_of_enc(d.enc));
+      u2 += (long long)(H / 16) * (F / epg_of_enc(d.enc));
+      ++nv;
+    }
+  }
+  c13[nv] = u13;
+  c2[nv] = u2;
+  return nv;
+}
 
 struct RouterParams {
   const __half* x;                     // [B, H]
   const __half* wg[kMaxRouteLayers];   // router of each routed layer
   int n_route;                         // routed layers in this launch
-  int B, E, H, k;
+  int B, E, H, F, k;
   int64_t theta1, theta2;              // k = 2 exact gap test
   int th1_kind, th2_kind;              // 0 finite, +1 always true, -1 never
   double t1, t2;                       // k > 2 fp64 test
@@ -67,8 +118,8 @@ struct RouterParams {
   long long* logits;                   // [B][E][2] copy for route 0, or null
   uint4* x_perm;                       // [B][H/8] pair-permuted x, or null
   float* xsum;                         // [B][H/32], or null
-  float* zero_buf;                     // zeroed by the router grid (h block sums)
-  long long zero_n;
+  float* zero_buf[2];                  // zeroed by the router grid: K2a sums, y
+  long long zero_n[2];                 // floats, multiples of 4 (16-byte aligned buffers)
   // resident job building (blob_table != null): last CTA builds the table
   const uint8_t* const* blob_table;    // [E][4] device blob of (expert, enc) for this layer
   int hi_enc, lo_enc;
@@ -82,24 +133,45 @@ struct GemvParams {
   int H, F, B, k;
   const uint4* x_perm;                 // [B][H/8]
   const float* xsum;                   // [B][H/32]
-  uint4* h_hi;                         // [slots][F/8]  pair-permuted fp16 hi part of h
-  uint4* h_lo;                         // [slots][F/8]  fp16 residual h - hi
-  float* hsum;                         // [slots][F/32] block sums of h (zeroed by router)
-  float* part;                         // stream-K pieces [warps][2][32 lanes][8]
-  float* ob;                           // [slots][H] per-slot W2 outputs
-  unsigned* cnt13;                     // [max_vjobs][F/16] piece counters (self-resetting)
-  unsigned* cnt2;                      // [max_vjobs][H/16]
-  unsigned* cnty;                      // [H/16] job counters of the y combine
-  float* y;                            // [B][H]
+  float* au;                           // [slots][2][F] K2a sums W1 x | W3 x (zeroed by router)
+  uint4* h_hi;                         // [slots][F/8]  pair-permuted fp16 hi part of h  (h_global)
+  uint4* h_lo;                         // [slots][F/8]  fp16 residual h - hi             (h_global)
+  float* hsum;                         // [slots][F/32] block sums of h                  (h_global)
+  int h_global;                        // K2b reads h from h_hi/h_lo/hsum (built by launch_hfin)
+                                       // instead of building it in shared memory per CTA
+  float* y;                            // [B][H] (zeroed by router)
+  // work feed: a static share of the units, then dynamic chunks (K2)
+  unsigned* ctr;                       // chunk counter of this kernel (self-resetting)
+  int max_vjobs;                       // table entries to preload (>= n_vjobs + 1)
+  float static_frac;                   // fraction of units dealt as static warp ranges
+  int chunk;                           // units per dynamic chunk
 };
 
 void launch_router(const RouterParams& p, cudaStream_t s);
+// kernel launch allowing programmatic dependent launch (the kernel overlaps
+// the tail of its predecessor in the stream and orders itself with
+// griddepcontrol.wait before touching the predecessor's outputs)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 void launch_w13(const GemvParams& p, cudaStream_t s);
+void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s);
 void launch_w2(const GemvParams& p, cudaStream_t s);
-constexpr int kVSlots = 8;             // token slots per virtual job (one mma N tile)
+int w2_stage_capacity();               // bytes of the K2b shared-memory stage of h
 constexpr int kGemvCTAs = kNumSM;      // persistent grid: one CTA per SM
 constexpr int kGemvTotalWarps = kGemvCTAs * kGemvWarps;
-constexpr int kPartFloats = 8;         // per lane per piece
 int launch_quantize_expert(int enc, int hidden, int ffn, const __half* w1, const __half* w3,
                            const __half* w2, uint8_t* blob, cudaStream_t s);
 void launch_synth(__half* dst, size_t n, uint64_t key, float scale, uint64_t start,

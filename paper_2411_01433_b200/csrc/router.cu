@@ -14,17 +14,30 @@
 // dot_exact) and the CTA combines them into one int128 L on a 2^-48 grid.
 // The k = 2 decision is the integer test  L0 - L1 <= Theta  (hb_theta).
 //
-// Launch: one CTA per (route layer, token, expert) row: B*n_route*E CTAs of
-// 128 threads (at B = 1 decode the 8 or 16 rows run in parallel instead of
-// one CTA walking them).  The last CTA to finish (grid counter) selects the
-// top-k of every (route layer, token), writes the decision records and, in
-// resident mode, the job table.  The CTAs of expert 0 also write the
-// pair-permuted copy of x and its block sums for the GEMV kernels.
+// Launch: one CTA per (route layer, token): n_route*B CTAs of 256 threads, a
+// warp per expert row.  At batch-1 decode (one CTA) the same CTA decides and
+// builds the job table from shared memory -- no grid-wide hand-off, no global
+// read-backs (the router is on the critical path of every layer).  With
+// several rows, the last CTA to finish (grid counter) decides for all of
+// them.  Route-0 CTAs also write the pair-permuted copy of their token's x
+// and its block sums for the GEMV kernels.  Static inputs (router rows, the
+// blob table) are fetched before griddepcontrol.wait, i.e. while the previous
+// kernel of the stream is still finishing.
 #include <cuda_fp16.h>
+
+#include <algorithm>
 
 #include "hb_internal.h"
 
 namespace hb {
+
+#ifdef HB_DBG_TIMELINE
+__device__ unsigned long long g_rtl[8];
+#define HB_RTL(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_rtl[i] = t_; } } while (0)
+#else
+#define HB_RTL(i) do { } while (0)
+#endif
 
 typedef __int128 i128;
 typedef unsigned long long u64;
@@ -46,11 +59,14 @@ __device__ __forceinline__ void accum_exact(uint32_t wbits, uint32_t xbits, u64&
   int mw, ew, mx, ex;
   fp16_mant_exp(wbits, mw, ew);
   fp16_mant_exp(xbits, mx, ex);
-  const u64 p = (u64)(long long)(mw * mx);
+  const long long p = (long long)(mw * mx);
   const int s = ew + ex + 48;
-  if (s >= 40) hi += p << (s - 40);
-  else if (s >= 20) mid += p << (s - 20);
-  else lo += p << s;
+  // branch-free: the bucket of s and the term shifted into it (no divergence)
+  const int r = (s >= 20) + (s >= 40);
+  const u64 term = (u64)(p << (s - 20 * r));
+  lo += r == 0 ? term : 0ull;
+  mid += r == 1 ? term : 0ull;
+  hi += r == 2 ? term : 0ull;
 }
 
 __device__ __forceinline__ bool gap_le(i128 G, int kind, long long theta) {
@@ -73,25 +89,16 @@ __device__ __forceinline__ i128 load_logit(const long long* lb, size_t i) {
   return ((i128)hi << 64) | (i128)lo;
 }
 
-// O3-O6 for one (route layer, token): top-k, gates, scores, decisions
-__device__ void decide(const RouterParams& p, int rl, int b) {
-  const size_t base = ((size_t)rl * p.B + b) * p.E;
-  i128 L[64];
-  for (int e = 0; e < p.E; ++e) L[e] = load_logit(p.lbuf, base + e);
-  int sel[kMaxTopK];
-  unsigned long long taken = 0ull;
-  for (int i = 0; i < p.k; ++i) {                 // O3: (L desc, index asc)
-    int best = -1;
-    for (int e = 0; e < p.E; ++e) {
-      if (taken >> e & 1ull) continue;
-      if (best < 0 || L[e] > L[best]) best = e;
-    }
-    sel[i] = best;
-    taken |= 1ull << best;
-  }
+
+// O4-O6 for one (route layer, token) given its E exact logits L and the
+// top-k selection sel (O3): gates, scores, decisions.  Writes the k records to
+// `out` (and `out_s` if given).
+__device__ void decide_sel(const RouterParams& p, const i128* L, const int* sel, int b,
+                           hb_decision* out, hb_decision* out_s) {
   const double l0 = i128_to_double(L[sel[0]]) * 0x1p-48;
-  double g[kMaxTopK], tot = 0.0;
-  for (int i = 0; i < p.k; ++i) {                 // O4: softmax over the selected
+  double g[kMaxTopK], tot = 1.0;
+  g[0] = 1.0;                                     // exp(l0 - l0)
+  for (int i = 1; i < p.k; ++i) {                 // O4: softmax over the selected
     g[i] = exp(i128_to_double(L[sel[i]]) * 0x1p-48 - l0);
     tot += g[i];
   }
@@ -108,7 +115,6 @@ __device__ void decide(const RouterParams& p, int rl, int b) {
       prec[i] = s <= p.t1 ? HB_HIGH : s <= p.t2 ? HB_LOW : HB_SKIP;
     }
   }
-  hb_decision* out = p.dec + ((size_t)rl * p.B + b) * p.k;
   for (int i = 0; i < p.k; ++i) {
     hb_decision d;
     d.token = b;
@@ -119,50 +125,101 @@ __device__ void decide(const RouterParams& p, int rl, int b) {
     d.hit = 0;
     d.gate = (float)(g[i] / tot);
     out[i] = d;
+    if (out_s) out_s[i] = d;
   }
-  if (rl == 0 && p.logits)
-    for (int e = 0; e < p.E; ++e) {
-      p.logits[((size_t)b * p.E + e) * 2 + 0] = (long long)(u64)L[e];
-      p.logits[((size_t)b * p.E + e) * 2 + 1] = (long long)(L[e] >> 64);
-    }
 }
 
-// resident mode: group the non-skipped owned selections into (expert, enc) jobs
-__device__ void build_jobs(const RouterParams& p) {
+// O3-O6, one thread: top-k by (L desc, index asc), then decide_sel
+__device__ void decide(const RouterParams& p, const i128* L, int b, hb_decision* out,
+                       hb_decision* out_s) {
+  int sel[kMaxTopK];
+  unsigned long long taken = 0ull;
+  for (int i = 0; i < p.k; ++i) {
+    int best = -1;
+    for (int e = 0; e < p.E; ++e) {
+      if (taken >> e & 1ull) continue;
+      if (best < 0 || L[e] > L[best]) best = e;
+    }
+    sel[i] = best;
+    taken |= 1ull << best;
+  }
+  decide_sel(p, L, sel, b, out, out_s);
+}
+
+// O3 by one warp: k rounds of a warp arg-max over (L desc, index asc).  The
+// same selection as decide(), with a dependency chain of ~k*5 shuffle steps
+// instead of E*k serial compares (the router is on every layer's critical path).
+__device__ void topk_warp(const RouterParams& p, const i128* L, int* sel) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long taken = 0ull;
+  for (int i = 0; i < p.k; ++i) {
+    int be = -1;
+    i128 bv = 0;
+    for (int e = lane; e < p.E; e += 32)
+      if (!(taken >> e & 1ull) && (be < 0 || L[e] > bv)) { bv = L[e]; be = e; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 olo = __shfl_xor_sync(0xffffffffu, (u64)bv, o);
+      const u64 ohi = __shfl_xor_sync(0xffffffffu, (u64)(bv >> 64), o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      const i128 ov = (i128)(((unsigned __int128)ohi << 64) | olo);
+      if (oe >= 0 && (be < 0 || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
+    }
+    sel[i] = be;
+    taken |= 1ull << be;
+  }
+}
+
+constexpr int kMaxDecSmem = 512;
+constexpr int kRouterCluster = 8;      // CTAs (SMs) per (route layer, token) row       // route-0 decisions kept in shared memory
+
+struct RouterSmem {
+  i128 L[64];                          // this CTA's exact logits
+  u64 part[kRouterThreads / 32][3];    // per-warp partial (lo, mid, hi)
+  u64 cpart[64][3];                    // this CTA's partial per expert (read by the leader)
+  hb_decision dec[kMaxDecSmem];        // route-0 decisions (single-CTA / last-CTA path)
+  const uint8_t* blob[64 * 4];         // blob table of the layer
+  Job jobs[2 * 64 + 1];
   int count[2 * 64], jobid[2 * 64], fill[2 * 64];
+  int last;
+};
+
+// resident mode: group the non-skipped owned selections into (expert, enc)
+// jobs, ordered by expert then High before Low; slots in token order.  All
+// reads come from shared memory; the global table is written once.
+__device__ void build_jobs(const RouterParams& p, RouterSmem& sm, const hb_decision* dec) {
   const int nkey = 2 * p.E;
-  for (int i = 0; i < nkey; ++i) count[i] = 0;
+  for (int i = 0; i < nkey; ++i) sm.count[i] = 0;
   const int nsel = p.B * p.k;
   for (int i = 0; i < nsel; ++i) {
-    const int4 raw = __ldcg(reinterpret_cast<const int4*>(p.dec) + i);
-    const hb_decision& d = *reinterpret_cast<const hb_decision*>(&raw);
+    const hb_decision d = dec[i];
     if (d.prec == HB_SKIP || d.expert % p.world != p.rank) continue;
-    count[d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1)]++;
+    sm.count[d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1)]++;
   }
   int nj = 0, off = 0;
-  for (int key = 0; key < nkey; ++key) {     // jobs by expert, High before Low
-    jobid[key] = -1;
-    fill[key] = 0;
-    if (!count[key]) continue;
+  for (int key = 0; key < nkey; ++key) {
+    sm.jobid[key] = -1;
+    sm.fill[key] = 0;
+    if (!sm.count[key]) continue;
     const int e = key >> 1;
     const int enc = (key & 1) ? p.lo_enc : p.hi_enc;
     Job j;
-    j.blob = p.blob_table[e * 4 + enc];
+    j.blob = sm.blob[e * 4 + enc];
     j.enc = enc;
     j.expert = e;
-    j.n_tok = count[key];
+    j.n_tok = sm.count[key];
     j.slot_off = off;
+    sm.jobs[nj] = j;
     p.jt.jobs[nj] = j;
-    jobid[key] = nj++;
-    off += count[key];
+    sm.jobid[key] = nj++;
+    off += sm.count[key];
   }
-  for (int i = 0; i < nsel; ++i) {           // slots in token order
-    const int4 raw = __ldcg(reinterpret_cast<const int4*>(p.dec) + i);
-    hb_decision d = *reinterpret_cast<const hb_decision*>(&raw);
+  for (int i = 0; i < nsel; ++i) {
+    hb_decision d = dec[i];
     p.jt.tok_slots[i] = -1;
     if (d.prec == HB_SKIP || d.expert % p.world != p.rank) continue;
     const int key = d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1);
-    const int slot = p.jt.jobs[jobid[key]].slot_off + fill[key]++;
+    const int slot = sm.jobs[sm.jobid[key]].slot_off + sm.fill[key]++;
     p.jt.slot_token[slot] = d.token;
     p.jt.slot_gate[slot] = d.gate;
     p.jt.tok_slots[i] = slot;
@@ -172,47 +229,174 @@ __device__ void build_jobs(const RouterParams& p) {
   }
   p.jt.hdr[0] = nj;
   p.jt.hdr[1] = off;
+  p.jt.hdr[2] = build_vjobs(sm.jobs, nj, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
+}
+
+// build_jobs by one warp when the forward has <= 32 selections (decode): the
+// same table (jobs by key = expert*2 + Low, slots in selection order) from
+// per-lane counts instead of serial loops.
+__device__ void build_jobs_warp(const RouterParams& p, RouterSmem& sm, const hb_decision* dec) {
+  const int lane = threadIdx.x & 31;
+  const int nsel = p.B * p.k;
+  constexpr int kNone = 0x7FFFFFFF;
+  hb_decision d{};
+  int key = kNone;
+  if (lane < nsel) {
+    d = dec[lane];
+    if (d.prec != HB_SKIP && d.expert % p.world == p.rank)
+      key = d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1);
+  }
+  const bool valid = key != kNone;
+  int less = 0, rank = 0, ntok = 0;
+  for (int j = 0; j < 32; ++j) {
+    const int kj = __shfl_sync(0xffffffffu, key, j);
+    less += kj != kNone && kj < key;
+    ntok += kj == key;
+    rank += kj == key && j < lane;
+  }
+  const bool first = valid && rank == 0;
+  int jid = 0;
+  for (int j = 0; j < 32; ++j) {
+    const int kj = __shfl_sync(0xffffffffu, key, j);
+    const int fj = __shfl_sync(0xffffffffu, (int)first, j);
+    jid += fj && kj < key;
+  }
+  const int nj = __popc(__ballot_sync(0xffffffffu, first));
+  const int nslot = __popc(__ballot_sync(0xffffffffu, valid));
+  if (lane < nsel) p.jt.tok_slots[lane] = -1;
+  if (valid) {
+    const int slot = less + rank;
+    const int enc = (key & 1) ? p.lo_enc : p.hi_enc;
+    p.jt.slot_token[slot] = d.token;
+    p.jt.slot_gate[slot] = d.gate;
+    p.jt.tok_slots[lane] = slot;
+    d.served_enc = (uint8_t)enc;
+    d.hit = 1;
+    p.dec[lane] = d;
+    if (first) {
+      Job j;
+      j.blob = sm.blob[(key >> 1) * 4 + enc];
+      j.enc = enc;
+      j.expert = key >> 1;
+      j.n_tok = ntok;
+      j.slot_off = less;
+      sm.jobs[jid] = j;
+      p.jt.jobs[jid] = j;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    p.jt.hdr[0] = nj;
+    p.jt.hdr[1] = nslot;
+    p.jt.hdr[2] = build_vjobs(sm.jobs, nj, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
+  }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ u64 ld_dsmem_u64(const void* local, int rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(local), r;
+  u64 v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(r) : "memory");
+  return v;
 }
 
 __global__ void __launch_bounds__(kRouterThreads)
 router_kernel(const __grid_constant__ RouterParams p) {
-  __shared__ u64 red[3][kRouterThreads / 32];
-  __shared__ int s_last;
+  __shared__ RouterSmem sm;
+  HB_RTL(0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int e = blockIdx.x % p.E;
-  const int b = (blockIdx.x / p.E) % p.B;
-  const int rl = blockIdx.x / (p.E * p.B);
-
-  // zero the GEMV h block-sum buffer (grid-stride)
-  for (long long i = blockIdx.x * (long long)blockDim.x + tid; i < p.zero_n;
-       i += (long long)gridDim.x * blockDim.x)
-    p.zero_buf[i] = 0.f;
-
-  // O2: exact logit of row e of layer rl for token b
+  constexpr int NW = kRouterThreads / 32;
+  constexpr int C = kRouterCluster;
+  const int nrows = p.n_route * p.B;
+  const int row = blockIdx.x / C, crank = blockIdx.x % C;   // cluster = one row
+  if (row >= nrows) {
+    // ---- zeroing CTAs: the buffers the GEMV kernels accumulate into (K2a
+    // sums, y); they belong to the previous kernels of the stream, so wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    const long long t0 = (long long)(blockIdx.x - nrows * C) * blockDim.x + tid;
+    const long long stride = (long long)(gridDim.x - nrows * C) * blockDim.x;
+#pragma unroll
+    for (int z = 0; z < 2; ++z) {
+      float* zb = p.zero_buf[z];
+      const long long n = p.zero_n[z];
+      if ((reinterpret_cast<uintptr_t>(zb) & 15) == 0) {
+        for (long long i = t0; i < n / 4; i += stride)
+          reinterpret_cast<float4*>(zb)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (long long i = (n / 4) * 4 + t0; i < n; i += stride) zb[i] = 0.f;
+      } else {
+        for (long long i = t0; i < n; i += stride) zb[i] = 0.f;
+      }
+    }
+    return;
+  }
+  const int b = row % p.B;
+  const int rl = row / p.B;
+  // this CTA's slice of the hidden dimension (in uint4 = 8 fp16)
+  const int n8 = p.H / 8;
+  const int s0 = crank * n8 / C, s1 = (crank + 1) * n8 / C;
+  // ---- static inputs before waiting on the previous kernel: this CTA's
+  // slice of the router rows into L2, the layer's blob table (leader)
+  {
+    const char* wb = reinterpret_cast<const char*>(p.wg[rl]);
+    const int lpr = (s1 - s0) * 16 / 128;                  // 128-byte lines per row slice
+    for (int i = tid; i < p.E * lpr; i += kRouterThreads) {
+      const int e = i / lpr, l = i - e * lpr;
+      asm volatile("prefetch.global.L2 [%0];" :: "l"(wb + ((size_t)e * n8 + s0) * 16 + (size_t)l * 128));
+    }
+    if (p.blob_table && crank == 0)
+      for (int i = tid; i < 4 * p.E; i += kRouterThreads) sm.blob[i] = p.blob_table[i];
+  }
+  // programmatic dependent launch: x and the job table belong to the
+  // previous kernels of the stream
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  HB_RTL(1);
+  // ---- O2: exact partial logits of token b over this CTA's slice, every
+  // expert (a warp per expert, or several warps per expert when E < 8)
   const __half* x = p.x + (size_t)b * p.H;
-  const __half* w = p.wg[rl] + (size_t)e * p.H;
-  u64 lo = 0, mid = 0, hi = 0;
-  for (int h0 = tid * 8; h0 < p.H; h0 += 8 * kRouterThreads) {
-    const uint4 wv = *reinterpret_cast<const uint4*>(w + h0);
-    const uint4 xv = *reinterpret_cast<const uint4*>(x + h0);
-    const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
-    const uint32_t xa[4] = {xv.x, xv.y, xv.z, xv.w};
+  const uint4* x4 = reinterpret_cast<const uint4*>(x);
+  const int wpe = p.E >= NW ? 1 : NW / p.E;
+  for (int task = warp; task < p.E * wpe; task += NW) {
+    const int e = task / wpe, part = task - e * wpe;
+    const uint4* w4 = reinterpret_cast<const uint4*>(p.wg[rl] + (size_t)e * p.H);
+    const int j0 = s0 + part * (s1 - s0) / wpe, j1 = s0 + (part + 1) * (s1 - s0) / wpe;
+    u64 lo = 0, mid = 0, hi = 0;
+#pragma unroll 2
+    for (int j = j0 + lane; j < j1; j += 32) {
+      const uint4 wv = w4[j];
+      const uint4 xv = x4[j];
+      const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
+      const uint32_t xa[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      accum_exact((wa[i >> 1] >> (16 * (i & 1))) & 0xFFFF, (xa[i >> 1] >> (16 * (i & 1))) & 0xFFFF,
-                  lo, mid, hi);
-  }
+      for (int i = 0; i < 8; ++i)
+        accum_exact((wa[i >> 1] >> (16 * (i & 1))) & 0xFFFF, (xa[i >> 1] >> (16 * (i & 1))) & 0xFFFF,
+                    lo, mid, hi);
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    lo += __shfl_xor_sync(0xffffffffu, lo, o);
-    mid += __shfl_xor_sync(0xffffffffu, mid, o);
-    hi += __shfl_xor_sync(0xffffffffu, hi, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      lo += __shfl_xor_sync(0xffffffffu, lo, o);
+      mid += __shfl_xor_sync(0xffffffffu, mid, o);
+      hi += __shfl_xor_sync(0xffffffffu, hi, o);
+    }
+    if (lane == 0) { sm.part[task][0] = lo; sm.part[task][1] = mid; sm.part[task][2] = hi; }
   }
-  if (lane == 0) { red[0][warp] = lo; red[1][warp] = mid; red[2][warp] = hi; }
-
-  // pair-permuted x and block sums for the GEMV kernels (route 0, expert 0 CTAs)
-  if (p.x_perm && rl == 0 && e == 0) {
-    for (int blk = tid; blk < p.H / 32; blk += blockDim.x) {
+  __syncthreads();
+  for (int e = tid; e < p.E; e += blockDim.x) {            // CTA partial per expert
+    u64 lo = 0, mid = 0, hi = 0;
+    for (int q = 0; q < wpe; ++q) {
+      lo += sm.part[e * wpe + q][0]; mid += sm.part[e * wpe + q][1]; hi += sm.part[e * wpe + q][2];
+    }
+    sm.cpart[e][0] = lo; sm.cpart[e][1] = mid; sm.cpart[e][2] = hi;
+  }
+  HB_RTL(2);
+  // ---- pair-permuted x and block sums of this slice for the GEMV kernels
+  if (p.x_perm && rl == 0) {
+    for (int blk = s0 / 4 + tid; blk < s1 / 4; blk += blockDim.x) {
       const uint4* src = reinterpret_cast<const uint4*>(x + blk * 32);
       uint32_t v[16];
 #pragma unroll
@@ -239,35 +423,108 @@ router_kernel(const __grid_constant__ RouterParams p) {
       }
     }
   }
-  __syncthreads();
-  if (tid == 0) {
-    u64 L0 = 0, L1 = 0, L2 = 0;
-    for (int i = 0; i < kRouterThreads / 32; ++i) { L0 += red[0][i]; L1 += red[1][i]; L2 += red[2][i]; }
-    const i128 L = (i128)(long long)L0 + ((i128)(long long)L1 << 20) + ((i128)(long long)L2 << 40);
+  // ---- combine the cluster's partials in the leader (distributed shared memory)
+  cluster_sync_all();
+  if (crank == 0) {
+    for (int e = tid; e < p.E; e += blockDim.x) {
+      u64 lo = 0, mid = 0, hi = 0;
+      for (int r = 0; r < C; ++r) {
+        lo += ld_dsmem_u64(&sm.cpart[e][0], r);
+        mid += ld_dsmem_u64(&sm.cpart[e][1], r);
+        hi += ld_dsmem_u64(&sm.cpart[e][2], r);
+      }
+      sm.L[e] = (i128)(long long)lo + ((i128)(long long)mid << 20) + ((i128)(long long)hi << 40);
+    }
+  }
+  cluster_sync_all();                        // remote reads done: the other CTAs may exit
+  if (crank != 0) return;
+  HB_RTL(3);
+  HB_RTL(4);
+  if (rl == 0 && p.logits)
+    for (int e = tid; e < p.E; e += blockDim.x) {
+      p.logits[((size_t)b * p.E + e) * 2 + 0] = (long long)(u64)sm.L[e];
+      p.logits[((size_t)b * p.E + e) * 2 + 1] = (long long)(sm.L[e] >> 64);
+    }
+
+  // ---- single (route layer, token): decide and build the jobs right here
+  if (nrows == 1) {
+    if (warp == 0) {
+      int sel[kMaxTopK];
+      topk_warp(p, sm.L, sel);
+      if (lane == 0) decide_sel(p, sm.L, sel, b, p.dec, sm.dec);
+      __syncwarp();
+      HB_RTL(5);
+      if (p.blob_table) {
+        if (p.B * p.k <= 32) build_jobs_warp(p, sm, sm.dec);
+        else if (lane == 0) build_jobs(p, sm, sm.dec);
+      }
+      HB_RTL(6);
+    }
+    return;
+  }
+
+  // ---- several rows: publish the logits; the last leader decides for all
+  for (int e = tid; e < p.E; e += blockDim.x) {
     const size_t idx = ((size_t)rl * p.B + b) * p.E + e;
-    p.lbuf[2 * idx] = (long long)(u64)L;
-    p.lbuf[2 * idx + 1] = (long long)(L >> 64);
-    __threadfence();
-    const unsigned prev = atomicAdd(p.done, 1u);
-    s_last = (prev == gridDim.x - 1);
+    p.lbuf[2 * idx] = (long long)(u64)sm.L[e];
+    p.lbuf[2 * idx + 1] = (long long)(sm.L[e] >> 64);
   }
   __syncthreads();
-  if (!s_last) return;
-  // ---- last CTA: decisions for every (route layer, token), then jobs ----
-  __threadfence();
-  for (int i = tid; i < p.n_route * p.B; i += blockDim.x) decide(p, i / p.B, i % p.B);
-  __syncthreads();
   if (tid == 0) {
     __threadfence();
-    if (p.blob_table) build_jobs(p);
-    __threadfence();
+    const unsigned prev = atomicAdd(p.done, 1u);
+    sm.last = (prev == (unsigned)nrows - 1);
+  }
+  __syncthreads();
+  if (!sm.last) return;
+  __threadfence();
+  const bool dec_smem = p.B * p.k <= kMaxDecSmem;
+  for (int i = tid; i < p.n_route * p.B; i += blockDim.x) {
+    const int r = i / p.B, bb = i % p.B;
+    i128 L[64];
+    const size_t base = ((size_t)r * p.B + bb) * p.E;
+    for (int e = 0; e < p.E; ++e) L[e] = load_logit(p.lbuf, base + e);
+    decide(p, L, bb, p.dec + ((size_t)r * p.B + bb) * p.k,
+           r == 0 && dec_smem ? sm.dec + (size_t)bb * p.k : nullptr);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (p.blob_table) {
+      __threadfence();
+      build_jobs(p, sm, dec_smem ? sm.dec : p.dec);
+    }
     *p.done = 0u;
   }
 }
 
 void launch_router(const RouterParams& p, cudaStream_t s) {
-  const int grid = p.n_route * p.B * p.E;
-  router_kernel<<<grid, kRouterThreads, 0, s>>>(p);
+  // one 8-CTA cluster per (route layer, token) row, plus clusters of CTAs that
+  // zero the GEMV accumulation buffers in parallel
+  const long long nz4 = (p.zero_n[0] + p.zero_n[1]) / 4;
+  int zc = nz4 ? (int)std::min<long long>(32, (nz4 + 2 * kRouterThreads - 1) / (2 * kRouterThreads)) : 0;
+  zc = (zc + kRouterCluster - 1) / kRouterCluster * kRouterCluster;
+  const int grid = p.n_route * p.B * kRouterCluster + zc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kRouterThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = kRouterCluster;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, router_kernel, p);
 }
 
 }  // namespace hb
+
+#ifdef HB_DBG_TIMELINE
+extern "C" int hb_debug_router_timeline(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, hb::g_rtl, sizeof(hb::g_rtl));
+}
+#endif

@@ -134,6 +134,24 @@ def test_layer_parity_tiny(pair, B):
                 assert nw <= 1e-4, (b, nw)       # expected ~1e-6 with exact codes
 
 
+@pytest.mark.parametrize("pair", PAIRS, ids=lambda p: f"{fm.ENC_NAMES[p[0]]}-{fm.ENC_NAMES[p[1]]}")
+def test_layer_parity_h_global(pair, monkeypatch):
+    """K2b with h built in global memory (hfin kernel + global B-operand path),
+    the configuration large batches take when h does not fit the CTA stage."""
+    monkeypatch.setenv("HB_FORCE_H_GLOBAL", "1")
+    sh = sg.TINY
+    hi, lo = pair
+    ctx = _resident(sh, [0], hi, lo, max_batch=8)
+    store = OracleStore(sh)
+    x16 = sg.hidden_states(sh, 21, 0, batch=8)
+    y = _run(ctx, 0, x16)
+    ref, routes = om.moe_layer(x16, sg.router_weights(sh, 0), store, 0, 2, 0.6, 0.9, hi, lo)
+    _check_routes(ctx, routes, 8, 2)
+    for b in range(8):
+        nw, el = rel_err(y[b], ref[b])
+        assert nw <= 1e-4, (b, nw, el)
+
+
 @pytest.mark.parametrize("t1,t2", [(1.0, 1.0), (0.0, 0.0), (0.5, 0.5), (0.6, 0.6)])
 def test_layer_threshold_edges(t1, t2):
     sh = sg.TINY
@@ -169,7 +187,9 @@ def test_ep_partition_on_one_gpu(world):
     np.testing.assert_allclose(np.sum(parts, axis=0), full, rtol=1e-5, atol=1e-6)
 
 
-def test_cuda_graph_capture_replays_identically():
+def test_cuda_graph_capture_replays():
+    """Graph replay = eager launch (pieces are added with fp32 atomics, so the
+    last bits may differ between runs: DESIGN.md R24)."""
     sh = sg.TINY
     ctx = _resident(sh, [0, 1], fm.F16, fm.Q4, max_batch=1)
     x = torch.from_numpy(sg.hidden_states(sh, 1, 0)).cuda()
@@ -187,7 +207,8 @@ def test_cuda_graph_capture_replays_identically():
     y.zero_()
     g.replay()
     torch.cuda.synchronize()
-    assert torch.equal(y, ref)
+    torch.testing.assert_close(y, ref, rtol=1e-5, atol=1e-6)
+    assert ctx.launch_count() > 0
 
 
 # ------------------------------------------------------------ full size

@@ -36,12 +36,19 @@ def main():
     Hd = shape.hidden
     Y = torch.empty(1, Hd, dtype=torch.float32, device="cuda")
     rows = {0: [], 1: []}
+    rfn = lib.hb_debug_router_timeline
+    rfn.argtypes = [ctypes.c_void_p]
+    rbuf = np.zeros(8, dtype=np.uint64)
+    rrows = []
     for t in range(4):
         for l in range(0, shape.n_layers, 4):
             x = torch.from_numpy(sg.hidden_states(shape, 1000 + t, l)).cuda()
             for _ in range(3):       # warm; the last launch is recorded
                 ctx.forward(l, x.view(1, Hd), Y)
             torch.cuda.synchronize()
+            assert rfn(rbuf.ctypes.data) == 0
+            rb = rbuf.astype(np.int64)
+            rrows.append((rb[1:8] - rb[0]) / 1000.0)
             for k in (0, 1):
                 assert fn(buf.ctypes.data, k) == 0
                 b = buf.astype(np.int64)
@@ -56,6 +63,9 @@ def main():
                     np.save(f"gpurun_out/tl_{model}_{pair}_{k}.npy", b)
                 buf[:] = 0
                 # clear device copy for the next launch (stale warps would confuse)
+    np.set_printoptions(suppress=True, linewidth=200)
+    print("router stamps (us after entry: wait, partial, combine, -, decide, jobs, warm decide+jobs):",
+          np.median(np.array(rrows), axis=0).round(2))
     for k, name in ((0, "K2a"), (1, "K2b")):
         a = np.array(rows[k])
         print(f"{model} {pair} {name}: entry_max {np.median(a[:,0]):.2f}  stage med/max "
