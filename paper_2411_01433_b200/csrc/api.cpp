@@ -81,6 +81,7 @@ struct hb_ctx {
   float* hsum = nullptr;
   bool force_h_global = false;            // HB_FORCE_H_GLOBAL=1 (tests of that path)
   unsigned* done = nullptr;
+  unsigned* gctr = nullptr;               // GEMV chunk counters [2 + kMaxVJobs] (self-resetting)
   JobTable jt{};
   void* jt_dev = nullptr;
   void* jt_host = nullptr;                // pinned staging
@@ -179,7 +180,7 @@ static void free_ctx(hb_ctx* c) {
   cudaDeviceSynchronize();
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
                    c->logits, c->lbuf, c->x_perm, c->xsum, c->au, c->h_hi, c->h_lo,
-                   c->hsum, c->done, c->jt_dev};
+                   c->hsum, c->done, c->gctr, c->jt_dev};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
@@ -254,7 +255,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
             dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->hsum, (size_t)c->max_slots * (F / 32) * 4) &&
-            dm((void**)&c->done, 16);
+            dm((void**)&c->done, 16) && dm((void**)&c->gctr, sizeof(unsigned) * (2 + kMaxVJobs));
   if (!ok) return bail(HB_ENOMEM, "device allocation of scratch failed");
   {
     const char* fh = std::getenv("HB_FORCE_H_GLOBAL");
@@ -265,6 +266,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     if (ch) c->chunk = std::max(1, std::atoi(ch));
   }
   cudaMemset(c->done, 0, 16);
+  cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + kMaxVJobs));
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
   // job table: hdr | jobs | slot_token | slot_gate | tok_slots
   const size_t o_jobs = 64, o_tok = align_up(o_jobs + sizeof(Job) * c->max_jobs, 64),
@@ -430,11 +432,16 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
   g.h_lo = c->h_lo;
   g.hsum = c->hsum;
   // K2b builds h in each CTA's shared memory when every possible slot fits
+  // K2b builds h in shared memory per CTA group (one group per vjob) when the
+  // slots of any vjob fit its stage and every vjob can get a CTA
   const size_t slot_bytes = (size_t)k.ffn * 2 * 2 + (size_t)(k.ffn / 32) * 4;
-  g.h_global = c->force_h_global ||
-               (size_t)batch * k.top_k * slot_bytes > (size_t)w2_stage_capacity();
+  const int max_ns = std::min(kVSlots, batch);
+  const int nv_bound = std::min(2 * k.n_experts, batch * k.top_k) +
+                       (batch * k.top_k + kVSlots - 1) / kVSlots;
+  g.h_global = c->force_h_global || (size_t)max_ns * slot_bytes > (size_t)w2_stage_capacity() ||
+               nv_bound > kGemvCTAs;
   g.y = (float*)y;
-  g.ctr = c->done + 1;
+  g.ctr = c->gctr;
   g.max_vjobs = c->max_vjobs;
   g.static_frac = c->static_frac;
   g.chunk = c->chunk;
@@ -447,10 +454,8 @@ static void launch_gemv(hb_ctx* c, const GemvParams& gp, cudaStream_t s) {
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
   if (ev) cudaEventRecord(ev[0], s);
   launch_w13(gp, s);
-  if (gp.h_global) {
-    launch_hfin(gp, c->last_batch * c->cfg.top_k, s);
-    c->launches += 1;
-  }
+  launch_hfin(gp, c->last_batch * c->cfg.top_k, s);
+  c->launches += 1;
   if (ev) cudaEventRecord(ev[1], s);
   launch_w2(gp, s);
   if (ev) cudaEventRecord(ev[2], s);

@@ -172,9 +172,9 @@ template <> struct KCfg<true> {        // K2a: x is small (8 KB per token at H=4
   static constexpr int RING = 16 * 12 * 1024 / kGemvWarps / 128 * 128;
   static constexpr int XSTAGE = 28 * 1024;  // 3 tokens at H = 4096
 };
-template <> struct KCfg<false> {       // K2b: h of two slots is 118 KB at F=14336
-  static constexpr int RING = 16 * 6656 / kGemvWarps / 128 * 128;
-  static constexpr int XSTAGE = 116 * 1024; // 2 slots at F = 14336 (118272 B)
+template <> struct KCfg<false> {       // K2b: h of one slot is 59 KB at F=14336
+  static constexpr int RING = 16 * 10240 / kGemvWarps / 128 * 128;
+  static constexpr int XSTAGE = 60 * 1024;  // 1 slot at F = 14336 (59136 B), 2 at F = 6400
 };
 template <bool W13>
 constexpr int gemv_smem_bytes() { return kGemvWarps * KCfg<W13>::RING + KCfg<W13>::XSTAGE; }
@@ -271,16 +271,18 @@ __device__ __forceinline__ float h_block(const float* au, int F, int s, int j, u
 //   part 0 (x / h hi) [nrows][K/8] uint4 | part 1 (h lo, K2b) | sums [nrows][K/32] f32
 // Warp `w` of the CTA builds its share (items w, w + kGemvWarps, ...).
 template <bool W13>
-__device__ void stage_share(const GemvParams& p, int w, uint8_t* st, int nrows) {
+__device__ void stage_share(const GemvParams& p, int w, uint8_t* st, int row0, int nrows) {
   const int lane = threadIdx.x & 31;
   if constexpr (W13) {
     const int K = p.H;
     const int n16 = nrows * (K / 8);
     uint4* dst = reinterpret_cast<uint4*>(st);
-    for (int i = w * 32 + lane; i < n16; i += kGemvWarps * 32) dst[i] = __ldcg(p.x_perm + i);
+    const uint4* xs = p.x_perm + (size_t)row0 * (K / 8);
+    for (int i = w * 32 + lane; i < n16; i += kGemvWarps * 32) dst[i] = __ldcg(xs + i);
     const int nz = nrows * (K / 32);
     float* zd = reinterpret_cast<float*>(st + (size_t)n16 * 16);
-    for (int i = w * 32 + lane; i < nz; i += kGemvWarps * 32) zd[i] = __ldcg(p.xsum + i);
+    const float* zs = p.xsum + (size_t)row0 * (K / 32);
+    for (int i = w * 32 + lane; i < nz; i += kGemvWarps * 32) zd[i] = __ldcg(zs + i);
   } else {
     const int K = p.F, nb = K / 32;
     uint4* dhi = reinterpret_cast<uint4*>(st);
@@ -289,7 +291,7 @@ __device__ void stage_share(const GemvParams& p, int w, uint8_t* st, int nrows) 
     for (int i = w * 32 + lane; i < nrows * nb; i += kGemvWarps * 32) {
       const int s = i / nb, j = i - s * nb;
       uint4 hi[4], lo[4];
-      const float hs = h_block(p.au, K, s, j, hi, lo);
+      const float hs = h_block(p.au, K, row0 + s, j, hi, lo);
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         dhi[(size_t)s * (K / 8) + j * 4 + t] = hi[t];
@@ -321,13 +323,35 @@ struct Stage {
   uint8_t* ptr;      // generic pointer of the stage
   uint32_t xst;      // its shared address
   uint32_t bar;      // mbarrier (count = blockDim.x)
+  int row0;          // first staged row (token for x, slot for h)
   int nrows;
   bool on;           // B operand read from the stage (else from global memory)
 };
 
+// K2b: h rows [row0, row0 + nrows) of h_hi | h_lo | hsum (built by hfin) into
+// the stage with three bulk (TMA) copies issued by thread 0; every thread
+// waits on the mbarrier's transaction count.
+__device__ __forceinline__ void stage_h_bulk_and_wait(const GemvParams& p, const Stage& S) {
+  if (threadIdx.x == 0) {
+    const uint32_t nh = (uint32_t)S.nrows * p.F * 2, nz = (uint32_t)S.nrows * (p.F / 32) * 4;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(S.bar), "r"(2 * nh + nz) : "memory");
+    const char* src[3] = {reinterpret_cast<const char*>(p.h_hi + (size_t)S.row0 * (p.F / 8)),
+                          reinterpret_cast<const char*>(p.h_lo + (size_t)S.row0 * (p.F / 8)),
+                          reinterpret_cast<const char*>(p.hsum + (size_t)S.row0 * (p.F / 32))};
+    const uint32_t off[3] = {0u, nh, 2 * nh}, len[3] = {nh, nh, nz};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          :: "r"(S.xst + off[i]), "l"(src[i]), "r"(len[i]), "r"(S.bar) : "memory");
+  }
+  mbar_wait(S.bar, 0);
+}
+
 template <bool W13>
 __device__ __forceinline__ void stage_build_and_wait(const GemvParams& p, const Stage& S) {
-  stage_share<W13>(p, threadIdx.x >> 5, S.ptr, S.nrows);
+  stage_share<W13>(p, threadIdx.x >> 5, S.ptr, S.row0, S.nrows);
   mbar_arrive(S.bar);
   mbar_wait(S.bar, 0);
 }
@@ -353,7 +377,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // next chunk index is fetched one chunk ahead, so the atomic's latency is
 // hidden behind the current chunk's loads.
 struct FeedConst {         // per launch, in shared memory (CTA-wide constants)
-  int S, U;                // static units, all units (< 2^31: checked by the host)
+  int base;                // first unit of the space this CTA works in
+  int S, U;                // static units, all units of the space (< 2^31: checked by the host)
   int nch;                 // dynamic chunks
   int chunk;
   int nwarps;              // warps taking part (each fetches until it sees >= nch)
@@ -378,8 +403,8 @@ struct Feed {
       done = true;
       return false;
     }
-    a = k->S + c * k->chunk;
-    b = min(a + k->chunk, k->U);
+    a = k->base + k->S + c * k->chunk;
+    b = min(a + k->chunk, k->base + k->U);
     prefetch();
     return true;
   }
@@ -468,15 +493,15 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
 #pragma unroll 1
   for (int s = 0; s < DEPTH - 1; ++s) issue();
   if (!W13 && first) {
-    pdl_wait();                                // h comes from K2a
-    if (S.on) stage_build_and_wait<W13>(p, S);
+    pdl_wait();                                // h comes from hfin (after K2a)
+    if (S.on) stage_h_bulk_and_wait(p, S);
   }
   if (first) HB_TL(W13, (threadIdx.x >> 5) * gridDim.x + blockIdx.x, 2);
 
   // ---- lane constants: B-operand rows, outputs of the lane's two slots
   const int xg = min(g, ns - 1);
   const int z0 = min(2 * t, ns - 1), z1 = min(2 * t + 1, ns - 1);
-  auto row_of = [&](int s) -> int {          // stage row: token (x) or slot (h)
+  auto row_of = [&](int s) -> int {          // token (x) or slot (h) of vjob slot s
     const int sl = vj.slot0 + s;
     return W13 ? p.jt.slot_token[sl] : sl;
   };
@@ -496,11 +521,11 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
       gz1 = p.hsum + (size_t)row_of(z1) * (K / 32);
     }
   }
-  const uint32_t sxb = S.xst + (uint32_t)row_of(xg) * K * 2 + t * 16;
+  const uint32_t sxb = S.xst + (uint32_t)(row_of(xg) - S.row0) * K * 2 + t * 16;
   const uint32_t sxl = sxb + (uint32_t)S.nrows * K * 2;
   const uint32_t szb = S.xst + (uint32_t)XS * S.nrows * K * 2;
-  const uint32_t sz0 = szb + (uint32_t)row_of(z0) * (K / 32) * 4;
-  const uint32_t sz1 = szb + (uint32_t)row_of(z1) * (K / 32) * 4;
+  const uint32_t sz0 = szb + (uint32_t)(row_of(z0) - S.row0) * (K / 32) * 4;
+  const uint32_t sz1 = szb + (uint32_t)(row_of(z1) - S.row0) * (K / 32) * 4;
   // output targets of the lane's slots 2t, 2t+1 (K2a: a/u rows; K2b: y rows, gate)
   const bool v0 = 2 * t < ns, v1 = 2 * t + 1 < ns;
   float* out0;
@@ -644,34 +669,67 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   const int nslots = __ldcg(p.jt.hdr + 1);
   constexpr int XS = W13 ? 1 : 2;
   const int K = W13 ? p.H : p.F;
-  // ---- CTA stage of the B operand (all rows: tokens for x, slots for h)
+  // stage hand-off: K2a every thread arrives after its share of the x copy;
+  // K2b thread 0 arrives once with the bulk copies' transaction count
+  if (threadIdx.x == 0) mbar_init(smem_u32(&s_bar), W13 ? blockDim.x : 1);
+  __syncthreads();
+  if (nv == 0) return;                       // nothing owned: y stays zero (router)
+  const int U = s_cum[nv];
+  // ---- the space this CTA works in.  K2a: all units, B operand = x of all
+  // tokens.  K2b with h in shared memory: the CTAs are split into one group
+  // per vjob (sizes proportional to its units, >= 1 CTA each), so a CTA
+  // stages h of its vjob's slots only (59 KB per slot at F = 14336) and
+  // keeps a deeper weight ring; its warps' feed covers that vjob alone.
   Stage S;
   S.ptr = gemv_smem + kGemvWarps * KCfg<W13>::RING;
   S.xst = smem_u32(S.ptr);
   S.bar = smem_u32(&s_bar);
-  S.nrows = W13 ? p.B : nslots;
-  const size_t stage_bytes = (size_t)S.nrows * (XS * K * 2 + (K / 32) * 4);
-  S.on = W13 ? stage_bytes <= (size_t)KCfg<W13>::XSTAGE : !p.h_global;
-  if (threadIdx.x == 0) mbar_init(S.bar, blockDim.x);
-  __syncthreads();
-  if (nv == 0) return;                       // nothing owned: y stays zero (router)
+  int base = 0, Usp = U, ncta = gridDim.x, cta = blockIdx.x, vsp = -1;
+  if constexpr (W13) {
+    S.row0 = 0;
+    S.nrows = p.B;
+    S.on = (size_t)S.nrows * (XS * K * 2 + (K / 32) * 4) <= (size_t)KCfg<W13>::XSTAGE;
+  } else {
+    S.on = !p.h_global;
+    S.row0 = 0;
+    S.nrows = nslots;
+    if (S.on) {
+      // group of vjob v: CTAs [c0(v), c0(v+1)), c0(v) = v + floor(cum[v] (n - nv) / U)
+      const int spare = (int)gridDim.x - nv;
+      auto c0 = [&](int v) { return v + (int)((long long)s_cum[v] * spare / U); };
+      int lo = 0, hi = nv - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (c0(mid) <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+      }
+      vsp = lo;
+      base = s_cum[lo];
+      Usp = s_cum[lo + 1] - base;
+      cta = blockIdx.x - c0(lo);
+      ncta = (lo + 1 < nv ? c0(lo + 1) : (int)gridDim.x) - c0(lo);
+      const VJobD d = p.jt.vjobs[lo];
+      S.row0 = d.slot0;
+      S.nrows = d.nslot;
+    }
+  }
   if (threadIdx.x == 0) {
-    const int U = s_cum[nv];
-    s_fk.U = U;
-    s_fk.S = min(U, (int)((double)U * p.static_frac));
+    s_fk.base = base;
+    s_fk.U = Usp;
+    s_fk.S = min(Usp, (int)((double)Usp * p.static_frac));
     s_fk.chunk = p.chunk;
-    s_fk.nch = (U - s_fk.S + p.chunk - 1) / p.chunk;
-    s_fk.nwarps = gridDim.x * kGemvWarps;
-    s_fk.ctr = p.ctr + (W13 ? 0 : 1);
+    s_fk.nch = (Usp - s_fk.S + p.chunk - 1) / p.chunk;
+    s_fk.nwarps = ncta * kGemvWarps;
+    s_fk.ctr = W13 ? p.ctr : p.ctr + 1 + (vsp < 0 ? 0 : 1 + vsp);
   }
   __syncthreads();
   Feed fd;
   fd.k = &s_fk;
   fd.done = false;
-  // static ranges are dealt SM-interleaved (gw = warp * #CTAs + CTA):
-  // consecutive ranges (same job, same encoding) land on different SMs
-  fd.a = (int)((long long)s_fk.S * gw / s_fk.nwarps);
-  fd.b = (int)((long long)s_fk.S * (gw + 1) / s_fk.nwarps);
+  // static ranges are dealt SM-interleaved (warp * #CTAs + CTA): consecutive
+  // ranges (same job, same encoding) land on different SMs
+  const int gwl = warp * ncta + cta;
+  fd.a = base + (int)((long long)s_fk.S * gwl / s_fk.nwarps);
+  fd.b = base + (int)((long long)s_fk.S * (gwl + 1) / s_fk.nwarps);
   fd.prefetch();
   const uint32_t ring = smem_u32(gemv_smem) + warp * KCfg<W13>::RING;
   uint2* meta = s_meta[warp];
@@ -700,28 +758,63 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
 #undef HB_RUN
     first = false;
   }
-  if (first && S.on) {                       // no units at all: still build the stage share
-    if constexpr (!W13) pdl_wait();
-    stage_build_and_wait<W13>(p, S);
+  if (first && S.on) {                       // no units at all: still take part in the stage
+    if constexpr (W13) {
+      stage_build_and_wait<W13>(p, S);
+    } else {
+      pdl_wait();
+      stage_h_bulk_and_wait(p, S);
+    }
   }
   HB_TL(W13, gw, 3);
 }
 
-// h in global memory for K2b launches whose stage would not fit (large batch):
-// one thread per (slot, 32-row block)
-__global__ void hfin_kernel(const __grid_constant__ GemvParams p) {
+// hfin: h = silu(a) * u of every slot from the K2a sums, as the fp16 hi/lo
+// pair-permuted rows + block sums K2b reads (staged per CTA group by bulk
+// copies, or straight from global memory at large batch).  Four threads per
+// (slot, 32-row block): thread t owns the 16-byte chunk t of hi and lo, i.e.
+// rows 8t..8t+7 (short dependency chains: this kernel sits between K2a and
+// K2b on every layer's critical path).
+__global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvParams p) {
+  pdl_trigger();                             // K2b may launch and prefetch its weights
+  pdl_wait();                                // the K2a sums
   const int nb = p.F / 32;
-  const int n = p.jt.hdr[1] * nb;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int s = i / nb, j = i - s * nb;
-    uint4 hi[4], lo[4];
-    const float hs = h_block(p.au, p.F, s, j, hi, lo);
+  const int n = __ldcg(p.jt.hdr + 1) * nb * 4;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ((n + 31) & ~31)) return;
+  const bool act = i < n;
+  const int q = act ? i : 0;
+  const int item = q >> 2, t = q & 3;
+  const int s = item / nb, j = item - s * nb;
+  const float* pa = p.au + (size_t)s * 2 * p.F + (size_t)j * 32 + 8 * t;
+  const float* pu = pa + p.F;
+  const float4 a0 = __ldcg(reinterpret_cast<const float4*>(pa));
+  const float4 a1 = __ldcg(reinterpret_cast<const float4*>(pa) + 1);
+  const float4 u0 = __ldcg(reinterpret_cast<const float4*>(pu));
+  const float4 u1 = __ldcg(reinterpret_cast<const float4*>(pu) + 1);
+  const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+  const float uv[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+  float h[8], hs = 0.f;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      p.h_hi[(size_t)s * (p.F / 8) + j * 4 + t] = hi[t];
-      p.h_lo[(size_t)s * (p.F / 8) + j * 4 + t] = lo[t];
-    }
-    p.hsum[i] = hs;
+  for (int r = 0; r < 8; ++r) {
+    h[r] = av[r] / (1.f + expf(-av[r])) * uv[r];
+    hs += h[r];
+  }
+  uint32_t wh[4], wl[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {              // Q_c = (h[8t+c], h[8t+c+4])
+    const __half h0 = __float2half_rn(h[c]), h1 = __float2half_rn(h[c + 4]);
+    const __half l0 = __float2half_rn(h[c] - __half2float(h0));
+    const __half l1 = __float2half_rn(h[c + 4] - __half2float(h1));
+    wh[c] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+    wl[c] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+  }
+  hs += __shfl_xor_sync(0xffffffffu, hs, 1);
+  hs += __shfl_xor_sync(0xffffffffu, hs, 2);
+  if (act) {
+    p.h_hi[(size_t)s * (p.F / 8) + j * 4 + t] = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+    p.h_lo[(size_t)s * (p.F / 8) + j * 4 + t] = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+    if (t == 0) p.hsum[item] = hs;
   }
 }
 
@@ -740,8 +833,8 @@ void launch_w13(const GemvParams& p, cudaStream_t s) {
   launch_pdl(gemv_kernel<true>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
 }
 void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
-  const int n = max_slots * (p.F / 32);
-  hfin_kernel<<<(n + 255) / 256, 256, 0, s>>>(p);
+  const int n = max_slots * (p.F / 32) * 4;
+  launch_pdl(hfin_kernel, (n + 255) / 256, 256, 0, s, p);
 }
 void launch_w2(const GemvParams& p, cudaStream_t s) {
   static bool d = false;

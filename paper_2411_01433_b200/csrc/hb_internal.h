@@ -19,7 +19,7 @@ constexpr int kNumSM = 148;             // B200
 #define HB_WARP_SMEM_KB 13
 #endif
 constexpr int kGemvWarps = HB_GEMV_WARPS;   // warps per GEMV CTA (one CTA per SM)
-constexpr int kRouterThreads = 256;
+constexpr int kRouterThreads = 512;
 
 // Byte offsets of the sections of one matrix inside an expert blob.
 // Tile-major layout: unit (tile of 16 rows, 64-byte group) = 1 KB of codes at
@@ -141,7 +141,7 @@ struct GemvParams {
                                        // instead of building it in shared memory per CTA
   float* y;                            // [B][H] (zeroed by router)
   // work feed: a static share of the units, then dynamic chunks (K2)
-  unsigned* ctr;                       // chunk counter of this kernel (self-resetting)
+  unsigned* ctr;                       // chunk counters: [0] K2a, [1] K2b, [2 + v] K2b group of vjob v
   int max_vjobs;                       // table entries to preload (>= n_vjobs + 1)
   float static_frac;                   // fraction of units dealt as static warp ranges
   int chunk;                           // units per dynamic chunk

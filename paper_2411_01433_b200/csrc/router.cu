@@ -170,6 +170,43 @@ __device__ void topk_warp(const RouterParams& p, const i128* L, int* sel) {
   }
 }
 
+// O3-O6 for top-2 routing (the paper's models) by one warp, shortest
+// dependency chain: lane e ranks its logit against all E in parallel (same
+// order as decide(): L desc, index asc), the two winners come from ballots,
+// the decision is the exact integer gap test and the two gates follow from
+// one exp: g0 = 1 / (1 + exp(l1 - l0)), g1 = 1 - g0 (fp64, as decide()).
+__device__ void decide_k2_warp(const RouterParams& p, const i128* L, int b, hb_decision* out,
+                               hb_decision* out_s) {
+  const int lane = threadIdx.x & 31;
+  int rank = 2;
+  if (lane < p.E) {
+    const i128 v = L[lane];
+    rank = 0;
+    for (int e = 0; e < p.E; ++e) {
+      const i128 o = L[e];
+      rank += (o > v) || (o == v && e < lane);
+    }
+  }
+  const unsigned m0 = __ballot_sync(0xffffffffu, rank == 0);
+  const unsigned m1 = __ballot_sync(0xffffffffu, rank == 1);
+  if (lane == 0) {
+    const int e0 = __ffs(m0) - 1, e1 = __ffs(m1) - 1;
+    const i128 G = L[e0] - L[e1];                  // >= 0
+    const uint8_t prec1 = gap_le(G, p.th1_kind, p.theta1) ? HB_HIGH
+                        : gap_le(G, p.th2_kind, p.theta2) ? HB_LOW : HB_SKIP;
+    const double d = G >= ((i128)1 << 62) ? 1e300 : (double)(long long)G * 0x1p-48;
+    const double ex = exp(-d);
+    const double g0 = 1.0 / (1.0 + ex), g1 = ex / (1.0 + ex);
+    hb_decision r0, r1;
+    r0.token = b; r0.expert = e0; r0.sel_rank = 0; r0.prec = HB_HIGH;
+    r0.served_enc = HB_ENC_NONE; r0.hit = 0; r0.gate = (float)g0;
+    r1.token = b; r1.expert = e1; r1.sel_rank = 1; r1.prec = prec1;
+    r1.served_enc = HB_ENC_NONE; r1.hit = 0; r1.gate = (float)g1;
+    out[0] = r0; out[1] = r1;
+    out_s[0] = r0; out_s[1] = r1;
+  }
+}
+
 constexpr int kMaxDecSmem = 512;
 constexpr int kRouterCluster = 8;      // CTAs (SMs) per (route layer, token) row       // route-0 decisions kept in shared memory
 
@@ -248,7 +285,7 @@ __device__ void build_jobs_warp(const RouterParams& p, RouterSmem& sm, const hb_
   }
   const bool valid = key != kNone;
   int less = 0, rank = 0, ntok = 0;
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < nsel; ++j) {
     const int kj = __shfl_sync(0xffffffffu, key, j);
     less += kj != kNone && kj < key;
     ntok += kj == key;
@@ -256,7 +293,7 @@ __device__ void build_jobs_warp(const RouterParams& p, RouterSmem& sm, const hb_
   }
   const bool first = valid && rank == 0;
   int jid = 0;
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < nsel; ++j) {
     const int kj = __shfl_sync(0xffffffffu, key, j);
     const int fj = __shfl_sync(0xffffffffu, (int)first, j);
     jid += fj && kj < key;
@@ -449,9 +486,13 @@ router_kernel(const __grid_constant__ RouterParams p) {
   // ---- single (route layer, token): decide and build the jobs right here
   if (nrows == 1) {
     if (warp == 0) {
-      int sel[kMaxTopK];
-      topk_warp(p, sm.L, sel);
-      if (lane == 0) decide_sel(p, sm.L, sel, b, p.dec, sm.dec);
+      if (p.k == 2 && p.E <= 32) {
+        decide_k2_warp(p, sm.L, b, p.dec, sm.dec);
+      } else {
+        int sel[kMaxTopK];
+        topk_warp(p, sm.L, sel);
+        if (lane == 0) decide_sel(p, sm.L, sel, b, p.dec, sm.dec);
+      }
       __syncwarp();
       HB_RTL(5);
       if (p.blob_table) {

@@ -40,6 +40,7 @@ def main():
     rfn.argtypes = [ctypes.c_void_p]
     rbuf = np.zeros(8, dtype=np.uint64)
     rrows = []
+    lay = []
     for t in range(4):
         for l in range(0, shape.n_layers, 4):
             x = torch.from_numpy(sg.hidden_states(shape, 1000 + t, l)).cuda()
@@ -49,6 +50,15 @@ def main():
             assert rfn(rbuf.ctypes.data) == 0
             rb = rbuf.astype(np.int64)
             rrows.append((rb[1:8] - rb[0]) / 1000.0)
+            # absolute layer timeline relative to router entry
+            ab = []
+            for k in (0, 1):
+                assert fn(buf.ctypes.data, k) == 0
+                bk = buf.astype(np.int64)
+                act = bk[:, 3] > 0
+                ab.append(((bk[:, 0].min() - rb[0]) / 1e3, (np.median(bk[act, 2]) - rb[0]) / 1e3,
+                           (bk[act, 3].max() - rb[0]) / 1e3))
+            lay.append([(rb[6] - rb[0]) / 1e3, *ab[0], *ab[1]])
             for k in (0, 1):
                 assert fn(buf.ctypes.data, k) == 0
                 b = buf.astype(np.int64)
@@ -66,6 +76,8 @@ def main():
     np.set_printoptions(suppress=True, linewidth=200)
     print("router stamps (us after entry: wait, partial, combine, -, decide, jobs, warm decide+jobs):",
           np.median(np.array(rrows), axis=0).round(2))
+    print("layer (us from router entry): router_end | K2a entry, first-run med, end | "
+          "K2b entry, first-run med, end:", np.median(np.array(lay), axis=0).round(2))
     for k, name in ((0, "K2a"), (1, "K2b")):
         a = np.array(rows[k])
         print(f"{model} {pair} {name}: entry_max {np.median(a[:,0]):.2f}  stage med/max "
