@@ -87,7 +87,8 @@ struct hb_ctx {
   void* jt_host = nullptr;                // pinned staging
   size_t jt_bytes = 0;
   int max_jobs = 0, max_slots = 0, max_vjobs = 0;
-  float static_frac = 0.6f;               // GEMV work feed (HB_STATIC_FRAC, HB_CHUNK)
+  float static_frac = 0.7f;               // GEMV work feed K2a (HB_STATIC_FRAC, HB_CHUNK)
+  float static_frac2 = 0.9f;              // K2b (HB_STATIC_FRAC2)
   int chunk = 8;
   cudaEvent_t dec_ready = nullptr;
   // kernel timing (hb_profile)
@@ -262,8 +263,10 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     c->force_h_global = fh && fh[0] == '1';
     const char* sf = std::getenv("HB_STATIC_FRAC");
     if (sf) c->static_frac = std::min(1.0f, std::max(0.0f, (float)std::atof(sf)));
+    const char* sf2 = std::getenv("HB_STATIC_FRAC2");
+    if (sf2) c->static_frac2 = std::min(1.0f, std::max(0.0f, (float)std::atof(sf2)));
     const char* ch = std::getenv("HB_CHUNK");
-    if (ch) c->chunk = std::max(1, std::atoi(ch));
+    if (ch) c->chunk = (std::max(2, std::atoi(ch)) + 1) & ~1;   // even: K2b stages hold 2 units
   }
   cudaMemset(c->done, 0, 16);
   cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + kMaxVJobs));
@@ -432,18 +435,24 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
   g.h_lo = c->h_lo;
   g.hsum = c->hsum;
   // K2b builds h in each CTA's shared memory when every possible slot fits
-  // K2b builds h in shared memory per CTA group (one group per vjob) when the
-  // slots of any vjob fit its stage and every vjob can get a CTA
-  const size_t slot_bytes = (size_t)k.ffn * 2 * 2 + (size_t)(k.ffn / 32) * 4;
+  // K2b stages one column slice of h per CTA group (one group per vjob and
+  // slice; 2 slices when a slice has an even number of groups) when the slots
+  // of any vjob fit the stage and every sub-space can get a CTA
   const int max_ns = std::min(kVSlots, batch);
   const int nv_bound = std::min(2 * k.n_experts, batch * k.top_k) +
                        (batch * k.top_k + kVSlots - 1) / kVSlots;
-  g.h_global = c->force_h_global || (size_t)max_ns * slot_bytes > (size_t)w2_stage_capacity() ||
-               nv_bound > kGemvCTAs;
+  bool fits = true;
+  for (int enc : {k.hi_enc, k.lo_enc}) {
+    const int G = k.ffn / epg_of_enc(enc), nh = G % 4 == 0 ? 2 : 1;
+    const size_t slice = (size_t)(k.ffn / nh) * 4 + (size_t)(k.ffn / nh / 32) * 4;
+    fits = fits && (size_t)max_ns * slice <= (size_t)w2_stage_capacity();
+  }
+  g.h_global = c->force_h_global || !fits || 2 * nv_bound > kGemvCTAs;
   g.y = (float*)y;
   g.ctr = c->gctr;
   g.max_vjobs = c->max_vjobs;
   g.static_frac = c->static_frac;
+  g.static_frac2 = c->static_frac2;
   g.chunk = c->chunk;
   return g;
 }

@@ -66,8 +66,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 __device__ __forceinline__ void cp_async16_ef(uint32_t dst, const void* src, uint64_t pol) {
+#ifdef HB_NO_EVICT_HINT
+  (void)pol;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src));
+#else
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
                :: "r"(dst), "l"(src), "l"(pol));
+#endif
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src));
@@ -85,6 +90,10 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+// fire-and-forget fp32 add into global memory (no generic-address fallback)
+__device__ __forceinline__ void red_add(float* a, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(v) : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 r;
@@ -105,6 +114,10 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
+#ifdef HB_DBG_NOMMA
+  d[0] += __uint_as_float((a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1) & 0x3F800000u);
+  return;
+#endif
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
@@ -172,21 +185,24 @@ template <> struct KCfg<true> {        // K2a: x is small (8 KB per token at H=4
   static constexpr int RING = 16 * 12 * 1024 / kGemvWarps / 128 * 128;
   static constexpr int XSTAGE = 28 * 1024;  // 3 tokens at H = 4096
 };
-template <> struct KCfg<false> {       // K2b: h of one slot is 59 KB at F=14336
-  static constexpr int RING = 16 * 10240 / kGemvWarps / 128 * 128;
-  static constexpr int XSTAGE = 60 * 1024;  // 1 slot at F = 14336 (59136 B), 2 at F = 6400
+template <> struct KCfg<false> {       // K2b: h of one slot, half the columns: 29.6 KB at F=14336
+  static constexpr int RING = 16 * 12288 / kGemvWarps / 128 * 128;
+  static constexpr int XSTAGE = 30 * 1024;
 };
 template <bool W13>
 constexpr int gemv_smem_bytes() { return kGemvWarps * KCfg<W13>::RING + KCfg<W13>::XSTAGE; }
 
 // Ring stage layout of one unit: W codes | S scales
-template <int ENC, int NMAT, int RINGB>
+template <int ENC, int NMAT, int NU, int RINGB>
 struct Ring {
   static constexpr int BPG = Enc<ENC>::BPG, SB = Enc<ENC>::SB;
-  static constexpr int W = NMAT * 1024;
-  static constexpr int S = NMAT * 16 * SB;
+  static constexpr int W = NMAT * NU * 1024;          // NU consecutive units per stage
+  static constexpr int S = NMAT * NU * 16 * SB;
   static constexpr int STAGE = (W + S + 127) / 128 * 128;
-  static constexpr int DEPTH = RINGB / STAGE >= 16 ? 16 : RINGB / STAGE;
+#ifndef HB_MAX_DEPTH
+#define HB_MAX_DEPTH 16
+#endif
+  static constexpr int DEPTH = RINGB / STAGE >= HB_MAX_DEPTH ? HB_MAX_DEPTH : RINGB / STAGE;
   static_assert(DEPTH >= 2, "ring too small");
 };
 
@@ -325,6 +341,8 @@ struct Stage {
   uint32_t bar;      // mbarrier (count = blockDim.x)
   int row0;          // first staged row (token for x, slot for h)
   int nrows;
+  int kcols;         // columns staged per row (K2b: one column slice of h)
+  int nh, hs;        // K2b: column slices of the vjob, this CTA's slice
   bool on;           // B operand read from the stage (else from global memory)
 };
 
@@ -333,18 +351,23 @@ struct Stage {
 // waits on the mbarrier's transaction count.
 __device__ __forceinline__ void stage_h_bulk_and_wait(const GemvParams& p, const Stage& S) {
   if (threadIdx.x == 0) {
-    const uint32_t nh = (uint32_t)S.nrows * p.F * 2, nz = (uint32_t)S.nrows * (p.F / 32) * 4;
+    const uint32_t rh = (uint32_t)S.kcols * 2, rz = (uint32_t)(S.kcols / 32) * 4;
+    const uint32_t nh = S.nrows * rh;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                 :: "r"(S.bar), "r"(2 * nh + nz) : "memory");
-    const char* src[3] = {reinterpret_cast<const char*>(p.h_hi + (size_t)S.row0 * (p.F / 8)),
-                          reinterpret_cast<const char*>(p.h_lo + (size_t)S.row0 * (p.F / 8)),
-                          reinterpret_cast<const char*>(p.hsum + (size_t)S.row0 * (p.F / 32))};
-    const uint32_t off[3] = {0u, nh, 2 * nh}, len[3] = {nh, nh, nz};
+                 :: "r"(S.bar), "r"(S.nrows * (2 * rh + rz)) : "memory");
+    for (int r = 0; r < S.nrows; ++r) {
+      const size_t row = (size_t)(S.row0 + r);
+      const char* src[3] = {
+          reinterpret_cast<const char*>(p.h_hi) + row * p.F * 2 + (size_t)S.hs * rh,
+          reinterpret_cast<const char*>(p.h_lo) + row * p.F * 2 + (size_t)S.hs * rh,
+          reinterpret_cast<const char*>(p.hsum) + row * (p.F / 32) * 4 + (size_t)S.hs * rz};
+      const uint32_t dst[3] = {r * rh, nh + r * rh, 2 * nh + r * rz}, len[3] = {rh, rh, rz};
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-          :: "r"(S.xst + off[i]), "l"(src[i]), "r"(len[i]), "r"(S.bar) : "memory");
+      for (int i = 0; i < 3; ++i)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            :: "r"(S.xst + dst[i]), "l"(src[i]), "r"(len[i]), "r"(S.bar) : "memory");
+    }
   }
   mbar_wait(S.bar, 0);
 }
@@ -429,15 +452,23 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
   constexpr int NMAT = W13 ? 2 : 1;
   constexpr bool SPLIT = !W13;
   constexpr int XS = SPLIT ? 2 : 1;
-  using R = Ring<ENC, NMAT, KCfg<W13>::RING>;
+  // K2b streams two units (2 KB) per ring stage: half the per-stage overhead
+  // and two independent MMA chains per iteration (K2b is issue-bound); K2a's
+  // 2-matrix units are already 2 KB
+  constexpr int NU = (!W13 && XR) ? 2 : 1;
+  using R = Ring<ENC, NMAT, NU, KCfg<W13>::RING>;
   constexpr int BPG = R::BPG, SB = R::SB, DEPTH = R::DEPTH;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const bool lane0 = lane == 0;
   const int K = W13 ? p.H : p.F;
   const int G = K / Enc<ENC>::EPG;
+  // K2b with a staged column slice: the space covers groups [goff, goff + Gs)
+  // of every tile (Gs even, so a stage's NU = 2 units never straddle tiles)
+  const int Gs = (!W13 && XR) ? G / S.nh : G;
+  const int goff = (!W13 && XR) ? S.hs * Gs : 0;
   const uint64_t pol = evict_first_policy();
   // tile-major blobs: unit l (tile l/G, group l%G) = 1 KB of codes at q + 1024*l,
   // its 16 scale records at s + 16*SB*l -- a segment is one contiguous span
-  const bool s_act = lane < SB;               // 16*SB bytes of scales per unit = SB lanes x 16 B
   const int ns = vj.nslot;
 
   // ---- producer: weights + scales
@@ -452,13 +483,14 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
     pl = fd.a - cum;
     pe = min(fd.b, cum + Uv) - cum;
     fd.a = cum + pe;                           // a remainder past the vjob stays in the feed
-    ptile = pl / G;
-    pgrp = pl - ptile * G;
+    ptile = pl / Gs;
+    pgrp = pl - ptile * Gs;
+    const size_t u = (size_t)ptile * G + goff + pgrp;      // unit in the blob
 #pragma unroll
     for (int m = 0; m < NMAT; ++m) {
       const MatLayout& L = p.lay[ENC].mat[W13 ? m : 2];
-      qp[m] = vj.blob + L.q + (size_t)pl * 1024 + 16 * lane;
-      sp_[m] = vj.blob + L.s + (size_t)pl * 16 * SB + 16 * lane;
+      qp[m] = vj.blob + L.q + u * 1024 + 16 * lane;
+      sp_[m] = vj.blob + L.s + u * 16 * SB + 16 * lane;
     }
     return true;
   };
@@ -467,19 +499,32 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
     if (pactive) {
       const uint32_t st = ring + pslot * R::STAGE;
 #pragma unroll
-      for (int m = 0; m < NMAT; ++m) {                 // 2 x 512 contiguous bytes
-        cp_async16_ef(st + m * 1024 + 16 * lane, qp[m], pol);
-        cp_async16_ef(st + m * 1024 + 512 + 16 * lane, qp[m] + 512, pol);
-        if constexpr (SB > 0)
-          if (s_act) cp_async16_ef(st + R::W + m * 16 * SB + 16 * lane, sp_[m], pol);
-      }
-      const bool flush = pgrp == G - 1 || pl + 1 == pe;   // last unit of a tile piece
-      if (lane == 0) meta[pslot] = make_uint2((uint32_t)ptile, (uint32_t)pgrp | (flush ? 0x80000000u : 0u));
-      ++pl;
+      for (int m = 0; m < NMAT; ++m) {                 // NU x 1 KB contiguous per matrix
 #pragma unroll
-      for (int m = 0; m < NMAT; ++m) { qp[m] += 1024; sp_[m] += 16 * SB; }
-      if (++pgrp == G) { pgrp = 0; ++ptile; }
-      if (++pslot == DEPTH) pslot = 0;
+        for (int i = 0; i < 2 * NU; ++i)
+          cp_async16_ef(st + m * NU * 1024 + 512 * i + 16 * lane, qp[m] + 512 * i, pol);
+        if constexpr (SB > 0) {
+#pragma unroll
+          for (int o = 0; o < NU * 16 * SB; o += 512)
+            if (o + 16 * lane < NU * 16 * SB)
+              cp_async16_ef(st + R::W + m * NU * 16 * SB + o + 16 * lane, sp_[m] + o, pol);
+        }
+      }
+      // meta: tile / group of the stage's first unit; bit 30 + u: unit u ends a
+      // tile piece (tile end, or segment end).  Segments and Gs are multiples
+      // of NU, so only the stage's last unit can end a piece.
+      pl += NU;
+      pgrp += NU;
+      const bool endp = pgrp == Gs || pl == pe;
+      if (lane0) meta[pslot] = make_uint2((uint32_t)ptile, (uint32_t)(pgrp - NU) | (endp ? 1u << (29 + NU) : 0u));
+      int skip = 0;
+      if (pgrp == Gs) { pgrp = 0; ++ptile; skip = G - Gs; }  // next tile's slice
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) {
+        qp[m] += (size_t)(NU + skip) * 1024;
+        sp_[m] += (size_t)(NU + skip) * 16 * SB;
+      }
+      pslot = pslot + 1 == DEPTH ? 0 : pslot + 1;
       ++iss;
     }
     cp_commit();
@@ -521,11 +566,12 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
       gz1 = p.hsum + (size_t)row_of(z1) * (K / 32);
     }
   }
-  const uint32_t sxb = S.xst + (uint32_t)(row_of(xg) - S.row0) * K * 2 + t * 16;
-  const uint32_t sxl = sxb + (uint32_t)S.nrows * K * 2;
-  const uint32_t szb = S.xst + (uint32_t)XS * S.nrows * K * 2;
-  const uint32_t sz0 = szb + (uint32_t)(row_of(z0) - S.row0) * (K / 32) * 4;
-  const uint32_t sz1 = szb + (uint32_t)(row_of(z1) - S.row0) * (K / 32) * 4;
+  const int KC = S.kcols;
+  const uint32_t sxb = S.xst + (uint32_t)(row_of(xg) - S.row0) * KC * 2 + t * 16;
+  const uint32_t sxl = sxb + (uint32_t)S.nrows * KC * 2;
+  const uint32_t szb = S.xst + (uint32_t)XS * S.nrows * KC * 2;
+  const uint32_t sz0 = szb + (uint32_t)(row_of(z0) - S.row0) * (KC / 32) * 4;
+  const uint32_t sz1 = szb + (uint32_t)(row_of(z1) - S.row0) * (KC / 32) * 4;
   // output targets of the lane's slots 2t, 2t+1 (K2a: a/u rows; K2b: y rows, gate)
   const bool v0 = 2 * t < ns, v1 = 2 * t + 1 < ns;
   float* out0;
@@ -548,24 +594,17 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
     for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
   int cslot = 0;
 
-  for (int con = 0; con < iss; ++con) {            // iss grows while the producer runs
-    __syncwarp();                                  // slot being refilled is consumed
-    issue();
-    cp_wait<DEPTH - 1>();
-    __syncwarp();                                  // everyone's copies of unit con visible
-    const uint2 md = meta[cslot];
-    const uint32_t st = ring + cslot * R::STAGE;
-    if (++cslot == DEPTH) cslot = 0;
-    const int c_tile = (int)md.x, c_grp = (int)(md.y & 0x7FFFFFFFu);
+  // dot products of one unit (codes at wst, scales at sst, group c_grp) into r
+  auto unit_dot = [&](uint32_t wst, uint32_t sst, int c_grp, float (&r)[NMAT][4]) {
     uint4 w[NMAT][2];
 #pragma unroll
     for (int m = 0; m < NMAT; ++m) {
-      w[m][0] = lds128(st + m * 1024 + g * 64 + 16 * t);
-      w[m][1] = lds128(st + m * 1024 + (g + 8) * 64 + 16 * t);
+      w[m][0] = lds128(wst + m * NU * 1024 + g * 64 + 16 * t);
+      w[m][1] = lds128(wst + m * NU * 1024 + (g + 8) * 64 + 16 * t);
     }
 #ifdef HB_DBG_NOCOMPUTE
-    acc[0][0] += __uint_as_float((w[0][0].x ^ w[0][1].y) & 0x3F800000u);
-    if (false)
+    r[0][0] += __uint_as_float((w[0][0].x ^ w[0][1].y) & 0x3F800000u);
+    return;
 #endif
 #pragma unroll
     for (int blk = 0; blk < BPG; ++blk) {
@@ -573,8 +612,13 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
       float s0 = 0.f, s1 = 0.f;
       if constexpr (XR) {
         const uint32_t gb = (uint32_t)(c_grp * BPG + blk);
+#ifdef HB_DBG_NOBLDS
+        xb = make_uint4(gb, gb + 1, gb + 2, gb + 3);
+        xl = xb;
+#else
         xb = lds128(sxb + gb * 64);
         if constexpr (SPLIT) xl = lds128(sxl + gb * 64);
+#endif
         if constexpr (ENC == HB_Q2) {
           s0 = lds_f32(sz0 + gb * 4);
           s1 = lds_f32(sz1 + gb * 4);
@@ -591,14 +635,14 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
         dequant<ENC>(w[m][0], blk, Pg);
         dequant<ENC>(w[m][1], blk, Ph);
         if constexpr (ENC == HB_F16) {
-          mma16816(acc[m], Pg[0], Ph[0], Pg[1], Ph[1], xb.x, xb.y);
-          mma16816(acc[m], Pg[2], Ph[2], Pg[3], Ph[3], xb.z, xb.w);
+          mma16816(r[m], Pg[0], Ph[0], Pg[1], Ph[1], xb.x, xb.y);
+          mma16816(r[m], Pg[2], Ph[2], Pg[3], Ph[3], xb.z, xb.w);
           if constexpr (SPLIT) {
-            mma16816(acc[m], Pg[0], Ph[0], Pg[1], Ph[1], xl.x, xl.y);
-            mma16816(acc[m], Pg[2], Ph[2], Pg[3], Ph[3], xl.z, xl.w);
+            mma16816(r[m], Pg[0], Ph[0], Pg[1], Ph[1], xl.x, xl.y);
+            mma16816(r[m], Pg[2], Ph[2], Pg[3], Ph[3], xl.z, xl.w);
           }
         } else {
-          const uint32_t sd = st + R::W + m * 16 * SB;
+          const uint32_t sd = sst + m * NU * 16 * SB;
           const float dg = lds_half(sd + g * SB + 2 * blk);
           const float dh = lds_half(sd + (g + 8) * SB + 2 * blk);
           float D[4] = {0.f, 0.f, 0.f, 0.f};
@@ -608,38 +652,74 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
             mma16816(D, Pg[0], Ph[0], Pg[1], Ph[1], xl.x, xl.y);
             mma16816(D, Pg[2], Ph[2], Pg[3], Ph[3], xl.z, xl.w);
           }
-          acc[m][0] = fmaf(dg, D[0], acc[m][0]);
-          acc[m][1] = fmaf(dg, D[1], acc[m][1]);
-          acc[m][2] = fmaf(dh, D[2], acc[m][2]);
-          acc[m][3] = fmaf(dh, D[3], acc[m][3]);
+          r[m][0] = fmaf(dg, D[0], r[m][0]);
+          r[m][1] = fmaf(dg, D[1], r[m][1]);
+          r[m][2] = fmaf(dh, D[2], r[m][2]);
+          r[m][3] = fmaf(dh, D[3], r[m][3]);
           if constexpr (ENC == HB_Q2) {               // + m_row * sum_block(x)
             const float mg = lds_half(sd + g * SB + 16 + 2 * blk);
             const float mh = lds_half(sd + (g + 8) * SB + 16 + 2 * blk);
-            acc[m][0] = fmaf(mg, s0, acc[m][0]);
-            acc[m][1] = fmaf(mg, s1, acc[m][1]);
-            acc[m][2] = fmaf(mh, s0, acc[m][2]);
-            acc[m][3] = fmaf(mh, s1, acc[m][3]);
+            r[m][0] = fmaf(mg, s0, r[m][0]);
+            r[m][1] = fmaf(mg, s1, r[m][1]);
+            r[m][2] = fmaf(mh, s0, r[m][2]);
+            r[m][3] = fmaf(mh, s1, r[m][3]);
           }
         }
       }
     }
-    // ---- end of a tile piece: add it into the output (fire-and-forget)
-    if (md.y & 0x80000000u) {
-      const int r0 = c_tile * 16 + g;
+  };
+  // end of a tile piece: add it into the output (fire-and-forget reductions)
+  auto flush = [&](int c_tile) {
+    const int r0 = c_tile * 16 + g;
 #pragma unroll
-      for (int m = 0; m < NMAT; ++m) {
-        const int off = W13 ? m * p.F + r0 : r0;
-        if (v0) {
-          atomicAdd(out0 + off, W13 ? acc[m][0] : gate0 * acc[m][0]);
-          atomicAdd(out0 + off + 8, W13 ? acc[m][2] : gate0 * acc[m][2]);
-        }
-        if (v1) {
-          atomicAdd(out1 + off, W13 ? acc[m][1] : gate1 * acc[m][1]);
-          atomicAdd(out1 + off + 8, W13 ? acc[m][3] : gate1 * acc[m][3]);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
+    for (int m = 0; m < NMAT; ++m) {
+      const int off = W13 ? m * p.F + r0 : r0;
+      if (v0) {
+        red_add(out0 + off, W13 ? acc[m][0] : gate0 * acc[m][0]);
+        red_add(out0 + off + 8, W13 ? acc[m][2] : gate0 * acc[m][2]);
       }
+      if (v1) {
+        red_add(out1 + off, W13 ? acc[m][1] : gate1 * acc[m][1]);
+        red_add(out1 + off + 8, W13 ? acc[m][3] : gate1 * acc[m][3]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
+    }
+  };
+
+  for (int con = 0; con < iss; ++con) {            // iss grows while the producer runs
+    __syncwarp();                                  // slot being refilled is consumed
+    issue();
+    cp_wait<DEPTH - 1>();
+    __syncwarp();                                  // everyone's copies of stage con visible
+    const uint2 md = meta[cslot];
+    const uint32_t st = ring + cslot * R::STAGE;
+    if (++cslot == DEPTH) cslot = 0;
+    if constexpr (NU == 1) {
+      unit_dot(st, st + R::W, (int)(md.y & 0x3FFFFFFFu), acc);
+      if (md.y & 0x40000000u) flush((int)md.x);
+    } else {
+      // two units: independent partial sums, then in order into acc with the
+      // piece boundaries between them
+      const int tile0 = (int)md.x, grp0 = (int)(md.y & 0x3FFFFFFFu);
+      const bool e0 = (md.y >> 30) & 1u, e1 = md.y >> 31;
+      float r0[NMAT][4], r1[NMAT][4];
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { r0[m][i] = 0.f; r1[m][i] = 0.f; }
+      unit_dot(st, st + R::W, grp0, r0);
+      unit_dot(st + 1024, st + R::W + 16 * SB, e0 ? 0 : grp0 + 1, r1);
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[m][i] += r0[m][i];
+      if (e0) flush(tile0);
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[m][i] += r1[m][i];
+      if (e1) flush(e0 ? tile0 + 1 : tile0);
     }
   }
   cp_wait<0>();
@@ -655,6 +735,9 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   __shared__ int s_cum[kMaxVJobs + 1];
   __shared__ uint2 s_meta[kGemvWarps][16];
   __shared__ FeedConst s_fk;
+  __shared__ int s_subb[kGemvCTAs + 1];         // K2b sub-space first units (+ total)
+  __shared__ int s_subvh[kGemvCTAs];            // vjob | slice << 16 | slices << 24
+  __shared__ int s_nsub;
   const int warp = threadIdx.x >> 5;
   const int gw = warp * gridDim.x + blockIdx.x;
   HB_TL(W13, gw, 0);
@@ -669,6 +752,7 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   const int nslots = __ldcg(p.jt.hdr + 1);
   constexpr int XS = W13 ? 1 : 2;
   const int K = W13 ? p.H : p.F;
+  const bool part = !W13 && !p.h_global;     // K2b CTA groups per (vjob, column slice)
   // stage hand-off: K2a every thread arrives after its share of the x copy;
   // K2b thread 0 arrives once with the bulk copies' transaction count
   if (threadIdx.x == 0) mbar_init(smem_u32(&s_bar), W13 ? blockDim.x : 1);
@@ -685,37 +769,67 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   S.xst = smem_u32(S.ptr);
   S.bar = smem_u32(&s_bar);
   int base = 0, Usp = U, ncta = gridDim.x, cta = blockIdx.x, vsp = -1;
+  S.nh = 1;
+  S.hs = 0;
   if constexpr (W13) {
     S.row0 = 0;
     S.nrows = p.B;
+    S.kcols = K;
     S.on = (size_t)S.nrows * (XS * K * 2 + (K / 32) * 4) <= (size_t)KCfg<W13>::XSTAGE;
   } else {
-    S.on = !p.h_global;
+    S.on = false;
     S.row0 = 0;
     S.nrows = nslots;
-    if (S.on) {
-      // group of vjob v: CTAs [c0(v), c0(v+1)), c0(v) = v + floor(cum[v] (n - nv) / U)
-      const int spare = (int)gridDim.x - nv;
-      auto c0 = [&](int v) { return v + (int)((long long)s_cum[v] * spare / U); };
-      int lo = 0, hi = nv - 1;
+    S.kcols = K;
+    if (part) {
+      // sub-spaces (vjob v, column slice h < nh(v)), nh = 2 when the slice has
+      // an even number of groups; CTAs [c0(q), c0(q+1)) work on sub-space q,
+      // c0(q) = q + floor(first unit of q * (n - nsub) / U)
+      if (threadIdx.x == 0) {
+        int q = 0;
+        for (int v = 0; v < nv; ++v) {
+          const int G = K / epg_of(__ldcg(&p.jt.vjobs[v].enc));
+          const int nh = (G % 4 == 0) ? 2 : 1;
+          const int uq = (s_cum[v + 1] - s_cum[v]) / nh;
+          for (int h = 0; h < nh; ++h, ++q) {
+            s_subvh[q] = v | (h << 16) | (nh << 24);
+            s_subb[q] = s_cum[v] + h * uq;
+          }
+        }
+        s_subb[q] = U;
+        s_nsub = q;
+      }
+      __syncthreads();
+      const int nsub = s_nsub;
+      const int spare = (int)gridDim.x - nsub;
+      auto c0 = [&](int q) { return q + (int)((long long)s_subb[q] * spare / U); };
+      int lo = 0, hi = nsub - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (c0(mid) <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
       }
+      const int v = s_subvh[lo] & 0xFFFF;
       vsp = lo;
-      base = s_cum[lo];
-      Usp = s_cum[lo + 1] - base;
+      base = s_subb[lo];
+      Usp = s_subb[lo + 1] - base;
       cta = blockIdx.x - c0(lo);
-      ncta = (lo + 1 < nv ? c0(lo + 1) : (int)gridDim.x) - c0(lo);
-      const VJobD d = p.jt.vjobs[lo];
+      ncta = (lo + 1 < nsub ? c0(lo + 1) : (int)gridDim.x) - c0(lo);
+      const VJobD d = p.jt.vjobs[v];
       S.row0 = d.slot0;
       S.nrows = d.nslot;
+      S.nh = s_subvh[lo] >> 24;
+      S.hs = (s_subvh[lo] >> 16) & 0xFF;
+      S.kcols = K / S.nh;
+      // staged (2 units per ring stage) when the slice has an even number of
+      // groups; otherwise this group reads h from global memory
+      S.on = (K / epg_of(d.enc) / S.nh) % 2 == 0;
     }
   }
+  const int KNU = (!W13 && S.on) ? 2 : 1;    // units per ring stage (segments KNU-aligned)
   if (threadIdx.x == 0) {
     s_fk.base = base;
     s_fk.U = Usp;
-    s_fk.S = min(Usp, (int)((double)Usp * p.static_frac));
+    s_fk.S = min(Usp, (int)((double)Usp * (W13 ? p.static_frac : p.static_frac2))) & ~(KNU - 1);
     s_fk.chunk = p.chunk;
     s_fk.nch = (Usp - s_fk.S + p.chunk - 1) / p.chunk;
     s_fk.nwarps = ncta * kGemvWarps;
@@ -728,22 +842,30 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   // static ranges are dealt SM-interleaved (warp * #CTAs + CTA): consecutive
   // ranges (same job, same encoding) land on different SMs
   const int gwl = warp * ncta + cta;
-  fd.a = base + (int)((long long)s_fk.S * gwl / s_fk.nwarps);
-  fd.b = base + (int)((long long)s_fk.S * (gwl + 1) / s_fk.nwarps);
+  fd.a = base + ((int)((long long)s_fk.S * gwl / s_fk.nwarps) & ~(KNU - 1));
+  fd.b = base + ((int)((long long)s_fk.S * (gwl + 1) / s_fk.nwarps) & ~(KNU - 1));
   fd.prefetch();
   const uint32_t ring = smem_u32(gemv_smem) + warp * KCfg<W13>::RING;
   uint2* meta = s_meta[warp];
   bool first = true;
   HB_TL(W13, gw, 1);
   while (fd.a < fd.b || fd.refill()) {
-    int lo = 0, hi = nv - 1;                   // vjob containing unit fd.a
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_cum[mid] <= fd.a) lo = mid; else hi = mid - 1;
+    int lo = 0, cv, Uv;
+    if (part) {                                // the CTA's sub-space (one vjob slice)
+      lo = s_subvh[vsp] & 0xFFFF;
+      cv = base;
+      Uv = Usp;
+    } else {
+      int hi = nv - 1;                         // vjob containing unit fd.a
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_cum[mid] <= fd.a) lo = mid; else hi = mid - 1;
+      }
+      cv = s_cum[lo];
+      Uv = s_cum[lo + 1] - cv;
     }
     const VJobD d = p.jt.vjobs[lo];
     const VJob vj{d.blob, d.enc, d.slot0, d.nslot};
-    const int cv = s_cum[lo], Uv = s_cum[lo + 1] - cv;
 #define HB_RUN(E, X) run<E, W13, X>(p, vj, cv, Uv, fd, ring, meta, S, first)
     switch (vj.enc * 2 + (S.on ? 1 : 0)) {
       case 2 * HB_F16 + 1: HB_RUN(HB_F16, true); break;

@@ -143,7 +143,8 @@ struct GemvParams {
   // work feed: a static share of the units, then dynamic chunks (K2)
   unsigned* ctr;                       // chunk counters: [0] K2a, [1] K2b, [2 + v] K2b group of vjob v
   int max_vjobs;                       // table entries to preload (>= n_vjobs + 1)
-  float static_frac;                   // fraction of units dealt as static warp ranges
+  float static_frac;                   // K2a: fraction of units dealt as static warp ranges
+  float static_frac2;                  // K2b
   int chunk;                           // units per dynamic chunk
 };
 

@@ -32,7 +32,7 @@
 namespace hb {
 
 #ifdef HB_DBG_TIMELINE
-__device__ unsigned long long g_rtl[8];
+__device__ unsigned long long g_rtl[16];
 #define HB_RTL(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) { unsigned long long t_; \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_rtl[i] = t_; } } while (0)
 #else
@@ -149,7 +149,7 @@ __device__ void decide(const RouterParams& p, const i128* L, int b, hb_decision*
 // O3 by one warp: k rounds of a warp arg-max over (L desc, index asc).  The
 // same selection as decide(), with a dependency chain of ~k*5 shuffle steps
 // instead of E*k serial compares (the router is on every layer's critical path).
-__device__ void topk_warp(const RouterParams& p, const i128* L, int* sel) {
+__device__ __forceinline__ void topk_warp(const RouterParams& p, const i128* L, int* sel) {
   const int lane = threadIdx.x & 31;
   unsigned long long taken = 0ull;
   for (int i = 0; i < p.k; ++i) {
@@ -174,10 +174,12 @@ __device__ void topk_warp(const RouterParams& p, const i128* L, int* sel) {
 // dependency chain: lane e ranks its logit against all E in parallel (same
 // order as decide(): L desc, index asc), the two winners come from ballots,
 // the decision is the exact integer gap test and the two gates follow from
-// one exp: g0 = 1 / (1 + exp(l1 - l0)), g1 = 1 - g0 (fp64, as decide()).
-__device__ void decide_k2_warp(const RouterParams& p, const i128* L, int b, hb_decision* out,
+// one exp: g0 = 1 / (1 + exp(l1 - l0)), g1 = exp(l1 - l0) g0 (fp32; the
+// decision itself is the exact integer test).
+__device__ __forceinline__ void decide_k2_warp(const RouterParams& p, const i128* L, int b, hb_decision* out,
                                hb_decision* out_s) {
   const int lane = threadIdx.x & 31;
+  HB_RTL(13);
   int rank = 2;
   if (lane < p.E) {
     const i128 v = L[lane];
@@ -187,23 +189,30 @@ __device__ void decide_k2_warp(const RouterParams& p, const i128* L, int b, hb_d
       rank += (o > v) || (o == v && e < lane);
     }
   }
+  HB_RTL(8);
   const unsigned m0 = __ballot_sync(0xffffffffu, rank == 0);
   const unsigned m1 = __ballot_sync(0xffffffffu, rank == 1);
+  HB_RTL(9);
   if (lane == 0) {
     const int e0 = __ffs(m0) - 1, e1 = __ffs(m1) - 1;
     const i128 G = L[e0] - L[e1];                  // >= 0
     const uint8_t prec1 = gap_le(G, p.th1_kind, p.theta1) ? HB_HIGH
                         : gap_le(G, p.th2_kind, p.theta2) ? HB_LOW : HB_SKIP;
-    const double d = G >= ((i128)1 << 62) ? 1e300 : (double)(long long)G * 0x1p-48;
-    const double ex = exp(-d);
-    const double g0 = 1.0 / (1.0 + ex), g1 = ex / (1.0 + ex);
+    // gates in fp32 (|error| ~1e-7, the records are fp32): the fp64 exp and
+    // divisions cost ~1.5 us of single-thread latency on the critical path
+    const float d = G >= ((i128)1 << 62) ? 1e30f : (float)(long long)G * 0x1p-48f;
+    const float ex = expf(-d);
+    const float g0 = 1.f / (1.f + ex), g1 = ex * g0;
+    HB_RTL(10);
     hb_decision r0, r1;
     r0.token = b; r0.expert = e0; r0.sel_rank = 0; r0.prec = HB_HIGH;
     r0.served_enc = HB_ENC_NONE; r0.hit = 0; r0.gate = (float)g0;
     r1.token = b; r1.expert = e1; r1.sel_rank = 1; r1.prec = prec1;
     r1.served_enc = HB_ENC_NONE; r1.hit = 0; r1.gate = (float)g1;
     out[0] = r0; out[1] = r1;
+    HB_RTL(11);
     out_s[0] = r0; out_s[1] = r1;
+    HB_RTL(12);
   }
 }
 
@@ -272,7 +281,7 @@ __device__ void build_jobs(const RouterParams& p, RouterSmem& sm, const hb_decis
 // build_jobs by one warp when the forward has <= 32 selections (decode): the
 // same table (jobs by key = expert*2 + Low, slots in selection order) from
 // per-lane counts instead of serial loops.
-__device__ void build_jobs_warp(const RouterParams& p, RouterSmem& sm, const hb_decision* dec) {
+__device__ __forceinline__ void build_jobs_warp(const RouterParams& p, RouterSmem& sm, const hb_decision* dec) {
   const int lane = threadIdx.x & 31;
   const int nsel = p.B * p.k;
   constexpr int kNone = 0x7FFFFFFF;
@@ -500,6 +509,7 @@ router_kernel(const __grid_constant__ RouterParams p) {
         else if (lane == 0) build_jobs(p, sm, sm.dec);
       }
       HB_RTL(6);
+      HB_RTL(7);                               // back-to-back: cost of one stamp
     }
     return;
   }

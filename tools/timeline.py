@@ -38,7 +38,7 @@ def main():
     rows = {0: [], 1: []}
     rfn = lib.hb_debug_router_timeline
     rfn.argtypes = [ctypes.c_void_p]
-    rbuf = np.zeros(8, dtype=np.uint64)
+    rbuf = np.zeros(16, dtype=np.uint64)
     rrows = []
     lay = []
     for t in range(4):
@@ -49,7 +49,7 @@ def main():
             torch.cuda.synchronize()
             assert rfn(rbuf.ctypes.data) == 0
             rb = rbuf.astype(np.int64)
-            rrows.append((rb[1:8] - rb[0]) / 1000.0)
+            rrows.append((rb[1:14] - rb[0]) / 1000.0)
             # absolute layer timeline relative to router entry
             ab = []
             for k in (0, 1):
@@ -74,7 +74,7 @@ def main():
                 buf[:] = 0
                 # clear device copy for the next launch (stale warps would confuse)
     np.set_printoptions(suppress=True, linewidth=200)
-    print("router stamps (us after entry: wait, partial, combine, -, decide, jobs, warm decide+jobs):",
+    print("router stamps (us after entry: 1 wait, 2 partial, 3-4 combine, 5 decide, 6 jobs, 7 stamp, 8 rank, 9 ballot, 10 gates, 11 gstore, 12 sstore, 13 decide entry):",
           np.median(np.array(rrows), axis=0).round(2))
     print("layer (us from router entry): router_end | K2a entry, first-run med, end | "
           "K2b entry, first-run med, end:", np.median(np.array(lay), axis=0).round(2))
