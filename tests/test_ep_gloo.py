@@ -1,0 +1,84 @@
+"""Expert parallelism (O11) across processes on CPU: world-size-2 `gloo`.
+
+The N>1 path of bench.py shards the experts of every layer by owner(e) =
+e mod world: each rank computes the selected experts
+it owns and the partial layer outputs are summed by an all-reduce.  Here two
+processes run the oracle's per-rank layer (the same partition rule the CUDA
+path implements, checked on one GPU by test_gpu_parity::test_ep_partition_on_one_gpu)
+and all-reduce over gloo; the sum must equal the single-process layer and the
+ranks must split the experts exactly."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synthgen as sg
+from oracle import formats as fm
+from oracle import moe as om
+from oracle import router as rt
+
+SH = sg.TINY
+LAYER = 1
+B = 6
+
+
+def _store():
+    blobs = {}
+
+    def blob(layer, e, enc):
+        if (layer, e, enc) not in blobs:
+            w1, w3, w2 = sg.expert_weights(SH, layer, e)
+            blobs[(layer, e, enc)] = fm.quantize_blob(enc, w1, w3, w2)
+        return blobs[(layer, e, enc)]
+
+    return om.ExpertStore(blob, SH.hidden, SH.ffn)
+
+
+def _worker(rank, world, port, out_dir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        x16 = sg.hidden_states(SH, 31, LAYER, batch=B)
+        wg = sg.router_weights(SH, LAYER)
+        y, routes = om.moe_layer(x16, wg, _store(), LAYER, SH.top_k, 0.6, 0.9, fm.F16, fm.Q4,
+                                 rank=rank, world=world)
+        owned = sorted({e for r in routes for e, d in zip(r.experts, r.decisions)
+                        if d != rt.SKIP and om.owner(e, world) == rank})
+        t = torch.from_numpy(np.ascontiguousarray(y))
+        dist.all_reduce(t)                      # Eq. 1 summed over ranks
+        own = torch.zeros(SH.n_experts, dtype=torch.int64)
+        own[owned] = rank + 1
+        dist.all_reduce(own)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "y.npy"), t.numpy())
+            np.save(os.path.join(out_dir, "own.npy"), own.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2])
+def test_ep_gloo_allreduce_equals_single_process(world):
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        y = np.load(os.path.join(d, "y.npy"))
+        own = np.load(os.path.join(d, "own.npy"))
+    x16 = sg.hidden_states(SH, 31, LAYER, batch=B)
+    ref, routes = om.moe_layer(x16, sg.router_weights(SH, LAYER), _store(), LAYER, SH.top_k,
+                               0.6, 0.9, fm.F16, fm.Q4)
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
+    # every served expert was computed by exactly its owner rank (no overlap,
+    # no gap): own[e] = owner + 1 for the selected, non-skipped experts
+    used = {e for r in routes for e, d in zip(r.experts, r.decisions) if d != rt.SKIP}
+    for e in range(SH.n_experts):
+        assert own[e] == ((om.owner(e, world) + 1) if e in used else 0), (e, own)
