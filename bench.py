@@ -130,11 +130,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ our arm
-def build_model(h, sg, fm, shape, hi, lo, rank, world, dev):
+def build_model(h, sg, fm, shape, hi, lo, rank, world, dev, t1=0.6, t2=0.9):
     import torch
     cfg = h.default_config(n_layers=shape.n_layers, n_experts=shape.n_experts, top_k=shape.top_k,
-                           hidden=shape.hidden, ffn=shape.ffn, hi_enc=hi, lo_enc=lo, t1=0.6,
-                           t2=0.9, max_batch=1, rank=rank, world=world)
+                           hidden=shape.hidden, ffn=shape.ffn, hi_enc=hi, lo_enc=lo, t1=t1,
+                           t2=t2, max_batch=1, rank=rank, world=world)
     ctx = h.Context(cfg, dev)
     H, F = shape.hidden, shape.ffn
     tmp = [torch.empty(n * k, dtype=torch.float16, device="cuda")

@@ -81,14 +81,14 @@ struct hb_ctx {
   float* hsum = nullptr;
   bool force_h_global = false;            // HB_FORCE_H_GLOBAL=1 (tests of that path)
   unsigned* done = nullptr;
-  unsigned* gctr = nullptr;               // GEMV chunk counters [2 + kMaxVJobs] (self-resetting)
+  unsigned* gctr = nullptr;               // GEMV chunk counters [2 + 2 * kGemvCTAs] (self-resetting)
   JobTable jt{};
   void* jt_dev = nullptr;
   void* jt_host = nullptr;                // pinned staging
   size_t jt_bytes = 0;
   int max_jobs = 0, max_slots = 0, max_vjobs = 0;
-  float static_frac = 0.7f;               // GEMV work feed K2a (HB_STATIC_FRAC, HB_CHUNK)
-  float static_frac2 = 0.9f;              // K2b (HB_STATIC_FRAC2)
+  float static_frac = 0.8f;               // GEMV work feed K2a (HB_STATIC_FRAC, HB_CHUNK)
+  float static_frac2 = 0.8f;              // K2b (HB_STATIC_FRAC2)
   int chunk = 8;
   cudaEvent_t dec_ready = nullptr;
   // kernel timing (hb_profile)
@@ -256,7 +256,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
             dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->hsum, (size_t)c->max_slots * (F / 32) * 4) &&
-            dm((void**)&c->done, 16) && dm((void**)&c->gctr, sizeof(unsigned) * (2 + kMaxVJobs));
+            dm((void**)&c->done, 16) && dm((void**)&c->gctr, sizeof(unsigned) * (2 + 2 * kGemvCTAs));
   if (!ok) return bail(HB_ENOMEM, "device allocation of scratch failed");
   {
     const char* fh = std::getenv("HB_FORCE_H_GLOBAL");
@@ -269,7 +269,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     if (ch) c->chunk = (std::max(2, std::atoi(ch)) + 1) & ~1;   // even: K2b stages hold 2 units
   }
   cudaMemset(c->done, 0, 16);
-  cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + kMaxVJobs));
+  cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + 2 * kGemvCTAs));
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
   // job table: hdr | jobs | slot_token | slot_gate | tok_slots
   const size_t o_jobs = 64, o_tok = align_up(o_jobs + sizeof(Job) * c->max_jobs, 64),

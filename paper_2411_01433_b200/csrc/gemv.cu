@@ -150,6 +150,12 @@ __device__ __forceinline__ uint32_t u4get(const uint4& v, int i) {
   return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
+#ifdef HB_DBG_NOLO
+constexpr bool kDbgNoLo = true;              // diagnostic: K2b without the h-lo MMAs
+#else
+constexpr bool kDbgNoLo = false;
+#endif
+
 // fp16 pair constants
 constexpr uint32_t kH1032 = 0x64086408u;    // 1032 = 1024 + 8
 constexpr uint32_t kH1152 = 0x64806480u;    // 1152 = 1024 + 128
@@ -409,10 +415,10 @@ struct FeedConst {         // per launch, in shared memory (CTA-wide constants)
 };
 struct Feed {
   int a, b;                // pending segment [a, b) (global units); empty when a >= b
-  unsigned pre;            // lane 0: the prefetched chunk index
+  unsigned pre;            // lane 0: the prefetched fetch index
   bool done;
   const FeedConst* k;
-  __device__ __forceinline__ void prefetch() {
+  __device__ __forceinline__ void start() {
     if ((threadIdx.x & 31) == 0) pre = atomicAdd(k->ctr, 1u);
   }
   // next chunk into [a, b); false when the launch's work is exhausted
@@ -428,7 +434,7 @@ struct Feed {
     }
     a = k->base + k->S + c * k->chunk;
     b = min(a + k->chunk, k->base + k->U);
-    prefetch();
+    if ((threadIdx.x & 31) == 0) pre = atomicAdd(k->ctr, 1u);
     return true;
   }
 };
@@ -479,7 +485,7 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
   const uint8_t* sp_[NMAT];
   auto take = [&]() -> bool {                  // the feed's next segment, if it is in this vjob
     if (fd.a >= fd.b && !fd.refill()) return false;
-    if (fd.a >= cum + Uv) return false;
+    if (fd.a < cum || fd.a >= cum + Uv) return false;
     pl = fd.a - cum;
     pe = min(fd.b, cum + Uv) - cum;
     fd.a = cum + pe;                           // a remainder past the vjob stays in the feed
@@ -637,7 +643,7 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
         if constexpr (ENC == HB_F16) {
           mma16816(r[m], Pg[0], Ph[0], Pg[1], Ph[1], xb.x, xb.y);
           mma16816(r[m], Pg[2], Ph[2], Pg[3], Ph[3], xb.z, xb.w);
-          if constexpr (SPLIT) {
+          if constexpr (SPLIT && !kDbgNoLo) {
             mma16816(r[m], Pg[0], Ph[0], Pg[1], Ph[1], xl.x, xl.y);
             mma16816(r[m], Pg[2], Ph[2], Pg[3], Ph[3], xl.z, xl.w);
           }
@@ -648,7 +654,7 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
           float D[4] = {0.f, 0.f, 0.f, 0.f};
           mma16816(D, Pg[0], Ph[0], Pg[1], Ph[1], xb.x, xb.y);
           mma16816(D, Pg[2], Ph[2], Pg[3], Ph[3], xb.z, xb.w);
-          if constexpr (SPLIT) {
+          if constexpr (SPLIT && !kDbgNoLo) {
             mma16816(D, Pg[0], Ph[0], Pg[1], Ph[1], xl.x, xl.y);
             mma16816(D, Pg[2], Ph[2], Pg[3], Ph[3], xl.z, xl.w);
           }
@@ -752,18 +758,20 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   const int nslots = __ldcg(p.jt.hdr + 1);
   constexpr int XS = W13 ? 1 : 2;
   const int K = W13 ? p.H : p.F;
-  const bool part = !W13 && !p.h_global;     // K2b CTA groups per (vjob, column slice)
   // stage hand-off: K2a every thread arrives after its share of the x copy;
   // K2b thread 0 arrives once with the bulk copies' transaction count
   if (threadIdx.x == 0) mbar_init(smem_u32(&s_bar), W13 ? blockDim.x : 1);
   __syncthreads();
   if (nv == 0) return;                       // nothing owned: y stays zero (router)
   const int U = s_cum[nv];
-  // ---- the space this CTA works in.  K2a: all units, B operand = x of all
-  // tokens.  K2b with h in shared memory: the CTAs are split into one group
-  // per vjob (sizes proportional to its units, >= 1 CTA each), so a CTA
-  // stages h of its vjob's slots only (59 KB per slot at F = 14336) and
-  // keeps a deeper weight ring; its warps' feed covers that vjob alone.
+  // ---- the space this CTA works in.  K2a: all units (every SM gets the same
+  // mix of fp16 = HBM-heavy and low-bit = ALU-heavy units; measured: splitting
+  // K2a's CTAs per job leaves the low-bit group compute-bound and late).  K2b
+  // with h in shared memory: the CTAs are split into groups, one per
+  // sub-space (a vjob's column slice of h), sizes proportional to its units
+  // (>= 1 CTA each), so a CTA stages only its slice of h and keeps a deep
+  // ring; its warps' feed covers that slice alone.
+  const bool part = !W13 && !p.h_global;
   Stage S;
   S.ptr = gemv_smem + kGemvWarps * KCfg<W13>::RING;
   S.xst = smem_u32(S.ptr);
@@ -771,50 +779,44 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   int base = 0, Usp = U, ncta = gridDim.x, cta = blockIdx.x, vsp = -1;
   S.nh = 1;
   S.hs = 0;
-  if constexpr (W13) {
-    S.row0 = 0;
-    S.nrows = p.B;
-    S.kcols = K;
-    S.on = (size_t)S.nrows * (XS * K * 2 + (K / 32) * 4) <= (size_t)KCfg<W13>::XSTAGE;
-  } else {
-    S.on = false;
-    S.row0 = 0;
-    S.nrows = nslots;
-    S.kcols = K;
-    if (part) {
-      // sub-spaces (vjob v, column slice h < nh(v)), nh = 2 when the slice has
-      // an even number of groups; CTAs [c0(q), c0(q+1)) work on sub-space q,
-      // c0(q) = q + floor(first unit of q * (n - nsub) / U)
-      if (threadIdx.x == 0) {
-        int q = 0;
-        for (int v = 0; v < nv; ++v) {
-          const int G = K / epg_of(__ldcg(&p.jt.vjobs[v].enc));
-          const int nh = (G % 4 == 0) ? 2 : 1;
-          const int uq = (s_cum[v + 1] - s_cum[v]) / nh;
-          for (int h = 0; h < nh; ++h, ++q) {
-            s_subvh[q] = v | (h << 16) | (nh << 24);
-            s_subb[q] = s_cum[v] + h * uq;
-          }
+  S.row0 = 0;
+  S.nrows = W13 ? p.B : nslots;
+  S.kcols = K;
+  S.on = W13 && (size_t)S.nrows * (XS * K * 2 + (K / 32) * 4) <= (size_t)KCfg<W13>::XSTAGE;
+  if (part) {
+    // sub-spaces (vjob v, column slice h < nh(v)); K2b: nh = 2 when the slice
+    // has an even number of groups.  CTAs [c0(q), c0(q+1)) work on
+    // sub-space q, c0(q) = q + floor(first unit of q * (n - nsub) / U)
+    if (threadIdx.x == 0) {
+      int q = 0;
+      for (int v = 0; v < nv; ++v) {
+        const int G = K / epg_of(__ldcg(&p.jt.vjobs[v].enc));
+        const int nh = (!W13 && G % 4 == 0) ? 2 : 1;
+        const int uq = (s_cum[v + 1] - s_cum[v]) / nh;
+        for (int h = 0; h < nh; ++h, ++q) {
+          s_subvh[q] = v | (h << 16) | (nh << 24);
+          s_subb[q] = s_cum[v] + h * uq;
         }
-        s_subb[q] = U;
-        s_nsub = q;
       }
-      __syncthreads();
-      const int nsub = s_nsub;
-      const int spare = (int)gridDim.x - nsub;
-      auto c0 = [&](int q) { return q + (int)((long long)s_subb[q] * spare / U); };
-      int lo = 0, hi = nsub - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (c0(mid) <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
-      }
-      const int v = s_subvh[lo] & 0xFFFF;
-      vsp = lo;
-      base = s_subb[lo];
-      Usp = s_subb[lo + 1] - base;
-      cta = blockIdx.x - c0(lo);
-      ncta = (lo + 1 < nsub ? c0(lo + 1) : (int)gridDim.x) - c0(lo);
-      const VJobD d = p.jt.vjobs[v];
+      s_subb[q] = U;
+      s_nsub = q;
+    }
+    __syncthreads();
+    const int nsub = s_nsub;
+    const int spare = (int)gridDim.x - nsub;
+    auto c0 = [&](int q) { return q + (int)((long long)s_subb[q] * spare / U); };
+    int lo = 0, hi = nsub - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (c0(mid) <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    vsp = lo;
+    base = s_subb[lo];
+    Usp = s_subb[lo + 1] - base;
+    cta = blockIdx.x - c0(lo);
+    ncta = (lo + 1 < nsub ? c0(lo + 1) : (int)gridDim.x) - c0(lo);
+    if constexpr (!W13) {
+      const VJobD d = p.jt.vjobs[s_subvh[lo] & 0xFFFF];
       S.row0 = d.slot0;
       S.nrows = d.nslot;
       S.nh = s_subvh[lo] >> 24;
@@ -833,7 +835,9 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
     s_fk.chunk = p.chunk;
     s_fk.nch = (Usp - s_fk.S + p.chunk - 1) / p.chunk;
     s_fk.nwarps = ncta * kGemvWarps;
-    s_fk.ctr = W13 ? p.ctr : p.ctr + 1 + (vsp < 0 ? 0 : 1 + vsp);
+    // counters: [0] K2a all units, [1] K2b all units, [2 + q] K2a group q,
+    // [2 + kGemvCTAs + q] K2b group q (K2b fetches while K2a still runs)
+    s_fk.ctr = p.ctr + (vsp < 0 ? (W13 ? 0 : 1) : 2 + (W13 ? 0 : kGemvCTAs) + vsp);
   }
   __syncthreads();
   Feed fd;
@@ -844,7 +848,7 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   const int gwl = warp * ncta + cta;
   fd.a = base + ((int)((long long)s_fk.S * gwl / s_fk.nwarps) & ~(KNU - 1));
   fd.b = base + ((int)((long long)s_fk.S * (gwl + 1) / s_fk.nwarps) & ~(KNU - 1));
-  fd.prefetch();
+  fd.start();
   const uint32_t ring = smem_u32(gemv_smem) + warp * KCfg<W13>::RING;
   uint2* meta = s_meta[warp];
   bool first = true;

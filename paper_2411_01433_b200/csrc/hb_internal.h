@@ -141,7 +141,7 @@ struct GemvParams {
                                        // instead of building it in shared memory per CTA
   float* y;                            // [B][H] (zeroed by router)
   // work feed: a static share of the units, then dynamic chunks (K2)
-  unsigned* ctr;                       // chunk counters: [0] K2a, [1] K2b, [2 + v] K2b group of vjob v
+  unsigned* ctr;                       // chunk counters: [0] K2a, [1] K2b, [2 + q] K2a group q, [2 + 148 + q] K2b group q
   int max_vjobs;                       // table entries to preload (>= n_vjobs + 1)
   float static_frac;                   // K2a: fraction of units dealt as static warp ranges
   float static_frac2;                  // K2b

@@ -27,7 +27,9 @@ def main():
     shape = {"mixtral": sg.MIXTRAL, "phi": sg.PHI}[model]
     hi, lo = bench.PAIRS[pair]
     torch.cuda.set_device(0)
-    ctx, blobs = bench.build_model(h, sg, None, shape, hi, lo, 0, 1, 0)
+    t1 = float(os.environ.get("TL_T1", "0.6"))
+    t2 = float(os.environ.get("TL_T2", "0.9"))
+    ctx, blobs = bench.build_model(h, sg, None, shape, hi, lo, 0, 1, 0, t1, t2)
     lib = _lib.lib
     fn = lib.hb_debug_timeline
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
