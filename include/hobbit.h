@@ -172,6 +172,15 @@ int prefetch_next_layer(hb_ctx* ctx, int layer, const void* x, int batch, void* 
 int moe_layer_forward(hb_ctx* ctx, int layer, const void* x, int batch,
                       void* y, void* stream);
 
+/* Batched decode / prefill (P:820 batch 1 only, P:1018
+ * "prefill ... nearly all experts"): resident-mode forwards with
+ * batch >= min_batch run the expert FFN as a grouped GEMM on the tcgen05
+ * tensor cores (weights dequantised to fp16 in shared memory, fp32 TMEM
+ * accumulation, h rounded to fp16: DESIGN.md R26) instead of the dequant-GEMV.
+ * Decisions are unchanged.  0 = never.  Default 32 (env HB_K3_MIN_BATCH).
+ * HB_EUNSUPPORTED if the context was created with max_batch == 1. */
+int hb_set_batched_min(hb_ctx* ctx, int min_batch);
+
 /* ------------------------------------------------------------ inspection */
 /* Decisions of the last forward: batch*top_k records (synchronises). */
 int hb_get_decisions(hb_ctx* ctx, hb_decision* out, int cap);

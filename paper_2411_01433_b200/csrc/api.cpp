@@ -15,6 +15,7 @@
 
 #include "cache.h"
 #include "hb_internal.h"
+#include "k3.h"
 #include "hobbit.h"
 
 namespace hb {
@@ -90,6 +91,14 @@ struct hb_ctx {
   float static_frac = 0.8f;               // GEMV work feed K2a (HB_STATIC_FRAC, HB_CHUNK)
   float static_frac2 = 0.8f;              // K2b (HB_STATIC_FRAC2)
   int chunk = 8;
+  // K3: tcgen05 grouped GEMM for batches >= k3_min_batch (A9); buffers exist
+  // when max_batch > 1 and the vjob3 table bound fits
+  int k3_min_batch = 32;                  // HB_K3_MIN_BATCH / hb_set_batched_min
+  bool k3_ok = false;
+  int k3_ks = 1;
+  __half* k3_xg = nullptr;
+  __half* k3_hB = nullptr;
+  K3Table* k3_tab = nullptr;
   cudaEvent_t dec_ready = nullptr;
   // kernel timing (hb_profile)
   std::vector<cudaEvent_t> prof_ev;       // 3 per recorded forward
@@ -181,7 +190,7 @@ static void free_ctx(hb_ctx* c) {
   cudaDeviceSynchronize();
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
                    c->logits, c->lbuf, c->x_perm, c->xsum, c->au, c->h_hi, c->h_lo,
-                   c->hsum, c->done, c->gctr, c->jt_dev};
+                   c->hsum, c->done, c->gctr, c->jt_dev, c->k3_xg, c->k3_hB, c->k3_tab};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
@@ -267,6 +276,21 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     if (sf2) c->static_frac2 = std::min(1.0f, std::max(0.0f, (float)std::atof(sf2)));
     const char* ch = std::getenv("HB_CHUNK");
     if (ch) c->chunk = (std::max(2, std::atoi(ch)) + 1) & ~1;   // even: K2b stages hold 2 units
+  }
+  {
+    // K3 scratch: X and h of every vjob3 in canonical blocks (rows padded to 16)
+    const int max_v3 = c->max_jobs + (c->max_slots + kK3MaxN - 1) / kK3MaxN;
+    const size_t rows = (size_t)c->max_slots + 16 * (size_t)max_v3;
+    if (B > 1 && max_v3 <= kK3MaxV3) {
+      if (!dm((void**)&c->k3_xg, rows * H * 2) || !dm((void**)&c->k3_hB, rows * F * 2) ||
+          !dm((void**)&c->k3_tab, sizeof(K3Table)))
+        return bail(HB_ENOMEM, "K3 scratch allocation failed");
+      c->k3_ok = true;
+      c->k3_ks = (F / 2) % 256 == 0 ? 2 : 1;
+      cudaMemset(c->k3_tab, 0, sizeof(K3Table));
+    }
+    const char* km = std::getenv("HB_K3_MIN_BATCH");
+    if (km) c->k3_min_batch = std::atoi(km);
   }
   cudaMemset(c->done, 0, 16);
   cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + 2 * kGemvCTAs));
@@ -471,6 +495,29 @@ static void launch_gemv(hb_ctx* c, const GemvParams& gp, cudaStream_t s) {
   c->launches += 2;
 }
 
+// K3 chain (batched decode / prefill): vjob3 table + X gather, K3a, K3b
+static void launch_batched(hb_ctx* c, const void* x, void* y, cudaStream_t s) {
+  K3Params kp{};
+  kp.jt = c->jt;
+  for (int e = 0; e < 4; ++e) kp.lay[e] = c->lay[e];
+  kp.H = c->cfg.hidden;
+  kp.F = c->cfg.ffn;
+  kp.ks = c->k3_ks;
+  kp.xg = c->k3_xg;
+  kp.hB = c->k3_hB;
+  kp.y = (float*)y;
+  kp.tab = c->k3_tab;
+  cudaEvent_t* ev = nullptr;
+  if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
+  launch_k3_prep(kp, (const __half*)x, s);
+  if (ev) cudaEventRecord(ev[0], s);
+  launch_k3a(kp, s);
+  if (ev) cudaEventRecord(ev[1], s);
+  launch_k3b(kp, s);
+  if (ev) cudaEventRecord(ev[2], s);
+  c->launches += 3;
+}
+
 static const __half* router_of(hb_ctx* c, int layer) {
   return c->wg + (size_t)layer * c->cfg.n_experts * c->cfg.hidden;
 }
@@ -527,10 +574,16 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
 
   if (c->resident) {
     rp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
+    const bool k3 = c->k3_ok && c->k3_min_batch > 0 && batch >= c->k3_min_batch;
+    if (k3) rp.zero_n[0] = 0;                          // K3 does not use the K2a sums
     launch_router(rp, s);
     c->launches += 1;
-    GemvParams gp = gemv_params(c, batch, y);
-    launch_gemv(c, gp, s);
+    if (k3) {
+      launch_batched(c, x, y, s);
+    } else {
+      GemvParams gp = gemv_params(c, batch, y);
+      launch_gemv(c, gp, s);
+    }
     c->last_host_decisions = false;
     CUDA_TRY(c, cudaGetLastError());
     return HB_OK;
@@ -717,6 +770,14 @@ int hb_last_expert_bytes(hb_ctx* c, uint64_t* out) {
     tot += c->bbytes[d[i].served_enc];
   }
   *out = tot;
+  return HB_OK;
+}
+
+int hb_set_batched_min(hb_ctx* c, int min_batch) {
+  if (!c || min_batch < 0) return fail(c, HB_EINVAL, "bad argument");
+  if (min_batch > 0 && !c->k3_ok)
+    return fail(c, HB_EUNSUPPORTED, "batched GEMM path needs max_batch > 1 (and <= 64 vjob3 per forward)");
+  c->k3_min_batch = min_batch;
   return HB_OK;
 }
 

@@ -1,0 +1,526 @@
+// K3: batched-decode / prefill expert FFN as a grouped
+// mixed-precision GEMM on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// Eq. 1 for a batch: for every (expert, served encoding) job the
+// tokens routed to it form the N side of two GEMMs,
+//     K3a:  a = W1 X^T, u = W3 X^T  -> h = silu(a) * u        (SwiGLU epilogue)
+//     K3b:  o = W2 h^T              -> y[token] += g * o       (Eq. 1 epilogue)
+// P:820 / P:1018: the paper runs batch 1 only and notes that prefill touches
+// nearly every expert; at B >= 32 tokens per layer the per-expert token count
+// M_e = B*k/E makes these real dense contractions.
+//
+// Design ("K3"):
+//  * vjob3 = <= 128 tokens of one job (MMA N = np = round-up-16 of the count).
+//    k3_prep (one launch) builds the vjob3 table from the router's job table
+//    and gathers X of every vjob3 into xg in the UMMA canonical K-major layout
+//    (8x8 core matrices, 16-byte rows), so each K3a stage gets X with ONE bulk
+//    copy; K3a's epilogue writes h straight into the same layout for K3b.
+//  * Item = (vjob3, 128-row weight tile[, K split]); persistent grid, one CTA
+//    per SM, items dealt round-robin.  Warp roles:
+//      warp 13  producer: TMA bulk copies (cp.async.bulk) of the raw units of
+//               the tile (codes + scales, our tile-major blob layout) into a
+//               3-slot raw ring (mbarrier complete_tx);
+//      warps 0-7 converters: raw units -> fp16 canonical A tiles (F16 is a
+//               relayout, Q8/Q4/Q2 dequantise with half2 magic numbers) in a
+//               2-slot canonical ring; thread 0 also bulk-copies the B tile;
+//      warp 12  MMA issuer: one thread issues tcgen05.mma.kind::f16 (M=128,
+//               N=np, K=16) into a TMEM accumulator, tcgen05.commit frees the
+//               canonical slot / signals the epilogue;
+//      warps 8-11 epilogue: tcgen05.ld the accumulator (warp w%4 owns TMEM
+//               lanes 32(w%4)..+31 = tile rows), SwiGLU -> h (K3a) or
+//               g-weighted red.add into y (K3b).  Two TMEM accumulator buffers
+//               let the epilogue of item i overlap the main loop of item i+1.
+//  * Weights are dequantised to fp16 (one rounding of d*q, d*q+m) because the
+//    tensor core accumulates across blocks; h is rounded to fp16 for K3b
+//    (R26).  Accumulation is fp32 in TMEM.
+#include "hb_internal.h"
+#include "k3.h"
+
+namespace hb {
+
+namespace {
+
+constexpr int kRows = 128;                 // weight rows per tile = MMA M
+constexpr int kBK = 64;                    // K elements per canonical stage
+constexpr int kRawSlots = 3;
+constexpr int kCanSlots = 2;
+constexpr int kConvWarps = 8;
+constexpr int kMmaWarp = 12;
+constexpr int kProdWarp = 13;
+constexpr int kThreads = 14 * 32;
+constexpr int kRawCode = 32768;            // 2 matrices x 8 tiles of 16 rows x 2 units
+constexpr int kRawScale = 8192;
+constexpr int kRawBytes = kRawCode + kRawScale;
+constexpr int kAMat = kRows * kBK * 2;     // 16 KB canonical A per matrix
+constexpr int kABytes = 2 * kAMat;
+constexpr int kBBytes = kK3MaxN * kBK * 2; // 16 KB canonical B
+constexpr int kCanBytes = kABytes + kBBytes;
+constexpr int kBarOff = kRawSlots * kRawBytes + kCanSlots * kCanBytes;
+constexpr int kSmem = kBarOff + 256;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint32_t b, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(b), "r"(n));
+}
+__device__ __forceinline__ void bar_arrive(uint32_t b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(b) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint32_t b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_add_tx(uint32_t b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" :: "r"(b), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+        : "=r"(done) : "r"(b), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+// K-major, no swizzle: 8x(16 B) core matrices; K-adjacent core matrices 128 B
+// apart (LBO), 8-row groups 1024 B apart (SBO); version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46);
+}
+// kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N, M=128
+__device__ __forceinline__ uint32_t idesc_f16(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                     uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; "
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
+      :: "r"(tmem_d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint16_t lds16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" :: "r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+__device__ __forceinline__ __half2 bcast(uint16_t h) {
+  return u2h((uint32_t)h | ((uint32_t)h << 16));
+}
+
+// 8 consecutive K elements of one row, dequantised to fp16 (element order).
+// code: shared address of the row's 64-byte piece of the unit; sc: its scale
+// record; e: K offset inside the group (multiple of 8).  Layout formulas:
+// oracle/formats.py docstring (the definition; tests/golden pins it).
+__device__ __forceinline__ uint4 dequant8(int enc, uint32_t code, uint32_t sc, int e) {
+  const int j = e >> 5, t = (e & 31) >> 3;
+  if (enc == HB_F16) return lds128(code + 2 * e);
+  const __half2 d = bcast(lds16(sc + 2 * j));
+  uint4 o;
+  if (enc == HB_Q4) {
+    // nibble i = element i; (1024 + q) via the 0x6400 exponent, - 1032 exact
+    const uint32_t v = lds32(code + 16 * t + 4 * j);
+    const uint32_t A = v & 0x0F0F0F0Fu, B = (v >> 4) & 0x0F0F0F0Fu;
+    const __half2 off = u2h(0x64086408u);                  // (1032, 1032)
+    o.x = h2u(__hmul2(__hsub2(u2h((prmt(A, B, 0x0400) & 0x00FF00FFu) | 0x64006400u), off), d));
+    o.y = h2u(__hmul2(__hsub2(u2h((prmt(A, B, 0x0501) & 0x00FF00FFu) | 0x64006400u), off), d));
+    o.z = h2u(__hmul2(__hsub2(u2h((prmt(A, B, 0x0602) & 0x00FF00FFu) | 0x64006400u), off), d));
+    o.w = h2u(__hmul2(__hsub2(u2h((prmt(A, B, 0x0703) & 0x00FF00FFu) | 0x64006400u), off), d));
+  } else if (enc == HB_Q8) {
+    // int8 ^ 0x80 = q + 128 in [1, 255]: (1024 + q + 128) - 1152 exact
+    const uint32_t a = lds32(code + 16 * t + 8 * j) ^ 0x80808080u;
+    const uint32_t b = lds32(code + 16 * t + 8 * j + 4) ^ 0x80808080u;
+    const uint32_t M = 0x64646464u;
+    const __half2 off = u2h(0x64806480u);                  // (1152, 1152)
+    o.x = h2u(__hmul2(__hsub2(u2h(prmt(a, M, 0x5150)), off), d));
+    o.y = h2u(__hmul2(__hsub2(u2h(prmt(a, M, 0x5352)), off), d));
+    o.z = h2u(__hmul2(__hsub2(u2h(prmt(b, M, 0x5150)), off), d));
+    o.w = h2u(__hmul2(__hsub2(u2h(prmt(b, M, 0x5352)), off), d));
+  } else {  // HB_Q2: w = d*q + m; elements 0-3 in byte c0, 4-7 in byte c0 + 2
+    const __half2 m = bcast(lds16(sc + 16 + 2 * j));
+    const uint32_t v = lds32(code + 16 * t + 4 * (j >> 1));
+    const uint32_t s0 = (j & 1) ? 0x0101u : 0u;             // byte (j%2) into bytes 0 and 2
+    const uint32_t c0 = prmt(v, 0, 0x4040u + s0), c1 = prmt(v, 0, 0x4242u + s0);
+    // (q0 bits 0-1 | q1 bits 18-19) and (q2 bits 4-5 | q3 bits 22-23), magic 0x6400
+    const __half2 n01 = u2h(0x34003C00u), b01 = u2h(0xDC00E400u);  // (1, 1/4), (-1024, -256)
+    const __half2 n23 = u2h(0x24002C00u), b23 = u2h(0xCC00D400u);  // (1/16, 1/64), (-64, -16)
+    o.x = h2u(__hfma2(__hfma2(u2h((c0 & 0x000C0003u) | 0x64006400u), n01, b01), d, m));
+    o.y = h2u(__hfma2(__hfma2(u2h((c0 & 0x00C00030u) | 0x64006400u), n23, b23), d, m));
+    o.z = h2u(__hfma2(__hfma2(u2h((c1 & 0x000C0003u) | 0x64006400u), n01, b01), d, m));
+    o.w = h2u(__hfma2(__hfma2(u2h((c1 & 0x00C00030u) | 0x64006400u), n23, b23), d, m));
+  }
+  return o;
+}
+
+__device__ __forceinline__ int scale_rec(int enc) {   // SB, bytes per (unit, row)
+  return enc == HB_Q8 ? 4 : enc == HB_Q4 ? 8 : enc == HB_Q2 ? 32 : 0;
+}
+__device__ __forceinline__ int raw_units(int enc) { return enc == HB_Q2 ? 1 : 2; }
+
+struct Item {
+  const V3* v;
+  int tile;      // 128-row tile of the weight matrix
+  int ks;        // K split index (K3b)
+};
+
+template <int NMAT>
+__device__ __forceinline__ Item item_of(const K3Params& p, int it) {
+  Item r;
+  if (NMAT == 2) {
+    const int tpv = p.F / kRows;
+    r.v = p.tab->v + it / tpv;
+    r.tile = it % tpv;
+    r.ks = 0;
+  } else {
+    const int tpv = (p.H / kRows) * p.ks;
+    r.v = p.tab->v + it / tpv;
+    r.tile = (it % tpv) / p.ks;
+    r.ks = (it % tpv) % p.ks;
+  }
+  return r;
+}
+
+// Persistent tcgen05 GEMM.  NMAT = 2: K3a (W1, W3 over K = H; SwiGLU
+// epilogue); NMAT = 1: K3b (W2 over K = F / ks; Eq. 1 epilogue).
+template <int NMAT>
+__global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t sbase = su32(sm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bars = sbase + kBarOff;
+  // barriers: raw_full[3] raw_empty[3] can_full[2] can_empty[2] tm_full[2] tm_empty[2]
+  auto raw_full = [&](int i) { return bars + 8 * i; };
+  auto raw_empty = [&](int i) { return bars + 8 * (3 + i); };
+  auto can_full = [&](int i) { return bars + 8 * (6 + i); };
+  auto can_empty = [&](int i) { return bars + 8 * (8 + i); };
+  auto tm_full = [&](int i) { return bars + 8 * (10 + i); };
+  auto tm_empty = [&](int i) { return bars + 8 * (12 + i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kBarOff + 128);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRawSlots; ++i) {
+      bar_init(raw_full(i), 1);
+      bar_init(raw_empty(i), kConvWarps);
+    }
+    for (int i = 0; i < kCanSlots; ++i) {
+      bar_init(can_full(i), kConvWarps);
+      bar_init(can_empty(i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(tm_full(i), 1);
+      bar_init(tm_empty(i), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 :: "r"(su32(tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  const int nv = p.tab->n;
+  const int per_v = NMAT == 2 ? p.F / kRows : (p.H / kRows) * p.ks;
+  const int n_items = nv * per_v;
+  const int Kdim = NMAT == 2 ? p.H : p.F;          // reduction length of the matrix
+  const int Kitem = NMAT == 2 ? p.H : p.F / p.ks;  // K per item
+
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      int rs = 0;
+      uint32_t rph = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item I = item_of<NMAT>(p, it);
+        const int enc = I.v->enc;
+        const int epg = epg_of_enc(enc), ru = raw_units(enc), sb = scale_rec(enc);
+        const int G = Kdim / epg;
+        const int nraw = Kitem / (ru * epg);
+        const int g0 = I.ks * (Kitem / epg);
+        const uint32_t cbytes = ru * 1024, sbytes = ru * 16 * sb;
+        const uint32_t tx = NMAT * 8 * (cbytes + sbytes);
+        const uint8_t* blob = I.v->blob;
+        for (int r = 0; r < nraw; ++r) {
+          bar_wait(raw_empty(rs), rph ^ 1);
+          bar_expect_tx(raw_full(rs), tx);
+          const uint32_t dst = sbase + rs * kRawBytes;
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) {
+            const MatLayout& ML = p.lay[enc].mat[NMAT == 2 ? m : 2];
+            for (int t = 0; t < 8; ++t) {
+              const long long unit = (long long)(I.tile * 8 + t) * G + g0 + r * ru;
+              bulk_g2s(dst + (m * 8 + t) * cbytes, blob + ML.q + 1024 * unit, cbytes, raw_full(rs));
+              if (sb)
+                bulk_g2s(dst + kRawCode + (m * 8 + t) * sbytes, blob + ML.s + 16 * sb * unit,
+                         sbytes, raw_full(rs));
+            }
+          }
+          if (++rs == kRawSlots) { rs = 0; rph ^= 1; }
+        }
+      }
+    }
+  } else if (warp < kConvWarps) {
+    const int tid = threadIdx.x;
+    int rs = 0, cs = 0;
+    uint32_t rph = 0, cph = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item I = item_of<NMAT>(p, it);
+      const int enc = I.v->enc, np = I.v->np;
+      const int epg = epg_of_enc(enc), ru = raw_units(enc), sb = scale_rec(enc);
+      const int nraw = Kitem / (ru * epg);
+      const int cpr = ru * epg / kBK;               // canonical stages per raw slot
+      const __half* bsrc = (NMAT == 2 ? p.xg + I.v->xoff : p.hB + I.v->hoff) +
+                           (size_t)I.ks * (Kitem / kBK) * np * kBK;
+      for (int r = 0; r < nraw; ++r) {
+        bar_wait(raw_full(rs), rph);
+        const uint32_t raw = sbase + rs * kRawBytes;
+        for (int c = 0; c < cpr; ++c) {
+          bar_wait(can_empty(cs), cph ^ 1);
+          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kCanBytes;
+          if (tid == 0) {
+            const int kstep = r * cpr + c;
+            bar_add_tx(can_full(cs), np * kBK * 2);
+            bulk_g2s(can + kABytes, bsrc + (size_t)kstep * np * kBK, np * kBK * 2, can_full(cs));
+          }
+#pragma unroll
+          for (int i = 0; i < 4 * NMAT; ++i) {
+            const int idx = i * 256 + tid;
+            const int m = idx >> 10, ci = idx & 1023;
+            const int q = ci & 7, kcrot = (ci >> 3) & 7, rb = ci >> 6;
+            const int row = rb * 8 + q, kc = (kcrot + (q >> 1)) & 7;
+            const int kr = c * kBK + kc * 8;       // K offset inside the raw slot
+            const int u = kr / epg, e = kr % epg;
+            const int tl = row >> 4, rr = row & 15;
+            const int su = (m * 8 + tl) * ru + u;
+            const uint32_t code = raw + su * 1024 + rr * 64;
+            const uint32_t sc = raw + kRawCode + su * 16 * sb + rr * sb;
+            const uint4 w = dequant8(enc, code, sc, e);
+            sts128(can + m * kAMat + (row >> 3) * 1024 + kc * 128 + (row & 7) * 16, w);
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) bar_arrive(can_full(cs));
+          if (++cs == kCanSlots) { cs = 0; cph ^= 1; }
+        }
+        __syncwarp();
+        if (lane == 0) bar_arrive(raw_empty(rs));
+        if (++rs == kRawSlots) { rs = 0; rph ^= 1; }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (lane == 0) {
+      int cs = 0, ab = 0;
+      uint32_t cph = 0, abph = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item I = item_of<NMAT>(p, it);
+        const int np = I.v->np;
+        const uint32_t idesc = idesc_f16(np);
+        const int nsteps = Kitem / kBK;
+        bar_wait(tm_empty(ab), abph ^ 1);
+        tc_fence_after();
+        const uint32_t tacc = tbase + ab * 256;
+        for (int s = 0; s < nsteps; ++s) {
+          bar_wait(can_full(cs), cph);
+          tc_fence_after();
+          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kCanBytes;
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma(tacc + m * 128, sdesc(can + m * kAMat + kk * 256), sdesc(can + kABytes + kk * 256),
+                   idesc, (s | kk) ? 1u : 0u);
+          umma_commit(can_empty(cs));
+          if (++cs == kCanSlots) { cs = 0; cph ^= 1; }
+        }
+        umma_commit(tm_full(ab));
+        if (++ab == 2) { ab = 0; abph ^= 1; }
+      }
+    }
+  } else {  // epilogue warps 8..11
+    const int q4 = warp & 3;
+    int ab = 0;
+    uint32_t abph = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item I = item_of<NMAT>(p, it);
+      const int np = I.v->np, n_real = I.v->n;
+      bar_wait(tm_full(ab), abph);
+      tc_fence_after();
+      const int row = I.tile * kRows + q4 * 32 + lane;   // weight row of this thread
+      const uint32_t tacc = tbase + ((uint32_t)(q4 * 32) << 16) + ab * 256;
+      for (int n0 = 0; n0 < np; n0 += 16) {
+        if (NMAT == 2) {
+          float a[16], uu[16];
+          tmem_ld16(tacc + n0, a);
+          tmem_ld16(tacc + 128 + n0, uu);
+          // h (fp16) into hB in K3b's canonical B layout: K index = row (of F)
+          __half* hb = p.hB + I.v->hoff + (size_t)(row >> 6) * np * kBK +
+                       ((row & 63) >> 3) * 64 + (row & 7);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = n0 + i;
+            const float s = a[i] / (1.0f + __expf(-a[i]));
+            const float hv = n < n_real ? s * uu[i] : 0.0f;
+            hb[(n >> 3) * 512 + (n & 7) * 8] = __float2half_rn(hv);
+          }
+        } else {
+          float o[16];
+          tmem_ld16(tacc + n0, o);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = n0 + i;
+            if (n < n_real) {
+              const int slot = I.v->slot0 + n;
+              const int tok = p.jt.slot_token[slot];
+              const float g = p.jt.slot_gate[slot];
+              atomicAdd(p.y + (size_t)tok * p.H + row, g * o[i]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(tm_empty(ab));
+      if (++ab == 2) { ab = 0; abph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tbase) : "memory");
+  }
+}
+
+// vjob3 table from the router's job table (every CTA rebuilds it in shared
+// memory; CTA 0 publishes it) + gather of X into xg (canonical B layout).
+__global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* __restrict__ x) {
+  __shared__ V3 tab[kK3MaxV3];
+  __shared__ int s_n;
+  if (threadIdx.x == 0) {
+    const int nj = p.jt.hdr[0];
+    int n = 0;
+    long long xo = 0, ho = 0;
+    for (int j = 0; j < nj; ++j) {
+      const Job J = p.jt.jobs[j];
+      for (int s = 0; s < J.n_tok && n < kK3MaxV3; s += kK3MaxN) {
+        V3 v;
+        v.blob = J.blob;
+        v.enc = J.enc;
+        v.slot0 = J.slot_off + s;
+        v.n = J.n_tok - s < kK3MaxN ? J.n_tok - s : kK3MaxN;
+        v.np = (v.n + 15) & ~15;
+        v.xoff = xo;
+        v.hoff = ho;
+        xo += (long long)v.np * p.H;
+        ho += (long long)v.np * p.F;
+        tab[n++] = v;
+      }
+    }
+    s_n = n;
+    if (blockIdx.x == 0) p.tab->n = n;
+  }
+  __syncthreads();
+  const int nv = s_n;
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) p.tab->v[i] = tab[i];
+  // gather: block (v, kstep) = np rows x 64 K in canonical order; chunk c of
+  // 16 B sits at byte 16c: row n = (c/64)*8 + c%8, K chunk kc = (c/8)%8
+  const int steps = p.H / kBK;
+  for (int w = blockIdx.x; w < nv * steps; w += gridDim.x) {
+    const V3& v = tab[w / steps];
+    const int ks = w % steps;
+    uint4* dst = reinterpret_cast<uint4*>(p.xg + v.xoff + (size_t)ks * v.np * kBK);
+    for (int c = threadIdx.x; c < v.np * 8; c += blockDim.x) {
+      const int n = (c >> 6) * 8 + (c & 7), kc = (c >> 3) & 7;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (n < v.n) {
+        const int tok = p.jt.slot_token[v.slot0 + n];
+        val = *reinterpret_cast<const uint4*>(x + (size_t)tok * p.H + ks * kBK + kc * 8);
+      }
+      dst[c] = val;
+    }
+  }
+}
+
+template <typename K>
+void set_smem_once(K kernel, int bytes, bool& done) {
+  if (!done) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done = true;
+  }
+}
+
+}  // namespace
+
+int k3_smem_bytes() { return kSmem; }
+
+void launch_k3_prep(const K3Params& p, const __half* x, cudaStream_t s) {
+  k3_prep_kernel<<<2 * kNumSM, 256, 0, s>>>(p, x);
+}
+void launch_k3a(const K3Params& p, cudaStream_t s) {
+  static bool d = false;
+  set_smem_once(k3_kernel<2>, kSmem, d);
+  k3_kernel<2><<<kNumSM, kThreads, kSmem, s>>>(p);
+}
+void launch_k3b(const K3Params& p, cudaStream_t s) {
+  static bool d = false;
+  set_smem_once(k3_kernel<1>, kSmem, d);
+  k3_kernel<1><<<kNumSM, kThreads, kSmem, s>>>(p);
+}
+
+}  // namespace hb

@@ -1,0 +1,43 @@
+// K3: tcgen05 grouped GEMM for batched decode / prefill.
+#pragma once
+
+#include "hb_internal.h"
+
+namespace hb {
+
+constexpr int kK3MaxN = 128;    // tokens per vjob3 (MMA N, two TMEM accumulators per buffer)
+constexpr int kK3MaxV3 = 64;    // vjob3 entries per forward
+
+// <= 128 token slots of one job; np = count rounded up to 16 (MMA N)
+struct V3 {
+  const uint8_t* blob;
+  int32_t enc;
+  int32_t slot0;
+  int32_t n;
+  int32_t np;
+  long long xoff;                // fp16 elements: this vjob3's X in xg (np * H)
+  long long hoff;                // fp16 elements: its h in hB (np * F)
+};
+struct K3Table {
+  int32_t n;
+  int32_t pad[3];
+  V3 v[kK3MaxV3];
+};
+
+struct K3Params {
+  JobTable jt;
+  BlobLayout lay[4];
+  int H, F;
+  int ks;                        // K3b K split (F / ks multiple of 256)
+  __half* xg;                    // gathered X, canonical UMMA K-major blocks [v][H/64][np x 64]
+  __half* hB;                    // h, same layout [v][F/64][np x 64]
+  float* y;                      // [B][H] fp32, zeroed by the router
+  K3Table* tab;
+};
+
+int k3_smem_bytes();
+void launch_k3_prep(const K3Params& p, const __half* x, cudaStream_t s);
+void launch_k3a(const K3Params& p, cudaStream_t s);
+void launch_k3b(const K3Params& p, cudaStream_t s);
+
+}  // namespace hb

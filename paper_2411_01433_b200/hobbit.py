@@ -145,7 +145,7 @@ class Context:
         return int(v.value)
 
     def profile(self, max_calls: int):
-        """Record K2a/K2b CUDA events for the next max_calls forwards (0 = off)."""
+        """Record K2a/K2b (or K3a/K3b) CUDA events for the next max_calls forwards (0 = off)."""
         self._check(lib.hb_profile(self._h, max_calls))
 
     def profile_read(self, cap: int = 1 << 16):
@@ -153,6 +153,10 @@ class Context:
         buf = (C.c_float * (2 * cap))()
         n = self._check(lib.hb_profile_read(self._h, buf, cap))
         return [(buf[2 * i], buf[2 * i + 1]) for i in range(n)]
+
+    def set_batched_min(self, min_batch: int):
+        """Batches >= min_batch take the tcgen05 grouped-GEMM path K3 (0 = never)."""
+        self._check(lib.hb_set_batched_min(self._h, min_batch))
 
     def launch_count(self) -> int:
         v = C.c_uint64()
