@@ -130,17 +130,17 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ our arm
-def build_model(h, sg, fm, shape, hi, lo, rank, world, dev, t1=0.6, t2=0.9):
+def build_model(h, sg, fm, shape, hi, lo, rank, world, dev, t1=0.6, t2=0.9, max_batch=1, layers=None):
     import torch
     cfg = h.default_config(n_layers=shape.n_layers, n_experts=shape.n_experts, top_k=shape.top_k,
                            hidden=shape.hidden, ffn=shape.ffn, hi_enc=hi, lo_enc=lo, t1=t1,
-                           t2=t2, max_batch=1, rank=rank, world=world)
+                           t2=t2, max_batch=max_batch, rank=rank, world=world)
     ctx = h.Context(cfg, dev)
     H, F = shape.hidden, shape.ffn
     tmp = [torch.empty(n * k, dtype=torch.float16, device="cuda")
            for n, k in ((F, H), (F, H), (H, F))]
     blobs = []
-    for l in range(shape.n_layers):
+    for l in range(shape.n_layers if layers is None else layers):
         ctx.set_router(l, sg.router_weights(shape, l))
         for e in range(shape.n_experts):
             if e % world != rank:

@@ -99,6 +99,7 @@ struct hb_ctx {
   __half* k3_xg = nullptr;
   __half* k3_hB = nullptr;
   K3Table* k3_tab = nullptr;
+  CUtensorMap* k3_tmap = nullptr;         // [L][E][3] device tensor maps of F16 blobs
   cudaEvent_t dec_ready = nullptr;
   // kernel timing (hb_profile)
   std::vector<cudaEvent_t> prof_ev;       // 3 per recorded forward
@@ -190,7 +191,7 @@ static void free_ctx(hb_ctx* c) {
   cudaDeviceSynchronize();
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
                    c->logits, c->lbuf, c->x_perm, c->xsum, c->au, c->h_hi, c->h_lo,
-                   c->hsum, c->done, c->gctr, c->jt_dev, c->k3_xg, c->k3_hB, c->k3_tab};
+                   c->hsum, c->done, c->gctr, c->jt_dev, c->k3_xg, c->k3_hB, c->k3_tab, c->k3_tmap};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
@@ -283,7 +284,9 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     const size_t rows = (size_t)c->max_slots + 16 * (size_t)max_v3;
     if (B > 1 && max_v3 <= kK3MaxV3) {
       if (!dm((void**)&c->k3_xg, rows * H * 2) || !dm((void**)&c->k3_hB, rows * F * 2) ||
-          !dm((void**)&c->k3_tab, sizeof(K3Table)))
+          !dm((void**)&c->k3_tab, sizeof(K3Table)) ||
+          (resident && (k.hi_enc == HB_F16 || k.lo_enc == HB_F16) &&
+           !dm((void**)&c->k3_tmap, sizeof(CUtensorMap) * (size_t)L * E * 3)))
         return bail(HB_ENOMEM, "K3 scratch allocation failed");
       c->k3_ok = true;
       c->k3_ks = (F / 2) % 256 == 0 ? 2 : 1;
@@ -385,6 +388,15 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
     if (flags != HB_REG_DEVICE_BORROW) return fail(c, HB_EINVAL, "resident mode takes device blobs");
     c->dev_blob[idx] = (const uint8_t*)blob;
     CUDA_TRY(c, cudaSetDevice(c->device));
+    if (enc == HB_F16 && c->k3_tmap) {          // K3 F16 path: TMA tensor maps of W1, W3, W2
+      CUtensorMap m[3];
+      const int rows[3] = {k.ffn, k.ffn, k.hidden}, cols[3] = {k.hidden, k.hidden, k.ffn};
+      for (int i = 0; i < 3; ++i)
+        if (k3_encode_f16_map(&m[i], (const uint8_t*)blob + c->lay[HB_F16].mat[i].q, rows[i], cols[i]))
+          return fail(c, HB_ECUDA, "cuTensorMapEncodeTiled failed");
+      CUDA_TRY(c, cudaMemcpy(c->k3_tmap + ((size_t)layer * k.n_experts + expert) * 3, m, sizeof(m),
+                             cudaMemcpyHostToDevice));
+    }
     CUDA_TRY(c, cudaMemcpy(c->dev_blob_table + idx, &c->dev_blob[idx], sizeof(void*),
                            cudaMemcpyHostToDevice));
     return HB_OK;
@@ -496,7 +508,7 @@ static void launch_gemv(hb_ctx* c, const GemvParams& gp, cudaStream_t s) {
 }
 
 // K3 chain (batched decode / prefill): vjob3 table + X gather, K3a, K3b
-static void launch_batched(hb_ctx* c, const void* x, void* y, cudaStream_t s) {
+static void launch_batched(hb_ctx* c, int layer, const void* x, void* y, cudaStream_t s) {
   K3Params kp{};
   kp.jt = c->jt;
   for (int e = 0; e < 4; ++e) kp.lay[e] = c->lay[e];
@@ -507,6 +519,8 @@ static void launch_batched(hb_ctx* c, const void* x, void* y, cudaStream_t s) {
   kp.hB = c->k3_hB;
   kp.y = (float*)y;
   kp.tab = c->k3_tab;
+  kp.tmap = c->k3_tmap ? c->k3_tmap + (size_t)layer * c->cfg.n_experts * 3 : nullptr;
+  kp.has_q = c->cfg.hi_enc != HB_F16 || c->cfg.lo_enc != HB_F16;
   cudaEvent_t* ev = nullptr;
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
   launch_k3_prep(kp, (const __half*)x, s);
@@ -515,7 +529,7 @@ static void launch_batched(hb_ctx* c, const void* x, void* y, cudaStream_t s) {
   if (ev) cudaEventRecord(ev[1], s);
   launch_k3b(kp, s);
   if (ev) cudaEventRecord(ev[2], s);
-  c->launches += 3;
+  c->launches += 1 + 2 * ((kp.tmap != nullptr) + kp.has_q);
 }
 
 static const __half* router_of(hb_ctx* c, int layer) {
@@ -579,7 +593,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
     launch_router(rp, s);
     c->launches += 1;
     if (k3) {
-      launch_batched(c, x, y, s);
+      launch_batched(c, layer, x, y, s);
     } else {
       GemvParams gp = gemv_params(c, batch, y);
       launch_gemv(c, gp, s);

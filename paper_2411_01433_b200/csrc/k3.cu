@@ -42,12 +42,13 @@ namespace {
 
 constexpr int kRows = 128;                 // weight rows per tile = MMA M
 constexpr int kBK = 64;                    // K elements per canonical stage
-constexpr int kRawSlots = 3;
-constexpr int kCanSlots = 2;
-constexpr int kConvWarps = 8;
-constexpr int kMmaWarp = 12;
-constexpr int kProdWarp = 13;
-constexpr int kThreads = 14 * 32;
+constexpr int kRawSlots = 2;
+constexpr int kCanSlots = 3;
+constexpr int kConvWarps = 16;             // warps 0..15 dequantise
+constexpr int kConvThreads = kConvWarps * 32;
+constexpr int kMmaWarp = 20;               // warps 16..19 epilogue (warp % 4 = lane quarter)
+constexpr int kProdWarp = 21;
+constexpr int kThreads = 22 * 32;
 constexpr int kRawCode = 32768;            // 2 matrices x 8 tiles of 16 rows x 2 units
 constexpr int kRawScale = 8192;
 constexpr int kRawBytes = kRawCode + kRawScale;
@@ -58,6 +59,20 @@ constexpr int kCanBytes = kABytes + kBBytes;
 constexpr int kBarOff = kRawSlots * kRawBytes + kCanSlots * kCanBytes;
 constexpr int kSmem = kBarOff + 256;
 
+#ifdef HB_K3_TRACE
+// diagnostic timeline (tools/k3_trace.py): CTA 0 stamps %globaltimer per event
+__device__ unsigned long long g_k3_trace[4][4096];
+__device__ __forceinline__ void k3_stamp(int ch, int i) {
+  if (blockIdx.x == 0 && i < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k3_trace[ch][i] = t;
+  }
+}
+#define K3_STAMP(ch, i) k3_stamp(ch, i)
+#else
+#define K3_STAMP(ch, i)
+#endif
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -218,20 +233,60 @@ struct Item {
 };
 
 template <int NMAT>
-__device__ __forceinline__ Item item_of(const K3Params& p, int it) {
+__device__ __forceinline__ Item item_of(const K3Params& p, int it, int v0) {
   Item r;
   if (NMAT == 2) {
     const int tpv = p.F / kRows;
-    r.v = p.tab->v + it / tpv;
+    r.v = p.tab->v + v0 + it / tpv;
     r.tile = it % tpv;
     r.ks = 0;
   } else {
     const int tpv = (p.H / kRows) * p.ks;
-    r.v = p.tab->v + it / tpv;
+    r.v = p.tab->v + v0 + it / tpv;
     r.tile = (it % tpv) / p.ks;
     r.ks = (it % tpv) % p.ks;
   }
   return r;
+}
+
+// Epilogue of one item: warp quarter q4 holds TMEM lanes (= tile rows)
+// 32*q4 .. +31.  K3a: h = silu(a) * u to hB (K3b's canonical B layout);
+// K3b: y[token] += g * o (Eq. 1) with fp32 reductions.
+template <int NMAT>
+__device__ __forceinline__ void epilogue_item(const K3Params& p, const Item& I, uint32_t tacc,
+                                              int q4, int lane) {
+  const int np = I.v->np, n_real = I.v->n;
+  const int row = I.tile * kRows + q4 * 32 + lane;   // weight row of this thread
+  for (int n0 = 0; n0 < np; n0 += 16) {
+    if (NMAT == 2) {
+      float a[16], uu[16];
+      tmem_ld16(tacc + n0, a);
+      tmem_ld16(tacc + 128 + n0, uu);
+      // h (fp16) into hB in K3b's canonical B layout: K index = row (of F)
+      __half* hb = p.hB + I.v->hoff + (size_t)(row >> 6) * np * kBK +
+                   ((row & 63) >> 3) * 64 + (row & 7);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int n = n0 + i;
+        const float s = a[i] / (1.0f + __expf(-a[i]));
+        const float hv = n < n_real ? s * uu[i] : 0.0f;
+        hb[(n >> 3) * 512 + (n & 7) * 8] = __float2half_rn(hv);
+      }
+    } else {
+      float o[16];
+      tmem_ld16(tacc + n0, o);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int n = n0 + i;
+        if (n < n_real) {
+          const int slot = I.v->slot0 + n;
+          const int tok = p.jt.slot_token[slot];
+          const float g = p.jt.slot_gate[slot];
+          atomicAdd(p.y + (size_t)tok * p.H + row, g * o[i]);
+        }
+      }
+    }
+  }
 }
 
 // Persistent tcgen05 GEMM.  NMAT = 2: K3a (W1, W3 over K = H; SwiGLU
@@ -242,17 +297,22 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
   const uint32_t sbase = su32(sm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bars = sbase + kBarOff;
-  // barriers: raw_full[3] raw_empty[3] can_full[2] can_empty[2] tm_full[2] tm_empty[2]
+  // barriers: raw_full[R] raw_empty[R] can_full[C] can_empty[C] tm_full[2] tm_empty[2]
+  constexpr int R = kRawSlots, CS = kCanSlots;
   auto raw_full = [&](int i) { return bars + 8 * i; };
-  auto raw_empty = [&](int i) { return bars + 8 * (3 + i); };
-  auto can_full = [&](int i) { return bars + 8 * (6 + i); };
-  auto can_empty = [&](int i) { return bars + 8 * (8 + i); };
-  auto tm_full = [&](int i) { return bars + 8 * (10 + i); };
-  auto tm_empty = [&](int i) { return bars + 8 * (12 + i); };
+  auto raw_empty = [&](int i) { return bars + 8 * (R + i); };
+  auto can_full = [&](int i) { return bars + 8 * (2 * R + i); };
+  auto can_empty = [&](int i) { return bars + 8 * (2 * R + CS + i); };
+  auto tm_full = [&](int i) { return bars + 8 * (2 * R + 2 * CS + i); };
+  auto tm_empty = [&](int i) { return bars + 8 * (2 * R + 2 * CS + 2 + i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kBarOff + 128);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRawSlots; ++i) {
+#ifdef HB_K3_LDGSTS
+      bar_init(raw_full(i), 32);
+#else
       bar_init(raw_full(i), 1);
+#endif
       bar_init(raw_empty(i), kConvWarps);
     }
     for (int i = 0; i < kCanSlots; ++i) {
@@ -275,18 +335,23 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  const int nv = p.tab->n;
+  const int v0 = p.tab->n16;                      // F16 vjob3 go to k3d_kernel
+  const int nv = p.tab->n - v0;
   const int per_v = NMAT == 2 ? p.F / kRows : (p.H / kRows) * p.ks;
   const int n_items = nv * per_v;
   const int Kdim = NMAT == 2 ? p.H : p.F;          // reduction length of the matrix
   const int Kitem = NMAT == 2 ? p.H : p.F / p.ks;  // K per item
 
   if (warp == kProdWarp) {
+#ifdef HB_K3_LDGSTS
+    if (true) {
+#else
     if (lane == 0) {
-      int rs = 0;
+#endif
+      int rs = 0, ntr = 0;
       uint32_t rph = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const Item I = item_of<NMAT>(p, it);
+        const Item I = item_of<NMAT>(p, it, v0);
         const int enc = I.v->enc;
         const int epg = epg_of_enc(enc), ru = raw_units(enc), sb = scale_rec(enc);
         const int G = Kdim / epg;
@@ -297,29 +362,45 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
         const uint8_t* blob = I.v->blob;
         for (int r = 0; r < nraw; ++r) {
           bar_wait(raw_empty(rs), rph ^ 1);
+#ifndef HB_K3_LDGSTS
           bar_expect_tx(raw_full(rs), tx);
+#endif
           const uint32_t dst = sbase + rs * kRawBytes;
 #pragma unroll
           for (int m = 0; m < NMAT; ++m) {
             const MatLayout& ML = p.lay[enc].mat[NMAT == 2 ? m : 2];
             for (int t = 0; t < 8; ++t) {
               const long long unit = (long long)(I.tile * 8 + t) * G + g0 + r * ru;
+#ifdef HB_K3_LDGSTS
+              for (uint32_t o = lane * 16; o < cbytes; o += 512)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             :: "r"(dst + (m * 8 + t) * cbytes + o), "l"(blob + ML.q + 1024 * unit + o));
+              for (uint32_t o = lane * 16; o < sbytes; o += 512)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             :: "r"(dst + kRawCode + (m * 8 + t) * sbytes + o),
+                                "l"(blob + ML.s + 16 * sb * unit + o));
+#else
               bulk_g2s(dst + (m * 8 + t) * cbytes, blob + ML.q + 1024 * unit, cbytes, raw_full(rs));
               if (sb)
                 bulk_g2s(dst + kRawCode + (m * 8 + t) * sbytes, blob + ML.s + 16 * sb * unit,
                          sbytes, raw_full(rs));
+#endif
             }
           }
+#ifdef HB_K3_LDGSTS
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(raw_full(rs)) : "memory");
+#endif
+          K3_STAMP(0, ntr++);
           if (++rs == kRawSlots) { rs = 0; rph ^= 1; }
         }
       }
     }
   } else if (warp < kConvWarps) {
     const int tid = threadIdx.x;
-    int rs = 0, cs = 0;
+    int rs = 0, cs = 0, ntr = 0, ntc = 0;
     uint32_t rph = 0, cph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const Item I = item_of<NMAT>(p, it);
+      const Item I = item_of<NMAT>(p, it, v0);
       const int enc = I.v->enc, np = I.v->np;
       const int epg = epg_of_enc(enc), ru = raw_units(enc), sb = scale_rec(enc);
       const int nraw = Kitem / (ru * epg);
@@ -328,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
                            (size_t)I.ks * (Kitem / kBK) * np * kBK;
       for (int r = 0; r < nraw; ++r) {
         bar_wait(raw_full(rs), rph);
+        if (tid == 0) K3_STAMP(1, ntr++);
         const uint32_t raw = sbase + rs * kRawBytes;
         for (int c = 0; c < cpr; ++c) {
           bar_wait(can_empty(cs), cph ^ 1);
@@ -338,8 +420,8 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
             bulk_g2s(can + kABytes, bsrc + (size_t)kstep * np * kBK, np * kBK * 2, can_full(cs));
           }
 #pragma unroll
-          for (int i = 0; i < 4 * NMAT; ++i) {
-            const int idx = i * 256 + tid;
+          for (int i = 0; i < 2 * NMAT; ++i) {
+            const int idx = i * kConvThreads + tid;
             const int m = idx >> 10, ci = idx & 1023;
             const int q = ci & 7, kcrot = (ci >> 3) & 7, rb = ci >> 6;
             const int row = rb * 8 + q, kc = (kcrot + (q >> 1)) & 7;
@@ -349,12 +431,19 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
             const int su = (m * 8 + tl) * ru + u;
             const uint32_t code = raw + su * 1024 + rr * 64;
             const uint32_t sc = raw + kRawCode + su * 16 * sb + rr * sb;
+#ifdef HB_K3_NOCONV
+            const uint4 w = make_uint4(code, sc, e, 0);
+#else
             const uint4 w = dequant8(enc, code, sc, e);
+#endif
             sts128(can + m * kAMat + (row >> 3) * 1024 + kc * 128 + (row & 7) * 16, w);
           }
+#ifndef HB_K3_NOFENCE
           fence_async_smem();
+#endif
           __syncwarp();
           if (lane == 0) bar_arrive(can_full(cs));
+          if (tid == 0) K3_STAMP(2, ntc++);
           if (++cs == kCanSlots) { cs = 0; cph ^= 1; }
         }
         __syncwarp();
@@ -364,10 +453,10 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
     }
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
-      int cs = 0, ab = 0;
+      int cs = 0, ab = 0, ntm = 0;
       uint32_t cph = 0, abph = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const Item I = item_of<NMAT>(p, it);
+        const Item I = item_of<NMAT>(p, it, v0);
         const int np = I.v->np;
         const uint32_t idesc = idesc_f16(np);
         const int nsteps = Kitem / kBK;
@@ -377,13 +466,16 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
         for (int s = 0; s < nsteps; ++s) {
           bar_wait(can_full(cs), cph);
           tc_fence_after();
+          K3_STAMP(3, ntm++);
           const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kCanBytes;
+#ifndef HB_K3_NOMMA
 #pragma unroll
           for (int m = 0; m < NMAT; ++m)
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
               umma(tacc + m * 128, sdesc(can + m * kAMat + kk * 256), sdesc(can + kABytes + kk * 256),
                    idesc, (s | kk) ? 1u : 0u);
+#endif
           umma_commit(can_empty(cs));
           if (++cs == kCanSlots) { cs = 0; cph ^= 1; }
         }
@@ -391,47 +483,15 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
         if (++ab == 2) { ab = 0; abph ^= 1; }
       }
     }
-  } else {  // epilogue warps 8..11
+  } else {  // epilogue warps 16..19
     const int q4 = warp & 3;
     int ab = 0;
     uint32_t abph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const Item I = item_of<NMAT>(p, it);
-      const int np = I.v->np, n_real = I.v->n;
+      const Item I = item_of<NMAT>(p, it, v0);
       bar_wait(tm_full(ab), abph);
       tc_fence_after();
-      const int row = I.tile * kRows + q4 * 32 + lane;   // weight row of this thread
-      const uint32_t tacc = tbase + ((uint32_t)(q4 * 32) << 16) + ab * 256;
-      for (int n0 = 0; n0 < np; n0 += 16) {
-        if (NMAT == 2) {
-          float a[16], uu[16];
-          tmem_ld16(tacc + n0, a);
-          tmem_ld16(tacc + 128 + n0, uu);
-          // h (fp16) into hB in K3b's canonical B layout: K index = row (of F)
-          __half* hb = p.hB + I.v->hoff + (size_t)(row >> 6) * np * kBK +
-                       ((row & 63) >> 3) * 64 + (row & 7);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int n = n0 + i;
-            const float s = a[i] / (1.0f + __expf(-a[i]));
-            const float hv = n < n_real ? s * uu[i] : 0.0f;
-            hb[(n >> 3) * 512 + (n & 7) * 8] = __float2half_rn(hv);
-          }
-        } else {
-          float o[16];
-          tmem_ld16(tacc + n0, o);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int n = n0 + i;
-            if (n < n_real) {
-              const int slot = I.v->slot0 + n;
-              const int tok = p.jt.slot_token[slot];
-              const float g = p.jt.slot_gate[slot];
-              atomicAdd(p.y + (size_t)tok * p.H + row, g * o[i]);
-            }
-          }
-        }
-      }
+      epilogue_item<NMAT>(p, I, tbase + ((uint32_t)(q4 * 32) << 16) + ab * 256, q4, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(tm_empty(ab));
@@ -446,6 +506,148 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
   }
 }
 
+// ---------------------------------------------------------------- F16 direct
+// F16 items: the fp16 weights need no conversion, so the producer moves them
+// with 4-D TMA tensor copies (tensor map per matrix over our unit layout:
+// dims k%32 | row-in-tile | tile | group, box 32 x 16 x 8 x 2 = 128 rows x 64 K)
+// straight into shared memory in the UMMA K-major SWIZZLE_64B layout (8-row x
+// 64 B atoms, 16-byte chunks XOR (row/2)%4).  No converter warps; the ring
+// holds 4 (K3a) / 6 (K3b) stages.
+constexpr int kDThreads = 256;            // warp 0 producer, 1 MMA, 4..7 epilogue
+template <int NMAT>
+constexpr int d_slots() { return NMAT == 2 ? 4 : 6; }
+template <int NMAT>
+constexpr int d_slot_bytes() { return NMAT * kAMat + kBBytes; }
+template <int NMAT>
+constexpr int d_smem() { return d_slots<NMAT>() * d_slot_bytes<NMAT>() + 1024 + 256; }
+
+__device__ __forceinline__ void tma4(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c3,
+                                     uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];"
+      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar) : "memory");
+}
+// K-major SWIZZLE_64B: LBO field 1 (unused), SBO = 8 rows x 64 B = 512 B
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) |
+         ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+template <int NMAT>
+__global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
+  constexpr int S = d_slots<NMAT>(), SB = d_slot_bytes<NMAT>();
+  extern __shared__ uint8_t smd[];
+  const uint32_t raw0 = su32(smd);
+  const uint32_t sbase = (raw0 + 1023) & ~1023u;            // swizzle atoms: 1 KB aligned
+  const uint32_t bars = sbase + S * SB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto full = [&](int i) { return bars + 8 * i; };
+  auto empty = [&](int i) { return bars + 8 * (S + i); };
+  auto tm_full = [&](int i) { return bars + 8 * (2 * S + i); };
+  auto tm_empty = [&](int i) { return bars + 8 * (2 * S + 2 + i); };
+  const uint32_t tslot = bars + 8 * (2 * S + 4);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      bar_init(full(i), 1);
+      bar_init(empty(i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(tm_full(i), 1);
+      bar_init(tm_empty(i), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 :: "r"(tslot) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tbase;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tbase) : "r"(tslot));
+
+  const int nv = p.tab->n16;
+  const int per_v = NMAT == 2 ? p.F / kRows : (p.H / kRows) * p.ks;
+  const int n_items = nv * per_v;
+  const int Kitem = NMAT == 2 ? p.H : p.F / p.ks;
+  const int nsteps = Kitem / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int cs = 0;
+      uint32_t cph = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item I = item_of<NMAT>(p, it, 0);
+        const int np = I.v->np;
+        const CUtensorMap* tm = p.tmap + I.v->expert * 3;
+        const __half* bsrc = (NMAT == 2 ? p.xg + I.v->xoff : p.hB + I.v->hoff) +
+                             (size_t)I.ks * nsteps * np * kBK;
+        const int g0 = I.ks * (Kitem / 32);
+        for (int s = 0; s < nsteps; ++s) {
+          bar_wait(empty(cs), cph ^ 1);
+          const uint32_t dst = sbase + cs * SB;
+          bar_expect_tx(full(cs), NMAT * kAMat + np * kBK * 2);
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m)
+            tma4(dst + m * kAMat, tm + (NMAT == 2 ? m : 2), 0, 0, I.tile * 8, g0 + 2 * s, full(cs));
+          bulk_g2s(dst + NMAT * kAMat, bsrc + (size_t)s * np * kBK, np * kBK * 2, full(cs));
+          if (++cs == S) { cs = 0; cph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int cs = 0, ab = 0;
+      uint32_t cph = 0, abph = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item I = item_of<NMAT>(p, it, 0);
+        const uint32_t idesc = idesc_f16(I.v->np);
+        bar_wait(tm_empty(ab), abph ^ 1);
+        tc_fence_after();
+        const uint32_t tacc = tbase + ab * 256;
+        for (int s = 0; s < nsteps; ++s) {
+          bar_wait(full(cs), cph);
+          tc_fence_after();
+          const uint32_t st = sbase + cs * SB;
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma(tacc + m * 128, sdesc_sw64(st + m * kAMat + (kk >> 1) * 8192 + (kk & 1) * 32),
+                   sdesc(st + NMAT * kAMat + kk * 256), idesc, (s | kk) ? 1u : 0u);
+          umma_commit(empty(cs));
+          if (++cs == S) { cs = 0; cph ^= 1; }
+        }
+        umma_commit(tm_full(ab));
+        if (++ab == 2) { ab = 0; abph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    int ab = 0;
+    uint32_t abph = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item I = item_of<NMAT>(p, it, 0);
+      bar_wait(tm_full(ab), abph);
+      tc_fence_after();
+      epilogue_item<NMAT>(p, I, tbase + ((uint32_t)(q4 * 32) << 16) + ab * 256, q4, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(tm_empty(ab));
+      if (++ab == 2) { ab = 0; abph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tbase) : "memory");
+  }
+}
+
 // vjob3 table from the router's job table (every CTA rebuilds it in shared
 // memory; CTA 0 publishes it) + gather of X into xg (canonical B layout).
 __global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* __restrict__ x) {
@@ -453,14 +655,19 @@ __global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* 
   __shared__ int s_n;
   if (threadIdx.x == 0) {
     const int nj = p.jt.hdr[0];
-    int n = 0;
+    int n = 0, n16 = 0;
     long long xo = 0, ho = 0;
+    // F16 jobs first (k3d_kernel: TMA straight into the MMA layout), then the rest
+    for (int pass = 0; pass < 2; ++pass)
     for (int j = 0; j < nj; ++j) {
       const Job J = p.jt.jobs[j];
+      if ((J.enc == HB_F16) != (pass == 0)) continue;
       for (int s = 0; s < J.n_tok && n < kK3MaxV3; s += kK3MaxN) {
         V3 v;
         v.blob = J.blob;
         v.enc = J.enc;
+        v.expert = J.expert;
+        n16 += pass == 0;
         v.slot0 = J.slot_off + s;
         v.n = J.n_tok - s < kK3MaxN ? J.n_tok - s : kK3MaxN;
         v.np = (v.n + 15) & ~15;
@@ -472,7 +679,10 @@ __global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* 
       }
     }
     s_n = n;
-    if (blockIdx.x == 0) p.tab->n = n;
+    if (blockIdx.x == 0) {
+      p.tab->n = n;
+      p.tab->n16 = n16;
+    }
   }
   __syncthreads();
   const int nv = s_n;
@@ -509,18 +719,57 @@ void set_smem_once(K kernel, int bytes, bool& done) {
 
 int k3_smem_bytes() { return kSmem; }
 
+// Tensor map of an F16 matrix [n, k] stored as units (oracle/formats.py):
+// element (row, kk) at byte 1024*(G*(row/16) + kk/32) + 64*(row%16) + 2*(kk%32).
+int k3_encode_f16_map(CUtensorMap* out, const void* q, int n, int k) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                          CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                          CUtensorMapFloatOOBfill);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess || !f)
+      return -1;
+    fn = reinterpret_cast<Fn>(f);
+  }
+  const cuuint64_t G = (cuuint64_t)k / 32;
+  const cuuint64_t dims[4] = {32, 16, (cuuint64_t)n / 16, G};
+  const cuuint64_t strides[3] = {64, G * 1024, 1024};          // bytes, dims 1..3
+  const cuuint32_t box[4] = {32, 16, 8, 2};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(q), dims, strides, box,
+                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+}  // namespace hb
+#ifdef HB_K3_TRACE
+extern "C" int hb_k3_trace(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, hb::g_k3_trace, bytes) == cudaSuccess ? 0 : -4;
+}
+#endif
+namespace hb {
+
 void launch_k3_prep(const K3Params& p, const __half* x, cudaStream_t s) {
   k3_prep_kernel<<<2 * kNumSM, 256, 0, s>>>(p, x);
 }
 void launch_k3a(const K3Params& p, cudaStream_t s) {
-  static bool d = false;
+  static bool d = false, dd = false;
   set_smem_once(k3_kernel<2>, kSmem, d);
-  k3_kernel<2><<<kNumSM, kThreads, kSmem, s>>>(p);
+  set_smem_once(k3d_kernel<2>, d_smem<2>(), dd);
+  if (p.tmap) k3d_kernel<2><<<kNumSM, kDThreads, d_smem<2>(), s>>>(p);
+  if (p.has_q) k3_kernel<2><<<kNumSM, kThreads, kSmem, s>>>(p);
 }
 void launch_k3b(const K3Params& p, cudaStream_t s) {
-  static bool d = false;
+  static bool d = false, dd = false;
   set_smem_once(k3_kernel<1>, kSmem, d);
-  k3_kernel<1><<<kNumSM, kThreads, kSmem, s>>>(p);
+  set_smem_once(k3d_kernel<1>, d_smem<1>(), dd);
+  if (p.tmap) k3d_kernel<1><<<kNumSM, kDThreads, d_smem<1>(), s>>>(p);
+  if (p.has_q) k3_kernel<1><<<kNumSM, kThreads, kSmem, s>>>(p);
 }
 
 }  // namespace hb

@@ -1,6 +1,8 @@
 // K3: tcgen05 grouped GEMM for batched decode / prefill.
 #pragma once
 
+#include <cuda.h>
+
 #include "hb_internal.h"
 
 namespace hb {
@@ -15,12 +17,15 @@ struct V3 {
   int32_t slot0;
   int32_t n;
   int32_t np;
+  int32_t expert;
+  int32_t pad;
   long long xoff;                // fp16 elements: this vjob3's X in xg (np * H)
   long long hoff;                // fp16 elements: its h in hB (np * F)
 };
 struct K3Table {
   int32_t n;
-  int32_t pad[3];
+  int32_t n16;                   // entries [0, n16) are F16 (k3d_kernel), the rest quantised
+  int32_t pad[2];
   V3 v[kK3MaxV3];
 };
 
@@ -33,7 +38,11 @@ struct K3Params {
   __half* hB;                    // h, same layout [v][F/64][np x 64]
   float* y;                      // [B][H] fp32, zeroed by the router
   K3Table* tab;
+  const CUtensorMap* tmap;       // [E][3] F16 tensor maps of this layer (null: no F16 path)
+  int has_q;                     // quantised encodings in the pair (launch k3_kernel)
 };
+// 4-D tensor map of one F16 matrix [n rows, k] in the unit layout (host)
+int k3_encode_f16_map(CUtensorMap* out, const void* q, int n, int k);
 
 int k3_smem_bytes();
 void launch_k3_prep(const K3Params& p, const __half* x, cudaStream_t s);
