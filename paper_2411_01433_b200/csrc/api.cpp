@@ -93,13 +93,13 @@ struct hb_ctx {
   int chunk = 8;
   // K3: tcgen05 grouped GEMM for batches >= k3_min_batch (A9); buffers exist
   // when max_batch > 1 and the vjob3 table bound fits
-  int k3_min_batch = 32;                  // HB_K3_MIN_BATCH / hb_set_batched_min
+  int k3_min_batch = 8;                   // HB_K3_MIN_BATCH / hb_set_batched_min (K3 wins from B = 8, profiles/r01_batched.md)
   bool k3_ok = false;
   int k3_ks = 1;
   __half* k3_xg = nullptr;
   __half* k3_hB = nullptr;
   K3Table* k3_tab = nullptr;
-  CUtensorMap* k3_tmap = nullptr;         // [L][E][3] device tensor maps of F16 blobs
+  CUtensorMap* k3_tmap = nullptr;         // [L][E][4][6] device tensor maps of the blobs (K3)
   cudaEvent_t dec_ready = nullptr;
   // kernel timing (hb_profile)
   std::vector<cudaEvent_t> prof_ev;       // 3 per recorded forward
@@ -285,8 +285,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     if (B > 1 && max_v3 <= kK3MaxV3) {
       if (!dm((void**)&c->k3_xg, rows * H * 2) || !dm((void**)&c->k3_hB, rows * F * 2) ||
           !dm((void**)&c->k3_tab, sizeof(K3Table)) ||
-          (resident && (k.hi_enc == HB_F16 || k.lo_enc == HB_F16) &&
-           !dm((void**)&c->k3_tmap, sizeof(CUtensorMap) * (size_t)L * E * 3)))
+          (resident && !dm((void**)&c->k3_tmap, sizeof(CUtensorMap) * (size_t)L * E * 24)))
         return bail(HB_ENOMEM, "K3 scratch allocation failed");
       c->k3_ok = true;
       c->k3_ks = (F / 2) % 256 == 0 ? 2 : 1;
@@ -388,14 +387,20 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
     if (flags != HB_REG_DEVICE_BORROW) return fail(c, HB_EINVAL, "resident mode takes device blobs");
     c->dev_blob[idx] = (const uint8_t*)blob;
     CUDA_TRY(c, cudaSetDevice(c->device));
-    if (enc == HB_F16 && c->k3_tmap) {          // K3 F16 path: TMA tensor maps of W1, W3, W2
-      CUtensorMap m[3];
+    if (c->k3_tmap) {                           // K3: TMA tensor maps of W1, W3, W2
+      CUtensorMap m[6];
+      std::memset(m, 0, sizeof(m));
       const int rows[3] = {k.ffn, k.ffn, k.hidden}, cols[3] = {k.hidden, k.hidden, k.ffn};
-      for (int i = 0; i < 3; ++i)
-        if (k3_encode_f16_map(&m[i], (const uint8_t*)blob + c->lay[HB_F16].mat[i].q, rows[i], cols[i]))
-          return fail(c, HB_ECUDA, "cuTensorMapEncodeTiled failed");
-      CUDA_TRY(c, cudaMemcpy(c->k3_tmap + ((size_t)layer * k.n_experts + expert) * 3, m, sizeof(m),
-                             cudaMemcpyHostToDevice));
+      const uint8_t* b = (const uint8_t*)blob;
+      for (int i = 0; i < 3; ++i) {
+        const MatLayout& ML = c->lay[enc].mat[i];
+        const int rc = enc == HB_F16 ? k3_encode_f16_map(&m[i], b + ML.q, rows[i], cols[i])
+                                     : k3_encode_q_maps(&m[i], &m[3 + i], enc, b + ML.q, b + ML.s,
+                                                        rows[i], cols[i]);
+        if (rc) return fail(c, HB_ECUDA, "cuTensorMapEncodeTiled failed");
+      }
+      CUDA_TRY(c, cudaMemcpy(c->k3_tmap + (((size_t)layer * k.n_experts + expert) * 4 + enc) * 6, m,
+                             sizeof(m), cudaMemcpyHostToDevice));
     }
     CUDA_TRY(c, cudaMemcpy(c->dev_blob_table + idx, &c->dev_blob[idx], sizeof(void*),
                            cudaMemcpyHostToDevice));
@@ -519,7 +524,8 @@ static void launch_batched(hb_ctx* c, int layer, const void* x, void* y, cudaStr
   kp.hB = c->k3_hB;
   kp.y = (float*)y;
   kp.tab = c->k3_tab;
-  kp.tmap = c->k3_tmap ? c->k3_tmap + (size_t)layer * c->cfg.n_experts * 3 : nullptr;
+  kp.tmap = c->k3_tmap + (size_t)layer * c->cfg.n_experts * 24;
+  kp.has_f16 = c->cfg.hi_enc == HB_F16 || c->cfg.lo_enc == HB_F16;
   kp.has_q = c->cfg.hi_enc != HB_F16 || c->cfg.lo_enc != HB_F16;
   cudaEvent_t* ev = nullptr;
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
@@ -529,7 +535,7 @@ static void launch_batched(hb_ctx* c, int layer, const void* x, void* y, cudaStr
   if (ev) cudaEventRecord(ev[1], s);
   launch_k3b(kp, s);
   if (ev) cudaEventRecord(ev[2], s);
-  c->launches += 1 + 2 * ((kp.tmap != nullptr) + kp.has_q);
+  c->launches += 1 + 2 * (kp.has_f16 + kp.has_q);
 }
 
 static const __half* router_of(hb_ctx* c, int layer) {

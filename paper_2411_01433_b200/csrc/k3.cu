@@ -42,22 +42,25 @@ namespace {
 
 constexpr int kRows = 128;                 // weight rows per tile = MMA M
 constexpr int kBK = 64;                    // K elements per canonical stage
-constexpr int kRawSlots = 2;
+constexpr int kRawSlots = 4;
 constexpr int kCanSlots = 3;
+constexpr int kMaxBSlots = 8;
 constexpr int kConvWarps = 16;             // warps 0..15 dequantise
 constexpr int kConvThreads = kConvWarps * 32;
-constexpr int kMmaWarp = 20;               // warps 16..19 epilogue (warp % 4 = lane quarter)
-constexpr int kProdWarp = 21;
-constexpr int kThreads = 22 * 32;
-constexpr int kRawCode = 32768;            // 2 matrices x 8 tiles of 16 rows x 2 units
+constexpr int kEpiWarp0 = 16;              // warps 16..19 epilogue (warp % 4 = TMEM lane quarter)
+constexpr int kMmaWarp = 20;
+constexpr int kProdWarp = 21;              // raw codes + scales
+constexpr int kBProdWarp = 22;             // B tiles
+constexpr int kThreads = 23 * 32;
+constexpr int kRawCode = 16384;            // NMAT x 8 tiles x ru units of 1 KB
 constexpr int kRawScale = 8192;
 constexpr int kRawBytes = kRawCode + kRawScale;
-constexpr int kAMat = kRows * kBK * 2;     // 16 KB canonical A per matrix
+constexpr int kAMat = kRows * kBK * 2;     // 16 KB fp16 A tile per matrix
 constexpr int kABytes = 2 * kAMat;
-constexpr int kBBytes = kK3MaxN * kBK * 2; // 16 KB canonical B
-constexpr int kCanBytes = kABytes + kBBytes;
-constexpr int kBarOff = kRawSlots * kRawBytes + kCanSlots * kCanBytes;
-constexpr int kSmem = kBarOff + 256;
+constexpr int kBBytes = kK3MaxN * kBK * 2; // 16 KB: largest B tile (np = 128)
+constexpr int kBRing = 32768;
+constexpr int kBarOff = kRawSlots * kRawBytes + kCanSlots * kABytes + kBRing;
+constexpr int kSmem = kBarOff + 512 + 1024;   // + alignment slack (swizzle atoms: 1 KB)
 
 #ifdef HB_K3_TRACE
 // diagnostic timeline (tools/k3_trace.py): CTA 0 stamps %globaltimer per event
@@ -103,6 +106,20 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
       :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+__device__ __forceinline__ void tma4(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c3,
+                                     uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];"
+      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma3(uint32_t dst, const void* tmap, int c0, int c1, int c2,
+                                     uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];"
+      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -118,6 +135,12 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
          ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46);
 }
+// K-major SWIZZLE_64B: LBO field 1 (unused), SBO = 8 rows x 64 B = 512 B
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) |
+         ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
 // kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N, M=128
 __device__ __forceinline__ uint32_t idesc_f16(int n) {
   return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
@@ -150,6 +173,11 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
   return d;
+}
+__device__ __forceinline__ uint32_t and_or(uint32_t x, uint32_t m, uint32_t c) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(x), "r"(m), "r"(c));   // (a & b) | c
+  return r;
 }
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
@@ -191,10 +219,10 @@ __device__ __forceinline__ uint4 dequant8(int enc, uint32_t code, uint32_t sc, i
     const uint32_t v = lds32(code + 16 * t + 4 * j);
     const uint32_t A = v & 0x0F0F0F0Fu, B = (v >> 4) & 0x0F0F0F0Fu;
     const __half2 off = u2h(0x64086408u);                  // (1032, 1032)
-    o.x = h2u(__hmul2(__hsub2(u2h((prmt(A, B, 0x0400) & 0x00FF00FFu) | 0x64006400u), off), d));
-    o.y = h2u(__hmul2(__hsub2(u2h((prmt(A, B, 0x0501) & 0x00FF00FFu) | 0x64006400u), off), d));
-    o.z = h2u(__hmul2(__hsub2(u2h((prmt(A, B, 0x0602) & 0x00FF00FFu) | 0x64006400u), off), d));
-    o.w = h2u(__hmul2(__hsub2(u2h((prmt(A, B, 0x0703) & 0x00FF00FFu) | 0x64006400u), off), d));
+    o.x = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0400), 0x00FF00FFu, 0x64006400u)), off), d));
+    o.y = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0501), 0x00FF00FFu, 0x64006400u)), off), d));
+    o.z = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0602), 0x00FF00FFu, 0x64006400u)), off), d));
+    o.w = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0703), 0x00FF00FFu, 0x64006400u)), off), d));
   } else if (enc == HB_Q8) {
     // int8 ^ 0x80 = q + 128 in [1, 255]: (1024 + q + 128) - 1152 exact
     const uint32_t a = lds32(code + 16 * t + 8 * j) ^ 0x80808080u;
@@ -213,18 +241,82 @@ __device__ __forceinline__ uint4 dequant8(int enc, uint32_t code, uint32_t sc, i
     // (q0 bits 0-1 | q1 bits 18-19) and (q2 bits 4-5 | q3 bits 22-23), magic 0x6400
     const __half2 n01 = u2h(0x34003C00u), b01 = u2h(0xDC00E400u);  // (1, 1/4), (-1024, -256)
     const __half2 n23 = u2h(0x24002C00u), b23 = u2h(0xCC00D400u);  // (1/16, 1/64), (-64, -16)
-    o.x = h2u(__hfma2(__hfma2(u2h((c0 & 0x000C0003u) | 0x64006400u), n01, b01), d, m));
-    o.y = h2u(__hfma2(__hfma2(u2h((c0 & 0x00C00030u) | 0x64006400u), n23, b23), d, m));
-    o.z = h2u(__hfma2(__hfma2(u2h((c1 & 0x000C0003u) | 0x64006400u), n01, b01), d, m));
-    o.w = h2u(__hfma2(__hfma2(u2h((c1 & 0x00C00030u) | 0x64006400u), n23, b23), d, m));
+    o.x = h2u(__hfma2(__hfma2(u2h(and_or(c0, 0x000C0003u, 0x64006400u)), n01, b01), d, m));
+    o.y = h2u(__hfma2(__hfma2(u2h(and_or(c0, 0x00C00030u, 0x64006400u)), n23, b23), d, m));
+    o.z = h2u(__hfma2(__hfma2(u2h(and_or(c1, 0x000C0003u, 0x64006400u)), n01, b01), d, m));
+    o.w = h2u(__hfma2(__hfma2(u2h(and_or(c1, 0x00C00030u, 0x64006400u)), n23, b23), d, m));
   }
   return o;
+}
+
+__device__ __forceinline__ uint4 q4_chunk(uint32_t v, __half2 d) {
+  const uint32_t A = v & 0x0F0F0F0Fu, B = (v >> 4) & 0x0F0F0F0Fu;
+  const __half2 off = u2h(0x64086408u);                    // (1032, 1032)
+  uint4 o;
+  o.x = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0400), 0x00FF00FFu, 0x64006400u)), off), d));
+  o.y = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0501), 0x00FF00FFu, 0x64006400u)), off), d));
+  o.z = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0602), 0x00FF00FFu, 0x64006400u)), off), d));
+  o.w = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0703), 0x00FF00FFu, 0x64006400u)), off), d));
+  return o;
+}
+__device__ __forceinline__ uint4 q8_chunk(uint32_t a, uint32_t b, __half2 d) {
+  a ^= 0x80808080u;
+  b ^= 0x80808080u;
+  const uint32_t M = 0x64646464u;
+  const __half2 off = u2h(0x64806480u);                    // (1152, 1152)
+  uint4 o;
+  o.x = h2u(__hmul2(__hsub2(u2h(prmt(a, M, 0x5150)), off), d));
+  o.y = h2u(__hmul2(__hsub2(u2h(prmt(a, M, 0x5352)), off), d));
+  o.z = h2u(__hmul2(__hsub2(u2h(prmt(b, M, 0x5150)), off), d));
+  o.w = h2u(__hmul2(__hsub2(u2h(prmt(b, M, 0x5352)), off), d));
+  return o;
+}
+// c0 = [byte(q0..3), 0, byte(q0..3), 0], c1 likewise for q4..7
+__device__ __forceinline__ uint4 q2_chunk(uint32_t c0, uint32_t c1, __half2 d, __half2 m) {
+  const __half2 n01 = u2h(0x34003C00u), b01 = u2h(0xDC00E400u);  // (1, 1/4), (-1024, -256)
+  const __half2 n23 = u2h(0x24002C00u), b23 = u2h(0xCC00D400u);  // (1/16, 1/64), (-64, -16)
+  uint4 o;
+  o.x = h2u(__hfma2(__hfma2(u2h(and_or(c0, 0x000C0003u, 0x64006400u)), n01, b01), d, m));
+  o.y = h2u(__hfma2(__hfma2(u2h(and_or(c0, 0x00C00030u, 0x64006400u)), n23, b23), d, m));
+  o.z = h2u(__hfma2(__hfma2(u2h(and_or(c1, 0x000C0003u, 0x64006400u)), n01, b01), d, m));
+  o.w = h2u(__hfma2(__hfma2(u2h(and_or(c1, 0x00C00030u, 0x64006400u)), n23, b23), d, m));
+  return o;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+// Two consecutive 8-element K chunks (blocks j0, j0 + 1, same 8-element
+// position t) of one row: code/sc point at this step's bytes of the row.
+__device__ __forceinline__ void dequant16(int enc, uint32_t code, uint32_t sc, uint4& w0, uint4& w1) {
+  const uint32_t dd = lds32(sc);                           // d[j0] | d[j0 + 1] << 16
+  const __half2 d0 = u2h(prmt(dd, 0, 0x1010)), d1 = u2h(prmt(dd, 0, 0x3232));
+  if (enc == HB_Q4) {
+    const uint2 v = lds64(code);
+    w0 = q4_chunk(v.x, d0);
+    w1 = q4_chunk(v.y, d1);
+  } else if (enc == HB_Q8) {
+    const uint4 v = lds128(code);
+    w0 = q8_chunk(v.x, v.y, d0);
+    w1 = q8_chunk(v.z, v.w, d1);
+  } else {
+    const uint32_t mm = lds32(sc + 16);
+    const __half2 m0 = u2h(prmt(mm, 0, 0x1010)), m1 = u2h(prmt(mm, 0, 0x3232));
+    const uint32_t v = lds32(code);
+    w0 = q2_chunk(prmt(v, 0, 0x4040), prmt(v, 0, 0x4242), d0, m0);
+    w1 = q2_chunk(prmt(v, 0, 0x4141), prmt(v, 0, 0x4343), d1, m1);
+  }
 }
 
 __device__ __forceinline__ int scale_rec(int enc) {   // SB, bytes per (unit, row)
   return enc == HB_Q8 ? 4 : enc == HB_Q4 ? 8 : enc == HB_Q2 ? 32 : 0;
 }
-__device__ __forceinline__ int raw_units(int enc) { return enc == HB_Q2 ? 1 : 2; }
+// raw units per (matrix, 16-row tile) in one raw slot: 16 KB of codes per slot
+template <int NMAT>
+__device__ __forceinline__ int raw_units(int enc, int kitem) {
+  return NMAT == 2 ? 1 : (kitem % (2 * epg_of_enc(enc)) == 0 ? 2 : 1);
+}
 
 struct Item {
   const V3* v;
@@ -289,35 +381,39 @@ __device__ __forceinline__ void epilogue_item(const K3Params& p, const Item& I, 
   }
 }
 
-// Persistent tcgen05 GEMM.  NMAT = 2: K3a (W1, W3 over K = H; SwiGLU
-// epilogue); NMAT = 1: K3b (W2 over K = F / ks; Eq. 1 epilogue).
+// Quantised items (Q8/Q4/Q2): persistent tcgen05 GEMM.  NMAT = 2: K3a (W1, W3
+// over K = H; SwiGLU epilogue); NMAT = 1: K3b (W2 over K = F / ks; Eq. 1).
+// Rings: raw codes + scales (bulk copies, 4 x 24 KB) -> 16 converter warps ->
+// fp16 A tiles (2 x 32 KB); B tiles (X or h, np x 64) in their own ring of up
+// to 8 stages fed by a second producer, so their L2 latency is hidden.
 template <int NMAT>
 __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  const uint32_t sbase = su32(sm);
+  const uint32_t sbase = (su32(sm) + 1023) & ~1023u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bars = sbase + kBarOff;
-  // barriers: raw_full[R] raw_empty[R] can_full[C] can_empty[C] tm_full[2] tm_empty[2]
-  constexpr int R = kRawSlots, CS = kCanSlots;
+  constexpr int R = kRawSlots, CS = kCanSlots, BS = kMaxBSlots;
   auto raw_full = [&](int i) { return bars + 8 * i; };
   auto raw_empty = [&](int i) { return bars + 8 * (R + i); };
   auto can_full = [&](int i) { return bars + 8 * (2 * R + i); };
   auto can_empty = [&](int i) { return bars + 8 * (2 * R + CS + i); };
-  auto tm_full = [&](int i) { return bars + 8 * (2 * R + 2 * CS + i); };
-  auto tm_empty = [&](int i) { return bars + 8 * (2 * R + 2 * CS + 2 + i); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kBarOff + 128);
+  auto b_full = [&](int i) { return bars + 8 * (2 * R + 2 * CS + i); };
+  auto b_empty = [&](int i) { return bars + 8 * (2 * R + 2 * CS + BS + i); };
+  auto tm_full = [&](int i) { return bars + 8 * (2 * R + 2 * CS + 2 * BS + i); };
+  auto tm_empty = [&](int i) { return bars + 8 * (2 * R + 2 * CS + 2 * BS + 2 + i); };
+  const uint32_t tslot = bars + 8 * (2 * R + 2 * CS + 2 * BS + 4);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kRawSlots; ++i) {
-#ifdef HB_K3_LDGSTS
-      bar_init(raw_full(i), 32);
-#else
+    for (int i = 0; i < R; ++i) {
       bar_init(raw_full(i), 1);
-#endif
       bar_init(raw_empty(i), kConvWarps);
     }
-    for (int i = 0; i < kCanSlots; ++i) {
+    for (int i = 0; i < CS; ++i) {
       bar_init(can_full(i), kConvWarps);
       bar_init(can_empty(i), 1);
+    }
+    for (int i = 0; i < BS; ++i) {
+      bar_init(b_full(i), 1);
+      bar_init(b_empty(i), 1);
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(tm_full(i), 1);
@@ -327,13 +423,14 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
   }
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
-                 :: "r"(su32(tmem_slot)) : "memory");
+                 :: "r"(tslot) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
+  uint32_t tbase;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tbase) : "r"(tslot));
 
   const int v0 = p.tab->n16;                      // F16 vjob3 go to k3d_kernel
   const int nv = p.tab->n - v0;
@@ -341,149 +438,154 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
   const int n_items = nv * per_v;
   const int Kdim = NMAT == 2 ? p.H : p.F;          // reduction length of the matrix
   const int Kitem = NMAT == 2 ? p.H : p.F / p.ks;  // K per item
+  const int nsteps = Kitem / kBK;
+  // B ring geometry from the largest np of this launch's vjob3
+  int npmax = 16;
+  for (int v = v0; v < p.tab->n; ++v) npmax = max(npmax, p.tab->v[v].np);
+  const int bslot = npmax * kBK * 2;
+  const int nb = min(BS, kBRing / bslot);
+  const uint32_t bring = sbase + kRawSlots * kRawBytes + kCanSlots * kABytes;
 
   if (warp == kProdWarp) {
-#ifdef HB_K3_LDGSTS
-    if (true) {
-#else
-    if (lane == 0) {
-#endif
-      int rs = 0, ntr = 0;
+    if (lane == 0) {                               // raw codes + scales
+      int rs = 0, ntp = 0;
       uint32_t rph = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const Item I = item_of<NMAT>(p, it, v0);
         const int enc = I.v->enc;
-        const int epg = epg_of_enc(enc), ru = raw_units(enc), sb = scale_rec(enc);
+        const int epg = epg_of_enc(enc), ru = raw_units<NMAT>(enc, Kitem), sb = scale_rec(enc);
         const int G = Kdim / epg;
         const int nraw = Kitem / (ru * epg);
         const int g0 = I.ks * (Kitem / epg);
-        const uint32_t cbytes = ru * 1024, sbytes = ru * 16 * sb;
-        const uint32_t tx = NMAT * 8 * (cbytes + sbytes);
-        const uint8_t* blob = I.v->blob;
+        const uint32_t cbytes = 8 * ru * 1024, sbytes = 8 * ru * 16 * sb;   // per matrix
+        const uint32_t tx = NMAT * (cbytes + sbytes);
+        const CUtensorMap* tm = p.tmap + (I.v->expert * 4 + enc) * 6;
+        (void)G;
         for (int r = 0; r < nraw; ++r) {
           bar_wait(raw_empty(rs), rph ^ 1);
-#ifndef HB_K3_LDGSTS
+          if (NMAT == 2) K3_STAMP(0, ntp++);
           bar_expect_tx(raw_full(rs), tx);
-#endif
           const uint32_t dst = sbase + rs * kRawBytes;
+          // one tensor copy per (matrix, unit column): 8 tiles x 16 rows x 64 B
+          // of codes, 8 tiles x 16 scale records; raw slot [m][u][tile][...]
 #pragma unroll
           for (int m = 0; m < NMAT; ++m) {
-            const MatLayout& ML = p.lay[enc].mat[NMAT == 2 ? m : 2];
-            for (int t = 0; t < 8; ++t) {
-              const long long unit = (long long)(I.tile * 8 + t) * G + g0 + r * ru;
-#ifdef HB_K3_LDGSTS
-              for (uint32_t o = lane * 16; o < cbytes; o += 512)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                             :: "r"(dst + (m * 8 + t) * cbytes + o), "l"(blob + ML.q + 1024 * unit + o));
-              for (uint32_t o = lane * 16; o < sbytes; o += 512)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                             :: "r"(dst + kRawCode + (m * 8 + t) * sbytes + o),
-                                "l"(blob + ML.s + 16 * sb * unit + o));
-#else
-              bulk_g2s(dst + (m * 8 + t) * cbytes, blob + ML.q + 1024 * unit, cbytes, raw_full(rs));
-              if (sb)
-                bulk_g2s(dst + kRawCode + (m * 8 + t) * sbytes, blob + ML.s + 16 * sb * unit,
-                         sbytes, raw_full(rs));
-#endif
+            const int mi = NMAT == 2 ? m : 2;
+            for (int u = 0; u < ru; ++u) {
+              const int g = g0 + r * ru + u;
+              tma4(dst + m * cbytes + u * 8192, tm + mi, 0, 0, I.tile * 8, g, raw_full(rs));
+              tma3(dst + kRawCode + m * sbytes + u * 128 * sb, tm + 3 + mi, 0, I.tile * 8, g,
+                   raw_full(rs));
             }
           }
-#ifdef HB_K3_LDGSTS
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(raw_full(rs)) : "memory");
-#endif
-          K3_STAMP(0, ntr++);
-          if (++rs == kRawSlots) { rs = 0; rph ^= 1; }
+          if (++rs == R) { rs = 0; rph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == kBProdWarp) {
+    if (lane == 0) {                               // B tiles, one per canonical step
+      int bs = 0;
+      uint32_t bph = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item I = item_of<NMAT>(p, it, v0);
+        const int np = I.v->np;
+        const __half* bsrc = (NMAT == 2 ? p.xg + I.v->xoff : p.hB + I.v->hoff) +
+                             (size_t)I.ks * nsteps * np * kBK;
+        for (int s = 0; s < nsteps; ++s) {
+          bar_wait(b_empty(bs), bph ^ 1);
+          bar_expect_tx(b_full(bs), np * kBK * 2);
+          bulk_g2s(bring + bs * bslot, bsrc + (size_t)s * np * kBK, np * kBK * 2, b_full(bs));
+          if (++bs == nb) { bs = 0; bph ^= 1; }
         }
       }
     }
   } else if (warp < kConvWarps) {
     const int tid = threadIdx.x;
-    int rs = 0, cs = 0, ntr = 0, ntc = 0;
+    // thread = (row, t): its share of the row's raw piece for one 64-K step
+    // -> K chunks kc = t and 4 + t (blocks j0, j0 + 1).  Quarter-warps store
+    // 8 rows of one chunk: conflict-free 16-byte stores.
+    const int t = (tid >> 3) & 3, row = (tid & 7) + 8 * (tid >> 5);
+    const int tl = row >> 4, rr = row & 15;
+    int rs = 0, cs = 0, ntc = 0, ntr = 0;
     uint32_t rph = 0, cph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const Item I = item_of<NMAT>(p, it, v0);
-      const int enc = I.v->enc, np = I.v->np;
-      const int epg = epg_of_enc(enc), ru = raw_units(enc), sb = scale_rec(enc);
+      const int enc = I.v->enc;
+      const int epg = epg_of_enc(enc), ru = raw_units<NMAT>(enc, Kitem), sb = scale_rec(enc);
       const int nraw = Kitem / (ru * epg);
       const int cpr = ru * epg / kBK;               // canonical stages per raw slot
-      const __half* bsrc = (NMAT == 2 ? p.xg + I.v->xoff : p.hB + I.v->hoff) +
-                           (size_t)I.ks * (Kitem / kBK) * np * kBK;
       for (int r = 0; r < nraw; ++r) {
-        bar_wait(raw_full(rs), rph);
-        if (tid == 0) K3_STAMP(1, ntr++);
+        if (lane == 0) bar_wait(raw_full(rs), rph);     // one poller per warp
+        __syncwarp();
+        if (NMAT == 2 && tid == 0) K3_STAMP(1, ntr++);
         const uint32_t raw = sbase + rs * kRawBytes;
         for (int c = 0; c < cpr; ++c) {
-          bar_wait(can_empty(cs), cph ^ 1);
-          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kCanBytes;
-          if (tid == 0) {
-            const int kstep = r * cpr + c;
-            bar_add_tx(can_full(cs), np * kBK * 2);
-            bulk_g2s(can + kABytes, bsrc + (size_t)kstep * np * kBK, np * kBK * 2, can_full(cs));
-          }
+          if (lane == 0) bar_wait(can_empty(cs), cph ^ 1);
+          __syncwarp();
+          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
+          // step-uniform offsets inside the raw slot (oracle/formats.py layout)
+          const int u = enc == HB_Q8 ? c : enc == HB_Q4 ? (c >> 1) : (c >> 2);
+          const int coff = enc == HB_Q8 ? 0 : enc == HB_Q4 ? 8 * (c & 1) : 4 * (c & 3);
+          const int soff = enc == HB_Q8 ? 0 : enc == HB_Q4 ? 4 * (c & 1) : 4 * (c & 3);
 #pragma unroll
-          for (int i = 0; i < 2 * NMAT; ++i) {
-            const int idx = i * kConvThreads + tid;
-            const int m = idx >> 10, ci = idx & 1023;
-            const int q = ci & 7, kcrot = (ci >> 3) & 7, rb = ci >> 6;
-            const int row = rb * 8 + q, kc = (kcrot + (q >> 1)) & 7;
-            const int kr = c * kBK + kc * 8;       // K offset inside the raw slot
-            const int u = kr / epg, e = kr % epg;
-            const int tl = row >> 4, rr = row & 15;
-            const int su = (m * 8 + tl) * ru + u;
-            const uint32_t code = raw + su * 1024 + rr * 64;
-            const uint32_t sc = raw + kRawCode + su * 16 * sb + rr * sb;
-#ifdef HB_K3_NOCONV
-            const uint4 w = make_uint4(code, sc, e, 0);
-#else
-            const uint4 w = dequant8(enc, code, sc, e);
-#endif
-            sts128(can + m * kAMat + (row >> 3) * 1024 + kc * 128 + (row & 7) * 16, w);
+          for (int m = 0; m < NMAT; ++m) {
+            const int su = u * 8 + tl;                // raw slot [m][u][tile]
+            const uint32_t code = raw + m * (8 * ru * 1024) + su * 1024 + rr * 64 + 16 * t + coff;
+            const uint32_t sc = raw + kRawCode + m * (8 * ru * 16 * sb) + su * 16 * sb + rr * sb + soff;
+            uint4 w0, w1;
+            dequant16(enc, code, sc, w0, w1);
+            // UMMA K-major SWIZZLE_64B (as the TMA path): K chunk kc of a row in
+            // block kc / 4 (8 KB = 128 rows x 64 B), 16-byte slot (kc % 4) ^ ((row / 2) % 4)
+            const uint32_t dst = can + m * kAMat + row * 64 + ((t ^ ((row >> 1) & 3)) << 4);
+            sts128(dst, w0);
+            sts128(dst + 8192, w1);
           }
 #ifndef HB_K3_NOFENCE
           fence_async_smem();
 #endif
           __syncwarp();
           if (lane == 0) bar_arrive(can_full(cs));
-          if (tid == 0) K3_STAMP(2, ntc++);
-          if (++cs == kCanSlots) { cs = 0; cph ^= 1; }
+          if (NMAT == 2 && tid == 0) K3_STAMP(2, ntc++);
+          if (++cs == CS) { cs = 0; cph ^= 1; }
         }
         __syncwarp();
         if (lane == 0) bar_arrive(raw_empty(rs));
-        if (++rs == kRawSlots) { rs = 0; rph ^= 1; }
+        if (++rs == R) { rs = 0; rph ^= 1; }
       }
     }
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
-      int cs = 0, ab = 0, ntm = 0;
-      uint32_t cph = 0, abph = 0;
+      int cs = 0, bs = 0, ab = 0, ntm = 0;
+      uint32_t cph = 0, bph = 0, abph = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const Item I = item_of<NMAT>(p, it, v0);
-        const int np = I.v->np;
-        const uint32_t idesc = idesc_f16(np);
-        const int nsteps = Kitem / kBK;
+        const uint32_t idesc = idesc_f16(I.v->np);
         bar_wait(tm_empty(ab), abph ^ 1);
         tc_fence_after();
         const uint32_t tacc = tbase + ab * 256;
         for (int s = 0; s < nsteps; ++s) {
           bar_wait(can_full(cs), cph);
+          bar_wait(b_full(bs), bph);
+          if (NMAT == 2) K3_STAMP(3, ntm++);
           tc_fence_after();
-          K3_STAMP(3, ntm++);
-          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kCanBytes;
-#ifndef HB_K3_NOMMA
+          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
+          const uint32_t bt = bring + bs * bslot;
 #pragma unroll
           for (int m = 0; m < NMAT; ++m)
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
-              umma(tacc + m * 128, sdesc(can + m * kAMat + kk * 256), sdesc(can + kABytes + kk * 256),
-                   idesc, (s | kk) ? 1u : 0u);
-#endif
+              umma(tacc + m * 128, sdesc_sw64(can + m * kAMat + (kk >> 1) * 8192 + (kk & 1) * 32),
+                   sdesc(bt + kk * 256), idesc, (s | kk) ? 1u : 0u);
           umma_commit(can_empty(cs));
-          if (++cs == kCanSlots) { cs = 0; cph ^= 1; }
+          umma_commit(b_empty(bs));
+          if (++cs == CS) { cs = 0; cph ^= 1; }
+          if (++bs == nb) { bs = 0; bph ^= 1; }
         }
         umma_commit(tm_full(ab));
         if (++ab == 2) { ab = 0; abph ^= 1; }
       }
     }
-  } else {  // epilogue warps 16..19
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
     const int q4 = warp & 3;
     int ab = 0;
     uint32_t abph = 0;
@@ -520,19 +622,6 @@ template <int NMAT>
 constexpr int d_slot_bytes() { return NMAT * kAMat + kBBytes; }
 template <int NMAT>
 constexpr int d_smem() { return d_slots<NMAT>() * d_slot_bytes<NMAT>() + 1024 + 256; }
-
-__device__ __forceinline__ void tma4(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c3,
-                                     uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4, %5}], [%6];"
-      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar) : "memory");
-}
-// K-major SWIZZLE_64B: LBO field 1 (unused), SBO = 8 rows x 64 B = 512 B
-__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) |
-         ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
-}
 
 template <int NMAT>
 __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
@@ -582,7 +671,7 @@ __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const Item I = item_of<NMAT>(p, it, 0);
         const int np = I.v->np;
-        const CUtensorMap* tm = p.tmap + I.v->expert * 3;
+        const CUtensorMap* tm = p.tmap + (I.v->expert * 4 + HB_F16) * 6;
         const __half* bsrc = (NMAT == 2 ? p.xg + I.v->xoff : p.hB + I.v->hoff) +
                              (size_t)I.ks * nsteps * np * kBK;
         const int g0 = I.ks * (Kitem / 32);
@@ -721,7 +810,38 @@ int k3_smem_bytes() { return kSmem; }
 
 // Tensor map of an F16 matrix [n, k] stored as units (oracle/formats.py):
 // element (row, kk) at byte 1024*(G*(row/16) + kk/32) + 64*(row%16) + 2*(kk%32).
+static int encode_tiled(CUtensorMap* out, CUtensorMapDataType dt, int rank, const void* base,
+                        const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                        CUtensorMapSwizzle sw);
 int k3_encode_f16_map(CUtensorMap* out, const void* q, int n, int k) {
+  const cuuint64_t G = (cuuint64_t)k / 32;
+  const cuuint64_t dims[4] = {32, 16, (cuuint64_t)n / 16, G};
+  const cuuint64_t strides[3] = {64, G * 1024, 1024};          // bytes, dims 1..3
+  const cuuint32_t box[4] = {32, 16, 8, 2};
+  return encode_tiled(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, q, dims, strides, box,
+                      CU_TENSOR_MAP_SWIZZLE_64B);
+}
+// Quantised matrix [n, k] of encoding enc: codes as 4-D u8 (64 B | row | tile
+// | group), box = 8 tiles x 1 unit; scales as 3-D u16 (unit record block |
+// tile | group), box = 8 tiles x 1 unit.
+int k3_encode_q_maps(CUtensorMap* code, CUtensorMap* scale, int enc, const void* q, const void* s,
+                     int n, int k) {
+  const cuuint64_t G = (cuuint64_t)k / epg_of_enc(enc);
+  const cuuint64_t sb = enc == HB_Q8 ? 4 : enc == HB_Q4 ? 8 : 32;
+  const cuuint64_t cd[4] = {64, 16, (cuuint64_t)n / 16, G};
+  const cuuint64_t cs[3] = {64, G * 1024, 1024};
+  const cuuint32_t cb[4] = {64, 16, 8, 1};
+  if (encode_tiled(code, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, q, cd, cs, cb, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return -1;
+  const cuuint64_t sd[3] = {8 * sb, (cuuint64_t)n / 16, G};
+  const cuuint64_t ss[2] = {G * 16 * sb, 16 * sb};
+  const cuuint32_t sbx[3] = {(cuuint32_t)(8 * sb), 8, 1};
+  return encode_tiled(scale, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, s, sd, ss, sbx,
+                      CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+static int encode_tiled(CUtensorMap* out, CUtensorMapDataType dt, int rank, const void* base,
+                        const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                        CUtensorMapSwizzle sw) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -735,14 +855,10 @@ int k3_encode_f16_map(CUtensorMap* out, const void* q, int n, int k) {
       return -1;
     fn = reinterpret_cast<Fn>(f);
   }
-  const cuuint64_t G = (cuuint64_t)k / 32;
-  const cuuint64_t dims[4] = {32, 16, (cuuint64_t)n / 16, G};
-  const cuuint64_t strides[3] = {64, G * 1024, 1024};          // bytes, dims 1..3
-  const cuuint32_t box[4] = {32, 16, 8, 2};
-  const cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(q), dims, strides, box,
-                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(out, dt, rank, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -1;
 }
 
@@ -761,14 +877,14 @@ void launch_k3a(const K3Params& p, cudaStream_t s) {
   static bool d = false, dd = false;
   set_smem_once(k3_kernel<2>, kSmem, d);
   set_smem_once(k3d_kernel<2>, d_smem<2>(), dd);
-  if (p.tmap) k3d_kernel<2><<<kNumSM, kDThreads, d_smem<2>(), s>>>(p);
+  if (p.has_f16) k3d_kernel<2><<<kNumSM, kDThreads, d_smem<2>(), s>>>(p);
   if (p.has_q) k3_kernel<2><<<kNumSM, kThreads, kSmem, s>>>(p);
 }
 void launch_k3b(const K3Params& p, cudaStream_t s) {
   static bool d = false, dd = false;
   set_smem_once(k3_kernel<1>, kSmem, d);
   set_smem_once(k3d_kernel<1>, d_smem<1>(), dd);
-  if (p.tmap) k3d_kernel<1><<<kNumSM, kDThreads, d_smem<1>(), s>>>(p);
+  if (p.has_f16) k3d_kernel<1><<<kNumSM, kDThreads, d_smem<1>(), s>>>(p);
   if (p.has_q) k3_kernel<1><<<kNumSM, kThreads, kSmem, s>>>(p);
 }
 

@@ -38,11 +38,14 @@ struct K3Params {
   __half* hB;                    // h, same layout [v][F/64][np x 64]
   float* y;                      // [B][H] fp32, zeroed by the router
   K3Table* tab;
-  const CUtensorMap* tmap;       // [E][3] F16 tensor maps of this layer (null: no F16 path)
-  int has_q;                     // quantised encodings in the pair (launch k3_kernel)
+  const CUtensorMap* tmap;       // [E][4 enc][6] tensor maps of this layer's blobs:
+                                 //   F16: [0..2] W1, W3, W2; Q: [0..2] codes, [3..5] scales
+  int has_f16, has_q;            // encodings in the pair (launch k3d_kernel / k3_kernel)
 };
 // 4-D tensor map of one F16 matrix [n rows, k] in the unit layout (host)
 int k3_encode_f16_map(CUtensorMap* out, const void* q, int n, int k);
+int k3_encode_q_maps(CUtensorMap* code, CUtensorMap* scale, int enc, const void* q, const void* s,
+                     int n, int k);
 
 int k3_smem_bytes();
 void launch_k3_prep(const K3Params& p, const __half* x, cudaStream_t s);

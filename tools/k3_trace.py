@@ -27,15 +27,11 @@ torch.cuda.synchronize()
 buf = np.zeros((4, 4096), np.uint64)
 assert _lib.lib.hb_k3_trace(C.c_void_p(buf.ctypes.data), C.c_size_t(buf.nbytes)) == 0
 t0 = min(int(v) for v in buf.ravel() if v)
-names = ["prod_issue", "conv_rawfull", "conv_canfull", "mma_start"]
+names = ["prod_rawissue", "conv_rawfull", "conv_arrive", "mma_go"]
+v = [buf[ch][buf[ch] > 0].astype(np.int64) - t0 for ch in range(4)]
 for ch in range(4):
-    v = buf[ch][buf[ch] > 0].astype(np.int64) - t0
-    d = np.diff(v)
-    print(f"{names[ch]:13s} n={len(v):4d} first={v[:6].tolist()} median_dt={np.median(d) if len(d) else 0:.0f}ns "
-          f"p90_dt={np.percentile(d, 90) if len(d) else 0:.0f}ns span={v[-1] if len(v) else 0}ns")
-p, r = buf[0][buf[0] > 0].astype(np.int64), buf[1][buf[1] > 0].astype(np.int64)
-n = min(len(p), len(r))
-print("issue->rawfull latency median", np.median(r[:n] - p[:n]), "ns; p90", np.percentile(r[:n] - p[:n], 90))
-c, m = buf[2][buf[2] > 0].astype(np.int64), buf[3][buf[3] > 0].astype(np.int64)
-n = min(len(c), len(m))
-print("canfull arrive->mma wake median", np.median(m[:n] - c[:n]), "ns")
+    d = np.diff(v[ch])
+    print(f"{names[ch]:13s} n={len(v[ch]):4d} first={v[ch][:10].tolist()} median_dt={np.median(d):.0f}ns")
+n = min(len(v[0]), len(v[1]))
+print("raw issue -> converter wake (median, p10, p90):", np.median(v[1][:n] - v[0][:n]),
+      np.percentile(v[1][:n] - v[0][:n], 10), np.percentile(v[1][:n] - v[0][:n], 90))
