@@ -61,7 +61,7 @@ def test_k3_parity_tiny(pair, B):
 def test_k3_many_tokens_per_expert():
     """> 128 tokens of one (expert, encoding): several vjob3 per job, ragged tail."""
     sh = sg.TINY
-    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=600)
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=600, batched_min=8)
     x16 = sg.hidden_states(sh, 31, 0, batch=600)
     _check_layer(ctx, sh, 0, x16, fm.F16, fm.Q4)
 
@@ -97,6 +97,63 @@ def test_k3_parity_full_size(shape, pair, B):
     ctx.set_batched_min(32)
     x16 = sg.hidden_states(sh1, 200, layer, batch=B)
     _check_layer(ctx, sh1, layer, x16, hi, lo, tokens=[0, B // 2, B - 1])
+
+
+@pytest.mark.parametrize("t1,t2", [(1.0, 1.0), (0.0, 0.0), (0.5, 0.5)])
+def test_k3_threshold_edges(t1, t2):
+    """All-High (dense top-k MoE), all-Skip-but-rank-0, tie edge through K3."""
+    sh = sg.TINY
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, t1=t1, t2=t2, max_batch=32, batched_min=1)
+    store = OracleStore(sh)
+    x16 = sg.hidden_states(sh, 33, 0, batch=32)
+    y = _run(ctx, 0, x16)
+    ref, routes = om.moe_layer(x16, sg.router_weights(sh, 0), store, 0, 2, t1, t2, fm.F16, fm.Q4)
+    _check_routes(ctx, routes, 32, 2)
+    for b in range(32):
+        assert rel_err(y[b], ref[b])[0] <= TOL
+
+
+def test_k3_zero_input():
+    sh = sg.TINY
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=16, batched_min=1)
+    y = _run(ctx, 0, np.zeros((16, sh.hidden), np.float16))
+    assert np.all(y == 0)
+
+
+def test_k3_default_threshold_routes_batches():
+    """Default context: batch >= 8 takes K3 (launch count says which chain ran)."""
+    sh = sg.TINY
+    from paper_2411_01433_b200 import hobbit as h
+    cfg = h.default_config(n_layers=1, n_experts=8, top_k=2, hidden=256, ffn=512, max_batch=16)
+    ctx = h.Context(cfg)
+    ctx.set_router(0, sg.router_weights(sh, 0))
+    for (e, enc), b in gpu_blobs(sh, 0, range(8), [fm.F16, fm.Q4]).items():
+        ctx.register_expert(0, e, enc, b)
+    x = torch.from_numpy(sg.hidden_states(sh, 34, 0, batch=16)).cuda()
+    y = torch.empty(16, sh.hidden, dtype=torch.float32, device="cuda")
+    n0 = ctx.launch_count()
+    ctx.forward(0, x[:4], y[:4])
+    n1 = ctx.launch_count()
+    ctx.forward(0, x, y)
+    n2 = ctx.launch_count()
+    assert n1 - n0 == 4            # router, K2a, hfin, K2b
+    assert n2 - n1 == 6            # router, prep, K3a (F16, Q), K3b (F16, Q)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_k3_ep_partition_on_one_gpu(world):
+    """O11 through K3: per-rank contexts (same GPU) sum to the 1-rank output,
+    every served expert computed by exactly its owner."""
+    sh = sg.TINY
+    x16 = sg.hidden_states(sh, 35, 1, batch=24)
+    full = _run(_resident(sh, [1], fm.F16, fm.Q4, max_batch=24, batched_min=1), 1, x16)
+    parts = []
+    for r in range(world):
+        ctx = _resident(sh, [1], fm.F16, fm.Q4, max_batch=24, batched_min=1, rank=r, world=world)
+        parts.append(_run(ctx, 1, x16))
+        d = ctx.decisions(24)
+        assert all((v.served_enc == 255) == (v.prec == 2 or v.expert % world != r) for v in d)
+    np.testing.assert_allclose(np.sum(parts, axis=0), full, rtol=1e-5, atol=1e-6)
 
 
 def test_k3_setter_errors():

@@ -64,8 +64,12 @@ def _ctx(shape, hi, lo, t1=0.6, t2=0.9, max_batch=1, **kw):
     return h.Context(cfg)
 
 
-def _resident(shape, layers, hi, lo, **kw):
+def _resident(shape, layers, hi, lo, batched_min=0, **kw):
+    """Fully resident context.  batched_min=0 keeps every batch on the exact-code
+    dequant-GEMV path (K2); the tcgen05 GEMM path (K3) has its own tests."""
     ctx = _ctx(shape, hi, lo, **kw)
+    if kw.get("max_batch", 1) > 1:
+        ctx.set_batched_min(batched_min)
     world = kw.get("world", 1)
     rank = kw.get("rank", 0)
     for l in layers:
