@@ -278,6 +278,77 @@ __device__ void build_jobs(const RouterParams& p, RouterSmem& sm, const hb_decis
   p.jt.hdr[2] = build_vjobs(sm.jobs, nj, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
 }
 
+// build_jobs for batches, by the whole (last) CTA: per-key counts with shared
+// atomics, job offsets by one thread (<= 2E keys), then slots in token order
+// by warp 0 (ballot ranks within each 32-selection chunk).  Same table as
+// build_jobs; the serial version read the decisions from global memory one
+// dependent load at a time (~0.5 us per selection at B = 512).
+__device__ void build_jobs_cta(const RouterParams& p, RouterSmem& sm, const hb_decision* dec) {
+  const int nkey = 2 * p.E, nsel = p.B * p.k, tid = threadIdx.x;
+  for (int i = tid; i < nkey; i += blockDim.x) { sm.count[i] = 0; sm.fill[i] = 0; }
+  __syncthreads();
+  for (int i = tid; i < nsel; i += blockDim.x) {
+    const hb_decision d = dec[i];
+    if (d.prec == HB_SKIP || d.expert % p.world != p.rank) continue;
+    atomicAdd(&sm.count[d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1)], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int nj = 0, off = 0;
+    for (int key = 0; key < nkey; ++key) {
+      sm.jobid[key] = -1;
+      if (!sm.count[key]) continue;
+      const int e = key >> 1;
+      const int enc = (key & 1) ? p.lo_enc : p.hi_enc;
+      Job j;
+      j.blob = sm.blob[e * 4 + enc];
+      j.enc = enc;
+      j.expert = e;
+      j.n_tok = sm.count[key];
+      j.slot_off = off;
+      sm.jobs[nj] = j;
+      p.jt.jobs[nj] = j;
+      sm.jobid[key] = nj++;
+      off += sm.count[key];
+    }
+    p.jt.hdr[0] = nj;
+    p.jt.hdr[1] = off;
+    sm.last = nj;                                  // reused: number of jobs
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const int lane = tid;
+    for (int base = 0; base < nsel; base += 32) {
+      const int i = base + lane;
+      int key = -1;
+      hb_decision d;
+      if (i < nsel) {
+        d = dec[i];
+        if (d.prec != HB_SKIP && d.expert % p.world == p.rank)
+          key = d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      if (key >= 0) {
+        const int slot = sm.jobs[sm.jobid[key]].slot_off + sm.fill[key] + rank;
+        p.jt.slot_token[slot] = d.token;
+        p.jt.slot_gate[slot] = d.gate;
+        p.jt.tok_slots[i] = slot;
+        d.served_enc = (uint8_t)((key & 1) ? p.lo_enc : p.hi_enc);
+        d.hit = 1;
+        p.dec[i] = d;
+      } else if (i < nsel) {
+        p.jt.tok_slots[i] = -1;
+      }
+      __syncwarp();
+      if (key >= 0 && rank == __popc(peers) - 1) sm.fill[key] += __popc(peers);
+      __syncwarp();
+    }
+    if (lane == 0)
+      p.jt.hdr[2] = build_vjobs(sm.jobs, sm.last, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
+  }
+}
+
 // build_jobs by one warp when the forward has <= 32 selections (decode): the
 // same table (jobs by key = expert*2 + Low, slots in selection order) from
 // per-lane counts instead of serial loops.
@@ -350,13 +421,16 @@ __device__ __forceinline__ u64 ld_dsmem_u64(const void* local, int rank) {
   return v;
 }
 
+// C = CTAs per (route layer, token) row: 8 (a cluster, decode: the token's
+// logits in ~1/8 of the latency) or 1 (batches: one CTA per row, no cluster --
+// 8-CTA clusters per token cost ~1 us per token at B = 512)
+template <int C>
 __global__ void __launch_bounds__(kRouterThreads)
 router_kernel(const __grid_constant__ RouterParams p) {
   __shared__ RouterSmem sm;
   HB_RTL(0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int NW = kRouterThreads / 32;
-  constexpr int C = kRouterCluster;
   const int nrows = p.n_route * p.B;
   const int row = blockIdx.x / C, crank = blockIdx.x % C;   // cluster = one row
   if (row >= nrows) {
@@ -470,19 +544,25 @@ router_kernel(const __grid_constant__ RouterParams p) {
     }
   }
   // ---- combine the cluster's partials in the leader (distributed shared memory)
-  cluster_sync_all();
+  if (C > 1) cluster_sync_all();
+  else __syncthreads();
   if (crank == 0) {
     for (int e = tid; e < p.E; e += blockDim.x) {
       u64 lo = 0, mid = 0, hi = 0;
       for (int r = 0; r < C; ++r) {
-        lo += ld_dsmem_u64(&sm.cpart[e][0], r);
-        mid += ld_dsmem_u64(&sm.cpart[e][1], r);
-        hi += ld_dsmem_u64(&sm.cpart[e][2], r);
+        if (C > 1) {
+          lo += ld_dsmem_u64(&sm.cpart[e][0], r);
+          mid += ld_dsmem_u64(&sm.cpart[e][1], r);
+          hi += ld_dsmem_u64(&sm.cpart[e][2], r);
+        } else {
+          lo += sm.cpart[e][0]; mid += sm.cpart[e][1]; hi += sm.cpart[e][2];
+        }
       }
       sm.L[e] = (i128)(long long)lo + ((i128)(long long)mid << 20) + ((i128)(long long)hi << 40);
     }
   }
-  cluster_sync_all();                        // remote reads done: the other CTAs may exit
+  if (C > 1) cluster_sync_all();             // remote reads done: the other CTAs may exit
+  else __syncthreads();
   if (crank != 0) return;
   HB_RTL(3);
   HB_RTL(4);
@@ -539,22 +619,21 @@ router_kernel(const __grid_constant__ RouterParams p) {
            r == 0 && dec_smem ? sm.dec + (size_t)bb * p.k : nullptr);
   }
   __syncthreads();
-  if (tid == 0) {
-    if (p.blob_table) {
-      __threadfence();
-      build_jobs(p, sm, dec_smem ? sm.dec : p.dec);
-    }
-    *p.done = 0u;
+  if (p.blob_table) {
+    __threadfence();
+    build_jobs_cta(p, sm, dec_smem ? sm.dec : p.dec);
   }
+  if (tid == 0) *p.done = 0u;
 }
 
 void launch_router(const RouterParams& p, cudaStream_t s) {
   // one 8-CTA cluster per (route layer, token) row, plus clusters of CTAs that
   // zero the GEMV accumulation buffers in parallel
+  const int C = p.n_route * p.B >= 16 ? 1 : kRouterCluster;
   const long long nz4 = (p.zero_n[0] + p.zero_n[1]) / 4;
   int zc = nz4 ? (int)std::min<long long>(32, (nz4 + 2 * kRouterThreads - 1) / (2 * kRouterThreads)) : 0;
-  zc = (zc + kRouterCluster - 1) / kRouterCluster * kRouterCluster;
-  const int grid = p.n_route * p.B * kRouterCluster + zc;
+  zc = (zc + C - 1) / C * C;
+  const int grid = p.n_route * p.B * C + zc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kRouterThreads);
@@ -568,8 +647,13 @@ void launch_router(const RouterParams& p, cudaStream_t s) {
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, router_kernel, p);
+  if (C == 1) {
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, router_kernel<1>, p);
+  } else {
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, router_kernel<kRouterCluster>, p);
+  }
 }
 
 }  // namespace hb
