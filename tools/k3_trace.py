@@ -27,11 +27,12 @@ torch.cuda.synchronize()
 buf = np.zeros((4, 4096), np.uint64)
 assert _lib.lib.hb_k3_trace(C.c_void_p(buf.ctypes.data), C.c_size_t(buf.nbytes)) == 0
 t0 = min(int(v) for v in buf.ravel() if v)
-names = ["prod_rawissue", "conv_rawfull", "conv_arrive", "mma_go"]
+names = ["b_issue", "raw_issue", "conv_arrive_g0", "mma_go"]
 v = [buf[ch][buf[ch] > 0].astype(np.int64) - t0 for ch in range(4)]
 for ch in range(4):
     d = np.diff(v[ch])
     print(f"{names[ch]:13s} n={len(v[ch]):4d} first={v[ch][:10].tolist()} median_dt={np.median(d):.0f}ns")
-n = min(len(v[0]), len(v[1]))
-print("raw issue -> converter wake (median, p10, p90):", np.median(v[1][:n] - v[0][:n]),
-      np.percentile(v[1][:n] - v[0][:n], 10), np.percentile(v[1][:n] - v[0][:n], 90))
+n = min(len(v[0]), len(v[3]))
+print("b issue -> mma go (median)", np.median(v[3][:n] - v[0][:n]))
+for ch in range(4):
+    print(names[ch], "last", v[ch][-1] if len(v[ch]) else None)
