@@ -42,24 +42,23 @@ namespace {
 
 constexpr int kRows = 128;                 // weight rows per tile = MMA M
 constexpr int kBK = 64;                    // K elements per canonical stage
-constexpr int kRawSlots = 3;
-constexpr int kConvGroups = 4;            // converter warp groups = A slots
-constexpr int kCanSlots = kConvGroups;
+constexpr int kRawSlots = 4;
+constexpr int kCanSlots = 3;
 constexpr int kMaxBSlots = 8;
-constexpr int kConvWarps = 16;             // warps 0..15 dequantise
+constexpr int kConvWarps = 16;             // warps 0..15 dequantise (all on one step)
 constexpr int kConvThreads = kConvWarps * 32;
-constexpr int kEpiWarp0 = 16;              // warps 16..19 epilogue (warp % 4 = TMEM lane quarter)
-constexpr int kMmaWarp = 20;
-constexpr int kProdWarp = 21;              // raw codes + scales
-constexpr int kBProdWarp = 22;             // B tiles
-constexpr int kThreads = 23 * 32;
+constexpr int kEpiWarp0 = kConvWarps;      // 4 epilogue warps (warp % 4 = TMEM lane quarter)
+constexpr int kMmaWarp = kConvWarps + 4;
+constexpr int kProdWarp = kConvWarps + 5;  // raw codes + scales
+constexpr int kBProdWarp = kConvWarps + 6; // B tiles
+constexpr int kThreads = (kConvWarps + 7) * 32;
 constexpr int kRawCode = 16384;            // NMAT x 8 tiles x ru units of 1 KB
 constexpr int kRawScale = 8192;
 constexpr int kRawBytes = kRawCode + kRawScale;
 constexpr int kAMat = kRows * kBK * 2;     // 16 KB fp16 A tile per matrix
 constexpr int kABytes = 2 * kAMat;
 constexpr int kBBytes = kK3MaxN * kBK * 2; // 16 KB: largest B tile (np = 128)
-constexpr int kBRing = 24576;
+constexpr int kBRing = 32768;
 constexpr int kBarOff = kRawSlots * kRawBytes + kCanSlots * kABytes + kBRing;
 constexpr int kSmem = kBarOff + 512 + 1024;   // + alignment slack (swizzle atoms: 1 KB)
 
@@ -409,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
       bar_init(raw_empty(i), kConvWarps);
     }
     for (int i = 0; i < CS; ++i) {
-      bar_init(can_full(i), kConvWarps / kConvGroups);
+      bar_init(can_full(i), kConvWarps);
       bar_init(can_empty(i), 1);
     }
     for (int i = 0; i < BS; ++i) {
@@ -502,19 +501,13 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
       }
     }
   } else if (warp < kConvWarps) {
-    // 4 groups of 4 warps; group q converts the canonical steps s with
-    // s % 4 == q into A slot q, so four steps are in flight at once.  Thread =
-    // one weight row of the 128-row tile: all 8 K chunks of the step (t = 0..3,
-    // blocks j0 and j0 + 1).  Quarter-warps store 8 consecutive rows of one
-    // chunk: conflict-free in the SWIZZLE_64B layout.
-    constexpr int WPG = kConvWarps / kConvGroups;      // warps per group
-    constexpr int TSPLIT = WPG / 4;                    // threads per row
-    const int grp = warp / WPG, gt = (warp % WPG) * 32 + lane;
-    const int row = gt & 127, tpart = gt >> 7;        // this thread's t range
+    const int tid = threadIdx.x;
+    // thread = (row, t): its share of the row's raw piece for one 64-K step
+    // -> K chunks kc = t and 4 + t (blocks j0, j0 + 1).  Quarter-warps store
+    // 8 rows of one chunk: conflict-free 16-byte stores.
+    const int t = (tid >> 3) & 3, row = (tid & 7) + 8 * (tid >> 5);
     const int tl = row >> 4, rr = row & 15;
-    const uint32_t swz = (uint32_t)((row >> 1) & 3);
-    const uint32_t can = sbase + kRawSlots * kRawBytes + grp * kABytes;
-    int rs = 0, sglob = 0, ntc = 0;
+    int rs = 0, cs = 0, ntc = 0, ntr = 0;
     uint32_t rph = 0, cph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const Item I = item_of<NMAT>(p, it, v0);
@@ -525,39 +518,36 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
       for (int r = 0; r < nraw; ++r) {
         if (lane == 0) bar_wait(raw_full(rs), rph);     // one poller per warp
         __syncwarp();
+        if (NMAT == 2 && tid == 0) K3_STAMP(1, ntr++);
         const uint32_t raw = sbase + rs * kRawBytes;
-        for (int c = 0; c < cpr; ++c, ++sglob) {
-          if ((sglob & (kConvGroups - 1)) != grp) continue;
-          if (lane == 0) bar_wait(can_empty(grp), cph ^ 1);
+        for (int c = 0; c < cpr; ++c) {
+          if (lane == 0) bar_wait(can_empty(cs), cph ^ 1);
           __syncwarp();
+          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
           // step-uniform offsets inside the raw slot (oracle/formats.py layout)
           const int u = enc == HB_Q8 ? c : enc == HB_Q4 ? (c >> 1) : (c >> 2);
           const int coff = enc == HB_Q8 ? 0 : enc == HB_Q4 ? 8 * (c & 1) : 4 * (c & 3);
           const int soff = enc == HB_Q8 ? 0 : enc == HB_Q4 ? 4 * (c & 1) : 4 * (c & 3);
-          const int su = u * 8 + tl;                  // raw slot [m][u][tile]
 #pragma unroll
           for (int m = 0; m < NMAT; ++m) {
-            const uint32_t code = raw + m * (8 * ru * 1024) + su * 1024 + rr * 64 + coff;
+            const int su = u * 8 + tl;                // raw slot [m][u][tile]
+            const uint32_t code = raw + m * (8 * ru * 1024) + su * 1024 + rr * 64 + 16 * t + coff;
             const uint32_t sc = raw + kRawCode + m * (8 * ru * 16 * sb) + su * 16 * sb + rr * sb + soff;
-            const uint32_t dst = can + m * kAMat + row * 64;
-#pragma unroll
-            for (int ti = 0; ti < 4 / TSPLIT; ++ti) {
-              const int t = tpart * (4 / TSPLIT) + ti;
-              uint4 w0, w1;
-              dequant16(enc, code + 16 * t, sc, w0, w1);
-              // UMMA K-major SWIZZLE_64B (as the TMA path): K chunk kc of a row in
-              // block kc / 4 (8 KB = 128 rows x 64 B), 16-byte slot (kc % 4) ^ ((row / 2) % 4)
-              sts128(dst + (((uint32_t)t ^ swz) << 4), w0);
-              sts128(dst + 8192 + (((uint32_t)t ^ swz) << 4), w1);
-            }
+            uint4 w0, w1;
+            dequant16(enc, code, sc, w0, w1);
+            // UMMA K-major SWIZZLE_64B (as the TMA path): K chunk kc of a row in
+            // block kc / 4 (8 KB = 128 rows x 64 B), 16-byte slot (kc % 4) ^ ((row / 2) % 4)
+            const uint32_t dst = can + m * kAMat + row * 64 + ((t ^ ((row >> 1) & 3)) << 4);
+            sts128(dst, w0);
+            sts128(dst + 8192, w1);
           }
 #ifndef HB_K3_NOFENCE
           fence_async_smem();
 #endif
           __syncwarp();
-          if (lane == 0) bar_arrive(can_full(grp));
-          if (NMAT == 2 && threadIdx.x == 0) K3_STAMP(2, ntc++);
-          cph ^= 1;
+          if (lane == 0) bar_arrive(can_full(cs));
+          if (NMAT == 2 && tid == 0) K3_STAMP(2, ntc++);
+          if (++cs == CS) { cs = 0; cph ^= 1; }
         }
         __syncwarp();
         if (lane == 0) bar_arrive(raw_empty(rs));

@@ -49,6 +49,9 @@ def main():
     ap.add_argument("--tokens", type=int, default=24)
     ap.add_argument("--p", default="0,1,2")
     ap.add_argument("--rho", type=float, default=0.5)
+    ap.add_argument("--policies", default="",
+                    help="Eq. 3 weight sets a:b:c:d (LRU:LFU:LHU:FLD) run at p=1, e.g. "
+                         "1:0:0:0,0:1:0:0,0:0:1:0,0:0:0:1,1:1:1:1 (SURVEY 8(f) f2, P:631, P:1040)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     base = sg.MIXTRAL
@@ -81,11 +84,13 @@ def main():
     cap_h, cap_l = max(3, round(48 * L / 32)), max(3, round(56 * L / 32))
     xs = torch.from_numpy(sg.correlated_states(shape, args.tokens + 1, 0.999, args.rho)).cuda()
     y = torch.empty(1, H, dtype=torch.float32, device="cuda")
-    runs = [(int(p), 0.6, 0.9) for p in args.p.split(",")] + [(1, 1.0, 1.0)]
-    for p, t1, t2 in runs:
+    runs = [(int(p), 0.6, 0.9, (1, 1, 1, 1)) for p in args.p.split(",") if p] + [(1, 1.0, 1.0, (1, 1, 1, 1))]
+    runs += [(1, 0.6, 0.9, tuple(int(v) for v in w.split(":"))) for w in args.policies.split(",") if w]
+    for p, t1, t2, w in runs:
         cfg = h.default_config(n_layers=L, n_experts=E, top_k=2, hidden=H, ffn=F, hi_enc=hi,
                                lo_enc=lo, t1=t1, t2=t2, max_batch=1, cap_high=cap_h,
-                               cap_low=cap_l, lookahead_p=p)
+                               cap_low=cap_l, lookahead_p=p, w_lru=w[0], w_lfu=w[1], w_lhu=w[2],
+                               w_fld=w[3])
         ctx = h.Context(cfg)
         for l in range(L):
             ctx.set_router(l, sg.router_weights(shape, l))
@@ -120,7 +125,7 @@ def main():
         n_pref = sum(1 for e in loads if e[1] == 1)
         n = args.tokens
         out = {"config": "C4 constrained cache", "layers": L, "tokens": n, "rho": args.rho, "p": p,
-               "t1": t1, "t2": t2, "cap_high": cap_h, "cap_low": cap_l,
+               "t1": t1, "t2": t2, "eq3_weights": list(w), "cap_high": cap_h, "cap_low": cap_l,
                "tok_s": round(n * 1000.0 / ms, 3), "ms_per_token": round(ms / n, 3),
                "wall_ms_per_token": round(wall * 1000 / n, 3),
                "h2d_bytes_per_token": int(h2d / n), "h2d_gbs": round(h2d / (ms * 1e-3) / 1e9, 2),
