@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -91,6 +92,7 @@ struct hb_ctx {
   float static_frac = 0.8f;               // GEMV work feed K2a (HB_STATIC_FRAC, HB_CHUNK)
   float static_frac2 = 0.8f;              // K2b (HB_STATIC_FRAC2)
   int chunk = 8;
+  float k2b_w[4] = {1.f, 2.f, 4.f, 8.f};  // HB_K2B_W: K2b CTA-split cost per unit (~ weights per KB)
   // K3: tcgen05 grouped GEMM for batches >= k3_min_batch (A9); buffers exist
   // when max_batch > 1 and the vjob3 table bound fits
   int k3_min_batch = 8;                   // HB_K3_MIN_BATCH / hb_set_batched_min (K3 wins from B = 8, profiles/r01_batched.md)
@@ -275,6 +277,12 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     if (sf) c->static_frac = std::min(1.0f, std::max(0.0f, (float)std::atof(sf)));
     const char* sf2 = std::getenv("HB_STATIC_FRAC2");
     if (sf2) c->static_frac2 = std::min(1.0f, std::max(0.0f, (float)std::atof(sf2)));
+    const char* kw = std::getenv("HB_K2B_W");        // "f16,q8,q4,q2"
+    if (kw) {
+      float w[4];
+      if (std::sscanf(kw, "%f,%f,%f,%f", &w[0], &w[1], &w[2], &w[3]) == 4)
+        for (int e = 0; e < 4; ++e) c->k2b_w[e] = std::max(0.05f, w[e]);
+    }
     const char* ch = std::getenv("HB_CHUNK");
     if (ch) c->chunk = (std::max(2, std::atoi(ch)) + 1) & ~1;   // even: K2b stages hold 2 units
   }
@@ -495,6 +503,7 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
   g.static_frac = c->static_frac;
   g.static_frac2 = c->static_frac2;
   g.chunk = c->chunk;
+  for (int e = 0; e < 4; ++e) g.k2b_w[e] = c->k2b_w[e];
   return g;
 }
 

@@ -742,6 +742,7 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   __shared__ uint2 s_meta[kGemvWarps][16];
   __shared__ FeedConst s_fk;
   __shared__ int s_subb[kGemvCTAs + 1];         // K2b sub-space first units (+ total)
+  __shared__ float s_subc[kGemvCTAs + 1];       // K2b sub-space cumulative cost (+ total)
   __shared__ int s_subvh[kGemvCTAs];            // vjob | slice << 16 | slices << 24
   __shared__ int s_nsub;
   const int warp = threadIdx.x >> 5;
@@ -788,23 +789,32 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
     // has an even number of groups.  CTAs [c0(q), c0(q+1)) work on
     // sub-space q, c0(q) = q + floor(first unit of q * (n - nsub) / U)
     if (threadIdx.x == 0) {
+      // CTAs per sub-space proportional to its cost: units x the per-encoding
+      // weight (quantised units are ALU-heavier than F16 ones; HB_K2B_W)
       int q = 0;
+      float cc = 0.f;
       for (int v = 0; v < nv; ++v) {
-        const int G = K / epg_of(__ldcg(&p.jt.vjobs[v].enc));
+        const int enc = __ldcg(&p.jt.vjobs[v].enc);
+        const int G = K / epg_of(enc);
         const int nh = (!W13 && G % 4 == 0) ? 2 : 1;
         const int uq = (s_cum[v + 1] - s_cum[v]) / nh;
+        const float w = p.k2b_w[enc & 3];
         for (int h = 0; h < nh; ++h, ++q) {
           s_subvh[q] = v | (h << 16) | (nh << 24);
           s_subb[q] = s_cum[v] + h * uq;
+          s_subc[q] = cc;
+          cc += w * (h + 1 < nh ? uq : (s_cum[v + 1] - s_cum[v]) - h * uq);
         }
       }
       s_subb[q] = U;
+      s_subc[q] = cc;
       s_nsub = q;
     }
     __syncthreads();
     const int nsub = s_nsub;
     const int spare = (int)gridDim.x - nsub;
-    auto c0 = [&](int q) { return q + (int)((long long)s_subb[q] * spare / U); };
+    const float ctot = s_subc[nsub];
+    auto c0 = [&](int q) { return q + (int)((double)s_subc[q] * spare / ctot); };
     int lo = 0, hi = nsub - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;

@@ -146,6 +146,7 @@ struct GemvParams {
   float static_frac;                   // K2a: fraction of units dealt as static warp ranges
   float static_frac2;                  // K2b
   int chunk;                           // units per dynamic chunk
+  float k2b_w[4];                      // K2b CTA split: cost of a unit per encoding (F16 = 1)
 };
 
 void launch_router(const RouterParams& p, cudaStream_t s);
