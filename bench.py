@@ -338,6 +338,11 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_e2e = float(tt.item())
 
+    # ---- batched decode / prefill through K3 on the same weights (N=1, diagnostic)
+    batched = None
+    if world == 1 and not args.no_batched:
+        batched = batched_leg(h, sg, shape, hi, lo, blobs, local, stream)
+
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -373,12 +378,71 @@ def run_ours(args):
         "clocks": clk_sum,
         "init_s": round(t_init, 1),
     }
+    if batched is not None:
+        out["batched_k3"] = batched          # tok/s normalised to 32-layer tokens
     if cpu is not None:
         out["cpu_baseline"] = cpu
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ batched leg (A9)
+def batched_leg(h, sg, shape, hi, lo, blobs, dev, stream, Bs=(256, 512), layers=8, steps=5):
+    """SURVEY 8(d) C5 on the same resident weights (1 GPU): batched decode (B=256)
+    and a 512-token prefill through the tcgen05 grouped-GEMM path K3, first
+    `layers` layers rotating (>= 3.6 GB of expert weights per step, >> L2).
+    Diagnostic extra of the bench line: tokens/s and step-level GB/s of the
+    served blobs (each (expert, encoding) blob once per layer + X + h + y)."""
+    import torch
+    E, Hd, F = shape.n_experts, shape.hidden, shape.ffn
+    cfg = h.default_config(n_layers=shape.n_layers, n_experts=E, top_k=shape.top_k, hidden=Hd,
+                           ffn=F, hi_enc=hi, lo_enc=lo, max_batch=max(Bs))
+    ctx = h.Context(cfg, dev)
+    i = 0
+    for l in range(shape.n_layers):
+        ctx.set_router(l, sg.router_weights(shape, l))
+        for e in range(E):
+            for enc in (hi, lo):
+                ctx.register_expert(l, e, enc, blobs[i])
+                i += 1
+    bb = {hi: h.blob_bytes(hi, Hd, F), lo: h.blob_bytes(lo, Hd, F)}
+    out = {}
+    with torch.cuda.stream(stream):
+        for B in Bs:
+            X = torch.from_numpy(np.stack([sg.hidden_states(shape, 7000 + B, l, batch=B)
+                                           for l in range(layers)])).cuda()
+            Y = torch.empty(layers, B, Hd, dtype=torch.float32, device="cuda")
+            nbytes = 0
+            for l in range(layers):
+                ctx.forward(l, X[l], Y[l], stream=stream)
+                jobs, nsel = set(), 0
+                for d in ctx.decisions(B):
+                    if d.served_enc != h.HB_ENC_NONE:
+                        jobs.add((d.expert, d.served_enc))
+                        nsel += 1
+                nbytes += sum(bb[e] for _, e in jobs) + 2 * B * Hd + 2 * 2 * nsel * F + 4 * B * Hd
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for l in range(layers):
+                    ctx.forward(l, X[l], Y[l], stream=stream)
+            for _ in range(2):
+                g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            out[f"B{B}"] = {"tok_s": round(B * layers / shape.n_layers * 1000.0 / ms, 1),
+                            "ms_per_step": round(ms, 4), "layers": layers,
+                            "step_gbs": round(nbytes / ms / 1e6, 1), "path": "K3 tcgen05 GEMM"}
+            del X, Y, g
+    ctx.close()
+    return out
 
 
 # ------------------------------------------------------------ oracle timings
@@ -471,6 +535,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batched", action="store_true", help="skip the K3 batched/prefill extra")
     ap.add_argument("--cpu-sample", type=int, default=2)
     ap.add_argument("--ref-max-steps", type=int, default=12)
     ap.add_argument("--model", choices=["mixtral", "phi"], default="mixtral",
