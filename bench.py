@@ -177,6 +177,12 @@ def run_ours(args):
     L, Hd = shape.n_layers, shape.hidden
     t_init = time.time()
     ctx, blobs = build_model(h, sg, None, shape, hi, lo, rank, world, local)
+    # EP exchange (A10): by default inside the library (hb_nccl_init: the
+    # forward ends with the NCCL all-reduce of y); HB_BENCH_TORCH_ALLREDUCE=1
+    # reduces with torch.distributed instead
+    torch_reduce = world > 1 and os.environ.get("HB_BENCH_TORCH_ALLREDUCE") == "1"
+    if world > 1 and not torch_reduce:
+        ctx.nccl_init()
     t_init = time.time() - t_init
 
     # token inputs: a pool of P tokens x 32 layers, resident on the device
@@ -191,7 +197,8 @@ def run_ours(args):
         for l in range(L):
             ctx.forward(l, X[t % P, l].view(1, Hd), Y[l].view(1, Hd), stream=s)
             if world > 1:
-                dist.all_reduce(Y[l])
+                if torch_reduce:
+                    dist.all_reduce(Y[l])
 
     # ---- realised algorithmic bytes of the pool's tokens (decisions, untimed)
     blob_b = {hi: h.blob_bytes(hi, Hd, shape.ffn), lo: h.blob_bytes(lo, Hd, shape.ffn)}
@@ -289,7 +296,8 @@ def run_ours(args):
             for l in range(L):
                 ctx.forward(l, X[t, l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
                 if world > 1:
-                    dist.all_reduce(Y[l])
+                    if torch_reduce:
+                        dist.all_reduce(Y[l])
         prof = ctx.profile_read()
         ctx.profile(0)
     # bytes per K2a / K2b launch, from the decisions of the same tokens
@@ -328,7 +336,8 @@ def run_ours(args):
             for l in range(L):
                 ctx.forward(l, Xd[l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
                 if world > 1:
-                    dist.all_reduce(Y[l])
+                    if torch_reduce:
+                        dist.all_reduce(Y[l])
             Yh.copy_(Y, non_blocking=True)
         e3.record(stream)
         torch.cuda.synchronize()

@@ -181,6 +181,18 @@ int moe_layer_forward(hb_ctx* ctx, int layer, const void* x, int batch,
  * HB_EUNSUPPORTED if the context was created with max_batch == 1. */
 int hb_set_batched_min(hb_ctx* ctx, int min_batch);
 
+/* Expert-parallel exchange: after hb_nccl_init the
+ * library sums y over the cfg.world EP ranks itself -- moe_layer_forward
+ * ends with an in-place ncclAllReduce(sum, fp32) of y [batch, hidden] on the
+ * forward's stream, so y is the full Eq. 1 output on every rank (without it
+ * y is this rank's part and the caller reduces).  unique_id: 128 bytes from
+ * hb_nccl_unique_id on one rank, shared by the caller (e.g. torch.distributed
+ * broadcast); collective over the ranks (cfg.rank / cfg.world).  NCCL is
+ * resolved at run time (the process's libnccl.so.2, or HB_NCCL_LIB);
+ * HB_EUNSUPPORTED if it cannot be found. */
+int hb_nccl_unique_id(void* unique_id_out /* 128 bytes */);
+int hb_nccl_init(hb_ctx* ctx, const void* unique_id);
+
 /* ------------------------------------------------------------ inspection */
 /* Decisions of the last forward: batch*top_k records (synchronises). */
 int hb_get_decisions(hb_ctx* ctx, hb_decision* out, int cap);

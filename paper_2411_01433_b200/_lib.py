@@ -80,6 +80,8 @@ _SIGS = {
     "hb_last_expert_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "hb_launch_count": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "hb_set_batched_min": (C.c_int, [_P, C.c_int]),
+    "hb_nccl_unique_id": (C.c_int, [_P]),
+    "hb_nccl_init": (C.c_int, [_P, _P]),
     "hb_profile": (C.c_int, [_P, C.c_int]),
     "hb_profile_read": (C.c_int, [_P, C.POINTER(C.c_float), C.c_int]),
     "hb_quantize_expert": (C.c_int, [C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <dlfcn.h>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -101,6 +102,9 @@ struct hb_ctx {
   __half* k3_xg = nullptr;
   __half* k3_hB = nullptr;
   K3Table* k3_tab = nullptr;
+  // EP exchange (A10) inside the library: NCCL all-reduce of y after the
+  // expert kernels (hb_nccl_init); NCCL is dlopen'ed (the process's copy)
+  void* nccl_comm = nullptr;
   CUtensorMap* k3_tmap = nullptr;         // [L][E][4][6] device tensor maps of the blobs (K3)
   cudaEvent_t dec_ready = nullptr;
   // kernel timing (hb_profile)
@@ -130,6 +134,39 @@ static int fail(hb_ctx* c, int code, const std::string& msg) {
 }
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---- NCCL, resolved at run time (libnccl.so.2 already loaded by the process,
+// e.g. torch's, or found on the library path; HB_NCCL_LIB overrides)
+struct NcclId { char internal[128]; };
+struct NcclApi {
+  int (*get_unique_id)(NcclId*) = nullptr;
+  int (*comm_init_rank)(void**, int, NcclId, int) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  bool ok = false;
+};
+static NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    const char* env = std::getenv("HB_NCCL_LIB");
+    void* h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.get_unique_id = (int (*)(NcclId*))dlsym(h, "ncclGetUniqueId");
+      api.comm_init_rank = (int (*)(void**, int, NcclId, int))dlsym(h, "ncclCommInitRank");
+      api.all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+          h, "ncclAllReduce");
+      api.comm_destroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+      api.error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+      api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy;
+    }
+  }
+  return api;
+}
+constexpr int kNcclFloat32 = 7, kNcclSum = 0;
 
 extern "C" {
 
@@ -206,6 +243,7 @@ static void free_ctx(hb_ctx* c) {
   if (c->dec_ready) cudaEventDestroy(c->dec_ready);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->nccl_comm) nccl_api().comm_destroy(c->nccl_comm);
   delete c->cache;
   delete c;
 }
@@ -521,6 +559,17 @@ static void launch_gemv(hb_ctx* c, const GemvParams& gp, cudaStream_t s) {
   c->launches += 2;
 }
 
+// A10: sum this rank's partial y over the EP ranks (in place, on the stream)
+static int ep_reduce(hb_ctx* c, void* y, int batch, cudaStream_t s) {
+  if (!c->nccl_comm) return HB_OK;
+  const int r = nccl_api().all_reduce(y, y, (size_t)batch * c->cfg.hidden, kNcclFloat32, kNcclSum,
+                                      c->nccl_comm, s);
+  if (r != 0)
+    return fail(c, HB_ECUDA, std::string("ncclAllReduce: ") +
+                                 (nccl_api().error_string ? nccl_api().error_string(r) : "error"));
+  return HB_OK;
+}
+
 // K3 chain (batched decode / prefill): vjob3 table + X gather, K3a, K3b
 static void launch_batched(hb_ctx* c, int layer, const void* x, void* y, cudaStream_t s) {
   K3Params kp{};
@@ -615,7 +664,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
     }
     c->last_host_decisions = false;
     CUDA_TRY(c, cudaGetLastError());
-    return HB_OK;
+    return ep_reduce(c, y, batch, s);
   }
 
   // ---- offload mode: decisions to the host, cache state machine, loads ----
@@ -685,7 +734,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
       CUDA_TRY(c, cudaEventRecord(c->slot_free[pool[i]][slot[i]], s));
   c->last_host_decisions = true;
   CUDA_TRY(c, cudaGetLastError());
-  return HB_OK;
+  return ep_reduce(c, y, batch, s);
 }
 
 int expert_cache_load(hb_ctx* c, int layer, int expert, int enc, void* stream) {
@@ -799,6 +848,34 @@ int hb_last_expert_bytes(hb_ctx* c, uint64_t* out) {
     tot += c->bbytes[d[i].served_enc];
   }
   *out = tot;
+  return HB_OK;
+}
+
+int hb_nccl_unique_id(void* out) {
+  if (!out) return fail(nullptr, HB_EINVAL, "null argument");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(nullptr, HB_EUNSUPPORTED, "libnccl.so.2 not found (HB_NCCL_LIB)");
+  NcclId id;
+  const int r = api.get_unique_id(&id);
+  if (r != 0) return fail(nullptr, HB_ECUDA, "ncclGetUniqueId failed");
+  std::memcpy(out, &id, sizeof(id));
+  return HB_OK;
+}
+
+int hb_nccl_init(hb_ctx* c, const void* unique_id) {
+  if (!c || !unique_id) return fail(c, HB_EINVAL, "null argument");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(c, HB_EUNSUPPORTED, "libnccl.so.2 not found (HB_NCCL_LIB)");
+  if (c->nccl_comm) return fail(c, HB_ESTATE, "NCCL communicator already initialised");
+  NcclId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int r = api.comm_init_rank(&c->nccl_comm, c->cfg.world, id, c->cfg.rank);
+  if (r != 0) {
+    c->nccl_comm = nullptr;
+    return fail(c, HB_ECUDA, std::string("ncclCommInitRank: ") +
+                                 (api.error_string ? api.error_string(r) : "error"));
+  }
   return HB_OK;
 }
 

@@ -154,6 +154,20 @@ class Context:
         n = self._check(lib.hb_profile_read(self._h, buf, cap))
         return [(buf[2 * i], buf[2 * i + 1]) for i in range(n)]
 
+    def nccl_init(self, group=None):
+        """EP exchange inside the library (A10): rank 0 makes an NCCL unique id,
+        torch.distributed broadcasts it, every rank joins; afterwards forward()
+        returns the EP-reduced y.  Single process (no process group): world 1."""
+        import torch.distributed as dist
+        uid = (C.c_char * 128)()
+        if not dist.is_available() or not dist.is_initialized() or dist.get_rank(group) == 0:
+            check(lib.hb_nccl_unique_id(uid))
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            C.memmove(uid, obj[0], 128)
+        self._check(lib.hb_nccl_init(self._h, uid))
+
     def set_batched_min(self, min_batch: int):
         """Batches >= min_batch take the tcgen05 grouped-GEMM path K3 (0 = never)."""
         self._check(lib.hb_set_batched_min(self._h, min_batch))

@@ -324,3 +324,17 @@ def test_errors_are_loud():
     off.set_router(0, sg.router_weights(sh, 0))
     with pytest.raises(h.HobbitError):          # forward before token_begin
         off.forward(0, x[:1], y[:1])
+
+
+def test_ep_nccl_reduce_inside_library_world1():
+    """A10 inside the library: after hb_nccl_init (one rank, the only case one
+    GPU can run) moe_layer_forward ends with the NCCL all-reduce of y; with
+    world = 1 it is the identity, for the K2 and the K3 path."""
+    sh = sg.TINY
+    x16 = sg.hidden_states(sh, 8, 0, batch=12)
+    for bm in (0, 8):
+        ref = _run(_resident(sh, [0], fm.F16, fm.Q4, max_batch=12, batched_min=bm), 0, x16)
+        ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=12, batched_min=bm)
+        ctx.nccl_init()
+        y = _run(ctx, 0, x16)
+        np.testing.assert_allclose(y, ref, rtol=1e-5, atol=1e-6)
