@@ -177,7 +177,7 @@ int moe_layer_forward(hb_ctx* ctx, int layer, const void* x, int batch,
  * batch >= min_batch run the expert FFN as a grouped GEMM on the tcgen05
  * tensor cores (weights dequantised to fp16 in shared memory, fp32 TMEM
  * accumulation, h rounded to fp16: DESIGN.md R26) instead of the dequant-GEMV.
- * Decisions are unchanged.  0 = never.  Default 8 (env HB_K3_MIN_BATCH).
+ * Decisions are unchanged.  0 = never.  Default 4 (env HB_K3_MIN_BATCH).
  * HB_EUNSUPPORTED if the context was created with max_batch == 1. */
 int hb_set_batched_min(hb_ctx* ctx, int min_batch);
 

@@ -96,7 +96,7 @@ struct hb_ctx {
   float k2b_w[4] = {1.f, 2.f, 4.f, 8.f};  // HB_K2B_W: K2b CTA-split cost per unit (~ weights per KB)
   // K3: tcgen05 grouped GEMM for batches >= k3_min_batch (A9); buffers exist
   // when max_batch > 1 and the vjob3 table bound fits
-  int k3_min_batch = 8;                   // HB_K3_MIN_BATCH / hb_set_batched_min (K3 wins from B = 8, profiles/r01_batched.md)
+  int k3_min_batch = 4;                   // HB_K3_MIN_BATCH / hb_set_batched_min (K3 wins from B = 4, profiles/r01_batched.md)
   bool k3_ok = false;
   int k3_ks = 1;
   __half* k3_xg = nullptr;

@@ -121,7 +121,7 @@ def test_k3_zero_input():
 
 
 def test_k3_default_threshold_routes_batches():
-    """Default context: batch >= 8 takes K3 (launch count says which chain ran)."""
+    """Default context: batch >= 4 takes K3 (launch count says which chain ran)."""
     sh = sg.TINY
     from paper_2411_01433_b200 import hobbit as h
     cfg = h.default_config(n_layers=1, n_experts=8, top_k=2, hidden=256, ffn=512, max_batch=16)
@@ -132,7 +132,7 @@ def test_k3_default_threshold_routes_batches():
     x = torch.from_numpy(sg.hidden_states(sh, 34, 0, batch=16)).cuda()
     y = torch.empty(16, sh.hidden, dtype=torch.float32, device="cuda")
     n0 = ctx.launch_count()
-    ctx.forward(0, x[:4], y[:4])
+    ctx.forward(0, x[:3], y[:3])
     n1 = ctx.launch_count()
     ctx.forward(0, x, y)
     n2 = ctx.launch_count()
