@@ -521,25 +521,30 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
         if (NMAT == 2 && tid == 0) K3_STAMP(1, ntr++);
         const uint32_t raw = sbase + rs * kRawBytes;
         for (int c = 0; c < cpr; ++c) {
-          if (lane == 0) bar_wait(can_empty(cs), cph ^ 1);
-          __syncwarp();
-          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
           // step-uniform offsets inside the raw slot (oracle/formats.py layout)
           const int u = enc == HB_Q8 ? c : enc == HB_Q4 ? (c >> 1) : (c >> 2);
           const int coff = enc == HB_Q8 ? 0 : enc == HB_Q4 ? 8 * (c & 1) : 4 * (c & 3);
           const int soff = enc == HB_Q8 ? 0 : enc == HB_Q4 ? 4 * (c & 1) : 4 * (c & 3);
+          // dequantise into registers first (the raw slot is ready), then wait
+          // for the A stage: the ALU chain overlaps the MMA of older stages
+          uint4 w[NMAT][2];
 #pragma unroll
           for (int m = 0; m < NMAT; ++m) {
             const int su = u * 8 + tl;                // raw slot [m][u][tile]
             const uint32_t code = raw + m * (8 * ru * 1024) + su * 1024 + rr * 64 + 16 * t + coff;
             const uint32_t sc = raw + kRawCode + m * (8 * ru * 16 * sb) + su * 16 * sb + rr * sb + soff;
-            uint4 w0, w1;
-            dequant16(enc, code, sc, w0, w1);
+            dequant16(enc, code, sc, w[m][0], w[m][1]);
+          }
+          if (lane == 0) bar_wait(can_empty(cs), cph ^ 1);
+          __syncwarp();
+          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) {
             // UMMA K-major SWIZZLE_64B (as the TMA path): K chunk kc of a row in
             // block kc / 4 (8 KB = 128 rows x 64 B), 16-byte slot (kc % 4) ^ ((row / 2) % 4)
             const uint32_t dst = can + m * kAMat + row * 64 + ((t ^ ((row >> 1) & 3)) << 4);
-            sts128(dst, w0);
-            sts128(dst + 8192, w1);
+            sts128(dst, w[m][0]);
+            sts128(dst + 8192, w[m][1]);
           }
 #ifndef HB_K3_NOFENCE
           fence_async_smem();
