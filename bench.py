@@ -375,6 +375,7 @@ def run_ours(args):
         "gpu_launches": int(gpu_launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "frac_vs_8000_spec": round(achieved / 8000.0, 4),
                      "traffic": traffic, "traffic_source": traffic_src,
                      "alg_bytes_per_launch_pair": int(gemv_bytes / (nprof * L)),
                      "kernel": "K2a+K2b dequant-GEMV (gemv_kernel<1>, gemv_kernel<0>)",
