@@ -217,7 +217,10 @@ __device__ __forceinline__ void decide_k2_warp(const RouterParams& p, const i128
 }
 
 constexpr int kMaxDecSmem = 512;
-constexpr int kRouterCluster = 8;      // CTAs (SMs) per (route layer, token) row       // route-0 decisions kept in shared memory
+#ifndef HB_ROUTER_CLUSTER
+#define HB_ROUTER_CLUSTER 8
+#endif
+constexpr int kRouterCluster = HB_ROUTER_CLUSTER;   // CTAs (SMs) per (route layer, token) row (decode)
 
 struct RouterSmem {
   i128 L[64];                          // this CTA's exact logits
