@@ -13,7 +13,7 @@ constexpr int kMaxTopK = 8;
 constexpr int kMaxRouteLayers = 4;      // 1 + max lookahead p handled per launch
 constexpr int kNumSM = 148;             // B200
 #ifndef HB_GEMV_WARPS
-#define HB_GEMV_WARPS 16
+#define HB_GEMV_WARPS 12   // 12 x 168 registers: no spills (16 x 128 spilled 700 B; r01 sweep 8/10/12/14/16)
 #endif
 #ifndef HB_WARP_SMEM_KB
 #define HB_WARP_SMEM_KB 13
