@@ -93,7 +93,7 @@ struct hb_ctx {
   float static_frac = 0.8f;               // GEMV work feed K2a (HB_STATIC_FRAC, HB_CHUNK)
   float static_frac2 = 0.8f;              // K2b (HB_STATIC_FRAC2)
   int chunk = 8;
-  float k2b_w[4] = {1.f, 2.f, 4.f, 8.f};  // HB_K2B_W: K2b CTA-split cost per unit (~ weights per KB)
+  float k2b_w[4] = {1.f, 2.f, 3.f, 8.f};  // HB_K2B_W: K2b CTA-split cost per unit (~ weights per KB)
   // K3: tcgen05 grouped GEMM for batches >= k3_min_batch (A9); buffers exist
   // when max_batch > 1 and the vjob3 table bound fits
   int k3_min_batch = 4;                   // HB_K3_MIN_BATCH / hb_set_batched_min (K3 wins from B = 4, profiles/r01_batched.md)
