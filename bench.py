@@ -176,7 +176,7 @@ def run_ours(args):
     hi, lo = PAIRS[args.pair]
     L, Hd = shape.n_layers, shape.hidden
     t_init = time.time()
-    ctx, blobs = build_model(h, sg, None, shape, hi, lo, rank, world, local)
+    ctx, blobs = build_model(h, sg, None, shape, hi, lo, rank, world, local, t1=args.t1, t2=args.t2)
     # EP exchange (A10): by default inside the library (hb_nccl_init: the
     # forward ends with the NCCL all-reduce of y); HB_BENCH_TORCH_ALLREDUCE=1
     # reduces with torch.distributed instead
@@ -364,7 +364,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f16 weights / q4 codes, fp32 accumulate", "data": "synthetic",
-        "config": {"workload": WORKLOAD if (args.model, args.pair) == ("mixtral", "f16q4")
+        "config": {"workload": WORKLOAD if (args.model, args.pair, args.t1, args.t2) == ("mixtral", "f16q4", 0.6, 0.9)
                    else f"DIAGNOSTIC {shape.name} pair {args.pair} (not the headline workload)",
                    "global_batch": 1, "layers": L, "experts": shape.n_experts,
                    "top_k": shape.top_k, "hidden": Hd, "ffn": shape.ffn, "pair": args.pair,
@@ -546,6 +546,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batched", action="store_true", help="skip the K3 batched/prefill extra")
+    ap.add_argument("--t1", type=float, default=0.6, help="diagnostics only (1.0/1.0 = all-High)")
+    ap.add_argument("--t2", type=float, default=0.9, help="diagnostics only")
     ap.add_argument("--cpu-sample", type=int, default=2)
     ap.add_argument("--ref-max-steps", type=int, default=12)
     ap.add_argument("--model", choices=["mixtral", "phi"], default="mixtral",
