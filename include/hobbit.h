@@ -26,8 +26,10 @@
  *    the device and is OVERWRITTEN with this rank's part of Eq. 1.
  *  - A context is not thread-safe: one context per GPU per host thread.
  *  - Expert-parallel (EP): rank r owns experts e with e % world == r.  Each
- *    rank computes the exact router itself (no decision exchange); the caller
- *    sums y over ranks (NCCL all-reduce).
+ *    rank computes the exact router itself (no decision exchange).  Without
+ *    hb_nccl_init y is this rank's part of Eq. 1; after it the library sums y
+ *    over the ranks itself (in-place NCCL all-reduce at the end of
+ *    moe_layer_forward), and hb_ep_broadcast_x replicates x from a root rank.
  */
 #ifndef HOBBIT_H
 #define HOBBIT_H
@@ -47,6 +49,7 @@ extern "C" {
 #define HB_ECUDA        -4  /* CUDA runtime error */
 #define HB_ENOMEM       -5  /* host or device allocation failed */
 #define HB_EUNSUPPORTED -6  /* e.g. constrained cache with batch > 1 */
+#define HB_ENCCL        -7  /* NCCL call failed (EP exchange) */
 
 /* ------------------------------------------------------ encodings, levels */
 /* Expert encodings (fp16+int4 and int8+int2 pairs).  Block = 32
@@ -55,10 +58,17 @@ extern "C" {
  *   HB_Q8   w = d*q,      q int8 [-127,127] 8.5 bits/weight
  *   HB_Q4   w = d*(q-8),  q in [0,15]       4.5 bits/weight
  *   HB_Q2   w = d*q + m,  q in [0,3]        3.0 bits/weight
- * Blob = W1 [F,H], W3 [F,H], W2 [H,F]; each matrix = a code section and a
- * scale section (d, and m for Q2), each 256-byte aligned.  Codes are stored
- * tile-major: 16 rows x one 64-byte group of K = one contiguous 1 KB "unit";
- * exact element order in DESIGN.md "Blob layout" (hb_blob_section()). */
+ * Blob = W1 [F,H], W3 [F,H], W2 [H,F], two layouts of the same size:
+ *  - CANONICAL (the interchange format): per matrix the code
+ *    section q, [N,K] row-major, element k of a row at bit (k*b) mod 8 of
+ *    byte floor(k*b/8) (LSB first; Q4 low nibble = even element; Q8 int8),
+ *    F16 values row-major; then d [N][K/32] fp16; then (Q2) m [N][K/32] fp16;
+ *    each section 256-byte aligned (hb_canonical_section()).
+ *  - DEVICE (what the kernels stream): per matrix a code
+ *    section stored tile-major -- 16 rows x one 64-byte group of K = one
+ *    contiguous 1 KB "unit" -- and one scale section of per-(unit,row) d/m
+ *    records (hb_blob_section()).  hb_repack_canonical converts; the
+ *    quantiser writes it directly. */
 enum { HB_F16 = 0, HB_Q8 = 1, HB_Q4 = 2, HB_Q2 = 3 };
 /* Precision decision of one selected expert. */
 enum { HB_HIGH = 0, HB_LOW = 1, HB_SKIP = 2 };
@@ -75,6 +85,11 @@ typedef struct {
   int allow_upgrade;                /* Low request served by a cached High copy (1) */
   int rank, world;                  /* EP: owner(e) = e % world */
   int max_batch;                    /* tokens per forward call */
+  int strict;                       /* 1 (default): every Low selection is computed from
+                                       lo_enc.  0: in resident mode a Low selection of an
+                                       expert that some token of the same forward selected
+                                       High is served by the hi_enc copy -- one weight stream
+                                       per touched expert (R27; needs allow_upgrade) */
 } hb_config;
 
 /* One routed (token, rank) pair of the last forward (inspection / parity). */
@@ -103,10 +118,18 @@ typedef struct hb_ctx hb_ctx;
 void        hb_config_default(hb_config* cfg);
 size_t      hb_blob_bytes(int enc, int hidden, int ffn);
 /* Offset/size of section sec (0 codes / fp16 values, 1 scales) of matrix mat
- * (0 W1, 1 W3, 2 W2) inside a blob.  HB_EINVAL if the section does not exist
- * (F16 has no scale section). */
+ * (0 W1, 1 W3, 2 W2) inside a DEVICE-layout blob.  HB_EINVAL if the section
+ * does not exist (F16 has no scale section). */
 int         hb_blob_section(int enc, int hidden, int ffn, int mat, int sec,
                             size_t* offset, size_t* nbytes);
+/* Same for a CANONICAL blob: sec 0 codes / fp16 values, 1 d, 2 m (Q2 only). */
+int         hb_canonical_section(int enc, int hidden, int ffn, int mat, int sec,
+                                 size_t* offset, size_t* nbytes);
+/* Convert a canonical blob into the device layout: src and dst are device
+ * pointers of hb_blob_bytes(enc, H, F) bytes each, not overlapping, owned by
+ * the caller; stream-ordered (SURVEY.md 8(b) "canonical expert blob"). */
+int         hb_repack_canonical(int enc, int hidden, int ffn, const void* src, void* dst,
+                                void* stream);
 /* k = 2 gap threshold floor(ln(T/(1-T)) * 2^48) (exact-integer form of the
  * T1/T2 test, R9).  *kind = 0 finite, +1 T>=1 (always), -1 T<=0. */
 int64_t     hb_theta(double t, int* kind);
@@ -125,17 +148,28 @@ int hb_destroy(hb_ctx* ctx);
  * copy on the null stream).  Stacked prediction reads these per layer. */
 int hb_set_router(hb_ctx* ctx, int layer, const void* w, int on_device);
 
-/* Register the blob of expert (layer, expert) in encoding enc.
+/* Register the blob of expert (layer, expert) in encoding enc.  flags = a
+ * mode, optionally | HB_REG_CANONICAL:
  *   HB_REG_DEVICE_BORROW  blob is device memory owned by the caller that
  *                         outlives ctx (fully resident mode: cap_* = -1);
+ *                         device layout only;
+ *   HB_REG_DEVICE_COPY    blob is device memory; copied into HBM owned by
+ *                         the library (resident mode); the caller may free it
+ *                         on return;
  *   HB_REG_HOST_PINNED    blob is caller-owned pinned host memory that
  *                         outlives ctx (offload mode: next-level storage);
- *   HB_REG_HOST_COPY      blob is any host memory; copied into the
- *                         library's pinned arena (offload mode).
- * nbytes must equal hb_blob_bytes(enc, H, F).  Only owned experts. */
+ *                         device layout only;
+ *   HB_REG_HOST_COPY      blob is any host memory; copied into the library's
+ *                         pinned arena (offload mode) or its HBM (resident).
+ *   HB_REG_CANONICAL      the blob is in the canonical layout; the library
+ *                         converts it (hb_repack_canonical) while copying.
+ * nbytes must equal hb_blob_bytes(enc, H, F).  Only owned experts.  The COPY
+ * modes synchronise the device. */
 #define HB_REG_DEVICE_BORROW 1
 #define HB_REG_HOST_PINNED   2
 #define HB_REG_HOST_COPY     3
+#define HB_REG_DEVICE_COPY   4
+#define HB_REG_CANONICAL     0x100
 int hb_register_expert(hb_ctx* ctx, int layer, int expert, int enc,
                        const void* blob, size_t nbytes, int flags);
 
@@ -192,6 +226,10 @@ int hb_set_batched_min(hb_ctx* ctx, int min_batch);
  * HB_EUNSUPPORTED if it cannot be found. */
 int hb_nccl_unique_id(void* unique_id_out /* 128 bytes */);
 int hb_nccl_init(hb_ctx* ctx, const void* unique_id);
+/* X1: replicate the gating input x [batch, hidden] fp16 (device,
+ * caller-owned) from EP rank `root` to every rank, in place, on `stream`
+ * (ncclBroadcast; collective, after hb_nccl_init; HB_ESTATE without it). */
+int hb_ep_broadcast_x(hb_ctx* ctx, void* x, int batch, int root, void* stream);
 
 /* ------------------------------------------------------------ inspection */
 /* Decisions of the last forward: batch*top_k records (synchronises). */

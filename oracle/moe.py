@@ -12,6 +12,7 @@ Everything below is fp64 on the exactly decoded weights.
 from __future__ import annotations
 
 import numpy as np
+from scipy.special import expit
 
 from .formats import decode_blob
 from .router import HIGH, LOW, SKIP, route
@@ -38,6 +39,32 @@ def served_encoding_strict(decision: int, hi_enc: int, lo_enc: int):
     if decision == LOW:
         return lo_enc
     return None
+
+
+def served_encodings_resident(routes, hi_enc: int, lo_enc: int, strict: bool = True):
+    """O7 for one fully resident forward over a batch of tokens -> served[b][i].
+
+    strict (the benches' default): High -> hi_enc, Low -> lo_enc, Skip -> None.
+    Non-strict (R27; SURVEY 8(d) C5 "allow_upgrade = 1, one stream
+    per touched expert"; reading A6 "Low is served by High when allow_upgrade"):
+    both versions are resident, and a Low selection of expert e is served by
+    the hi_enc copy when some token of the SAME forward selected e as High --
+    that expert's High weights are streamed anyway, so the Low request costs
+    no extra bytes.  Otherwise Low -> lo_enc.
+    """
+    high = {e for r in routes for e, d in zip(r.experts, r.decisions) if d == HIGH}
+    out = []
+    for r in routes:
+        row = []
+        for e, d in zip(r.experts, r.decisions):
+            if d == SKIP:
+                row.append(None)
+            elif d == HIGH or (not strict and e in high):
+                row.append(hi_enc)
+            else:
+                row.append(lo_enc)
+        out.append(row)
+    return out
 
 
 class ExpertStore:
@@ -102,7 +129,9 @@ def dense_topk_moe(x16: np.ndarray, wg16: np.ndarray, experts_f64, k: int) -> np
     W2 = np.stack([w[2] for w in experts_f64])                  # [E,H,F]
     a = np.einsum("efh,bh->bef", W1, x)
     u = np.einsum("efh,bh->bef", W3, x)
-    h = silu(a) * u
+    # SwiGLU activation taken independently of silu() above: the logistic
+    # function from scipy.special.expit, so a slip in silu() fails the pin
+    h = a * expit(a) * u
     o = np.einsum("ehf,bef->beh", W2, h)                         # [B,E,H]
     p = np.exp(logits - logits.max(axis=1, keepdims=True))
     p /= p.sum(axis=1, keepdims=True)

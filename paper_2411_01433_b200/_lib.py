@@ -17,13 +17,15 @@ ROOT = os.path.dirname(PKG)
 LIB_PATH = os.environ.get("HOBBIT_LIB") or os.path.join(PKG, "libhobbit.so")
 HEADER = os.path.join(ROOT, "include", "hobbit.h")
 
-HB_OK, HB_EINVAL, HB_ECAPACITY, HB_ESTATE, HB_ECUDA, HB_ENOMEM, HB_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+HB_OK, HB_EINVAL, HB_ECAPACITY, HB_ESTATE, HB_ECUDA, HB_ENOMEM, HB_EUNSUPPORTED, HB_ENCCL = \
+    0, -1, -2, -3, -4, -5, -6, -7
 ERR_NAMES = {-1: "HB_EINVAL", -2: "HB_ECAPACITY", -3: "HB_ESTATE", -4: "HB_ECUDA",
-             -5: "HB_ENOMEM", -6: "HB_EUNSUPPORTED"}
+             -5: "HB_ENOMEM", -6: "HB_EUNSUPPORTED", -7: "HB_ENCCL"}
 HB_F16, HB_Q8, HB_Q4, HB_Q2 = 0, 1, 2, 3
 HB_HIGH, HB_LOW, HB_SKIP = 0, 1, 2
 HB_ENC_NONE = 255
-HB_REG_DEVICE_BORROW, HB_REG_HOST_PINNED, HB_REG_HOST_COPY = 1, 2, 3
+HB_REG_DEVICE_BORROW, HB_REG_HOST_PINNED, HB_REG_HOST_COPY, HB_REG_DEVICE_COPY = 1, 2, 3, 4
+HB_REG_CANONICAL = 0x100
 
 
 class HobbitError(RuntimeError):
@@ -38,7 +40,8 @@ class hb_config(C.Structure):
                 ("t1", C.c_double), ("t2", C.c_double), ("lookahead_p", C.c_int),
                 ("w_lru", C.c_int), ("w_lfu", C.c_int), ("w_lhu", C.c_int), ("w_fld", C.c_int),
                 ("cap_high", C.c_int), ("cap_low", C.c_int), ("allow_upgrade", C.c_int),
-                ("rank", C.c_int), ("world", C.c_int), ("max_batch", C.c_int)]
+                ("rank", C.c_int), ("world", C.c_int), ("max_batch", C.c_int),
+                ("strict", C.c_int)]
 
 
 class hb_decision(C.Structure):
@@ -62,6 +65,9 @@ _SIGS = {
     "hb_blob_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
     "hb_blob_section": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "hb_canonical_section": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "hb_repack_canonical": (C.c_int, [C.c_int, C.c_int, C.c_int, _P, _P, _P]),
     "hb_theta": (C.c_int64, [C.c_double, C.POINTER(C.c_int)]),
     "hb_last_error": (C.c_char_p, [_P]),
     "hb_version": (C.c_char_p, []),
@@ -82,6 +88,7 @@ _SIGS = {
     "hb_set_batched_min": (C.c_int, [_P, C.c_int]),
     "hb_nccl_unique_id": (C.c_int, [_P]),
     "hb_nccl_init": (C.c_int, [_P, _P]),
+    "hb_ep_broadcast_x": (C.c_int, [_P, _P, C.c_int, C.c_int, _P]),
     "hb_profile": (C.c_int, [_P, C.c_int]),
     "hb_profile_read": (C.c_int, [_P, C.POINTER(C.c_float), C.c_int]),
     "hb_quantize_expert": (C.c_int, [C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
@@ -146,6 +153,12 @@ def blob_bytes(enc, hidden, ffn) -> int:
 def blob_section(enc, hidden, ffn, mat, sec):
     off, nb = C.c_size_t(), C.c_size_t()
     check(lib.hb_blob_section(enc, hidden, ffn, mat, sec, C.byref(off), C.byref(nb)))
+    return off.value, nb.value
+
+
+def canonical_section(enc, hidden, ffn, mat, sec):
+    off, nb = C.c_size_t(), C.c_size_t()
+    check(lib.hb_canonical_section(enc, hidden, ffn, mat, sec, C.byref(off), C.byref(nb)))
     return off.value, nb.value
 
 

@@ -11,7 +11,9 @@
 #include <dlfcn.h>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -21,6 +23,19 @@
 #include "hobbit.h"
 
 namespace hb {
+
+cudaError_t set_max_dyn_smem_impl(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kernel, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kernel, dev});
+  return e;
+}
 
 int blob_layout(int enc, int hidden, int ffn, BlobLayout* out) {
   if (enc < HB_F16 || enc > HB_Q2 || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
@@ -64,6 +79,7 @@ struct hb_ctx {
   // offload registry: host blobs [L][E][4]
   std::vector<const uint8_t*> host_blob;
   std::vector<void*> arena;               // pinned copies owned by the library
+  std::vector<void*> dev_owned;           // resident blobs copied into library HBM
   uint8_t* pool_mem[2] = {nullptr, nullptr};
   size_t slot_bytes[2] = {0, 0};
   std::vector<cudaEvent_t> slot_ready[2], slot_free[2];
@@ -143,6 +159,7 @@ struct NcclApi {
   int (*comm_init_rank)(void**, int, NcclId, int) = nullptr;
   int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*comm_destroy)(void*) = nullptr;
+  int (*broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   const char* (*error_string)(int) = nullptr;
   bool ok = false;
 };
@@ -160,13 +177,16 @@ static NcclApi& nccl_api() {
       api.all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
           h, "ncclAllReduce");
       api.comm_destroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+      api.broadcast = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+          h, "ncclBroadcast");
       api.error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
-      api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy;
+      api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy &&
+               api.broadcast;
     }
   }
   return api;
 }
-constexpr int kNcclFloat32 = 7, kNcclSum = 0;
+constexpr int kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclSum = 0;
 
 extern "C" {
 
@@ -189,6 +209,7 @@ void hb_config_default(hb_config* c) {
   c->rank = 0;
   c->world = 1;
   c->max_batch = 1;
+  c->strict = 1;
 }
 
 size_t hb_blob_bytes(int enc, int hidden, int ffn) {
@@ -208,6 +229,29 @@ int hb_blob_section(int enc, int hidden, int ffn, int mat, int sec, size_t* offs
   if (enc == HB_F16 || sec == 2) return fail(nullptr, HB_EINVAL, "section does not exist");
   *offset = L.mat[mat].s;
   *nbytes = (size_t)N * (K / 32) * 2 * (enc == HB_Q2 ? 2 : 1);
+  return HB_OK;
+}
+
+int hb_canonical_section(int enc, int hidden, int ffn, int mat, int sec, size_t* offset,
+                         size_t* nbytes) {
+  CanonLayout C;
+  if (canonical_layout(enc, hidden, ffn, &C) || mat < 0 || mat > 2 || sec < 0 || sec > 2 ||
+      !offset || !nbytes)
+    return fail(nullptr, HB_EINVAL, "bad canonical section query");
+  const int N = mat < 2 ? ffn : hidden, K = mat < 2 ? hidden : ffn;
+  const int bits = enc == HB_F16 ? 16 : enc == HB_Q8 ? 8 : enc == HB_Q4 ? 4 : 2;
+  if (sec == 0) { *offset = C.q[mat]; *nbytes = (size_t)N * K * bits / 8; return HB_OK; }
+  if (enc == HB_F16 || (sec == 2 && enc != HB_Q2)) return fail(nullptr, HB_EINVAL, "section does not exist");
+  *offset = sec == 1 ? C.d[mat] : C.m[mat];
+  *nbytes = (size_t)N * (K / 32) * 2;
+  return HB_OK;
+}
+
+int hb_repack_canonical(int enc, int hidden, int ffn, const void* src, void* dst, void* stream) {
+  if (!src || !dst) return fail(nullptr, HB_EINVAL, "null argument");
+  const int rc = launch_repack_canonical(enc, hidden, ffn, (const uint8_t*)src, (uint8_t*)dst,
+                                         (cudaStream_t)stream);
+  if (rc) return fail(nullptr, rc, rc == HB_EINVAL ? "bad enc / dims" : "repack launch failed");
   return HB_OK;
 }
 
@@ -236,6 +280,7 @@ static void free_ctx(hb_ctx* c) {
   if (c->dec_host) cudaFreeHost(c->dec_host);
   if (c->jt_host) cudaFreeHost(c->jt_host);
   for (void* p : c->arena) cudaFreeHost(p);
+  for (void* p : c->dev_owned) cudaFree(p);
   for (int i = 0; i < 2; ++i) {
     for (cudaEvent_t e : c->slot_ready[i]) cudaEventDestroy(e);
     for (cudaEvent_t e : c->slot_free[i]) cudaEventDestroy(e);
@@ -419,6 +464,37 @@ int hb_set_router(hb_ctx* c, int layer, const void* w, int on_device) {
   return HB_OK;
 }
 
+// a blob in device memory (library-owned), converted from the canonical
+// layout when asked: src is host or device memory of nbytes
+static int copy_to_device(hb_ctx* c, const void* src, bool src_host, bool canonical,
+                          size_t nbytes, int enc, uint8_t** out) {
+  uint8_t* dst = nullptr;
+  if (cudaMalloc((void**)&dst, nbytes) != cudaSuccess) return fail(c, HB_ENOMEM, "device blob allocation failed");
+  uint8_t* tmp = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (!canonical) {
+    e = cudaMemcpy(dst, src, nbytes, src_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice);
+  } else {
+    const uint8_t* csrc = (const uint8_t*)src;
+    if (src_host) {
+      e = cudaMalloc((void**)&tmp, nbytes);
+      if (e == cudaSuccess) e = cudaMemcpy(tmp, src, nbytes, cudaMemcpyHostToDevice);
+      csrc = tmp;
+    }
+    if (e == cudaSuccess &&
+        launch_repack_canonical(enc, c->cfg.hidden, c->cfg.ffn, csrc, dst, nullptr) != HB_OK)
+      e = cudaErrorLaunchFailure;
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  if (tmp) cudaFree(tmp);
+  if (e != cudaSuccess) {
+    cudaFree(dst);
+    return fail(c, HB_ECUDA, std::string("blob copy / repack: ") + cudaGetErrorString(e));
+  }
+  *out = dst;
+  return HB_OK;
+}
+
 int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* blob,
                        size_t nbytes, int flags) {
   if (!c || !blob) return fail(c, HB_EINVAL, "null argument");
@@ -428,20 +504,32 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
   if (enc != k.hi_enc && enc != k.lo_enc) return fail(c, HB_EINVAL, "encoding is neither hi_enc nor lo_enc");
   if (nbytes != c->bbytes[enc]) return fail(c, HB_EINVAL, "blob size != hb_blob_bytes(enc, H, F)");
   if (expert % k.world != k.rank) return fail(c, HB_EINVAL, "expert not owned by this rank");
+  const bool canonical = (flags & HB_REG_CANONICAL) != 0;
+  const int mode = flags & ~HB_REG_CANONICAL;
   const size_t idx = ((size_t)layer * k.n_experts + expert) * 4 + enc;
+  CUDA_TRY(c, cudaSetDevice(c->device));
   if (c->resident) {
-    if (flags != HB_REG_DEVICE_BORROW) return fail(c, HB_EINVAL, "resident mode takes device blobs");
-    c->dev_blob[idx] = (const uint8_t*)blob;
-    CUDA_TRY(c, cudaSetDevice(c->device));
+    const uint8_t* dblob = (const uint8_t*)blob;
+    if (mode == HB_REG_DEVICE_BORROW) {
+      if (canonical) return fail(c, HB_EINVAL, "a borrowed blob must be in the device layout");
+    } else if (mode == HB_REG_DEVICE_COPY || mode == HB_REG_HOST_COPY) {
+      uint8_t* owned = nullptr;
+      if (int rc = copy_to_device(c, blob, mode == HB_REG_HOST_COPY, canonical, nbytes, enc, &owned))
+        return rc;
+      c->dev_owned.push_back(owned);
+      dblob = owned;
+    } else {
+      return fail(c, HB_EINVAL, "resident mode takes HB_REG_DEVICE_BORROW / DEVICE_COPY / HOST_COPY");
+    }
+    c->dev_blob[idx] = dblob;
     if (c->k3_tmap) {                           // K3: TMA tensor maps of W1, W3, W2
       CUtensorMap m[6];
       std::memset(m, 0, sizeof(m));
       const int rows[3] = {k.ffn, k.ffn, k.hidden}, cols[3] = {k.hidden, k.hidden, k.ffn};
-      const uint8_t* b = (const uint8_t*)blob;
       for (int i = 0; i < 3; ++i) {
         const MatLayout& ML = c->lay[enc].mat[i];
-        const int rc = enc == HB_F16 ? k3_encode_f16_map(&m[i], b + ML.q, rows[i], cols[i])
-                                     : k3_encode_q_maps(&m[i], &m[3 + i], enc, b + ML.q, b + ML.s,
+        const int rc = enc == HB_F16 ? k3_encode_f16_map(&m[i], dblob + ML.q, rows[i], cols[i])
+                                     : k3_encode_q_maps(&m[i], &m[3 + i], enc, dblob + ML.q, dblob + ML.s,
                                                         rows[i], cols[i]);
         if (rc) return fail(c, HB_ECUDA, "cuTensorMapEncodeTiled failed");
       }
@@ -452,17 +540,32 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
                            cudaMemcpyHostToDevice));
     return HB_OK;
   }
-  if (flags == HB_REG_HOST_PINNED) {
+  if (mode == HB_REG_HOST_PINNED) {
+    if (canonical) return fail(c, HB_EINVAL, "a borrowed blob must be in the device layout");
     c->host_blob[idx] = (const uint8_t*)blob;
-  } else if (flags == HB_REG_HOST_COPY) {
+  } else if (mode == HB_REG_HOST_COPY) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, nbytes, cudaHostAllocDefault) != cudaSuccess)
       return fail(c, HB_ENOMEM, "pinned arena allocation failed");
-    std::memcpy(p, blob, nbytes);
+    if (canonical) {                            // convert on the device, back into the arena
+      uint8_t* dev = nullptr;
+      if (int rc = copy_to_device(c, blob, true, true, nbytes, enc, &dev)) {
+        cudaFreeHost(p);
+        return rc;
+      }
+      const cudaError_t e = cudaMemcpy(p, dev, nbytes, cudaMemcpyDeviceToHost);
+      cudaFree(dev);
+      if (e != cudaSuccess) {
+        cudaFreeHost(p);
+        return fail(c, HB_ECUDA, "arena copy-back failed");
+      }
+    } else {
+      std::memcpy(p, blob, nbytes);
+    }
     c->arena.push_back(p);
     c->host_blob[idx] = (const uint8_t*)p;
   } else {
-    return fail(c, HB_EINVAL, "offload mode takes host blobs");
+    return fail(c, HB_EINVAL, "offload mode takes HB_REG_HOST_PINNED / HB_REG_HOST_COPY");
   }
   return HB_OK;
 }
@@ -477,6 +580,9 @@ int hb_token_begin(hb_ctx* c) {
 int hb_reset_sequence(hb_ctx* c) {
   if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
   if (c->cache) c->cache->reset_sequence();
+  // T = 0 after a reset: Eq. 3 divides by T, so the next forward needs
+  // hb_token_begin first (T >= 1)
+  c->token_started = false;
   return HB_OK;
 }
 
@@ -498,6 +604,7 @@ static RouterParams router_params(hb_ctx* c, const void* x, int batch) {
   p.t2 = k.t2;
   p.rank = k.rank;
   p.world = k.world;
+  p.strict = k.strict || !k.allow_upgrade || !c->resident;
   p.hi_enc = k.hi_enc;
   p.lo_enc = k.lo_enc;
   p.jt = c->jt;
@@ -565,7 +672,7 @@ static int ep_reduce(hb_ctx* c, void* y, int batch, cudaStream_t s) {
   const int r = nccl_api().all_reduce(y, y, (size_t)batch * c->cfg.hidden, kNcclFloat32, kNcclSum,
                                       c->nccl_comm, s);
   if (r != 0)
-    return fail(c, HB_ECUDA, std::string("ncclAllReduce: ") +
+    return fail(c, HB_ENCCL, std::string("ncclAllReduce: ") +
                                  (nccl_api().error_string ? nccl_api().error_string(r) : "error"));
   return HB_OK;
 }
@@ -687,8 +794,13 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   const size_t ev0 = c->cache->events.size();
   int rc = c->cache->forward(layer, ex, pr, served, pool, slot, hit);
   if (rc) {
+    // inserts made before the failing selection are real: their copies must
+    // still be issued, or the cache would map keys to slots holding the
+    // victims' weights
+    const std::string why = c->cache->err;
+    const int lrc = issue_loads(c, ev0);
     drain_events(c);
-    return fail(c, rc, c->cache->err);
+    return lrc ? lrc : fail(c, rc, why);
   }
   rc = issue_loads(c, ev0);
   drain_events(c);
@@ -792,7 +904,12 @@ int prefetch_next_layer(hb_ctx* c, int layer, const void* x, int batch, void* st
   const size_t ev0 = c->cache->events.size();
   int pl = -1;
   int rc = c->cache->prefetch(layer, n, ex.data(), pr.data(), &pl);
-  if (rc) return fail(c, rc, c->cache->err);
+  if (rc) {                                          // issue the inserts made so far
+    const std::string why = c->cache->err;
+    const int lrc = issue_loads(c, ev0);
+    drain_events(c);
+    return lrc ? lrc : fail(c, rc, why);
+  }
   int queued = 0;
   for (size_t i = ev0; i < c->cache->events.size(); ++i) queued += c->cache->events[i].type == 1;
   rc = issue_loads(c, ev0);
@@ -857,7 +974,7 @@ int hb_nccl_unique_id(void* out) {
   if (!api.ok) return fail(nullptr, HB_EUNSUPPORTED, "libnccl.so.2 not found (HB_NCCL_LIB)");
   NcclId id;
   const int r = api.get_unique_id(&id);
-  if (r != 0) return fail(nullptr, HB_ECUDA, "ncclGetUniqueId failed");
+  if (r != 0) return fail(nullptr, HB_ENCCL, "ncclGetUniqueId failed");
   std::memcpy(out, &id, sizeof(id));
   return HB_OK;
 }
@@ -873,9 +990,23 @@ int hb_nccl_init(hb_ctx* c, const void* unique_id) {
   const int r = api.comm_init_rank(&c->nccl_comm, c->cfg.world, id, c->cfg.rank);
   if (r != 0) {
     c->nccl_comm = nullptr;
-    return fail(c, HB_ECUDA, std::string("ncclCommInitRank: ") +
+    return fail(c, HB_ENCCL, std::string("ncclCommInitRank: ") +
                                  (api.error_string ? api.error_string(r) : "error"));
   }
+  return HB_OK;
+}
+
+int hb_ep_broadcast_x(hb_ctx* c, void* x, int batch, int root, void* stream) {
+  if (!c || !x) return fail(c, HB_EINVAL, "null argument");
+  if (batch <= 0 || batch > c->cfg.max_batch) return fail(c, HB_EINVAL, "batch must be in [1, max_batch]");
+  if (root < 0 || root >= c->cfg.world) return fail(c, HB_EINVAL, "bad root rank");
+  if (!c->nccl_comm) return fail(c, HB_ESTATE, "hb_nccl_init first");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int r = nccl_api().broadcast(x, x, (size_t)batch * c->cfg.hidden, kNcclFloat16, root,
+                                     c->nccl_comm, (cudaStream_t)stream);
+  if (r != 0)
+    return fail(c, HB_ENCCL, std::string("ncclBroadcast: ") +
+                                 (nccl_api().error_string ? nccl_api().error_string(r) : "error"));
   return HB_OK;
 }
 

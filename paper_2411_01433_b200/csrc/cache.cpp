@@ -97,6 +97,10 @@ int ExpertCache::insert(int pool, int key, int cur_layer, bool exclude_current) 
 
 int ExpertCache::forward(int layer, const int32_t* experts, const uint8_t* prec,
                          uint8_t* served, int* pool_out, int* slot_out, uint8_t* hit_out) {
+  if (T_ == 0) {               // Eq. 3 divides by T: a forward needs token_begin first
+    err = "forward before token_begin (T = 0)";
+    return HB_ESTATE;
+  }
   drop_masks(layer - 1);
   for (int k : cur_list_) cur_[k] = 0;
   cur_list_.clear();
@@ -221,8 +225,25 @@ int ExpertCache::load(int layer, int expert, int enc, bool* queued) {
 struct hb_cache {
   hb::ExpertCache* c;
   int top_k;
+  int n_layers, n_experts, hi_enc, lo_enc;
   std::string err;
 };
+
+// argument validation of the host-only ABI (the device context checks the same)
+static int bad(hb_cache* c, const char* why) {
+  c->err = why;
+  return HB_EINVAL;
+}
+static int check_layer(hb_cache* c, int layer) {
+  return layer < 0 || layer >= c->n_layers ? bad(c, "bad layer") : HB_OK;
+}
+static int check_sel(hb_cache* c, int n, const int32_t* experts, const uint8_t* prec) {
+  for (int i = 0; i < n; ++i) {
+    if (experts[i] < 0 || experts[i] >= c->n_experts) return bad(c, "bad expert id");
+    if (prec[i] > HB_SKIP) return bad(c, "bad precision code");
+  }
+  return HB_OK;
+}
 
 static int check_cfg_cache(const hb_config* cfg, std::string* err) {
   if (!cfg || cfg->n_layers <= 0 || cfg->n_experts <= 0 || cfg->top_k <= 0 ||
@@ -250,6 +271,10 @@ int hbc_create(const hb_config* cfg, hb_cache** out) {
                                             cfg->world);
   if (!c->c) { delete c; return HB_ENOMEM; }
   c->top_k = cfg->top_k;
+  c->n_layers = cfg->n_layers;
+  c->n_experts = cfg->n_experts;
+  c->hi_enc = cfg->hi_enc;
+  c->lo_enc = cfg->lo_enc;
   *out = c;
   return HB_OK;
 }
@@ -267,6 +292,8 @@ int hbc_reset_sequence(hb_cache* c) { if (!c) return HB_EINVAL; c->c->reset_sequ
 int hbc_forward(hb_cache* c, int layer, const int32_t* experts, const uint8_t* prec,
                 uint8_t* served) {
   if (!c || !experts || !prec || !served) return HB_EINVAL;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (int rc = check_sel(c, c->top_k, experts, prec)) return rc;
   std::vector<int> pool(c->top_k), slot(c->top_k);
   std::vector<uint8_t> hit(c->top_k);
   int rc = c->c->forward(layer, experts, prec, served, pool.data(), slot.data(), hit.data());
@@ -276,12 +303,21 @@ int hbc_forward(hb_cache* c, int layer, const int32_t* experts, const uint8_t* p
 
 int hbc_prefetch(hb_cache* c, int layer, int n_pred, const int32_t* experts,
                  const uint8_t* prec, int* prefetched) {
-  if (!c || !prefetched || n_pred < 0) return HB_EINVAL;
-  return c->c->prefetch(layer, n_pred, experts, prec, prefetched);
+  if (!c || !prefetched || n_pred < 0 || (n_pred > 0 && (!experts || !prec))) return HB_EINVAL;
+  if (int rc = check_layer(c, layer)) return rc;
+  const int np = std::min(n_pred, c->n_layers - 1 - layer);
+  if (np > 0)
+    if (int rc = check_sel(c, np * c->top_k, experts, prec)) return rc;
+  const int rc = c->c->prefetch(layer, n_pred, experts, prec, prefetched);
+  if (rc) c->err = c->c->err;
+  return rc;
 }
 
 int hbc_load(hb_cache* c, int layer, int expert, int enc) {
   if (!c) return HB_EINVAL;
+  if (int rc = check_layer(c, layer)) return rc;
+  if (expert < 0 || expert >= c->n_experts) return bad(c, "bad expert id");
+  if (enc != c->hi_enc && enc != c->lo_enc) return bad(c, "encoding is neither hi_enc nor lo_enc");
   bool q;
   int rc = c->c->load(layer, expert, enc, &q);
   if (rc) c->err = c->c->err;

@@ -954,18 +954,9 @@ __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvP
   }
 }
 
-template <typename Kern>
-static void set_smem(Kern kernel, int bytes, bool& done) {
-  if (!done) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    done = true;
-  }
-}
-
 void launch_w13(const GemvParams& p, cudaStream_t s) {
-  static bool d = false;
   constexpr int smem = gemv_smem_bytes<true>();
-  set_smem(gemv_kernel<true>, smem, d);
+  set_max_dyn_smem(gemv_kernel<true>, smem);
   launch_pdl(gemv_kernel<true>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
 }
 void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
@@ -973,9 +964,8 @@ void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
   launch_pdl(hfin_kernel, (n + 255) / 256, 256, 0, s, p);
 }
 void launch_w2(const GemvParams& p, cudaStream_t s) {
-  static bool d = false;
   constexpr int smem = gemv_smem_bytes<false>();
-  set_smem(gemv_kernel<false>, smem, d);
+  set_max_dyn_smem(gemv_kernel<false>, smem);
   launch_pdl(gemv_kernel<false>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
 }
 int w2_stage_capacity() { return KCfg<false>::XSTAGE; }

@@ -33,6 +33,16 @@ struct BlobLayout {
   uint64_t total;
 };
 int blob_layout(int enc, int hidden, int ffn, BlobLayout* out);   // host
+// Canonical blob (include/hobbit.h): per matrix the code
+// section q (row-major, LSB first), d [N][K/32] and (Q2) m, 256-byte aligned.
+struct CanonLayout {
+  uint64_t q[3], d[3], m[3];   // section offsets per matrix (0 when absent)
+  uint64_t total;
+};
+int canonical_layout(int enc, int hidden, int ffn, CanonLayout* out);   // host
+// canonical (device) -> device layout (device), stream-ordered
+int launch_repack_canonical(int enc, int hidden, int ffn, const uint8_t* src, uint8_t* dst,
+                            cudaStream_t s);
 
 // One (expert, served encoding) group of a layer on this rank: the GEMV
 // kernels stream its blob once for all of its token slots.
@@ -113,6 +123,7 @@ struct RouterParams {
   int th1_kind, th2_kind;              // 0 finite, +1 always true, -1 never
   double t1, t2;                       // k > 2 fp64 test
   int rank, world;
+  int strict;                          // 0: Low served by hi_enc when the expert is touched High (R27)
   hb_decision* dec;                    // [n_route][B][k]
   long long* lbuf;                     // [n_route][B][E][2] exact logits (scratch)
   long long* logits;                   // [B][E][2] copy for route 0, or null
@@ -167,6 +178,13 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device: set it once per
+// (kernel, current device), thread-safe (a process may drive several GPUs)
+cudaError_t set_max_dyn_smem_impl(const void* kernel, int bytes);
+template <typename... KArgs>
+inline cudaError_t set_max_dyn_smem(void (*kernel)(KArgs...), int bytes) {
+  return set_max_dyn_smem_impl(reinterpret_cast<const void*>(kernel), bytes);
 }
 void launch_w13(const GemvParams& p, cudaStream_t s);
 void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s);

@@ -802,14 +802,6 @@ __global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* 
   }
 }
 
-template <typename K>
-void set_smem_once(K kernel, int bytes, bool& done) {
-  if (!done) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    done = true;
-  }
-}
-
 }  // namespace
 
 int k3_smem_bytes() { return kSmem; }
@@ -880,16 +872,14 @@ void launch_k3_prep(const K3Params& p, const __half* x, cudaStream_t s) {
   k3_prep_kernel<<<2 * kNumSM, 256, 0, s>>>(p, x);
 }
 void launch_k3a(const K3Params& p, cudaStream_t s) {
-  static bool d = false, dd = false;
-  set_smem_once(k3_kernel<2>, kSmem, d);
-  set_smem_once(k3d_kernel<2>, d_smem<2>(), dd);
+  set_max_dyn_smem(k3_kernel<2>, kSmem);
+  set_max_dyn_smem(k3d_kernel<2>, d_smem<2>());
   if (p.has_f16) k3d_kernel<2><<<kNumSM, kDThreads, d_smem<2>(), s>>>(p);
   if (p.has_q) k3_kernel<2><<<kNumSM, kThreads, kSmem, s>>>(p);
 }
 void launch_k3b(const K3Params& p, cudaStream_t s) {
-  static bool d = false, dd = false;
-  set_smem_once(k3_kernel<1>, kSmem, d);
-  set_smem_once(k3d_kernel<1>, d_smem<1>(), dd);
+  set_max_dyn_smem(k3_kernel<1>, kSmem);
+  set_max_dyn_smem(k3d_kernel<1>, d_smem<1>());
   if (p.has_f16) k3d_kernel<1><<<kNumSM, kDThreads, d_smem<1>(), s>>>(p);
   if (p.has_q) k3_kernel<1><<<kNumSM, kThreads, kSmem, s>>>(p);
 }

@@ -224,14 +224,29 @@ constexpr int kRouterCluster = HB_ROUTER_CLUSTER;   // CTAs (SMs) per (route lay
 
 struct RouterSmem {
   i128 L[64];                          // this CTA's exact logits
-  u64 part[kRouterThreads / 32][3];    // per-warp partial (lo, mid, hi)
+  u64 part[64 > kRouterThreads / 32 ? 64 : kRouterThreads / 32][3];  // per task (E*wpe <= max(64, NW))
   u64 cpart[64][3];                    // this CTA's partial per expert (read by the leader)
   hb_decision dec[kMaxDecSmem];        // route-0 decisions (single-CTA / last-CTA path)
   const uint8_t* blob[64 * 4];         // blob table of the layer
   Job jobs[2 * 64 + 1];
   int count[2 * 64], jobid[2 * 64], fill[2 * 64];
+  unsigned long long hmask;            // experts with a High selection (non-strict upgrade)
   int last;
 };
+
+// Job key of a selection: expert * 2 + (served from lo_enc), or -1 (Skip /
+// not owned).  Non-strict mode (R27): a Low selection of an expert
+// that a High selection of the same forward also touches is served by the
+// hi_enc copy (hmask bit e), so every touched expert is streamed once.
+__device__ __forceinline__ int sel_key(const RouterParams& p, const hb_decision& d,
+                                       unsigned long long hmask) {
+  if (d.prec == HB_SKIP || d.expert < 0 || d.expert % p.world != p.rank) return -1;
+  const bool hi = d.prec == HB_HIGH || (!p.strict && ((hmask >> d.expert) & 1ull));
+  return d.expert * 2 + (hi ? 0 : 1);
+}
+__device__ __forceinline__ unsigned long long high_bit(const RouterParams& p, const hb_decision& d) {
+  return (d.prec == HB_HIGH && d.expert >= 0 && d.expert % p.world == p.rank) ? 1ull << d.expert : 0ull;
+}
 
 // resident mode: group the non-skipped owned selections into (expert, enc)
 // jobs, ordered by expert then High before Low; slots in token order.  All
@@ -240,10 +255,11 @@ __device__ void build_jobs(const RouterParams& p, RouterSmem& sm, const hb_decis
   const int nkey = 2 * p.E;
   for (int i = 0; i < nkey; ++i) sm.count[i] = 0;
   const int nsel = p.B * p.k;
+  unsigned long long hmask = 0ull;
+  for (int i = 0; i < nsel; ++i) hmask |= high_bit(p, dec[i]);
   for (int i = 0; i < nsel; ++i) {
-    const hb_decision d = dec[i];
-    if (d.prec == HB_SKIP || d.expert % p.world != p.rank) continue;
-    sm.count[d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1)]++;
+    const int key = sel_key(p, dec[i], hmask);
+    if (key >= 0) sm.count[key]++;
   }
   int nj = 0, off = 0;
   for (int key = 0; key < nkey; ++key) {
@@ -266,8 +282,8 @@ __device__ void build_jobs(const RouterParams& p, RouterSmem& sm, const hb_decis
   for (int i = 0; i < nsel; ++i) {
     hb_decision d = dec[i];
     p.jt.tok_slots[i] = -1;
-    if (d.prec == HB_SKIP || d.expert % p.world != p.rank) continue;
-    const int key = d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1);
+    const int key = sel_key(p, d, hmask);
+    if (key < 0) continue;
     const int slot = sm.jobs[sm.jobid[key]].slot_off + sm.fill[key]++;
     p.jt.slot_token[slot] = d.token;
     p.jt.slot_gate[slot] = d.gate;
@@ -289,11 +305,18 @@ __device__ void build_jobs(const RouterParams& p, RouterSmem& sm, const hb_decis
 __device__ void build_jobs_cta(const RouterParams& p, RouterSmem& sm, const hb_decision* dec) {
   const int nkey = 2 * p.E, nsel = p.B * p.k, tid = threadIdx.x;
   for (int i = tid; i < nkey; i += blockDim.x) { sm.count[i] = 0; sm.fill[i] = 0; }
+  if (tid == 0) sm.hmask = 0ull;
   __syncthreads();
+  if (!p.strict) {
+    unsigned long long hm = 0ull;
+    for (int i = tid; i < nsel; i += blockDim.x) hm |= high_bit(p, dec[i]);
+    if (hm) atomicOr(&sm.hmask, hm);
+    __syncthreads();
+  }
+  const unsigned long long hmask = sm.hmask;
   for (int i = tid; i < nsel; i += blockDim.x) {
-    const hb_decision d = dec[i];
-    if (d.prec == HB_SKIP || d.expert % p.world != p.rank) continue;
-    atomicAdd(&sm.count[d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1)], 1);
+    const int key = sel_key(p, dec[i], hmask);
+    if (key >= 0) atomicAdd(&sm.count[key], 1);
   }
   __syncthreads();
   if (tid == 0) {
@@ -327,8 +350,7 @@ __device__ void build_jobs_cta(const RouterParams& p, RouterSmem& sm, const hb_d
       hb_decision d;
       if (i < nsel) {
         d = dec[i];
-        if (d.prec != HB_SKIP && d.expert % p.world == p.rank)
-          key = d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1);
+        key = sel_key(p, d, hmask);
       }
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       const int rank = __popc(peers & ((1u << lane) - 1u));
@@ -361,10 +383,14 @@ __device__ __forceinline__ void build_jobs_warp(const RouterParams& p, RouterSme
   constexpr int kNone = 0x7FFFFFFF;
   hb_decision d{};
   int key = kNone;
+  if (lane < nsel) d = dec[lane];
+  const unsigned long long hb = lane < nsel ? high_bit(p, d) : 0ull;
+  const unsigned long long hmask =
+      ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(hb >> 32)) << 32) |
+      __reduce_or_sync(0xffffffffu, (unsigned)hb);
   if (lane < nsel) {
-    d = dec[lane];
-    if (d.prec != HB_SKIP && d.expert % p.world == p.rank)
-      key = d.expert * 2 + (d.prec == HB_HIGH ? 0 : 1);
+    const int k0 = sel_key(p, d, hmask);
+    if (k0 >= 0) key = k0;
   }
   const bool valid = key != kNone;
   int less = 0, rank = 0, ntok = 0;

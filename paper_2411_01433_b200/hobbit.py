@@ -20,8 +20,9 @@ import torch
 
 from . import _lib as L
 from ._lib import (HB_ENC_NONE, HB_F16, HB_HIGH, HB_LOW, HB_Q2, HB_Q4, HB_Q8,  # noqa: F401
-                   HB_REG_DEVICE_BORROW, HB_REG_HOST_COPY, HB_REG_HOST_PINNED, HB_SKIP,
-                   HobbitError, blob_bytes, blob_section, default_config, theta)
+                   HB_REG_CANONICAL, HB_REG_DEVICE_BORROW, HB_REG_DEVICE_COPY, HB_REG_HOST_COPY,
+                   HB_REG_HOST_PINNED, HB_SKIP, HobbitError, blob_bytes, blob_section,
+                   canonical_section, default_config, theta)
 
 check = L.check
 lib = L.lib
@@ -82,17 +83,26 @@ class Context:
             w = np.ascontiguousarray(w, dtype=np.float16)
         self._check(lib.hb_set_router(self._h, layer, _ptr(w), 1 if on_dev else 0))
 
-    def register_expert(self, layer: int, expert: int, enc: int, blob, flags: int | None = None):
+    def register_expert(self, layer: int, expert: int, enc: int, blob, flags: int | None = None,
+                        canonical: bool = False):
+        """Device-layout blobs are borrowed (device / pinned host) or copied;
+        canonical=True (SURVEY 8(b) layout, e.g. the oracle's) is always copied
+        and converted by the library."""
         if flags is None:
-            if isinstance(blob, torch.Tensor) and blob.is_cuda:
+            dev = isinstance(blob, torch.Tensor) and blob.is_cuda
+            if canonical:
+                flags = HB_REG_DEVICE_COPY if dev else HB_REG_HOST_COPY
+            elif dev:
                 flags = HB_REG_DEVICE_BORROW
             elif isinstance(blob, torch.Tensor) and blob.is_pinned():
                 flags = HB_REG_HOST_PINNED
             else:
                 flags = HB_REG_HOST_COPY
+            if canonical:
+                flags |= HB_REG_CANONICAL
         self._check(lib.hb_register_expert(self._h, layer, expert, enc, _ptr(blob),
                                            _nbytes(blob), flags))
-        if flags != HB_REG_HOST_COPY:
+        if (flags & ~HB_REG_CANONICAL) in (HB_REG_DEVICE_BORROW, HB_REG_HOST_PINNED):
             self._keep.append(blob)
 
     def token_begin(self):
@@ -168,6 +178,11 @@ class Context:
             C.memmove(uid, obj[0], 128)
         self._check(lib.hb_nccl_init(self._h, uid))
 
+    def broadcast_x(self, x: torch.Tensor, root: int = 0, stream=None):
+        """X1: x [B,H] fp16 (device) replicated from EP rank root, in place."""
+        assert x.dtype == torch.float16
+        self._check(lib.hb_ep_broadcast_x(self._h, _ptr(x), x.shape[0], root, _stream(stream)))
+
     def set_batched_min(self, min_batch: int):
         """Batches >= min_batch take the tcgen05 grouped-GEMM path K3 (0 = never)."""
         self._check(lib.hb_set_batched_min(self._h, min_batch))
@@ -241,6 +256,17 @@ def quantize_expert(enc: int, w1: torch.Tensor, w3: torch.Tensor, w2: torch.Tens
     assert out.numel() == nb
     check(lib.hb_quantize_expert(enc, hidden, ffn, _ptr(w1), _ptr(w3), _ptr(w2), _ptr(out),
                                  _stream(stream)))
+    return out
+
+
+def repack_canonical(enc: int, hidden: int, ffn: int, src: torch.Tensor,
+                     out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Device-layout blob from a canonical one (both uint8, device)."""
+    nb = blob_bytes(enc, hidden, ffn)
+    assert src.numel() == nb and src.is_cuda
+    if out is None:
+        out = torch.zeros(nb, dtype=torch.uint8, device=src.device)
+    check(lib.hb_repack_canonical(enc, hidden, ffn, _ptr(src), _ptr(out), _stream(stream)))
     return out
 
 

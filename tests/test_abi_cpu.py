@@ -9,7 +9,9 @@ from oracle import cache as oc
 from oracle import formats as fm
 from oracle import router as rt
 from paper_2411_01433_b200 import _lib as L
-from paper_2411_01433_b200.hobbit import HostCache, blob_bytes, blob_section, default_config, theta
+from paper_2411_01433_b200.hobbit import (HostCache, blob_bytes, blob_section, canonical_section,
+                                          default_config, theta)
+from tests import layout_spec as ls
 
 
 def test_every_header_symbol_is_exported_and_bound():
@@ -28,17 +30,28 @@ def test_version_and_error_string():
 @pytest.mark.parametrize("enc", [fm.F16, fm.Q8, fm.Q4, fm.Q2])
 @pytest.mark.parametrize("hf", [(256, 512), (4096, 14336), (4096, 6400), (512, 256)])
 def test_blob_layout_matches_oracle(enc, hf):
+    """hb_canonical_section = the oracle's canonical sections; hb_blob_section =
+    the device layout of tests/layout_spec.py; both the same total size."""
     H, F = hf
     assert blob_bytes(enc, H, F) == fm.blob_bytes(enc, H, F)
     lay, _ = fm.blob_layout(enc, H, F)
     for mat in range(3):
-        for sec, name in enumerate(["q", "s", "none"]):
+        for sec, name in enumerate(["q", "d", "m"]):
             key = "w" if (enc == fm.F16 and name == "q") else name
             if key not in lay[mat]:
                 with pytest.raises(L.HobbitError):
-                    blob_section(enc, H, F, mat, sec)
+                    canonical_section(enc, H, F, mat, sec)
                 continue
-            assert blob_section(enc, H, F, mat, sec) == lay[mat][key]
+            assert canonical_section(enc, H, F, mat, sec) == lay[mat][key]
+    secs, total = ls.sections(enc, H, F)
+    assert total == blob_bytes(enc, H, F)
+    for mat, (q, s) in enumerate(secs):
+        assert blob_section(enc, H, F, mat, 0)[0] == q
+        if s is None:
+            with pytest.raises(L.HobbitError):
+                blob_section(enc, H, F, mat, 1)
+        else:
+            assert blob_section(enc, H, F, mat, 1)[0] == s
 
 
 def test_blob_layout_rejects_bad_dims():

@@ -47,12 +47,24 @@ def test_synth_kernel_bit_exact(n, sigma, start):
 @pytest.mark.parametrize("shape", [sg.TINY, sg.MoEShape("phi-slice", 1, 1, 2, 4096, 6400, 1.8)],
                          ids=["tiny", "phi"])
 def test_quantiser_bytes_bit_exact(enc, shape):
-    blob = gpu_blobs(shape, 0, [0], [enc])[(0, enc)].cpu().numpy()
+    """Three ways to the same device-layout bytes: the library's quantiser on
+    the library's generated weights; hb_repack_canonical of the ORACLE's
+    canonical blob (oracle generator + oracle quantiser); and the written
+    layout specification (tests/layout_spec.py) applied to that canonical blob
+    on the CPU.  Quantiser codes bit-exact, conversion bit-exact."""
+    from tests import layout_spec as ls
+    lib_blob = gpu_blobs(shape, 0, [0], [enc])[(0, enc)]
     w1, w3, w2 = sg.expert_weights(shape, 0, 0)
-    ref = fm.quantize_blob(enc, w1, w3, w2)
-    assert blob.shape == ref.shape
-    bad = np.nonzero(blob != ref)[0]
-    assert bad.size == 0, f"{bad.size} bytes differ, first at {bad[:8]}"
+    canon = fm.quantize_blob(enc, w1, w3, w2)
+    rep = H().repack_canonical(enc, shape.hidden, shape.ffn, torch.from_numpy(canon).cuda())
+    torch.cuda.synchronize()
+    a, b = lib_blob.cpu().numpy(), rep.cpu().numpy()
+    assert a.shape == b.shape == canon.shape
+    bad = np.nonzero(a != b)[0]
+    assert bad.size == 0, f"{bad.size} bytes differ (quantiser vs oracle), first at {bad[:8]}"
+    spec = ls.device_blob(enc, canon, shape.hidden, shape.ffn)
+    bad = np.nonzero(b != spec)[0]
+    assert bad.size == 0, f"{bad.size} bytes differ (repack vs layout spec), first at {bad[:8]}"
 
 
 # ------------------------------------------------------------ helpers
@@ -218,11 +230,14 @@ def test_cuda_graph_capture_replays():
 # ------------------------------------------------------------ full size
 @pytest.mark.parametrize("shape,pair,tokens", [
     (sg.MIXTRAL, (fm.F16, fm.Q4), 3), (sg.MIXTRAL, (fm.F16, fm.Q2), 2),
-    (sg.MIXTRAL, (fm.Q8, fm.Q2), 2), (sg.PHI, (fm.F16, fm.Q4), 3)],
-    ids=["mixtral-f16q4", "mixtral-f16q2", "mixtral-q8q2", "phi-f16q4"])
+    (sg.MIXTRAL, (fm.Q8, fm.Q2), 2), (sg.PHI, (fm.F16, fm.Q4), 3), (sg.PHI, (fm.F16, fm.Q2), 2)],
+    ids=["mixtral-f16q4", "mixtral-f16q2", "mixtral-q8q2", "phi-f16q4", "phi-f16q2"])
 def test_layer_parity_full_size(shape, pair, tokens):
     """BASELINE.json full shapes, batch-1 decode, the launch configuration the
-    bench times (one layer; all E experts of that layer resident)."""
+    bench times (one layer; all E experts of that layer resident).  Phi F16/Q2
+    takes K2b's unstaged-h path (G = 25 groups per row slice is odd).  Bar:
+    1e-4 normwise (the path keeps exact codes, ~1e-6 expected; a dropped h-lo
+    MMA would show ~2e-4), inside the north-star 2e-3."""
     hi, lo = pair
     layer = 5
     sh1 = sg.MoEShape(shape.name, shape.n_layers, shape.n_experts, 2, shape.hidden, shape.ffn,
@@ -236,7 +251,7 @@ def test_layer_parity_full_size(shape, pair, tokens):
         ref, routes = om.moe_layer(x16, wg, store, layer, 2, 0.6, 0.9, hi, lo)
         _check_routes(ctx, routes, 1, 2)
         nw, el = rel_err(y[0], ref[0])
-        assert nw <= TOL, (nw, el)
+        assert nw <= TOL and nw <= 1e-4, (nw, el)
 
 
 # ------------------------------------------------------------ offload path

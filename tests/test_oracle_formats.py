@@ -16,7 +16,7 @@ ENC = {"F16": fm.F16, "Q8": fm.Q8, "Q4": fm.Q4, "Q2": fm.Q2}
 
 
 def _load_fixture(name):
-    spec = {"bytes": {}, "expect": {}, "mins": None}
+    spec = {"bytes": {}, "expect": {}, "d": {}, "m": {}}
     with open(os.path.join(GOLDEN, name)) as f:
         for line in f:
             line = line.split("#", 1)[0].strip()
@@ -25,43 +25,44 @@ def _load_fixture(name):
             tok = line.split()
             if tok[0] == "enc":
                 spec["enc"] = ENC[tok[1]]
-            elif tok[0] == "K":
-                spec["K"] = int(tok[1])
-            elif tok[0] == "scales":
-                spec["scales"] = [int(v, 16) for v in tok[1:]]
-            elif tok[0] == "mins":
-                spec["mins"] = [int(v, 16) for v in tok[1:]]
+            elif tok[0] in ("N", "K"):
+                spec[tok[0]] = int(tok[1])
+            elif tok[0] in ("d", "m"):
+                spec[tok[0]][(int(tok[1]), int(tok[2]))] = int(tok[3], 16)
             elif tok[0] == "default":
                 spec["default"] = int(tok[1], 16)
             elif tok[0] == "byte":
                 spec["bytes"][int(tok[1])] = int(tok[2], 16)
             elif tok[0] == "expect":
-                spec["expect"][int(tok[1])] = float(tok[2])
+                spec["expect"][(int(tok[1]), int(tok[2]))] = float(tok[3])
     return spec
 
 
 @pytest.mark.parametrize("name", ["formats_q4.txt", "formats_q2.txt", "formats_q8.txt"])
 def test_decode_hand_worked(name):
-    # one 16-row tile, one group (K = EPG): row 0's 64 bytes are the first 64
-    # bytes of the code section and its scale record the first SB bytes of the
-    # scale section (d of each block, then m for Q2); other rows are defaults
+    """Canonical sections built from the fixture (code bytes, d/m per (row,
+    block)) decode to the hand-worked values, rows 0 and 1, blocks 0 and 1."""
     spec = _load_fixture(name)
-    enc, K = spec["enc"], spec["K"]
-    assert K == fm.EPG[enc]
-    q = np.full(16 * 64, spec["default"], dtype=np.uint8)
+    enc, N, K = spec["enc"], spec["N"], spec["K"]
+    q = np.full(N * K * fm.QBITS[enc] // 8, spec["default"], dtype=np.uint8)
     for off, v in spec["bytes"].items():
         q[off] = v
-    rec = spec["scales"] + (spec["mins"] or [])
-    s = np.zeros(16 * fm.scale_record_bytes(enc) // 2, dtype=np.uint16)
-    s[:len(rec)] = rec
-    blob = np.concatenate([q, s.view(np.uint8)])
-    secs = {"q": (0, q.size), "s": (q.size, s.nbytes)}
-    w = fm.decode_matrix(enc, blob, secs, 16, K)[0]
-    for k, v in spec["expect"].items():
-        assert w[k] == v, (name, k, w[k], v)
+    secs, parts, off = {"q": (0, q.size)}, [q], q.size
+    for which in ("d", "m"):
+        if not spec[which]:
+            continue
+        a = np.zeros((N, K // 32), dtype=np.uint16)
+        for (r, b), v in spec[which].items():
+            a[r, b] = v
+        secs[which] = (off, a.nbytes)
+        parts.append(a.view(np.uint8).ravel())
+        off += a.nbytes
+    w = fm.decode_matrix(enc, np.concatenate(parts), secs, N, K)
+    for (r, k), v in spec["expect"].items():
+        assert w[r, k] == v, (name, r, k, w[r, k], v)
     if enc == fm.Q4:      # every unlisted element has the default code 8 -> 0
         listed = set(spec["expect"])
-        assert all(w[k] == 0.0 for k in range(K) if k not in listed)
+        assert all(w[r, k] == 0.0 for r in range(N) for k in range(K) if (r, k) not in listed)
 
 
 def test_fp16_values():
@@ -69,36 +70,22 @@ def test_fp16_values():
     assert list(v.astype(np.float64)) == [0.5, 0.25, -0.375, 2.0 ** -6, 1.0]
 
 
-@pytest.mark.parametrize("enc", [fm.F16, fm.Q8, fm.Q4, fm.Q2])
-def test_code_offset_is_a_bijection(enc):
-    """Every bit of a 2-tile x 2-group code section is written by exactly one
-    element, and every scale byte by exactly one (row, block, d/m)."""
-    N, K = 32, 2 * fm.EPG[enc]
-    b = fm.QBITS[enc]
-    n, k = np.meshgrid(np.arange(N), np.arange(K), indexing="ij")
-    pos, shift = fm.code_offset(enc, n, k, K)
-    bits = (pos * 8 + shift)[..., None] + np.arange(b)
-    assert np.array_equal(np.sort(bits.ravel()), np.arange(N * K * b))
-    if enc == fm.F16:
-        return
-    nb, blk = np.meshgrid(np.arange(N), np.arange(K // 32), indexing="ij")
-    offs = [fm.scale_offset(enc, nb, blk, K, "d")]
-    if enc == fm.Q2:
-        offs.append(fm.scale_offset(enc, nb, blk, K, "m"))
-    allb = np.concatenate([(o[..., None] + np.arange(2)).ravel() for o in offs])
-    assert np.array_equal(np.sort(allb), np.arange(N * (K // fm.EPG[enc]) * fm.scale_record_bytes(enc)))
+def test_pack_codes_lsb_first_worked_example():
+    """element k at bit (k*b) mod 8 of byte floor(k*b/8).
+    Q4 codes (1, 2, 3, 4) -> bytes 0x21, 0x43; Q2 codes (1, 2, 3, 0, 3, ...) ->
+    0b00_11_10_01 = 0x39 then 0x03; Q8 -5 -> 0xFB (two's complement)."""
+    assert list(fm.pack_codes(fm.Q4, np.array([[1, 2, 3, 4] + [8] * 28]))[:2]) == [0x21, 0x43]
+    assert list(fm.pack_codes(fm.Q2, np.array([[1, 2, 3, 0, 3] + [0] * 27]))[:2]) == [0x39, 0x03]
+    assert fm.pack_codes(fm.Q8, np.array([[-5] + [0] * 31]))[0] == 0xFB
 
 
-def test_unit_is_contiguous():
-    """A unit (16 rows x one group) occupies one contiguous 1 KB of the code section."""
-    for enc in (fm.F16, fm.Q8, fm.Q4, fm.Q2):
-        K = 4 * fm.EPG[enc]
-        n, k = np.meshgrid(np.arange(16, 32), np.arange(2 * fm.EPG[enc], 3 * fm.EPG[enc]),
-                           indexing="ij")
-        pos, _ = fm.code_offset(enc, n, k, K)
-        unit = 1 * 4 + 2                      # tile 1, group 2
-        last = pos.max() + (1 if enc == fm.F16 else 0)    # fp16: 2-byte elements
-        assert pos.min() == 1024 * unit and last == 1024 * unit + 1023
+def test_f16_section_worked_example():
+    """F16 canonical section: element (1, 3) of a [2, 32] matrix is the fp16
+    at byte offset 2*(32*1 + 3) = 70, little endian; 0x3C00 -> 1.0."""
+    sec = np.zeros(2 * 32 * 2, dtype=np.uint8)
+    sec[70], sec[71] = 0x00, 0x3C
+    w = fm.decode_matrix(fm.F16, sec, {"w": (0, sec.size)}, 2, 32)
+    assert w[1, 3] == 1.0 and np.count_nonzero(w) == 1
 
 
 def test_quantiser_q4_worked_example():
@@ -112,6 +99,46 @@ def test_quantiser_q4_worked_example():
     blob = fm.quantize_blob(fm.Q4, np.zeros((256, 128), np.float16),
                             np.zeros((256, 128), np.float16), np.zeros((128, 256), np.float16))
     assert blob.size == fm.blob_bytes(fm.Q4, 128, 256)
+
+
+def test_quantiser_q8_ties_round_half_away():
+    """A8 reading (Q8 round-half-away, as ggml's roundf).  Block with amax
+    127/128 -> d = f16(127/128 / 127) = 2^-7 exactly; x/d is exact in fp32:
+    x = 2.5 d -> 3 (half-even would give 2), -2.5 d -> -3, 0.5 d -> 1 (half-even 0),
+    -0.5 d -> -1, 3.5 d -> 4, 1.25 d -> 1, amax -> 127."""
+    d = 2.0 ** -7
+    vals = [127 * d, 2.5 * d, -2.5 * d, 0.5 * d, -0.5 * d, 3.5 * d, 1.25 * d]
+    x = np.zeros((1, 32), dtype=np.float16)
+    x[0, :len(vals)] = vals
+    assert all(float(a) == b for a, b in zip(x[0, :len(vals)], vals))   # fp16-exact inputs
+    codes, d16, _ = fm.quantize_codes(fm.Q8, x)
+    assert float(d16[0, 0]) == d
+    assert list(codes[0, :len(vals)]) == [127, 3, -3, 1, -1, 4, 1]
+
+
+def test_quantiser_q2_ties_round_half_even():
+    """A8 reading (Q2 round-half-even).  Block min 0, max 3 -> d = f16(3/3) = 1,
+    m = 0; (x - m)/d = x: 0.5 -> 0 (half-away would give 1), 1.5 -> 2,
+    2.5 -> 2 (half-away 3), 2.75 -> 3, 3 -> 3."""
+    vals = [0.0, 3.0, 0.5, 1.5, 2.5, 2.75, 0.25]
+    x = np.zeros((1, 32), dtype=np.float16)
+    x[0, :len(vals)] = vals
+    codes, d16, m16 = fm.quantize_codes(fm.Q2, x)
+    assert float(d16[0, 0]) == 1.0 and float(m16[0, 0]) == 0.0
+    assert list(codes[0, :len(vals)]) == [0, 3, 0, 2, 2, 3, 0]
+
+
+def test_quantiser_q4_ties_floor_plus_half():
+    """A8 reading (Q4 q = floor(x/d + 8.5), ggml Q4_0).  Block max-magnitude
+    -1.0 -> d = -1/-8 = 0.125: x/d = 0.5 (x = 0.0625) -> floor(9.0) = 9;
+    x/d = -0.5 (x = -0.0625) -> floor(8.0) = 8; x/d = 1.5 -> 10; x/d = -1.5 -> 7;
+    +1.0 -> x/d = 8 -> floor(16.5) = 16 -> clamp 15."""
+    vals = [-1.0, 0.0625, -0.0625, 0.1875, -0.1875, 1.0]
+    x = np.zeros((1, 32), dtype=np.float16)
+    x[0, :len(vals)] = vals
+    codes, d16, _ = fm.quantize_codes(fm.Q4, x)
+    assert float(d16[0, 0]) == 0.125
+    assert list(codes[0, :len(vals)]) == [0, 9, 8, 10, 7, 15]
 
 
 def test_quantiser_zero_block_codes():
@@ -128,10 +155,14 @@ def test_quantiser_roundtrip_bound(enc):
     n, k = 64, 512
     w = (rng.standard_normal((n, k)) * 0.02).astype(np.float16)
     codes, d16, m16 = fm.quantize_codes(enc, w)
-    q = fm.pack_codes(enc, codes)
-    s = fm.pack_scales(enc, d16, m16)
-    blob = np.concatenate([q, s])
-    sec = {"q": (0, q.size), "s": (q.size, s.size)}
+    parts = [fm.pack_codes(enc, codes), d16.view(np.uint8).ravel()]
+    if m16 is not None:
+        parts.append(m16.view(np.uint8).ravel())
+    blob = np.concatenate(parts)
+    sizes = [p.size for p in parts]
+    sec = {"q": (0, sizes[0]), "d": (sizes[0], sizes[1])}
+    if m16 is not None:
+        sec["m"] = (sizes[0] + sizes[1], sizes[2])
     deq = fm.decode_matrix(enc, blob, sec, n, k)
     # and the decode reproduces the codes' own dequantisation element-wise
     dd = np.repeat(d16.astype(np.float64), 32, axis=1)

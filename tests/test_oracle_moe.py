@@ -129,3 +129,48 @@ def test_low_uses_quantised_version(store):
              + r.gates[1] * moe.expert_ffn(*store.get(0, r.experts[1], fm.F16), xf))
     np.testing.assert_allclose(y[b], want, rtol=1e-13)
     assert np.abs(y[b] - wrong).max() > 1e-6
+
+
+def test_silu_closed_form_values():
+    """silu(z) = z / (1 + e^-z) = z * sigmoid(z) (reading R10, SwiGLU as in
+    Mixtral/Phi).  Values worked from e = 2.718281828459045...:
+    sigmoid(1) = 1/(1 + 0.36787944117144233) = 0.7310585786300049, so
+    silu(1) = 0.7310585786300049 and silu(-1) = -sigmoid(-1) = -0.2689414213699951;
+    silu(4) = 4/(1 + 0.01831563888873418) = 3.928055160151634,
+    silu(-4) = -4 * 0.01798620996209156 = -0.07194483984836624.
+    A slip such as z/(1 + e^z) gives silu(1) = 0.2689..., caught here; the
+    identity silu(z) - silu(-z) = z and silu -> z (z >> 0), -> 0 (z << 0) too."""
+    z = np.array([1.0, -1.0, 4.0, -4.0, 0.0])
+    ref = np.array([0.7310585786300049, -0.2689414213699951, 3.928055160151634,
+                    -0.07194483984836624, 0.0])
+    assert np.allclose(moe.silu(z), ref, rtol=1e-15, atol=0)
+    w = np.linspace(-30, 30, 601)
+    assert np.allclose(moe.silu(w) - moe.silu(-w), w, rtol=0, atol=1e-12)
+    assert abs(moe.silu(np.array([40.0]))[0] - 40.0) < 1e-12
+    assert abs(moe.silu(np.array([-40.0]))[0]) < 1e-15
+
+
+def test_dense_reference_activation_matches_silu_independently():
+    """The dense top-k reference takes the logistic function from
+    scipy.special.expit, not through silu(): the two agree to rounding, and the
+    tanh form (1 + tanh(z/2))/2 agrees too away from its cancellation range."""
+    from scipy.special import expit
+    a = np.linspace(-20, 20, 4001)
+    assert np.allclose(a * expit(a), moe.silu(a), rtol=1e-14, atol=0)
+    b = np.linspace(-4, 20, 2401)
+    assert np.allclose(b * 0.5 * (1.0 + np.tanh(0.5 * b)), moe.silu(b), rtol=1e-12, atol=0)
+
+
+def test_served_encodings_resident_upgrade_rule():
+    """R27 worked example: token 0 selects (e3 High, e5 Low), token 1 (e5 High,
+    e3 Low), token 2 (e1 High, e3 Skip), token 3 (e6 High, e2 Low).
+    Strict: Low -> lo.  Non-strict: e5's and e3's Low requests are served by hi
+    (both touched High in this forward); e2's is not (never High); Skip stays."""
+    R = rt.Route
+    routes = [R([3, 5], [0.7, 0.3], [rt.HIGH, rt.LOW], None), R([5, 3], [0.6, 0.4], [rt.HIGH, rt.LOW], None),
+              R([1, 3], [0.95, 0.05], [rt.HIGH, rt.SKIP], None), R([6, 2], [0.8, 0.2], [rt.HIGH, rt.LOW], None)]
+    F, Q = fm.F16, fm.Q4
+    assert moe.served_encodings_resident(routes, F, Q, strict=True) == \
+        [[F, Q], [F, Q], [F, None], [F, Q]]
+    assert moe.served_encodings_resident(routes, F, Q, strict=False) == \
+        [[F, F], [F, F], [F, None], [F, Q]]
