@@ -252,6 +252,19 @@ int hb_launch_count(hb_ctx* ctx, uint64_t* out);
 int hb_profile(hb_ctx* ctx, int max_calls);
 int hb_profile_read(hb_ctx* ctx, float* ms, int cap);
 
+/* In-kernel timing of the fused batch-1 decode kernel (router + K2a + K2b in
+ * one launch), for the roofline: with max_forwards > 0
+ * the next max_forwards fused forwards -- including replays of CUDA graphs
+ * captured while it is on -- record %globaltimer stamps from inside the
+ * kernel (device atomics, no events, no serialisation).  Synchronises and
+ * clears the records; 0 disables for forwards issued afterwards.
+ * hb_stamps_read synchronises and returns n records of 5 uint64 ns each:
+ * [kernel start (first CTA past its wait on the previous kernel), decisions
+ * done (last CTA), K2a done (last CTA), grid barrier passed (first CTA),
+ * kernel end (last CTA)]; returns n. */
+int hb_stamps(hb_ctx* ctx, int max_forwards);
+int hb_stamps_read(hb_ctx* ctx, uint64_t* out, int cap);
+
 /* ------------------------------------------- offline quantiser, generator */
 /* Quantise an fp16 expert (W1 [F,H], W3 [F,H], W2 [H,F], device pointers)
  * into a device blob of hb_blob_bytes(enc, H, F) bytes (R8). */

@@ -91,6 +91,8 @@ _SIGS = {
     "hb_ep_broadcast_x": (C.c_int, [_P, _P, C.c_int, C.c_int, _P]),
     "hb_profile": (C.c_int, [_P, C.c_int]),
     "hb_profile_read": (C.c_int, [_P, C.POINTER(C.c_float), C.c_int]),
+    "hb_stamps": (C.c_int, [_P, C.c_int]),
+    "hb_stamps_read": (C.c_int, [_P, C.POINTER(C.c_uint64), C.c_int]),
     "hb_quantize_expert": (C.c_int, [C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
     "hb_synth_fill_f16": (C.c_int, [_P, C.c_size_t, C.c_uint64, C.c_float, C.c_uint64, _P]),
     "hbc_create": (C.c_int, [C.POINTER(hb_config), C.POINTER(_P)]),

@@ -94,7 +94,17 @@ struct hb_ctx {
   long long* lbuf = nullptr;              // [P][B][E][2] router scratch
   uint4* x_perm = nullptr;
   float* xsum = nullptr;
-  float* au = nullptr;                    // [slots][2][F] K2a sums
+  float* au = nullptr;                    // 2 x [slots][2][F] K2a sums (double-buffered)
+  int au_cur = 0;                         // buffer of the last GEMV forward
+  long long au_dirty[2] = {0, 0};         // floats of each buffer not yet zeroed again
+  bool fused_ok = false;                  // fused decode kernel usable (B = 1, top-2, fits)
+  unsigned* gbar = nullptr;               // fused kernel grid barrier [count, generation]
+  unsigned* fwd_idx = nullptr;            // profile record index, exit counter
+  unsigned long long* stamps = nullptr;   // [stamp_cap][8] per-forward %globaltimer records
+  int stamp_cap = 0;
+  bool stamps_on = false;
+  __half* x_save = nullptr;               // x of the last fused forward (lazy exact logits)
+  bool last_fused = false;
   uint4* h_hi = nullptr;                  // h in global memory (large batches only)
   uint4* h_lo = nullptr;
   float* hsum = nullptr;
@@ -274,7 +284,8 @@ static void free_ctx(hb_ctx* c) {
   cudaDeviceSynchronize();
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
                    c->logits, c->lbuf, c->x_perm, c->xsum, c->au, c->h_hi, c->h_lo,
-                   c->hsum, c->done, c->gctr, c->jt_dev, c->k3_xg, c->k3_hB, c->k3_tab, c->k3_tmap};
+                   c->hsum, c->done, c->gctr, c->jt_dev, c->k3_xg, c->k3_hB, c->k3_tab, c->k3_tmap,
+                   c->gbar, c->fwd_idx, c->stamps, c->x_save};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
@@ -347,7 +358,9 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
             dm((void**)&c->logits, sizeof(long long) * B * E * 2) &&
             dm((void**)&c->lbuf, sizeof(long long) * P * B * E * 2) &&
             dm((void**)&c->x_perm, (size_t)B * H * 2) && dm((void**)&c->xsum, (size_t)B * (H / 32) * 4) &&
-            dm((void**)&c->au, (size_t)c->max_slots * 2 * F * 4) &&
+            dm((void**)&c->au, 2 * (size_t)c->max_slots * 2 * F * 4) &&
+            dm((void**)&c->gbar, 16) && dm((void**)&c->fwd_idx, 16) &&
+            dm((void**)&c->x_save, (size_t)H * 2) &&
             dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->hsum, (size_t)c->max_slots * (F / 32) * 4) &&
@@ -386,6 +399,14 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     if (km) c->k3_min_batch = std::atoi(km);
   }
   cudaMemset(c->done, 0, 16);
+  cudaMemset(c->au, 0, 2 * (size_t)c->max_slots * 2 * F * 4);
+  cudaMemset(c->gbar, 0, 16);
+  cudaMemset(c->fwd_idx, 0, 16);
+  {
+    const char* nf = std::getenv("HB_NO_FUSED");
+    c->fused_ok = resident && K == 2 && !(nf && nf[0] == '1') &&
+                  fused_fits(E, H, F, k.hi_enc, k.lo_enc);
+  }
   cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + 2 * kGemvCTAs));
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
   // job table: hdr | jobs | slot_token | slot_gate | tok_slots
@@ -613,7 +634,11 @@ static RouterParams router_params(hb_ctx* c, const void* x, int batch) {
   return p;
 }
 
-static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
+static float* au_buf(hb_ctx* c, int i) {
+  return c->au + (size_t)i * c->max_slots * 2 * c->cfg.ffn;
+}
+
+static GemvParams gemv_params(hb_ctx* c, int batch, void* y, float* au) {
   const hb_config& k = c->cfg;
   GemvParams g{};
   g.jt = c->jt;
@@ -624,7 +649,7 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
   g.k = k.top_k;
   g.x_perm = c->x_perm;
   g.xsum = c->xsum;
-  g.au = c->au;
+  g.au = au;
   g.h_hi = c->h_hi;
   g.h_lo = c->h_lo;
   g.hsum = c->hsum;
@@ -650,6 +675,61 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y) {
   g.chunk = c->chunk;
   for (int e = 0; e < 4; ++e) g.k2b_w[e] = c->k2b_w[e];
   return g;
+}
+
+// The legacy GEMV chain's K2a-sum buffer: the one the previous GEMV forward
+// did not use; the router grid zeroes it and the other one (so both are
+// clean afterwards except this forward's).  Returns the buffer index.
+static int legacy_au(hb_ctx* c, RouterParams& rp, int batch) {
+  const int cn = c->au_cur ^ 1;
+  rp.zero_buf[0] = au_buf(c, cn);
+  rp.zero_n[0] = (long long)batch * c->cfg.top_k * 2 * c->cfg.ffn;
+  rp.zero_buf[2] = au_buf(c, cn ^ 1);
+  rp.zero_n[2] = c->au_dirty[cn ^ 1];
+  c->au_dirty[cn] = rp.zero_n[0];
+  c->au_dirty[cn ^ 1] = 0;
+  c->au_cur = cn;
+  return cn;
+}
+
+// Fused decode kernel (batch 1): router + K2a + K2b in one launch.  Uses the
+// sum buffer the previous GEMV forward did not use (clean) and zeroes the
+// other one for the next forward.
+static int launch_fused_forward(hb_ctx* c, int layer, const void* x, void* y, cudaStream_t s) {
+  const hb_config& k = c->cfg;
+  const int cn = c->au_cur ^ 1;
+  if (c->au_dirty[cn])                       // not expected: every GEMV forward leaves it clean
+    CUDA_TRY(c, cudaMemsetAsync(au_buf(c, cn), 0, (size_t)c->au_dirty[cn] * 4, s));
+  FusedParams fp{};
+  fp.g = gemv_params(c, 1, y, au_buf(c, cn));
+  fp.g.x_raw = (const __half*)x;
+  fp.wg = c->wg + (size_t)layer * k.n_experts * k.hidden;
+  fp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
+  fp.E = k.n_experts;
+  fp.theta1 = hb_theta(k.t1, &fp.th1_kind);
+  fp.theta2 = hb_theta(k.t2, &fp.th2_kind);
+  fp.rank = k.rank;
+  fp.world = k.world;
+  fp.hi_enc = k.hi_enc;
+  fp.lo_enc = k.lo_enc;
+  fp.dec = c->dec;
+  fp.x_save = c->x_save;
+  fp.zero_other = au_buf(c, cn ^ 1);
+  fp.zero_n = c->au_dirty[cn ^ 1];
+  fp.gbar = c->gbar;
+  fp.stamps = c->stamps_on ? c->stamps : nullptr;
+  fp.stamp_cap = c->stamp_cap;
+  fp.fwd_idx = c->fwd_idx;
+  cudaEvent_t* ev = nullptr;
+  if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
+  if (ev) cudaEventRecord(ev[0], s);
+  launch_fused(fp, s);
+  if (ev) { cudaEventRecord(ev[1], s); cudaEventRecord(ev[2], s); }
+  c->au_dirty[cn ^ 1] = 0;
+  c->au_dirty[cn] = (long long)2 * 2 * k.ffn;      // top-2: at most two slots
+  c->au_cur = cn;
+  c->launches += 1;
+  return HB_OK;
 }
 
 // K2a + K2b, bracketed by timing events when hb_profile is on
@@ -749,8 +829,6 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   rp.logits = c->logits;
   rp.x_perm = c->x_perm;
   rp.xsum = c->xsum;
-  rp.zero_buf[0] = c->au;
-  rp.zero_n[0] = (long long)batch * k.top_k * 2 * k.ffn;
   rp.zero_buf[1] = (float*)y;
   rp.zero_n[1] = (long long)batch * k.hidden;
 
@@ -760,16 +838,24 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   if (c->resident) {
     rp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
     const bool k3 = c->k3_ok && c->k3_min_batch > 0 && batch >= c->k3_min_batch;
+    c->last_host_decisions = false;
+    if (!k3 && batch == 1 && c->fused_ok) {
+      c->last_fused = true;
+      if (int rc = launch_fused_forward(c, layer, x, y, s)) return rc;
+      CUDA_TRY(c, cudaGetLastError());
+      return ep_reduce(c, y, batch, s);
+    }
+    c->last_fused = false;
     if (k3) rp.zero_n[0] = 0;                          // K3 does not use the K2a sums
+    const int cn = k3 ? 0 : legacy_au(c, rp, batch);
     launch_router(rp, s);
     c->launches += 1;
     if (k3) {
       launch_batched(c, layer, x, y, s);
     } else {
-      GemvParams gp = gemv_params(c, batch, y);
+      GemvParams gp = gemv_params(c, batch, y, au_buf(c, cn));
       launch_gemv(c, gp, s);
     }
-    c->last_host_decisions = false;
     CUDA_TRY(c, cudaGetLastError());
     return ep_reduce(c, y, batch, s);
   }
@@ -778,6 +864,8 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   if (batch != 1) return fail(c, HB_EUNSUPPORTED, "constrained cache supports batch 1 decode (v1)");
   if (!c->token_started) return fail(c, HB_ESTATE, "forward before hb_token_begin");
   rp.blob_table = nullptr;
+  c->last_fused = false;
+  const int cn = legacy_au(c, rp, batch);
   launch_router(rp, s);
   c->launches += 1;
   const int K = k.top_k;
@@ -839,7 +927,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   for (int i = 0; i < K; ++i)
     if (served[i] != HB_ENC_NONE)
       CUDA_TRY(c, cudaStreamWaitEvent(s, c->slot_ready[pool[i]][slot[i]], 0));
-  GemvParams gp = gemv_params(c, batch, y);
+  GemvParams gp = gemv_params(c, batch, y, au_buf(c, cn));
   launch_gemv(c, gp, s);
   for (int i = 0; i < K; ++i)
     if (served[i] != HB_ENC_NONE)
@@ -888,6 +976,8 @@ int prefetch_next_layer(hb_ctx* c, int layer, const void* x, int batch, void* st
   for (int j = 0; j < n; ++j) rp.wg[j] = router_of(c, layer + 1 + j);   // Stacking Computer
   rp.dec = c->dec_pred;
   rp.blob_table = nullptr;
+  c->last_fused = false;
+  const int cn = legacy_au(c, rp, batch);
   launch_router(rp, s);
   c->launches += 1;
   const int K = k.top_k;
@@ -937,6 +1027,18 @@ int hb_get_logits(hb_ctx* c, int64_t* out, int cap_pairs) {
   if (n <= 0) return 0;
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaDeviceSynchronize());
+  if (c->last_fused) {
+    // the fused kernel decides without materialising the exact logits: run
+    // the exact router on its saved copy of x (inspection only)
+    RouterParams rp = router_params(c, c->x_save, 1);
+    rp.wg[0] = router_of(c, c->last_layer);
+    rp.n_route = 1;
+    rp.dec = c->dec_pred;
+    rp.logits = c->logits;
+    launch_router(rp, nullptr);
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaDeviceSynchronize());
+  }
   CUDA_TRY(c, cudaMemcpy(out, c->logits, sizeof(long long) * 2 * n, cudaMemcpyDeviceToHost));
   return n;
 }
@@ -1045,6 +1147,46 @@ int hb_profile_read(hb_ctx* c, float* ms, int cap) {
     CUDA_TRY(c, cudaEventSynchronize(c->prof_ev[3 * i + 2]));
     CUDA_TRY(c, cudaEventElapsedTime(&ms[2 * i], c->prof_ev[3 * i], c->prof_ev[3 * i + 1]));
     CUDA_TRY(c, cudaEventElapsedTime(&ms[2 * i + 1], c->prof_ev[3 * i + 1], c->prof_ev[3 * i + 2]));
+  }
+  return n;
+}
+
+int hb_stamps(hb_ctx* c, int max_forwards) {
+  if (!c || max_forwards < 0) return fail(c, HB_EINVAL, "bad argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  if (max_forwards > c->stamp_cap) {
+    if (c->stamps) cudaFree(c->stamps);
+    c->stamps = nullptr;
+    c->stamp_cap = 0;
+    CUDA_TRY(c, cudaMalloc((void**)&c->stamps, sizeof(unsigned long long) * 8 * (size_t)max_forwards));
+    c->stamp_cap = max_forwards;
+  }
+  if (c->stamps)
+    CUDA_TRY(c, cudaMemset(c->stamps, 0, sizeof(unsigned long long) * 8 * (size_t)c->stamp_cap));
+  CUDA_TRY(c, cudaMemset(c->fwd_idx, 0, 16));
+  c->stamps_on = max_forwards > 0;
+  return HB_OK;
+}
+
+int hb_stamps_read(hb_ctx* c, uint64_t* out, int cap) {
+  if (!c || (cap > 0 && !out)) return fail(c, HB_EINVAL, "bad argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  unsigned idx[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpy(idx, c->fwd_idx, 8, cudaMemcpyDeviceToHost));
+  const int n = std::min<int>(std::min<int>((int)idx[0], c->stamp_cap), cap);
+  if (n <= 0) return 0;
+  std::vector<unsigned long long> raw((size_t)n * 8);
+  CUDA_TRY(c, cudaMemcpy(raw.data(), c->stamps, raw.size() * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i) {
+    const unsigned long long* r = &raw[(size_t)i * 8];
+    uint64_t* o = out + (size_t)i * 5;
+    o[0] = ~r[0];                 // first CTA past griddepcontrol.wait
+    o[1] = r[1];                  // last CTA with its decisions / job table
+    o[2] = r[2];                  // last CTA done with K2a (grid barrier arrival)
+    o[3] = ~r[3];                 // first CTA released by the grid barrier
+    o[4] = r[4];                  // last CTA done
   }
   return n;
 }

@@ -44,6 +44,7 @@
 #include <cuda_fp16.h>
 
 #include "hb_internal.h"
+#include "exact_dot.cuh"
 
 namespace hb {
 
@@ -65,6 +66,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ uint32_t smem_u32_(const void* p) { return smem_u32(p); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void cp_async16_ef(uint32_t dst, const void* src, uint64_t pol) {
 #ifdef HB_NO_EVICT_HINT
   (void)pol;
@@ -289,38 +293,76 @@ __device__ __forceinline__ float h_block(const float* au, int F, int s, int j, u
 }
 
 // ------------------------------------------------------------ CTA stage
-// Shared-memory layout of the B operand (nrows = tokens for K2a, slots for K2b):
-//   part 0 (x / h hi) [nrows][K/8] uint4 | part 1 (h lo, K2b) | sums [nrows][K/32] f32
+// Shared-memory layout of the B operand (nrows = tokens for K2a, slots for K2b;
+// kcols = staged columns per row):
+//   part 0 (x / h hi) [nrows][kcols/8] uint4 | part 1 (h lo, K2b) | sums [nrows][kcols/32] f32
 // Warp `w` of the CTA builds its share (items w, w + kGemvWarps, ...).
-template <bool W13>
-__device__ void stage_share(const GemvParams& p, int w, uint8_t* st, int row0, int nrows) {
+// K2a, legacy chain: copy the router's pair-permuted x and block sums.
+__device__ void stage_share_xperm(const GemvParams& p, int w, uint8_t* st, int row0, int nrows) {
   const int lane = threadIdx.x & 31;
-  if constexpr (W13) {
-    const int K = p.H;
-    const int n16 = nrows * (K / 8);
-    uint4* dst = reinterpret_cast<uint4*>(st);
-    const uint4* xs = p.x_perm + (size_t)row0 * (K / 8);
-    for (int i = w * 32 + lane; i < n16; i += kGemvWarps * 32) dst[i] = __ldcg(xs + i);
-    const int nz = nrows * (K / 32);
-    float* zd = reinterpret_cast<float*>(st + (size_t)n16 * 16);
-    const float* zs = p.xsum + (size_t)row0 * (K / 32);
-    for (int i = w * 32 + lane; i < nz; i += kGemvWarps * 32) zd[i] = __ldcg(zs + i);
-  } else {
-    const int K = p.F, nb = K / 32;
-    uint4* dhi = reinterpret_cast<uint4*>(st);
-    uint4* dlo = dhi + (size_t)nrows * (K / 8);
-    float* zd = reinterpret_cast<float*>(dlo + (size_t)nrows * (K / 8));
-    for (int i = w * 32 + lane; i < nrows * nb; i += kGemvWarps * 32) {
-      const int s = i / nb, j = i - s * nb;
-      uint4 hi[4], lo[4];
-      const float hs = h_block(p.au, K, row0 + s, j, hi, lo);
+  const int K = p.H;
+  const int n16 = nrows * (K / 8);
+  uint4* dst = reinterpret_cast<uint4*>(st);
+  const uint4* xs = p.x_perm + (size_t)row0 * (K / 8);
+  for (int i = w * 32 + lane; i < n16; i += kGemvWarps * 32) dst[i] = __ldcg(xs + i);
+  const int nz = nrows * (K / 32);
+  float* zd = reinterpret_cast<float*>(st + (size_t)n16 * 16);
+  const float* zs = p.xsum + (size_t)row0 * (K / 32);
+  for (int i = w * 32 + lane; i < nz; i += kGemvWarps * 32) zd[i] = __ldcg(zs + i);
+}
+// K2a, fused decode: pair-permute x (Q_c = (x[8t+c], x[8t+c+4])) and sum each
+// 32-element block (the Q2 m-term) straight from the caller's fp16 x.
+__device__ void stage_share_xraw(const GemvParams& p, int w, uint8_t* st, int row0, int nrows) {
+  const int lane = threadIdx.x & 31;
+  const int K = p.H, nb = K / 32;
+  uint4* dst = reinterpret_cast<uint4*>(st);
+  float* zd = reinterpret_cast<float*>(st + (size_t)nrows * K * 2);
+  for (int i = w * 32 + lane; i < nrows * nb; i += kGemvWarps * 32) {
+    const int r = i / nb, blk = i - r * nb;
+    const uint4* src = reinterpret_cast<const uint4*>(p.x_raw + (size_t)(row0 + r) * K + blk * 32);
+    uint32_t v[16];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        dhi[(size_t)s * (K / 8) + j * 4 + t] = hi[t];
-        dlo[(size_t)s * (K / 8) + j * 4 + t] = lo[t];
-      }
-      zd[i] = hs;
+    for (int q = 0; q < 4; ++q) {
+      const uint4 t = __ldcg(src + q);
+      v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
     }
+    float sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      sum += __half2float(__ushort_as_half((unsigned short)(v[e >> 1] >> (16 * (e & 1)))));
+    zd[i] = sum;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      uint32_t q[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e0 = 8 * t + c, e1 = e0 + 4;
+        q[c] = ((v[e0 >> 1] >> (16 * (e0 & 1))) & 0xFFFF) | (((v[e1 >> 1] >> (16 * (e1 & 1))) & 0xFFFF) << 16);
+      }
+      dst[(size_t)r * (K / 8) + blk * 4 + t] = make_uint4(q[0], q[1], q[2], q[3]);
+    }
+  }
+}
+// K2b, fused decode: this CTA's column slice [c0, c0 + kcols) of h for slots
+// [row0, row0 + nrows), h = silu(a) * u from the K2a sums (fp16 hi/lo pair +
+// block sums), computed redundantly by every CTA of the slice's group.
+__device__ void stage_share_h(const GemvParams& p, int w, uint8_t* st, int row0, int nrows,
+                              int c0, int kcols) {
+  const int lane = threadIdx.x & 31;
+  const int nb = kcols / 32, K = p.F;
+  uint4* dhi = reinterpret_cast<uint4*>(st);
+  uint4* dlo = dhi + (size_t)nrows * (kcols / 8);
+  float* zd = reinterpret_cast<float*>(dlo + (size_t)nrows * (kcols / 8));
+  for (int i = w * 32 + lane; i < nrows * nb; i += kGemvWarps * 32) {
+    const int s = i / nb, j = i - s * nb;
+    uint4 hi[4], lo[4];
+    const float hs = h_block(p.au, K, row0 + s, c0 / 32 + j, hi, lo);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      dhi[(size_t)s * (kcols / 8) + j * 4 + t] = hi[t];
+      dlo[(size_t)s * (kcols / 8) + j * 4 + t] = lo[t];
+    }
+    zd[i] = hs;
   }
 }
 
@@ -352,6 +394,61 @@ struct Stage {
   bool on;           // B operand read from the stage (else from global memory)
 };
 
+// Fused decode: every warp reports the end of its K2a work; the CTA's last warp
+// takes part in the grid-wide barrier (all K2a sums complete), then releases
+// the CTA's warps.
+struct FusedSync {
+  unsigned* gcount;          // global arrivals (self-resetting)
+  unsigned* ggen;            // global generation
+  int* warps_done;           // shared: warps of this CTA past K2a
+  int* released;             // shared: 1 once the grid barrier passed
+  unsigned long long* stamp; // per-forward profile record or null
+};
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* a, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int* a) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32_(a)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* a, int v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" :: "r"(smem_u32_(a)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ void fused_grid_barrier(const FusedSync& fs) {
+  __threadfence();                     // this lane's K2a reductions before the arrival
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    if (atomicAdd(fs.warps_done, 1) == kGemvWarps - 1) {
+      // last warp of the CTA: every warp's reductions are fenced
+      __threadfence();
+      if (fs.stamp) atomicMax(fs.stamp + 2, gtimer_ns());
+      const unsigned g = ld_acquire_gpu(fs.ggen);
+      if (atomicAdd(fs.gcount, 1u) == gridDim.x - 1) {
+        *fs.gcount = 0u;
+        st_release_gpu(fs.ggen, g + 1u);
+      } else {
+        while (ld_acquire_gpu(fs.ggen) == g) __nanosleep(64);
+      }
+      if (fs.stamp) atomicMax(fs.stamp + 3, ~gtimer_ns());   // min, stored complemented
+      st_release_cta(fs.released, 1);
+    } else {
+      while (!ld_acquire_cta(fs.released)) __nanosleep(32);
+    }
+  }
+  __syncwarp();
+}
+
 // K2b: h rows [row0, row0 + nrows) of h_hi | h_lo | hsum (built by hfin) into
 // the stage with three bulk (TMA) copies issued by thread 0; every thread
 // waits on the mbarrier's transaction count.
@@ -378,11 +475,59 @@ __device__ __forceinline__ void stage_h_bulk_and_wait(const GemvParams& p, const
   mbar_wait(S.bar, 0);
 }
 
-template <bool W13>
-__device__ __forceinline__ void stage_build_and_wait(const GemvParams& p, const Stage& S) {
-  stage_share<W13>(p, threadIdx.x >> 5, S.ptr, S.row0, S.nrows);
+// The fused decode kernel's own job table (built by every CTA, in shared
+// memory; file-scope __shared__, so only that kernel allocates it) and the
+// grid barrier it meets between K2a and K2b.
+constexpr int kFusedMaxV = 4;
+__shared__ VJobD fz_vj[kFusedMaxV];
+__shared__ int32_t fz_stok[kFusedMaxV];
+__shared__ float fz_sgate[kFusedMaxV];
+__shared__ int fz_nv, fz_nslot;
+__shared__ FusedSync fz_fs;
+
+// Job table access: the router's global table (legacy chain, FUSED = false)
+// or the fused kernel's shared copy.  Templated so that the legacy kernels
+// keep these in the constant bank instead of registers.
+template <bool FUSED> struct JT;
+template <> struct JT<false> {
+  static __device__ __forceinline__ int nv(const GemvParams& p) { return __ldcg(p.jt.hdr + 2); }
+  static __device__ __forceinline__ int nslots(const GemvParams& p) { return __ldcg(p.jt.hdr + 1); }
+  static __device__ __forceinline__ VJobD vjob(const GemvParams& p, int v) { return p.jt.vjobs[v]; }
+  static __device__ __forceinline__ int stok(const GemvParams& p, int s) { return p.jt.slot_token[s]; }
+  static __device__ __forceinline__ float sgate(const GemvParams& p, int s) { return p.jt.slot_gate[s]; }
+};
+template <> struct JT<true> {
+  static __device__ __forceinline__ int nv(const GemvParams&) { return fz_nv; }
+  static __device__ __forceinline__ int nslots(const GemvParams&) { return fz_nslot; }
+  static __device__ __forceinline__ VJobD vjob(const GemvParams&, int v) { return fz_vj[v]; }
+  static __device__ __forceinline__ int stok(const GemvParams&, int s) { return fz_stok[s]; }
+  static __device__ __forceinline__ float sgate(const GemvParams&, int s) { return fz_sgate[s]; }
+};
+
+// K2a's x stage: every thread builds its share, arrives, waits
+template <bool FUSED>
+__device__ __forceinline__ void stage_x_and_wait(const GemvParams& p, const Stage& S) {
+  if (FUSED) stage_share_xraw(p, threadIdx.x >> 5, S.ptr, S.row0, S.nrows);
+  else stage_share_xperm(p, threadIdx.x >> 5, S.ptr, S.row0, S.nrows);
   mbar_arrive(S.bar);
   mbar_wait(S.bar, 0);
+}
+// K2b's h stage once the K2a sums are complete: legacy chain = wait for the
+// previous kernels (K2a, hfin) and bulk-copy h; fused kernel = grid barrier,
+// then build h from the sums
+template <bool FUSED>
+__device__ __forceinline__ void stage_h_and_wait(const GemvParams& p, const Stage& S) {
+  if (!FUSED) {
+    pdl_wait();
+    if (S.on) stage_h_bulk_and_wait(p, S);
+    return;
+  }
+  fused_grid_barrier(fz_fs);
+  if (S.on) {
+    stage_share_h(p, threadIdx.x >> 5, S.ptr, S.row0, S.nrows, S.hs * S.kcols, S.kcols);
+    mbar_arrive(S.bar);
+    mbar_wait(S.bar, 0);
+  }
 }
 
 // ---------------------------------------------------------- work feed
@@ -394,8 +539,6 @@ struct VJob {
   int nslot;
 };
 
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 // The units of a launch (ordered vjob, tile, group; vjob v owns
 // [cum[v], cum[v+1])) are dealt in two phases: the first S = static_frac * U
@@ -452,7 +595,7 @@ struct Feed {
 #else
 #define HB_RUN_ATTR
 #endif
-template <int ENC, bool W13, bool XR>
+template <int ENC, bool W13, bool XR, bool FUSED>
 __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, int Uv, Feed& fd,
                     uint32_t ring, uint2* meta, const Stage& S, bool first) {
   constexpr int NMAT = W13 ? 2 : 1;
@@ -540,13 +683,10 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
   // queued (behind ~24 MB of ring prologues it would wait microseconds).
   // K2b: the ring prologue (W2 is independent of K2a) goes out first, during
   // K2a's tail; then wait for K2a and build h.
-  if (W13 && first && S.on) stage_build_and_wait<W13>(p, S);
+  if (W13 && first && S.on) stage_x_and_wait<FUSED>(p, S);
 #pragma unroll 1
   for (int s = 0; s < DEPTH - 1; ++s) issue();
-  if (!W13 && first) {
-    pdl_wait();                                // h comes from hfin (after K2a)
-    if (S.on) stage_h_bulk_and_wait(p, S);
-  }
+  if (!W13 && first) stage_h_and_wait<FUSED>(p, S);  // h after K2a (hfin or the grid barrier)
   if (first) HB_TL(W13, (threadIdx.x >> 5) * gridDim.x + blockIdx.x, 2);
 
   // ---- lane constants: B-operand rows, outputs of the lane's two slots
@@ -554,7 +694,7 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
   const int z0 = min(2 * t, ns - 1), z1 = min(2 * t + 1, ns - 1);
   auto row_of = [&](int s) -> int {          // token (x) or slot (h) of vjob slot s
     const int sl = vj.slot0 + s;
-    return W13 ? p.jt.slot_token[sl] : sl;
+    return W13 ? JT<FUSED>::stok(p, sl) : sl;
   };
   const uint4* gx0 = nullptr;
   const uint4* gx1 = nullptr;
@@ -587,10 +727,10 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
     out0 = p.au + (size_t)(vj.slot0 + z0) * 2 * p.F;
     out1 = p.au + (size_t)(vj.slot0 + z1) * 2 * p.F;
   } else {
-    out0 = p.y + (size_t)p.jt.slot_token[vj.slot0 + z0] * p.H;
-    out1 = p.y + (size_t)p.jt.slot_token[vj.slot0 + z1] * p.H;
-    gate0 = p.jt.slot_gate[vj.slot0 + z0];
-    gate1 = p.jt.slot_gate[vj.slot0 + z1];
+    out0 = p.y + (size_t)JT<FUSED>::stok(p, vj.slot0 + z0) * p.H;
+    out1 = p.y + (size_t)JT<FUSED>::stok(p, vj.slot0 + z1) * p.H;
+    gate0 = JT<FUSED>::sgate(p, vj.slot0 + z0);
+    gate1 = JT<FUSED>::sgate(p, vj.slot0 + z1);
   }
 
   float acc[NMAT][4];
@@ -734,71 +874,68 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
 
 extern __shared__ __align__(128) uint8_t gemv_smem[];
 
-template <bool W13>
-__global__ void __launch_bounds__(kGemvWarps * 32, 1)
-gemv_kernel(const __grid_constant__ GemvParams p) {
-  __shared__ __align__(8) uint64_t s_bar;
-  __shared__ int s_cum[kMaxVJobs + 1];
-  __shared__ uint2 s_meta[kGemvWarps][16];
-  __shared__ FeedConst s_fk;
-  __shared__ int s_subb[kGemvCTAs + 1];         // K2b sub-space first units (+ total)
-  __shared__ float s_subc[kGemvCTAs + 1];       // K2b sub-space cumulative cost (+ total)
-  __shared__ int s_subvh[kGemvCTAs];            // vjob | slice << 16 | slices << 24
-  __shared__ int s_nsub;
-  const int warp = threadIdx.x >> 5;
-  const int gw = warp * gridDim.x + blockIdx.x;
-  HB_TL(W13, gw, 0);
-  // K2a needs the router's job table and x; K2b may read the table before
-  // waiting (K2a triggers its dependents only after its own wait, i.e. after
-  // the router completed) and waits for K2a's sums inside its first run
-  if constexpr (W13) pdl_wait();
-  pdl_trigger();
-  const long long* cum = W13 ? p.jt.vcum13 : p.jt.vcum2;
-  for (int i = threadIdx.x; i <= p.max_vjobs; i += blockDim.x) s_cum[i] = (int)__ldcg(cum + i);
-  const int nv = __ldcg(p.jt.hdr + 2);
-  const int nslots = __ldcg(p.jt.hdr + 1);
+// The fused kernel calls each run<> through a non-inlined wrapper: the
+// wrapper gets its own register allocation, so the kernel's other live state
+// (router results, the K2b setup) is saved around the call instead of
+// competing with the streaming loop's registers.
+template <int ENC, bool W13, bool XR>
+__device__ __noinline__ void run_fused(const GemvParams& p, const VJob& vj, int cum, int Uv,
+                                       Feed& fd, uint32_t ring, uint2* meta, const Stage& S,
+                                       bool first) {
+  run<ENC, W13, XR, true>(p, vj, cum, Uv, fd, ring, meta, S, first);
+}
+
+// What phase_setup decides for this CTA (every thread holds a copy).
+struct PhaseCtx {
+  bool part;               // K2b: CTA groups per sub-space (staged h slices)
+  int base, Usp, vsp;      // sub-space of this CTA: first unit, units, index (-1: all)
+  int ncta, cta;           // CTAs sharing the space, this CTA's index among them
+  int KNU;                 // units per ring stage
+};
+
+// ---- the space this CTA works in.  K2a: all units (every SM gets the same
+// mix of fp16 = HBM-heavy and low-bit = ALU-heavy units; measured: splitting
+// K2a's CTAs per job leaves the low-bit group compute-bound and late).  K2b
+// with h in shared memory: the CTAs are split into groups, one per sub-space
+// (a vjob's column slice of h), sizes proportional to its cost (>= 1 CTA
+// each), so a CTA stages only its slice of h and keeps a deep ring; its
+// warps' feed covers that slice alone.  Contains __syncthreads.
+template <bool W13, bool FUSED>
+__device__ void phase_setup(const GemvParams& p, const int* s_cum, FeedConst* s_fk, int* s_subb,
+                            float* s_subc, int* s_subvh, int* s_nsub, uint32_t bar,
+                            bool h_global, Stage& S, PhaseCtx& pc) {
+  const int nv = JT<FUSED>::nv(p);
+  const int U = s_cum[nv];
   constexpr int XS = W13 ? 1 : 2;
   const int K = W13 ? p.H : p.F;
-  // stage hand-off: K2a every thread arrives after its share of the x copy;
-  // K2b thread 0 arrives once with the bulk copies' transaction count
-  if (threadIdx.x == 0) mbar_init(smem_u32(&s_bar), W13 ? blockDim.x : 1);
-  __syncthreads();
-  if (nv == 0) return;                       // nothing owned: y stays zero (router)
-  const int U = s_cum[nv];
-  // ---- the space this CTA works in.  K2a: all units (every SM gets the same
-  // mix of fp16 = HBM-heavy and low-bit = ALU-heavy units; measured: splitting
-  // K2a's CTAs per job leaves the low-bit group compute-bound and late).  K2b
-  // with h in shared memory: the CTAs are split into groups, one per
-  // sub-space (a vjob's column slice of h), sizes proportional to its units
-  // (>= 1 CTA each), so a CTA stages only its slice of h and keeps a deep
-  // ring; its warps' feed covers that slice alone.
-  const bool part = !W13 && !p.h_global;
-  Stage S;
+  pc.part = !W13 && !h_global;
   S.ptr = gemv_smem + kGemvWarps * KCfg<W13>::RING;
   S.xst = smem_u32(S.ptr);
-  S.bar = smem_u32(&s_bar);
-  int base = 0, Usp = U, ncta = gridDim.x, cta = blockIdx.x, vsp = -1;
+  S.bar = bar;
+  pc.base = 0;
+  pc.Usp = U;
+  pc.ncta = gridDim.x;
+  pc.cta = blockIdx.x;
+  pc.vsp = -1;
   S.nh = 1;
   S.hs = 0;
   S.row0 = 0;
-  S.nrows = W13 ? p.B : nslots;
+  S.nrows = W13 ? p.B : JT<FUSED>::nslots(p);
   S.kcols = K;
   S.on = W13 && (size_t)S.nrows * (XS * K * 2 + (K / 32) * 4) <= (size_t)KCfg<W13>::XSTAGE;
-  if (part) {
-    // sub-spaces (vjob v, column slice h < nh(v)); K2b: nh = 2 when the slice
-    // has an even number of groups.  CTAs [c0(q), c0(q+1)) work on
-    // sub-space q, c0(q) = q + floor(first unit of q * (n - nsub) / U)
+  if (pc.part) {
+    // sub-spaces (vjob v, column slice h < nh(v)); nh = 2 when the slice has
+    // an even number of groups.  CTAs [c0(q), c0(q+1)) work on sub-space q,
+    // c0(q) = q + floor(cost before q * (n - nsub) / total cost)
     if (threadIdx.x == 0) {
-      // CTAs per sub-space proportional to its cost: units x the per-encoding
-      // weight (quantised units are ALU-heavier than F16 ones; HB_K2B_W)
       int q = 0;
       float cc = 0.f;
       for (int v = 0; v < nv; ++v) {
-        const int enc = __ldcg(&p.jt.vjobs[v].enc);
+        const int enc = JT<FUSED>::vjob(p, v).enc;
         const int G = K / epg_of(enc);
-        const int nh = (!W13 && G % 4 == 0) ? 2 : 1;
+        const int nh = G % 4 == 0 ? 2 : 1;
         const int uq = (s_cum[v + 1] - s_cum[v]) / nh;
-        const float w = p.k2b_w[enc & 3];
+        const float w = p.k2b_w[enc & 3];   // quantised units are ALU-heavier (HB_K2B_W)
         for (int h = 0; h < nh; ++h, ++q) {
           s_subvh[q] = v | (h << 16) | (nh << 24);
           s_subb[q] = s_cum[v] + h * uq;
@@ -808,10 +945,10 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
       }
       s_subb[q] = U;
       s_subc[q] = cc;
-      s_nsub = q;
+      *s_nsub = q;
     }
     __syncthreads();
-    const int nsub = s_nsub;
+    const int nsub = *s_nsub;
     const int spare = (int)gridDim.x - nsub;
     const float ctot = s_subc[nsub];
     auto c0 = [&](int q) { return q + (int)((double)s_subc[q] * spare / ctot); };
@@ -820,55 +957,60 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
       const int mid = (lo + hi + 1) >> 1;
       if (c0(mid) <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
     }
-    vsp = lo;
-    base = s_subb[lo];
-    Usp = s_subb[lo + 1] - base;
-    cta = blockIdx.x - c0(lo);
-    ncta = (lo + 1 < nsub ? c0(lo + 1) : (int)gridDim.x) - c0(lo);
-    if constexpr (!W13) {
-      const VJobD d = p.jt.vjobs[s_subvh[lo] & 0xFFFF];
-      S.row0 = d.slot0;
-      S.nrows = d.nslot;
-      S.nh = s_subvh[lo] >> 24;
-      S.hs = (s_subvh[lo] >> 16) & 0xFF;
-      S.kcols = K / S.nh;
-      // staged (2 units per ring stage) when the slice has an even number of
-      // groups; otherwise this group reads h from global memory
-      S.on = (K / epg_of(d.enc) / S.nh) % 2 == 0;
-    }
+    pc.vsp = lo;
+    pc.base = s_subb[lo];
+    pc.Usp = s_subb[lo + 1] - pc.base;
+    pc.cta = blockIdx.x - c0(lo);
+    pc.ncta = (lo + 1 < nsub ? c0(lo + 1) : (int)gridDim.x) - c0(lo);
+    const VJobD d = JT<FUSED>::vjob(p, s_subvh[lo] & 0xFFFF);
+    S.row0 = d.slot0;
+    S.nrows = d.nslot;
+    S.nh = s_subvh[lo] >> 24;
+    S.hs = (s_subvh[lo] >> 16) & 0xFF;
+    S.kcols = K / S.nh;
+    // staged (2 units per ring stage) when the slice has an even number of
+    // groups; otherwise this group reads h from global memory
+    S.on = (K / epg_of(d.enc) / S.nh) % 2 == 0;
   }
-  const int KNU = (!W13 && S.on) ? 2 : 1;    // units per ring stage (segments KNU-aligned)
+  pc.KNU = (!W13 && S.on) ? 2 : 1;
   if (threadIdx.x == 0) {
-    s_fk.base = base;
-    s_fk.U = Usp;
-    s_fk.S = min(Usp, (int)((double)Usp * (W13 ? p.static_frac : p.static_frac2))) & ~(KNU - 1);
-    s_fk.chunk = p.chunk;
-    s_fk.nch = (Usp - s_fk.S + p.chunk - 1) / p.chunk;
-    s_fk.nwarps = ncta * kGemvWarps;
+    s_fk->base = pc.base;
+    s_fk->U = pc.Usp;
+    s_fk->S = min(pc.Usp, (int)((double)pc.Usp * (W13 ? p.static_frac : p.static_frac2))) & ~(pc.KNU - 1);
+    s_fk->chunk = p.chunk;
+    s_fk->nch = (pc.Usp - s_fk->S + p.chunk - 1) / p.chunk;
+    s_fk->nwarps = pc.ncta * kGemvWarps;
     // counters: [0] K2a all units, [1] K2b all units, [2 + q] K2a group q,
     // [2 + kGemvCTAs + q] K2b group q (K2b fetches while K2a still runs)
-    s_fk.ctr = p.ctr + (vsp < 0 ? (W13 ? 0 : 1) : 2 + (W13 ? 0 : kGemvCTAs) + vsp);
+    s_fk->ctr = p.ctr + (pc.vsp < 0 ? (W13 ? 0 : 1) : 2 + (W13 ? 0 : kGemvCTAs) + pc.vsp);
   }
   __syncthreads();
+}
+
+// Every warp streams its static range, then dynamic chunks, through its ring
+// (no CTA-wide synchronisation: warps leave at different times).
+template <bool W13, bool FUSED>
+__device__ void phase_run(const GemvParams& p, const int* s_cum, const FeedConst* s_fk,
+                          const int* s_subvh, const PhaseCtx& pc, const Stage& S, uint2* meta) {
+  const int warp = threadIdx.x >> 5;
   Feed fd;
-  fd.k = &s_fk;
+  fd.k = s_fk;
   fd.done = false;
   // static ranges are dealt SM-interleaved (warp * #CTAs + CTA): consecutive
   // ranges (same job, same encoding) land on different SMs
-  const int gwl = warp * ncta + cta;
-  fd.a = base + ((int)((long long)s_fk.S * gwl / s_fk.nwarps) & ~(KNU - 1));
-  fd.b = base + ((int)((long long)s_fk.S * (gwl + 1) / s_fk.nwarps) & ~(KNU - 1));
+  const int gwl = warp * pc.ncta + pc.cta;
+  fd.a = pc.base + ((int)((long long)s_fk->S * gwl / s_fk->nwarps) & ~(pc.KNU - 1));
+  fd.b = pc.base + ((int)((long long)s_fk->S * (gwl + 1) / s_fk->nwarps) & ~(pc.KNU - 1));
   fd.start();
   const uint32_t ring = smem_u32(gemv_smem) + warp * KCfg<W13>::RING;
-  uint2* meta = s_meta[warp];
   bool first = true;
-  HB_TL(W13, gw, 1);
+  const int nv = JT<FUSED>::nv(p);
   while (fd.a < fd.b || fd.refill()) {
     int lo = 0, cv, Uv;
-    if (part) {                                // the CTA's sub-space (one vjob slice)
-      lo = s_subvh[vsp] & 0xFFFF;
-      cv = base;
-      Uv = Usp;
+    if (pc.part) {                             // the CTA's sub-space (one vjob slice)
+      lo = s_subvh[pc.vsp] & 0xFFFF;
+      cv = pc.base;
+      Uv = pc.Usp;
     } else {
       int hi = nv - 1;                         // vjob containing unit fd.a
       while (lo < hi) {
@@ -878,9 +1020,13 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
       cv = s_cum[lo];
       Uv = s_cum[lo + 1] - cv;
     }
-    const VJobD d = p.jt.vjobs[lo];
+    const VJobD d = JT<FUSED>::vjob(p, lo);
     const VJob vj{d.blob, d.enc, d.slot0, d.nslot};
-#define HB_RUN(E, X) run<E, W13, X>(p, vj, cv, Uv, fd, ring, meta, S, first)
+#define HB_RUN(E, X)                                                   \
+  do {                                                                 \
+    if constexpr (FUSED) run_fused<E, W13, X>(p, vj, cv, Uv, fd, ring, meta, S, first); \
+    else run<E, W13, X, false>(p, vj, cv, Uv, fd, ring, meta, S, first); \
+  } while (0)
     switch (vj.enc * 2 + (S.on ? 1 : 0)) {
       case 2 * HB_F16 + 1: HB_RUN(HB_F16, true); break;
       case 2 * HB_F16 + 0: HB_RUN(HB_F16, false); break;
@@ -894,15 +1040,405 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
 #undef HB_RUN
     first = false;
   }
-  if (first && S.on) {                       // no units at all: still take part in the stage
+  if (first) {                               // no units at all: still take part in the stage
     if constexpr (W13) {
-      stage_build_and_wait<W13>(p, S);
+      if (S.on) stage_x_and_wait<FUSED>(p, S);
     } else {
-      pdl_wait();
-      stage_h_bulk_and_wait(p, S);
+      stage_h_and_wait<FUSED>(p, S);
     }
   }
-  HB_TL(W13, gw, 3);
+}
+
+// Legacy chain (router kernel -> K2a -> hfin -> K2b): batches, the offload
+// path and configurations the fused kernel does not cover.
+template <bool W13>
+__global__ void __launch_bounds__(kGemvWarps * 32, 1)
+gemv_kernel(const __grid_constant__ GemvParams p) {
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ int s_cum[kMaxVJobs + 1];
+  __shared__ uint2 s_meta[kGemvWarps][16];
+  __shared__ FeedConst s_fk;
+  __shared__ int s_subb[kGemvCTAs + 1];         // K2b sub-space first units (+ total)
+  __shared__ float s_subc[kGemvCTAs + 1];       // K2b sub-space cumulative cost (+ total)
+  __shared__ int s_subvh[kGemvCTAs];            // vjob | slice << 16 | slices << 24
+  __shared__ int s_nsub;
+  const int warp = threadIdx.x >> 5;
+  HB_TL(W13, warp * gridDim.x + blockIdx.x, 0);
+  // K2a needs the router's job table and x; K2b may read the table before
+  // waiting (K2a triggers its dependents only after its own wait, i.e. after
+  // the router completed) and waits for K2a's sums inside its first run
+  if constexpr (W13) pdl_wait();
+  pdl_trigger();
+  const long long* cum = W13 ? p.jt.vcum13 : p.jt.vcum2;
+  for (int i = threadIdx.x; i <= p.max_vjobs; i += blockDim.x) s_cum[i] = (int)__ldcg(cum + i);
+  // stage hand-off: K2a every thread arrives after its share of the x copy;
+  // K2b thread 0 arrives once with the bulk copies' transaction count
+  if (threadIdx.x == 0) mbar_init(smem_u32(&s_bar), W13 ? blockDim.x : 1);
+  __syncthreads();
+  if (JT<false>::nv(p) == 0) return;        // nothing owned: y stays zero (router)
+  Stage S;
+  PhaseCtx pc;
+  phase_setup<W13, false>(p, s_cum, &s_fk, s_subb, s_subc, s_subvh, &s_nsub, smem_u32(&s_bar),
+                          p.h_global, S, pc);
+  phase_run<W13, false>(p, s_cum, &s_fk, s_subvh, pc, S, s_meta[warp]);
+  HB_TL(W13, warp * gridDim.x + blockIdx.x, 3);
+}
+
+// ------------------------------------------------------------ fused decode
+// One kernel per layer for batch-1 decode in resident mode (DESIGN.md "fused
+// decode kernel"): every CTA
+//   1. (before griddepcontrol.wait) bulk-copies the layer's router rows into
+//      its shared memory;
+//   2. routes the token itself: fp32 products (exact for fp16 x fp16) summed
+//      in runs of 8 with FFMA, runs summed in fp64, together with a rigorous
+//      bound on the rounding error; the top-2 order and the T1/T2 tests are
+//      decided from these when every comparison clears the bound, else from
+//      the exact integer logits (the same exact arithmetic as the router
+//      kernel) -- so the decisions are the exact ones either way, and every
+//      CTA derives the same decisions from the same operations (no hand-off);
+//   3. builds the job table in shared memory;
+//   4. runs K2a (W1/W3 + sums into au), then, per warp as soon as its K2a
+//      work is done, issues the first W2 ring stages, meets the other CTAs
+//      at a grid barrier (K2a sums complete), builds its slice of h from the
+//      sums and runs K2b.
+// Replaces router kernel + K2a + hfin + K2b and their three hand-offs.
+constexpr int kFusedScratch = 160 * 1024;   // router scratch offset in dynamic smem (W_g below)
+// |sum of 8 products in fp32 FFMA - exact| <= gamma_7 sum|p| (gamma_7 =
+// 7u/(1-7u), u = 2^-24); the fp64 sums over runs add < 1e-13 relative; the
+// bound sum itself is an fp32/fp64 sum of |p| (relative error <= gamma_7).
+// 4.6e-7 * A >= (gamma_7 + 1e-13) (1 + gamma_7) (1 + 1e-13) * A.
+constexpr double kEpsRel = 4.6e-7;
+
+__device__ __forceinline__ void h2f8(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__global__ void __launch_bounds__(kGemvWarps * 32, 1)
+fused_decode_kernel(const __grid_constant__ FusedParams fp) {
+  const GemvParams& p = fp.g;
+  __shared__ __align__(8) uint64_t s_wbar, s_bar13, s_bar2;
+  __shared__ int s_cum13[kFusedMaxV + 1], s_cum2[kFusedMaxV + 1];
+  __shared__ uint2 s_meta[kGemvWarps][16];
+  __shared__ FeedConst s_fk13, s_fk2;
+  __shared__ int s_subb[kGemvCTAs + 1];
+  __shared__ float s_subc[kGemvCTAs + 1];
+  __shared__ int s_subvh[kGemvCTAs];
+  __shared__ int s_nsub, s_nsub13;
+  __shared__ int s_ok, s_warps_done, s_released;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int E = fp.E, H = p.H, n8 = H / 8;
+  uint8_t* dyn = gemv_smem;
+  double* red = reinterpret_cast<double*>(dyn + kFusedScratch);          // [12][8][2]
+  const uint8_t** s_blob = reinterpret_cast<const uint8_t**>(dyn + kFusedScratch + 2048);  // [E][4]
+  u64* xpart = reinterpret_cast<u64*>(dyn + kFusedScratch + 4096);       // [12][64][3] (exact fallback)
+  i128* s_Lx = reinterpret_cast<i128*>(dyn + kFusedScratch + 4096 + 12 * 64 * 24);   // [64]
+  double* s_L = reinterpret_cast<double*>(dyn + kFusedScratch + 4096 + 12 * 64 * 24 + 1024);  // [64]
+  double* s_A = s_L + 64;                                                               // [64]
+
+  // ---- 1. before waiting on the previous kernel: router rows (static) into
+  // shared memory with bulk copies, blob table of the layer
+  const uint32_t wbar = smem_u32(&s_wbar);
+  if (tid == 0) {
+    mbar_init(wbar, 1);
+    mbar_init(smem_u32(&s_bar13), blockDim.x);
+    mbar_init(smem_u32(&s_bar2), blockDim.x);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t total = (uint32_t)E * H * 2;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(wbar), "r"(total) : "memory");
+    for (uint32_t off = 0; off < total; off += 16384) {
+      const uint32_t len = total - off < 16384 ? total - off : 16384;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          :: "r"(smem_u32(dyn) + off), "l"(reinterpret_cast<const char*>(fp.wg) + off), "r"(len),
+             "r"(wbar) : "memory");
+    }
+  }
+  for (int i = tid; i < 4 * E; i += blockDim.x) s_blob[i] = fp.blob_table[i];
+  if (tid == 0) { s_warps_done = 0; s_released = 0; }
+  __syncthreads();
+  pdl_wait();                                  // x (and y, the sums) belong to earlier work
+  pdl_trigger();
+  unsigned long long* rec = nullptr;
+  if (fp.stamps) {
+    const unsigned idx = __ldcg(fp.fwd_idx);
+    if (idx < (unsigned)fp.stamp_cap) rec = fp.stamps + (size_t)idx * 8;
+    if (rec && tid == 0) atomicMax(rec + 0, ~gtimer_ns());
+  }
+
+  // ---- 2. route the token (B = 1): x chunks of this thread, in registers
+  constexpr int kXC = 3;                       // H <= 9216
+  uint4 xr[kXC];
+  float xf[kXC][8];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < kXC; ++i) {
+    const int c = tid + i * kGemvWarps * 32;
+    xr[i] = c < n8 ? __ldcg(reinterpret_cast<const uint4*>(p.x_raw) + c) : make_uint4(0, 0, 0, 0);
+    h2f8(xr[i], xf[i]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bad |= !isfinite(xf[i][j]);
+  }
+  const int nonfinite = __syncthreads_or(bad);
+  mbar_wait(wbar, 0);                          // router rows landed
+  const uint4* w4 = reinterpret_cast<const uint4*>(dyn);
+  for (int e0 = 0; e0 < E; e0 += 8) {
+    double acc[8], ab[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { acc[j] = 0.0; ab[j] = 0.0; }
+#pragma unroll
+    for (int i = 0; i < kXC; ++i) {
+      const int c = tid + i * kGemvWarps * 32;
+      if (c >= n8) break;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (e0 + j >= E) break;
+        float wf[8];
+        h2f8(w4[(size_t)(e0 + j) * n8 + c], wf);
+        float s = 0.f, a = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          s = fmaf(wf[q], xf[i][q], s);
+          a = fmaf(fabsf(wf[q]), fabsf(xf[i][q]), a);
+        }
+        acc[j] += (double)s;
+        ab[j] += (double)a;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+        ab[j] += __shfl_xor_sync(0xffffffffu, ab[j], o);
+      }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { red[(warp * 8 + j) * 2] = acc[j]; red[(warp * 8 + j) * 2 + 1] = ab[j]; }
+    __syncthreads();
+    if (tid < 8 && e0 + tid < E) {
+      double l = 0.0, a = 0.0;
+      for (int w = 0; w < kGemvWarps; ++w) { l += red[(w * 8 + tid) * 2]; a += red[(w * 8 + tid) * 2 + 1]; }
+      s_L[e0 + tid] = l;
+      s_A[e0 + tid] = a;
+    }
+    __syncthreads();
+  }
+  // top-2 by (L desc, index asc) and the certainty of every comparison
+  int e0 = -1, e1 = -1;
+  if (warp == 0 && !nonfinite) {
+    int rk[2] = {64, 64};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h;
+      if (e < E) {
+        const double v = s_L[e];
+        int r = 0;
+        for (int f = 0; f < E; ++f) { const double o = s_L[f]; r += (o > v) || (o == v && f < e); }
+        rk[h] = r;
+      }
+    }
+    const unsigned m0 = __ballot_sync(0xffffffffu, rk[0] == 0), m0b = __ballot_sync(0xffffffffu, rk[1] == 0);
+    const unsigned m1 = __ballot_sync(0xffffffffu, rk[0] == 1), m1b = __ballot_sync(0xffffffffu, rk[1] == 1);
+    e0 = m0 ? __ffs(m0) - 1 : 32 + __ffs(m0b) - 1;
+    e1 = m1 ? __ffs(m1) - 1 : 32 + __ffs(m1b) - 1;
+    double rest = -1e300;                      // max over ranks >= 2 of L + eps
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h;
+      if (e < E && rk[h] >= 2) rest = fmax(rest, s_L[e] + kEpsRel * s_A[e]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rest = fmax(rest, __shfl_xor_sync(0xffffffffu, rest, o));
+    if (lane == 0) {
+      const double L0 = s_L[e0], L1 = s_L[e1];
+      const double ep0 = kEpsRel * s_A[e0], ep1 = kEpsRel * s_A[e1];
+      const double G = L0 - L1, m = ep0 + ep1 + 1e-12 * (1.0 + fabs(L0) + fabs(L1));
+      bool ok = (L0 - ep0 > L1 + ep1) && (L1 - ep1 > rest);
+      if (fp.th1_kind == 0) ok = ok && fabs(G - (double)fp.theta1 * 0x1p-48) > m;
+      if (fp.th2_kind == 0) ok = ok && fabs(G - (double)fp.theta2 * 0x1p-48) > m;
+      s_ok = ok;
+    }
+  }
+  __syncthreads();
+  uint8_t prec1 = HB_HIGH;
+  float g0 = 0.f, g1 = 0.f;
+  if (!nonfinite && !s_ok) {
+    // ---- exact fallback: integer logits (every CTA takes this branch alike)
+    for (int e = 0; e < E; ++e) {
+      u64 lo = 0, mid = 0, hi = 0;
+#pragma unroll
+      for (int i = 0; i < kXC; ++i) {
+        const int c = tid + i * kGemvWarps * 32;
+        if (c >= n8) break;
+        const uint4 wv = w4[(size_t)e * n8 + c];
+        const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
+        const uint32_t xa[4] = {xr[i].x, xr[i].y, xr[i].z, xr[i].w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          accum_exact((wa[q >> 1] >> (16 * (q & 1))) & 0xFFFF, (xa[q >> 1] >> (16 * (q & 1))) & 0xFFFF,
+                      lo, mid, hi);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+        mid += __shfl_xor_sync(0xffffffffu, mid, o);
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+      if (lane == 0) {
+        u64* d = xpart + ((size_t)warp * 64 + e) * 3;
+        d[0] = lo; d[1] = mid; d[2] = hi;
+      }
+    }
+    __syncthreads();
+    if (tid < E) {
+      u64 lo = 0, mid = 0, hi = 0;
+      for (int w = 0; w < kGemvWarps; ++w) {
+        const u64* d = xpart + ((size_t)w * 64 + tid) * 3;
+        lo += d[0]; mid += d[1]; hi += d[2];
+      }
+      s_Lx[tid] = (i128)(long long)lo + ((i128)(long long)mid << 20) + ((i128)(long long)hi << 40);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int rk[2] = {64, 64};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = lane + 32 * h;
+        if (e < E) {
+          const i128 v = s_Lx[e];
+          int r = 0;
+          for (int f = 0; f < E; ++f) { const i128 o = s_Lx[f]; r += (o > v) || (o == v && f < e); }
+          rk[h] = r;
+        }
+      }
+      const unsigned m0 = __ballot_sync(0xffffffffu, rk[0] == 0), m0b = __ballot_sync(0xffffffffu, rk[1] == 0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, rk[0] == 1), m1b = __ballot_sync(0xffffffffu, rk[1] == 1);
+      e0 = m0 ? __ffs(m0) - 1 : 32 + __ffs(m0b) - 1;
+      e1 = m1 ? __ffs(m1) - 1 : 32 + __ffs(m1b) - 1;
+      const i128 G = s_Lx[e0] - s_Lx[e1];      // >= 0
+      prec1 = gap_le(G, fp.th1_kind, fp.theta1) ? HB_HIGH
+            : gap_le(G, fp.th2_kind, fp.theta2) ? HB_LOW : HB_SKIP;
+      const float d = G >= ((i128)1 << 62) ? 1e30f : (float)(long long)G * 0x1p-48f;
+      const float ex = expf(-d);
+      g0 = 1.f / (1.f + ex);
+      g1 = ex * g0;
+    }
+  } else if (warp == 0 && !nonfinite) {
+    const double G = s_L[e0] - s_L[e1];
+    prec1 = (fp.th1_kind > 0 || (fp.th1_kind == 0 && G <= (double)fp.theta1 * 0x1p-48)) ? HB_HIGH
+          : (fp.th2_kind > 0 || (fp.th2_kind == 0 && G <= (double)fp.theta2 * 0x1p-48)) ? HB_LOW : HB_SKIP;
+    const float d = (float)G;
+    const float ex = expf(-d);
+    g0 = 1.f / (1.f + ex);
+    g1 = ex * g0;
+  }
+  // ---- 3. decision records and the job table (warp 0, lane 0)
+  if (tid == 0) {
+    hb_decision r[2];
+    int nj = 0;
+    if (nonfinite) {
+      for (int i = 0; i < 2; ++i) {
+        r[i].token = 0; r[i].expert = -1; r[i].sel_rank = (uint8_t)i; r[i].prec = HB_SKIP;
+        r[i].served_enc = HB_ENC_NONE; r[i].hit = 0; r[i].gate = __int_as_float(0x7fc00000);
+      }
+    } else {
+      const int ex[2] = {e0, e1};
+      const uint8_t pr[2] = {HB_HIGH, prec1};
+      const float gt[2] = {g0, g1};
+      int key[2];
+      for (int i = 0; i < 2; ++i) {
+        r[i].token = 0; r[i].expert = ex[i]; r[i].sel_rank = (uint8_t)i; r[i].prec = pr[i];
+        r[i].served_enc = HB_ENC_NONE; r[i].hit = 0; r[i].gate = gt[i];
+        key[i] = (pr[i] == HB_SKIP || ex[i] % fp.world != fp.rank) ? -1 : ex[i] * 2 + (pr[i] == HB_HIGH ? 0 : 1);
+      }
+      // jobs by key (expert, then High before Low), one slot each
+      const int order[2] = {key[1] >= 0 && (key[0] < 0 || key[1] < key[0]) ? 1 : 0,
+                            key[1] >= 0 && (key[0] < 0 || key[1] < key[0]) ? 0 : 1};
+      Job jobs[2];
+      for (int o = 0; o < 2; ++o) {
+        const int i = order[o];
+        if (key[i] < 0) continue;
+        const int enc = (key[i] & 1) ? fp.lo_enc : fp.hi_enc;
+        jobs[nj].blob = s_blob[ex[i] * 4 + enc];
+        jobs[nj].enc = enc;
+        jobs[nj].expert = ex[i];
+        jobs[nj].n_tok = 1;
+        jobs[nj].slot_off = nj;
+        fz_stok[nj] = 0;
+        fz_sgate[nj] = gt[i];
+        r[i].served_enc = (uint8_t)enc;
+        r[i].hit = 1;
+        ++nj;
+      }
+      long long c13[kFusedMaxV + 1], c2[kFusedMaxV + 1];
+      const int nv = build_vjobs(jobs, nj, H, p.F, fz_vj, c13, c2);
+      for (int v = 0; v <= nv; ++v) { s_cum13[v] = (int)c13[v]; s_cum2[v] = (int)c2[v]; }
+    }
+    fz_nv = nj;                                 // B = 1: one vjob per job
+    fz_nslot = nj;
+    if (blockIdx.x == 0) { fp.dec[0] = r[0]; fp.dec[1] = r[1]; }
+  }
+  // CTA 0 keeps x for the lazy exact logits (hb_get_logits)
+  if (blockIdx.x == 0 && fp.x_save)
+    for (int c = tid; c < n8; c += blockDim.x)
+      reinterpret_cast<uint4*>(fp.x_save)[c] = __ldcg(reinterpret_cast<const uint4*>(p.x_raw) + c);
+  // y row: 0 (the expert kernels add into it), NaN for a non-finite input
+  {
+    const float yv = nonfinite ? __int_as_float(0x7fc00000) : 0.f;
+    for (int i = blockIdx.x * blockDim.x + tid; i < H; i += gridDim.x * blockDim.x) p.y[i] = yv;
+    // the other K2a-sum buffer, for the next forward (not touched by this one)
+    for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < fp.zero_n;
+         i += (long long)gridDim.x * blockDim.x)
+      fp.zero_other[i] = 0.f;
+  }
+  __syncthreads();
+  if (tid == 0) fz_fs = FusedSync{fp.gbar, fp.gbar + 1, &s_warps_done, &s_released, rec};
+  if (rec && tid == 0) atomicMax(rec + 1, gtimer_ns());
+  if (fz_nv > 0) {
+    // ---- 4. K2a, then K2b (the grid barrier sits in K2b's first run)
+    // K2b's setup is stashed in shared memory while K2a runs: values held in
+    // registers across the inlined K2a loops would spill inside them
+    __shared__ Stage s_S2;
+    __shared__ PhaseCtx s_pc2;
+    {
+      Stage S2;
+      PhaseCtx pc2;
+      phase_setup<false, true>(p, s_cum2, &s_fk2, s_subb, s_subc, s_subvh, &s_nsub,
+                               smem_u32(&s_bar2), false, S2, pc2);
+      if (tid == 0) { s_S2 = S2; s_pc2 = pc2; }
+    }
+    {
+      Stage S13;
+      PhaseCtx pc13;
+      phase_setup<true, true>(p, s_cum13, &s_fk13, s_subb, s_subc, s_subvh, &s_nsub13,
+                              smem_u32(&s_bar13), false, S13, pc13);
+      phase_run<true, true>(p, s_cum13, &s_fk13, s_subvh, pc13, S13, s_meta[warp]);
+    }
+    {
+      const Stage S2 = s_S2;
+      const PhaseCtx pc2 = s_pc2;
+      phase_run<false, true>(p, s_cum2, &s_fk2, s_subvh, pc2, S2, s_meta[warp]);
+    }
+  }
+  if (fp.stamps) {
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long* rec_end = fz_fs.stamp;
+      if (rec_end) atomicMax(rec_end + 4, gtimer_ns());
+      __threadfence();
+      if (atomicAdd(fp.fwd_idx + 1, 1u) == gridDim.x - 1) {   // last CTA: next record
+        fp.fwd_idx[1] = 0u;
+        fp.fwd_idx[0] += 1u;
+      }
+    }
+  }
 }
 
 // hfin: h = silu(a) * u of every slot from the K2a sums, as the fp16 hi/lo
@@ -958,6 +1494,23 @@ void launch_w13(const GemvParams& p, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<true>();
   set_max_dyn_smem(gemv_kernel<true>, smem);
   launch_pdl(gemv_kernel<true>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
+}
+void launch_fused(const FusedParams& p, cudaStream_t s) {
+  constexpr int smem = gemv_smem_bytes<false>() > gemv_smem_bytes<true>() ? gemv_smem_bytes<false>()
+                                                                          : gemv_smem_bytes<true>();
+  set_max_dyn_smem(fused_decode_kernel, smem);
+  launch_pdl(fused_decode_kernel, kGemvCTAs, kGemvWarps * 32, smem, s, p);
+}
+bool fused_fits(int E, int H, int F, int hi_enc, int lo_enc) {
+  if (E > 64 || (long long)E * H * 2 > kFusedScratch || H / 8 > 3 * kGemvWarps * 32) return false;
+  if ((size_t)(2 * H + (H / 32) * 4) > (size_t)KCfg<true>::XSTAGE) return false;
+  for (int enc : {hi_enc, lo_enc}) {          // every K2b sub-space stages its slice of h
+    const int G = F / epg_of(enc), nh = G % 4 == 0 ? 2 : 1;
+    if ((G / nh) % 2) return false;
+    const size_t slice = (size_t)(F / nh) * 4 + (size_t)(F / nh / 32) * 4;
+    if (slice > (size_t)KCfg<false>::XSTAGE) return false;
+  }
+  return true;
 }
 void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
   const int n = max_slots * (p.F / 32) * 4;

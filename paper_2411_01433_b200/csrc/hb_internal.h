@@ -129,8 +129,8 @@ struct RouterParams {
   long long* logits;                   // [B][E][2] copy for route 0, or null
   uint4* x_perm;                       // [B][H/8] pair-permuted x, or null
   float* xsum;                         // [B][H/32], or null
-  float* zero_buf[2];                  // zeroed by the router grid: K2a sums, y
-  long long zero_n[2];                 // floats, multiples of 4 (16-byte aligned buffers)
+  float* zero_buf[3];                  // zeroed by the router grid: K2a sums, y, the other sum buffer
+  long long zero_n[3];                 // floats
   // resident job building (blob_table != null): last CTA builds the table
   const uint8_t* const* blob_table;    // [E][4] device blob of (expert, enc) for this layer
   int hi_enc, lo_enc;
@@ -142,6 +142,7 @@ struct GemvParams {
   JobTable jt;
   BlobLayout lay[4];
   int H, F, B, k;
+  const __half* x_raw;                 // [B][H] the caller's x (fused decode kernel)
   const uint4* x_perm;                 // [B][H/8]
   const float* xsum;                   // [B][H/32]
   float* au;                           // [slots][2][F] K2a sums W1 x | W3 x (zeroed by router)
@@ -160,6 +161,27 @@ struct GemvParams {
   float k2b_w[4];                      // K2b CTA split: cost of a unit per encoding (F16 = 1)
 };
 
+// Fused decode kernel (batch 1, top-2, resident): router + K2a + K2b in one
+// launch per layer (gemv.cu)
+struct FusedParams {
+  GemvParams g;                        // g.x_raw = x, g.au = this forward's sum buffer
+  const __half* wg;                    // router rows of the layer [E][H]
+  const uint8_t* const* blob_table;    // [E][4] device blob of (expert, enc)
+  int E;
+  int64_t theta1, theta2;
+  int th1_kind, th2_kind;
+  int rank, world, hi_enc, lo_enc;
+  hb_decision* dec;                    // [2] decision records (written by CTA 0)
+  __half* x_save;                      // [H] copy of x for hb_get_logits, or null
+  float* zero_other;                   // the other sum buffer, zeroed for the next forward
+  long long zero_n;
+  unsigned* gbar;                      // grid barrier [count, generation] (self-resetting)
+  unsigned long long* stamps;          // profile records [cap][8] or null
+  int stamp_cap;
+  unsigned* fwd_idx;                   // [record index, exit counter]
+};
+void launch_fused(const FusedParams& p, cudaStream_t s);
+bool fused_fits(int E, int H, int F, int hi_enc, int lo_enc);
 void launch_router(const RouterParams& p, cudaStream_t s);
 // kernel launch allowing programmatic dependent launch (the kernel overlaps
 // the tail of its predecessor in the stream and orders itself with

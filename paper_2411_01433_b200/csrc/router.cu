@@ -28,6 +28,7 @@
 #include <algorithm>
 
 #include "hb_internal.h"
+#include "exact_dot.cuh"
 
 namespace hb {
 
@@ -38,42 +39,6 @@ __device__ unsigned long long g_rtl[16];
 #else
 #define HB_RTL(i) do { } while (0)
 #endif
-
-typedef __int128 i128;
-typedef unsigned long long u64;
-
-__device__ __forceinline__ void fp16_mant_exp(uint32_t bits, int& m, int& e) {
-  const int ex = (bits >> 10) & 0x1F;
-  const int man = bits & 0x3FF;
-  m = ex ? (man | 0x400) : man;
-  e = ex ? ex - 25 : -24;              // value = m * 2^e
-  if (bits & 0x8000) m = -m;
-}
-
-// Products m_w*m_x (|.| < 2^22) shifted by s = e_w+e_x+48 in [0, 58] go to
-// three int64 accumulators by s range: [0,20) -> lo, [20,40) -> mid (shifted
-// by s-20), [40,58] -> hi (shifted by s-40).  Each term is < 2^41, so up to
-// 2^20 terms cannot overflow; L = lo + mid*2^20 + hi*2^40 exactly.
-__device__ __forceinline__ void accum_exact(uint32_t wbits, uint32_t xbits, u64& lo, u64& mid,
-                                            u64& hi) {
-  int mw, ew, mx, ex;
-  fp16_mant_exp(wbits, mw, ew);
-  fp16_mant_exp(xbits, mx, ex);
-  const long long p = (long long)(mw * mx);
-  const int s = ew + ex + 48;
-  // branch-free: the bucket of s and the term shifted into it (no divergence)
-  const int r = (s >= 20) + (s >= 40);
-  const u64 term = (u64)(p << (s - 20 * r));
-  lo += r == 0 ? term : 0ull;
-  mid += r == 1 ? term : 0ull;
-  hi += r == 2 ? term : 0ull;
-}
-
-__device__ __forceinline__ bool gap_le(i128 G, int kind, long long theta) {
-  if (kind > 0) return true;
-  if (kind < 0) return false;
-  return G <= (i128)theta;
-}
 
 __device__ double i128_to_double(i128 v) {
   const bool neg = v < 0;
@@ -470,7 +435,7 @@ router_kernel(const __grid_constant__ RouterParams p) {
     const long long t0 = (long long)(blockIdx.x - nrows * C) * blockDim.x + tid;
     const long long stride = (long long)(gridDim.x - nrows * C) * blockDim.x;
 #pragma unroll
-    for (int z = 0; z < 2; ++z) {
+    for (int z = 0; z < 3; ++z) {
       float* zb = p.zero_buf[z];
       const long long n = p.zero_n[z];
       if ((reinterpret_cast<uintptr_t>(zb) & 15) == 0) {
@@ -659,7 +624,7 @@ void launch_router(const RouterParams& p, cudaStream_t s) {
   // one 8-CTA cluster per (route layer, token) row, plus clusters of CTAs that
   // zero the GEMV accumulation buffers in parallel
   const int C = p.n_route * p.B >= 16 ? 1 : kRouterCluster;
-  const long long nz4 = (p.zero_n[0] + p.zero_n[1]) / 4;
+  const long long nz4 = (p.zero_n[0] + p.zero_n[1] + p.zero_n[2]) / 4;
   int zc = nz4 ? (int)std::min<long long>(32, (nz4 + 2 * kRouterThreads - 1) / (2 * kRouterThreads)) : 0;
   zc = (zc + C - 1) / C * C;
   const int grid = p.n_route * p.B * C + zc;

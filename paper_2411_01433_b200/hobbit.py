@@ -164,6 +164,16 @@ class Context:
         n = self._check(lib.hb_profile_read(self._h, buf, cap))
         return [(buf[2 * i], buf[2 * i + 1]) for i in range(n)]
 
+    def stamps(self, max_forwards: int):
+        """Arm in-kernel %globaltimer records for the next max_forwards fused forwards (0 = off)."""
+        self._check(lib.hb_stamps(self._h, max_forwards))
+
+    def stamps_read(self, cap: int = 1 << 16):
+        """[(start, decided, k2a_done, released, end)] ns per recorded fused forward."""
+        buf = (C.c_uint64 * (5 * cap))()
+        n = self._check(lib.hb_stamps_read(self._h, buf, cap))
+        return [tuple(buf[5 * i:5 * i + 5]) for i in range(n)]
+
     def nccl_init(self, group=None):
         """EP exchange inside the library (A10): rank 0 makes an NCCL unique id,
         torch.distributed broadcasts it, every rank joins; afterwards forward()
