@@ -258,10 +258,13 @@ int hb_profile_read(hb_ctx* ctx, float* ms, int cap);
  * captured while it is on -- record %globaltimer stamps from inside the
  * kernel (device atomics, no events, no serialisation).  Synchronises and
  * clears the records; 0 disables for forwards issued afterwards.
- * hb_stamps_read synchronises and returns n records of 5 uint64 ns each:
+ * hb_stamps_read synchronises and returns n records of 15 uint64 each (ns):
  * [kernel start (first CTA past its wait on the previous kernel), decisions
- * done (last CTA), K2a done (last CTA), grid barrier passed (first CTA),
- * kernel end (last CTA)]; returns n. */
+ * done (last CTA), K2a done (last CTA), grid barrier passed / K2b h staged
+ * (first CTA), kernel end (last CTA), router rows landed (last CTA), logits
+ * done (last CTA), decisions + job table done (last CTA), h staged (last
+ * CTA), h staged (first CTA), router sub-steps (diagnostic) x4, number of
+ * exact-fallback decisions]; 0 where a path has no such point; returns n. */
 int hb_stamps(hb_ctx* ctx, int max_forwards);
 int hb_stamps_read(hb_ctx* ctx, uint64_t* out, int cap);
 

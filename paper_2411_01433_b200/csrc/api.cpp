@@ -72,6 +72,7 @@ struct hb_ctx {
   size_t bbytes[4]{};
   // router weights [L][E][H]
   __half* wg = nullptr;
+  float* wnorm = nullptr;                 // [L][E] ||W_e||_2 rounded up (fused router's error bound)
   std::vector<char> router_set;
   // resident registry: device blobs [L][E][4]
   std::vector<const uint8_t*> dev_blob;
@@ -92,6 +93,7 @@ struct hb_ctx {
   hb_decision* dec_host = nullptr;        // pinned [(1+p)][B][k]
   long long* logits = nullptr;            // [B][E][2]
   long long* lbuf = nullptr;              // [P][B][E][2] router scratch
+  int* rowbad = nullptr;                  // [P][B] non-finite flags (router scratch)
   uint4* x_perm = nullptr;
   float* xsum = nullptr;
   float* au = nullptr;                    // 2 x [slots][2][F] K2a sums (double-buffered)
@@ -105,6 +107,8 @@ struct hb_ctx {
   bool stamps_on = false;
   __half* x_save = nullptr;               // x of the last fused forward (lazy exact logits)
   bool last_fused = false;
+  bool fused_split = false;               // HB_FUSED_SPLIT=1: router+K2a kernel, then hfin + K2b
+  bool fused_router = false;              // HB_FUSED_ROUTER=1: one-CTA router kernel + legacy K2a/hfin/K2b
   uint4* h_hi = nullptr;                  // h in global memory (large batches only)
   uint4* h_lo = nullptr;
   float* hsum = nullptr;
@@ -285,7 +289,7 @@ static void free_ctx(hb_ctx* c) {
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
                    c->logits, c->lbuf, c->x_perm, c->xsum, c->au, c->h_hi, c->h_lo,
                    c->hsum, c->done, c->gctr, c->jt_dev, c->k3_xg, c->k3_hB, c->k3_tab, c->k3_tmap,
-                   c->gbar, c->fwd_idx, c->stamps, c->x_save};
+                   c->gbar, c->fwd_idx, c->stamps, c->x_save, c->wnorm, c->rowbad};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
@@ -357,9 +361,11 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
             dm((void**)&c->dec_pred, sizeof(hb_decision) * P * B * K) &&
             dm((void**)&c->logits, sizeof(long long) * B * E * 2) &&
             dm((void**)&c->lbuf, sizeof(long long) * P * B * E * 2) &&
+            dm((void**)&c->rowbad, sizeof(int) * P * B) &&
             dm((void**)&c->x_perm, (size_t)B * H * 2) && dm((void**)&c->xsum, (size_t)B * (H / 32) * 4) &&
             dm((void**)&c->au, 2 * (size_t)c->max_slots * 2 * F * 4) &&
             dm((void**)&c->gbar, 16) && dm((void**)&c->fwd_idx, 16) &&
+            dm((void**)&c->wnorm, (size_t)L * E * 4) &&
             dm((void**)&c->x_save, (size_t)H * 2) &&
             dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
@@ -403,9 +409,15 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   cudaMemset(c->gbar, 0, 16);
   cudaMemset(c->fwd_idx, 0, 16);
   {
-    const char* nf = std::getenv("HB_NO_FUSED");
-    c->fused_ok = resident && K == 2 && !(nf && nf[0] == '1') &&
-                  fused_fits(E, H, F, k.hi_enc, k.lo_enc);
+    // batch-1 decode chain: HB_DECODE = legacy (router
+    // kernel, K2a, hfin, K2b: the default, fastest measured), fused (one
+    // kernel per layer), split (router+K2a kernel, hfin, K2b) or router
+    // (one-CTA filtered router kernel, K2a, hfin, K2b)
+    const char* dm_ = std::getenv("HB_DECODE");
+    const std::string mode = dm_ ? dm_ : "legacy";
+    c->fused_ok = resident && K == 2 && mode != "legacy" && fused_fits(E, H, F, k.hi_enc, k.lo_enc);
+    c->fused_split = mode == "split";
+    c->fused_router = mode == "router";
   }
   cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + 2 * kGemvCTAs));
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
@@ -479,8 +491,25 @@ int hb_set_router(hb_ctx* c, int layer, const void* w, int on_device) {
   if (layer < 0 || layer >= c->cfg.n_layers) return fail(c, HB_EINVAL, "bad layer");
   const size_t n = (size_t)c->cfg.n_experts * c->cfg.hidden * 2;
   CUDA_TRY(c, cudaSetDevice(c->device));
+  // host copy: finiteness check and the row norms of the fused router's error bound
+  std::vector<uint16_t> hw(n / 2);
+  CUDA_TRY(c, cudaMemcpy(hw.data(), w, n, on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+  const int E = c->cfg.n_experts, H = c->cfg.hidden;
+  std::vector<float> wn(E);
+  for (int e = 0; e < E; ++e) {
+    double ss = 0.0;
+    for (int i = 0; i < H; ++i) {
+      const uint16_t b = hw[(size_t)e * H + i];
+      if ((b & 0x7C00) == 0x7C00) return fail(c, HB_EINVAL, "router weights must be finite");
+      const int ex = (b >> 10) & 0x1F, man = b & 0x3FF;
+      const double v = ex ? std::ldexp((double)(man | 0x400), ex - 25) : std::ldexp((double)man, -24);
+      ss += v * v;
+    }
+    wn[e] = (float)(std::sqrt(ss) * (1.0 + 1e-9)) * (1.0f + 1e-6f);   // rounded up
+  }
   CUDA_TRY(c, cudaMemcpy((uint8_t*)c->wg + (size_t)layer * n, w, n,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMemcpy(c->wnorm + (size_t)layer * E, wn.data(), 4 * E, cudaMemcpyHostToDevice));
   c->router_set[layer] = 1;
   return HB_OK;
 }
@@ -631,6 +660,7 @@ static RouterParams router_params(hb_ctx* c, const void* x, int batch) {
   p.jt = c->jt;
   p.done = c->done;
   p.lbuf = c->lbuf;
+  p.rowbad = c->rowbad;
   return p;
 }
 
@@ -674,6 +704,9 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y, float* au) {
   g.static_frac2 = c->static_frac2;
   g.chunk = c->chunk;
   for (int e = 0; e < 4; ++e) g.k2b_w[e] = c->k2b_w[e];
+  g.stamps = c->stamps_on ? c->stamps : nullptr;
+  g.stamp_cap = c->stamp_cap;
+  g.fwd_idx = c->fwd_idx;
   return g;
 }
 
@@ -706,6 +739,7 @@ static int launch_fused_forward(hb_ctx* c, int layer, const void* x, void* y, cu
   fp.wg = c->wg + (size_t)layer * k.n_experts * k.hidden;
   fp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
   fp.E = k.n_experts;
+  fp.wnorm = c->wnorm + (size_t)layer * k.n_experts;
   fp.theta1 = hb_theta(k.t1, &fp.th1_kind);
   fp.theta2 = hb_theta(k.t2, &fp.th2_kind);
   fp.rank = k.rank;
@@ -717,14 +751,30 @@ static int launch_fused_forward(hb_ctx* c, int layer, const void* x, void* y, cu
   fp.zero_other = au_buf(c, cn ^ 1);
   fp.zero_n = c->au_dirty[cn ^ 1];
   fp.gbar = c->gbar;
-  fp.stamps = c->stamps_on ? c->stamps : nullptr;
-  fp.stamp_cap = c->stamp_cap;
-  fp.fwd_idx = c->fwd_idx;
+  fp.stamps = fp.g.stamps;
+  fp.stamp_cap = fp.g.stamp_cap;
+  fp.fwd_idx = fp.g.fwd_idx;
+  const GemvParams gp2 = fp.g;               // split mode: hfin + K2b (legacy) stamp through it
+  fp.g.stamps = nullptr;                     // the fused kernel stamps through fp
   cudaEvent_t* ev = nullptr;
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
   if (ev) cudaEventRecord(ev[0], s);
-  launch_fused(fp, s);
-  if (ev) { cudaEventRecord(ev[1], s); cudaEventRecord(ev[2], s); }
+  fp.router_only = c->fused_router;
+  launch_fused(fp, c->fused_split, s);
+  if (c->fused_router) {
+    launch_w13(gp2, s);
+    c->launches += 1;
+  }
+  if (c->fused_split || c->fused_router) {
+    launch_hfin(gp2, 2, s);
+    if (ev) cudaEventRecord(ev[1], s);
+    launch_w2(gp2, s);
+    c->launches += 2;
+    if (ev) cudaEventRecord(ev[2], s);
+  } else if (ev) {
+    cudaEventRecord(ev[1], s);
+    cudaEventRecord(ev[2], s);
+  }
   c->au_dirty[cn ^ 1] = 0;
   c->au_dirty[cn] = (long long)2 * 2 * k.ffn;      // top-2: at most two slots
   c->au_cur = cn;
@@ -819,6 +869,8 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   const hb_config& k = c->cfg;
   if (layer < 0 || layer >= k.n_layers) return fail(c, HB_EINVAL, "bad layer");
   if (batch <= 0 || batch > k.max_batch) return fail(c, HB_EINVAL, "batch must be in [1, max_batch]");
+  if (((uintptr_t)x & 15) || ((uintptr_t)y & 15))
+    return fail(c, HB_EINVAL, "x and y must be 16-byte aligned");
   if (!c->router_set[layer]) return fail(c, HB_ESTATE, "router of this layer not set");
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(c, cudaSetDevice(c->device));
@@ -1159,11 +1211,11 @@ int hb_stamps(hb_ctx* c, int max_forwards) {
     if (c->stamps) cudaFree(c->stamps);
     c->stamps = nullptr;
     c->stamp_cap = 0;
-    CUDA_TRY(c, cudaMalloc((void**)&c->stamps, sizeof(unsigned long long) * 8 * (size_t)max_forwards));
+    CUDA_TRY(c, cudaMalloc((void**)&c->stamps, sizeof(unsigned long long) * kStampStride * (size_t)max_forwards));
     c->stamp_cap = max_forwards;
   }
   if (c->stamps)
-    CUDA_TRY(c, cudaMemset(c->stamps, 0, sizeof(unsigned long long) * 8 * (size_t)c->stamp_cap));
+    CUDA_TRY(c, cudaMemset(c->stamps, 0, sizeof(unsigned long long) * kStampStride * (size_t)c->stamp_cap));
   CUDA_TRY(c, cudaMemset(c->fwd_idx, 0, 16));
   c->stamps_on = max_forwards > 0;
   return HB_OK;
@@ -1177,16 +1229,22 @@ int hb_stamps_read(hb_ctx* c, uint64_t* out, int cap) {
   CUDA_TRY(c, cudaMemcpy(idx, c->fwd_idx, 8, cudaMemcpyDeviceToHost));
   const int n = std::min<int>(std::min<int>((int)idx[0], c->stamp_cap), cap);
   if (n <= 0) return 0;
-  std::vector<unsigned long long> raw((size_t)n * 8);
+  std::vector<unsigned long long> raw((size_t)n * kStampStride);
   CUDA_TRY(c, cudaMemcpy(raw.data(), c->stamps, raw.size() * 8, cudaMemcpyDeviceToHost));
   for (int i = 0; i < n; ++i) {
-    const unsigned long long* r = &raw[(size_t)i * 8];
-    uint64_t* o = out + (size_t)i * 5;
+    const unsigned long long* r = &raw[(size_t)i * kStampStride];
+    uint64_t* o = out + (size_t)i * 15;
     o[0] = ~r[0];                 // first CTA past griddepcontrol.wait
     o[1] = r[1];                  // last CTA with its decisions / job table
     o[2] = r[2];                  // last CTA done with K2a (grid barrier arrival)
     o[3] = ~r[3];                 // first CTA released by the grid barrier
     o[4] = r[4];                  // last CTA done
+    o[5] = r[5];                  // last CTA with the router rows in shared memory
+    o[6] = r[6];                  // last CTA with its (filtered) logits
+    o[7] = r[7];                  // last CTA past decisions + job table
+    o[8] = r[8];                  // last CTA with h staged (fused kernel)
+    o[9] = r[9] ? ~r[9] : 0;      // first CTA with h staged (fused kernel)
+    for (int j = 10; j < 15; ++j) o[j] = r[j];   // router sub-steps (diagnostic), [14] fallbacks
   }
   return n;
 }

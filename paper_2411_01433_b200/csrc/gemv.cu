@@ -312,7 +312,7 @@ __device__ void stage_share_xperm(const GemvParams& p, int w, uint8_t* st, int r
 }
 // K2a, fused decode: pair-permute x (Q_c = (x[8t+c], x[8t+c+4])) and sum each
 // 32-element block (the Q2 m-term) straight from the caller's fp16 x.
-__device__ void stage_share_xraw(const GemvParams& p, int w, uint8_t* st, int row0, int nrows) {
+__device__ __noinline__ void stage_share_xraw(const GemvParams& p, int w, uint8_t* st, int row0, int nrows) {
   const int lane = threadIdx.x & 31;
   const int K = p.H, nb = K / 32;
   uint4* dst = reinterpret_cast<uint4*>(st);
@@ -345,7 +345,9 @@ __device__ void stage_share_xraw(const GemvParams& p, int w, uint8_t* st, int ro
 }
 // K2b, fused decode: this CTA's column slice [c0, c0 + kcols) of h for slots
 // [row0, row0 + nrows), h = silu(a) * u from the K2a sums (fp16 hi/lo pair +
-// block sums), computed redundantly by every CTA of the slice's group.
+// block sums), computed redundantly by every CTA of the slice's group.  Four
+// lanes per 32-row block (lane t of the quad owns rows 8t..8t+7, i.e. chunk t
+// of the pair-permuted hi / lo rows), as in hfin: short dependency chains.
 __device__ void stage_share_h(const GemvParams& p, int w, uint8_t* st, int row0, int nrows,
                               int c0, int kcols) {
   const int lane = threadIdx.x & 31;
@@ -353,16 +355,43 @@ __device__ void stage_share_h(const GemvParams& p, int w, uint8_t* st, int row0,
   uint4* dhi = reinterpret_cast<uint4*>(st);
   uint4* dlo = dhi + (size_t)nrows * (kcols / 8);
   float* zd = reinterpret_cast<float*>(dlo + (size_t)nrows * (kcols / 8));
-  for (int i = w * 32 + lane; i < nrows * nb; i += kGemvWarps * 32) {
-    const int s = i / nb, j = i - s * nb;
-    uint4 hi[4], lo[4];
-    const float hs = h_block(p.au, K, row0 + s, c0 / 32 + j, hi, lo);
+  const int n = nrows * nb * 4;
+  for (int i0 = w * 32; i0 < n; i0 += kGemvWarps * 32) {
+    const int i = i0 + lane;
+    const bool act = i < n;
+    const int q = act ? i : 0;
+    const int item = q >> 2, t = q & 3;
+    const int s = item / nb, j = item - s * nb;
+    const float* pa = p.au + (size_t)(row0 + s) * 2 * K + (size_t)c0 + (size_t)j * 32 + 8 * t;
+    const float* pu = pa + K;
+    const float4 a0 = __ldcg(reinterpret_cast<const float4*>(pa));
+    const float4 a1 = __ldcg(reinterpret_cast<const float4*>(pa) + 1);
+    const float4 u0 = __ldcg(reinterpret_cast<const float4*>(pu));
+    const float4 u1 = __ldcg(reinterpret_cast<const float4*>(pu) + 1);
+    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float uv[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+    float h[8], hs = 0.f;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      dhi[(size_t)s * (kcols / 8) + j * 4 + t] = hi[t];
-      dlo[(size_t)s * (kcols / 8) + j * 4 + t] = lo[t];
+    for (int r = 0; r < 8; ++r) {
+      h[r] = av[r] / (1.f + expf(-av[r])) * uv[r];
+      hs += h[r];
     }
-    zd[i] = hs;
+    uint32_t wh[4], wl[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {              // Q_c = (h[8t+c], h[8t+c+4])
+      const __half h0 = __float2half_rn(h[c]), h1 = __float2half_rn(h[c + 4]);
+      const __half l0 = __float2half_rn(h[c] - __half2float(h0));
+      const __half l1 = __float2half_rn(h[c + 4] - __half2float(h1));
+      wh[c] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+      wl[c] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+    }
+    hs += __shfl_xor_sync(0xffffffffu, hs, 1);
+    hs += __shfl_xor_sync(0xffffffffu, hs, 2);
+    if (act) {
+      dhi[(size_t)s * (kcols / 8) + j * 4 + t] = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+      dlo[(size_t)s * (kcols / 8) + j * 4 + t] = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+      if (t == 0) zd[item] = hs;
+    }
   }
 }
 
@@ -520,6 +549,10 @@ __device__ __forceinline__ void stage_h_and_wait(const GemvParams& p, const Stag
   if (!FUSED) {
     pdl_wait();
     if (S.on) stage_h_bulk_and_wait(p, S);
+    if (p.stamps && threadIdx.x == 0) {
+      const unsigned idx = __ldcg(p.fwd_idx);
+      if (idx < (unsigned)p.stamp_cap) atomicMax(p.stamps + (size_t)idx * kStampStride + 3, ~gtimer_ns());
+    }
     return;
   }
   fused_grid_barrier(fz_fs);
@@ -527,6 +560,10 @@ __device__ __forceinline__ void stage_h_and_wait(const GemvParams& p, const Stag
     stage_share_h(p, threadIdx.x >> 5, S.ptr, S.row0, S.nrows, S.hs * S.kcols, S.kcols);
     mbar_arrive(S.bar);
     mbar_wait(S.bar, 0);
+  }
+  if (fz_fs.stamp && threadIdx.x == 0) {
+    atomicMax(fz_fs.stamp + 8, gtimer_ns());           // last CTA with h staged
+    atomicMax(fz_fs.stamp + 9, ~gtimer_ns());          // first CTA with h staged
   }
 }
 
@@ -684,9 +721,32 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
   // K2b: the ring prologue (W2 is independent of K2a) goes out first, during
   // K2a's tail; then wait for K2a and build h.
   if (W13 && first && S.on) stage_x_and_wait<FUSED>(p, S);
+  if constexpr (FUSED && !W13) {
+    // fused kernel, first K2b run: before the grid barrier, pull the units of
+    // the ring prologue into L2 (prefetch: keeps HBM busy during the barrier
+    // without queueing ring loads in front of the h build's reads), then the
+    // barrier and h, then the prologue (now L2 hits)
+    if (first) {
+      const int n = min((DEPTH - 1) * NU, fd.b - fd.a);
+      const int l = fd.a - cum + lane;
+      if (lane < n && l < Uv) {
+        const int tl = l / Gs, gr = l - tl * Gs;
+        const size_t u = (size_t)tl * G + goff + gr;
+        const MatLayout& L = p.lay[ENC].mat[2];
+        const char* q = reinterpret_cast<const char*>(vj.blob + L.q + u * 1024);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) asm volatile("prefetch.global.L2 [%0];" :: "l"(q + 128 * i));
+        if constexpr (SB > 0) {
+          const char* sc = reinterpret_cast<const char*>(vj.blob + L.s + u * 16 * SB);
+          for (int i = 0; i < 16 * SB; i += 128) asm volatile("prefetch.global.L2 [%0];" :: "l"(sc + i));
+        }
+      }
+      stage_h_and_wait<FUSED>(p, S);
+    }
+  }
 #pragma unroll 1
   for (int s = 0; s < DEPTH - 1; ++s) issue();
-  if (!W13 && first) stage_h_and_wait<FUSED>(p, S);  // h after K2a (hfin or the grid barrier)
+  if (!FUSED && !W13 && first) stage_h_and_wait<FUSED>(p, S);  // h after K2a (hfin)
   if (first) HB_TL(W13, (threadIdx.x >> 5) * gridDim.x + blockIdx.x, 2);
 
   // ---- lane constants: B-operand rows, outputs of the lane's two slots
@@ -874,16 +934,6 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
 
 extern __shared__ __align__(128) uint8_t gemv_smem[];
 
-// The fused kernel calls each run<> through a non-inlined wrapper: the
-// wrapper gets its own register allocation, so the kernel's other live state
-// (router results, the K2b setup) is saved around the call instead of
-// competing with the streaming loop's registers.
-template <int ENC, bool W13, bool XR>
-__device__ __noinline__ void run_fused(const GemvParams& p, const VJob& vj, int cum, int Uv,
-                                       Feed& fd, uint32_t ring, uint2* meta, const Stage& S,
-                                       bool first) {
-  run<ENC, W13, XR, true>(p, vj, cum, Uv, fd, ring, meta, S, first);
-}
 
 // What phase_setup decides for this CTA (every thread holds a copy).
 struct PhaseCtx {
@@ -1022,11 +1072,7 @@ __device__ void phase_run(const GemvParams& p, const int* s_cum, const FeedConst
     }
     const VJobD d = JT<FUSED>::vjob(p, lo);
     const VJob vj{d.blob, d.enc, d.slot0, d.nslot};
-#define HB_RUN(E, X)                                                   \
-  do {                                                                 \
-    if constexpr (FUSED) run_fused<E, W13, X>(p, vj, cv, Uv, fd, ring, meta, S, first); \
-    else run<E, W13, X, false>(p, vj, cv, Uv, fd, ring, meta, S, first); \
-  } while (0)
+#define HB_RUN(E, X) run<E, W13, X, FUSED>(p, vj, cv, Uv, fd, ring, meta, S, first)
     switch (vj.enc * 2 + (S.on ? 1 : 0)) {
       case 2 * HB_F16 + 1: HB_RUN(HB_F16, true); break;
       case 2 * HB_F16 + 0: HB_RUN(HB_F16, false); break;
@@ -1045,6 +1091,24 @@ __device__ void phase_run(const GemvParams& p, const int* s_cum, const FeedConst
       if (S.on) stage_x_and_wait<FUSED>(p, S);
     } else {
       stage_h_and_wait<FUSED>(p, S);
+    }
+  }
+}
+
+// hb_stamps records of the legacy chain: K2a end (last CTA); K2b end (last
+// CTA), and K2b's last CTA moves the record index on
+template <bool W13>
+__device__ __forceinline__ void legacy_stamp_end(const GemvParams& p) {
+  if (!p.stamps) return;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const unsigned idx = __ldcg(p.fwd_idx);
+  if (idx < (unsigned)p.stamp_cap) atomicMax(p.stamps + (size_t)idx * kStampStride + (W13 ? 2 : 4), gtimer_ns());
+  if (!W13) {
+    __threadfence();
+    if (atomicAdd(p.fwd_idx + 1, 1u) == gridDim.x - 1) {
+      p.fwd_idx[1] = 0u;
+      p.fwd_idx[0] += 1u;
     }
   }
 }
@@ -1075,13 +1139,24 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   // K2b thread 0 arrives once with the bulk copies' transaction count
   if (threadIdx.x == 0) mbar_init(smem_u32(&s_bar), W13 ? blockDim.x : 1);
   __syncthreads();
-  if (JT<false>::nv(p) == 0) return;        // nothing owned: y stays zero (router)
+  if (W13 && p.stamps && threadIdx.x == 0) {
+    const unsigned idx = __ldcg(p.fwd_idx);
+    if (idx < (unsigned)p.stamp_cap) {
+      atomicMax(p.stamps + (size_t)idx * kStampStride + 0, ~gtimer_ns());
+      atomicMax(p.stamps + (size_t)idx * kStampStride + 1, gtimer_ns());
+    }
+  }
+  if (JT<false>::nv(p) == 0) {               // nothing owned: y stays zero (router)
+    legacy_stamp_end<W13>(p);
+    return;
+  }
   Stage S;
   PhaseCtx pc;
   phase_setup<W13, false>(p, s_cum, &s_fk, s_subb, s_subc, s_subvh, &s_nsub, smem_u32(&s_bar),
                           p.h_global, S, pc);
   phase_run<W13, false>(p, s_cum, &s_fk, s_subvh, pc, S, s_meta[warp]);
   HB_TL(W13, warp * gridDim.x + blockIdx.x, 3);
+  legacy_stamp_end<W13>(p);
 }
 
 // ------------------------------------------------------------ fused decode
@@ -1109,6 +1184,129 @@ constexpr int kFusedScratch = 160 * 1024;   // router scratch offset in dynamic 
 // 4.6e-7 * A >= (gamma_7 + 1e-13) (1 + gamma_7) (1 + 1e-13) * A.
 constexpr double kEpsRel = 4.6e-7;
 
+// The fused kernel runs each phase in a non-inlined function whose code is
+// the legacy kernel's (run<> inlined into phase_run): a separate register
+// allocation, so the router's state never competes with the streaming loops.
+// p lives in shared memory (fz_p) so the functions address it cheaply.
+__shared__ GemvParams fz_p;
+__device__ __noinline__ void fused_k2a(const GemvParams& p, int* s_cum, FeedConst* s_fk,
+                                       int* s_subb, float* s_subc, int* s_subvh, int* s_nsub,
+                                       uint32_t bar, uint2* meta) {
+  Stage S;
+  PhaseCtx pc;
+  phase_setup<true, true>(p, s_cum, s_fk, s_subb, s_subc, s_subvh, s_nsub, bar, false, S, pc);
+  phase_run<true, true>(p, s_cum, s_fk, s_subvh, pc, S, meta);
+}
+__device__ __noinline__ void fused_k2b(const GemvParams& p, const int* s_cum, const FeedConst* s_fk,
+                                       const int* s_subvh, const Stage* sS, const PhaseCtx* spc,
+                                       uint2* meta) {
+  const Stage S = *sS;
+  const PhaseCtx pc = *spc;
+  phase_run<false, true>(p, s_cum, s_fk, s_subvh, pc, S, meta);
+}
+
+// Decision records and the job table of the token (B = 1, top-2), by lane 0
+// of warp 0 from the decided experts: gates g0 = 1/(1+e), g1 = e*g0 with
+// e = exp(-gap) (reading R25); jobs by key (expert, High before Low), one
+// slot each; shared copies for this CTA, and (CTA 0) the decision records
+// and, in split mode, the global job table the K2b kernel reads.
+// What the fused kernel's router needs, passed BY VALUE to the non-inlined
+// router function (no generic accesses to the kernel parameter space there)
+struct RouteArgs {
+  const __half* x;
+  __half* x_save;
+  int E, H, F;
+  int64_t theta1, theta2;
+  int th1_kind, th2_kind;
+  int rank, world, hi_enc, lo_enc;
+  hb_decision* dec;
+  JobTable jt;
+};
+
+template <bool K2B>
+__device__ __forceinline__ void fused_jobs(const RouteArgs& fp, const uint8_t* const* s_blob,
+                                           int e0, int e1,
+                                           uint8_t prec1, float gd, int nonfinite, int* s_cum13,
+                                           int* s_cum2) {
+  if ((threadIdx.x & 31) != 0) return;
+  const bool cta0 = blockIdx.x == 0;
+  hb_decision r0, r1;
+  s_cum13[0] = 0;
+  s_cum2[0] = 0;
+  if (!K2B && cta0) {
+    fp.jt.vcum13[0] = 0;
+    fp.jt.vcum2[0] = 0;
+    fp.jt.tok_slots[0] = -1;
+    fp.jt.tok_slots[1] = -1;
+  }
+  int nj = 0;
+  if (nonfinite) {
+    const float nan = __int_as_float(0x7fc00000);
+    r0 = hb_decision{0, -1, 0, HB_SKIP, HB_ENC_NONE, 0, nan};
+    r1 = hb_decision{0, -1, 1, HB_SKIP, HB_ENC_NONE, 0, nan};
+  } else {
+    const float ex = expf(-gd);
+    const float g0 = 1.f / (1.f + ex), g1 = ex * g0;
+    r0 = hb_decision{0, e0, 0, HB_HIGH, HB_ENC_NONE, 0, g0};
+    r1 = hb_decision{0, e1, 1, prec1, HB_ENC_NONE, 0, g1};
+    const bool v0 = e0 % fp.world == fp.rank;
+    const bool v1 = prec1 != HB_SKIP && e1 % fp.world == fp.rank;
+    const int enc1 = prec1 == HB_HIGH ? fp.hi_enc : fp.lo_enc;
+    const bool swap = v0 && v1 && (e1 * 2 + (prec1 == HB_HIGH ? 0 : 1)) < e0 * 2;
+    auto put = [&](int sel, int e, int enc, float g) {
+      VJobD d;
+      d.blob = s_blob[e * 4 + enc];
+      d.enc = enc;
+      d.slot0 = nj;
+      d.nslot = 1;
+      d.pad = 0;
+      fz_vj[nj] = d;
+      fz_stok[nj] = 0;
+      fz_sgate[nj] = g;
+      const int epg = epg_of_enc(enc);
+      s_cum13[nj + 1] = s_cum13[nj] + (fp.F / 16) * (fp.H / epg);
+      s_cum2[nj + 1] = s_cum2[nj] + (fp.H / 16) * (fp.F / epg);
+      if (!K2B && cta0) {
+        Job j;
+        j.blob = d.blob;
+        j.enc = enc;
+        j.expert = e;
+        j.n_tok = 1;
+        j.slot_off = nj;
+        fp.jt.jobs[nj] = j;
+        fp.jt.slot_token[nj] = 0;
+        fp.jt.slot_gate[nj] = g;
+        fp.jt.vjobs[nj] = d;
+        fp.jt.vcum13[nj + 1] = s_cum13[nj + 1];
+        fp.jt.vcum2[nj + 1] = s_cum2[nj + 1];
+        fp.jt.tok_slots[sel] = nj;
+      }
+      hb_decision& r = sel ? r1 : r0;
+      r.served_enc = (uint8_t)enc;
+      r.hit = 1;
+      ++nj;
+    };
+    if (swap) {
+      put(1, e1, enc1, g1);
+      put(0, e0, fp.hi_enc, g0);
+    } else {
+      if (v0) put(0, e0, fp.hi_enc, g0);
+      if (v1) put(1, e1, enc1, g1);
+    }
+  }
+  fz_nv = nj;
+  fz_nslot = nj;
+  if (!K2B && cta0) {
+    fp.jt.hdr[0] = nj;
+    fp.jt.hdr[1] = nj;
+    fp.jt.hdr[2] = nj;
+  }
+  if (cta0) {
+    fp.dec[0] = r0;
+    fp.dec[1] = r1;
+  }
+}
+
 __device__ __forceinline__ void h2f8(const uint4& v, float (&f)[8]) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -1119,78 +1317,56 @@ __device__ __forceinline__ void h2f8(const uint4& v, float (&f)[8]) {
   }
 }
 
-__global__ void __launch_bounds__(kGemvWarps * 32, 1)
-fused_decode_kernel(const __grid_constant__ FusedParams fp) {
-  const GemvParams& p = fp.g;
-  __shared__ __align__(8) uint64_t s_wbar, s_bar13, s_bar2;
-  __shared__ int s_cum13[kFusedMaxV + 1], s_cum2[kFusedMaxV + 1];
-  __shared__ uint2 s_meta[kGemvWarps][16];
-  __shared__ FeedConst s_fk13, s_fk2;
-  __shared__ int s_subb[kGemvCTAs + 1];
-  __shared__ float s_subc[kGemvCTAs + 1];
-  __shared__ int s_subvh[kGemvCTAs];
-  __shared__ int s_nsub, s_nsub13;
-  __shared__ int s_ok, s_warps_done, s_released;
+// Steps 2-3 of the fused kernel (route the token, decide, build the job
+// table).  Returns the non-finite flag.
+template <bool K2B>
+__device__ __noinline__ int fused_route(const RouteArgs fp, int* s_cum13, int* s_cum2, int* s_ok,
+                                       uint32_t wbar, unsigned long long* rec) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int E = fp.E, H = p.H, n8 = H / 8;
+  const int E = fp.E, H = fp.H, n8 = H / 8;
   uint8_t* dyn = gemv_smem;
-  double* red = reinterpret_cast<double*>(dyn + kFusedScratch);          // [12][8][2]
-  const uint8_t** s_blob = reinterpret_cast<const uint8_t**>(dyn + kFusedScratch + 2048);  // [E][4]
-  u64* xpart = reinterpret_cast<u64*>(dyn + kFusedScratch + 4096);       // [12][64][3] (exact fallback)
-  i128* s_Lx = reinterpret_cast<i128*>(dyn + kFusedScratch + 4096 + 12 * 64 * 24);   // [64]
-  double* s_L = reinterpret_cast<double*>(dyn + kFusedScratch + 4096 + 12 * 64 * 24 + 1024);  // [64]
-  double* s_A = s_L + 64;                                                               // [64]
-
-  // ---- 1. before waiting on the previous kernel: router rows (static) into
-  // shared memory with bulk copies, blob table of the layer
-  const uint32_t wbar = smem_u32(&s_wbar);
-  if (tid == 0) {
-    mbar_init(wbar, 1);
-    mbar_init(smem_u32(&s_bar13), blockDim.x);
-    mbar_init(smem_u32(&s_bar2), blockDim.x);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t total = (uint32_t)E * H * 2;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(wbar), "r"(total) : "memory");
-    for (uint32_t off = 0; off < total; off += 16384) {
-      const uint32_t len = total - off < 16384 ? total - off : 16384;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-          :: "r"(smem_u32(dyn) + off), "l"(reinterpret_cast<const char*>(fp.wg) + off), "r"(len),
-             "r"(wbar) : "memory");
-    }
-  }
-  for (int i = tid; i < 4 * E; i += blockDim.x) s_blob[i] = fp.blob_table[i];
-  if (tid == 0) { s_warps_done = 0; s_released = 0; }
-  __syncthreads();
-  pdl_wait();                                  // x (and y, the sums) belong to earlier work
-  pdl_trigger();
-  unsigned long long* rec = nullptr;
-  if (fp.stamps) {
-    const unsigned idx = __ldcg(fp.fwd_idx);
-    if (idx < (unsigned)fp.stamp_cap) rec = fp.stamps + (size_t)idx * 8;
-    if (rec && tid == 0) atomicMax(rec + 0, ~gtimer_ns());
-  }
-
-  // ---- 2. route the token (B = 1): x chunks of this thread, in registers
+  double* red = reinterpret_cast<double*>(dyn + kFusedScratch);          // [12 warps][64] partial logits
+  float* s_xq = reinterpret_cast<float*>(dyn + kFusedScratch + 12 * 64 * 8);              // [12] sum x^2
+  float* s_wn = s_xq + 16;                                                                // [64] ||W_e||_2
+  const uint8_t** s_blob = reinterpret_cast<const uint8_t**>(dyn + kFusedScratch + 8192);  // [E][4]
+  u64* xpart = reinterpret_cast<u64*>(dyn + kFusedScratch + 12288);                       // [12][64][3]
+  i128* s_Lx = reinterpret_cast<i128*>(dyn + kFusedScratch + 12288 + 12 * 64 * 24);       // [64]
+  double* s_Lf = reinterpret_cast<double*>(dyn + kFusedScratch + 12288 + 12 * 64 * 24 + 1024);  // [64]
+  double* s_ep = s_Lf + 64;                                                                     // [64]
+  // ---- 2. route the token (B = 1).  x chunks of this thread in registers;
+  // CTA 0 keeps a copy for the lazy exact logits (hb_get_logits)
   constexpr int kXC = 3;                       // H <= 9216
   uint4 xr[kXC];
   float xf[kXC][8];
   bool bad = false;
+  float xq = 0.f;
 #pragma unroll
   for (int i = 0; i < kXC; ++i) {
     const int c = tid + i * kGemvWarps * 32;
-    xr[i] = c < n8 ? __ldcg(reinterpret_cast<const uint4*>(p.x_raw) + c) : make_uint4(0, 0, 0, 0);
+    xr[i] = c < n8 ? __ldcg(reinterpret_cast<const uint4*>(fp.x) + c) : make_uint4(0, 0, 0, 0);
+    if (blockIdx.x == 0 && c < n8 && fp.x_save) reinterpret_cast<uint4*>(fp.x_save)[c] = xr[i];
     h2f8(xr[i], xf[i]);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) bad |= !isfinite(xf[i][j]);
+    for (int j = 0; j < 8; ++j) {
+      bad |= !isfinite(xf[i][j]);
+      xq = fmaf(xf[i][j], xf[i][j], xq);
+    }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) xq += __shfl_xor_sync(0xffffffffu, xq, o);
+  if (lane == 0) s_xq[warp] = xq;
   const int nonfinite = __syncthreads_or(bad);
   mbar_wait(wbar, 0);                          // router rows landed
+  if (rec && tid == 0) atomicMax(rec + 5, gtimer_ns());
+  // filtered logits: per thread an fp32 FFMA chain over its <= 24 products
+  // (fp16 x fp16 products are exact in fp32), warp sums in fp32 (5 levels),
+  // the 12 warp partials summed in fp64 by warp 0 in a fixed order (every CTA
+  // performs the same operations, so every CTA gets bit-identical values)
   const uint4* w4 = reinterpret_cast<const uint4*>(dyn);
   for (int e0 = 0; e0 < E; e0 += 8) {
-    double acc[8], ab[8];
+    float acc[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) { acc[j] = 0.0; ab[j] = 0.0; }
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
 #pragma unroll
     for (int i = 0; i < kXC; ++i) {
       const int c = tid + i * kGemvWarps * 32;
@@ -1200,76 +1376,92 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
         if (e0 + j >= E) break;
         float wf[8];
         h2f8(w4[(size_t)(e0 + j) * n8 + c], wf);
-        float s = 0.f, a = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          s = fmaf(wf[q], xf[i][q], s);
-          a = fmaf(fabsf(wf[q]), fabsf(xf[i][q]), a);
-        }
-        acc[j] += (double)s;
-        ab[j] += (double)a;
+        for (int q = 0; q < 8; ++q) acc[j] = fmaf(wf[q], xf[i][q], acc[j]);
       }
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
+      float d = acc[j];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-        ab[j] += __shfl_xor_sync(0xffffffffu, ab[j], o);
-      }
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      if (lane == 0 && e0 + j < E) red[warp * 64 + e0 + j] = (double)d;
     }
-    if (lane == 0)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) { red[(warp * 8 + j) * 2] = acc[j]; red[(warp * 8 + j) * 2 + 1] = ab[j]; }
-    __syncthreads();
-    if (tid < 8 && e0 + tid < E) {
-      double l = 0.0, a = 0.0;
-      for (int w = 0; w < kGemvWarps; ++w) { l += red[(w * 8 + tid) * 2]; a += red[(w * 8 + tid) * 2 + 1]; }
-      s_L[e0 + tid] = l;
-      s_A[e0 + tid] = a;
-    }
-    __syncthreads();
   }
-  // top-2 by (L desc, index asc) and the certainty of every comparison
-  int e0 = -1, e1 = -1;
-  if (warp == 0 && !nonfinite) {
-    int rk[2] = {64, 64};
+  __syncthreads();
+  if (rec && tid == 0) atomicMax(rec + 6, gtimer_ns());
+  // ---- 3. warp 0: top-2 by (L desc, index asc), the certainty of every
+  // comparison, decisions, gates and (lanes 0/1) the job table
+  if (warp == 0) {
+    // lane l handles experts l and l + 32; the logits go through shared
+    // memory (broadcast reads) for the ranking
+    double xs = 0.0;
+    for (int w = 0; w < kGemvWarps; ++w) xs += (double)s_xq[w];
+    // Cauchy-Schwarz: sum |w_h x_h| <= ||w_e|| ||x||; ||x|| rounded up (the
+    // fp32 squares carry a relative error < 1e-5).  Error of a logit: the fp32
+    // chains (<= 24 products, gamma_23) and warp trees (gamma_5) plus the
+    // fp64 sum over warps: <= 29.1 * 2^-24 * sum|p| < 1.74e-6 * sum|p|, so
+    // 2.2e-6 * ||w_e|| ||x|| bounds it
+    const double xn = (double)sqrtf((float)xs * 1.00002f) * 1.000001;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = lane + 32 * h;
       if (e < E) {
-        const double v = s_L[e];
-        int r = 0;
-        for (int f = 0; f < E; ++f) { const double o = s_L[f]; r += (o > v) || (o == v && f < e); }
-        rk[h] = r;
+        double l = 0.0;
+#pragma unroll
+        for (int w = 0; w < kGemvWarps; ++w) l += red[w * 64 + e];
+        s_Lf[e] = l;
+        s_ep[e] = 2.2e-6 * (double)s_wn[e] * xn;
       }
     }
-    const unsigned m0 = __ballot_sync(0xffffffffu, rk[0] == 0), m0b = __ballot_sync(0xffffffffu, rk[1] == 0);
-    const unsigned m1 = __ballot_sync(0xffffffffu, rk[0] == 1), m1b = __ballot_sync(0xffffffffu, rk[1] == 1);
-    e0 = m0 ? __ffs(m0) - 1 : 32 + __ffs(m0b) - 1;
-    e1 = m1 ? __ffs(m1) - 1 : 32 + __ffs(m1b) - 1;
+    __syncwarp();
+    if (rec && lane == 0) atomicMax(rec + 10, gtimer_ns());
+    int rk[2] = {64, 64};
     double rest = -1e300;                      // max over ranks >= 2 of L + eps
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = lane + 32 * h;
-      if (e < E && rk[h] >= 2) rest = fmax(rest, s_L[e] + kEpsRel * s_A[e]);
+      if (e < E) {
+        const double v = s_Lf[e];
+        int r = 0;
+        for (int f = 0; f < E; ++f) {
+          const double o = s_Lf[f];
+          r += (o > v) || (o == v && f < e);
+        }
+        rk[h] = r;
+        if (r >= 2) rest = fmax(rest, v + s_ep[e]);
+      }
     }
+    const unsigned m0 = __ballot_sync(0xffffffffu, rk[0] == 0), m0b = __ballot_sync(0xffffffffu, rk[1] == 0);
+    const unsigned m1 = __ballot_sync(0xffffffffu, rk[0] == 1), m1b = __ballot_sync(0xffffffffu, rk[1] == 1);
+    const int e0 = m0 ? __ffs(m0) - 1 : 32 + __ffs(m0b) - 1;
+    const int e1 = m1 ? __ffs(m1) - 1 : 32 + __ffs(m1b) - 1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rest = fmax(rest, __shfl_xor_sync(0xffffffffu, rest, o));
-    if (lane == 0) {
-      const double L0 = s_L[e0], L1 = s_L[e1];
-      const double ep0 = kEpsRel * s_A[e0], ep1 = kEpsRel * s_A[e1];
-      const double G = L0 - L1, m = ep0 + ep1 + 1e-12 * (1.0 + fabs(L0) + fabs(L1));
-      bool ok = (L0 - ep0 > L1 + ep1) && (L1 - ep1 > rest);
-      if (fp.th1_kind == 0) ok = ok && fabs(G - (double)fp.theta1 * 0x1p-48) > m;
-      if (fp.th2_kind == 0) ok = ok && fabs(G - (double)fp.theta2 * 0x1p-48) > m;
-      s_ok = ok;
+    if (rec && lane == 0) atomicMax(rec + 11, gtimer_ns());
+    const double L0 = s_Lf[e0], L1 = s_Lf[e1], ep0 = s_ep[e0], ep1 = s_ep[e1];
+    const double G = L0 - L1, m = ep0 + ep1 + 1e-12 * (1.0 + fabs(L0) + fabs(L1));
+    bool ok = !nonfinite && (L0 - ep0 > L1 + ep1) && (L1 - ep1 > rest);
+    if (fp.th1_kind == 0) ok = ok && fabs(G - (double)fp.theta1 * 0x1p-48) > m;
+    if (fp.th2_kind == 0) ok = ok && fabs(G - (double)fp.theta2 * 0x1p-48) > m;
+    uint8_t prec1 = (fp.th1_kind > 0 || (fp.th1_kind == 0 && G <= (double)fp.theta1 * 0x1p-48)) ? HB_HIGH
+                  : (fp.th2_kind > 0 || (fp.th2_kind == 0 && G <= (double)fp.theta2 * 0x1p-48)) ? HB_LOW
+                                                                                                 : HB_SKIP;
+    float gd = (float)G;
+    if (rec && lane == 0) {
+      atomicMax(rec + 12, gtimer_ns());
+      if (!(ok || nonfinite) && blockIdx.x == 0) atomicAdd(rec + 14, 1ull);   // exact fallbacks
     }
+    if (ok || nonfinite) {
+      fused_jobs<K2B>(fp, s_blob, e0, e1, prec1, gd, nonfinite, s_cum13, s_cum2);
+      if (lane == 0) (*s_ok) = 1;
+    } else if (lane == 0) {
+      (*s_ok) = 0;
+    }
+    if (rec && lane == 0) atomicMax(rec + 13, gtimer_ns());
   }
   __syncthreads();
-  uint8_t prec1 = HB_HIGH;
-  float g0 = 0.f, g1 = 0.f;
-  if (!nonfinite && !s_ok) {
+  if (!(*s_ok)) {
     // ---- exact fallback: integer logits (every CTA takes this branch alike)
     for (int e = 0; e < E; ++e) {
       u64 lo = 0, mid = 0, hi = 0;
@@ -1320,93 +1512,155 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
       }
       const unsigned m0 = __ballot_sync(0xffffffffu, rk[0] == 0), m0b = __ballot_sync(0xffffffffu, rk[1] == 0);
       const unsigned m1 = __ballot_sync(0xffffffffu, rk[0] == 1), m1b = __ballot_sync(0xffffffffu, rk[1] == 1);
-      e0 = m0 ? __ffs(m0) - 1 : 32 + __ffs(m0b) - 1;
-      e1 = m1 ? __ffs(m1) - 1 : 32 + __ffs(m1b) - 1;
+      const int e0 = m0 ? __ffs(m0) - 1 : 32 + __ffs(m0b) - 1;
+      const int e1 = m1 ? __ffs(m1) - 1 : 32 + __ffs(m1b) - 1;
       const i128 G = s_Lx[e0] - s_Lx[e1];      // >= 0
-      prec1 = gap_le(G, fp.th1_kind, fp.theta1) ? HB_HIGH
-            : gap_le(G, fp.th2_kind, fp.theta2) ? HB_LOW : HB_SKIP;
-      const float d = G >= ((i128)1 << 62) ? 1e30f : (float)(long long)G * 0x1p-48f;
-      const float ex = expf(-d);
-      g0 = 1.f / (1.f + ex);
-      g1 = ex * g0;
+      const uint8_t prec1 = gap_le(G, fp.th1_kind, fp.theta1) ? HB_HIGH
+                          : gap_le(G, fp.th2_kind, fp.theta2) ? HB_LOW : HB_SKIP;
+      const float gd = G >= ((i128)1 << 62) ? 1e30f : (float)(long long)G * 0x1p-48f;
+      fused_jobs<K2B>(fp, s_blob, e0, e1, prec1, gd, 0, s_cum13, s_cum2);
     }
-  } else if (warp == 0 && !nonfinite) {
-    const double G = s_L[e0] - s_L[e1];
-    prec1 = (fp.th1_kind > 0 || (fp.th1_kind == 0 && G <= (double)fp.theta1 * 0x1p-48)) ? HB_HIGH
-          : (fp.th2_kind > 0 || (fp.th2_kind == 0 && G <= (double)fp.theta2 * 0x1p-48)) ? HB_LOW : HB_SKIP;
-    const float d = (float)G;
-    const float ex = expf(-d);
-    g0 = 1.f / (1.f + ex);
-    g1 = ex * g0;
+    __syncthreads();
   }
-  // ---- 3. decision records and the job table (warp 0, lane 0)
+  return nonfinite;
+}
+
+template <bool K2B>
+__global__ void __launch_bounds__(kGemvWarps * 32, 1)
+fused_decode_kernel(const __grid_constant__ FusedParams fp) {
+  const GemvParams& p = fp.g;
+  __shared__ __align__(8) uint64_t s_wbar, s_bar13, s_bar2;
+  __shared__ int s_cum13[kFusedMaxV + 1], s_cum2[kFusedMaxV + 1];
+  __shared__ uint2 s_meta[kGemvWarps][16];
+  __shared__ FeedConst s_fk13, s_fk2;
+  __shared__ int s_subb[kGemvCTAs + 1];
+  __shared__ float s_subc[kGemvCTAs + 1];
+  __shared__ int s_subvh[kGemvCTAs];
+  __shared__ int s_nsub, s_nsub13;
+  __shared__ int s_ok, s_warps_done, s_released;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int E = fp.E, H = p.H, n8 = H / 8;
+  uint8_t* dyn = gemv_smem;
+  // router scratch above the router rows (W_g takes E*H*2 <= kFusedScratch)
+  double* red = reinterpret_cast<double*>(dyn + kFusedScratch);          // [12 warps][64] partial logits
+  float* s_xq = reinterpret_cast<float*>(dyn + kFusedScratch + 12 * 64 * 8);              // [12] sum x^2
+  float* s_wn = s_xq + 16;                                                                // [64] ||W_e||_2
+  const uint8_t** s_blob = reinterpret_cast<const uint8_t**>(dyn + kFusedScratch + 8192);  // [E][4]
+  u64* xpart = reinterpret_cast<u64*>(dyn + kFusedScratch + 12288);                       // [12][64][3]
+  i128* s_Lx = reinterpret_cast<i128*>(dyn + kFusedScratch + 12288 + 12 * 64 * 24);       // [64]
+  double* s_Lf = reinterpret_cast<double*>(dyn + kFusedScratch + 12288 + 12 * 64 * 24 + 1024);  // [64]
+  double* s_ep = s_Lf + 64;                                                                     // [64]
+
+  // ---- 1. before waiting on the previous kernel: router rows (static) into
+  // shared memory with bulk copies, blob table and row norms of the layer
+  const uint32_t wbar = smem_u32(&s_wbar);
   if (tid == 0) {
-    hb_decision r[2];
-    int nj = 0;
-    if (nonfinite) {
-      for (int i = 0; i < 2; ++i) {
-        r[i].token = 0; r[i].expert = -1; r[i].sel_rank = (uint8_t)i; r[i].prec = HB_SKIP;
-        r[i].served_enc = HB_ENC_NONE; r[i].hit = 0; r[i].gate = __int_as_float(0x7fc00000);
-      }
-    } else {
-      const int ex[2] = {e0, e1};
-      const uint8_t pr[2] = {HB_HIGH, prec1};
-      const float gt[2] = {g0, g1};
-      int key[2];
-      for (int i = 0; i < 2; ++i) {
-        r[i].token = 0; r[i].expert = ex[i]; r[i].sel_rank = (uint8_t)i; r[i].prec = pr[i];
-        r[i].served_enc = HB_ENC_NONE; r[i].hit = 0; r[i].gate = gt[i];
-        key[i] = (pr[i] == HB_SKIP || ex[i] % fp.world != fp.rank) ? -1 : ex[i] * 2 + (pr[i] == HB_HIGH ? 0 : 1);
-      }
-      // jobs by key (expert, then High before Low), one slot each
-      const int order[2] = {key[1] >= 0 && (key[0] < 0 || key[1] < key[0]) ? 1 : 0,
-                            key[1] >= 0 && (key[0] < 0 || key[1] < key[0]) ? 0 : 1};
-      Job jobs[2];
-      for (int o = 0; o < 2; ++o) {
-        const int i = order[o];
-        if (key[i] < 0) continue;
-        const int enc = (key[i] & 1) ? fp.lo_enc : fp.hi_enc;
-        jobs[nj].blob = s_blob[ex[i] * 4 + enc];
-        jobs[nj].enc = enc;
-        jobs[nj].expert = ex[i];
-        jobs[nj].n_tok = 1;
-        jobs[nj].slot_off = nj;
-        fz_stok[nj] = 0;
-        fz_sgate[nj] = gt[i];
-        r[i].served_enc = (uint8_t)enc;
-        r[i].hit = 1;
-        ++nj;
-      }
-      long long c13[kFusedMaxV + 1], c2[kFusedMaxV + 1];
-      const int nv = build_vjobs(jobs, nj, H, p.F, fz_vj, c13, c2);
-      for (int v = 0; v <= nv; ++v) { s_cum13[v] = (int)c13[v]; s_cum2[v] = (int)c2[v]; }
+    mbar_init(wbar, 1);
+    mbar_init(smem_u32(&s_bar13), blockDim.x);
+    mbar_init(smem_u32(&s_bar2), blockDim.x);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t total = (uint32_t)E * H * 2;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(wbar), "r"(total) : "memory");
+    for (uint32_t off = 0; off < total; off += 16384) {
+      const uint32_t len = total - off < 16384 ? total - off : 16384;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          :: "r"(smem_u32(dyn) + off), "l"(reinterpret_cast<const char*>(fp.wg) + off), "r"(len),
+             "r"(wbar) : "memory");
     }
-    fz_nv = nj;                                 // B = 1: one vjob per job
-    fz_nslot = nj;
-    if (blockIdx.x == 0) { fp.dec[0] = r[0]; fp.dec[1] = r[1]; }
   }
-  // CTA 0 keeps x for the lazy exact logits (hb_get_logits)
-  if (blockIdx.x == 0 && fp.x_save)
-    for (int c = tid; c < n8; c += blockDim.x)
-      reinterpret_cast<uint4*>(fp.x_save)[c] = __ldcg(reinterpret_cast<const uint4*>(p.x_raw) + c);
+  for (int i = tid; i < 4 * E; i += blockDim.x) s_blob[i] = fp.blob_table[i];
+  for (int i = tid; i < E; i += blockDim.x) s_wn[i] = fp.wnorm[i];
+  if (tid == 0) { s_warps_done = 0; s_released = 0; }
+  __syncthreads();
+  pdl_wait();                                  // x (and y, the sums) belong to earlier work
+  if (K2B) pdl_trigger();
+  unsigned long long* rec = nullptr;
+  if (fp.stamps) {
+    const unsigned idx = __ldcg(fp.fwd_idx);
+    if (idx < (unsigned)fp.stamp_cap) rec = fp.stamps + (size_t)idx * kStampStride;
+    if (rec && tid == 0) atomicMax(rec + 0, ~gtimer_ns());
+  }
+
+  const RouteArgs ra{p.x_raw, fp.x_save, fp.E, p.H, p.F, fp.theta1, fp.theta2, fp.th1_kind,
+                     fp.th2_kind, fp.rank, fp.world, fp.hi_enc, fp.lo_enc, fp.dec, p.jt};
+  const int nonfinite = fused_route<K2B>(ra, s_cum13, s_cum2, &s_ok, wbar, rec);
+  const int nonfinite_tok = nonfinite;
+  if (rec && tid == 0) atomicMax(rec + 7, gtimer_ns());
+
   // y row: 0 (the expert kernels add into it), NaN for a non-finite input
   {
-    const float yv = nonfinite ? __int_as_float(0x7fc00000) : 0.f;
+    const float yv = nonfinite_tok ? __int_as_float(0x7fc00000) : 0.f;
     for (int i = blockIdx.x * blockDim.x + tid; i < H; i += gridDim.x * blockDim.x) p.y[i] = yv;
     // the other K2a-sum buffer, for the next forward (not touched by this one)
     for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < fp.zero_n;
          i += (long long)gridDim.x * blockDim.x)
       fp.zero_other[i] = 0.f;
   }
+  // split mode: CTA 0 wrote the global job table; it becomes visible before
+  // this CTA's trigger (the K2b kernel launches after every CTA triggered)
+  if (!K2B && blockIdx.x == 0 && tid == 0) __threadfence();
   __syncthreads();
+  if (!K2B) pdl_trigger();
   if (tid == 0) fz_fs = FusedSync{fp.gbar, fp.gbar + 1, &s_warps_done, &s_released, rec};
   if (rec && tid == 0) atomicMax(rec + 1, gtimer_ns());
+  if (!K2B && fp.router_only) {
+    // router kernel (one CTA): the pair-permuted x and its block sums for the
+    // K2a kernel that follows (stage_share_xperm reads them)
+    const int nb = H / 32;
+    for (int i = tid; i < nb; i += blockDim.x) {
+      const uint4* src = reinterpret_cast<const uint4*>(p.x_raw + (size_t)i * 32);
+      uint32_t v[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 t = __ldcg(src + q);
+        v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        sum += __half2float(__ushort_as_half((unsigned short)(v[e >> 1] >> (16 * (e & 1)))));
+      const_cast<float*>(p.xsum)[i] = sum;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        uint32_t q[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int e0 = 8 * t + c, e1 = e0 + 4;
+          q[c] = ((v[e0 >> 1] >> (16 * (e0 & 1))) & 0xFFFF) | (((v[e1 >> 1] >> (16 * (e1 & 1))) & 0xFFFF) << 16);
+        }
+        const_cast<uint4*>(p.x_perm)[i * 4 + t] = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+    }
+    if (fp.stamps) {
+      __syncthreads();
+      if (tid == 0 && rec) atomicMax(rec + 2, gtimer_ns());   // router kernel end
+    }
+    return;
+  }
+  if (!K2B) {
+    // split mode: K2a only; hfin and the K2b kernel follow
+    if (fz_nv > 0) {
+      Stage S;
+      PhaseCtx pc;
+      phase_setup<true, true>(p, s_cum13, &s_fk13, s_subb, s_subc, s_subvh, &s_nsub13,
+                              smem_u32(&s_bar13), false, S, pc);
+      phase_run<true, true>(p, s_cum13, &s_fk13, s_subvh, pc, S, s_meta[warp]);
+    }
+    if (fp.stamps) {
+      __syncthreads();
+      if (tid == 0 && fz_fs.stamp) atomicMax(fz_fs.stamp + 2, gtimer_ns());
+    }
+    return;
+  }
   if (fz_nv > 0) {
     // ---- 4. K2a, then K2b (the grid barrier sits in K2b's first run)
-    // K2b's setup is stashed in shared memory while K2a runs: values held in
-    // registers across the inlined K2a loops would spill inside them
+    // K2b's setup first (it has CTA-wide barriers; K2b's ring prologue is
+    // issued per warp as soon as the warp's K2a work is done), stashed in
+    // shared memory while K2a runs
     __shared__ Stage s_S2;
     __shared__ PhaseCtx s_pc2;
+    if (tid == 0) fz_p = p;
     {
       Stage S2;
       PhaseCtx pc2;
@@ -1414,18 +1668,10 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
                                smem_u32(&s_bar2), false, S2, pc2);
       if (tid == 0) { s_S2 = S2; s_pc2 = pc2; }
     }
-    {
-      Stage S13;
-      PhaseCtx pc13;
-      phase_setup<true, true>(p, s_cum13, &s_fk13, s_subb, s_subc, s_subvh, &s_nsub13,
-                              smem_u32(&s_bar13), false, S13, pc13);
-      phase_run<true, true>(p, s_cum13, &s_fk13, s_subvh, pc13, S13, s_meta[warp]);
-    }
-    {
-      const Stage S2 = s_S2;
-      const PhaseCtx pc2 = s_pc2;
-      phase_run<false, true>(p, s_cum2, &s_fk2, s_subvh, pc2, S2, s_meta[warp]);
-    }
+    __syncthreads();
+    fused_k2a(fz_p, s_cum13, &s_fk13, s_subb, s_subc, s_subvh, &s_nsub13, smem_u32(&s_bar13),
+              s_meta[warp]);
+    fused_k2b(fz_p, s_cum2, &s_fk2, s_subvh, &s_S2, &s_pc2, s_meta[warp]);
   }
   if (fp.stamps) {
     __syncthreads();
@@ -1495,11 +1741,16 @@ void launch_w13(const GemvParams& p, cudaStream_t s) {
   set_max_dyn_smem(gemv_kernel<true>, smem);
   launch_pdl(gemv_kernel<true>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
 }
-void launch_fused(const FusedParams& p, cudaStream_t s) {
+void launch_fused(const FusedParams& p, bool split, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<false>() > gemv_smem_bytes<true>() ? gemv_smem_bytes<false>()
                                                                           : gemv_smem_bytes<true>();
-  set_max_dyn_smem(fused_decode_kernel, smem);
-  launch_pdl(fused_decode_kernel, kGemvCTAs, kGemvWarps * 32, smem, s, p);
+  if (split || p.router_only) {
+    set_max_dyn_smem(fused_decode_kernel<false>, smem);
+    launch_pdl(fused_decode_kernel<false>, p.router_only ? 1 : kGemvCTAs, kGemvWarps * 32, smem, s, p);
+  } else {
+    set_max_dyn_smem(fused_decode_kernel<true>, smem);
+    launch_pdl(fused_decode_kernel<true>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
+  }
 }
 bool fused_fits(int E, int H, int F, int hi_enc, int lo_enc) {
   if (E > 64 || (long long)E * H * 2 > kFusedScratch || H / 8 > 3 * kGemvWarps * 32) return false;

@@ -10,6 +10,7 @@
 namespace hb {
 
 constexpr int kMaxTopK = 8;
+constexpr int kStampStride = 16;        // u64 per hb_stamps record
 constexpr int kMaxRouteLayers = 4;      // 1 + max lookahead p handled per launch
 constexpr int kNumSM = 148;             // B200
 #ifndef HB_GEMV_WARPS
@@ -126,6 +127,7 @@ struct RouterParams {
   int strict;                          // 0: Low served by hi_enc when the expert is touched High (R27)
   hb_decision* dec;                    // [n_route][B][k]
   long long* lbuf;                     // [n_route][B][E][2] exact logits (scratch)
+  int* rowbad;                         // [n_route][B] non-finite x flags (scratch)
   long long* logits;                   // [B][E][2] copy for route 0, or null
   uint4* x_perm;                       // [B][H/8] pair-permuted x, or null
   float* xsum;                         // [B][H/32], or null
@@ -159,6 +161,11 @@ struct GemvParams {
   float static_frac2;                  // K2b
   int chunk;                           // units per dynamic chunk
   float k2b_w[4];                      // K2b CTA split: cost of a unit per encoding (F16 = 1)
+  // in-kernel %globaltimer records (hb_stamps), legacy chain: K2a start/end,
+  // K2b h-staged/end; null = off
+  unsigned long long* stamps;
+  int stamp_cap;
+  unsigned* fwd_idx;                   // [record index, exit counter]
 };
 
 // Fused decode kernel (batch 1, top-2, resident): router + K2a + K2b in one
@@ -168,6 +175,7 @@ struct FusedParams {
   const __half* wg;                    // router rows of the layer [E][H]
   const uint8_t* const* blob_table;    // [E][4] device blob of (expert, enc)
   int E;
+  const float* wnorm;                  // [E] ||W_e||_2 rounded up (hb_set_router)
   int64_t theta1, theta2;
   int th1_kind, th2_kind;
   int rank, world, hi_enc, lo_enc;
@@ -176,11 +184,15 @@ struct FusedParams {
   float* zero_other;                   // the other sum buffer, zeroed for the next forward
   long long zero_n;
   unsigned* gbar;                      // grid barrier [count, generation] (self-resetting)
-  unsigned long long* stamps;          // profile records [cap][8] or null
+  unsigned long long* stamps;          // profile records [cap][kStampStride] or null
   int stamp_cap;
   unsigned* fwd_idx;                   // [record index, exit counter]
+  int router_only;                     // one CTA: decisions, job table, x_perm / xsum only
 };
-void launch_fused(const FusedParams& p, cudaStream_t s);
+// split = false: router + K2a + grid barrier + K2b (one kernel); true:
+// router + K2a only (writes the global job table), the caller follows with
+// launch_hfin + launch_w2
+void launch_fused(const FusedParams& p, bool split, cudaStream_t s);
 bool fused_fits(int E, int H, int F, int hi_enc, int lo_enc);
 void launch_router(const RouterParams& p, cudaStream_t s);
 // kernel launch allowing programmatic dependent launch (the kernel overlaps

@@ -94,6 +94,23 @@ __device__ void decide_sel(const RouterParams& p, const i128* L, const int* sel,
   }
 }
 
+// A token with a non-finite x element: every selection Skip, expert -1, gate
+// NaN (its y row is NaN, written by the zeroing CTAs); R28.
+__device__ void decide_nonfinite(const RouterParams& p, int b, hb_decision* out, hb_decision* out_s) {
+  for (int i = 0; i < p.k; ++i) {
+    hb_decision d;
+    d.token = b;
+    d.expert = -1;
+    d.sel_rank = (uint8_t)i;
+    d.prec = HB_SKIP;
+    d.served_enc = HB_ENC_NONE;
+    d.hit = 0;
+    d.gate = __int_as_float(0x7fc00000);
+    out[i] = d;
+    if (out_s) out_s[i] = d;
+  }
+}
+
 // O3-O6, one thread: top-k by (L desc, index asc), then decide_sel
 __device__ void decide(const RouterParams& p, const i128* L, int b, hb_decision* out,
                        hb_decision* out_s) {
@@ -196,6 +213,8 @@ struct RouterSmem {
   Job jobs[2 * 64 + 1];
   int count[2 * 64], jobid[2 * 64], fill[2 * 64];
   unsigned long long hmask;            // experts with a High selection (non-strict upgrade)
+  int bad;                             // this CTA's slice of x has a non-finite element
+  u64 bad2;                            // the same as a u64 (read by the cluster leader)
   int last;
 };
 
@@ -434,8 +453,28 @@ router_kernel(const __grid_constant__ RouterParams p) {
     asm volatile("griddepcontrol.launch_dependents;");
     const long long t0 = (long long)(blockIdx.x - nrows * C) * blockDim.x + tid;
     const long long stride = (long long)(gridDim.x - nrows * C) * blockDim.x;
+    // y rows: 0, or NaN for a token whose x has a non-finite element (R28)
+    if (p.zero_n[1] > 0) {
+      const int zc = blockIdx.x - nrows * C, nzc = gridDim.x - nrows * C;
+      const int n8 = p.H / 8;
+      for (int r = zc; r < p.B; r += nzc) {
+        const uint4* xr = reinterpret_cast<const uint4*>(p.x + (size_t)r * p.H);
+        int bad = 0;
+        for (int j = tid; j < n8; j += blockDim.x) {
+          const uint4 v = __ldcg(xr + j);
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            bad |= ((w[q] & 0x7C00u) == 0x7C00u) | ((w[q] & 0x7C000000u) == 0x7C000000u);
+        }
+        const float val = __syncthreads_or(bad) ? __int_as_float(0x7fc00000) : 0.f;
+        float4* yr = reinterpret_cast<float4*>(p.zero_buf[1] + (size_t)r * p.H);
+        for (int j = tid; j < p.H / 4; j += blockDim.x) yr[j] = make_float4(val, val, val, val);
+      }
+    }
 #pragma unroll
     for (int z = 0; z < 3; ++z) {
+      if (z == 1) continue;
       float* zb = p.zero_buf[z];
       const long long n = p.zero_n[z];
       if ((reinterpret_cast<uintptr_t>(zb) & 15) == 0) {
@@ -499,7 +538,18 @@ router_kernel(const __grid_constant__ RouterParams p) {
     }
     if (lane == 0) { sm.part[task][0] = lo; sm.part[task][1] = mid; sm.part[task][2] = hi; }
   }
-  __syncthreads();
+  {
+    int bad = 0;                               // non-finite x in this CTA's slice
+    for (int j = s0 + tid; j < s1; j += blockDim.x) {
+      const uint4 v = x4[j];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        bad |= ((w[q] & 0x7C00u) == 0x7C00u) | ((w[q] & 0x7C000000u) == 0x7C000000u);
+    }
+    bad = __syncthreads_or(bad);
+    if (tid == 0) { sm.bad = bad; sm.bad2 = (u64)bad; }
+  }
   for (int e = tid; e < p.E; e += blockDim.x) {            // CTA partial per expert
     u64 lo = 0, mid = 0, hi = 0;
     for (int q = 0; q < wpe; ++q) {
@@ -541,6 +591,11 @@ router_kernel(const __grid_constant__ RouterParams p) {
   if (C > 1) cluster_sync_all();
   else __syncthreads();
   if (crank == 0) {
+    if (C > 1 && tid == 0) {
+      int bad = 0;
+      for (int r = 0; r < C; ++r) bad |= (int)ld_dsmem_u64(&sm.bad2, r);
+      sm.bad = bad;
+    }
     for (int e = tid; e < p.E; e += blockDim.x) {
       u64 lo = 0, mid = 0, hi = 0;
       for (int r = 0; r < C; ++r) {
@@ -569,7 +624,9 @@ router_kernel(const __grid_constant__ RouterParams p) {
   // ---- single (route layer, token): decide and build the jobs right here
   if (nrows == 1) {
     if (warp == 0) {
-      if (p.k == 2 && p.E <= 32) {
+      if (sm.bad) {
+        if (lane == 0) decide_nonfinite(p, b, p.dec, sm.dec);
+      } else if (p.k == 2 && p.E <= 32) {
         decide_k2_warp(p, sm.L, b, p.dec, sm.dec);
       } else {
         int sel[kMaxTopK];
@@ -589,6 +646,7 @@ router_kernel(const __grid_constant__ RouterParams p) {
   }
 
   // ---- several rows: publish the logits; the last leader decides for all
+  if (tid == 0) p.rowbad[(size_t)rl * p.B + b] = sm.bad;
   for (int e = tid; e < p.E; e += blockDim.x) {
     const size_t idx = ((size_t)rl * p.B + b) * p.E + e;
     p.lbuf[2 * idx] = (long long)(u64)sm.L[e];
@@ -608,6 +666,11 @@ router_kernel(const __grid_constant__ RouterParams p) {
     const int r = i / p.B, bb = i % p.B;
     i128 L[64];
     const size_t base = ((size_t)r * p.B + bb) * p.E;
+    if (__ldcg(p.rowbad + (size_t)r * p.B + bb)) {
+      decide_nonfinite(p, bb, p.dec + ((size_t)r * p.B + bb) * p.k,
+                       r == 0 && dec_smem ? sm.dec + (size_t)bb * p.k : nullptr);
+      continue;
+    }
     for (int e = 0; e < p.E; ++e) L[e] = load_logit(p.lbuf, base + e);
     decide(p, L, bb, p.dec + ((size_t)r * p.B + bb) * p.k,
            r == 0 && dec_smem ? sm.dec + (size_t)bb * p.k : nullptr);

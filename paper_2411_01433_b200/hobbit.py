@@ -169,10 +169,11 @@ class Context:
         self._check(lib.hb_stamps(self._h, max_forwards))
 
     def stamps_read(self, cap: int = 1 << 16):
-        """[(start, decided, k2a_done, released, end)] ns per recorded fused forward."""
-        buf = (C.c_uint64 * (5 * cap))()
+        """[(start, decided, k2a_done, released, end, wg_landed, logits, jobs, h_last, h_first)]
+        ns per recorded forward (hb_stamps_read)."""
+        buf = (C.c_uint64 * (15 * cap))()
         n = self._check(lib.hb_stamps_read(self._h, buf, cap))
-        return [tuple(buf[5 * i:5 * i + 5]) for i in range(n)]
+        return [tuple(buf[15 * i:15 * i + 15]) for i in range(n)]
 
     def nccl_init(self, group=None):
         """EP exchange inside the library (A10): rank 0 makes an NCCL unique id,

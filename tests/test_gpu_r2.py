@@ -273,3 +273,59 @@ def test_ep_two_processes_through_library(world, tmp_path):
         off += ref.size
         for b in range(ref.shape[0]):
             assert rel_err(y[b], ref[b])[0] <= TOL
+
+
+# ------------------------------------------------------------ non-finite inputs
+@pytest.mark.parametrize("mode", ["legacy", "fused"])
+@pytest.mark.parametrize("B,batched_min", [(1, 0), (3, 0), (12, 4)], ids=["B1", "B3", "K3-B12"])
+def test_nonfinite_input_documented_behaviour(mode, B, batched_min, monkeypatch):
+    """DESIGN.md R28: a token whose x holds an inf/nan gets Skip decisions
+    (expert -1, gate NaN) and a NaN output row; every other token is
+    unaffected (equal to the oracle)."""
+    monkeypatch.setenv("HB_DECODE", mode)
+    sh = sg.TINY
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=16, batched_min=batched_min)
+    store = OracleStore(sh)
+    x16 = sg.hidden_states(sh, 47, 0, batch=B)
+    bad = B // 2
+    x16[bad, 5] = np.float16(np.inf) if B % 2 else np.float16(np.nan)
+    y = _run(ctx, 0, x16)
+    dec = ctx.decisions(B)
+    assert all(d.expert == -1 and d.prec == rt.SKIP and np.isnan(d.gate) for d in dec[2 * bad:2 * bad + 2])
+    assert np.all(np.isnan(y[bad]))
+    good = [b for b in range(B) if b != bad]
+    if good:
+        ref, routes = om.moe_layer(x16[good], sg.router_weights(sh, 0), store, 0, 2, 0.6, 0.9,
+                                   fm.F16, fm.Q4)
+        for i, b in enumerate(good):
+            assert [d.expert for d in dec[2 * b:2 * b + 2]] == routes[i].experts
+            assert rel_err(y[b], ref[i])[0] <= TOL
+
+
+# ------------------------------------------------------------ decode variants
+@pytest.mark.parametrize("mode", ["fused", "split", "router"])
+def test_decode_variants_match_oracle(mode, monkeypatch):
+    """The alternative batch-1 decode chains (HB_DECODE):
+    decisions, logits and y equal the oracle's on the tiny layers and on one
+    full-size Mixtral F16/Q4 layer."""
+    monkeypatch.setenv("HB_DECODE", mode)
+    sh = sg.TINY
+    ctx = _resident(sh, [0, 1], fm.F16, fm.Q4, max_batch=1)
+    store = OracleStore(sh)
+    for t in range(4):
+        for l in range(2):
+            x16 = sg.hidden_states(sh, 48 + t, l)
+            y = _run(ctx, l, x16)
+            ref, routes = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9,
+                                       fm.F16, fm.Q4)
+            _check_routes(ctx, routes, 1, 2)
+            assert ctx.logits(1) == rt.exact_logits(x16, sg.router_weights(sh, l))
+            assert rel_err(y[0], ref[0])[0] <= 1e-4
+    big = sg.MoEShape("mixtral", 32, 8, 2, 4096, 14336, 1.5)
+    ctx = _resident(big, [9], fm.F16, fm.Q4, max_batch=1)
+    store = OracleStore(big)
+    x16 = sg.hidden_states(big, 49, 9)
+    y = _run(ctx, 9, x16)
+    ref, routes = om.moe_layer(x16, sg.router_weights(big, 9), store, 9, 2, 0.6, 0.9, fm.F16, fm.Q4)
+    _check_routes(ctx, routes, 1, 2)
+    assert rel_err(y[0], ref[0])[0] <= 1e-4
