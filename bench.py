@@ -51,24 +51,21 @@ def peaks():
 
 
 def ncu_traffic():
-    """DRAM bytes (read + write) of one K2a + one K2b launch from the newest committed
-    `ncu --set full` summary under profiles/ (tools/ncu_summary.py), or None."""
+    """DRAM bytes (read + write) of one K2a + K2b launch pair of one known
+    forward, with that forward's own algorithmic bytes, from the newest
+    committed profiles/*_k2pair.json (tools/ncu_k2pair.py); {} if none."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k2pair.json")))
     if not files:
-        return None, None
+        return {}
     try:
         with open(files[-1]) as f:
-            ks = json.load(f)["kernels"]
-        tot = {}
-        for k in ks:
-            if "gemv_kernel" in k["kernel"]:
-                tot.setdefault(k["kernel"], k["dram_read"] + k.get("dram_write", 0.0))
-        if len(tot) != 2:
-            return None, None
-        return int(sum(tot.values())), os.path.relpath(files[-1], ROOT)
+            d = json.load(f)
+        return {"traffic": int(d["dram_bytes"]), "traffic_alg_bytes": int(d["alg_bytes"]),
+                "traffic_over_alg": round(d["dram_bytes"] / d["alg_bytes"], 4),
+                "traffic_source": os.path.relpath(files[-1], ROOT)}
     except Exception:
-        return None, None
+        return {}
 
 
 # ------------------------------------------------------------ clocks
@@ -163,12 +160,14 @@ def run_ours(args):
     import torch.distributed as dist
 
     import synthgen as sg
-    from oracle import formats as fm  # noqa: F401  (enc constants only; cpu_baseline below)
     from paper_2411_01433_b200 import hobbit as h
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun "
+                         f"(python -m torch.distributed.run --nproc-per-node N bench.py --gpus N)")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -230,9 +229,13 @@ def run_ours(args):
     w13b = {e: mat_bytes(e, (0, 1)) for e in (hi, lo)}
     w2b = {e: mat_bytes(e, (2,)) for e in (hi, lo)}
 
-    # ---- CUDA graphs: one per pool token (32 layers x 3 kernels each), N=1
-    use_graph = world == 1
-    graphs = []
+    # ---- CUDA graphs, one per pool token (32 layers; at N > 1 the in-library
+    # NCCL all-reduce of every layer is captured too).  A second set is
+    # captured with the in-kernel %globaltimer stamps on (hb_stamps): it is
+    # replayed right after the timed region for the roofline, so the headline
+    # graphs carry no instrumentation.
+    use_graph = not torch_reduce
+    graphs, sgraphs = [], []
     launches_per_step = 0
     if use_graph:
         c0 = ctx.launch_count()
@@ -242,11 +245,20 @@ def run_ours(args):
                 with torch.cuda.graph(g, stream=stream):
                     step(t, stream)
                 graphs.append(g)
-        launches_per_step = (ctx.launch_count() - c0) // P
+            launches_per_step = (ctx.launch_count() - c0) // P
+            # record capacity fixed before capture (the stamped graphs keep the pointer)
+            stamp_cap = max(P, args.steps) * L
+            ctx.stamps(stamp_cap)
+            for t in range(P):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    step(t, stream)
+                sgraphs.append(g)
+            ctx.stamps(0)
 
-    def run_step(t):
+    def run_step(t, stamped=False):
         if use_graph:
-            graphs[t % P].replay()
+            (sgraphs if stamped else graphs)[t % P].replay()
         else:
             step(t, stream)
 
@@ -288,38 +300,58 @@ def run_ours(args):
     steps_tokens = [(args.warmup + k) % P for k in range(args.steps)]
     bytes_step = float(np.mean([bytes_tok[t] for t in steps_tokens]))
 
-    # ---- kernel timing for the roofline (eager, events around K2a / K2b)
-    with torch.cuda.stream(stream):
-        nprof = min(args.steps, P)
-        ctx.profile(nprof * L)
-        for t in range(nprof):
-            for l in range(L):
-                ctx.forward(l, X[t, l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
-                if world > 1:
-                    if torch_reduce:
-                        dist.all_reduce(Y[l])
-        prof = ctx.profile_read()
-        ctx.profile(0)
-    # bytes per K2a / K2b launch, from the decisions of the same tokens
-    k2a_bytes, k2b_bytes = [], []
-    with torch.cuda.stream(stream):
-        for t in range(nprof):
-            for l in range(L):
-                ctx.forward(l, X[t, l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
-                a = b = 0
-                for d in ctx.decisions(1):
-                    if d.served_enc != h.HB_ENC_NONE:
-                        a += w13b[d.served_enc]
-                        b += w2b[d.served_enc]
-                k2a_bytes.append(a + 2 * Hd + 2 * 2 * shape.ffn * 2)
-                k2b_bytes.append(b + 2 * 2 * shape.ffn * 2 + 4 * Hd)
-    k2a_ms = sum(p[0] for p in prof)
-    k2b_ms = sum(p[1] for p in prof)
-    gemv_ms = k2a_ms + k2b_ms
-    gemv_bytes = sum(k2a_bytes) + sum(k2b_bytes)
-    achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
+    # ---- roofline of the dominant kernels (K2a + K2b): the same K steps
+    # replayed from the stamped graphs; per forward the kernels' own in-kernel
+    # intervals: K2a = [first CTA past its wait, last CTA done], K2b = [first
+    # CTA with h staged, last CTA done]
+    roof = {}
+    if use_graph:
+        with torch.cuda.stream(stream):
+            ctx.stamps(stamp_cap)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e3 = torch.cuda.Event(enable_timing=True)
+            e2.record(stream)
+            for k in range(args.steps):
+                run_step(args.warmup + k, stamped=True)
+            e3.record(stream)
+            torch.cuda.synchronize()
+            rec = np.array(ctx.stamps_read(args.steps * L), dtype=np.float64)
+            ctx.stamps(0)
+        ms_stamped = e2.elapsed_time(e3) / args.steps
+        # bytes per forward of the same (token, layer) sequence, from its decisions
+        k2a_b, k2b_b = [], []
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                t = (args.warmup + k) % P
+                for l in range(L):
+                    ctx.forward(l, X[t, l].view(1, Hd), Y[l].view(1, Hd), stream=stream)
+                    a = b = ne = 0
+                    for d in ctx.decisions(1):
+                        if d.served_enc != h.HB_ENC_NONE:
+                            a += w13b[d.served_enc]
+                            b += w2b[d.served_enc]
+                            ne += 1
+                    # SURVEY 8(d) unit split over the two kernels: K2a = W1/W3 +
+                    # x + h written (4F per expert); K2b = W2 + h read + y
+                    k2a_b.append(a + 2 * Hd + 4 * shape.ffn * ne)
+                    k2b_b.append(b + 4 * shape.ffn * ne + 4 * Hd)
+        n = min(len(rec), len(k2a_b))
+        k2a_ns = rec[:n, 2] - rec[:n, 0]
+        k2b_ns = rec[:n, 4] - rec[:n, 3]
+        k2_ns = float(np.sum(k2a_ns + k2b_ns))
+        gemv_bytes = float(np.sum(k2a_b[:n]) + np.sum(k2b_b[:n]))
+        achieved = gemv_bytes / k2_ns                     # bytes/ns = GB/s
+        roof = {"achieved": round(achieved, 1),
+                "k2a_gbs": round(float(np.sum(k2a_b[:n]) / np.sum(k2a_ns)), 1),
+                "k2b_gbs": round(float(np.sum(k2b_b[:n]) / np.sum(k2b_ns)), 1),
+                "k2_share_of_step": round(k2_ns / n * L * 1e-6 / ms_stamped, 4),
+                "stamped_ms_per_step": round(ms_stamped, 4),
+                "alg_bytes_per_launch_pair": int(gemv_bytes / n),
+                "forwards": int(n),
+                "method": "in-kernel %globaltimer stamps (hb_stamps) over a graph replay of the "
+                          "timed steps; bytes from the same forwards' decisions"}
     peak, peak_kind = peaks()
-    traffic, traffic_src = ncu_traffic()
+    traffic = ncu_traffic()
 
     # ---- end to end through the public API with host buffers
     Xh = torch.empty(P, L, Hd, dtype=torch.float16, pin_memory=True)
@@ -373,15 +405,11 @@ def run_ours(args):
         "e2e": {"value": round(1000.0 / ms_e2e, 3), "unit": UNIT,
                 "h2d_bytes_per_step": L * Hd * 2, "d2h_bytes_per_step": L * Hd * 4},
         "gpu_launches": int(gpu_launches),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "frac_vs_8000_spec": round(achieved / 8000.0, 4),
-                     "traffic": traffic, "traffic_source": traffic_src,
-                     "alg_bytes_per_launch_pair": int(gemv_bytes / (nprof * L)),
-                     "kernel": "K2a+K2b dequant-GEMV (gemv_kernel<1>, gemv_kernel<0>)",
-                     "k2a_gbs": round(sum(k2a_bytes) / (k2a_ms * 1e-3) / 1e9, 1),
-                     "k2b_gbs": round(sum(k2b_bytes) / (k2b_ms * 1e-3) / 1e9, 1),
-                     "gemv_share_of_step": round(gemv_ms / nprof / ms_step, 4)},
+        "roofline": dict({"bound": "hbm", "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                          "frac": round(roof["achieved"] / peak, 4) if roof else None,
+                          "frac_vs_8000_spec": round(roof["achieved"] / 8000.0, 4) if roof else None,
+                          "kernel": "K2a+K2b dequant-GEMV (gemv_kernel<1>, gemv_kernel<0>)"},
+                         **roof, **traffic),
         "layer_gbs": round(bytes_step / (ms_step * 1e-3) / 1e9, 1),
         "bytes_per_step": int(bytes_step),
         "precision_mix": [round(v / tot_mix, 4) for v in mix],
@@ -456,9 +484,11 @@ def batched_leg(h, sg, shape, hi, lo, blobs, dev, stream, Bs=(256, 512), layers=
 
 
 # ------------------------------------------------------------ oracle timings
-def _oracle_sample(shape, n_token_layers, seed_tok=2000):
+def _oracle_sample(shape, n_token_layers, seed_tok=2000, layer=None):
     """Pre-generate blobs (untimed), then time the oracle as it stands on
-    n_token_layers (token, layer) pairs: exact router + decode + fp64 FFN."""
+    n_token_layers (token, layer) pairs: exact router + decode + fp64 FFN.
+    layer=None rotates through the layers; an int keeps one layer (its blobs
+    are then generated once for all samples)."""
     import synthgen as sg
     from oracle import formats as fm
     from oracle import moe as om
@@ -473,7 +503,7 @@ def _oracle_sample(shape, n_token_layers, seed_tok=2000):
 
     cases = []
     for i in range(n_token_layers):
-        l = i % shape.n_layers
+        l = i % shape.n_layers if layer is None else layer
         x16 = sg.hidden_states(shape, seed_tok + i, l)
         wg = sg.router_weights(shape, l)
         r = rt.route(x16, wg, 2, 0.6, 0.9)[0]
@@ -509,6 +539,12 @@ def cpu_baseline(shape, n_token_layers=2):
 
 
 def run_reference(args):
+    """The reference arm (tier rules: the oracle as it stands, on the host
+    cores).  One step = ONE token-layer of the workload (1/32 of a decode
+    token: exact router, blob decode, fp64 SwiGLU + Eq. 1), so the run is
+    --warmup + --steps token-layers of real work (~6 s each); ms_per_step is
+    that measured time and value = tokens/s = 1 / (32 * s per token-layer).
+    All steps use one layer's blobs (generated once, untimed)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -516,22 +552,23 @@ def run_reference(args):
     import synthgen as sg
     shape = sg.MIXTRAL
     t0 = time.time()
-    n = max(1, args.warmup + args.steps)
-    n = min(n, args.ref_max_steps)
-    times = _oracle_sample(shape, n)
-    timed = times[min(args.warmup, len(times) - 1):] or times
+    n = args.warmup + args.steps
+    times = _oracle_sample(shape, n, layer=0)
+    timed = times[args.warmup:]
     s_tl = float(np.mean(timed))
-    ms_step = 1000.0 * shape.n_layers * s_tl
+    ms_step = 1000.0 * s_tl
     cores = len(os.sched_getaffinity(0))
-    v = 1000.0 / ms_step
+    v = 1.0 / (shape.n_layers * s_tl)
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": UNIT,
-           "n_gpus": world, "steps": len(timed), "warmup": n - len(timed),
+           "n_gpus": world, "steps": len(timed), "warmup": args.warmup,
            "ms_per_step": round(ms_step, 1), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": WORKLOAD, "global_batch": 1},
+           "config": {"workload": WORKLOAD, "global_batch": 1,
+                      "step": "one token-layer (1/32 of a decode token) on the CPU oracle"},
            "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
-                            "sample": f"each step = 1 token-layer of the workload timed on the "
-                                      f"oracle, extrapolated x32 layers; {len(timed)} steps"},
+                            "sample": f"each step = 1 token-layer of the workload (layer 0) timed "
+                                      f"on the oracle; tokens/s = 1/(32 * s per token-layer); "
+                                      f"{len(timed)} steps"},
            "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
            "wall_s": round(time.time() - t0, 1)}
@@ -549,7 +586,6 @@ def main():
     ap.add_argument("--t1", type=float, default=0.6, help="diagnostics only (1.0/1.0 = all-High)")
     ap.add_argument("--t2", type=float, default=0.9, help="diagnostics only")
     ap.add_argument("--cpu-sample", type=int, default=2)
-    ap.add_argument("--ref-max-steps", type=int, default=12)
     ap.add_argument("--model", choices=["mixtral", "phi"], default="mixtral",
                     help="diagnostics only: the headline is mixtral")
     ap.add_argument("--pair", choices=sorted(PAIRS), default="f16q4",

@@ -1105,7 +1105,6 @@ __device__ __forceinline__ void legacy_stamp_end(const GemvParams& p) {
   const unsigned idx = __ldcg(p.fwd_idx);
   if (idx < (unsigned)p.stamp_cap) atomicMax(p.stamps + (size_t)idx * kStampStride + (W13 ? 2 : 4), gtimer_ns());
   if (!W13) {
-    __threadfence();
     if (atomicAdd(p.fwd_idx + 1, 1u) == gridDim.x - 1) {
       p.fwd_idx[1] = 0u;
       p.fwd_idx[0] += 1u;
@@ -1678,7 +1677,6 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
     if (tid == 0) {
       unsigned long long* rec_end = fz_fs.stamp;
       if (rec_end) atomicMax(rec_end + 4, gtimer_ns());
-      __threadfence();
       if (atomicAdd(fp.fwd_idx + 1, 1u) == gridDim.x - 1) {   // last CTA: next record
         fp.fwd_idx[1] = 0u;
         fp.fwd_idx[0] += 1u;

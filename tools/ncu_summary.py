@@ -74,6 +74,17 @@ def full(path):
                 except ValueError:
                     pass
         d["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:8])
+        # tensor-pipe utilisation (legacy HMMA and tcgen05 pipes): every raw
+        # metric of the capture that names the tensor pipe, as reported
+        tp = {}
+        for i, h in enumerate(hdr):
+            if ("pipe_tensor" in h or "pipe_tc" in h or "tcgen05" in h or "utc" in h.lower()) and \
+                    ("pct" in h or h.endswith(".sum") or h.endswith(".avg")):
+                try:
+                    tp[h] = float(r[i].replace(",", ""))
+                except ValueError:
+                    pass
+        d["tensor_pipe"] = tp
         res.append(d)
     return res
 
@@ -84,6 +95,8 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--full")
     ap.add_argument("--note", default="")
+    ap.add_argument("--k2pair", help="JSON from tools/ncu_k2pair.py: algorithmic bytes of the "
+                                     "captured K2a + K2b launch pair")
     a = ap.parse_args()
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
     if a.launches:
@@ -117,7 +130,23 @@ def main():
                 if "duration" in d and "dram_read" in d:
                     gbs = (d["dram_read"] + d.get("dram_write", 0)) / (d["duration"] * 1e-6) / 1e9
                     f.write(f"- DRAM GB/s over the launch: {gbs:,.1f}\n")
-                f.write(f"- top stalls (warps per issue): {d['stalls_per_issue']}\n\n")
+                f.write(f"- top stalls (warps per issue): {d['stalls_per_issue']}\n")
+                if d.get("tensor_pipe"):
+                    f.write(f"- tensor pipe: {d['tensor_pipe']}\n")
+                f.write("\n")
+        if a.k2pair:
+            with open(a.k2pair) as f:
+                alg = json.load(f)
+            pair = [d for d in res if "gemv_kernel" in d["kernel"]][:2]
+            dram = sum(d["dram_read"] + d.get("dram_write", 0.0) for d in pair)
+            dur = sum(d["duration"] for d in pair)
+            out = {"kernels": [d["kernel"] for d in pair], "dram_bytes": dram,
+                   "alg_bytes": alg["alg_bytes"], "alg_detail": alg,
+                   "duration_us_serialised": dur,
+                   "note": "one K2a + K2b launch pair of one known forward (same decisions every "
+                           "repeat), ncu --set full; DRAM bytes vs that forward's algorithmic bytes"}
+            with open(os.path.join(root, f"{a.tag}_k2pair.json"), "w") as f:
+                json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":
