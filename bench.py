@@ -305,7 +305,7 @@ def run_ours(args):
     # intervals: K2a = [first CTA past its wait, last CTA done], K2b = [first
     # CTA with h staged, last CTA done]
     roof = {}
-    if use_graph:
+    if use_graph and not args.no_roofline:
         with torch.cuda.stream(stream):
             ctx.stamps(stamp_cap)
             e2 = torch.cuda.Event(enable_timing=True)
@@ -583,6 +583,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batched", action="store_true", help="skip the K3 batched/prefill extra")
+    ap.add_argument("--no-roofline", action="store_true", help="diagnostics: skip the stamped replay")
     ap.add_argument("--t1", type=float, default=0.6, help="diagnostics only (1.0/1.0 = all-High)")
     ap.add_argument("--t2", type=float, default=0.9, help="diagnostics only")
     ap.add_argument("--cpu-sample", type=int, default=2)

@@ -107,6 +107,8 @@ struct hb_ctx {
   bool stamps_on = false;
   __half* x_save = nullptr;               // x of the last fused forward (lazy exact logits)
   bool last_fused = false;
+  bool last_filtered = false;             // last forward's router kept no exact logits
+  bool router_filtered = false;           // HB_ROUTER=filtered: batch-1 decode router kernel (diagnostic)
   bool fused_split = false;               // HB_FUSED_SPLIT=1: router+K2a kernel, then hfin + K2b
   bool fused_router = false;              // HB_FUSED_ROUTER=1: one-CTA router kernel + legacy K2a/hfin/K2b
   uint4* h_hi = nullptr;                  // h in global memory (large batches only)
@@ -418,6 +420,8 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     c->fused_ok = resident && K == 2 && mode != "legacy" && fused_fits(E, H, F, k.hi_enc, k.lo_enc);
     c->fused_split = mode == "split";
     c->fused_router = mode == "router";
+    const char* re = std::getenv("HB_ROUTER");
+    c->router_filtered = re && std::string(re) == "filtered";
   }
   cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + 2 * kGemvCTAs));
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
@@ -698,6 +702,7 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y, float* au) {
   }
   g.h_global = c->force_h_global || !fits || 2 * nv_bound > kGemvCTAs;
   g.y = (float*)y;
+  g.rowbad = c->rowbad;
   g.ctr = c->gctr;
   g.max_vjobs = c->max_vjobs;
   g.static_frac = c->static_frac;
@@ -710,18 +715,16 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y, float* au) {
   return g;
 }
 
-// The legacy GEMV chain's K2a-sum buffer: the one the previous GEMV forward
-// did not use; the router grid zeroes it and the other one (so both are
-// clean afterwards except this forward's).  Returns the buffer index.
+// The legacy GEMV chain's K2a-sum buffer: the router grid zeroes the one it
+// uses (the current buffer; the legacy chain keeps using it).  The fused
+// kernel switches to the other one, which it expects clean.
 static int legacy_au(hb_ctx* c, RouterParams& rp, int batch) {
-  const int cn = c->au_cur ^ 1;
+  const int cn = c->au_cur;
   rp.zero_buf[0] = au_buf(c, cn);
   rp.zero_n[0] = (long long)batch * c->cfg.top_k * 2 * c->cfg.ffn;
-  rp.zero_buf[2] = au_buf(c, cn ^ 1);
-  rp.zero_n[2] = c->au_dirty[cn ^ 1];
+  rp.zero_buf[2] = nullptr;
+  rp.zero_n[2] = 0;
   c->au_dirty[cn] = rp.zero_n[0];
-  c->au_dirty[cn ^ 1] = 0;
-  c->au_cur = cn;
   return cn;
 }
 
@@ -818,6 +821,8 @@ static void launch_batched(hb_ctx* c, int layer, const void* x, void* y, cudaStr
   kp.xg = c->k3_xg;
   kp.hB = c->k3_hB;
   kp.y = (float*)y;
+  kp.rowbad = c->rowbad;
+  kp.B = c->last_batch;
   kp.tab = c->k3_tab;
   kp.tmap = c->k3_tmap + (size_t)layer * c->cfg.n_experts * 24;
   kp.has_f16 = c->cfg.hi_enc == HB_F16 || c->cfg.lo_enc == HB_F16;
@@ -891,8 +896,17 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
     rp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
     const bool k3 = c->k3_ok && c->k3_min_batch > 0 && batch >= c->k3_min_batch;
     c->last_host_decisions = false;
+    // batch-1 decode: the filtered router (exact decisions, logits on demand)
+    if (batch == 1 && k.top_k == 2 && k.n_experts <= 32 && c->router_filtered) {
+      rp.filtered = 1;
+      rp.wnorm = c->wnorm + (size_t)layer * k.n_experts;
+      rp.x_save = c->x_save;
+      rp.logits = nullptr;
+    }
+    c->last_filtered = rp.filtered != 0;
     if (!k3 && batch == 1 && c->fused_ok) {
       c->last_fused = true;
+      c->last_filtered = false;
       if (int rc = launch_fused_forward(c, layer, x, y, s)) return rc;
       CUDA_TRY(c, cudaGetLastError());
       return ep_reduce(c, y, batch, s);
@@ -917,6 +931,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   if (!c->token_started) return fail(c, HB_ESTATE, "forward before hb_token_begin");
   rp.blob_table = nullptr;
   c->last_fused = false;
+  c->last_filtered = false;
   const int cn = legacy_au(c, rp, batch);
   launch_router(rp, s);
   c->launches += 1;
@@ -1029,6 +1044,7 @@ int prefetch_next_layer(hb_ctx* c, int layer, const void* x, int batch, void* st
   rp.dec = c->dec_pred;
   rp.blob_table = nullptr;
   c->last_fused = false;
+  c->last_filtered = false;
   const int cn = legacy_au(c, rp, batch);
   launch_router(rp, s);
   c->launches += 1;
@@ -1079,7 +1095,7 @@ int hb_get_logits(hb_ctx* c, int64_t* out, int cap_pairs) {
   if (n <= 0) return 0;
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaDeviceSynchronize());
-  if (c->last_fused) {
+  if (c->last_fused || c->last_filtered) {
     // the fused kernel decides without materialising the exact logits: run
     // the exact router on its saved copy of x (inspection only)
     RouterParams rp = router_params(c, c->x_save, 1);

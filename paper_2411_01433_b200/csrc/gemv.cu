@@ -43,6 +43,8 @@
 //    MMAs per k-step, so W2 sees h at ~fp32 precision.
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "hb_internal.h"
 #include "exact_dot.cuh"
 
@@ -429,8 +431,8 @@ struct Stage {
 struct FusedSync {
   unsigned* gcount;          // global arrivals (self-resetting)
   unsigned* ggen;            // global generation
-  int* warps_done;           // shared: warps of this CTA past K2a
-  int* released;             // shared: 1 once the grid barrier passed
+  uint64_t* warps_done;      // shared mbarrier (count = CTA threads): threads past K2a
+  uint64_t* released;        // shared mbarrier (count 1): completes once the grid barrier passed
   unsigned long long* stamp; // per-forward profile record or null
 };
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* a) {
@@ -441,41 +443,31 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* a) {
 __device__ __forceinline__ void st_release_gpu(unsigned* a, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ int ld_acquire_cta(const int* a) {
-  int v;
-  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32_(a)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_cta(int* a, int v) {
-  asm volatile("st.release.cta.shared.u32 [%0], %1;" :: "r"(smem_u32_(a)), "r"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long gtimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 __device__ void fused_grid_barrier(const FusedSync& fs) {
-  __threadfence();                     // this lane's K2a reductions before the arrival
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) {
-    if (atomicAdd(fs.warps_done, 1) == kGemvWarps - 1) {
-      // last warp of the CTA: every warp's reductions are fenced
-      __threadfence();
-      if (fs.stamp) atomicMax(fs.stamp + 2, gtimer_ns());
-      const unsigned g = ld_acquire_gpu(fs.ggen);
-      if (atomicAdd(fs.gcount, 1u) == gridDim.x - 1) {
-        *fs.gcount = 0u;
-        st_release_gpu(fs.ggen, g + 1u);
-      } else {
-        while (ld_acquire_gpu(fs.ggen) == g) __nanosleep(64);
-      }
-      if (fs.stamp) atomicMax(fs.stamp + 3, ~gtimer_ns());   // min, stored complemented
-      st_release_cta(fs.released, 1);
+  __threadfence();                     // this thread's K2a reductions before the arrival
+  const uint32_t done = smem_u32(fs.warps_done), rel = smem_u32(fs.released);
+  mbar_arrive(done);                   // every thread: its K2a work is done
+  if (threadIdx.x == 0) {
+    // thread 0 meets the other CTAs once every thread of this CTA arrived
+    mbar_wait(done, 0);
+    __threadfence();
+    if (fs.stamp) atomicMax(fs.stamp + 2, gtimer_ns());
+    const unsigned g = ld_acquire_gpu(fs.ggen);
+    if (atomicAdd(fs.gcount, 1u) == gridDim.x - 1) {
+      *fs.gcount = 0u;
+      st_release_gpu(fs.ggen, g + 1u);
     } else {
-      while (!ld_acquire_cta(fs.released)) __nanosleep(32);
+      while (ld_acquire_gpu(fs.ggen) == g) __nanosleep(64);
     }
+    if (fs.stamp) atomicMax(fs.stamp + 3, ~gtimer_ns());   // min, stored complemented
+    mbar_arrive(rel);                                     // release the CTA
   }
-  __syncwarp();
+  mbar_wait(rel, 0);                   // every thread: ordered after the whole grid's K2a
 }
 
 // K2b: h rows [row0, row0 + nrows) of h_hi | h_lo | hsum (built by hfin) into
@@ -518,9 +510,10 @@ __shared__ FusedSync fz_fs;
 // or the fused kernel's shared copy.  Templated so that the legacy kernels
 // keep these in the constant bank instead of registers.
 template <bool FUSED> struct JT;
+__shared__ int lg_nv, lg_nslot;     // legacy kernels: the header, read once per launch
 template <> struct JT<false> {
-  static __device__ __forceinline__ int nv(const GemvParams& p) { return __ldcg(p.jt.hdr + 2); }
-  static __device__ __forceinline__ int nslots(const GemvParams& p) { return __ldcg(p.jt.hdr + 1); }
+  static __device__ __forceinline__ int nv(const GemvParams&) { return lg_nv; }
+  static __device__ __forceinline__ int nslots(const GemvParams&) { return lg_nslot; }
   static __device__ __forceinline__ VJobD vjob(const GemvParams& p, int v) { return p.jt.vjobs[v]; }
   static __device__ __forceinline__ int stok(const GemvParams& p, int s) { return p.jt.slot_token[s]; }
   static __device__ __forceinline__ float sgate(const GemvParams& p, int s) { return p.jt.slot_gate[s]; }
@@ -549,7 +542,11 @@ __device__ __forceinline__ void stage_h_and_wait(const GemvParams& p, const Stag
   if (!FUSED) {
     pdl_wait();
     if (S.on) stage_h_bulk_and_wait(p, S);
+#ifdef HB_NO_STAMPS
+    if (false) {
+#else
     if (p.stamps && threadIdx.x == 0) {
+#endif
       const unsigned idx = __ldcg(p.fwd_idx);
       if (idx < (unsigned)p.stamp_cap) atomicMax(p.stamps + (size_t)idx * kStampStride + 3, ~gtimer_ns());
     }
@@ -950,8 +947,13 @@ struct PhaseCtx {
 // (a vjob's column slice of h), sizes proportional to its cost (>= 1 CTA
 // each), so a CTA stages only its slice of h and keeps a deep ring; its
 // warps' feed covers that slice alone.  Contains __syncthreads.
+#ifdef HB_PHASE_FI
+#define HB_PHASE_ATTR __forceinline__
+#else
+#define HB_PHASE_ATTR
+#endif
 template <bool W13, bool FUSED>
-__device__ void phase_setup(const GemvParams& p, const int* s_cum, FeedConst* s_fk, int* s_subb,
+__device__ HB_PHASE_ATTR void phase_setup(const GemvParams& p, const int* s_cum, FeedConst* s_fk, int* s_subb,
                             float* s_subc, int* s_subvh, int* s_nsub, uint32_t bar,
                             bool h_global, Stage& S, PhaseCtx& pc) {
   const int nv = JT<FUSED>::nv(p);
@@ -1040,7 +1042,7 @@ __device__ void phase_setup(const GemvParams& p, const int* s_cum, FeedConst* s_
 // Every warp streams its static range, then dynamic chunks, through its ring
 // (no CTA-wide synchronisation: warps leave at different times).
 template <bool W13, bool FUSED>
-__device__ void phase_run(const GemvParams& p, const int* s_cum, const FeedConst* s_fk,
+__device__ HB_PHASE_ATTR void phase_run(const GemvParams& p, const int* s_cum, const FeedConst* s_fk,
                           const int* s_subvh, const PhaseCtx& pc, const Stage& S, uint2* meta) {
   const int warp = threadIdx.x >> 5;
   Feed fd;
@@ -1098,8 +1100,7 @@ __device__ void phase_run(const GemvParams& p, const int* s_cum, const FeedConst
 // hb_stamps records of the legacy chain: K2a end (last CTA); K2b end (last
 // CTA), and K2b's last CTA moves the record index on
 template <bool W13>
-__device__ __forceinline__ void legacy_stamp_end(const GemvParams& p) {
-  if (!p.stamps) return;
+__device__ __noinline__ void legacy_stamp_end_(const GemvParams& p) {
   __syncthreads();
   if (threadIdx.x != 0) return;
   const unsigned idx = __ldcg(p.fwd_idx);
@@ -1109,6 +1110,20 @@ __device__ __forceinline__ void legacy_stamp_end(const GemvParams& p) {
       p.fwd_idx[1] = 0u;
       p.fwd_idx[0] += 1u;
     }
+  }
+}
+
+template <bool W13>
+__device__ __forceinline__ void legacy_stamp_end(const GemvParams& p) {
+#ifndef HB_NO_STAMPS
+  if (p.stamps) legacy_stamp_end_<W13>(p);
+#endif
+}
+__device__ __noinline__ void legacy_stamp_start(const GemvParams& p) {
+  const unsigned idx = __ldcg(p.fwd_idx);
+  if (idx < (unsigned)p.stamp_cap) {
+    atomicMax(p.stamps + (size_t)idx * kStampStride + 0, ~gtimer_ns());
+    atomicMax(p.stamps + (size_t)idx * kStampStride + 1, gtimer_ns());
   }
 }
 
@@ -1134,17 +1149,17 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   pdl_trigger();
   const long long* cum = W13 ? p.jt.vcum13 : p.jt.vcum2;
   for (int i = threadIdx.x; i <= p.max_vjobs; i += blockDim.x) s_cum[i] = (int)__ldcg(cum + i);
+  if (threadIdx.x == 0) {
+    lg_nv = __ldcg(p.jt.hdr + 2);
+    lg_nslot = __ldcg(p.jt.hdr + 1);
+  }
   // stage hand-off: K2a every thread arrives after its share of the x copy;
   // K2b thread 0 arrives once with the bulk copies' transaction count
   if (threadIdx.x == 0) mbar_init(smem_u32(&s_bar), W13 ? blockDim.x : 1);
   __syncthreads();
-  if (W13 && p.stamps && threadIdx.x == 0) {
-    const unsigned idx = __ldcg(p.fwd_idx);
-    if (idx < (unsigned)p.stamp_cap) {
-      atomicMax(p.stamps + (size_t)idx * kStampStride + 0, ~gtimer_ns());
-      atomicMax(p.stamps + (size_t)idx * kStampStride + 1, gtimer_ns());
-    }
-  }
+#ifndef HB_NO_STAMPS
+  if (W13 && p.stamps && threadIdx.x == 0) legacy_stamp_start(p);
+#endif
   if (JT<false>::nv(p) == 0) {               // nothing owned: y stays zero (router)
     legacy_stamp_end<W13>(p);
     return;
@@ -1536,7 +1551,8 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
   __shared__ float s_subc[kGemvCTAs + 1];
   __shared__ int s_subvh[kGemvCTAs];
   __shared__ int s_nsub, s_nsub13;
-  __shared__ int s_ok, s_warps_done, s_released;
+  __shared__ int s_ok;
+  __shared__ __align__(8) uint64_t s_released, s_warps_done;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int E = fp.E, H = p.H, n8 = H / 8;
   uint8_t* dyn = gemv_smem;
@@ -1570,7 +1586,10 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
   }
   for (int i = tid; i < 4 * E; i += blockDim.x) s_blob[i] = fp.blob_table[i];
   for (int i = tid; i < E; i += blockDim.x) s_wn[i] = fp.wnorm[i];
-  if (tid == 0) { s_warps_done = 0; s_released = 0; }
+  if (tid == 0) {
+    mbar_init(smem_u32(&s_warps_done), blockDim.x);
+    mbar_init(smem_u32(&s_released), 1);
+  }
   __syncthreads();
   pdl_wait();                                  // x (and y, the sums) belong to earlier work
   if (K2B) pdl_trigger();
@@ -1694,9 +1713,17 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
 __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvParams p) {
   pdl_trigger();                             // K2b may launch and prefetch its weights
   pdl_wait();                                // the K2a sums
+  // R28: CTA b writes the NaN y row of token b if its x had a non-finite
+  // element (the router zeroed y; K2b adds after this kernel).  The flag is
+  // loaded here, next to the sums, and used at the end.
+  const int rowbad = (p.rowbad && (int)blockIdx.x < p.B) ? __ldcg(p.rowbad + blockIdx.x) : 0;
   const int nb = p.F / 32;
   const int n = __ldcg(p.jt.hdr + 1) * nb * 4;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rowbad) {
+    for (int c = threadIdx.x; c < p.H; c += blockDim.x)
+      p.y[(size_t)blockIdx.x * p.H + c] = __int_as_float(0x7fc00000);
+  }
   if (i >= ((n + 31) & ~31)) return;
   const bool act = i < n;
   const int q = act ? i : 0;
@@ -1763,7 +1790,7 @@ bool fused_fits(int E, int H, int F, int hi_enc, int lo_enc) {
 }
 void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
   const int n = max_slots * (p.F / 32) * 4;
-  launch_pdl(hfin_kernel, (n + 255) / 256, 256, 0, s, p);
+  launch_pdl(hfin_kernel, std::max((n + 255) / 256, p.B), 256, 0, s, p);   // >= one CTA per token (R28)
 }
 void launch_w2(const GemvParams& p, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<false>();

@@ -128,6 +128,9 @@ struct RouterParams {
   hb_decision* dec;                    // [n_route][B][k]
   long long* lbuf;                     // [n_route][B][E][2] exact logits (scratch)
   int* rowbad;                         // [n_route][B] non-finite x flags (scratch)
+  int filtered;                        // decode (B = 1, k = 2, cluster): filtered router
+  const float* wnorm;                  // [E] ||W_e||_2 of route layer 0 (filtered router)
+  __half* x_save;                      // [H] copy of x (filtered router: lazy exact logits)
   long long* logits;                   // [B][E][2] copy for route 0, or null
   uint4* x_perm;                       // [B][H/8] pair-permuted x, or null
   float* xsum;                         // [B][H/32], or null
@@ -154,6 +157,7 @@ struct GemvParams {
   int h_global;                        // K2b reads h from h_hi/h_lo/hsum (built by launch_hfin)
                                        // instead of building it in shared memory per CTA
   float* y;                            // [B][H] (zeroed by router)
+  const int* rowbad;                   // [B] router's non-finite x flags: K2a writes NaN rows (R28)
   // work feed: a static share of the units, then dynamic chunks (K2)
   unsigned* ctr;                       // chunk counters: [0] K2a, [1] K2b, [2 + q] K2a group q, [2 + 148 + q] K2b group q
   int max_vjobs;                       // table entries to preload (>= n_vjobs + 1)

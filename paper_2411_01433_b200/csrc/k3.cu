@@ -748,6 +748,10 @@ __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
 __global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* __restrict__ x) {
   __shared__ V3 tab[kK3MaxV3];
   __shared__ int s_n;
+  // R28: NaN rows of y for tokens whose x had a non-finite element
+  for (int b = blockIdx.x; b < p.B; b += gridDim.x)
+    if (__ldcg(p.rowbad + b))
+      for (int i = threadIdx.x; i < p.H; i += blockDim.x) p.y[(size_t)b * p.H + i] = __int_as_float(0x7fc00000);
   if (threadIdx.x == 0) {
     const int nj = p.jt.hdr[0];
     int n = 0, n16 = 0;

@@ -37,6 +37,8 @@ struct K3Params {
   __half* xg;                    // gathered X, canonical UMMA K-major blocks [v][H/64][np x 64]
   __half* hB;                    // h, same layout [v][F/64][np x 64]
   float* y;                      // [B][H] fp32, zeroed by the router
+  const int* rowbad;             // [B] non-finite x flags (router): prep writes NaN rows (R28)
+  int B;
   K3Table* tab;
   const CUtensorMap* tmap;       // [E][4 enc][6] tensor maps of this layer's blobs:
                                  //   F16: [0..2] W1, W3, W2; Q: [0..2] codes, [3..5] scales

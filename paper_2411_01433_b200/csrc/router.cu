@@ -206,7 +206,11 @@ constexpr int kRouterCluster = HB_ROUTER_CLUSTER;   // CTAs (SMs) per (route lay
 
 struct RouterSmem {
   i128 L[64];                          // this CTA's exact logits
+#ifdef HB_PART16
+  u64 part[kRouterThreads / 32][3];
+#else
   u64 part[64 > kRouterThreads / 32 ? 64 : kRouterThreads / 32][3];  // per task (E*wpe <= max(64, NW))
+#endif
   u64 cpart[64][3];                    // this CTA's partial per expert (read by the leader)
   hb_decision dec[kMaxDecSmem];        // route-0 decisions (single-CTA / last-CTA path)
   const uint8_t* blob[64 * 4];         // blob table of the layer
@@ -216,6 +220,24 @@ struct RouterSmem {
   int bad;                             // this CTA's slice of x has a non-finite element
   u64 bad2;                            // the same as a u64 (read by the cluster leader)
   int last;
+};
+
+// Shared memory of the decode router kernel (router_dec_kernel): one token,
+// top-2, E <= 32 experts, the filtered router with its exact fallback.
+struct DecSmem {
+  i128 L[64];                          // exact logits (fallback, leader)
+  u64 part[64][3];                     // exact partial per task (fallback)
+  hb_decision dec[2];
+  const uint8_t* blob[64 * 4];         // blob table of the layer
+  Job jobs[33];
+  float fpart[64];                     // per task fp32 partial logit
+  double fcp[64];                      // this CTA's partial per expert (read by the leader)
+  float xqw[kRouterThreads / 32];      // per warp sum of x^2 of the slice
+  double cxq;                          // this CTA's sum of x^2
+  double Lf[64];                       // filtered logits (leader)
+  double xs;                           // ||x||^2 (leader)
+  u64 bad2;                            // non-finite x flag (read by the leader)
+  int bad, ok;
 };
 
 // Job key of a selection: expert * 2 + (served from lo_enc), or -1 (Skip /
@@ -361,7 +383,8 @@ __device__ void build_jobs_cta(const RouterParams& p, RouterSmem& sm, const hb_d
 // build_jobs by one warp when the forward has <= 32 selections (decode): the
 // same table (jobs by key = expert*2 + Low, slots in selection order) from
 // per-lane counts instead of serial loops.
-__device__ __forceinline__ void build_jobs_warp(const RouterParams& p, RouterSmem& sm, const hb_decision* dec) {
+template <typename SmemT>
+__device__ __forceinline__ void build_jobs_warp(const RouterParams& p, SmemT& sm, const hb_decision* dec) {
   const int lane = threadIdx.x & 31;
   const int nsel = p.B * p.k;
   constexpr int kNone = 0x7FFFFFFF;
@@ -437,6 +460,251 @@ __device__ __forceinline__ u64 ld_dsmem_u64(const void* local, int rank) {
 // C = CTAs per (route layer, token) row: 8 (a cluster, decode: the token's
 // logits in ~1/8 of the latency) or 1 (batches: one CTA per row, no cluster --
 // 8-CTA clusters per token cost ~1 us per token at B = 512)
+
+// fp16 x8 -> fp32 x8
+__device__ __forceinline__ void r_h2f8(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ double ld_dsmem_f64(const void* local, int rank) {
+  return __longlong_as_double((long long)ld_dsmem_u64(local, rank));
+}
+
+// pair-permuted x and block sums of the slice [s0, s1) (uint4 chunks) for
+// the GEMV kernels
+__device__ __forceinline__ void write_xperm(const RouterParams& p, const __half* x, int s0, int s1,
+                                            int b) {
+  for (int blk = s0 / 4 + threadIdx.x; blk < s1 / 4; blk += blockDim.x) {
+    const uint4* src = reinterpret_cast<const uint4*>(x + blk * 32);
+    uint32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 t = src[i];
+      v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      sum += __half2float(__ushort_as_half((unsigned short)(v[i >> 1] >> (16 * (i & 1)))));
+    p.xsum[(size_t)b * (p.H / 32) + blk] = sum;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {                  // uint4 t: Q_c = (x[8t+c], x[8t+c+4])
+      uint32_t q[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e0 = 8 * t + c, e1 = e0 + 4;
+        const uint32_t lo16 = (v[e0 >> 1] >> (16 * (e0 & 1))) & 0xFFFF;
+        const uint32_t hi16 = (v[e1 >> 1] >> (16 * (e1 & 1))) & 0xFFFF;
+        q[c] = lo16 | (hi16 << 16);
+      }
+      p.x_perm[(size_t)b * (p.H / 8) + blk * 4 + t] = make_uint4(q[0], q[1], q[2], q[3]);
+    }
+  }
+}
+
+// Batch-1 decode, k = 2, one cluster: the FILTERED router.  Every CTA sums
+// fp32 products (exact for fp16 x fp16) of its slice of H in FFMA chains and
+// warp trees; the leader adds the CTA partials in fp64 and decides the top-2
+// order and the T1/T2 tests from these when every comparison clears a
+// rigorous bound on the rounding error (Cauchy-Schwarz: sum |w x| <= ||w_e||
+// ||x||, R9'), else from the exact integer logits it computes itself
+// (rare).  Either way the decisions are the exact ones.  The gates come from
+// the filtered gap (R25).
+// Zeroing CTAs of the router grids: the buffers the GEMV kernels accumulate
+// into (K2a sums, y, ...); they belong to the previous kernels of the
+// stream, so wait first.  CTA zc of nzc.
+__device__ void zero_buffers(const RouterParams& p, int zc, int nzc) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int tid = threadIdx.x;
+  const long long t0 = (long long)zc * blockDim.x + tid;
+  const long long stride = (long long)nzc * blockDim.x;
+#pragma unroll
+  for (int z = 0; z < 3; ++z) {
+    float* zb = p.zero_buf[z];
+    const long long n = p.zero_n[z];
+    if ((reinterpret_cast<uintptr_t>(zb) & 15) == 0) {
+      for (long long i = t0; i < n / 4; i += stride)
+        reinterpret_cast<float4*>(zb)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (long long i = (n / 4) * 4 + t0; i < n; i += stride) zb[i] = 0.f;
+    } else {
+      for (long long i = t0; i < n; i += stride) zb[i] = 0.f;
+    }
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void route_filtered(const RouterParams& p, DecSmem& sm, int crank,
+                                               int s0, int s1, int b, int rl) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = kRouterThreads / 32;
+  const __half* x = p.x + (size_t)b * p.H;
+  const uint4* x4 = reinterpret_cast<const uint4*>(x);
+  const int wpe = p.E >= NW ? 1 : NW / p.E;
+  int xbad = 0;
+  float xq = 0.f;
+  for (int task = warp; task < p.E * wpe; task += NW) {
+    const int e = task / wpe, part = task - e * wpe;
+    const uint4* w4 = reinterpret_cast<const uint4*>(p.wg[rl] + (size_t)e * p.H);
+    const int j0 = s0 + part * (s1 - s0) / wpe, j1 = s0 + (part + 1) * (s1 - s0) / wpe;
+    float acc = 0.f;
+    for (int j = j0 + lane; j < j1; j += 32) {
+      const uint4 wv = w4[j];
+      const uint4 xv = x4[j];
+      float wf[8], xf[8];
+      r_h2f8(wv, wf);
+      r_h2f8(xv, xf);
+      if (e == 0) {                               // every chunk of the slice once
+        const uint32_t xa[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          xbad |= ((xa[q] & 0x7C00u) == 0x7C00u) | ((xa[q] & 0x7C000000u) == 0x7C000000u);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xq = fmaf(xf[q], xf[q], xq);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = fmaf(wf[q], xf[q], acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sm.fpart[task] = acc;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) xq += __shfl_xor_sync(0xffffffffu, xq, o);
+  if (lane == 0) sm.xqw[warp] = xq;
+  const int bad = __syncthreads_or(xbad);
+  if (tid < p.E) {
+    double v = 0.0;
+    for (int q = 0; q < wpe; ++q) v += (double)sm.fpart[tid * wpe + q];
+    sm.fcp[tid] = v;
+  }
+  if (tid == kRouterThreads - 1) {
+    double v = 0.0;
+    for (int w = 0; w < NW; ++w) v += (double)sm.xqw[w];
+    sm.cxq = v;
+    sm.bad2 = (u64)bad;
+  }
+  if (rl == 0) {
+    if (p.x_save)
+      for (int j = s0 + tid; j < s1; j += blockDim.x) reinterpret_cast<uint4*>(p.x_save)[j] = x4[j];
+    if (p.x_perm) write_xperm(p, x, s0, s1, b);
+  }
+  cluster_sync_all();
+  if (crank == 0) {
+    if (tid < p.E * C) {                        // e = tid / C, rank r = tid % C; C | 32
+      const int e = tid / C, r = tid - e * C;
+      double v = ld_dsmem_f64(&sm.fcp[e], r);
+#pragma unroll
+      for (int o = 1; o < C; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (r == 0) sm.Lf[e] = v;
+    }
+    if (tid == kRouterThreads - 1) {
+      double xs = 0.0;
+      int bd = 0;
+      for (int r = 0; r < C; ++r) {
+        xs += ld_dsmem_f64(&sm.cxq, r);
+        bd |= (int)ld_dsmem_u64(&sm.bad2, r);
+      }
+      sm.xs = xs;
+      sm.bad = bd;
+    }
+  }
+  cluster_sync_all();                             // remote reads done: the other CTAs may exit
+  if (crank != 0) return;
+  if (tid == 0) p.rowbad[b] = sm.bad;             // the expert kernels write NaN rows (R28)
+  if (warp == 0) {
+    if (sm.bad) {
+      if (lane == 0) { decide_nonfinite(p, b, p.dec, sm.dec); sm.ok = 1; }
+    } else {
+      // error of a logit: fp32 chains of m products per lane (gamma_{m-1}),
+      // warp trees (gamma_5), fp64 sums (negligible): (m + 5) * 2^-24 *
+      // sum|p| * (1 + 1e-6), with sum|p| <= ||w_e|| ||x|| (||x|| rounded up)
+      const int chunks = (s1 - s0) / wpe;
+      const int m = 8 * ((chunks + 31) / 32);
+      const double xn = sqrt(sm.xs) * (1.0 + 1e-6) + 1e-30;
+      const double c = (m + 6) * 0x1p-24 * 1.0001;
+      const int e = lane;
+      const double v = e < p.E ? sm.Lf[e] : -1e300;
+      const double ep = e < p.E ? c * (double)p.wnorm[e] * xn : 0.0;
+      int r = 0;
+      if (e < p.E)
+        for (int f = 0; f < p.E; ++f) { const double o = sm.Lf[f]; r += (o > v) || (o == v && f < e); }
+      const unsigned m0 = __ballot_sync(0xffffffffu, e < p.E && r == 0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, e < p.E && r == 1);
+      const int e0 = __ffs(m0) - 1, e1 = __ffs(m1) - 1;
+      double rest = (e < p.E && r >= 2) ? v + ep : -1e300;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rest = fmax(rest, __shfl_xor_sync(0xffffffffu, rest, o));
+      const double L0 = __shfl_sync(0xffffffffu, v, e0), L1 = __shfl_sync(0xffffffffu, v, e1);
+      const double ep0 = __shfl_sync(0xffffffffu, ep, e0), ep1 = __shfl_sync(0xffffffffu, ep, e1);
+      const double G = L0 - L1, mg = ep0 + ep1 + 1e-12 * (1.0 + fabs(L0) + fabs(L1));
+      bool ok = (L0 - ep0 > L1 + ep1) && (L1 - ep1 > rest);
+      if (p.th1_kind == 0) ok = ok && fabs(G - (double)p.theta1 * 0x1p-48) > mg;
+      if (p.th2_kind == 0) ok = ok && fabs(G - (double)p.theta2 * 0x1p-48) > mg;
+      if (ok && lane == 0) {
+        const uint8_t prec1 = (p.th1_kind > 0 || (p.th1_kind == 0 && G <= (double)p.theta1 * 0x1p-48)) ? HB_HIGH
+                            : (p.th2_kind > 0 || (p.th2_kind == 0 && G <= (double)p.theta2 * 0x1p-48)) ? HB_LOW
+                                                                                                    : HB_SKIP;
+        const float ex = expf(-(float)G);
+        const float g0 = 1.f / (1.f + ex), g1 = ex * g0;
+        hb_decision r0, r1;
+        r0.token = b; r0.expert = e0; r0.sel_rank = 0; r0.prec = HB_HIGH;
+        r0.served_enc = HB_ENC_NONE; r0.hit = 0; r0.gate = g0;
+        r1.token = b; r1.expert = e1; r1.sel_rank = 1; r1.prec = prec1;
+        r1.served_enc = HB_ENC_NONE; r1.hit = 0; r1.gate = g1;
+        p.dec[0] = r0; p.dec[1] = r1;
+        sm.dec[0] = r0; sm.dec[1] = r1;
+      }
+      if (lane == 0) sm.ok = ok;
+    }
+  }
+  __syncthreads();
+  if (!sm.ok) {
+    // ---- exact fallback by the leader alone over the whole of H (rare)
+    const int n8 = p.H / 8;
+    for (int task = warp; task < p.E * wpe; task += NW) {
+      const int e = task / wpe, part = task - e * wpe;
+      const uint4* w4 = reinterpret_cast<const uint4*>(p.wg[rl] + (size_t)e * p.H);
+      const int j0 = part * n8 / wpe, j1 = (part + 1) * n8 / wpe;
+      u64 lo = 0, mid = 0, hi = 0;
+      for (int j = j0 + lane; j < j1; j += 32) {
+        const uint4 wv = w4[j];
+        const uint4 xv = x4[j];
+        const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
+        const uint32_t xa[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          accum_exact((wa[i >> 1] >> (16 * (i & 1))) & 0xFFFF, (xa[i >> 1] >> (16 * (i & 1))) & 0xFFFF,
+                      lo, mid, hi);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+        mid += __shfl_xor_sync(0xffffffffu, mid, o);
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+      if (lane == 0) { sm.part[task][0] = lo; sm.part[task][1] = mid; sm.part[task][2] = hi; }
+    }
+    __syncthreads();
+    for (int e = tid; e < p.E; e += blockDim.x) {
+      u64 lo = 0, mid = 0, hi = 0;
+      for (int q = 0; q < wpe; ++q) {
+        lo += sm.part[e * wpe + q][0]; mid += sm.part[e * wpe + q][1]; hi += sm.part[e * wpe + q][2];
+      }
+      sm.L[e] = (i128)(long long)lo + ((i128)(long long)mid << 20) + ((i128)(long long)hi << 40);
+    }
+    __syncthreads();
+    if (warp == 0) decide_k2_warp(p, sm.L, b, p.dec, sm.dec);
+    __syncthreads();
+  }
+  if (warp == 0 && p.blob_table) build_jobs_warp(p, sm, sm.dec);
+}
+
 template <int C>
 __global__ void __launch_bounds__(kRouterThreads)
 router_kernel(const __grid_constant__ RouterParams p) {
@@ -447,44 +715,7 @@ router_kernel(const __grid_constant__ RouterParams p) {
   const int nrows = p.n_route * p.B;
   const int row = blockIdx.x / C, crank = blockIdx.x % C;   // cluster = one row
   if (row >= nrows) {
-    // ---- zeroing CTAs: the buffers the GEMV kernels accumulate into (K2a
-    // sums, y); they belong to the previous kernels of the stream, so wait
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;");
-    const long long t0 = (long long)(blockIdx.x - nrows * C) * blockDim.x + tid;
-    const long long stride = (long long)(gridDim.x - nrows * C) * blockDim.x;
-    // y rows: 0, or NaN for a token whose x has a non-finite element (R28)
-    if (p.zero_n[1] > 0) {
-      const int zc = blockIdx.x - nrows * C, nzc = gridDim.x - nrows * C;
-      const int n8 = p.H / 8;
-      for (int r = zc; r < p.B; r += nzc) {
-        const uint4* xr = reinterpret_cast<const uint4*>(p.x + (size_t)r * p.H);
-        int bad = 0;
-        for (int j = tid; j < n8; j += blockDim.x) {
-          const uint4 v = __ldcg(xr + j);
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            bad |= ((w[q] & 0x7C00u) == 0x7C00u) | ((w[q] & 0x7C000000u) == 0x7C000000u);
-        }
-        const float val = __syncthreads_or(bad) ? __int_as_float(0x7fc00000) : 0.f;
-        float4* yr = reinterpret_cast<float4*>(p.zero_buf[1] + (size_t)r * p.H);
-        for (int j = tid; j < p.H / 4; j += blockDim.x) yr[j] = make_float4(val, val, val, val);
-      }
-    }
-#pragma unroll
-    for (int z = 0; z < 3; ++z) {
-      if (z == 1) continue;
-      float* zb = p.zero_buf[z];
-      const long long n = p.zero_n[z];
-      if ((reinterpret_cast<uintptr_t>(zb) & 15) == 0) {
-        for (long long i = t0; i < n / 4; i += stride)
-          reinterpret_cast<float4*>(zb)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (long long i = (n / 4) * 4 + t0; i < n; i += stride) zb[i] = 0.f;
-      } else {
-        for (long long i = t0; i < n; i += stride) zb[i] = 0.f;
-      }
-    }
+    zero_buffers(p, blockIdx.x - nrows * C, gridDim.x - nrows * C);
     return;
   }
   const int b = row % p.B;
@@ -509,11 +740,13 @@ router_kernel(const __grid_constant__ RouterParams p) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   HB_RTL(1);
+
   // ---- O2: exact partial logits of token b over this CTA's slice, every
   // expert (a warp per expert, or several warps per expert when E < 8)
   const __half* x = p.x + (size_t)b * p.H;
   const uint4* x4 = reinterpret_cast<const uint4*>(x);
   const int wpe = p.E >= NW ? 1 : NW / p.E;
+  int xbad = 0;                                 // non-finite x in the slice (R28)
   for (int task = warp; task < p.E * wpe; task += NW) {
     const int e = task / wpe, part = task - e * wpe;
     const uint4* w4 = reinterpret_cast<const uint4*>(p.wg[rl] + (size_t)e * p.H);
@@ -525,6 +758,9 @@ router_kernel(const __grid_constant__ RouterParams p) {
       const uint4 xv = x4[j];
       const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
       const uint32_t xa[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        xbad |= ((xa[q] & 0x7C00u) == 0x7C00u) | ((xa[q] & 0x7C000000u) == 0x7C000000u);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         accum_exact((wa[i >> 1] >> (16 * (i & 1))) & 0xFFFF, (xa[i >> 1] >> (16 * (i & 1))) & 0xFFFF,
@@ -539,15 +775,8 @@ router_kernel(const __grid_constant__ RouterParams p) {
     if (lane == 0) { sm.part[task][0] = lo; sm.part[task][1] = mid; sm.part[task][2] = hi; }
   }
   {
-    int bad = 0;                               // non-finite x in this CTA's slice
-    for (int j = s0 + tid; j < s1; j += blockDim.x) {
-      const uint4 v = x4[j];
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        bad |= ((w[q] & 0x7C00u) == 0x7C00u) | ((w[q] & 0x7C000000u) == 0x7C000000u);
-    }
-    bad = __syncthreads_or(bad);
+    // every x chunk of the slice was read by the expert-0 tasks above
+    const int bad = __syncthreads_or(xbad);
     if (tid == 0) { sm.bad = bad; sm.bad2 = (u64)bad; }
   }
   for (int e = tid; e < p.E; e += blockDim.x) {            // CTA partial per expert
@@ -559,39 +788,12 @@ router_kernel(const __grid_constant__ RouterParams p) {
   }
   HB_RTL(2);
   // ---- pair-permuted x and block sums of this slice for the GEMV kernels
-  if (p.x_perm && rl == 0) {
-    for (int blk = s0 / 4 + tid; blk < s1 / 4; blk += blockDim.x) {
-      const uint4* src = reinterpret_cast<const uint4*>(x + blk * 32);
-      uint32_t v[16];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint4 t = src[i];
-        v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
-      }
-      float sum = 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        sum += __half2float(__ushort_as_half((unsigned short)(v[i >> 1] >> (16 * (i & 1)))));
-      p.xsum[(size_t)b * (p.H / 32) + blk] = sum;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {                  // uint4 t: Q_c = (x[8t+c], x[8t+c+4])
-        uint32_t q[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int e0 = 8 * t + c, e1 = e0 + 4;
-          const uint32_t lo16 = (v[e0 >> 1] >> (16 * (e0 & 1))) & 0xFFFF;
-          const uint32_t hi16 = (v[e1 >> 1] >> (16 * (e1 & 1))) & 0xFFFF;
-          q[c] = lo16 | (hi16 << 16);
-        }
-        p.x_perm[(size_t)b * (p.H / 8) + blk * 4 + t] = make_uint4(q[0], q[1], q[2], q[3]);
-      }
-    }
-  }
+  if (p.x_perm && rl == 0) write_xperm(p, x, s0, s1, b);
   // ---- combine the cluster's partials in the leader (distributed shared memory)
   if (C > 1) cluster_sync_all();
   else __syncthreads();
   if (crank == 0) {
-    if (C > 1 && tid == 0) {
+    if (C > 1 && tid == kRouterThreads - 1) {   // a thread the logit combine does not use
       int bad = 0;
       for (int r = 0; r < C; ++r) bad |= (int)ld_dsmem_u64(&sm.bad2, r);
       sm.bad = bad;
@@ -623,6 +825,7 @@ router_kernel(const __grid_constant__ RouterParams p) {
 
   // ---- single (route layer, token): decide and build the jobs right here
   if (nrows == 1) {
+    if (tid == 0) p.rowbad[b] = sm.bad;       // the expert kernels write NaN rows (R28)
     if (warp == 0) {
       if (sm.bad) {
         if (lane == 0) decide_nonfinite(p, b, p.dec, sm.dec);
@@ -683,10 +886,43 @@ router_kernel(const __grid_constant__ RouterParams p) {
   if (tid == 0) *p.done = 0u;
 }
 
+
+// Decode router (batch 1, top-2, E <= 32): one cluster of C CTAs runs the
+// filtered router (route_filtered), extra CTAs zero the accumulation
+// buffers.  A kernel of its own: small code and shared memory (the general
+// router kernel is measurably slower when this path is compiled into it).
+template <int C>
+__global__ void __launch_bounds__(kRouterThreads)
+router_dec_kernel(const __grid_constant__ RouterParams p) {
+  __shared__ DecSmem sm;
+  if ((int)blockIdx.x >= C) {
+    zero_buffers(p, blockIdx.x - C, gridDim.x - C);
+    return;
+  }
+  const int tid = threadIdx.x;
+  const int crank = blockIdx.x;
+  const int n8 = p.H / 8;
+  const int s0 = crank * n8 / C, s1 = (crank + 1) * n8 / C;
+  {
+    const char* wb = reinterpret_cast<const char*>(p.wg[0]);
+    const int lpr = (s1 - s0) * 16 / 128;
+    for (int i = tid; i < p.E * lpr; i += kRouterThreads) {
+      const int e = i / lpr, l = i - e * lpr;
+      asm volatile("prefetch.global.L2 [%0];" :: "l"(wb + ((size_t)e * n8 + s0) * 16 + (size_t)l * 128));
+    }
+    if (p.blob_table && crank == 0)
+      for (int i = tid; i < 4 * p.E; i += kRouterThreads) sm.blob[i] = p.blob_table[i];
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  route_filtered<C>(p, sm, crank, s0, s1, 0, 0);
+}
+
 void launch_router(const RouterParams& p, cudaStream_t s) {
   // one 8-CTA cluster per (route layer, token) row, plus clusters of CTAs that
   // zero the GEMV accumulation buffers in parallel
   const int C = p.n_route * p.B >= 16 ? 1 : kRouterCluster;
+  const bool dec = p.filtered && p.n_route == 1 && p.B == 1 && p.k == 2 && p.E <= 32;
   const long long nz4 = (p.zero_n[0] + p.zero_n[1] + p.zero_n[2]) / 4;
   int zc = nz4 ? (int)std::min<long long>(32, (nz4 + 2 * kRouterThreads - 1) / (2 * kRouterThreads)) : 0;
   zc = (zc + C - 1) / C * C;
@@ -704,7 +940,10 @@ void launch_router(const RouterParams& p, cudaStream_t s) {
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  if (C == 1) {
+  if (dec) {
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, router_dec_kernel<kRouterCluster>, p);
+  } else if (C == 1) {
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, router_kernel<1>, p);
   } else {

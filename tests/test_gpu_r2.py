@@ -329,3 +329,42 @@ def test_decode_variants_match_oracle(mode, monkeypatch):
     ref, routes = om.moe_layer(x16, sg.router_weights(big, 9), store, 9, 2, 0.6, 0.9, fm.F16, fm.Q4)
     _check_routes(ctx, routes, 1, 2)
     assert rel_err(y[0], ref[0])[0] <= 1e-4
+
+
+# ------------------------------------------------------------ slot WAR ordering
+def test_offload_slot_war_ordering():
+    """Offload path, pools of 2 slots, two layers with disjoint experts: every
+    forward evicts the slots the previous layer's GEMV kernels are still
+    reading (F = 4096: tens of microseconds of K2) while its ~100 MB copies
+    start on the copy stream right away.  The per-slot 'free' events must
+    order each copy after the readers: every output equals the oracle's."""
+    from oracle import cache as oc
+    sh = sg.MoEShape("war", 2, 8, 2, 4096, 4096, 1.5)
+    ctx = _ctx(sh, fm.F16, fm.Q4, max_batch=1, cap_high=2, cap_low=2, lookahead_p=0)
+    store = OracleStore(sh)
+    from tests.gpu_util import gpu_blobs
+    for l in range(2):
+        ctx.set_router(l, sg.router_weights(sh, l))
+        for (e, enc), b in gpu_blobs(sh, l, range(8), [fm.F16, fm.Q4]).items():
+            ctx.register_expert(l, e, enc, b.cpu().numpy())
+    ref_cache = oc.ExpertCache(2, 8, 2, 2, (1, 1, 1, 1), fm.F16, fm.Q4)
+    outs, refs = [], []
+    for t in range(6):
+        ctx.token_begin()
+        ref_cache.token_begin()
+        for l in range(2):
+            x16 = sg.hidden_states(sh, 80 + t, l)
+            x = torch.from_numpy(x16).cuda()
+            y = torch.empty(1, sh.hidden, dtype=torch.float32, device="cuda")
+            ctx.forward(l, x, y)                 # no synchronisation between forwards
+            outs.append(y)
+            route = rt.route(x16, sg.router_weights(sh, l), 2, 0.6, 0.9)[0]
+            served = ref_cache.forward(l, route)
+            refs.append((x16, l, served))
+    torch.cuda.synchronize()
+    evictions = [e for e in ctx.events() if e[0] == 1 and e[6] >= 0]
+    assert len(evictions) >= 8, "the trace must evict slots still in use by the previous layer"
+    for y, (x16, l, served) in zip(outs, refs):
+        ref, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9, fm.F16, fm.Q4,
+                              served=[served])
+        assert rel_err(y.cpu().numpy()[0], ref[0])[0] <= 1e-4
