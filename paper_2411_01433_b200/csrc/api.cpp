@@ -108,6 +108,7 @@ struct hb_ctx {
   __half* x_save = nullptr;               // x of the last fused forward (lazy exact logits)
   bool last_fused = false;
   bool last_filtered = false;             // last forward's router kept no exact logits
+  bool hfin_tail = false;                 // HB_HFIN_TAIL=1: h at the end of K2a (grid barrier), no hfin kernel
   bool router_filtered = false;           // HB_ROUTER=filtered: batch-1 decode router kernel (diagnostic)
   bool fused_split = false;               // HB_FUSED_SPLIT=1: router+K2a kernel, then hfin + K2b
   bool fused_router = false;              // HB_FUSED_ROUTER=1: one-CTA router kernel + legacy K2a/hfin/K2b
@@ -420,6 +421,10 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     c->fused_ok = resident && K == 2 && mode != "legacy" && fused_fits(E, H, F, k.hi_enc, k.lo_enc);
     c->fused_split = mode == "split";
     c->fused_router = mode == "router";
+    // measured slower (K2a CTAs held at the barrier: K2b's prologue cannot
+    // overlap the K2a tail), kept as a diagnostic variant
+    const char* hk = std::getenv("HB_HFIN_TAIL");
+    c->hfin_tail = hk && hk[0] == '1';
     const char* re = std::getenv("HB_ROUTER");
     c->router_filtered = re && std::string(re) == "filtered";
   }
@@ -703,6 +708,8 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y, float* au) {
   g.h_global = c->force_h_global || !fits || 2 * nv_bound > kGemvCTAs;
   g.y = (float*)y;
   g.rowbad = c->rowbad;
+  g.hfin_tail = c->hfin_tail;
+  g.gbar = c->gbar;
   g.ctr = c->gctr;
   g.max_vjobs = c->max_vjobs;
   g.static_frac = c->static_frac;
@@ -791,8 +798,10 @@ static void launch_gemv(hb_ctx* c, const GemvParams& gp, cudaStream_t s) {
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
   if (ev) cudaEventRecord(ev[0], s);
   launch_w13(gp, s);
-  launch_hfin(gp, c->last_batch * c->cfg.top_k, s);
-  c->launches += 1;
+  if (!gp.hfin_tail) {
+    launch_hfin(gp, c->last_batch * c->cfg.top_k, s);
+    c->launches += 1;
+  }
   if (ev) cudaEventRecord(ev[1], s);
   launch_w2(gp, s);
   if (ev) cudaEventRecord(ev[2], s);

@@ -1127,6 +1127,74 @@ __device__ __noinline__ void legacy_stamp_start(const GemvParams& p) {
   }
 }
 
+// hfin folded into the end of K2a (p.hfin_tail): the CTAs meet at a grid
+// barrier once every K2a sum is complete, then each computes its share of
+// h = silu(a) * u as the fp16 hi/lo rows + block sums K2b bulk-copies, and
+// CTA b writes the NaN y row of token b (R28).  Saves the hfin launch and its
+// hand-offs; K2b waits on K2a directly.  Cold code, not inlined.
+__device__ __noinline__ void k2a_hfin_tail(const GemvParams& p, bool any) {
+  if (any) {
+    __syncthreads();                           // every warp of the CTA is past its K2a work
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned g = ld_acquire_gpu(p.gbar + 1);
+      if (atomicAdd(p.gbar, 1u) == gridDim.x - 1) {
+        p.gbar[0] = 0u;
+        st_release_gpu(p.gbar + 1, g + 1u);
+      } else {
+        while (ld_acquire_gpu(p.gbar + 1) == g) __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    const int nb = p.F / 32;
+    const int n = lg_nslot * nb * 4;             // four threads per (slot, 32-row block)
+    const int lane = threadIdx.x & 31;
+    const int nthr = gridDim.x * blockDim.x;
+    for (int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += nthr) {
+      const int i = i0 + lane;
+      const bool act = i < n;
+      const int q = act ? i : 0;
+      const int item = q >> 2, t = q & 3;
+      const int sl = item / nb, j = item - sl * nb;
+      const float* pa = p.au + (size_t)sl * 2 * p.F + (size_t)j * 32 + 8 * t;
+      const float* pu = pa + p.F;
+      const float4 a0 = __ldcg(reinterpret_cast<const float4*>(pa));
+      const float4 a1 = __ldcg(reinterpret_cast<const float4*>(pa) + 1);
+      const float4 u0 = __ldcg(reinterpret_cast<const float4*>(pu));
+      const float4 u1 = __ldcg(reinterpret_cast<const float4*>(pu) + 1);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float uv[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+      float h[8], hs = 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        h[r] = av[r] / (1.f + expf(-av[r])) * uv[r];
+        hs += h[r];
+      }
+      uint32_t wh[4], wl[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {            // Q_c = (h[8t+c], h[8t+c+4])
+        const __half h0 = __float2half_rn(h[c]), h1 = __float2half_rn(h[c + 4]);
+        const __half l0 = __float2half_rn(h[c] - __half2float(h0));
+        const __half l1 = __float2half_rn(h[c + 4] - __half2float(h1));
+        wh[c] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+        wl[c] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+      }
+      hs += __shfl_xor_sync(0xffffffffu, hs, 1);
+      hs += __shfl_xor_sync(0xffffffffu, hs, 2);
+      if (act) {
+        p.h_hi[(size_t)sl * (p.F / 8) + j * 4 + t] = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+        p.h_lo[(size_t)sl * (p.F / 8) + j * 4 + t] = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+        if (t == 0) p.hsum[item] = hs;
+      }
+    }
+  }
+  if (p.rowbad)
+    for (int b = blockIdx.x; b < p.B; b += gridDim.x)
+      if (__ldcg(p.rowbad + b))
+        for (int c = threadIdx.x; c < p.H; c += blockDim.x)
+          p.y[(size_t)b * p.H + c] = __int_as_float(0x7fc00000);
+}
+
 // Legacy chain (router kernel -> K2a -> hfin -> K2b): batches, the offload
 // path and configurations the fused kernel does not cover.
 template <bool W13>
@@ -1161,6 +1229,7 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   if (W13 && p.stamps && threadIdx.x == 0) legacy_stamp_start(p);
 #endif
   if (JT<false>::nv(p) == 0) {               // nothing owned: y stays zero (router)
+    if (W13 && p.hfin_tail) k2a_hfin_tail(p, false);
     legacy_stamp_end<W13>(p);
     return;
   }
@@ -1170,6 +1239,7 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
                           p.h_global, S, pc);
   phase_run<W13, false>(p, s_cum, &s_fk, s_subvh, pc, S, s_meta[warp]);
   HB_TL(W13, warp * gridDim.x + blockIdx.x, 3);
+  if (W13 && p.hfin_tail) k2a_hfin_tail(p, true);
   legacy_stamp_end<W13>(p);
 }
 

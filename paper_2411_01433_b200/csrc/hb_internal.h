@@ -157,7 +157,9 @@ struct GemvParams {
   int h_global;                        // K2b reads h from h_hi/h_lo/hsum (built by launch_hfin)
                                        // instead of building it in shared memory per CTA
   float* y;                            // [B][H] (zeroed by router)
-  const int* rowbad;                   // [B] router's non-finite x flags: K2a writes NaN rows (R28)
+  const int* rowbad;                   // [B] router's non-finite x flags: NaN rows (R28)
+  int hfin_tail;                       // K2a ends with a grid barrier + h (no hfin kernel)
+  unsigned* gbar;                      // that grid barrier [count, generation] (self-resetting)
   // work feed: a static share of the units, then dynamic chunks (K2)
   unsigned* ctr;                       // chunk counters: [0] K2a, [1] K2b, [2 + q] K2a group q, [2 + 148 + q] K2b group q
   int max_vjobs;                       // table entries to preload (>= n_vjobs + 1)
