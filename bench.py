@@ -435,19 +435,22 @@ def batched_leg(h, sg, shape, hi, lo, blobs, dev, stream, Bs=(256, 512), layers=
     served blobs (each (expert, encoding) blob once per layer + X + h + y)."""
     import torch
     E, Hd, F = shape.n_experts, shape.hidden, shape.ffn
-    cfg = h.default_config(n_layers=shape.n_layers, n_experts=E, top_k=shape.top_k, hidden=Hd,
-                           ffn=F, hi_enc=hi, lo_enc=lo, max_batch=max(Bs))
-    ctx = h.Context(cfg, dev)
-    i = 0
-    for l in range(shape.n_layers):
-        ctx.set_router(l, sg.router_weights(shape, l))
-        for e in range(E):
-            for enc in (hi, lo):
-                ctx.register_expert(l, e, enc, blobs[i])
-                i += 1
     bb = {hi: h.blob_bytes(hi, Hd, F), lo: h.blob_bytes(lo, Hd, F)}
     out = {}
-    with torch.cuda.stream(stream):
+    # SURVEY 8(d) C5: allow_upgrade = 1, one stream per touched expert
+    # (strict = 0, DESIGN.md R27); the strict mix (every Low from lo_enc) too
+    for strict in (0, 1):
+      cfg = h.default_config(n_layers=shape.n_layers, n_experts=E, top_k=shape.top_k, hidden=Hd,
+                             ffn=F, hi_enc=hi, lo_enc=lo, max_batch=max(Bs), strict=strict)
+      ctx = h.Context(cfg, dev)
+      i = 0
+      for l in range(shape.n_layers):
+          ctx.set_router(l, sg.router_weights(shape, l))
+          for e in range(E):
+              for enc in (hi, lo):
+                  ctx.register_expert(l, e, enc, blobs[i])
+                  i += 1
+      with torch.cuda.stream(stream):
         for B in Bs:
             X = torch.from_numpy(np.stack([sg.hidden_states(shape, 7000 + B, l, batch=B)
                                            for l in range(layers)])).cuda()
@@ -475,11 +478,13 @@ def batched_leg(h, sg, shape, hi, lo, blobs, dev, stream, Bs=(256, 512), layers=
             e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / steps
-            out[f"B{B}"] = {"tok_s": round(B * layers / shape.n_layers * 1000.0 / ms, 1),
-                            "ms_per_step": round(ms, 4), "layers": layers,
-                            "step_gbs": round(nbytes / ms / 1e6, 1), "path": "K3 tcgen05 GEMM"}
+            out[f"B{B}" + ("" if strict == 0 else "_strict")] = {
+                "tok_s": round(B * layers / shape.n_layers * 1000.0 / ms, 1),
+                "ms_per_step": round(ms, 4), "layers": layers,
+                "step_gbs": round(nbytes / ms / 1e6, 1), "path": "K3 tcgen05 GEMM",
+                "strict": strict}
             del X, Y, g
-    ctx.close()
+      ctx.close()
     return out
 
 

@@ -110,6 +110,7 @@ struct hb_ctx {
   bool last_filtered = false;             // last forward's router kept no exact logits
   bool hfin_tail = false;                 // HB_HFIN_TAIL=1: h at the end of K2a (grid barrier), no hfin kernel
   bool router_filtered = false;           // HB_ROUTER=filtered: batch-1 decode router kernel (diagnostic)
+  bool router_batch = true;               // filtered router for batches (HB_ROUTER=exact: off)
   bool fused_split = false;               // HB_FUSED_SPLIT=1: router+K2a kernel, then hfin + K2b
   bool fused_router = false;              // HB_FUSED_ROUTER=1: one-CTA router kernel + legacy K2a/hfin/K2b
   uint4* h_hi = nullptr;                  // h in global memory (large batches only)
@@ -369,7 +370,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
             dm((void**)&c->au, 2 * (size_t)c->max_slots * 2 * F * 4) &&
             dm((void**)&c->gbar, 16) && dm((void**)&c->fwd_idx, 16) &&
             dm((void**)&c->wnorm, (size_t)L * E * 4) &&
-            dm((void**)&c->x_save, (size_t)H * 2) &&
+            dm((void**)&c->x_save, (size_t)B * H * 2) &&
             dm((void**)&c->h_hi, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->h_lo, (size_t)c->max_slots * F * 2) &&
             dm((void**)&c->hsum, (size_t)c->max_slots * (F / 32) * 4) &&
@@ -427,6 +428,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     c->hfin_tail = hk && hk[0] == '1';
     const char* re = std::getenv("HB_ROUTER");
     c->router_filtered = re && std::string(re) == "filtered";
+    c->router_batch = !(re && std::string(re) == "exact");
   }
   cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + 2 * kGemvCTAs));
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
@@ -905,14 +907,17 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
     rp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
     const bool k3 = c->k3_ok && c->k3_min_batch > 0 && batch >= c->k3_min_batch;
     c->last_host_decisions = false;
-    // batch-1 decode: the filtered router (exact decisions, logits on demand)
-    if (batch == 1 && k.top_k == 2 && k.n_experts <= 32 && c->router_filtered) {
-      rp.filtered = 1;
+    // the filtered routers (exact decisions, logits on demand): batch-1 decode
+    // (HB_ROUTER=filtered, diagnostic) and batches of >= 16 tokens (default;
+    // HB_ROUTER=exact turns it off)
+    if (batch == 1 && k.top_k == 2 && k.n_experts <= 32 && c->router_filtered) rp.filtered = 1;
+    if (batch >= 16 && k.top_k == 2 && k.n_experts <= 64 && c->router_batch) rp.filtered_batch = 1;
+    if (rp.filtered || rp.filtered_batch) {
       rp.wnorm = c->wnorm + (size_t)layer * k.n_experts;
       rp.x_save = c->x_save;
       rp.logits = nullptr;
     }
-    c->last_filtered = rp.filtered != 0;
+    c->last_filtered = rp.filtered || rp.filtered_batch;
     if (!k3 && batch == 1 && c->fused_ok) {
       c->last_fused = true;
       c->last_filtered = false;
@@ -1107,7 +1112,7 @@ int hb_get_logits(hb_ctx* c, int64_t* out, int cap_pairs) {
   if (c->last_fused || c->last_filtered) {
     // the fused kernel decides without materialising the exact logits: run
     // the exact router on its saved copy of x (inspection only)
-    RouterParams rp = router_params(c, c->x_save, 1);
+    RouterParams rp = router_params(c, c->x_save, c->last_batch);
     rp.wg[0] = router_of(c, c->last_layer);
     rp.n_route = 1;
     rp.dec = c->dec_pred;

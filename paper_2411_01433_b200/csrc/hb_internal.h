@@ -129,6 +129,7 @@ struct RouterParams {
   long long* lbuf;                     // [n_route][B][E][2] exact logits (scratch)
   int* rowbad;                         // [n_route][B] non-finite x flags (scratch)
   int filtered;                        // decode (B = 1, k = 2, cluster): filtered router
+  int filtered_batch;                  // batches (one CTA per row): filtered router
   const float* wnorm;                  // [E] ||W_e||_2 of route layer 0 (filtered router)
   __half* x_save;                      // [H] copy of x (filtered router: lazy exact logits)
   long long* logits;                   // [B][E][2] copy for route 0, or null

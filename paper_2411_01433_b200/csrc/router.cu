@@ -222,6 +222,21 @@ struct RouterSmem {
   int last;
 };
 
+// Shared memory of the batch router kernel (router_batch_kernel): one CTA per
+// token, the filtered router, the job table built by the last CTA.
+struct BatchSmem {
+  float red[kRouterThreads / 32][64];  // per warp fp32 partial logit per expert
+  float xqw[kRouterThreads / 32];      // per warp sum of x^2
+  double Lf[64];                       // filtered logits of the row
+  u64 part[64][3];                     // exact fallback: per task partial
+  i128 L[64];                          // exact fallback: logits
+  const uint8_t* blob[64 * 4];         // blob table of the layer (last CTA)
+  Job jobs[2 * 64 + 1];
+  int count[2 * 64], jobid[2 * 64], fill[2 * 64];
+  unsigned long long hmask;
+  int ok, last;
+};
+
 // Shared memory of the decode router kernel (router_dec_kernel): one token,
 // top-2, E <= 32 experts, the filtered router with its exact fallback.
 struct DecSmem {
@@ -308,7 +323,8 @@ __device__ void build_jobs(const RouterParams& p, RouterSmem& sm, const hb_decis
 // by warp 0 (ballot ranks within each 32-selection chunk).  Same table as
 // build_jobs; the serial version read the decisions from global memory one
 // dependent load at a time (~0.5 us per selection at B = 512).
-__device__ void build_jobs_cta(const RouterParams& p, RouterSmem& sm, const hb_decision* dec) {
+template <typename SmemT>
+__device__ void build_jobs_cta(const RouterParams& p, SmemT& sm, const hb_decision* dec) {
   const int nkey = 2 * p.E, nsel = p.B * p.k, tid = threadIdx.x;
   for (int i = tid; i < nkey; i += blockDim.x) { sm.count[i] = 0; sm.fill[i] = 0; }
   if (tid == 0) sm.hmask = 0ull;
@@ -918,6 +934,202 @@ router_dec_kernel(const __grid_constant__ RouterParams p) {
   route_filtered<C>(p, sm, crank, s0, s1, 0, 0);
 }
 
+
+// Router for batches (n_route = 1, top-2, E <= 64): one CTA per token row,
+// the filtered router (fp32 products in FFMA chains, warp trees, fp64 sums
+// over warps, Cauchy-Schwarz bound; the exact integer path for a row whose
+// comparisons do not clear the bound), each row decided in its own CTA; the
+// last CTA builds the job table.  Extra CTAs zero the accumulation buffers.
+// Replaces the exact per-row partials of router_kernel<1> (R9').
+__global__ void __launch_bounds__(kRouterThreads)
+router_batch_kernel(const __grid_constant__ RouterParams p) {
+  __shared__ BatchSmem sm;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = kRouterThreads / 32;
+  if ((int)blockIdx.x >= p.B) {
+    zero_buffers(p, blockIdx.x - p.B, gridDim.x - p.B);
+    return;
+  }
+  const int b = blockIdx.x;
+  const int E = p.E, n8 = p.H / 8;
+  if (p.blob_table)
+    for (int i = tid; i < 4 * E; i += kRouterThreads) sm.blob[i] = p.blob_table[i];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const __half* x = p.x + (size_t)b * p.H;
+  const uint4* x4 = reinterpret_cast<const uint4*>(x);
+  const uint4* w4 = reinterpret_cast<const uint4*>(p.wg[0]);
+  int xbad = 0;
+  float xq = 0.f;
+  int nch = 0;
+  for (int c = tid; c < n8; c += kRouterThreads) ++nch;
+  for (int e0 = 0; e0 < E; e0 += 16) {
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+    for (int c = tid; c < n8; c += kRouterThreads) {
+      const uint4 xv = x4[c];
+      float xf[8];
+      r_h2f8(xv, xf);
+      if (e0 == 0) {
+        const uint32_t xa[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          xbad |= ((xa[q] & 0x7C00u) == 0x7C00u) | ((xa[q] & 0x7C000000u) == 0x7C000000u);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xq = fmaf(xf[q], xf[q], xq);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (e0 + j >= E) break;
+        float wf[8];
+        r_h2f8(w4[(size_t)(e0 + j) * n8 + c], wf);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[j] = fmaf(wf[q], xf[q], acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float v = acc[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && e0 + j < E) sm.red[warp][e0 + j] = v;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) xq += __shfl_xor_sync(0xffffffffu, xq, o);
+  if (lane == 0) sm.xqw[warp] = xq;
+  const int bad = __syncthreads_or(xbad);
+  if (p.x_save)                                     // lazy exact logits (hb_get_logits)
+    for (int c = tid; c < n8; c += kRouterThreads)
+      reinterpret_cast<uint4*>(p.x_save + (size_t)b * p.H)[c] = x4[c];
+  if (p.x_perm) write_xperm(p, x, 0, n8, b);
+  if (tid < E) {
+    double v = 0.0;
+    for (int w = 0; w < NW; ++w) v += (double)sm.red[w][tid];
+    sm.Lf[tid] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (bad) {
+      if (lane == 0) { decide_nonfinite(p, b, p.dec + (size_t)b * 2, nullptr); sm.ok = 1; }
+    } else {
+      double xs = 0.0;
+      for (int w = 0; w < NW; ++w) xs += (double)sm.xqw[w];
+      // error of a logit: chains of m = 8 * nch products (gamma_{m-1}), warp
+      // trees (gamma_5), fp64 sums over warps (negligible): (m + 6) 2^-24
+      // (1 + 1e-4) sum|p|, sum|p| <= ||w_e|| ||x|| (||x|| rounded up)
+      const int m = 8 * __shfl_sync(0xffffffffu, nch, 0);
+      const double xn = sqrt(xs) * (1.0 + 1e-6) + 1e-30;
+      const double cb = (m + 6) * 0x1p-24 * 1.0001;
+      double vh[2] = {-1e300, -1e300}, eh[2] = {0.0, 0.0};
+      int rk[2] = {64, 64};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = lane + 32 * h;
+        if (e < E) {
+          vh[h] = sm.Lf[e];
+          eh[h] = cb * (double)p.wnorm[e] * xn;
+          int r = 0;
+          for (int f = 0; f < E; ++f) { const double o = sm.Lf[f]; r += (o > vh[h]) || (o == vh[h] && f < e); }
+          rk[h] = r;
+        }
+      }
+      const unsigned m0 = __ballot_sync(0xffffffffu, rk[0] == 0), m0b = __ballot_sync(0xffffffffu, rk[1] == 0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, rk[0] == 1), m1b = __ballot_sync(0xffffffffu, rk[1] == 1);
+      const int e0 = m0 ? __ffs(m0) - 1 : 32 + __ffs(m0b) - 1;
+      const int e1 = m1 ? __ffs(m1) - 1 : 32 + __ffs(m1b) - 1;
+      double rest = -1e300;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (lane + 32 * h < E && rk[h] >= 2) rest = fmax(rest, vh[h] + eh[h]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rest = fmax(rest, __shfl_xor_sync(0xffffffffu, rest, o));
+      if (lane == 0) {
+        const double L0 = sm.Lf[e0], L1 = sm.Lf[e1];
+        const double ep0 = cb * (double)p.wnorm[e0] * xn, ep1 = cb * (double)p.wnorm[e1] * xn;
+        const double G = L0 - L1, mg = ep0 + ep1 + 1e-12 * (1.0 + fabs(L0) + fabs(L1));
+        bool ok = (L0 - ep0 > L1 + ep1) && (L1 - ep1 > rest);
+        if (p.th1_kind == 0) ok = ok && fabs(G - (double)p.theta1 * 0x1p-48) > mg;
+        if (p.th2_kind == 0) ok = ok && fabs(G - (double)p.theta2 * 0x1p-48) > mg;
+        if (ok) {
+          const uint8_t prec1 = (p.th1_kind > 0 || (p.th1_kind == 0 && G <= (double)p.theta1 * 0x1p-48)) ? HB_HIGH
+                              : (p.th2_kind > 0 || (p.th2_kind == 0 && G <= (double)p.theta2 * 0x1p-48)) ? HB_LOW
+                                                                                                      : HB_SKIP;
+          const float ex = expf(-(float)G);
+          const float g0 = 1.f / (1.f + ex), g1 = ex * g0;
+          hb_decision r0, r1;
+          r0.token = b; r0.expert = e0; r0.sel_rank = 0; r0.prec = HB_HIGH;
+          r0.served_enc = HB_ENC_NONE; r0.hit = 0; r0.gate = g0;
+          r1.token = b; r1.expert = e1; r1.sel_rank = 1; r1.prec = prec1;
+          r1.served_enc = HB_ENC_NONE; r1.hit = 0; r1.gate = g1;
+          p.dec[(size_t)b * 2] = r0;
+          p.dec[(size_t)b * 2 + 1] = r1;
+        }
+        sm.ok = ok;
+      }
+    }
+  }
+  __syncthreads();
+  if (!sm.ok) {
+    // ---- exact fallback for this row (rare): integer logits over all of H
+    const int wpe = E >= NW ? 1 : NW / E;
+    for (int task = warp; task < E * wpe; task += NW) {
+      const int e = task / wpe, part = task - e * wpe;
+      const uint4* we = w4 + (size_t)e * n8;
+      const int j0 = part * n8 / wpe, j1 = (part + 1) * n8 / wpe;
+      u64 lo = 0, mid = 0, hi = 0;
+      for (int j = j0 + lane; j < j1; j += 32) {
+        const uint4 wv = we[j];
+        const uint4 xv = x4[j];
+        const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
+        const uint32_t xa[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          accum_exact((wa[i >> 1] >> (16 * (i & 1))) & 0xFFFF, (xa[i >> 1] >> (16 * (i & 1))) & 0xFFFF,
+                      lo, mid, hi);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+        mid += __shfl_xor_sync(0xffffffffu, mid, o);
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+      if (lane == 0) { sm.part[task][0] = lo; sm.part[task][1] = mid; sm.part[task][2] = hi; }
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += blockDim.x) {
+      u64 lo = 0, mid = 0, hi = 0;
+      for (int q = 0; q < wpe; ++q) {
+        lo += sm.part[e * wpe + q][0]; mid += sm.part[e * wpe + q][1]; hi += sm.part[e * wpe + q][2];
+      }
+      sm.L[e] = (i128)(long long)lo + ((i128)(long long)mid << 20) + ((i128)(long long)hi << 40);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      if (E <= 32) {
+        decide_k2_warp(p, sm.L, b, p.dec + (size_t)b * 2, p.dec + (size_t)b * 2);
+      } else {
+        int sel[kMaxTopK];
+        topk_warp(p, sm.L, sel);
+        if (lane == 0) decide_sel(p, sm.L, sel, b, p.dec + (size_t)b * 2, nullptr);
+      }
+    }
+  }
+  if (tid == 0) p.rowbad[b] = bad;
+  // ---- the last row CTA builds the job table from every row's decisions
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    sm.last = atomicAdd(p.done, 1u) == (unsigned)p.B - 1;
+  }
+  __syncthreads();
+  if (!sm.last) return;
+  __threadfence();
+  if (p.blob_table) build_jobs_cta(p, sm, p.dec);
+  if (tid == 0) *p.done = 0u;
+}
+
 void launch_router(const RouterParams& p, cudaStream_t s) {
   // one 8-CTA cluster per (route layer, token) row, plus clusters of CTAs that
   // zero the GEMV accumulation buffers in parallel
@@ -940,9 +1152,13 @@ void launch_router(const RouterParams& p, cudaStream_t s) {
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
+  const bool batch = p.filtered_batch && p.n_route == 1 && C == 1 && p.k == 2 && p.E <= 64;
   if (dec) {
     cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, router_dec_kernel<kRouterCluster>, p);
+  } else if (batch) {
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, router_batch_kernel, p);
   } else if (C == 1) {
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, router_kernel<1>, p);

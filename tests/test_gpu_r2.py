@@ -277,14 +277,15 @@ def test_ep_two_processes_through_library(world, tmp_path):
 
 # ------------------------------------------------------------ non-finite inputs
 @pytest.mark.parametrize("mode", ["legacy", "fused"])
-@pytest.mark.parametrize("B,batched_min", [(1, 0), (3, 0), (12, 4)], ids=["B1", "B3", "K3-B12"])
+@pytest.mark.parametrize("B,batched_min", [(1, 0), (3, 0), (12, 4), (20, 4), (20, 0)],
+                         ids=["B1", "B3", "K3-B12", "K3-B20", "GEMV-B20"])
 def test_nonfinite_input_documented_behaviour(mode, B, batched_min, monkeypatch):
     """DESIGN.md R28: a token whose x holds an inf/nan gets Skip decisions
     (expert -1, gate NaN) and a NaN output row; every other token is
     unaffected (equal to the oracle)."""
     monkeypatch.setenv("HB_DECODE", mode)
     sh = sg.TINY
-    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=16, batched_min=batched_min)
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=32, batched_min=batched_min)
     store = OracleStore(sh)
     x16 = sg.hidden_states(sh, 47, 0, batch=B)
     bad = B // 2

@@ -110,7 +110,9 @@ def main():
             ka = sum(p[0] for p in prof)
             kb = sum(p[1] for p in prof)
             out = {"B": B, "path": path, "layers": L, "pair": args.pair, "model": args.model,
-                   "tok_s": round(B * 1000.0 / ms, 1), "ms_per_step": round(ms, 4),
+                   # tokens through all 32 layers of the model (the step runs L layers)
+                   "tok_s": round(B * L / 32 * 1000.0 / ms, 1), "ms_per_step": round(ms, 4),
+                   "tok_s_L_layers": round(B * 1000.0 / ms, 1),
                    "step_gbs": round((a_bytes + b_bytes) / ms / 1e6, 1),
                    "ka_gbs": round(a_bytes / ka / 1e6, 1), "kb_gbs": round(b_bytes / kb / 1e6, 1),
                    "kab_frac": round((a_bytes + b_bytes) / (ka + kb) / 1e6 / peak, 4),

@@ -126,7 +126,9 @@ def main():
         n = args.tokens
         out = {"config": "C4 constrained cache", "layers": L, "tokens": n, "rho": args.rho, "p": p,
                "t1": t1, "t2": t2, "eq3_weights": list(w), "cap_high": cap_h, "cap_low": cap_l,
-               "tok_s": round(n * 1000.0 / ms, 3), "ms_per_token": round(ms / n, 3),
+               # 32-layer tokens (the run covers L layers per token)
+               "tok_s": round(n * L / 32 * 1000.0 / ms, 3), "ms_per_token": round(ms / n, 3),
+               "tok_s_L_layers": round(n * 1000.0 / ms, 3),
                "wall_ms_per_token": round(wall * 1000 / n, 3),
                "h2d_bytes_per_token": int(h2d / n), "h2d_gbs": round(h2d / (ms * 1e-3) / 1e9, 2),
                "h2d_peak_gbs": round(peak, 2), "h2d_frac": round(h2d / (ms * 1e-3) / 1e9 / peak, 4),
