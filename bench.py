@@ -127,15 +127,22 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ our arm
-def build_model(h, sg, fm, shape, hi, lo, rank, world, dev, t1=0.6, t2=0.9, max_batch=1, layers=None):
+def build_model(h, sg, fm, shape, hi, lo, rank, world, dev, t1=0.6, t2=0.9, max_batch=1, layers=None,
+                tp_rank=0, tp_world=1):
+    """Random-init weights of the shape (seeded generator), quantised on the
+    GPU and registered resident.  EP (world > 1): this rank's experts
+    (e % world == rank).  TP-within-expert (tp_world > 1): every expert, rows
+    [r F/R, (r+1) F/R) of W1/W3 and those columns of W2."""
     import torch
+    H, F = shape.hidden, shape.ffn
+    Fs = F // tp_world
     cfg = h.default_config(n_layers=shape.n_layers, n_experts=shape.n_experts, top_k=shape.top_k,
-                           hidden=shape.hidden, ffn=shape.ffn, hi_enc=hi, lo_enc=lo, t1=t1,
+                           hidden=H, ffn=Fs, hi_enc=hi, lo_enc=lo, t1=t1,
                            t2=t2, max_batch=max_batch, rank=rank, world=world)
     ctx = h.Context(cfg, dev)
-    H, F = shape.hidden, shape.ffn
     tmp = [torch.empty(n * k, dtype=torch.float16, device="cuda")
            for n, k in ((F, H), (F, H), (H, F))]
+    f0, f1 = tp_rank * Fs, (tp_rank + 1) * Fs
     blobs = []
     for l in range(shape.n_layers if layers is None else layers):
         ctx.set_router(l, sg.router_weights(shape, l))
@@ -146,10 +153,14 @@ def build_model(h, sg, fm, shape, hi, lo, rank, world, dev, t1=0.6, t2=0.9, max_
                 h.synth_fill(t, sg.expert_key(sg.DEFAULT_SEED, l, e, mat),
                              float(sg.scale_f32(sg.expert_sigma(shape, mat))))
             ws = [tmp[0].view(F, H), tmp[1].view(F, H), tmp[2].view(H, F)]
+            if tp_world > 1:
+                ws = [ws[0][f0:f1].contiguous(), ws[1][f0:f1].contiguous(),
+                      ws[2][:, f0:f1].contiguous()]
             for enc in (hi, lo):
                 b = h.quantize_expert(enc, *ws)
                 ctx.register_expert(l, e, enc, b)
                 blobs.append(b)
+            del ws
     del tmp
     torch.cuda.synchronize()
     return ctx, blobs
@@ -168,20 +179,38 @@ def run_ours(args):
     if args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun "
                          f"(python -m torch.distributed.run --nproc-per-node N bench.py --gpus N)")
+    # HB_BENCH_SAME_GPU=1 (plumbing check only, never a measurement): every
+    # rank on cuda:0, gloo, torch all-reduce -- the N > 1 code path on one GPU
+    same_gpu = os.environ.get("HB_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
+        os.environ["HB_BENCH_TORCH_ALLREDUCE"] = "1"
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     shape = {"mixtral": sg.MIXTRAL, "phi": sg.PHI}[args.model]
     hi, lo = PAIRS[args.pair]
     L, Hd = shape.n_layers, shape.hidden
+    # N > 1: TP-within-expert (every rank streams 1/N of every selected
+    # expert: batch-1 decode scales with N) when F/N is a multiple of 256,
+    # else expert parallelism (e % N; top-2 of 8 caps batch-1 at ~1.5x)
+    par = args.parallel
+    if par == "auto":
+        par = "tp" if world > 1 and (shape.ffn // world) % 256 == 0 and shape.ffn % world == 0 else "ep"
+    tp = par == "tp" and world > 1
     t_init = time.time()
-    ctx, blobs = build_model(h, sg, None, shape, hi, lo, rank, world, local, t1=args.t1, t2=args.t2)
-    # EP exchange (A10): by default inside the library (hb_nccl_init: the
-    # forward ends with the NCCL all-reduce of y); HB_BENCH_TORCH_ALLREDUCE=1
-    # reduces with torch.distributed instead
+    ctx, blobs = build_model(h, sg, None, shape, hi, lo, 0 if tp else rank, 1 if tp else world,
+                             local, t1=args.t1, t2=args.t2, tp_rank=rank if tp else 0,
+                             tp_world=world if tp else 1)
+    # the exchange (A10) inside the library: the forward ends with the NCCL
+    # all-reduce of y over the ranks; HB_BENCH_TORCH_ALLREDUCE=1 reduces with
+    # torch.distributed instead (eager)
     torch_reduce = world > 1 and os.environ.get("HB_BENCH_TORCH_ALLREDUCE") == "1"
     if world > 1 and not torch_reduce:
-        ctx.nccl_init()
+        ctx.nccl_init(tp=tp)
     t_init = time.time() - t_init
 
     # token inputs: a pool of P tokens x 32 layers, resident on the device
@@ -200,7 +229,8 @@ def run_ours(args):
                     dist.all_reduce(Y[l])
 
     # ---- realised algorithmic bytes of the pool's tokens (decisions, untimed)
-    blob_b = {hi: h.blob_bytes(hi, Hd, shape.ffn), lo: h.blob_bytes(lo, Hd, shape.ffn)}
+    Fr = shape.ffn // world if tp else shape.ffn          # this rank's F (TP slice)
+    blob_b = {hi: h.blob_bytes(hi, Hd, Fr), lo: h.blob_bytes(lo, Hd, Fr)}
     # SURVEY 8(d) unit: served blob bytes + router W_g + x + y + h (write + read)
     bytes_tok = []
     mix = [0, 0, 0]
@@ -212,7 +242,7 @@ def run_ours(args):
             for d in ctx.decisions(1):
                 mix[d.prec] += 1
                 if d.served_enc != h.HB_ENC_NONE:
-                    tot += blob_b[d.served_enc] + 2 * 4 * shape.ffn
+                    tot += blob_b[d.served_enc] + 2 * 4 * Fr
             tot += 2 * shape.n_experts * Hd + 2 * Hd + 4 * Hd
         bytes_tok.append(tot)
     torch.cuda.synchronize()
@@ -222,7 +252,7 @@ def run_ours(args):
         for m in mats:
             for sec in range(3):
                 try:
-                    tot += h.blob_section(enc, Hd, shape.ffn, m, sec)[1]
+                    tot += h.blob_section(enc, Hd, Fr, m, sec)[1]
                 except h.HobbitError:
                     pass
         return tot
@@ -333,8 +363,8 @@ def run_ours(args):
                             ne += 1
                     # SURVEY 8(d) unit split over the two kernels: K2a = W1/W3 +
                     # x + h written (4F per expert); K2b = W2 + h read + y
-                    k2a_b.append(a + 2 * Hd + 4 * shape.ffn * ne)
-                    k2b_b.append(b + 4 * shape.ffn * ne + 4 * Hd)
+                    k2a_b.append(a + 2 * Hd + 4 * Fr * ne)
+                    k2b_b.append(b + 4 * Fr * ne + 4 * Hd)
         n = min(len(rec), len(k2a_b))
         k2a_ns = rec[:n, 2] - rec[:n, 0]
         k2b_ns = rec[:n, 4] - rec[:n, 3]
@@ -400,7 +430,8 @@ def run_ours(args):
                    else f"DIAGNOSTIC {shape.name} pair {args.pair} (not the headline workload)",
                    "global_batch": 1, "layers": L, "experts": shape.n_experts,
                    "top_k": shape.top_k, "hidden": Hd, "ffn": shape.ffn, "pair": args.pair,
-                   "parallelism": f"ep{world}", "l2": "inputs > L2 (~17 GB of weights per step)",
+                   "parallelism": f"{'tp' if tp else 'ep'}{world}",
+                   "l2": "inputs > L2 (~17 GB of weights per step)",
                    "graph": use_graph},
         "e2e": {"value": round(1000.0 / ms_e2e, 3), "unit": UNIT,
                 "h2d_bytes_per_step": L * Hd * 2, "d2h_bytes_per_step": L * Hd * 4},
@@ -589,6 +620,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batched", action="store_true", help="skip the K3 batched/prefill extra")
     ap.add_argument("--no-roofline", action="store_true", help="diagnostics: skip the stamped replay")
+    ap.add_argument("--parallel", choices=["auto", "ep", "tp"], default="auto",
+                    help="N > 1: expert parallel or TP-within-expert (auto: tp when F/N fits)")
     ap.add_argument("--t1", type=float, default=0.6, help="diagnostics only (1.0/1.0 = all-High)")
     ap.add_argument("--t2", type=float, default=0.9, help="diagnostics only")
     ap.add_argument("--cpu-sample", type=int, default=2)

@@ -226,6 +226,12 @@ int hb_set_batched_min(hb_ctx* ctx, int min_batch);
  * HB_EUNSUPPORTED if it cannot be found. */
 int hb_nccl_unique_id(void* unique_id_out /* 128 bytes */);
 int hb_nccl_init(hb_ctx* ctx, const void* unique_id);
+/* The same over an explicit group of nranks ranks (this one = rank), for
+ * TP-within-expert: every rank owns every expert (cfg.world
+ * = 1) but holds the slice [r F/R, (r+1) F/R) of each expert's W1/W3 rows
+ * and W2 columns (a context created with ffn = F/R and blobs quantised from
+ * those slices); the library sums the partial y over the group. */
+int hb_nccl_init_ranks(hb_ctx* ctx, const void* unique_id, int nranks, int rank);
 /* X1: replicate the gating input x [batch, hidden] fp16 (device,
  * caller-owned) from EP rank `root` to every rank, in place, on `stream`
  * (ncclBroadcast; collective, after hb_nccl_init; HB_ESTATE without it). */

@@ -89,15 +89,25 @@ def owner(expert: int, world: int) -> int:
     return expert % world
 
 
+def tp_slice(w1: np.ndarray, w3: np.ndarray, w2: np.ndarray, tp_rank: int, tp_world: int):
+    """TP-within-expert: rank r of R holds rows [r F/R, (r+1) F/R)
+    of W1 and W3 and the same columns of W2.  SwiGLU acts row by row of F and
+    W2 h sums over F, so E(x) = sum_r W2[:, s_r] (silu(W1[s_r] x) * W3[s_r] x)."""
+    F = w1.shape[0]
+    f0, f1 = tp_rank * F // tp_world, (tp_rank + 1) * F // tp_world
+    return w1[f0:f1], w3[f0:f1], w2[:, f0:f1]
+
+
 def moe_layer(x16: np.ndarray, wg16: np.ndarray, store: ExpertStore, layer: int,
               k: int, t1: float, t2: float, hi_enc: int, lo_enc: int,
-              rank: int = 0, world: int = 1, served=None):
+              rank: int = 0, world: int = 1, served=None, tp_rank: int = 0, tp_world: int = 1):
     """One MoE layer for tokens x16 [B,H] (fp16): returns (y fp64 [B,H], routes).
 
     served[b][i], if given, overrides O7 with the encoding the cache state
     machine chose (O9); None there means Skip.  With world > 1 only the
     experts this rank owns are computed (O11): the layer output is the sum of
-    the per-rank outputs.
+    the per-rank outputs.  With tp_world > 1 every expert is computed on this
+    rank's slice of F (tp_slice): the layer output is again the sum over ranks.
     """
     routes = route(x16, wg16, k, t1, t2)
     B, H = x16.shape
@@ -111,6 +121,8 @@ def moe_layer(x16: np.ndarray, wg16: np.ndarray, store: ExpertStore, layer: int,
             if enc is None:
                 continue
             w1, w3, w2 = store.get(layer, e, enc)
+            if tp_world > 1:
+                w1, w3, w2 = tp_slice(w1, w3, w2, tp_rank, tp_world)
             y[b] += g * expert_ffn(w1, w3, w2, x)
     return y, routes
 

@@ -89,6 +89,7 @@ _SIGS = {
     "hb_nccl_unique_id": (C.c_int, [_P]),
     "hb_nccl_init": (C.c_int, [_P, _P]),
     "hb_ep_broadcast_x": (C.c_int, [_P, _P, C.c_int, C.c_int, _P]),
+    "hb_nccl_init_ranks": (C.c_int, [_P, _P, C.c_int, C.c_int]),
     "hb_profile": (C.c_int, [_P, C.c_int]),
     "hb_profile_read": (C.c_int, [_P, C.POINTER(C.c_float), C.c_int]),
     "hb_stamps": (C.c_int, [_P, C.c_int]),

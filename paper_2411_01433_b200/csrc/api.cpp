@@ -1163,15 +1163,27 @@ int hb_nccl_unique_id(void* out) {
   return HB_OK;
 }
 
+static int nccl_init_ranks(hb_ctx* c, const void* unique_id, int nranks, int rank);
+
 int hb_nccl_init(hb_ctx* c, const void* unique_id) {
   if (!c || !unique_id) return fail(c, HB_EINVAL, "null argument");
+  return nccl_init_ranks(c, unique_id, c->cfg.world, c->cfg.rank);
+}
+
+int hb_nccl_init_ranks(hb_ctx* c, const void* unique_id, int nranks, int rank) {
+  if (!c || !unique_id) return fail(c, HB_EINVAL, "null argument");
+  if (nranks <= 0 || rank < 0 || rank >= nranks) return fail(c, HB_EINVAL, "bad nranks / rank");
+  return nccl_init_ranks(c, unique_id, nranks, rank);
+}
+
+static int nccl_init_ranks(hb_ctx* c, const void* unique_id, int nranks, int rank) {
   NcclApi& api = nccl_api();
   if (!api.ok) return fail(c, HB_EUNSUPPORTED, "libnccl.so.2 not found (HB_NCCL_LIB)");
   if (c->nccl_comm) return fail(c, HB_ESTATE, "NCCL communicator already initialised");
   NcclId id;
   std::memcpy(&id, unique_id, sizeof(id));
   CUDA_TRY(c, cudaSetDevice(c->device));
-  const int r = api.comm_init_rank(&c->nccl_comm, c->cfg.world, id, c->cfg.rank);
+  const int r = api.comm_init_rank(&c->nccl_comm, nranks, id, rank);
   if (r != 0) {
     c->nccl_comm = nullptr;
     return fail(c, HB_ENCCL, std::string("ncclCommInitRank: ") +

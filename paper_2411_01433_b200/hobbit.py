@@ -175,19 +175,27 @@ class Context:
         n = self._check(lib.hb_stamps_read(self._h, buf, cap))
         return [tuple(buf[15 * i:15 * i + 15]) for i in range(n)]
 
-    def nccl_init(self, group=None):
+    def nccl_init(self, group=None, tp: bool = False):
         """EP exchange inside the library (A10): rank 0 makes an NCCL unique id,
         torch.distributed broadcasts it, every rank joins; afterwards forward()
-        returns the EP-reduced y.  Single process (no process group): world 1."""
+        returns the reduced y.  tp=True: the group is the torch.distributed
+        group (TP-within-expert, hb_nccl_init_ranks) instead of cfg.rank/world.
+        Single process (no process group): world 1."""
         import torch.distributed as dist
         uid = (C.c_char * 128)()
-        if not dist.is_available() or not dist.is_initialized() or dist.get_rank(group) == 0:
+        dist_on = dist.is_available() and dist.is_initialized()
+        if not dist_on or dist.get_rank(group) == 0:
             check(lib.hb_nccl_unique_id(uid))
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if dist_on and dist.get_world_size(group) > 1:
             obj = [bytes(uid)]
             dist.broadcast_object_list(obj, src=0, group=group)
             C.memmove(uid, obj[0], 128)
-        self._check(lib.hb_nccl_init(self._h, uid))
+        if tp:
+            n = dist.get_world_size(group) if dist_on else 1
+            r = dist.get_rank(group) if dist_on else 0
+            self._check(lib.hb_nccl_init_ranks(self._h, uid, n, r))
+        else:
+            self._check(lib.hb_nccl_init(self._h, uid))
 
     def broadcast_x(self, x: torch.Tensor, root: int = 0, stream=None):
         """X1: x [B,H] fp16 (device) replicated from EP rank root, in place."""

@@ -82,3 +82,42 @@ def test_ep_gloo_allreduce_equals_single_process(world):
     used = {e for r in routes for e, d in zip(r.experts, r.decisions) if d != rt.SKIP}
     for e in range(SH.n_experts):
         assert own[e] == ((om.owner(e, world) + 1) if e in used else 0), (e, own)
+
+
+def _tp_worker(rank, world, port, out_dir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        x16 = sg.hidden_states(SH, 32, LAYER, batch=B)
+        wg = sg.router_weights(SH, LAYER)
+        y, _ = om.moe_layer(x16, wg, _store(), LAYER, SH.top_k, 0.6, 0.9, fm.F16, fm.Q4,
+                            tp_rank=rank, tp_world=world)
+        t = torch.from_numpy(np.ascontiguousarray(y))
+        dist.all_reduce(t)                      # partial experts summed over the ranks
+        if rank == 0:
+            np.save(os.path.join(out_dir, "y.npy"), t.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_tp_within_expert_gloo_equals_single_process(world):
+    """SURVEY 8(f) f3, TP-within-expert: every rank computes every selected
+    expert on its slice of F (rows of W1/W3, columns of W2); the all-reduced
+    sum equals the single-process layer (fp64, to rounding)."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_tp_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        y = np.load(os.path.join(d, "y.npy"))
+    x16 = sg.hidden_states(SH, 32, LAYER, batch=B)
+    ref, _ = om.moe_layer(x16, sg.router_weights(SH, LAYER), _store(), LAYER, SH.top_k,
+                          0.6, 0.9, fm.F16, fm.Q4)
+    np.testing.assert_allclose(y, ref, rtol=1e-10, atol=1e-12)
+
+
+def test_tp_slice_is_a_restriction():
+    """tp_slice picks rows of W1/W3 and the matching columns of W2 only."""
+    w1 = np.arange(8 * 4).reshape(8, 4).astype(float)
+    w3 = -w1
+    w2 = np.arange(4 * 8).reshape(4, 8).astype(float)
+    a, b, c = om.tp_slice(w1, w3, w2, 1, 2)
+    assert np.array_equal(a, w1[4:]) and np.array_equal(b, w3[4:]) and np.array_equal(c, w2[:, 4:])

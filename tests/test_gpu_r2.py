@@ -369,3 +369,70 @@ def test_offload_slot_war_ordering():
         ref, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9, fm.F16, fm.Q4,
                               served=[served])
         assert rel_err(y.cpu().numpy()[0], ref[0])[0] <= 1e-4
+
+
+# ------------------------------------------------------------ TP-within-expert
+def _tp_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2411_01433_b200 import hobbit as h
+    from tests.gpu_util import gpu_expert_f16
+    sh = sg.TINY
+    Fs = sh.ffn // world
+    f0, f1 = rank * Fs, (rank + 1) * Fs
+    results = []
+    for B, bm in ((1, 0), (3, 0), (24, 4)):
+        cfg = h.default_config(n_layers=2, n_experts=8, top_k=2, hidden=sh.hidden, ffn=Fs,
+                               hi_enc=fm.F16, lo_enc=fm.Q4, max_batch=B)
+        ctx = h.Context(cfg)
+        if B > 1:
+            ctx.set_batched_min(bm)
+        keep = []
+        for l in range(2):
+            ctx.set_router(l, sg.router_weights(sh, l))
+            for e in range(8):
+                w1, w3, w2 = gpu_expert_f16(sh, l, e)
+                ws = [w1[f0:f1].contiguous(), w3[f0:f1].contiguous(), w2[:, f0:f1].contiguous()]
+                for enc in (fm.F16, fm.Q4):
+                    b = h.quantize_expert(enc, *ws)
+                    ctx.register_expert(l, e, enc, b)
+                    keep.append(b)
+        for l in range(2):
+            x16 = sg.hidden_states(sh, 90, l, batch=B)
+            y = torch.from_numpy(_run(ctx, l, x16))
+            dist.all_reduce(y)                       # partial experts summed over the ranks
+            results.append(y.numpy())
+        ctx.close()
+    if rank == 0:
+        np.save(out_path, np.concatenate([r.ravel() for r in results]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_tp_within_expert_two_processes_through_library(tmp_path):
+    """two processes (one context each, same GPU), each with
+    every expert's F/2 slice (rows of W1/W3, columns of W2, quantised by the
+    library); the gloo sum of the partial outputs equals the oracle's layer,
+    on the decode (B = 1), GEMV batch and tcgen05 (K3) paths."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "tp.npy")
+    mp.start_processes(_tp_worker, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    got = np.load(out)
+    sh = sg.TINY
+    store = OracleStore(sh)
+    off = 0
+    for B in (1, 3, 24):
+        for l in range(2):
+            x16 = sg.hidden_states(sh, 90, l, batch=B)
+            ref, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9, fm.F16, fm.Q4)
+            y = got[off:off + ref.size].reshape(ref.shape)
+            off += ref.size
+            bar = 1e-4 if B < 4 else 1e-3
+            for b in range(B):
+                assert rel_err(y[b], ref[b])[0] <= bar
