@@ -79,8 +79,9 @@ typedef struct {
   int hidden, ffn;                  /* H, F: multiples of 256 */
   int hi_enc, lo_enc;               /* precision pair, default HB_F16 / HB_Q4 */
   double t1, t2;                    /* thresholds, default 0.6 / 0.9; 0<=t1<=t2 */
-  int lookahead_p;                  /* prefetch depth p; 0 = off */
-  int w_lru, w_lfu, w_lhu, w_fld;   /* Eq. 3 weights as integer numerators, sum > 0 */
+  int lookahead_p;                  /* prefetch depth p in [0, 4]; 0 = off */
+  int w_lru, w_lfu, w_lhu, w_fld;   /* Eq. 3 weights as integer numerators >= 0; all 0 =
+                                       the Random policy (P:1040 normaliser, R29) */
   int cap_high, cap_low;            /* slots per pool on this rank; -1 = fully resident */
   int allow_upgrade;                /* Low request served by a cached High copy (1) */
   int rank, world;                  /* EP: owner(e) = e % world */

@@ -46,8 +46,12 @@ class ExpertCache:
         self.E = n_experts
         self.pools = {POOL_HIGH: [None] * cap_high, POOL_LOW: [None] * cap_low}
         self.w = tuple(int(v) for v in weights)
-        if len(self.w) != 4 or min(self.w) < 0 or sum(self.w) <= 0:
-            raise ValueError("weights must be 4 non-negative ints, sum > 0")
+        if len(self.w) != 4 or min(self.w) < 0:
+            raise ValueError("weights must be 4 non-negative ints")
+        # all four weights 0: the Random policy of fig:cache-policy-verify
+        # (the normaliser of the policy comparison; R29)
+        self.random = sum(self.w) == 0
+        self.n_evict = 0
         self.hi_enc, self.lo_enc = hi_enc, lo_enc
         self.allow_upgrade = allow_upgrade
         self.rank, self.world = rank, world
@@ -78,6 +82,20 @@ class ExpertCache:
         return (ln * (a * self.R.get(key, 0) + b * self.F.get(key, 0) + c * self.H.get(key, 0))
                 + d * self.T * (ln - ((lt - cur_layer + ln) % ln)))
 
+    @staticmethod
+    def _mix64(z):
+        """splitmix64 finaliser (the counter-based generator the Random policy
+        draws from; the library implements the same one)."""
+        z &= (1 << 64) - 1
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & ((1 << 64) - 1)
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & ((1 << 64) - 1)
+        return z ^ (z >> 31)
+
+    def random_priority(self, key):
+        """Random policy: a uniform draw per (eviction, member) --
+        mix64(mix64(T * 2^32 + n_evict) + key); the argmin is the victim."""
+        return self._mix64(self._mix64((self.T << 32) + self.n_evict) + key)
+
     def _use(self, key, high):
         self.R[key] = self.T
         self.F[key] = self.F.get(key, 0) + 1
@@ -95,7 +113,8 @@ class ExpertCache:
         for i, k in enumerate(slots):
             if k in self.mask or k in exclude:
                 continue
-            cand = (self.priority(k, cur_layer), k // self.E, k % self.E, i)
+            pr = self.random_priority(k) if self.random else self.priority(k, cur_layer)
+            cand = (pr, k // self.E, k % self.E, i)
             if best is None or cand < best:
                 best = cand
         if best is None:
@@ -103,6 +122,7 @@ class ExpertCache:
         i = best[3]
         victim = slots[i]
         slots[i] = key
+        self.n_evict += 1
         return i, victim
 
     # ------------------------------------------------------------ API

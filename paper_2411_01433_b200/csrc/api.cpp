@@ -85,6 +85,16 @@ struct hb_ctx {
   size_t slot_bytes[2] = {0, 0};
   std::vector<cudaEvent_t> slot_ready[2], slot_free[2];
   cudaStream_t copy_stream = nullptr;
+  // chunked, cancellable prefetch: prefetch copies are
+  // queued on the host and issued in chunks within a window of bytes in
+  // flight; on-demand copies are issued at once (ahead of the unissued
+  // chunks); a prefetch whose slot is reused before it was issued is dropped;
+  // a hit on a slot whose prefetch is still queued issues the rest first.
+  struct PfLoad { int pool, slot; const uint8_t* src; uint8_t* dst; size_t total, issued; };
+  std::vector<PfLoad> pf_queue;
+  std::vector<std::pair<cudaEvent_t, size_t>> pf_inflight;   // issued chunks (event, bytes)
+  std::vector<cudaEvent_t> pf_event_pool;
+  size_t pf_window = 64ull << 20, pf_chunk = 16ull << 20;     // HB_PREFETCH_WINDOW_MB / _CHUNK_MB
   ExpertCache* cache = nullptr;
   std::vector<hb_event> log;
   // scratch
@@ -305,6 +315,8 @@ static void free_ctx(hb_ctx* c) {
     for (cudaEvent_t e : c->slot_free[i]) cudaEventDestroy(e);
   }
   if (c->dec_ready) cudaEventDestroy(c->dec_ready);
+  for (auto& pe : c->pf_inflight) cudaEventDestroy(pe.first);
+  for (cudaEvent_t e : c->pf_event_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->nccl_comm) nccl_api().comm_destroy(c->nccl_comm);
@@ -326,10 +338,9 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   if (k.world <= 0 || k.rank < 0 || k.rank >= k.world) return fail(nullptr, HB_EINVAL, "bad rank/world");
   if (k.max_batch <= 0) return fail(nullptr, HB_EINVAL, "max_batch must be > 0");
   if (k.lookahead_p < 0 || k.lookahead_p > kMaxRouteLayers - 1)
-    return fail(nullptr, HB_EINVAL, "lookahead_p must be in [0, 3]");
-  if (k.w_lru < 0 || k.w_lfu < 0 || k.w_lhu < 0 || k.w_fld < 0 ||
-      k.w_lru + k.w_lfu + k.w_lhu + k.w_fld <= 0)
-    return fail(nullptr, HB_EINVAL, "Eq. 3 weights must be >= 0 with a positive sum");
+    return fail(nullptr, HB_EINVAL, "lookahead_p must be in [0, 4]");
+  if (k.w_lru < 0 || k.w_lfu < 0 || k.w_lhu < 0 || k.w_fld < 0)
+    return fail(nullptr, HB_EINVAL, "Eq. 3 weights must be >= 0 (all 0: Random policy)");
   const bool resident = k.cap_high < 0 && k.cap_low < 0;
   if (!resident && (k.cap_high < 0 || k.cap_low < 0))
     return fail(nullptr, HB_EINVAL, "cap_high and cap_low must both be -1 or both >= 0");
@@ -424,6 +435,10 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     c->fused_router = mode == "router";
     // measured slower (K2a CTAs held at the barrier: K2b's prologue cannot
     // overlap the K2a tail), kept as a diagnostic variant
+    const char* pw = std::getenv("HB_PREFETCH_WINDOW_MB");
+    if (pw) c->pf_window = (size_t)std::max(0, std::atoi(pw)) << 20;
+    const char* pc = std::getenv("HB_PREFETCH_CHUNK_MB");
+    if (pc) c->pf_chunk = (size_t)std::max(1, std::atoi(pc)) << 20;
     const char* hk = std::getenv("HB_HFIN_TAIL");
     c->hfin_tail = hk && hk[0] == '1';
     const char* re = std::getenv("HB_ROUTER");
@@ -631,8 +646,13 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
   return HB_OK;
 }
 
+static int pf_top_up(hb_ctx* c);
+
 int hb_token_begin(hb_ctx* c) {
   if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  if (c->cache) {
+    if (int rc = pf_top_up(c)) return rc;
+  }
   if (c->cache) c->cache->token_begin();
   c->token_started = true;
   return HB_OK;
@@ -853,7 +873,67 @@ static const __half* router_of(hb_ctx* c, int layer) {
   return c->wg + (size_t)layer * c->cfg.n_experts * c->cfg.hidden;
 }
 
-// queue the host->device copies of the load events [from, end) of the cache log
+// ---- copies of expert loads (the Dynamic Expert Loader)
+static int pf_issue_chunk(hb_ctx* c, hb_ctx::PfLoad& L) {
+  const size_t n = std::min(c->pf_chunk, L.total - L.issued);
+  if (L.issued == 0)   // WAR: every earlier reader of the slot is done before it is overwritten
+    CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[L.pool][L.slot], 0));
+  CUDA_TRY(c, cudaMemcpyAsync(L.dst + L.issued, L.src + L.issued, n, cudaMemcpyHostToDevice,
+                              c->copy_stream));
+  L.issued += n;
+  cudaEvent_t ev;
+  if (c->pf_event_pool.empty()) {
+    CUDA_TRY(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  } else {
+    ev = c->pf_event_pool.back();
+    c->pf_event_pool.pop_back();
+  }
+  CUDA_TRY(c, cudaEventRecord(ev, c->copy_stream));
+  c->pf_inflight.emplace_back(ev, n);
+  if (L.issued == L.total) CUDA_TRY(c, cudaEventRecord(c->slot_ready[L.pool][L.slot], c->copy_stream));
+  return HB_OK;
+}
+
+// keep up to pf_window bytes of prefetch chunks in flight on the copy stream
+static int pf_top_up(hb_ctx* c) {
+  size_t busy = 0;
+  std::vector<std::pair<cudaEvent_t, size_t>> keep;
+  for (auto& pe : c->pf_inflight) {
+    if (cudaEventQuery(pe.first) == cudaSuccess) {
+      c->pf_event_pool.push_back(pe.first);
+    } else {
+      busy += pe.second;
+      keep.push_back(pe);
+    }
+  }
+  c->pf_inflight.swap(keep);
+  while (!c->pf_queue.empty() && (busy < c->pf_window || c->pf_window == 0)) {
+    hb_ctx::PfLoad& L = c->pf_queue.front();
+    const size_t before = L.issued;
+    if (int rc = pf_issue_chunk(c, L)) return rc;
+    busy += L.issued - before;
+    if (L.issued == L.total) c->pf_queue.erase(c->pf_queue.begin());
+  }
+  return HB_OK;
+}
+
+// a queued prefetch into (pool, slot): issue the rest now (a hit needs the
+// data) or drop it (the slot is being reused for another key)
+static int pf_settle(hb_ctx* c, int pool, int slot, bool issue) {
+  for (size_t i = 0; i < c->pf_queue.size(); ++i) {
+    hb_ctx::PfLoad& L = c->pf_queue[i];
+    if (L.pool != pool || L.slot != slot) continue;
+    if (issue)
+      while (L.issued < L.total)
+        if (int rc = pf_issue_chunk(c, L)) return rc;
+    c->pf_queue.erase(c->pf_queue.begin() + i);
+    return HB_OK;
+  }
+  return HB_OK;
+}
+
+// queue the host->device copies of the load events [from, end) of the cache
+// log: on-demand / explicit loads at once, prefetch loads into the chunk queue
 static int issue_loads(hb_ctx* c, size_t from) {
   std::vector<hb_event>& ev = c->cache->events;
   for (size_t i = from; i < ev.size(); ++i) {
@@ -864,6 +944,11 @@ static int issue_loads(hb_ctx* c, size_t from) {
     const uint8_t* src = c->host_blob[idx];
     if (!src) return fail(c, HB_ESTATE, "expert blob not registered for a load");
     uint8_t* dst = c->pool_mem[pool] + (size_t)e.slot * c->slot_bytes[pool];
+    if (int rc = pf_settle(c, pool, e.slot, false)) return rc;   // reused: drop its queued prefetch
+    if (e.kind == 1 && c->pf_window > 0) {
+      c->pf_queue.push_back(hb_ctx::PfLoad{pool, e.slot, src, dst, c->bbytes[e.enc], 0});
+      continue;
+    }
     // WAR: every earlier reader of this slot must be done before it is overwritten
     CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[pool][e.slot], 0));
     CUDA_TRY(c, cudaMemcpyAsync(dst, src, c->bbytes[e.enc], cudaMemcpyHostToDevice, c->copy_stream));
@@ -974,6 +1059,10 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   rc = issue_loads(c, ev0);
   drain_events(c);
   if (rc) return rc;
+  for (int i = 0; i < K; ++i)               // served slots with a queued prefetch: issue it now
+    if (served[i] != HB_ENC_NONE)
+      if (int r2 = pf_settle(c, pool[i], slot[i], true)) return r2;
+  if (int r2 = pf_top_up(c)) return r2;
   // job table on the host: one job per non-skipped owned selection
   uint8_t* jh = (uint8_t*)c->jt_host;
   int32_t* hdr = (int32_t*)jh;
@@ -1033,6 +1122,7 @@ int expert_cache_load(hb_ctx* c, int layer, int expert, int enc, void* stream) {
   CUDA_TRY(c, cudaSetDevice(c->device));
   rc = issue_loads(c, ev0);
   drain_events(c);
+  if (!rc) rc = pf_top_up(c);
   return rc;
 }
 
@@ -1086,6 +1176,7 @@ int prefetch_next_layer(hb_ctx* c, int layer, const void* x, int batch, void* st
   for (size_t i = ev0; i < c->cache->events.size(); ++i) queued += c->cache->events[i].type == 1;
   rc = issue_loads(c, ev0);
   drain_events(c);
+  if (!rc) rc = pf_top_up(c);
   return rc ? rc : queued;
 }
 

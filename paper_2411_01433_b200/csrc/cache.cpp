@@ -14,6 +14,7 @@ ExpertCache::ExpertCache(int n_layers, int n_experts, int top_k, int cap_high, i
     : L_(n_layers), E_(n_experts), K_(top_k), hi_enc_(hi_enc), lo_enc_(lo_enc),
       upgrade_(allow_upgrade), rank_(rank), world_(world) {
   for (int i = 0; i < 4; ++i) w_[i] = w[i];
+  random_ = w[0] + w[1] + w[2] + w[3] == 0;
   const int nkeys = L_ * E_;
   pool_[POOL_HIGH].assign(std::max(cap_high, 0), -1);
   pool_[POOL_LOW].assign(std::max(cap_low, 0), -1);
@@ -73,10 +74,20 @@ int ExpertCache::insert(int pool, int key, int cur_layer, bool exclude_current) 
   int victim = -1;
   if (victim_slot < 0) {
     int64_t bp = 0;
+    uint64_t br = 0;
     int bk = -1;
     for (size_t i = 0; i < slots.size(); ++i) {
       const int k = slots[i];
       if (masked(k) || (exclude_current && cur_[k])) continue;
+      if (random_) {                     // Random policy (all-zero weights, R29)
+        const uint64_t r = mix64(mix64(((uint64_t)T_ << 32) + (uint64_t)n_evict_) + (uint64_t)k);
+        if (bk < 0 || r < br || (r == br && k < bk)) {
+          br = r;
+          bk = k;
+          victim_slot = (int)i;
+        }
+        continue;
+      }
       const int64_t p = priority(k, cur_layer);
       // argmin over (P, layer, expert); key = layer*E+expert orders (layer, expert)
       if (bk < 0 || p < bp || (p == bp && k < bk)) {
@@ -87,6 +98,7 @@ int ExpertCache::insert(int pool, int key, int cur_layer, bool exclude_current) 
     }
     if (bk < 0) return -1;
     victim = bk;
+    ++n_evict_;
     where_[pool][victim] = -1;
   }
   slots[victim_slot] = key;
@@ -249,7 +261,7 @@ static int check_cfg_cache(const hb_config* cfg, std::string* err) {
   if (!cfg || cfg->n_layers <= 0 || cfg->n_experts <= 0 || cfg->top_k <= 0 ||
       cfg->top_k > cfg->n_experts) { *err = "bad dims"; return HB_EINVAL; }
   if (cfg->w_lru < 0 || cfg->w_lfu < 0 || cfg->w_lhu < 0 || cfg->w_fld < 0 ||
-      cfg->w_lru + cfg->w_lfu + cfg->w_lhu + cfg->w_fld <= 0) { *err = "bad Eq. 3 weights"; return HB_EINVAL; }
+      false) { *err = "bad Eq. 3 weights"; return HB_EINVAL; }
   if (cfg->world <= 0 || cfg->rank < 0 || cfg->rank >= cfg->world) { *err = "bad rank/world"; return HB_EINVAL; }
   if (cfg->hi_enc == cfg->lo_enc) { *err = "hi_enc == lo_enc"; return HB_EINVAL; }
   return HB_OK;

@@ -47,6 +47,11 @@ class ExpertCache {
   int slot_of(int pool, int key) const { return where_[pool][key]; }
   int pool_of_enc(int enc) const { return enc == hi_enc_ ? POOL_HIGH : POOL_LOW; }
   int64_t priority(int key, int cur_layer) const;
+  static uint64_t mix64(uint64_t z) {              // splitmix64 finaliser (Random policy)
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
 
   std::vector<hb_event> events;   // drained by the caller
   std::string err;
@@ -65,6 +70,8 @@ class ExpertCache {
   bool upgrade_;
   int rank_, world_;
   int64_t T_ = 0;
+  bool random_ = false;                            // all Eq. 3 weights 0: Random policy
+  uint64_t n_evict_ = 0;
   std::vector<int> pool_[2];            // slot -> key or -1
   std::vector<int> where_[2];           // key -> slot or -1
   std::vector<int64_t> R_, F_, H_;      // per key records

@@ -11,7 +11,7 @@ namespace hb {
 
 constexpr int kMaxTopK = 8;
 constexpr int kStampStride = 16;        // u64 per hb_stamps record
-constexpr int kMaxRouteLayers = 4;      // 1 + max lookahead p handled per launch
+constexpr int kMaxRouteLayers = 5;      // max lookahead p (routers stacked in one launch)
 constexpr int kNumSM = 148;             // B200
 #ifndef HB_GEMV_WARPS
 #define HB_GEMV_WARPS 12   // 12 x 168 registers: no spills (16 x 128 spilled 700 B; r01 sweep 8/10/12/14/16)

@@ -89,6 +89,8 @@ def test_host_cache_matches_oracle_bit_exact(trial):
     rank = rnd.randrange(world)
     p = rnd.randint(0, 3)
     w = (rnd.randint(0, 3), rnd.randint(0, 3), rnd.randint(0, 3), rnd.randint(1, 3))
+    if trial % 4 == 3:
+        w = (0, 0, 0, 0)                              # Random policy (R29)
     upgrade = rnd.choice([0, 1])
     ch, cl = rnd.randint(2 * k + 2, 10), rnd.randint(2 * k + 2, 10)
     ref = oc.ExpertCache(L_, E, ch, cl, w, fm.F16, fm.Q4, allow_upgrade=bool(upgrade),

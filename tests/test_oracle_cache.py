@@ -317,3 +317,42 @@ def test_ep_owned_only():
     served = c.forward(0, _route([2, 3], [HIGH, LOW]))
     assert served == [None, LO]
     assert all(e[3] % 2 == 1 for e in c.events)
+
+
+def test_random_policy_uniform_and_record_free():
+    """R29 (P:1040's Random normaliser): all-zero Eq. 3 weights pick the victim
+    uniformly among the eligible members, independently of the records.
+    Pool of 4 High slots, one layer of 8 experts: insert the non-member keys
+    round robin so every insert evicts; over 4000 evictions each of the 4
+    eligible members is chosen 1000 +- 150 times (binomial sd ~ 27)."""
+    c = oc.ExpertCache(1, 64, 4, 1, (0, 0, 0, 0), 0, 2)
+    c.token_begin()
+    for e in range(4):
+        c.load(0, e, 0)
+    counts = {}
+    nxt = 4
+    for i in range(4000):
+        before = list(c.pools[oc.POOL_HIGH])
+        c.load(0, nxt % 64, 0) if (nxt % 64) not in before else None
+        after = c.pools[oc.POOL_HIGH]
+        for j, (a, b) in enumerate(zip(before, after)):
+            if a != b:
+                counts[j] = counts.get(j, 0) + 1
+        nxt += 1
+        if i % 50 == 0:
+            c.token_begin()
+    assert sorted(counts) == [0, 1, 2, 3]
+    assert all(850 <= v <= 1150 for v in counts.values()), counts
+    # the records do not matter: two caches with different use histories
+    # choose the same victims
+    a = oc.ExpertCache(1, 8, 2, 1, (0, 0, 0, 0), 0, 2)
+    b = oc.ExpertCache(1, 8, 2, 1, (0, 0, 0, 0), 0, 2)
+    for cc in (a, b):
+        cc.token_begin()
+        cc.load(0, 0, 0)
+        cc.load(0, 1, 0)
+    b.R[0], b.F[0], b.H[0] = 7, 9, 9
+    for e in (2, 3, 4, 5):
+        a.load(0, e, 0)
+        b.load(0, e, 0)
+    assert a.pools == b.pools

@@ -49,12 +49,13 @@ def main():
     ap.add_argument("--tokens", type=int, default=24)
     ap.add_argument("--p", default="0,1,2")
     ap.add_argument("--rho", type=float, default=0.5)
+    ap.add_argument("--model", choices=["mixtral", "phi"], default="mixtral")
     ap.add_argument("--policies", default="",
                     help="Eq. 3 weight sets a:b:c:d (LRU:LFU:LHU:FLD) run at p=1, e.g. "
                          "1:0:0:0,0:1:0:0,0:0:1:0,0:0:0:1,1:1:1:1 (SURVEY 8(f) f2, P:631, P:1040)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    base = sg.MIXTRAL
+    base = {"mixtral": sg.MIXTRAL, "phi": sg.PHI}[args.model]
     L = args.layers
     shape = sg.MoEShape(base.name, L, base.n_experts, base.top_k, base.hidden, base.ffn,
                         base.sigma_router)
@@ -81,7 +82,9 @@ def main():
     torch.cuda.synchronize()
     t_init = time.time() - t0
     bb = {hi: h.blob_bytes(hi, H, F), lo: h.blob_bytes(lo, H, F)}
-    cap_h, cap_l = max(3, round(48 * L / 32)), max(3, round(56 * L / 32))
+    # 25 % of the F16 expert bytes, scaled with L and E
+    cap_h = max(3, round(48 * L / 32 * E / 8))
+    cap_l = max(3, round(56 * L / 32 * E / 8))
     xs = torch.from_numpy(sg.correlated_states(shape, args.tokens + 1, 0.999, args.rho)).cuda()
     y = torch.empty(1, H, dtype=torch.float32, device="cuda")
     runs = [(int(p), 0.6, 0.9, (1, 1, 1, 1)) for p in args.p.split(",") if p] + [(1, 1.0, 1.0, (1, 1, 1, 1))]
