@@ -120,6 +120,7 @@ struct hb_ctx {
   bool last_filtered = false;             // last forward's router kept no exact logits
   bool hfin_tail = false;                 // HB_HFIN_TAIL=1: h at the end of K2a (grid barrier), no hfin kernel
   bool router_filtered = false;           // HB_ROUTER=filtered: batch-1 decode router kernel (diagnostic)
+  bool router_solo = true;                // batch-1 decode: router_solo_kernel on a reserved SM (HB_ROUTER_SOLO=0: off)
   bool router_batch = true;               // filtered router for batches (HB_ROUTER=exact: off)
   bool fused_split = false;               // HB_FUSED_SPLIT=1: router+K2a kernel, then hfin + K2b
   bool fused_router = false;              // HB_FUSED_ROUTER=1: one-CTA router kernel + legacy K2a/hfin/K2b
@@ -444,6 +445,8 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     const char* re = std::getenv("HB_ROUTER");
     c->router_filtered = re && std::string(re) == "filtered";
     c->router_batch = !(re && std::string(re) == "exact");
+    const char* rs = std::getenv("HB_ROUTER_SOLO");
+    c->router_solo = !(rs && std::string(rs) == "0");
   }
   cudaMemset(c->gctr, 0, sizeof(unsigned) * (2 + 2 * kGemvCTAs));
   cudaMemset(c->wg, 0, (size_t)L * E * H * 2);
@@ -692,6 +695,9 @@ static RouterParams router_params(hb_ctx* c, const void* x, int batch) {
   p.done = c->done;
   p.lbuf = c->lbuf;
   p.rowbad = c->rowbad;
+  p.stamps = c->stamps_on ? c->stamps : nullptr;
+  p.stamp_cap = c->stamp_cap;
+  p.fwd_idx = c->fwd_idx;
   return p;
 }
 
@@ -731,6 +737,8 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y, float* au) {
   g.y = (float*)y;
   g.rowbad = c->rowbad;
   g.hfin_tail = c->hfin_tail;
+  g.ctas = kGemvCTAs;
+  g.clean = !c->hfin_tail;                   // hfin leaves the K2a sums clean, zeroes y
   g.gbar = c->gbar;
   g.ctr = c->gctr;
   g.max_vjobs = c->max_vjobs;
@@ -1011,6 +1019,26 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
       return ep_reduce(c, y, batch, s);
     }
     c->last_fused = false;
+    if (!k3 && batch == 1 && c->router_solo && !c->hfin_tail &&
+        router_solo_fits(k.n_experts, k.hidden, k.top_k)) {
+      // batch-1 decode: the router on one reserved SM, K2a / K2b on the
+      // others; nothing to zero (hfin cleaned the sums of the previous forward)
+      const int cn = c->au_cur;
+      if (c->au_dirty[cn])
+        CUDA_TRY(c, cudaMemsetAsync(au_buf(c, cn), 0, (size_t)c->au_dirty[cn] * 4, s));
+      c->au_dirty[cn] = 0;
+      rp.wnorm = c->wnorm + (size_t)layer * k.n_experts;
+      rp.x_save = c->x_save;
+      rp.logits = nullptr;
+      c->last_filtered = true;
+      launch_router_solo(rp, s);
+      c->launches += 1;
+      GemvParams gp = gemv_params(c, batch, y, au_buf(c, cn));
+      gp.ctas = kGemvCTAs - 1;
+      launch_gemv(c, gp, s);
+      CUDA_TRY(c, cudaGetLastError());
+      return ep_reduce(c, y, batch, s);
+    }
     if (k3) rp.zero_n[0] = 0;                          // K3 does not use the K2a sums
     const int cn = k3 ? 0 : legacy_au(c, rp, batch);
     launch_router(rp, s);
@@ -1020,6 +1048,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
     } else {
       GemvParams gp = gemv_params(c, batch, y, au_buf(c, cn));
       launch_gemv(c, gp, s);
+      if (gp.clean) c->au_dirty[cn] = 0;
     }
     CUDA_TRY(c, cudaGetLastError());
     return ep_reduce(c, y, batch, s);
@@ -1099,6 +1128,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
       CUDA_TRY(c, cudaStreamWaitEvent(s, c->slot_ready[pool[i]][slot[i]], 0));
   GemvParams gp = gemv_params(c, batch, y, au_buf(c, cn));
   launch_gemv(c, gp, s);
+  if (gp.clean) c->au_dirty[cn] = 0;
   for (int i = 0; i < K; ++i)
     if (served[i] != HB_ENC_NONE)
       CUDA_TRY(c, cudaEventRecord(c->slot_free[pool[i]][slot[i]], s));

@@ -46,6 +46,7 @@
 #include <algorithm>
 
 #include "hb_internal.h"
+#include "tl_stamps.cuh"
 #include "exact_dot.cuh"
 
 namespace hb {
@@ -510,6 +511,9 @@ __shared__ FusedSync fz_fs;
 // or the fused kernel's shared copy.  Templated so that the legacy kernels
 // keep these in the constant bank instead of registers.
 template <bool FUSED> struct JT;
+#if HB_LEGACY_TL == 1
+__shared__ unsigned long long tl_k2b_entry;
+#endif
 __shared__ int lg_nv, lg_nslot;     // legacy kernels: the header, read once per launch
 template <> struct JT<false> {
   static __device__ __forceinline__ int nv(const GemvParams&) { return lg_nv; }
@@ -541,6 +545,13 @@ template <bool FUSED>
 __device__ __forceinline__ void stage_h_and_wait(const GemvParams& p, const Stage& S) {
   if (!FUSED) {
     pdl_wait();
+#if HB_LEGACY_TL == 1
+    if (p.stamps && threadIdx.x == 0) {
+      unsigned long long* rec = tl_rec(p.stamps, p.stamp_cap, p.fwd_idx);
+      tl_min(rec, 12, tl_now());
+      tl_min(rec, 11, tl_k2b_entry);
+    }
+#endif
     if (S.on) stage_h_bulk_and_wait(p, S);
 #ifdef HB_NO_STAMPS
     if (false) {
@@ -1210,11 +1221,18 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   __shared__ int s_nsub;
   const int warp = threadIdx.x >> 5;
   HB_TL(W13, warp * gridDim.x + blockIdx.x, 0);
+#if HB_LEGACY_TL == 1
+  const unsigned long long tl_entry = tl_now();
+  if (!W13 && threadIdx.x == 0) tl_k2b_entry = tl_entry;
+#endif
   // K2a needs the router's job table and x; K2b may read the table before
   // waiting (K2a triggers its dependents only after its own wait, i.e. after
   // the router completed) and waits for K2a's sums inside its first run
   if constexpr (W13) pdl_wait();
   pdl_trigger();
+#if HB_LEGACY_TL == 1
+  if (W13 && threadIdx.x == 0) tl_min(tl_rec(p.stamps, p.stamp_cap, p.fwd_idx), 8, tl_entry);
+#endif
   const long long* cum = W13 ? p.jt.vcum13 : p.jt.vcum2;
   for (int i = threadIdx.x; i <= p.max_vjobs; i += blockDim.x) s_cum[i] = (int)__ldcg(cum + i);
   if (threadIdx.x == 0) {
@@ -1240,6 +1258,12 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   phase_run<W13, false>(p, s_cum, &s_fk, s_subvh, pc, S, s_meta[warp]);
   HB_TL(W13, warp * gridDim.x + blockIdx.x, 3);
   if (W13 && p.hfin_tail) k2a_hfin_tail(p, true);
+#if HB_LEGACY_TL == 1
+  if (W13) {
+    __syncthreads();
+    if (threadIdx.x == 0) tl_min(tl_rec(p.stamps, p.stamp_cap, p.fwd_idx), 14, tl_now());
+  }
+#endif
   legacy_stamp_end<W13>(p);
 }
 
@@ -1783,6 +1807,9 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
 __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvParams p) {
   pdl_trigger();                             // K2b may launch and prefetch its weights
   pdl_wait();                                // the K2a sums
+#if HB_LEGACY_TL == 1
+  if (threadIdx.x == 0) tl_min(tl_rec(p.stamps, p.stamp_cap, p.fwd_idx), 9, tl_now());
+#endif
   // R28: CTA b writes the NaN y row of token b if its x had a non-finite
   // element (the router zeroed y; K2b adds after this kernel).  The flag is
   // loaded here, next to the sums, and used at the end.
@@ -1790,9 +1817,9 @@ __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvP
   const int nb = p.F / 32;
   const int n = __ldcg(p.jt.hdr + 1) * nb * 4;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (rowbad) {
-    for (int c = threadIdx.x; c < p.H; c += blockDim.x)
-      p.y[(size_t)blockIdx.x * p.H + c] = __int_as_float(0x7fc00000);
+  if (rowbad || (p.clean && (int)blockIdx.x < p.B)) {
+    const float v = rowbad ? __int_as_float(0x7fc00000) : 0.f;
+    for (int c = threadIdx.x; c < p.H; c += blockDim.x) p.y[(size_t)blockIdx.x * p.H + c] = v;
   }
   if (i >= ((n + 31) & ~31)) return;
   const bool act = i < n;
@@ -1805,6 +1832,12 @@ __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvP
   const float4 a1 = __ldcg(reinterpret_cast<const float4*>(pa) + 1);
   const float4 u0 = __ldcg(reinterpret_cast<const float4*>(pu));
   const float4 u1 = __ldcg(reinterpret_cast<const float4*>(pu) + 1);
+  if (p.clean && act) {                      // leave the sums clean for the next forward
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4* wa = const_cast<float4*>(reinterpret_cast<const float4*>(pa));
+    float4* wu = const_cast<float4*>(reinterpret_cast<const float4*>(pu));
+    wa[0] = z; wa[1] = z; wu[0] = z; wu[1] = z;
+  }
   const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
   const float uv[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
   float h[8], hs = 0.f;
@@ -1829,12 +1862,15 @@ __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvP
     p.h_lo[(size_t)s * (p.F / 8) + j * 4 + t] = make_uint4(wl[0], wl[1], wl[2], wl[3]);
     if (t == 0) p.hsum[item] = hs;
   }
+#if HB_LEGACY_TL == 1
+  if ((threadIdx.x & 31) == 0) tl_max(tl_rec(p.stamps, p.stamp_cap, p.fwd_idx), 10, tl_now());
+#endif
 }
 
 void launch_w13(const GemvParams& p, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<true>();
   set_max_dyn_smem(gemv_kernel<true>, smem);
-  launch_pdl(gemv_kernel<true>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
+  launch_pdl(gemv_kernel<true>, p.ctas, kGemvWarps * 32, smem, s, p);
 }
 void launch_fused(const FusedParams& p, bool split, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<false>() > gemv_smem_bytes<true>() ? gemv_smem_bytes<false>()
@@ -1865,7 +1901,7 @@ void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
 void launch_w2(const GemvParams& p, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<false>();
   set_max_dyn_smem(gemv_kernel<false>, smem);
-  launch_pdl(gemv_kernel<false>, kGemvCTAs, kGemvWarps * 32, smem, s, p);
+  launch_pdl(gemv_kernel<false>, p.ctas, kGemvWarps * 32, smem, s, p);
 }
 int w2_stage_capacity() { return KCfg<false>::XSTAGE; }
 

@@ -142,6 +142,9 @@ struct RouterParams {
   int hi_enc, lo_enc;
   JobTable jt;
   unsigned* done;                      // grid completion counter (self-resetting)
+  unsigned long long* stamps;          // hb_stamps records (diagnostic HB_LEGACY_TL build only)
+  int stamp_cap;
+  const unsigned* fwd_idx;
 };
 
 struct GemvParams {
@@ -160,6 +163,9 @@ struct GemvParams {
   float* y;                            // [B][H] (zeroed by router)
   const int* rowbad;                   // [B] router's non-finite x flags: NaN rows (R28)
   int hfin_tail;                       // K2a ends with a grid barrier + h (no hfin kernel)
+  int ctas;                            // K2a / K2b grid (<= kGemvCTAs)
+  int clean;                           // hfin zeroes the K2a sums it read and the y rows (the
+                                       // solo router zeroes nothing)
   unsigned* gbar;                      // that grid barrier [count, generation] (self-resetting)
   // work feed: a static share of the units, then dynamic chunks (K2)
   unsigned* ctr;                       // chunk counters: [0] K2a, [1] K2b, [2 + q] K2a group q, [2 + 148 + q] K2b group q
@@ -202,6 +208,10 @@ struct FusedParams {
 void launch_fused(const FusedParams& p, bool split, cudaStream_t s);
 bool fused_fits(int E, int H, int F, int hi_enc, int lo_enc);
 void launch_router(const RouterParams& p, cudaStream_t s);
+// batch-1 decode router on one reserved SM (router.cu); the GEMV kernels then
+// run on kNumSM - 1 CTAs and hfin cleans the sums / zeroes y (GemvParams::clean)
+bool router_solo_fits(int E, int H, int k);
+void launch_router_solo(const RouterParams& p, cudaStream_t s);
 // kernel launch allowing programmatic dependent launch (the kernel overlaps
 // the tail of its predecessor in the stream and orders itself with
 // griddepcontrol.wait before touching the predecessor's outputs)

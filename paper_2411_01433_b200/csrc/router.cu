@@ -29,6 +29,7 @@
 
 #include "hb_internal.h"
 #include "exact_dot.cuh"
+#include "tl_stamps.cuh"
 
 namespace hb {
 
@@ -38,6 +39,14 @@ __device__ unsigned long long g_rtl[16];
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_rtl[i] = t_; } } while (0)
 #else
 #define HB_RTL(i) do { } while (0)
+#endif
+// HB_LEGACY_TL == 2: router sub-steps of the leader CTA in hb_stamps fields 8..14
+// (SM clock cycles after griddepcontrol.wait, kept in registers and written
+// once at the end: no stamp overhead inside the measured steps)
+#if HB_LEGACY_TL == 2
+#define HB_RSUB(f) do { tl_sub[(f) - 8] = clock64(); } while (0)
+#else
+#define HB_RSUB(f) do { } while (0)
 #endif
 
 __device__ double i128_to_double(i128 v) {
@@ -400,7 +409,8 @@ __device__ void build_jobs_cta(const RouterParams& p, SmemT& sm, const hb_decisi
 // same table (jobs by key = expert*2 + Low, slots in selection order) from
 // per-lane counts instead of serial loops.
 template <typename SmemT>
-__device__ __forceinline__ void build_jobs_warp(const RouterParams& p, SmemT& sm, const hb_decision* dec) {
+__device__ __forceinline__ void build_jobs_warp_to(const RouterParams& p, SmemT& sm, const hb_decision* dec,
+                                                   const JobTable& jt, hb_decision* dout) {
   const int lane = threadIdx.x & 31;
   const int nsel = p.B * p.k;
   constexpr int kNone = 0x7FFFFFFF;
@@ -432,16 +442,16 @@ __device__ __forceinline__ void build_jobs_warp(const RouterParams& p, SmemT& sm
   }
   const int nj = __popc(__ballot_sync(0xffffffffu, first));
   const int nslot = __popc(__ballot_sync(0xffffffffu, valid));
-  if (lane < nsel) p.jt.tok_slots[lane] = -1;
+  if (lane < nsel) jt.tok_slots[lane] = -1;
   if (valid) {
     const int slot = less + rank;
     const int enc = (key & 1) ? p.lo_enc : p.hi_enc;
-    p.jt.slot_token[slot] = d.token;
-    p.jt.slot_gate[slot] = d.gate;
-    p.jt.tok_slots[lane] = slot;
+    jt.slot_token[slot] = d.token;
+    jt.slot_gate[slot] = d.gate;
+    jt.tok_slots[lane] = slot;
     d.served_enc = (uint8_t)enc;
     d.hit = 1;
-    p.dec[lane] = d;
+    dout[lane] = d;
     if (first) {
       Job j;
       j.blob = sm.blob[(key >> 1) * 4 + enc];
@@ -450,15 +460,19 @@ __device__ __forceinline__ void build_jobs_warp(const RouterParams& p, SmemT& sm
       j.n_tok = ntok;
       j.slot_off = less;
       sm.jobs[jid] = j;
-      p.jt.jobs[jid] = j;
+      jt.jobs[jid] = j;
     }
   }
   __syncwarp();
   if (lane == 0) {
-    p.jt.hdr[0] = nj;
-    p.jt.hdr[1] = nslot;
-    p.jt.hdr[2] = build_vjobs(sm.jobs, nj, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
+    jt.hdr[0] = nj;
+    jt.hdr[1] = nslot;
+    jt.hdr[2] = build_vjobs(sm.jobs, nj, p.H, p.F, jt.vjobs, jt.vcum13, jt.vcum2);
   }
+}
+template <typename SmemT>
+__device__ __forceinline__ void build_jobs_warp(const RouterParams& p, SmemT& sm, const hb_decision* dec) {
+  build_jobs_warp_to(p, sm, dec, p.jt, p.dec);
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -726,12 +740,19 @@ __global__ void __launch_bounds__(kRouterThreads)
 router_kernel(const __grid_constant__ RouterParams p) {
   __shared__ RouterSmem sm;
   HB_RTL(0);
+#ifdef HB_LEGACY_TL
+  const unsigned long long tl_entry = tl_now();
+#endif
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int NW = kRouterThreads / 32;
   const int nrows = p.n_route * p.B;
   const int row = blockIdx.x / C, crank = blockIdx.x % C;   // cluster = one row
   if (row >= nrows) {
     zero_buffers(p, blockIdx.x - nrows * C, gridDim.x - nrows * C);
+#if HB_LEGACY_TL == 1
+    __syncthreads();
+    if (tid == 0) tl_max(tl_rec(p.stamps, p.stamp_cap, p.fwd_idx), 13, tl_now());
+#endif
     return;
   }
   const int b = row % p.B;
@@ -756,6 +777,17 @@ router_kernel(const __grid_constant__ RouterParams p) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   HB_RTL(1);
+#if HB_LEGACY_TL == 2
+  long long tl_sub[7] = {0, 0, 0, 0, 0, 0, 0};
+  const long long tl_c0 = clock64();
+#endif
+#ifdef HB_LEGACY_TL
+  if (tid == 0) {
+    unsigned long long* rec = tl_rec(p.stamps, p.stamp_cap, p.fwd_idx);
+    tl_min(rec, 6, tl_now());
+    tl_min(rec, 5, tl_entry);
+  }
+#endif
 
   // ---- O2: exact partial logits of token b over this CTA's slice, every
   // expert (a warp per expert, or several warps per expert when E < 8)
@@ -803,11 +835,14 @@ router_kernel(const __grid_constant__ RouterParams p) {
     sm.cpart[e][0] = lo; sm.cpart[e][1] = mid; sm.cpart[e][2] = hi;
   }
   HB_RTL(2);
+  HB_RSUB(8);
   // ---- pair-permuted x and block sums of this slice for the GEMV kernels
   if (p.x_perm && rl == 0) write_xperm(p, x, s0, s1, b);
+  HB_RSUB(9);
   // ---- combine the cluster's partials in the leader (distributed shared memory)
   if (C > 1) cluster_sync_all();
   else __syncthreads();
+  HB_RSUB(10);
   if (crank == 0) {
     if (C > 1 && tid == kRouterThreads - 1) {   // a thread the logit combine does not use
       int bad = 0;
@@ -828,10 +863,12 @@ router_kernel(const __grid_constant__ RouterParams p) {
       sm.L[e] = (i128)(long long)lo + ((i128)(long long)mid << 20) + ((i128)(long long)hi << 40);
     }
   }
+  HB_RSUB(11);
   if (C > 1) cluster_sync_all();             // remote reads done: the other CTAs may exit
   else __syncthreads();
   if (crank != 0) return;
   HB_RTL(3);
+  HB_RSUB(12);
   HB_RTL(4);
   if (rl == 0 && p.logits)
     for (int e = tid; e < p.E; e += blockDim.x) {
@@ -854,12 +891,24 @@ router_kernel(const __grid_constant__ RouterParams p) {
       }
       __syncwarp();
       HB_RTL(5);
+      HB_RSUB(13);
       if (p.blob_table) {
         if (p.B * p.k <= 32) build_jobs_warp(p, sm, sm.dec);
         else if (lane == 0) build_jobs(p, sm, sm.dec);
       }
       HB_RTL(6);
+      HB_RSUB(14);
       HB_RTL(7);                               // back-to-back: cost of one stamp
+#ifdef HB_LEGACY_TL
+      if (lane == 0) {
+        unsigned long long* rec = tl_rec(p.stamps, p.stamp_cap, p.fwd_idx);
+        tl_max(rec, 7, tl_now());
+#if HB_LEGACY_TL == 2
+        if (blockIdx.x == 0)
+          for (int f = 0; f < 7; ++f) tl_max(rec, 8 + f, (unsigned long long)(tl_sub[f] - tl_c0));
+#endif
+      }
+#endif
     }
     return;
   }
@@ -934,6 +983,377 @@ router_dec_kernel(const __grid_constant__ RouterParams p) {
   route_filtered<C>(p, sm, crank, s0, s1, 0, 0);
 }
 
+
+// Decode router on a reserved SM (batch 1, one route layer, top-2, E <= 32;
+// DESIGN.md section 5 "router").  One CTA of 1024 threads; the GEMV kernels of
+// the chain run on the other 147 SMs, so this CTA is resident as soon as the
+// previous K2b triggers its dependents, ~25 us before that K2b ends.  It uses
+// the time for everything that does not depend on x:
+//   * the layer's router rows W_g [E][H] into shared memory (bulk copies),
+//     the blob table and the row norms;
+//   * a complete dry run of the routing code on whatever x holds (results
+//     into shared-memory sinks, global stores predicated off): the router
+//     runs once per layer between much larger kernels, so otherwise every
+//     step of it starts from a cold instruction cache (measured: ~7800 SM
+//     cycles for the decide + job-table steps alone, tools/legacy_timeline.py).
+// After griddepcontrol.wait only x (8 KB) is loaded; the logits are the
+// filtered ones (R9': exact fp16 x fp16 products in fp32 FFMA chains of 8,
+// warp trees, fp64 sums over warps, Cauchy-Schwarz bound), the exact integer
+// path decides when a comparison does not clear the bound.  The accumulation
+// buffers are not zeroed here: hfin leaves the K2a sums clean and zeroes y
+// (GemvParams::clean).
+constexpr int kSoloThreads = 1024;
+constexpr int kSoloWarps = kSoloThreads / 32;
+struct SoloSmem {
+  float red[kSoloWarps][32];           // per warp fp32 partial logit per expert
+  float xqw[kSoloWarps];               // per warp sum of x^2
+  double Lf[32];                       // filtered logits
+  double xsq;                          // ||x||^2
+  u64 part[kSoloWarps][32][3];         // exact fallback: per warp partial per expert
+  i128 L[32];                          // exact fallback: logits
+  hb_decision dec[2];
+  const uint8_t* blob[32 * 4];
+  Job jobs[3];
+  float wn[32];
+  uint4 xs[1024];                      // x (H <= 8192)
+  // pass-0 destinations
+  hb_decision dry_dec[2];
+  int32_t dry_hdr[3], dry_slot_token[2], dry_tok_slots[2], dry_rowbad;
+  float dry_slot_gate[2];
+  Job dry_jobs[2];
+  VJobD dry_vjobs[2];
+  long long dry_vcum13[3], dry_vcum2[3];
+  uint64_t wbar;
+  int ok, bad;
+};
+extern __shared__ __align__(128) uint8_t solo_dyn[];   // W_g [E][H] fp16
+
+// The job table of one token's two selections (B = 1, k = 2) by lanes 0 and
+// 1 of a warp: the table build_jobs_warp writes for nsel = 2 (jobs and slots
+// by key = expert * 2 + served-from-lo_enc, one slot per job, vjob = job),
+// without its loops (the router is on every layer's critical path).
+__device__ __forceinline__ void build_jobs_k2(const RouterParams& p, const hb_decision* dec,
+                                              const uint8_t* const* blob, const JobTable& jt,
+                                              hb_decision* dout) {
+  const int lane = threadIdx.x & 31;
+  hb_decision d = dec[lane & 1];
+  const unsigned long long hb = lane < 2 ? high_bit(p, d) : 0ull;
+  const unsigned long long hmask = hb | __shfl_xor_sync(0xffffffffu, hb, 1);
+  const int key = lane < 2 ? sel_key(p, d, hmask) : -1;
+  const int ko = __shfl_xor_sync(0xffffffffu, key, 1);
+  const bool valid = key >= 0;
+  const int slot = valid ? (ko >= 0 && ko < key ? 1 : 0) : -1;
+  const int nj = (key >= 0) + (ko >= 0);
+  const int enc = (key & 1) ? p.lo_enc : p.hi_enc;
+  const long long u13 = valid ? (long long)(p.F / 16) * (p.H / epg_of_enc(enc)) : 0;
+  const long long u2 = valid ? (long long)(p.H / 16) * (p.F / epg_of_enc(enc)) : 0;
+  const long long o13 = __shfl_xor_sync(0xffffffffu, u13, 1), o2 = __shfl_xor_sync(0xffffffffu, u2, 1);
+  if (lane >= 2) return;
+  jt.tok_slots[lane] = slot;
+  if (valid) {
+    const uint8_t* b = blob[(key >> 1) * 4 + enc];
+    jt.slot_token[slot] = 0;
+    jt.slot_gate[slot] = d.gate;
+    Job j;
+    j.blob = b; j.enc = enc; j.expert = key >> 1; j.n_tok = 1; j.slot_off = slot;
+    jt.jobs[slot] = j;
+    VJobD v;
+    v.blob = b; v.enc = enc; v.slot0 = slot; v.nslot = 1; v.pad = 0;
+    jt.vjobs[slot] = v;
+    jt.vcum13[slot + 1] = slot ? u13 + o13 : u13;   // cumulative units, vjobs in slot order
+    jt.vcum2[slot + 1] = slot ? u2 + o2 : u2;
+    d.served_enc = (uint8_t)enc;
+    d.hit = 1;
+    dout[lane] = d;
+  }
+  if (lane == 0) {
+    jt.vcum13[0] = 0;
+    jt.vcum2[0] = 0;
+    jt.hdr[0] = nj;
+    jt.hdr[1] = nj;
+    jt.hdr[2] = nj;
+  }
+}
+
+__global__ void __launch_bounds__(kSoloThreads, 1)
+router_solo_kernel(const __grid_constant__ RouterParams p) {
+  __shared__ SoloSmem sm;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int E = p.E, n8 = p.H / 8;
+  const int G = kSoloThreads / n8;             // thread groups over the x chunks (n8 | 1024)
+  const int wpg = n8 / 32;                     // warps per group
+  const int c = tid % n8, g = tid / n8;        // this thread: chunk c, experts g, g + G, ...
+  const uint4* w4 = reinterpret_cast<const uint4*>(solo_dyn);
+  const uint32_t wbar = (uint32_t)__cvta_generic_to_shared(&sm.wbar);
+#ifdef HB_LEGACY_TL
+  const unsigned long long tl_entry = tl_now();
+#endif
+#if HB_LEGACY_TL == 2
+  long long tl_sub[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long tl_c0 = 0;
+#endif
+  // ---- static inputs: router rows by bulk copies, blob table, row norms
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(wbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t total = (uint32_t)E * p.H * 2;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(wbar), "r"(total) : "memory");
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(solo_dyn);
+    for (uint32_t off = 0; off < total; off += 16384) {
+      const uint32_t len = total - off < 16384 ? total - off : 16384;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          :: "r"(dst + off), "l"(reinterpret_cast<const char*>(p.wg[0]) + off), "r"(len), "r"(wbar)
+          : "memory");
+    }
+  }
+  if (p.blob_table)
+    for (int i = tid; i < 4 * E; i += kSoloThreads) sm.blob[i] = p.blob_table[i];
+  for (int i = tid; i < E; i += kSoloThreads) sm.wn[i] = p.wnorm[i];
+  JobTable dry_jt;
+  dry_jt.hdr = sm.dry_hdr;
+  dry_jt.jobs = sm.dry_jobs;
+  dry_jt.slot_token = sm.dry_slot_token;
+  dry_jt.slot_gate = sm.dry_slot_gate;
+  dry_jt.tok_slots = sm.dry_tok_slots;
+  dry_jt.vjobs = sm.dry_vjobs;
+  dry_jt.vcum13 = sm.dry_vcum13;
+  dry_jt.vcum2 = sm.dry_vcum2;
+  __syncthreads();
+  {                                            // router rows landed
+    uint32_t done;
+    do {
+      asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], 0; selp.u32 %0, 1, 0, P; }"
+                   : "=r"(done) : "r"(wbar) : "memory");
+    } while (!done);
+  }
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool live = pass == 1;
+    if (live) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");       // x belongs to earlier work
+      asm volatile("griddepcontrol.launch_dependents;");
+#ifdef HB_LEGACY_TL
+      if (tid == 0) {
+        unsigned long long* rec = tl_rec(p.stamps, p.stamp_cap, p.fwd_idx);
+        tl_min(rec, 6, tl_now());
+        tl_min(rec, 5, tl_entry);
+      }
+#endif
+#if HB_LEGACY_TL == 2
+      tl_c0 = clock64();
+#endif
+    }
+    // ---- x (L2 loads: the pass-0 x must never sit in L1), finiteness, ||x||^2
+    int xbad = 0;
+    float xq = 0.f;
+    if (tid < n8) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p.x) + tid);
+      sm.xs[tid] = v;
+      const uint32_t xa[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        xbad |= ((xa[q] & 0x7C00u) == 0x7C00u) | ((xa[q] & 0x7C000000u) == 0x7C000000u);
+      float xf[8];
+      r_h2f8(v, xf);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xq = fmaf(xf[q], xf[q], xq);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xq += __shfl_xor_sync(0xffffffffu, xq, o);
+    if (lane == 0) sm.xqw[warp] = xq;
+    const int bad = __syncthreads_or(xbad);
+    HB_RSUB(8);
+    // ---- filtered partial logits: chunk c of x against experts g, g + G, ...
+    {
+      float xf[8];
+      r_h2f8(sm.xs[c], xf);
+      for (int e = g; e < E; e += G) {
+        float wf[8];
+        r_h2f8(w4[(size_t)e * n8 + c], wf);
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = fmaf(wf[q], xf[q], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) sm.red[warp][e] = acc;
+      }
+    }
+    __syncthreads();
+    // ---- fp64 sums: warp e < E sums expert e over the warps of its group,
+    // the last warp sums ||x||^2 (fixed shuffle trees: deterministic)
+    if (warp < E) {
+      const int w0 = (warp % G) * wpg;
+      double v = lane < wpg ? (double)sm.red[w0 + lane][warp] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) sm.Lf[warp] = v;
+    } else if (warp == kSoloWarps - 1) {
+      double v = (double)sm.xqw[lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) sm.xsq = v;
+    }
+    __syncthreads();
+    HB_RSUB(9);
+    if (warp == 0) {
+      // ---- warp 0: the certainty of every comparison, decisions, gates, jobs
+      hb_decision* dout = live ? p.dec : sm.dry_dec;
+      // error of a logit: fp32 chains of 8 products (gamma_7), warp trees
+      // (gamma_5), fp64 sums over warps (negligible): (8 + 6) * 2^-24 *
+      // sum|p| * (1 + 1e-4), with sum|p| <= ||w_e|| ||x|| (||x|| rounded up)
+      const double xn = sqrt(sm.xsq) * (1.0 + 1e-6) + 1e-30;
+      const double cb = 14.0 * 0x1p-24 * 1.0001;
+      const int e = lane;
+      const double v = e < E ? sm.Lf[e] : -1e300;
+      const double ep = e < E ? cb * (double)sm.wn[e] * xn : 0.0;
+      int r = 0;                                 // rank by (L desc, index asc); lanes >= E unused
+      for (int f = 0; f < E; ++f) {
+        const double o = sm.Lf[f];
+        r += (o > v) || (o == v && f < e);
+      }
+      const unsigned m0 = __ballot_sync(0xffffffffu, e < E && r == 0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, e < E && r == 1);
+      const int e0 = __ffs(m0) - 1, e1 = __ffs(m1) - 1;
+      double rest = (e < E && r >= 2) ? v + ep : -1e300;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rest = fmax(rest, __shfl_xor_sync(0xffffffffu, rest, o));
+      const double L0 = sm.Lf[e0], L1 = sm.Lf[e1];
+      const double ep0 = __shfl_sync(0xffffffffu, ep, e0), ep1 = __shfl_sync(0xffffffffu, ep, e1);
+      const double Gp = L0 - L1, mg = ep0 + ep1 + 1e-12 * (1.0 + fabs(L0) + fabs(L1));
+      bool ok = !bad && (L0 - ep0 > L1 + ep1) && (L1 - ep1 > rest);
+      if (p.th1_kind == 0) ok = ok && fabs(Gp - (double)p.theta1 * 0x1p-48) > mg;
+      if (p.th2_kind == 0) ok = ok && fabs(Gp - (double)p.theta2 * 0x1p-48) > mg;
+      if (lane < 2) {
+        // lane 0 writes selection 0, lane 1 selection 1
+        const uint8_t prec1 =
+            (p.th1_kind > 0 || (p.th1_kind == 0 && Gp <= (double)p.theta1 * 0x1p-48)) ? HB_HIGH
+            : (p.th2_kind > 0 || (p.th2_kind == 0 && Gp <= (double)p.theta2 * 0x1p-48)) ? HB_LOW
+                                                                                        : HB_SKIP;
+        const float ex = expf(-(float)Gp);
+        const float g0 = 1.f / (1.f + ex);
+        hb_decision d;
+        d.token = 0; d.sel_rank = (uint8_t)lane; d.served_enc = HB_ENC_NONE; d.hit = 0;
+        if (bad) {                               // R28: Skip, expert -1, gate NaN
+          d.expert = -1; d.prec = HB_SKIP; d.gate = __int_as_float(0x7fc00000);
+        } else {
+          d.expert = lane ? e1 : e0; d.prec = lane ? prec1 : (uint8_t)HB_HIGH; d.gate = lane ? ex * g0 : g0;
+        }
+        if (ok || bad) { dout[lane] = d; sm.dec[lane] = d; }
+        if (lane == 0) { *(live ? p.rowbad : &sm.dry_rowbad) = bad; sm.ok = ok || bad; }
+      }
+      __syncwarp();
+      HB_RSUB(10);
+      if ((ok || bad) && p.blob_table) build_jobs_k2(p, sm.dec, sm.blob, live ? p.jt : dry_jt, dout);
+      HB_RSUB(11);
+    } else if (live) {
+      // ---- the other warps meanwhile: pair-permuted x + block sums (K2a) and
+      // the copy for the lazy exact logits
+      const int t2 = tid - 32;
+      if (t2 < n8 / 4) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 t = sm.xs[4 * t2 + i];
+          v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
+        }
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          sum += __half2float(__ushort_as_half((unsigned short)(v[i >> 1] >> (16 * (i & 1)))));
+        p.xsum[t2] = sum;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {            // uint4 t: Q_c = (x[8t+c], x[8t+c+4])
+          uint32_t q[4];
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int e0 = 8 * t + cc, e1 = e0 + 4;
+            const uint32_t lo16 = (v[e0 >> 1] >> (16 * (e0 & 1))) & 0xFFFF;
+            const uint32_t hi16 = (v[e1 >> 1] >> (16 * (e1 & 1))) & 0xFFFF;
+            q[cc] = lo16 | (hi16 << 16);
+          }
+          p.x_perm[t2 * 4 + t] = make_uint4(q[0], q[1], q[2], q[3]);
+        }
+      }
+      if (p.x_save && t2 < n8) reinterpret_cast<uint4*>(p.x_save)[t2] = sm.xs[t2];
+    }
+    __syncthreads();
+    if (!sm.ok) {
+      // ---- exact fallback (rare): integer logits from the same shared rows
+      const uint4 xv = sm.xs[c];
+      const uint32_t xa[4] = {xv.x, xv.y, xv.z, xv.w};
+      for (int e = g; e < E; e += G) {
+        const uint4 wv = w4[(size_t)e * n8 + c];
+        const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
+        u64 lo = 0, mid = 0, hi = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          accum_exact((wa[i >> 1] >> (16 * (i & 1))) & 0xFFFF, (xa[i >> 1] >> (16 * (i & 1))) & 0xFFFF,
+                      lo, mid, hi);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lo += __shfl_xor_sync(0xffffffffu, lo, o);
+          mid += __shfl_xor_sync(0xffffffffu, mid, o);
+          hi += __shfl_xor_sync(0xffffffffu, hi, o);
+        }
+        if (lane == 0) { sm.part[warp][e][0] = lo; sm.part[warp][e][1] = mid; sm.part[warp][e][2] = hi; }
+      }
+      __syncthreads();
+      if (tid < E) {
+        const int w0 = (tid % G) * wpg;
+        u64 lo = 0, mid = 0, hi = 0;
+        for (int w = 0; w < wpg; ++w) {
+          lo += sm.part[w0 + w][tid][0]; mid += sm.part[w0 + w][tid][1]; hi += sm.part[w0 + w][tid][2];
+        }
+        sm.L[tid] = (i128)(long long)lo + ((i128)(long long)mid << 20) + ((i128)(long long)hi << 40);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        hb_decision* dout = live ? p.dec : sm.dry_dec;
+        decide_k2_warp(p, sm.L, 0, dout, sm.dec);
+        __syncwarp();
+        if (p.blob_table) build_jobs_k2(p, sm.dec, sm.blob, live ? p.jt : dry_jt, dout);
+      }
+    }
+#ifdef HB_LEGACY_TL
+    if (live && tid == 0) {
+      unsigned long long* rec = tl_rec(p.stamps, p.stamp_cap, p.fwd_idx);
+      tl_max(rec, 7, tl_now());
+#if HB_LEGACY_TL == 2
+      for (int f = 0; f < 4; ++f) tl_max(rec, 8 + f, (unsigned long long)(tl_sub[f] - tl_c0));
+#endif
+    }
+#endif
+    __syncthreads();
+  }
+}
+
+bool router_solo_fits(int E, int H, int k) {
+  const int n8 = H / 8;
+  return k == 2 && E >= 2 && E <= 31 && n8 >= 32 && n8 <= kSoloThreads && kSoloThreads % n8 == 0 &&
+         (long long)E * H * 2 + (long long)sizeof(SoloSmem) + 1024 <= 227 * 1024;
+}
+
+void launch_router_solo(const RouterParams& p, cudaStream_t s) {
+  const int smem = p.E * p.H * 2;
+  static int max_dyn = [] {                  // once: the largest the static part leaves
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, router_solo_kernel);
+    return 227 * 1024 - (int)fa.sharedSizeBytes;
+  }();
+  set_max_dyn_smem(router_solo_kernel, max_dyn);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kSoloThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, router_solo_kernel, p);
+}
 
 // Router for batches (n_route = 1, top-2, E <= 64): one CTA per token row,
 // the filtered router (fp32 products in FFMA chains, warp trees, fp64 sums
