@@ -91,6 +91,21 @@ typedef struct {
                                        expert that some token of the same forward selected
                                        High is served by the hi_enc copy -- one weight stream
                                        per touched expert (R27; needs allow_upgrade) */
+  int device_cache;                 /* offload mode only.  0 (default): the cache state machine
+                                       runs on the host, loads are copy-engine memcpys on a copy
+                                       stream (one host sync per layer).  1: the state machine
+                                       (Eq. 3, the prefetch walk, the event log) lives in HBM and
+                                       runs in a kernel after the router; loads are done by SMs
+                                       reading the mapped pinned host blobs in chunks --
+                                       on-demand chunks first, prefetch chunks in the background
+                                       and pre-empted by the next forward -- so the
+                                       offload forward never syncs with the host and can be
+                                       captured in a CUDA graph.  In this
+                                       mode prefetch_next_layer returns 0 (the queued loads are
+                                       in hb_get_events), errors of the state machine (pool full)
+                                       are sticky and reported by the next call, and a captured
+                                       sequence must end with a moe_layer_forward (it joins the
+                                       background copier) */
 } hb_config;
 
 /* One routed (token, rank) pair of the last forward (inspection / parity). */
@@ -246,6 +261,14 @@ int hb_get_decisions(hb_ctx* ctx, hb_decision* out, int cap);
 int hb_get_logits(hb_ctx* ctx, int64_t* out, int cap_pairs);
 /* Cache events since the last call (offload mode). Returns the count. */
 int hb_get_events(hb_ctx* ctx, hb_event* out, int cap);
+/* Bytes moved host -> HBM for expert loads since hb_create (offload mode;
+ * synchronises the device): out[0] foreground (on the forward's critical
+ * path: on-demand loads, and in device_cache mode the rest of a prefetch the
+ * forward needed), out[1] background (prefetch / expert_cache_load chunks).
+ * In device_cache mode a prefetch whose slot is reused before its chunks were
+ * copied never moves them: out[] counts what crossed the link, the events
+ * count logical loads. */
+int hb_copy_stats(hb_ctx* ctx, uint64_t out[2]);
 /* Realised bytes of expert weights read by the GEMV kernels in the last
  * forward (sum of served blob bytes), for the roofline. */
 int hb_last_expert_bytes(hb_ctx* ctx, uint64_t* out);

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <dlfcn.h>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -18,6 +19,7 @@
 #include <vector>
 
 #include "cache.h"
+#include "dcache.h"
 #include "hb_internal.h"
 #include "k3.h"
 #include "hobbit.h"
@@ -97,6 +99,19 @@ struct hb_ctx {
   size_t pf_window = 64ull << 20, pf_chunk = 16ull << 20;     // HB_PREFETCH_WINDOW_MB / _CHUNK_MB
   ExpertCache* cache = nullptr;
   std::vector<hb_event> log;
+  // device-resident cache manager (hb_config.device_cache):
+  // state in HBM, SM copies from the mapped host blobs (dcache.cu)
+  DcState* dc = nullptr;                  // device copy of the state
+  DcState dc_h{};                         // host mirror (array pointers)
+  const uint8_t** host_blob_dev = nullptr;   // [L][E][4] device addresses of the host blobs
+  int* err_host = nullptr;                // mapped pinned sticky error word
+  int* err_dev = nullptr;                 // its device address
+  cudaEvent_t ev_fork = nullptr, ev_side = nullptr;
+  bool side_pending = false;              // background copier not yet joined
+  int dc_reset = 0, dc_tadd = 0, dc_clear = 0;   // token_begin / reset since the last cache op
+  int dc_fg_ctas = 32, dc_bg_ctas = 16;   // HB_DC_FG_CTAS / HB_DC_BG_CTAS
+  size_t dc_chunk = 256u << 10;           // HB_DC_CHUNK_KB
+  uint64_t copied[2] = {0, 0};            // host path: bytes issued on demand / prefetch+explicit
   // scratch
   hb_decision* dec = nullptr;             // [B][k]
   hb_decision* dec_pred = nullptr;        // [p][B][k]
@@ -179,6 +194,7 @@ static int fail(hb_ctx* c, int code, const std::string& msg) {
 }
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+static int dc_create(hb_ctx* c);
 
 // ---- NCCL, resolved at run time (libnccl.so.2 already loaded by the process,
 // e.g. torch's, or found on the library path; HB_NCCL_LIB overrides)
@@ -304,10 +320,17 @@ static void free_ctx(hb_ctx* c) {
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
                    c->logits, c->lbuf, c->x_perm, c->xsum, c->au, c->h_hi, c->h_lo,
                    c->hsum, c->done, c->gctr, c->jt_dev, c->k3_xg, c->k3_hB, c->k3_tab, c->k3_tmap,
-                   c->gbar, c->fwd_idx, c->stamps, c->x_save, c->wnorm, c->rowbad};
+                   c->gbar, c->fwd_idx, c->stamps, c->x_save, c->wnorm, c->rowbad,
+                   c->dc, c->host_blob_dev, c->dc_h.pool[0], c->dc_h.pool[1], c->dc_h.where[0],
+                   c->dc_h.where[1], c->dc_h.R, c->dc_h.F, c->dc_h.H, c->dc_h.mask_exp,
+                   c->dc_h.masked_keys, c->dc_h.cur, c->dc_h.cur_list, c->dc_h.log,
+                   c->dc_h.task[0], c->dc_h.task[1]};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_side) cudaEventDestroy(c->ev_side);
   if (c->jt_host) cudaFreeHost(c->jt_host);
   for (void* p : c->arena) cudaFreeHost(p);
   for (void* p : c->dev_owned) cudaFree(p);
@@ -503,6 +526,9 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     c->cache = new (std::nothrow) ExpertCache(L, E, K, k.cap_high, k.cap_low, w, k.hi_enc,
                                               k.lo_enc, k.allow_upgrade != 0, k.rank, k.world);
     if (!c->cache) return bail(HB_ENOMEM, "cache allocation failed");
+    if (k.device_cache) {
+      if (int rc = dc_create(c)) return bail(rc, c->err);
+    }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(HB_ECUDA, "device sync failed");
   *out = c;
@@ -624,7 +650,7 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
     c->host_blob[idx] = (const uint8_t*)blob;
   } else if (mode == HB_REG_HOST_COPY) {
     void* p = nullptr;
-    if (cudaHostAlloc(&p, nbytes, cudaHostAllocDefault) != cudaSuccess)
+    if (cudaHostAlloc(&p, nbytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
       return fail(c, HB_ENOMEM, "pinned arena allocation failed");
     if (canonical) {                            // convert on the device, back into the arena
       uint8_t* dev = nullptr;
@@ -646,6 +672,14 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
   } else {
     return fail(c, HB_EINVAL, "offload mode takes HB_REG_HOST_PINNED / HB_REG_HOST_COPY");
   }
+  if (c->dc) {                                  // SM copies read the blob through its mapping
+    void* dptr = nullptr;
+    if (cudaHostGetDevicePointer(&dptr, (void*)c->host_blob[idx], 0) != cudaSuccess || !dptr) {
+      cudaGetLastError();
+      return fail(c, HB_EUNSUPPORTED, "device_cache needs mapped pinned host blobs");
+    }
+    CUDA_TRY(c, cudaMemcpy(c->host_blob_dev + idx, &dptr, sizeof(void*), cudaMemcpyHostToDevice));
+  }
   return HB_OK;
 }
 
@@ -657,6 +691,8 @@ int hb_token_begin(hb_ctx* c) {
     if (int rc = pf_top_up(c)) return rc;
   }
   if (c->cache) c->cache->token_begin();
+  c->dc_tadd += 1;                              // device cache: applied by the next cache op
+  c->dc_clear = 1;
   c->token_started = true;
   return HB_OK;
 }
@@ -664,6 +700,8 @@ int hb_token_begin(hb_ctx* c) {
 int hb_reset_sequence(hb_ctx* c) {
   if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
   if (c->cache) c->cache->reset_sequence();
+  c->dc_reset = 1;
+  c->dc_tadd = 0;
   // T = 0 after a reset: Eq. 3 divides by T, so the next forward needs
   // hb_token_begin first (T >= 1)
   c->token_started = false;
@@ -889,6 +927,7 @@ static int pf_issue_chunk(hb_ctx* c, hb_ctx::PfLoad& L) {
   CUDA_TRY(c, cudaMemcpyAsync(L.dst + L.issued, L.src + L.issued, n, cudaMemcpyHostToDevice,
                               c->copy_stream));
   L.issued += n;
+  c->copied[1] += n;
   cudaEvent_t ev;
   if (c->pf_event_pool.empty()) {
     CUDA_TRY(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -961,8 +1000,160 @@ static int issue_loads(hb_ctx* c, size_t from) {
     CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[pool][e.slot], 0));
     CUDA_TRY(c, cudaMemcpyAsync(dst, src, c->bbytes[e.enc], cudaMemcpyHostToDevice, c->copy_stream));
     CUDA_TRY(c, cudaEventRecord(c->slot_ready[pool][e.slot], c->copy_stream));
+    c->copied[e.kind == 0 ? 0 : 1] += c->bbytes[e.enc];
   }
   return HB_OK;
+}
+
+// ------------------------------------------- device-resident cache (f1)
+static int dc_create(hb_ctx* c) {
+  const hb_config& k = c->cfg;
+  const int L = k.n_layers, E = k.n_experts, nk = L * E;
+  DcState& h = c->dc_h;
+  h.L = L;
+  h.E = E;
+  h.K = k.top_k;
+  h.cap[0] = k.cap_high;
+  h.cap[1] = k.cap_low;
+  h.w[0] = k.w_lru;
+  h.w[1] = k.w_lfu;
+  h.w[2] = k.w_lhu;
+  h.w[3] = k.w_fld;
+  h.random = k.w_lru + k.w_lfu + k.w_lhu + k.w_fld == 0;
+  h.hi_enc = k.hi_enc;
+  h.lo_enc = k.lo_enc;
+  h.upgrade = k.allow_upgrade != 0;
+  h.rank = k.rank;
+  h.world = k.world;
+  h.log_cap = 1 << 16;
+  for (int p = 0; p < 2; ++p) {
+    h.pool_mem[p] = c->pool_mem[p];
+    h.slot_bytes[p] = c->slot_bytes[p];
+  }
+  for (int e = 0; e < 4; ++e) h.bbytes[e] = c->bbytes[e];
+  const char* v = std::getenv("HB_DC_CHUNK_KB");
+  if (v) c->dc_chunk = (size_t)std::max(16, std::atoi(v)) << 10;
+  v = std::getenv("HB_DC_FG_CTAS");
+  if (v) c->dc_fg_ctas = std::min(kGemvCTAs, std::max(1, std::atoi(v)));
+  v = std::getenv("HB_DC_BG_CTAS");
+  if (v) c->dc_bg_ctas = std::min(kGemvCTAs / 2, std::max(1, std::atoi(v)));
+  h.chunk = c->dc_chunk;
+  auto dm = [&](void** p, size_t n, int fill) {
+    if (cudaMalloc(p, std::max<size_t>(n, 16)) != cudaSuccess) return false;
+    return cudaMemset(*p, fill, std::max<size_t>(n, 16)) == cudaSuccess;
+  };
+  bool ok = true;
+  for (int p = 0; p < 2; ++p)
+    ok = ok && dm((void**)&h.pool[p], 4 * (size_t)h.cap[p], 0xff) &&
+         dm((void**)&h.where[p], 4 * (size_t)nk, 0xff) &&
+         dm((void**)&h.task[p], sizeof(DcTask) * h.cap[p], 0);
+  ok = ok && dm((void**)&h.R, 8 * (size_t)nk, 0) && dm((void**)&h.F, 8 * (size_t)nk, 0) &&
+       dm((void**)&h.H, 8 * (size_t)nk, 0) && dm((void**)&h.mask_exp, 4 * (size_t)nk, 0xff) &&
+       dm((void**)&h.masked_keys, 4 * (size_t)nk, 0) && dm((void**)&h.cur, (size_t)nk, 0) &&
+       dm((void**)&h.cur_list, 4 * (size_t)kMaxTopK, 0) &&
+       dm((void**)&h.log, sizeof(hb_event) * h.log_cap, 0) &&
+       dm((void**)&c->host_blob_dev, sizeof(void*) * (size_t)nk * 4, 0) &&
+       dm((void**)&c->dc, sizeof(DcState), 0);
+  if (!ok) return fail(c, HB_ENOMEM, "device cache allocation failed");
+  if (cudaMemcpy(c->dc, &h, sizeof(DcState), cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(c, HB_ECUDA, "device cache init failed");
+  if (cudaHostAlloc((void**)&c->err_host, 16, cudaHostAllocMapped) != cudaSuccess)
+    return fail(c, HB_ENOMEM, "mapped error word allocation failed");
+  *c->err_host = 0;
+  void* eh = nullptr;
+  if (cudaHostGetDevicePointer(&eh, c->err_host, 0) != cudaSuccess)
+    return fail(c, HB_ECUDA, "mapped error word has no device address");
+  c->err_dev = (int*)eh;
+  if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming) != cudaSuccess)
+    return fail(c, HB_ECUDA, "event creation failed");
+  return HB_OK;
+}
+
+static int dc_sticky(hb_ctx* c) {
+  const int e = *(volatile int*)c->err_host;
+  if (!e) return HB_OK;
+  return fail(c, e, e == HB_ECAPACITY ? "device cache: a pool was full and every member masked or in use"
+                                      : "device cache: forward before hb_token_begin (T = 0)");
+}
+
+// one op of the device state machine on stream s (pending token_begin /
+// reset_sequence calls ride along)
+static int dc_op(hb_ctx* c, int op, int layer, hb_decision* dec, int n_pred, int expert, int enc,
+                 cudaStream_t s) {
+  DcParams p{};
+  p.op = op;
+  p.layer = layer;
+  p.n_pred = n_pred;
+  p.expert = expert;
+  p.enc = enc;
+  p.do_reset = c->dc_reset;
+  p.t_add = c->dc_tadd;
+  p.clear_masks = c->dc_clear;
+  c->dc_reset = c->dc_tadd = c->dc_clear = 0;
+  p.dec = dec;
+  p.host_blob = c->host_blob_dev;
+  p.jt = c->jt;
+  p.H = c->cfg.hidden;
+  p.F = c->cfg.ffn;
+  p.err_host = c->err_dev;
+  CUDA_TRY(c, launch_dc_op(c->dc, p, s));
+  c->launches += 1;
+  return HB_OK;
+}
+
+// background copier on the side stream, forked from s (joined by the next forward)
+static int dc_fork_bg(hb_ctx* c, cudaStream_t s) {
+  CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_fork, 0));
+  CUDA_TRY(c, launch_dc_copy_bg(c->dc, c->dc_bg_ctas, c->copy_stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev_side, c->copy_stream));
+  c->side_pending = true;
+  c->launches += 1;
+  return HB_OK;
+}
+
+static int dc_forward(hb_ctx* c, int layer, RouterParams& rp, void* y, cudaStream_t s) {
+  const hb_config& k = c->cfg;
+  const int cn = legacy_au(c, rp, 1);
+  launch_router(rp, s);
+  c->launches += 1;
+  if (int rc = dc_op(c, DC_FORWARD, layer, c->dec, 0, 0, 0, s)) return rc;   // raises yield
+  if (c->side_pending) {                     // join the (yielding) background copier
+    CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_side, 0));
+    c->side_pending = false;
+  }
+  CUDA_TRY(c, launch_dc_copy_fg(c->dc, c->dc_fg_ctas, s));
+  c->launches += 1;
+  if (layer + 1 < k.n_layers)                // background chunks during K2
+    if (int rc = dc_fork_bg(c, s)) return rc;
+  GemvParams gp = gemv_params(c, 1, y, au_buf(c, cn));
+  gp.ctas = kGemvCTAs - c->dc_bg_ctas;       // the background copier keeps its SMs
+  launch_gemv(c, gp, s);
+  if (gp.clean) c->au_dirty[cn] = 0;
+  c->last_host_decisions = false;
+  CUDA_TRY(c, cudaGetLastError());
+  return ep_reduce(c, y, 1, s);
+}
+
+static int dc_events(hb_ctx* c, hb_event* out, int cap) {
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  DcState h;
+  CUDA_TRY(c, cudaMemcpy(&h, c->dc, sizeof(DcState), cudaMemcpyDeviceToHost));
+  if (h.log_overflow) return fail(c, HB_ECAPACITY, "device cache event log overflowed (drain it more often)");
+  if (int rc = dc_sticky(c)) return rc;
+  const int n = std::min(cap, h.log_n);
+  if (n > 0) CUDA_TRY(c, cudaMemcpy(out, h.log, sizeof(hb_event) * n, cudaMemcpyDeviceToHost));
+  // keep the undrained tail at the front of the log
+  if (n < h.log_n) {
+    std::vector<hb_event> rest(h.log_n - n);
+    CUDA_TRY(c, cudaMemcpy(rest.data(), h.log + n, sizeof(hb_event) * rest.size(), cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(h.log, rest.data(), sizeof(hb_event) * rest.size(), cudaMemcpyHostToDevice));
+  }
+  const int left = h.log_n - n;
+  CUDA_TRY(c, cudaMemcpy((char*)c->dc + offsetof(DcState, log_n), &left, sizeof(int), cudaMemcpyHostToDevice));
+  return n;
 }
 
 static void drain_events(hb_ctx* c) {
@@ -1060,6 +1251,10 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   rp.blob_table = nullptr;
   c->last_fused = false;
   c->last_filtered = false;
+  if (c->dc) {
+    if (int rc = dc_sticky(c)) return rc;
+    return dc_forward(c, layer, rp, y, s);
+  }
   const int cn = legacy_au(c, rp, batch);
   launch_router(rp, s);
   c->launches += 1;
@@ -1145,6 +1340,14 @@ int expert_cache_load(hb_ctx* c, int layer, int expert, int enc, void* stream) {
   if (layer < 0 || layer >= k.n_layers || expert < 0 || expert >= k.n_experts)
     return fail(c, HB_EINVAL, "bad layer / expert");
   if (expert % k.world != k.rank) return fail(c, HB_EINVAL, "expert not owned by this rank");
+  if (c->dc) {
+    if (enc != k.hi_enc && enc != k.lo_enc) return fail(c, HB_EINVAL, "encoding is neither hi_enc nor lo_enc");
+    if (int rc = dc_sticky(c)) return rc;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = dc_op(c, DC_LOAD, layer, nullptr, 0, expert, enc, s)) return rc;
+    return dc_fork_bg(c, s);
+  }
   const size_t ev0 = c->cache->events.size();
   bool queued = false;
   int rc = c->cache->load(layer, expert, enc, &queued);
@@ -1163,6 +1366,10 @@ int prefetch_next_layer(hb_ctx* c, int layer, const void* x, int batch, void* st
   if (c->resident) return 0;
   if (batch != 1) return fail(c, HB_EUNSUPPORTED, "prefetch supports batch 1 decode (v1)");
   const int n = std::min(k.lookahead_p, k.n_layers - 1 - layer);
+  if (c->dc && n <= 0) {                             // still expires masks
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    return dc_op(c, DC_PREFETCH, layer, c->dec_pred, 0, 0, 0, (cudaStream_t)stream);
+  }
   if (n <= 0) {
     int pl;
     c->cache->prefetch(layer, 0, nullptr, nullptr, &pl);   // still expires masks
@@ -1182,6 +1389,12 @@ int prefetch_next_layer(hb_ctx* c, int layer, const void* x, int batch, void* st
   const int cn = legacy_au(c, rp, batch);
   launch_router(rp, s);
   c->launches += 1;
+  if (c->dc) {                                       // device walk + background loads
+    (void)cn;
+    if (int rc = dc_op(c, DC_PREFETCH, layer, c->dec_pred, n, 0, 0, s)) return rc;
+    if (int rc = dc_fork_bg(c, s)) return rc;
+    return 0;
+  }
   const int K = k.top_k;
   hb_decision* hd = c->dec_host + K;                 // after the forward's record
   CUDA_TRY(c, cudaMemcpyAsync(hd, c->dec_pred, sizeof(hb_decision) * n * K, cudaMemcpyDeviceToHost, s));
@@ -1248,10 +1461,27 @@ int hb_get_logits(hb_ctx* c, int64_t* out, int cap_pairs) {
 
 int hb_get_events(hb_ctx* c, hb_event* out, int cap) {
   if (!c || (cap > 0 && !out)) return fail(c, HB_EINVAL, "null argument");
+  if (c->dc) return dc_events(c, out, cap);
   const int n = std::min<int>(cap, (int)c->log.size());
   for (int i = 0; i < n; ++i) out[i] = c->log[i];
   c->log.erase(c->log.begin(), c->log.begin() + n);
   return n;
+}
+
+int hb_copy_stats(hb_ctx* c, uint64_t* out) {
+  if (!c || !out) return fail(c, HB_EINVAL, "null argument");
+  if (c->dc) {
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    DcState h;
+    CUDA_TRY(c, cudaMemcpy(&h, c->dc, sizeof(DcState), cudaMemcpyDeviceToHost));
+    out[0] = h.bytes_fg;
+    out[1] = h.bytes_bg;
+  } else {
+    out[0] = c->copied[0];
+    out[1] = c->copied[1];
+  }
+  return HB_OK;
 }
 
 int hb_last_expert_bytes(hb_ctx* c, uint64_t* out) {

@@ -149,6 +149,12 @@ class Context:
         got = self._check(lib.hb_get_events(self._h, buf, cap))
         return [buf[i].as_tuple() for i in range(got)]
 
+    def copy_stats(self):
+        """(foreground, background) bytes copied host -> HBM since creation."""
+        out = (C.c_uint64 * 2)()
+        self._check(lib.hb_copy_stats(self._h, out))
+        return int(out[0]), int(out[1])
+
     def last_expert_bytes(self) -> int:
         v = C.c_uint64()
         self._check(lib.hb_last_expert_bytes(self._h, C.byref(v)))

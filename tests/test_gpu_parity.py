@@ -255,9 +255,9 @@ def test_layer_parity_full_size(shape, pair, tokens):
 
 
 # ------------------------------------------------------------ offload path
-def _offload_ctx(sh, ch, cl, p, w=(1, 1, 1, 1)):
+def _offload_ctx(sh, ch, cl, p, w=(1, 1, 1, 1), dc=0):
     ctx = _ctx(sh, fm.F16, fm.Q4, max_batch=1, cap_high=ch, cap_low=cl, lookahead_p=p,
-               w_lru=w[0], w_lfu=w[1], w_lhu=w[2], w_fld=w[3])
+               w_lru=w[0], w_lfu=w[1], w_lhu=w[2], w_fld=w[3], device_cache=dc)
     store = OracleStore(sh)
     for l in range(sh.n_layers):
         ctx.set_router(l, sg.router_weights(sh, l))
@@ -267,13 +267,15 @@ def _offload_ctx(sh, ch, cl, p, w=(1, 1, 1, 1)):
     return ctx, store
 
 
+@pytest.mark.parametrize("dc", [0, 1])
 @pytest.mark.parametrize("p", [0, 1, 2])
-def test_offload_cache_events_and_outputs(p):
+def test_offload_cache_events_and_outputs(p, dc):
     """Constrained cache (C4 on the tiny shape): cache events bit-exact with
-    O9/O10 and y equal to the oracle computed with the served encodings."""
+    O9/O10 and y equal to the oracle computed with the served encodings; dc=1:
+    the device-resident cache manager with SM copies (hb_config.device_cache)."""
     sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
     ch, cl = 6, 6
-    ctx, store = _offload_ctx(sh, ch, cl, p)
+    ctx, store = _offload_ctx(sh, ch, cl, p, dc=dc)
     ref_cache = oc.ExpertCache(sh.n_layers, sh.n_experts, ch, cl, (1, 1, 1, 1), fm.F16, fm.Q4)
     xs = sg.correlated_states(sh, 12, 0.999, 0.5)
     for t in range(12):
@@ -298,9 +300,10 @@ def test_offload_cache_events_and_outputs(p):
     assert ctx.events() == ref_cache.events
 
 
-def test_offload_explicit_load_and_reset():
+@pytest.mark.parametrize("dc", [0, 1])
+def test_offload_explicit_load_and_reset(dc):
     sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
-    ctx, store = _offload_ctx(sh, 5, 5, 0)
+    ctx, store = _offload_ctx(sh, 5, 5, 0, dc=dc)
     ref_cache = oc.ExpertCache(4, 8, 5, 5, (1, 1, 1, 1), fm.F16, fm.Q4)
     for l, e, enc in [(0, 1, fm.F16), (0, 2, fm.Q4), (1, 3, fm.F16), (0, 1, fm.F16)]:
         ctx.load(l, e, enc)

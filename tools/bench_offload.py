@@ -53,6 +53,15 @@ def main():
     ap.add_argument("--policies", default="",
                     help="Eq. 3 weight sets a:b:c:d (LRU:LFU:LHU:FLD) run at p=1, e.g. "
                          "1:0:0:0,0:1:0:0,0:0:1:0,0:0:0:1,1:1:1:1 (SURVEY 8(f) f2, P:631, P:1040)")
+    ap.add_argument("--device-cache", default="0",
+                    help="comma list of hb_config.device_cache values to run (1: device-resident "
+                         "cache manager + SM copies, SURVEY 8(f) f1)")
+    ap.add_argument("--graph", action="store_true",
+                    help="device_cache=1 runs: capture one token in a CUDA graph and replay it")
+    ap.add_argument("--no-off", action="store_true", help="skip the T1=T2=1 (dynamic loading off) run")
+    ap.add_argument("--env", default="",
+                    help="'|'-separated library env settings 'K=V,K=V' to run each config under "
+                         "(read at hb_create), e.g. HB_DC_FG_CTAS=16|HB_DC_FG_CTAS=64")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     base = {"mixtral": sg.MIXTRAL, "phi": sg.PHI}[args.model]
@@ -87,13 +96,22 @@ def main():
     cap_l = max(3, round(56 * L / 32 * E / 8))
     xs = torch.from_numpy(sg.correlated_states(shape, args.tokens + 1, 0.999, args.rho)).cuda()
     y = torch.empty(1, H, dtype=torch.float32, device="cuda")
-    runs = [(int(p), 0.6, 0.9, (1, 1, 1, 1)) for p in args.p.split(",") if p] + [(1, 1.0, 1.0, (1, 1, 1, 1))]
+    runs = [(int(p), 0.6, 0.9, (1, 1, 1, 1)) for p in args.p.split(",") if p]
+    if not args.no_off:
+        runs += [(1, 1.0, 1.0, (1, 1, 1, 1))]
     runs += [(1, 0.6, 0.9, tuple(int(v) for v in w.split(":"))) for w in args.policies.split(",") if w]
-    for p, t1, t2, w in runs:
+    runs = [r + (int(dc),) for dc in args.device_cache.split(",") for r in runs]
+    envs = args.env.split("|") if args.env else [""]
+    runs = [r + (e,) for e in envs for r in runs]
+    for p, t1, t2, w, dc, env in runs:
+        for kv in env.split(","):
+            if kv:
+                k_, v_ = kv.split("=")
+                os.environ[k_] = v_
         cfg = h.default_config(n_layers=L, n_experts=E, top_k=2, hidden=H, ffn=F, hi_enc=hi,
                                lo_enc=lo, t1=t1, t2=t2, max_batch=1, cap_high=cap_h,
                                cap_low=cap_l, lookahead_p=p, w_lru=w[0], w_lfu=w[1], w_lhu=w[2],
-                               w_fld=w[3])
+                               w_fld=w[3], device_cache=dc)
         ctx = h.Context(cfg)
         for l in range(L):
             ctx.set_router(l, sg.router_weights(shape, l))
@@ -112,16 +130,33 @@ def main():
             token(0)                                     # warm-up (cold cache)
             torch.cuda.synchronize()
             ctx.events()
+            graph = None
+            if dc and args.graph:                        # one token captured, replayed per token
+                xg = torch.empty(L, 1, H, dtype=torch.float16, device="cuda")
+                xg.copy_(xs[1].view(L, 1, H))
+                graph = torch.cuda.CUDAGraph()
+                ctx.token_begin()                        # baked into the captured first forward
+                with torch.cuda.graph(graph, stream=stream):
+                    for l in range(L):
+                        ctx.forward(l, xg[l], y, stream=stream)
+                        if p > 0:
+                            ctx.prefetch(l, xg[l], stream=stream)
+            c0 = ctx.copy_stats()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             w0 = time.time()
             for t in range(1, args.tokens + 1):
-                token(t)
+                if graph is not None:
+                    xg.copy_(xs[t].view(L, 1, H))
+                    graph.replay()
+                else:
+                    token(t)
             e1.record(stream)
             torch.cuda.synchronize()
             wall = time.time() - w0
             ms = e0.elapsed_time(e1)
             ev = ctx.events()
+            c1 = ctx.copy_stats()
         loads = [e for e in ev if e[0] == 1]
         hits = [e for e in ev if e[0] == 0]
         h2d = sum(bb[e[4]] for e in loads)
@@ -137,10 +172,17 @@ def main():
                "h2d_peak_gbs": round(peak, 2), "h2d_frac": round(h2d / (ms * 1e-3) / 1e9 / peak, 4),
                "loads_per_token": round(len(loads) / n, 2), "prefetch_loads": n_pref,
                "hit_ratio": round(len(hits) / max(1, len(hits) + len(loads) - n_pref), 4),
+               "device_cache": dc, "graph": bool(graph is not None), "env": env,
+               "copied_fg_bytes_per_token": int((c1[0] - c0[0]) / n),
+               "copied_bg_bytes_per_token": int((c1[1] - c0[1]) / n),
+               "copied_gbs": round((c1[0] + c1[1] - c0[0] - c0[1]) / (ms * 1e-3) / 1e9, 2),
                "init_s": round(t_init, 1)}
         print(json.dumps(out), flush=True)
         del ctx
         torch.cuda.empty_cache()
+        for kv in env.split(","):
+            if kv:
+                os.environ.pop(kv.split("=")[0], None)
 
 
 if __name__ == "__main__":
