@@ -752,9 +752,16 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
       stage_h_and_wait<FUSED>(p, S);
     }
   }
+#ifndef HB_K2B_PRE
+#define HB_K2B_PRE 64
+#endif
+  // K2b: HB_K2B_PRE stages before waiting for h (diagnostic knob), the rest after
+  constexpr int PRE = (!FUSED && !W13) ? (HB_K2B_PRE < DEPTH - 1 ? HB_K2B_PRE : DEPTH - 1) : DEPTH - 1;
 #pragma unroll 1
-  for (int s = 0; s < DEPTH - 1; ++s) issue();
+  for (int s = 0; s < PRE; ++s) issue();
   if (!FUSED && !W13 && first) stage_h_and_wait<FUSED>(p, S);  // h after K2a (hfin)
+#pragma unroll 1
+  for (int s = PRE; s < DEPTH - 1; ++s) issue();
   if (first) HB_TL(W13, (threadIdx.x >> 5) * gridDim.x + blockIdx.x, 2);
 
   // ---- lane constants: B-operand rows, outputs of the lane's two slots
@@ -1805,7 +1812,9 @@ fused_decode_kernel(const __grid_constant__ FusedParams fp) {
 // rows 8t..8t+7 (short dependency chains: this kernel sits between K2a and
 // K2b on every layer's critical path).
 __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvParams p) {
+#ifndef HB_HFIN_LATE
   pdl_trigger();                             // K2b may launch and prefetch its weights
+#endif
   pdl_wait();                                // the K2a sums
 #if HB_LEGACY_TL == 1
   if (threadIdx.x == 0) tl_min(tl_rec(p.stamps, p.stamp_cap, p.fwd_idx), 9, tl_now());
@@ -1843,7 +1852,8 @@ __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvP
   float h[8], hs = 0.f;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    h[r] = av[r] / (1.f + expf(-av[r])) * uv[r];
+    // silu(a) u with the SFU exp and reciprocal (~2 ulp; h feeds W2 at ~fp32 precision)
+    h[r] = av[r] * __frcp_rn(1.f + __expf(-av[r])) * uv[r];
     hs += h[r];
   }
   uint32_t wh[4], wl[4];
@@ -1864,6 +1874,9 @@ __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvP
   }
 #if HB_LEGACY_TL == 1
   if ((threadIdx.x & 31) == 0) tl_max(tl_rec(p.stamps, p.stamp_cap, p.fwd_idx), 10, tl_now());
+#endif
+#ifdef HB_HFIN_LATE
+  pdl_trigger();                             // diagnostic: K2b launches once h is written
 #endif
 }
 
@@ -1894,9 +1907,18 @@ bool fused_fits(int E, int H, int F, int hi_enc, int lo_enc) {
   }
   return true;
 }
+// hfin's CTAs are launched while K2a still holds every SM but the router's:
+// a large (unused) shared-memory request keeps them one per SM, so they do
+// not pile onto the first free SM and run serially there (measured: 8 CTAs
+// on one SM, ~6 us; HB_HFIN_SMEM_KB, 0 = no request)
+#ifndef HB_HFIN_SMEM_KB
+#define HB_HFIN_SMEM_KB 120
+#endif
 void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
   const int n = max_slots * (p.F / 32) * 4;
-  launch_pdl(hfin_kernel, std::max((n + 255) / 256, p.B), 256, 0, s, p);   // >= one CTA per token (R28)
+  constexpr int smem = HB_HFIN_SMEM_KB * 1024;
+  if (smem > 48 * 1024) set_max_dyn_smem(hfin_kernel, smem);
+  launch_pdl(hfin_kernel, std::max((n + 255) / 256, p.B), 256, smem, s, p);   // >= one CTA per token (R28)
 }
 void launch_w2(const GemvParams& p, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<false>();
