@@ -106,6 +106,18 @@ typedef struct {
                                        are sticky and reported by the next call, and a captured
                                        sequence must end with a moe_layer_forward (it joins the
                                        background copier) */
+  int token_sharded;                /* resident mode, strict.  1: token-sharded expert
+                                       parallelism: each rank passes ITS OWN
+                                       max_batch tokens; the router runs on them, every
+                                       non-skipped selection is sent (x row + hb_ts_meta) to the
+                                       rank owning the expert (e % world) in a fixed-capacity slot
+                                       (C = max_batch * top_k rows per peer), the owner computes
+                                       its received rows as one batch and sends the gate-weighted
+                                       outputs back, and y[b] = the sum of the token's k rows.
+                                       moe_layer_forward does the two exchanges with NCCL
+                                       (hb_nccl_init) -- for world 1 without NCCL, locally; the
+                                       staged calls hb_ts_dispatch / hb_ts_compute / hb_ts_combine
+                                       leave the exchanges to the caller */
 } hb_config;
 
 /* One routed (token, rank) pair of the last forward (inspection / parity). */
@@ -127,6 +139,16 @@ typedef struct {
   int32_t slot;                     /* slot index in the pool of enc */
   int32_t victim;                   /* evicted key layer*E+expert, or -1 */
 } hb_event;
+
+/* Token-sharded EP (hb_config.token_sharded): the record that travels with
+ * each dispatched selection (the x row travels in a parallel rows buffer). */
+typedef struct {
+  int32_t token;                    /* source token index, -1 = empty slot */
+  int32_t expert;                   /* e_i (owned by the receiving rank) */
+  uint8_t prec;                     /* HB_HIGH / HB_LOW */
+  uint8_t pad[3];
+  float gate;                       /* G(x)_{e_i} computed by the source's router */
+} hb_ts_meta;
 
 typedef struct hb_ctx hb_ctx;
 
@@ -261,6 +283,29 @@ int hb_get_decisions(hb_ctx* ctx, hb_decision* out, int cap);
 int hb_get_logits(hb_ctx* ctx, int64_t* out, int cap_pairs);
 /* Cache events since the last call (offload mode). Returns the count. */
 int hb_get_events(hb_ctx* ctx, hb_event* out, int cap);
+/* Token-sharded EP, staged (hb_config.token_sharded = 1).
+ * Buffers are device memory owned by the caller, laid out per peer rank r:
+ * meta [world][C] hb_ts_meta, rows [world][C][hidden] fp16, ret [world][C][hidden]
+ * fp32, C = max_batch * top_k; hb_ts_buffer_bytes gives the sizes.
+ *  hb_ts_dispatch: routes x [batch, hidden] (this rank's tokens, exact decisions)
+ *    and writes block r of meta_send / rows_send with the selections owned by
+ *    rank r (empty slots: token = -1).  The caller then sends block r to rank r
+ *    (all-to-all) and receives block r from rank r into meta_recv / rows_recv.
+ *  hb_ts_compute: the received rows as one batch (each row's selection, Eq. 1
+ *    terms g * E_e(x) of the source token) -> ret_send block r = the rows that
+ *    came from rank r.  The caller returns block r to rank r (all-to-all).
+ *  hb_ts_combine: y [batch, hidden] fp32 <- per token the sum of its returned
+ *    rows (rank order), NaN rows for non-finite x (R28).  Needs the dispatch of
+ *    the same batch on this context just before.
+ * Errors: HB_ESTATE if the context is not token-sharded; HB_EINVAL on bad
+ * sizes / pointers. */
+int hb_ts_buffer_bytes(hb_ctx* ctx, size_t* meta_bytes, size_t* rows_bytes, size_t* ret_bytes);
+int hb_ts_dispatch(hb_ctx* ctx, int layer, const void* x, int batch, void* meta_send,
+                   void* rows_send, void* stream);
+int hb_ts_compute(hb_ctx* ctx, int layer, const void* meta_recv, const void* rows_recv,
+                  void* ret_send, void* stream);
+int hb_ts_combine(hb_ctx* ctx, const void* ret_recv, int batch, void* y, void* stream);
+
 /* Bytes moved host -> HBM for expert loads since hb_create (offload mode;
  * synchronises the device): out[0] foreground (on the forward's critical
  * path: on-demand loads, and in device_cache mode the rest of a prefetch the

@@ -98,6 +98,48 @@ def tp_slice(w1: np.ndarray, w3: np.ndarray, w2: np.ndarray, tp_rank: int, tp_wo
     return w1[f0:f1], w3[f0:f1], w2[:, f0:f1]
 
 
+def ts_dispatch_plan(routes, world: int, capacity: int):
+    """Token-sharded EP, dispatch side: every non-skipped
+    selection (token b, rank i) goes to the owner of its expert, owner(e) =
+    e mod world, at the next free slot of that destination, selections taken
+    in (token, rank) order.  Returns pos[b][i] = dest * capacity + slot or -1,
+    and per destination the list of (token, expert, decision, gate)."""
+    pos = [[-1] * len(r.experts) for r in routes]
+    sent = [[] for _ in range(world)]
+    for b, r in enumerate(routes):
+        for i, (e, g, d) in enumerate(zip(r.experts, r.gates, r.decisions)):
+            if d == SKIP:
+                continue
+            q = owner(e, world)
+            if len(sent[q]) >= capacity:
+                raise ValueError("token-sharded capacity exceeded")
+            pos[b][i] = q * capacity + len(sent[q])
+            sent[q].append((b, e, d, g))
+    return pos, sent
+
+
+def ts_owner_rows(x_rows: np.ndarray, records, store: ExpertStore, layer: int, hi_enc: int,
+                  lo_enc: int) -> np.ndarray:
+    """Token-sharded EP, owner side: each received row is one term of Eq. 1,
+    g * E_e(x) with the source's gate and the strict served encoding."""
+    out = np.zeros((len(records), x_rows.shape[1]), dtype=np.float64)
+    for j, (_, e, d, g) in enumerate(records):
+        w1, w3, w2 = store.get(layer, e, served_encoding_strict(d, hi_enc, lo_enc))
+        out[j] = g * expert_ffn(w1, w3, w2, x_rows[j].astype(np.float64))
+    return out
+
+
+def ts_combine(pos, returned: np.ndarray, H: int) -> np.ndarray:
+    """Token-sharded EP, source side: y[b] = sum over the token's selections
+    (rank order) of its returned rows (returned[dest * capacity + slot])."""
+    y = np.zeros((len(pos), H), dtype=np.float64)
+    for b, row in enumerate(pos):
+        for p_ in row:
+            if p_ >= 0:
+                y[b] += returned[p_]
+    return y
+
+
 def moe_layer(x16: np.ndarray, wg16: np.ndarray, store: ExpertStore, layer: int,
               k: int, t1: float, t2: float, hi_enc: int, lo_enc: int,
               rank: int = 0, world: int = 1, served=None, tp_rank: int = 0, tp_world: int = 1):

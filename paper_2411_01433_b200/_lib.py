@@ -41,7 +41,7 @@ class hb_config(C.Structure):
                 ("w_lru", C.c_int), ("w_lfu", C.c_int), ("w_lhu", C.c_int), ("w_fld", C.c_int),
                 ("cap_high", C.c_int), ("cap_low", C.c_int), ("allow_upgrade", C.c_int),
                 ("rank", C.c_int), ("world", C.c_int), ("max_batch", C.c_int),
-                ("strict", C.c_int), ("device_cache", C.c_int)]
+                ("strict", C.c_int), ("device_cache", C.c_int), ("token_sharded", C.c_int)]
 
 
 class hb_decision(C.Structure):
@@ -85,6 +85,11 @@ _SIGS = {
     "hb_get_events": (C.c_int, [_P, C.POINTER(hb_event), C.c_int]),
     "hb_last_expert_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "hb_copy_stats": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "hb_ts_buffer_bytes": (C.c_int, [_P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                     C.POINTER(C.c_size_t)]),
+    "hb_ts_dispatch": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, _P]),
+    "hb_ts_compute": (C.c_int, [_P, C.c_int, _P, _P, _P, _P]),
+    "hb_ts_combine": (C.c_int, [_P, _P, C.c_int, _P, _P]),
     "hb_launch_count": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "hb_set_batched_min": (C.c_int, [_P, C.c_int]),
     "hb_nccl_unique_id": (C.c_int, [_P]),

@@ -112,6 +112,16 @@ struct hb_ctx {
   int dc_fg_ctas = 32, dc_bg_ctas = 16;   // HB_DC_FG_CTAS / HB_DC_BG_CTAS
   size_t dc_chunk = 256u << 10;           // HB_DC_CHUNK_KB
   uint64_t copied[2] = {0, 0};            // host path: bytes issued on demand / prefetch+explicit
+  // token-sharded EP (hb_config.token_sharded)
+  bool ts = false;
+  int ts_C = 0;                           // rows per (source, destination) = max_batch * top_k
+  hb_decision* ts_dec = nullptr;          // local decisions [max_batch][k]
+  int* ts_pos = nullptr;                  // [max_batch][k] dest * C + position or -1
+  int* ts_rowbad = nullptr;               // [max_batch]
+  int ts_batch = 0;                       // batch of the last dispatch
+  hb_ts_meta* ts_meta[2] = {nullptr, nullptr};   // one-shot forward: send / recv
+  __half* ts_rows[2] = {nullptr, nullptr};
+  float* ts_ret[2] = {nullptr, nullptr};
   // scratch
   hb_decision* dec = nullptr;             // [B][k]
   hb_decision* dec_pred = nullptr;        // [p][B][k]
@@ -206,6 +216,10 @@ struct NcclApi {
   int (*comm_destroy)(void*) = nullptr;
   int (*broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   const char* (*error_string)(int) = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
   bool ok = false;
 };
 static NcclApi& nccl_api() {
@@ -225,13 +239,17 @@ static NcclApi& nccl_api() {
       api.broadcast = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
           h, "ncclBroadcast");
       api.error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+      api.send = (int (*)(const void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclSend");
+      api.recv = (int (*)(void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclRecv");
+      api.group_start = (int (*)())dlsym(h, "ncclGroupStart");
+      api.group_end = (int (*)())dlsym(h, "ncclGroupEnd");
       api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy &&
                api.broadcast;
     }
   }
   return api;
 }
-constexpr int kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclSum = 0;
+constexpr int kNcclInt8 = 0, kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclSum = 0;
 
 extern "C" {
 
@@ -324,7 +342,9 @@ static void free_ctx(hb_ctx* c) {
                    c->dc, c->host_blob_dev, c->dc_h.pool[0], c->dc_h.pool[1], c->dc_h.where[0],
                    c->dc_h.where[1], c->dc_h.R, c->dc_h.F, c->dc_h.H, c->dc_h.mask_exp,
                    c->dc_h.masked_keys, c->dc_h.cur, c->dc_h.cur_list, c->dc_h.log,
-                   c->dc_h.task[0], c->dc_h.task[1]};
+                   c->dc_h.task[0], c->dc_h.task[1], c->ts_dec, c->ts_pos, c->ts_rowbad,
+                   c->ts_meta[0], c->ts_meta[1], c->ts_rows[0], c->ts_rows[1], c->ts_ret[0],
+                   c->ts_ret[1]};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (c->dec_host) cudaFreeHost(c->dec_host);
@@ -384,8 +404,13 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     return code;
   };
   if (cudaSetDevice(device) != cudaSuccess) return bail(HB_ECUDA, "cudaSetDevice failed");
-  const int L = k.n_layers, E = k.n_experts, B = k.max_batch, K = k.top_k, H = k.hidden,
-            F = k.ffn;
+  if (k.token_sharded && (!resident || !k.strict))
+    return fail(nullptr, HB_EINVAL, "token_sharded needs resident mode and strict = 1");
+  // token-sharded: the owner computes up to world * max_batch * top_k received
+  // rows per forward -- the batch every buffer below is sized for
+  const int L = k.n_layers, E = k.n_experts,
+            B = k.token_sharded ? k.world * k.max_batch * k.top_k : k.max_batch, K = k.top_k,
+            H = k.hidden, F = k.ffn;
   const int P = std::max(1, k.lookahead_p);
   c->max_slots = B * K;
   c->max_jobs = std::min(2 * E, B * K) + 1;
@@ -529,6 +554,18 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     if (k.device_cache) {
       if (int rc = dc_create(c)) return bail(rc, c->err);
     }
+  }
+  if (k.token_sharded) {
+    c->ts = true;
+    c->ts_C = k.max_batch * K;
+    const size_t nr = (size_t)k.world * c->ts_C;
+    bool tok = dm((void**)&c->ts_dec, sizeof(hb_decision) * k.max_batch * K) &&
+               dm((void**)&c->ts_pos, sizeof(int) * k.max_batch * K) &&
+               dm((void**)&c->ts_rowbad, sizeof(int) * k.max_batch);
+    for (int i = 0; i < 2; ++i)
+      tok = tok && dm((void**)&c->ts_meta[i], sizeof(hb_ts_meta) * nr) &&
+            dm((void**)&c->ts_rows[i], nr * H * 2) && dm((void**)&c->ts_ret[i], nr * H * 4);
+    if (!tok) return bail(HB_ENOMEM, "token-sharded buffers allocation failed");
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(HB_ECUDA, "device sync failed");
   *out = c;
@@ -1005,6 +1042,122 @@ static int issue_loads(hb_ctx* c, size_t from) {
   return HB_OK;
 }
 
+// ------------------------------------------- token-sharded EP (f3)
+static int ts_dispatch(hb_ctx* c, int layer, const void* x, int batch, hb_ts_meta* meta,
+                       __half* rows, cudaStream_t s) {
+  const hb_config& k = c->cfg;
+  RouterParams rp = router_params(c, x, batch);
+  rp.wg[0] = router_of(c, layer);
+  rp.n_route = 1;
+  rp.dec = c->ts_dec;
+  rp.rowbad = c->ts_rowbad;
+  rp.logits = nullptr;
+  rp.x_perm = nullptr;
+  rp.xsum = nullptr;
+  rp.blob_table = nullptr;
+  launch_router(rp, s);
+  CUDA_TRY(c, cudaMemsetAsync(meta, 0xff, sizeof(hb_ts_meta) * (size_t)k.world * c->ts_C, s));
+  TsParams tp{};
+  tp.dec = c->ts_dec;
+  tp.x = (const __half*)x;
+  tp.B = batch;
+  tp.k = k.top_k;
+  tp.H = k.hidden;
+  tp.R = k.world;
+  tp.C = c->ts_C;
+  tp.pos = c->ts_pos;
+  tp.meta_send = meta;
+  tp.rows_send = rows;
+  launch_ts_pack(tp, s);
+  c->launches += 2;
+  c->ts_batch = batch;
+  CUDA_TRY(c, cudaGetLastError());
+  return HB_OK;
+}
+
+static int ts_compute(hb_ctx* c, int layer, const hb_ts_meta* meta, const __half* rows, float* ret,
+                      cudaStream_t s) {
+  const hb_config& k = c->cfg;
+  const int n = k.world * c->ts_C;
+  RouterParams rp = router_params(c, rows, n);
+  rp.strict = 1;
+  rp.dec = c->dec;
+  rp.x_perm = c->x_perm;
+  rp.xsum = c->xsum;
+  rp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
+  launch_ts_jobs(rp, meta, rows, ret, s);
+  c->launches += 1;
+  c->last_batch = n;
+  c->last_layer = layer;
+  c->last_fused = false;
+  c->last_filtered = true;                   // no exact logits for hb_get_logits here
+  c->last_host_decisions = false;
+  if (c->k3_ok && c->k3_min_batch > 0 && n >= c->k3_min_batch) {
+    launch_batched(c, layer, rows, ret, s);
+  } else {
+    const int cn = c->au_cur;
+    if (c->au_dirty[cn]) CUDA_TRY(c, cudaMemsetAsync(au_buf(c, cn), 0, (size_t)c->au_dirty[cn] * 4, s));
+    c->au_dirty[cn] = 0;
+    GemvParams gp = gemv_params(c, n, ret, au_buf(c, cn));
+    launch_gemv(c, gp, s);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  return HB_OK;
+}
+
+static int ts_combine(hb_ctx* c, const float* ret, int batch, void* y, cudaStream_t s) {
+  TsParams tp{};
+  tp.B = batch;
+  tp.k = c->cfg.top_k;
+  tp.H = c->cfg.hidden;
+  tp.R = c->cfg.world;
+  tp.C = c->ts_C;
+  tp.pos = c->ts_pos;
+  tp.ret = ret;
+  tp.y = (float*)y;
+  tp.rowbad = c->ts_rowbad;
+  launch_ts_combine(tp, s);
+  c->launches += 1;
+  CUDA_TRY(c, cudaGetLastError());
+  return HB_OK;
+}
+
+// block r of send -> rank r, block r of recv <- rank r (bytes per block)
+static int ts_exchange(hb_ctx* c, const void* send, void* recv, size_t block, cudaStream_t s) {
+  NcclApi& api = nccl_api();
+  if (!api.send || !api.recv || !api.group_start || !api.group_end)
+    return fail(c, HB_EUNSUPPORTED, "ncclSend / ncclRecv not found");
+  int r = api.group_start();
+  for (int q = 0; q < c->cfg.world && r == 0; ++q) {
+    r = api.send((const char*)send + q * block, block, kNcclInt8, q, c->nccl_comm, s);
+    if (r == 0) r = api.recv((char*)recv + q * block, block, kNcclInt8, q, c->nccl_comm, s);
+  }
+  const int r2 = api.group_end();
+  if (r == 0) r = r2;
+  if (r != 0)
+    return fail(c, HB_ENCCL, std::string("token-sharded exchange: ") +
+                                 (api.error_string ? api.error_string(r) : "error"));
+  return HB_OK;
+}
+
+static int ts_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, cudaStream_t s) {
+  const hb_config& k = c->cfg;
+  if (!c->nccl_comm && k.world > 1)
+    return fail(c, HB_ESTATE, "token-sharded forward with world > 1 needs hb_nccl_init");
+  const size_t nr = (size_t)k.world * c->ts_C;
+  if (int rc = ts_dispatch(c, layer, x, batch, c->ts_meta[0], c->ts_rows[0], s)) return rc;
+  const int in = c->nccl_comm ? 1 : 0;       // world 1 without NCCL: the send buffers are the input
+  if (c->nccl_comm) {
+    if (int rc = ts_exchange(c, c->ts_meta[0], c->ts_meta[1], sizeof(hb_ts_meta) * c->ts_C, s)) return rc;
+    if (int rc = ts_exchange(c, c->ts_rows[0], c->ts_rows[1], (size_t)c->ts_C * k.hidden * 2, s)) return rc;
+  }
+  if (int rc = ts_compute(c, layer, c->ts_meta[in], c->ts_rows[in], c->ts_ret[0], s)) return rc;
+  if (c->nccl_comm)
+    if (int rc = ts_exchange(c, c->ts_ret[0], c->ts_ret[1], (size_t)c->ts_C * k.hidden * 4, s)) return rc;
+  (void)nr;
+  return ts_combine(c, c->ts_ret[in], batch, y, s);
+}
+
 // ------------------------------------------- device-resident cache (f1)
 static int dc_create(hb_ctx* c) {
   const hb_config& k = c->cfg;
@@ -1187,6 +1340,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
   c->last_batch = batch;
   c->last_layer = layer;
 
+  if (c->ts) return ts_forward(c, layer, x, batch, y, s);
   if (c->resident) {
     rp.blob_table = c->dev_blob_table + (size_t)layer * k.n_experts * 4;
     const bool k3 = c->k3_ok && c->k3_min_batch > 0 && batch >= c->k3_min_batch;
@@ -1482,6 +1636,54 @@ int hb_copy_stats(hb_ctx* c, uint64_t* out) {
     out[1] = c->copied[1];
   }
   return HB_OK;
+}
+
+int hb_ts_buffer_bytes(hb_ctx* c, size_t* meta_bytes, size_t* rows_bytes, size_t* ret_bytes) {
+  if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  if (!c->ts) return fail(c, HB_ESTATE, "context is not token-sharded");
+  const size_t nr = (size_t)c->cfg.world * c->ts_C;
+  if (meta_bytes) *meta_bytes = sizeof(hb_ts_meta) * nr;
+  if (rows_bytes) *rows_bytes = nr * c->cfg.hidden * 2;
+  if (ret_bytes) *ret_bytes = nr * c->cfg.hidden * 4;
+  return HB_OK;
+}
+
+static int ts_check(hb_ctx* c, int layer) {
+  if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  if (!c->ts) return fail(c, HB_ESTATE, "context is not token-sharded");
+  if (layer < 0 || layer >= c->cfg.n_layers) return fail(c, HB_EINVAL, "bad layer");
+  if (!c->router_set[layer]) return fail(c, HB_ESTATE, "router of this layer not set");
+  return HB_OK;
+}
+
+int hb_ts_dispatch(hb_ctx* c, int layer, const void* x, int batch, void* meta_send, void* rows_send,
+                   void* stream) {
+  if (int rc = ts_check(c, layer)) return rc;
+  if (!x || !meta_send || !rows_send) return fail(c, HB_EINVAL, "null argument");
+  if (batch <= 0 || batch > c->cfg.max_batch) return fail(c, HB_EINVAL, "batch must be in [1, max_batch]");
+  if (((uintptr_t)x & 15) || ((uintptr_t)rows_send & 15)) return fail(c, HB_EINVAL, "x / rows must be 16-byte aligned");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return ts_dispatch(c, layer, x, batch, (hb_ts_meta*)meta_send, (__half*)rows_send, (cudaStream_t)stream);
+}
+
+int hb_ts_compute(hb_ctx* c, int layer, const void* meta_recv, const void* rows_recv, void* ret_send,
+                  void* stream) {
+  if (int rc = ts_check(c, layer)) return rc;
+  if (!meta_recv || !rows_recv || !ret_send) return fail(c, HB_EINVAL, "null argument");
+  if (((uintptr_t)rows_recv & 15) || ((uintptr_t)ret_send & 15)) return fail(c, HB_EINVAL, "buffers must be 16-byte aligned");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return ts_compute(c, layer, (const hb_ts_meta*)meta_recv, (const __half*)rows_recv, (float*)ret_send,
+                    (cudaStream_t)stream);
+}
+
+int hb_ts_combine(hb_ctx* c, const void* ret_recv, int batch, void* y, void* stream) {
+  if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  if (!c->ts) return fail(c, HB_ESTATE, "context is not token-sharded");
+  if (!ret_recv || !y) return fail(c, HB_EINVAL, "null argument");
+  if (batch != c->ts_batch) return fail(c, HB_ESTATE, "combine needs the dispatch of the same batch");
+  if (((uintptr_t)ret_recv & 15) || ((uintptr_t)y & 15)) return fail(c, HB_EINVAL, "buffers must be 16-byte aligned");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return ts_combine(c, (const float*)ret_recv, batch, y, (cudaStream_t)stream);
 }
 
 int hb_last_expert_bytes(hb_ctx* c, uint64_t* out) {

@@ -208,6 +208,31 @@ struct FusedParams {
 void launch_fused(const FusedParams& p, bool split, cudaStream_t s);
 bool fused_fits(int E, int H, int F, int hi_enc, int lo_enc);
 void launch_router(const RouterParams& p, cudaStream_t s);
+
+// Token-sharded expert parallelism (router.cu): the tokens of
+// a layer are split over the ranks; each rank routes its own tokens, sends
+// every non-skipped selection (x row + this record) to the rank owning the
+// expert (e % R), computes the selections it received as a batch of rows with
+// one selection each, and sends the gate-weighted outputs back, where each
+// token sums its k contributions.  Fixed capacity C rows per (source, dest):
+// no counts exchange, no host sync.
+struct TsParams {
+  const hb_decision* dec;      // local decisions [B][k] (the router's)
+  const __half* x;             // local x [B][H]
+  int B, k, H, R, C;
+  int* pos;                    // [B][k] dest * C + position, or -1 (Skip)
+  hb_ts_meta* meta_send;       // [R][C]
+  __half* rows_send;           // [R][C][H]
+  const float* ret;            // [R][C][H] gate-weighted expert outputs of this rank's rows
+  float* y;                    // [B][H]
+  const int* rowbad;           // [B] non-finite x (R28): NaN row
+};
+void launch_ts_pack(const TsParams& p, cudaStream_t s);
+void launch_ts_combine(const TsParams& p, cudaStream_t s);
+// decisions (one selection per received row, the rest Skip), pair-permuted x,
+// zeroed rowbad and y, then the job table (p.blob_table) of the n = p.B rows
+void launch_ts_jobs(const RouterParams& p, const hb_ts_meta* meta, const __half* rows, float* y,
+                    cudaStream_t s);
 // batch-1 decode router on one reserved SM (router.cu); the GEMV kernels then
 // run on kNumSM - 1 CTAs and hfin cleans the sums / zeroes y (GemvParams::clean)
 bool router_solo_fits(int E, int H, int k);

@@ -1588,6 +1588,118 @@ void launch_router(const RouterParams& p, cudaStream_t s) {
   }
 }
 
+// ------------------------------------------------ token-sharded EP (f3)
+// One CTA per local selection j = b*k + i: its slot in the send buffer of the
+// owner rank (selections in (token, rank) order per destination: a prefix
+// count over the decisions, deterministic), the record and the x row.
+__global__ void __launch_bounds__(128) ts_pack_kernel(const __grid_constant__ TsParams p) {
+  const int j = blockIdx.x, tid = threadIdx.x;
+  __shared__ int s_pos;
+  const hb_decision d = p.dec[j];
+  const bool live = d.prec != HB_SKIP && d.expert >= 0;
+  if (tid == 0) {
+    int pos = -1;
+    if (live) {
+      const int dest = d.expert % p.R;
+      int n = 0;
+      for (int q = 0; q < j; ++q) {
+        const hb_decision o = p.dec[q];
+        n += (o.prec != HB_SKIP && o.expert >= 0 && o.expert % p.R == dest);
+      }
+      pos = dest * p.C + n;
+      hb_ts_meta m;
+      m.token = j / p.k;
+      m.expert = d.expert;
+      m.prec = d.prec;
+      m.pad[0] = m.pad[1] = m.pad[2] = 0;
+      m.gate = d.gate;
+      p.meta_send[pos] = m;
+    }
+    p.pos[j] = pos;
+    s_pos = pos;
+  }
+  __syncthreads();
+  const int pos = s_pos;
+  if (pos < 0) return;
+  const uint4* src = reinterpret_cast<const uint4*>(p.x + (size_t)(j / p.k) * p.H);
+  uint4* dst = reinterpret_cast<uint4*>(p.rows_send + (size_t)pos * p.H);
+  for (int i = tid; i < p.H / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+// y[b] = sum over the token's selections (rank order) of the returned rows;
+// NaN for a token whose x was non-finite (R28)
+__global__ void __launch_bounds__(256) ts_combine_kernel(const __grid_constant__ TsParams p) {
+  const int b = blockIdx.x;
+  const bool bad = p.rowbad && p.rowbad[b];
+  int pos[kMaxTopK];
+  for (int i = 0; i < p.k; ++i) pos[i] = p.pos[b * p.k + i];
+  for (int c = threadIdx.x * 4; c < p.H; c += blockDim.x * 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < p.k; ++i) {
+      if (pos[i] < 0) continue;
+      const float4 v = *reinterpret_cast<const float4*>(p.ret + (size_t)pos[i] * p.H + c);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (bad) acc = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
+                               __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+    *reinterpret_cast<float4*>(p.y + (size_t)b * p.H + c) = acc;
+  }
+}
+
+// Received rows -> the owner's batch: one CTA per row writes the row's k
+// decision records (its selection at rank 0, Skip after), its pair-permuted x
+// and block sums, zero rowbad and zero y; the last CTA builds the job table.
+__global__ void __launch_bounds__(kRouterThreads)
+ts_jobs_kernel(const __grid_constant__ RouterParams p, const hb_ts_meta* meta, const __half* rows,
+               float* y) {
+  __shared__ BatchSmem sm;
+  const int j = blockIdx.x, tid = threadIdx.x;
+  if (tid < p.k) {
+    const hb_ts_meta m = meta[j];
+    hb_decision d;
+    d.token = j;
+    d.sel_rank = (uint8_t)tid;
+    d.served_enc = HB_ENC_NONE;
+    d.hit = 0;
+    if (tid == 0 && m.token >= 0) {
+      d.expert = m.expert;
+      d.prec = m.prec;
+      d.gate = m.gate;
+    } else {
+      d.expert = -1;
+      d.prec = HB_SKIP;
+      d.gate = 0.f;
+    }
+    p.dec[j * p.k + tid] = d;
+  }
+  if (tid == 0) p.rowbad[j] = 0;
+  write_xperm(p, rows + (size_t)j * p.H, 0, p.H / 8, j);
+  for (int c = tid * 4; c < p.H; c += blockDim.x * 4)
+    *reinterpret_cast<float4*>(y + (size_t)j * p.H + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = tid; i < 4 * p.E; i += blockDim.x) sm.blob[i] = p.blob_table[i];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    sm.last = atomicAdd(p.done, 1u) == (unsigned)p.B - 1;
+  }
+  __syncthreads();
+  if (!sm.last) return;
+  __threadfence();
+  build_jobs_cta(p, sm, p.dec);
+  if (tid == 0) *p.done = 0u;
+}
+
+void launch_ts_pack(const TsParams& p, cudaStream_t s) {
+  if (p.B * p.k > 0) ts_pack_kernel<<<p.B * p.k, 128, 0, s>>>(p);
+}
+void launch_ts_combine(const TsParams& p, cudaStream_t s) {
+  if (p.B > 0) ts_combine_kernel<<<p.B, 256, 0, s>>>(p);
+}
+void launch_ts_jobs(const RouterParams& p, const hb_ts_meta* meta, const __half* rows, float* y,
+                    cudaStream_t s) {
+  ts_jobs_kernel<<<p.B, kRouterThreads, 0, s>>>(p, meta, rows, y);
+}
+
 }  // namespace hb
 
 #ifdef HB_DBG_TIMELINE

@@ -149,6 +149,28 @@ class Context:
         got = self._check(lib.hb_get_events(self._h, buf, cap))
         return [buf[i].as_tuple() for i in range(got)]
 
+    # ---- token-sharded EP, staged (hb_config.token_sharded)
+    def ts_buffers(self):
+        """Device buffers (meta, rows, ret) sized for one exchange direction."""
+        m, r, t = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        self._check(lib.hb_ts_buffer_bytes(self._h, C.byref(m), C.byref(r), C.byref(t)))
+        dev = torch.device("cuda", self.device)
+        return (torch.empty(m.value, dtype=torch.uint8, device=dev),
+                torch.empty(r.value // 2, dtype=torch.float16, device=dev),
+                torch.empty(t.value // 4, dtype=torch.float32, device=dev))
+
+    def ts_dispatch(self, layer: int, x: torch.Tensor, meta_send, rows_send, stream=None):
+        self._check(lib.hb_ts_dispatch(self._h, layer, _ptr(x), x.shape[0], _ptr(meta_send),
+                                       _ptr(rows_send), _stream(stream)))
+
+    def ts_compute(self, layer: int, meta_recv, rows_recv, ret_send, stream=None):
+        self._check(lib.hb_ts_compute(self._h, layer, _ptr(meta_recv), _ptr(rows_recv),
+                                      _ptr(ret_send), _stream(stream)))
+
+    def ts_combine(self, ret_recv, y: torch.Tensor, stream=None):
+        self._check(lib.hb_ts_combine(self._h, _ptr(ret_recv), y.shape[0], _ptr(y),
+                                      _stream(stream)))
+
     def copy_stats(self):
         """(foreground, background) bytes copied host -> HBM since creation."""
         out = (C.c_uint64 * 2)()

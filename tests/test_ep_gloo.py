@@ -121,3 +121,74 @@ def test_tp_slice_is_a_restriction():
     w2 = np.arange(4 * 8).reshape(4, 8).astype(float)
     a, b, c = om.tp_slice(w1, w3, w2, 1, 2)
     assert np.array_equal(a, w1[4:]) and np.array_equal(b, w3[4:]) and np.array_equal(c, w2[:, 4:])
+
+
+# ------------------------------------------------------- token-sharded EP (f3)
+TS_B = 5          # tokens per rank
+
+
+def _ts_worker(rank, world, port, out_dir):
+    """Each rank routes ITS tokens, sends every selection to the expert's owner
+    (all_to_all of fixed-capacity blocks), computes what it received, sends
+    the gate-weighted rows back and sums them per token."""
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        H, k = SH.hidden, SH.top_k
+        C = TS_B * k
+        x16 = sg.hidden_states(SH, 40 + rank, LAYER, batch=TS_B)
+        routes = rt.route(x16, sg.router_weights(SH, LAYER), k, 0.6, 0.9)
+        pos, sent = om.ts_dispatch_plan(routes, world, C)
+        rows = np.zeros((world, C, H), dtype=np.float64)
+        meta = np.full((world, C, 4), -1.0)
+        for q in range(world):
+            for j, (b, e, d, g) in enumerate(sent[q]):
+                rows[q, j] = x16[b].astype(np.float64)
+                meta[q, j] = (b, e, d, g)
+        rrows, rmeta = torch.empty(world * C * H, dtype=torch.float64), torch.empty(world * C * 4, dtype=torch.float64)
+        dist.all_to_all_single(rrows, torch.from_numpy(rows.ravel()))
+        dist.all_to_all_single(rmeta, torch.from_numpy(meta.ravel()))
+        rrows = rrows.numpy().reshape(world * C, H)
+        rmeta = rmeta.numpy().reshape(world * C, 4)
+        live = [j for j in range(world * C) if rmeta[j, 0] >= 0]
+        assert all(om.owner(int(rmeta[j, 1]), world) == rank for j in live)
+        recs = [(int(rmeta[j, 0]), int(rmeta[j, 1]), int(rmeta[j, 2]), rmeta[j, 3]) for j in live]
+        out = np.zeros((world * C, H))
+        out[live] = om.ts_owner_rows(rrows[live].astype(np.float16), recs, _store(), LAYER,
+                                     fm.F16, fm.Q4)
+        ret = torch.empty(world * C * H, dtype=torch.float64)
+        dist.all_to_all_single(ret, torch.from_numpy(out.ravel()))
+        y = om.ts_combine(pos, ret.numpy().reshape(world * C, H), H)
+        np.save(os.path.join(out_dir, f"y{rank}.npy"), y)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_token_sharded_gloo_equals_single_process(world):
+    """SURVEY 8(f) f3, token-sharded EP: dispatch -> owner compute -> combine
+    across two processes equals the single-process layer on each rank's tokens
+    (fp64, to rounding); the plan puts every selection at its owner."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_ts_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        ys = [np.load(os.path.join(d, f"y{r}.npy")) for r in range(world)]
+    for r in range(world):
+        x16 = sg.hidden_states(SH, 40 + r, LAYER, batch=TS_B)
+        ref, _ = om.moe_layer(x16, sg.router_weights(SH, LAYER), _store(), LAYER, SH.top_k,
+                              0.6, 0.9, fm.F16, fm.Q4)
+        np.testing.assert_allclose(ys[r], ref, rtol=1e-10, atol=1e-12)
+
+
+def test_ts_dispatch_plan_order_and_capacity():
+    """Slots per destination follow (token, rank) order; Skip sends nothing;
+    overflow raises."""
+    R = rt.Route
+    routes = [R(experts=[3, 0], gates=[0.7, 0.3], decisions=[rt.HIGH, rt.LOW], logits=None),
+              R(experts=[1, 2], gates=[0.9, 0.1], decisions=[rt.HIGH, rt.SKIP], logits=None),
+              R(experts=[2, 1], gates=[0.6, 0.4], decisions=[rt.HIGH, rt.HIGH], logits=None)]
+    pos, sent = om.ts_dispatch_plan(routes, 2, 4)
+    assert pos == [[4, 0], [5, -1], [1, 6]]
+    assert [s[:2] for s in sent[0]] == [(0, 0), (2, 2)]
+    assert [s[:2] for s in sent[1]] == [(0, 3), (1, 1), (2, 1)]
+    with pytest.raises(ValueError):
+        om.ts_dispatch_plan(routes, 1, 3)
