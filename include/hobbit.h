@@ -118,6 +118,11 @@ typedef struct {
                                        (hb_nccl_init) -- for world 1 without NCCL, locally; the
                                        staged calls hb_ts_dispatch / hb_ts_compute / hb_ts_combine
                                        leave the exchanges to the caller */
+  int prefetch_both;                /* offload mode: 0 (default) prefetch the predicted
+                                       precision; 1 prefetch both versions of each missing
+                                       predicted expert, Low first ("versions of the experts
+                                       with different precision levels", read as SPEC S:195;
+                                       DESIGN.md R30) */
 } hb_config;
 
 /* One routed (token, rank) pair of the last forward (inspection / parity). */

@@ -41,7 +41,7 @@ class CapacityError(RuntimeError):
 
 class ExpertCache:
     def __init__(self, n_layers, n_experts, cap_high, cap_low, weights,
-                 hi_enc, lo_enc, allow_upgrade=True, rank=0, world=1):
+                 hi_enc, lo_enc, allow_upgrade=True, rank=0, world=1, prefetch_both=False):
         self.L = n_layers
         self.E = n_experts
         self.pools = {POOL_HIGH: [None] * cap_high, POOL_LOW: [None] * cap_low}
@@ -54,6 +54,9 @@ class ExpertCache:
         self.n_evict = 0
         self.hi_enc, self.lo_enc = hi_enc, lo_enc
         self.allow_upgrade = allow_upgrade
+        # P:497 "we preload versions of the experts with different precision
+        # levels" read as SPEC S:195: both versions, Low first (R30)
+        self.prefetch_both = prefetch_both
         self.rank, self.world = rank, world
         self.R, self.F, self.H = {}, {}, {}
         self.T = 0
@@ -211,14 +214,20 @@ class ExpertCache:
             if not missing:
                 continue
             for e, d in missing:
-                pool = POOL_HIGH if d == HIGH else POOL_LOW
-                enc = self.hi_enc if d == HIGH else self.lo_enc
-                try:
-                    s, v = self._insert(pool, self.key(lp, e), layer, self.cur_keys)
-                except CapacityError:
-                    self.events.append((EV_DROP, K_PREFETCH, lp, e, enc, -1, -1))
-                    continue
-                self.events.append((EV_LOAD, K_PREFETCH, lp, e, enc, s, v))
+                if self.prefetch_both:
+                    # R30: the Low version, then the High one, each if its pool lacks the key
+                    todo = [p_ for p_ in (POOL_LOW, POOL_HIGH)
+                            if self.slot_of(p_, self.key(lp, e)) < 0]
+                else:
+                    todo = [POOL_HIGH if d == HIGH else POOL_LOW]
+                for pool in todo:
+                    enc = self.hi_enc if pool == POOL_HIGH else self.lo_enc
+                    try:
+                        s, v = self._insert(pool, self.key(lp, e), layer, self.cur_keys)
+                    except CapacityError:
+                        self.events.append((EV_DROP, K_PREFETCH, lp, e, enc, -1, -1))
+                        continue
+                    self.events.append((EV_LOAD, K_PREFETCH, lp, e, enc, s, v))
             return lp
         return -1
 

@@ -41,7 +41,8 @@ class hb_config(C.Structure):
                 ("w_lru", C.c_int), ("w_lfu", C.c_int), ("w_lhu", C.c_int), ("w_fld", C.c_int),
                 ("cap_high", C.c_int), ("cap_low", C.c_int), ("allow_upgrade", C.c_int),
                 ("rank", C.c_int), ("world", C.c_int), ("max_batch", C.c_int),
-                ("strict", C.c_int), ("device_cache", C.c_int), ("token_sharded", C.c_int)]
+                ("strict", C.c_int), ("device_cache", C.c_int), ("token_sharded", C.c_int),
+                ("prefetch_both", C.c_int)]
 
 
 class hb_decision(C.Structure):

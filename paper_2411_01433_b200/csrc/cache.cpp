@@ -10,9 +10,9 @@ namespace hb {
 
 ExpertCache::ExpertCache(int n_layers, int n_experts, int top_k, int cap_high, int cap_low,
                          const int w[4], int hi_enc, int lo_enc, bool allow_upgrade,
-                         int rank, int world)
+                         int rank, int world, bool prefetch_both)
     : L_(n_layers), E_(n_experts), K_(top_k), hi_enc_(hi_enc), lo_enc_(lo_enc),
-      upgrade_(allow_upgrade), rank_(rank), world_(world) {
+      upgrade_(allow_upgrade), both_(prefetch_both), rank_(rank), world_(world) {
   for (int i = 0; i < 4; ++i) w_[i] = w[i];
   random_ = w[0] + w[1] + w[2] + w[3] == 0;
   const int nkeys = L_ * E_;
@@ -203,14 +203,25 @@ int ExpertCache::prefetch(int layer, int n_pred, const int32_t* experts, const u
     if (!any_missing) continue;
     for (int i = 0; i < K_; ++i) {
       if (pr[i] == HB_SKIP || !owned(ex[i]) || present(lp, ex[i], pr[i])) continue;
-      const int pool = pr[i] == HB_HIGH ? POOL_HIGH : POOL_LOW;
-      const int enc = pr[i] == HB_HIGH ? hi_enc_ : lo_enc_;
-      const int s = insert(pool, key(lp, ex[i]), layer, true);
-      if (s < 0) {
-        events.push_back({EV_DROP, K_PREFETCH, lp, ex[i], enc, -1, -1});
-        continue;
+      // R30 (prefetch_both): the Low version, then the High one, each if its
+      // pool lacks the key; else the predicted precision only
+      int pools[2], np = 0;
+      if (both_) {
+        for (int pl : {POOL_LOW, POOL_HIGH})
+          if (slot_of(pl, key(lp, ex[i])) < 0) pools[np++] = pl;
+      } else {
+        pools[np++] = pr[i] == HB_HIGH ? POOL_HIGH : POOL_LOW;
       }
-      events.push_back({EV_LOAD, K_PREFETCH, lp, ex[i], enc, s, last_victim_});
+      for (int q = 0; q < np; ++q) {
+        const int pool = pools[q];
+        const int enc = pool == POOL_HIGH ? hi_enc_ : lo_enc_;
+        const int s = insert(pool, key(lp, ex[i]), layer, true);
+        if (s < 0) {
+          events.push_back({EV_DROP, K_PREFETCH, lp, ex[i], enc, -1, -1});
+          continue;
+        }
+        events.push_back({EV_LOAD, K_PREFETCH, lp, ex[i], enc, s, last_victim_});
+      }
     }
     *prefetched = lp;
     return HB_OK;
@@ -280,7 +291,7 @@ int hbc_create(const hb_config* cfg, hb_cache** out) {
   c->c = new (std::nothrow) hb::ExpertCache(cfg->n_layers, cfg->n_experts, cfg->top_k,
                                             cfg->cap_high, cfg->cap_low, w, cfg->hi_enc,
                                             cfg->lo_enc, cfg->allow_upgrade != 0, cfg->rank,
-                                            cfg->world);
+                                            cfg->world, cfg->prefetch_both != 0);
   if (!c->c) { delete c; return HB_ENOMEM; }
   c->top_k = cfg->top_k;
   c->n_layers = cfg->n_layers;

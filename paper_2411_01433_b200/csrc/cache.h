@@ -23,7 +23,7 @@ class ExpertCache {
  public:
   ExpertCache(int n_layers, int n_experts, int top_k, int cap_high, int cap_low,
               const int w[4], int hi_enc, int lo_enc, bool allow_upgrade, int rank,
-              int world);
+              int world, bool prefetch_both = false);
 
   void token_begin();
   void reset_sequence();
@@ -68,6 +68,7 @@ class ExpertCache {
   int w_[4];
   int hi_enc_, lo_enc_;
   bool upgrade_;
+  bool both_;                           // prefetch both versions, Low first (R30)
   int rank_, world_;
   int64_t T_ = 0;
   bool random_ = false;                            // all Eq. 3 weights 0: Random policy

@@ -301,16 +301,28 @@ struct Logic {
       for (int i = 0; i < K; ++i) {
         if (d[i].prec == HB_SKIP || !owned(d[i].expert) || present(lp, d[i].expert, d[i].prec))
           continue;
-        const int pool = d[i].prec == HB_HIGH ? 0 : 1;
-        const int enc = pool == 0 ? s.hi_enc : s.lo_enc;
-        int victim;
-        const int slot = insert(pool, key(lp, d[i].expert), layer, true, &victim);
-        if (slot < 0) {
-          log(2, 1, lp, d[i].expert, enc, -1, -1);
-          continue;
+        // R30 (both): the Low version, then the High one, each if its pool
+        // lacks the key; else the predicted precision only
+        int pools[2], np = 0;
+        const int kk = key(lp, d[i].expert);
+        if (s.both) {
+          if (s.where[1][kk] < 0) pools[np++] = 1;
+          if (s.where[0][kk] < 0) pools[np++] = 0;
+        } else {
+          pools[np++] = d[i].prec == HB_HIGH ? 0 : 1;
         }
-        log(1, 1, lp, d[i].expert, enc, slot, victim);
-        new_task(pool, slot, lp, d[i].expert, enc, 0);
+        for (int q = 0; q < np; ++q) {
+          const int pool = pools[q];
+          const int enc = pool == 0 ? s.hi_enc : s.lo_enc;
+          int victim;
+          const int slot = insert(pool, kk, layer, true, &victim);
+          if (slot < 0) {
+            log(2, 1, lp, d[i].expert, enc, -1, -1);
+            continue;
+          }
+          log(1, 1, lp, d[i].expert, enc, slot, victim);
+          new_task(pool, slot, lp, d[i].expert, enc, 0);
+        }
       }
       return;
     }

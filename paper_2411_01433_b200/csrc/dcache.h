@@ -25,6 +25,7 @@ struct DcTask {
 // Cache state in HBM (arrays allocated by the context; the struct itself too).
 struct DcState {
   int L, E, K, cap[2], w[4], hi_enc, lo_enc, upgrade, rank, world, random;
+  int both;                     // prefetch both versions, Low first (R30)
   long long T;
   unsigned long long n_evict;
   int* pool[2];                 // slot -> key or -1

@@ -66,11 +66,11 @@ def test_theta_matches_oracle():
         assert theta(t) == rt.theta(t) or (t <= 0 and theta(t) < -(1 << 100)), t
 
 
-def _cfg(L_, E, k, ch, cl, w, upgrade=1, rank=0, world=1, p=2):
+def _cfg(L_, E, k, ch, cl, w, upgrade=1, rank=0, world=1, p=2, both=0):
     return default_config(n_layers=L_, n_experts=E, top_k=k, hidden=256, ffn=512,
                           hi_enc=fm.F16, lo_enc=fm.Q4, w_lru=w[0], w_lfu=w[1], w_lhu=w[2],
                           w_fld=w[3], cap_high=ch, cap_low=cl, allow_upgrade=upgrade,
-                          rank=rank, world=world, lookahead_p=p)
+                          rank=rank, world=world, lookahead_p=p, prefetch_both=both)
 
 
 def _rand_route(rnd, E, k):
@@ -79,11 +79,13 @@ def _rand_route(rnd, E, k):
     return ex, dec
 
 
-@pytest.mark.parametrize("trial", range(12))
+@pytest.mark.parametrize("trial", range(16))
 def test_host_cache_matches_oracle_bit_exact(trial):
     """hbc_* (the library's cache) vs oracle O9/O10 on random traces, with
-    prefetch walks, explicit loads, sequence resets and EP ranks."""
+    prefetch walks (predicted precision, or both versions Low first: R30),
+    explicit loads, sequence resets and EP ranks."""
     rnd = random.Random(100 + trial)
+    both = int(trial >= 12)
     L_, E, k = rnd.choice([(4, 8, 2), (6, 8, 2), (5, 16, 2), (4, 8, 3)])
     world = rnd.choice([1, 1, 2])
     rank = rnd.randrange(world)
@@ -93,9 +95,11 @@ def test_host_cache_matches_oracle_bit_exact(trial):
         w = (0, 0, 0, 0)                              # Random policy (R29)
     upgrade = rnd.choice([0, 1])
     ch, cl = rnd.randint(2 * k + 2, 10), rnd.randint(2 * k + 2, 10)
+    if both:                                          # masks now reach both pools
+        ch, cl = ch + 2 * k, cl + 2 * k
     ref = oc.ExpertCache(L_, E, ch, cl, w, fm.F16, fm.Q4, allow_upgrade=bool(upgrade),
-                         rank=rank, world=world)
-    hc = HostCache(_cfg(L_, E, k, ch, cl, w, upgrade, rank, world, p))
+                         rank=rank, world=world, prefetch_both=bool(both))
+    hc = HostCache(_cfg(L_, E, k, ch, cl, w, upgrade, rank, world, p, both))
     for _ in range(3):
         e = rnd.randrange(E)
         if e % world == rank:

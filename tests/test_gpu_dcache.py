@@ -163,3 +163,44 @@ def test_dcache_offload_token_graph_captured(p):
             ref.prefetch(l, _predict(sh, x16, l, p))
     assert max(results) <= TOL
     assert ctx.events() == ref.events
+
+
+@pytest.mark.parametrize("dc", [0, 1])
+def test_offload_prefetch_both_versions(dc):
+    """R30 (prefetch_both): both versions of each missing predicted expert,
+    Low first, on the host manager (dc=0) and the device manager (dc=1):
+    events bit-exact with the oracle, outputs equal."""
+    sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
+    p, ch, cl = 2, 9, 9
+    ctx = _ctx(sh, fm.F16, fm.Q4, max_batch=1, cap_high=ch, cap_low=cl, lookahead_p=p,
+               device_cache=dc, prefetch_both=1)
+    for l in range(sh.n_layers):
+        ctx.set_router(l, sg.router_weights(sh, l))
+        for (e, enc), b in gpu_blobs(sh, l, range(sh.n_experts), [fm.F16, fm.Q4]).items():
+            ctx.register_expert(l, e, enc, b.cpu().numpy())
+    store = OracleStore(sh)
+    ref = oc.ExpertCache(sh.n_layers, sh.n_experts, ch, cl, (1, 1, 1, 1), fm.F16, fm.Q4,
+                         prefetch_both=True)
+    xs = sg.correlated_states(sh, 8, 0.999, 0.5)
+    outs = []
+    for t in range(8):
+        ctx.token_begin()
+        ref.token_begin()
+        for l in range(sh.n_layers):
+            x16 = xs[t, l][None, :]
+            x = torch.from_numpy(x16).cuda()
+            y = torch.empty(1, sh.hidden, dtype=torch.float32, device="cuda")
+            ctx.forward(l, x, y)
+            served = ref.forward(l, rt.route(x16, sg.router_weights(sh, l), 2, 0.6, 0.9)[0])
+            outs.append((y, x16, l, served))
+            ctx.prefetch(l, x)
+            ref.prefetch(l, _predict(sh, x16, l, p))
+    torch.cuda.synchronize()
+    ev = ctx.events()
+    assert ev == ref.events
+    pf = [e for e in ev if e[1] == 1 and e[0] == 1]
+    assert any(a[2:4] == b[2:4] and a[4] == fm.Q4 and b[4] == fm.F16 for a, b in zip(pf, pf[1:]))
+    for y, x16, l, served in outs:
+        r, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9, fm.F16, fm.Q4,
+                            served=[served])
+        assert rel_err(y.cpu().numpy()[0], r[0])[0] <= TOL

@@ -356,3 +356,29 @@ def test_random_policy_uniform_and_record_free():
         a.load(0, e, 0)
         b.load(0, e, 0)
     assert a.pools == b.pools
+
+
+def test_prefetch_both_versions_low_first():
+    """R30 ("versions ... with different precision levels"):
+    prefetch_both loads the Low version of each missing predicted expert, then
+    the High one, each only where its pool lacks the key; the walk itself
+    (which layer has a miss) is unchanged."""
+    c = oc.ExpertCache(8, 8, 8, 8, (1, 1, 1, 1), HI, LO, prefetch_both=True)
+    c.token_begin()
+    c.forward(0, _route([0, 1], [HIGH, LOW]))
+    c.load(1, 3, LO)                                   # expert 3 of layer 1: Low present
+    n = len(c.events)
+    assert c.prefetch(0, {1: _route([2, 3], [HIGH, HIGH])}) == 1
+    new = [(e[0], e[1], e[2], e[3], e[4]) for e in c.events[n:]]
+    assert new == [(oc.EV_LOAD, oc.K_PREFETCH, 1, 2, LO), (oc.EV_LOAD, oc.K_PREFETCH, 1, 2, HI),
+                   (oc.EV_LOAD, oc.K_PREFETCH, 1, 3, HI)]
+    # a predicted-Low miss also brings both versions
+    n = len(c.events)
+    assert c.prefetch(1, {2: _route([4, 5], [LOW, SKIP])}) == 2
+    assert [(e[3], e[4]) for e in c.events[n:]] == [(4, LO), (4, HI)]
+    # without the option: the predicted precision only
+    d = oc.ExpertCache(8, 8, 8, 8, (1, 1, 1, 1), HI, LO)
+    d.token_begin()
+    d.forward(0, _route([0, 1], [HIGH, LOW]))
+    d.prefetch(0, {1: _route([2, 3], [HIGH, LOW])})
+    assert [(e[3], e[4]) for e in d.events if e[1] == oc.K_PREFETCH] == [(2, HI), (3, LO)]

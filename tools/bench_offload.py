@@ -59,6 +59,8 @@ def main():
     ap.add_argument("--graph", action="store_true",
                     help="device_cache=1 runs: capture one token in a CUDA graph and replay it")
     ap.add_argument("--no-off", action="store_true", help="skip the T1=T2=1 (dynamic loading off) run")
+    ap.add_argument("--prefetch-both", default="0",
+                    help="comma list of hb_config.prefetch_both values (1: both versions, Low first, R30)")
     ap.add_argument("--env", default="",
                     help="'|'-separated library env settings 'K=V,K=V' to run each config under "
                          "(read at hb_create), e.g. HB_DC_FG_CTAS=16|HB_DC_FG_CTAS=64")
@@ -101,9 +103,10 @@ def main():
         runs += [(1, 1.0, 1.0, (1, 1, 1, 1))]
     runs += [(1, 0.6, 0.9, tuple(int(v) for v in w.split(":"))) for w in args.policies.split(",") if w]
     runs = [r + (int(dc),) for dc in args.device_cache.split(",") for r in runs]
+    runs = [r + (int(pb),) for pb in args.prefetch_both.split(",") for r in runs]
     envs = args.env.split("|") if args.env else [""]
     runs = [r + (e,) for e in envs for r in runs]
-    for p, t1, t2, w, dc, env in runs:
+    for p, t1, t2, w, dc, pboth, env in runs:
         for kv in env.split(","):
             if kv:
                 k_, v_ = kv.split("=")
@@ -111,7 +114,7 @@ def main():
         cfg = h.default_config(n_layers=L, n_experts=E, top_k=2, hidden=H, ffn=F, hi_enc=hi,
                                lo_enc=lo, t1=t1, t2=t2, max_batch=1, cap_high=cap_h,
                                cap_low=cap_l, lookahead_p=p, w_lru=w[0], w_lfu=w[1], w_lhu=w[2],
-                               w_fld=w[3], device_cache=dc)
+                               w_fld=w[3], device_cache=dc, prefetch_both=pboth)
         ctx = h.Context(cfg)
         for l in range(L):
             ctx.set_router(l, sg.router_weights(shape, l))
@@ -173,6 +176,7 @@ def main():
                "loads_per_token": round(len(loads) / n, 2), "prefetch_loads": n_pref,
                "hit_ratio": round(len(hits) / max(1, len(hits) + len(loads) - n_pref), 4),
                "device_cache": dc, "graph": bool(graph is not None), "env": env,
+               "prefetch_both": pboth,
                "copied_fg_bytes_per_token": int((c1[0] - c0[0]) / n),
                "copied_bg_bytes_per_token": int((c1[1] - c0[1]) / n),
                "copied_gbs": round((c1[0] + c1[1] - c0[0] - c0[1]) / (ms * 1e-3) / 1e9, 2),
