@@ -227,8 +227,10 @@ int hb_reset_sequence(hb_ctx* ctx);
  * insert of (layer, expert) into the high pool if enc == hi_enc, the low
  * pool if enc == lo_enc (evicting by Eq. 3 if full, no record update), and
  * an async host->device copy on the library's copy stream, ordered after
- * every earlier reader of the reused slot.  No-op if already resident.
- * Offload mode only (HB_ESTATE in resident mode). */
+ * the work already queued on `stream` and after every earlier reader of the
+ * reused slot (device_cache: the load is a background task forked from
+ * `stream`).  No-op if already resident.  Offload mode only (HB_ESTATE in
+ * resident mode). */
 int expert_cache_load(hb_ctx* ctx, int layer, int expert, int enc, void* stream);
 
 /* Stacked next-layer prediction + prefetch (Sec. 3.3): runs the

@@ -1487,7 +1487,6 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
 }
 
 int expert_cache_load(hb_ctx* c, int layer, int expert, int enc, void* stream) {
-  (void)stream;
   if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
   if (c->resident) return fail(c, HB_ESTATE, "expert_cache_load needs a constrained cache");
   const hb_config& k = c->cfg;
@@ -1507,6 +1506,10 @@ int expert_cache_load(hb_ctx* c, int layer, int expert, int enc, void* stream) {
   int rc = c->cache->load(layer, expert, enc, &queued);
   if (rc) return fail(c, rc, c->cache->err);
   CUDA_TRY(c, cudaSetDevice(c->device));
+  if (queued) {                    // the copy starts after the caller's work queued on `stream`
+    CUDA_TRY(c, cudaEventRecord(c->dec_ready, (cudaStream_t)stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dec_ready, 0));
+  }
   rc = issue_loads(c, ev0);
   drain_events(c);
   if (!rc) rc = pf_top_up(c);
