@@ -123,6 +123,11 @@ typedef struct {
                                        predicted expert, Low first ("versions of the experts
                                        with different precision levels", read as SPEC S:195;
                                        DESIGN.md R30) */
+  int deterministic;                /* 1: bit-reproducible y for top_k <= 2 (debugging): the
+                                       GEMV kernels deal whole row tiles statically (no dynamic
+                                       chunks), so every a/u element and every (expert, y row)
+                                       term is one fp32 reduction; h is read from global memory;
+                                       the batched GEMM does not split K.  Slower (R24) */
 } hb_config;
 
 /* One routed (token, rank) pair of the last forward (inspection / parity). */

@@ -42,7 +42,7 @@ class hb_config(C.Structure):
                 ("cap_high", C.c_int), ("cap_low", C.c_int), ("allow_upgrade", C.c_int),
                 ("rank", C.c_int), ("world", C.c_int), ("max_batch", C.c_int),
                 ("strict", C.c_int), ("device_cache", C.c_int), ("token_sharded", C.c_int),
-                ("prefetch_both", C.c_int)]
+                ("prefetch_both", C.c_int), ("deterministic", C.c_int)]
 
 
 class hb_decision(C.Structure):

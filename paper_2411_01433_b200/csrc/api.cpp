@@ -462,7 +462,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
           (resident && !dm((void**)&c->k3_tmap, sizeof(CUtensorMap) * (size_t)L * E * 24)))
         return bail(HB_ENOMEM, "K3 scratch allocation failed");
       c->k3_ok = true;
-      c->k3_ks = (F / 2) % 256 == 0 ? 2 : 1;
+      c->k3_ks = (F / 2) % 256 == 0 && !k.deterministic ? 2 : 1;   // deterministic: no K split
       cudaMemset(c->k3_tab, 0, sizeof(K3Table));
     }
     const char* km = std::getenv("HB_K3_MIN_BATCH");
@@ -549,7 +549,8 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
       return bail(HB_ECUDA, "copy stream creation failed");
     const int w[4] = {k.w_lru, k.w_lfu, k.w_lhu, k.w_fld};
     c->cache = new (std::nothrow) ExpertCache(L, E, K, k.cap_high, k.cap_low, w, k.hi_enc,
-                                              k.lo_enc, k.allow_upgrade != 0, k.rank, k.world);
+                                              k.lo_enc, k.allow_upgrade != 0, k.rank, k.world,
+                                              k.prefetch_both != 0);
     if (!c->cache) return bail(HB_ENOMEM, "cache allocation failed");
     if (k.device_cache) {
       if (int rc = dc_create(c)) return bail(rc, c->err);
@@ -819,6 +820,11 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y, float* au) {
   g.max_vjobs = c->max_vjobs;
   g.static_frac = c->static_frac;
   g.static_frac2 = c->static_frac2;
+  if (k.deterministic) {                     // whole tiles per warp, no column slices of h
+    g.det = 1;
+    g.h_global = 1;
+    g.static_frac = g.static_frac2 = 1.f;
+  }
   g.chunk = c->chunk;
   for (int e = 0; e < 4; ++e) g.k2b_w[e] = c->k2b_w[e];
   g.stamps = c->stamps_on ? c->stamps : nullptr;
@@ -1176,6 +1182,7 @@ static int dc_create(hb_ctx* c) {
   h.hi_enc = k.hi_enc;
   h.lo_enc = k.lo_enc;
   h.upgrade = k.allow_upgrade != 0;
+  h.both = k.prefetch_both != 0;
   h.rank = k.rank;
   h.world = k.world;
   h.log_cap = 1 << 16;

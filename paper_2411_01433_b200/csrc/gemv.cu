@@ -1071,6 +1071,19 @@ __device__ HB_PHASE_ATTR void phase_run(const GemvParams& p, const int* s_cum, c
   const int gwl = warp * pc.ncta + pc.cta;
   fd.a = pc.base + ((int)((long long)s_fk->S * gwl / s_fk->nwarps) & ~(pc.KNU - 1));
   fd.b = pc.base + ((int)((long long)s_fk->S * (gwl + 1) / s_fk->nwarps) & ~(pc.KNU - 1));
+  if (p.det && !pc.part) {
+    // deterministic mode: every warp gets whole row tiles (every vjob has the
+    // same number of tiles), so each output row of a vjob is one reduction
+    const int nvj = JT<FUSED>::nv(p);
+    const int tpv = (W13 ? p.F : p.H) / 16, T = nvj * tpv;
+    auto unit_of = [&](int tau) -> int {
+      if (tau >= T) return s_cum[nvj];
+      const int v = tau / tpv;
+      return s_cum[v] + (tau - v * tpv) * ((s_cum[v + 1] - s_cum[v]) / tpv);
+    };
+    fd.a = pc.base + unit_of((int)((long long)T * gwl / s_fk->nwarps));
+    fd.b = pc.base + unit_of((int)((long long)T * (gwl + 1) / s_fk->nwarps));
+  }
   fd.start();
   const uint32_t ring = smem_u32(gemv_smem) + warp * KCfg<W13>::RING;
   bool first = true;

@@ -163,6 +163,7 @@ struct GemvParams {
   float* y;                            // [B][H] (zeroed by router)
   const int* rowbad;                   // [B] router's non-finite x flags: NaN rows (R28)
   int hfin_tail;                       // K2a ends with a grid barrier + h (no hfin kernel)
+  int det;                             // hb_config.deterministic: whole row tiles dealt statically
   int ctas;                            // K2a / K2b grid (<= kGemvCTAs)
   int clean;                           // hfin zeroes the K2a sums it read and the y rows (the
                                        // solo router zeroes nothing)

@@ -436,3 +436,23 @@ def test_tp_within_expert_two_processes_through_library(tmp_path):
             bar = 1e-4 if B < 4 else 1e-3
             for b in range(B):
                 assert rel_err(y[b], ref[b])[0] <= bar
+
+
+# ------------------------------------------------------------ deterministic mode
+@pytest.mark.parametrize("B,bm,shape", [(1, 0, "mixtral"), (5, 0, "tiny"), (40, 4, "tiny")],
+                         ids=["B1-K2-mixtral", "B5-K2", "B40-K3"])
+def test_deterministic_mode_bit_reproducible(B, bm, shape):
+    """hb_config.deterministic (R24): whole row
+    tiles per warp, no dynamic chunks, no K split -- repeated forwards give
+    bit-identical y, and y still matches the oracle."""
+    sh = sg.TINY if shape == "tiny" else sg.MoEShape("mx1", 1, 8, 2, 4096, 14336, 1.5)
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=B, batched_min=bm, deterministic=1)
+    x16 = sg.hidden_states(sh, 90 + B, 0, batch=B)
+    outs = [_run(ctx, 0, x16) for _ in range(4)]
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+    store = OracleStore(sh)
+    ref, _ = om.moe_layer(x16, sg.router_weights(sh, 0), store, 0, 2, 0.6, 0.9, fm.F16, fm.Q4)
+    tol = 1e-3 if bm else 1e-4
+    for b in range(B):
+        assert rel_err(outs[0][b], ref[b])[0] <= tol
