@@ -56,20 +56,56 @@ run(ctx, 3)
 ctx.set_batched_min(4)
 run(ctx, 16)                                   # K3
 ctx.close()
-# offload: loads, evictions, prefetch
+# deterministic mode (GEMV and K3)
 cfg = h.default_config(n_layers=4, n_experts=8, top_k=2, hidden=256, ffn=512, hi_enc=F16,
-                       lo_enc=Q4, max_batch=1, cap_high=6, cap_low=6, lookahead_p=1)
+                       lo_enc=Q4, max_batch=16, deterministic=1)
 ctx = h.Context(cfg)
-for l in range(4):
+keep = []
+for l in range(2):
     ctx.set_router(l, sg.router_weights(sh, l))
     for (e, enc), b in gpu_blobs(sh, l, range(8), [F16, Q4]).items():
-        ctx.register_expert(l, e, enc, b.cpu().numpy())
-for t in range(3):
-    ctx.token_begin()
+        ctx.register_expert(l, e, enc, b)
+        keep.append(b)
+ctx.set_batched_min(0)
+run(ctx, 3)
+ctx.set_batched_min(4)
+run(ctx, 16)
+ctx.close()
+# token-sharded EP, world 1 (pack, owner batch, combine), K2 and K3
+for B, bm in ((2, 0), (12, 4)):
+    cfg = h.default_config(n_layers=4, n_experts=8, top_k=2, hidden=256, ffn=512, hi_enc=F16,
+                           lo_enc=Q4, max_batch=B, token_sharded=1)
+    ctx = h.Context(cfg)
+    keep = []
+    for l in range(2):
+        ctx.set_router(l, sg.router_weights(sh, l))
+        for (e, enc), b in gpu_blobs(sh, l, range(8), [F16, Q4]).items():
+            ctx.register_expert(l, e, enc, b)
+            keep.append(b)
+    ctx.set_batched_min(bm)
+    run(ctx, B)
+    ctx.close()
+# offload: loads, evictions, prefetch -- host manager, device manager (SM
+# copies, small chunks), both-versions prefetch
+for dc, both in ((0, 0), (1, 0), (1, 1)):
+    if dc:
+        os.environ["HB_DC_CHUNK_KB"] = "16"
+    cfg = h.default_config(n_layers=4, n_experts=8, top_k=2, hidden=256, ffn=512, hi_enc=F16,
+                           lo_enc=Q4, max_batch=1, cap_high=8, cap_low=8, lookahead_p=1,
+                           device_cache=dc, prefetch_both=both)
+    ctx = h.Context(cfg)
     for l in range(4):
-        x = torch.from_numpy(sg.hidden_states(sh, 70 + t, l)).cuda()
-        y = torch.empty(1, 256, dtype=torch.float32, device="cuda")
-        ctx.forward(l, x, y)
-        ctx.prefetch(l, x)
-torch.cuda.synchronize()
+        ctx.set_router(l, sg.router_weights(sh, l))
+        for (e, enc), b in gpu_blobs(sh, l, range(8), [F16, Q4]).items():
+            ctx.register_expert(l, e, enc, b.cpu().numpy())
+    for t in range(3):
+        ctx.token_begin()
+        for l in range(4):
+            x = torch.from_numpy(sg.hidden_states(sh, 70 + t, l)).cuda()
+            y = torch.empty(1, 256, dtype=torch.float32, device="cuda")
+            ctx.forward(l, x, y)
+            ctx.prefetch(l, x)
+    torch.cuda.synchronize()
+    ctx.events()
+    ctx.close()
 print("sanitize_run done")
