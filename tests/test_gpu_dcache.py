@@ -204,3 +204,28 @@ def test_offload_prefetch_both_versions(dc):
         r, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9, fm.F16, fm.Q4,
                             served=[served])
         assert rel_err(y.cpu().numpy()[0], r[0])[0] <= TOL
+
+
+@pytest.mark.parametrize("dc", [0, 1])
+def test_offload_capacity_error_is_loud(dc):
+    """A pool of one High slot and a token selecting two High experts: the
+    second insert has no eligible victim (the first is in use).  The host
+    manager fails that forward; the device manager records a sticky
+    HB_ECAPACITY that the next call reports (it cannot return it from an
+    asynchronous forward)."""
+    from paper_2411_01433_b200 import hobbit as H
+    sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
+    ctx = _ctx(sh, fm.F16, fm.Q4, max_batch=1, cap_high=1, cap_low=4, lookahead_p=0,
+               device_cache=dc, t1=1.0, t2=1.0)             # every selection High
+    for l in range(sh.n_layers):
+        ctx.set_router(l, sg.router_weights(sh, l))
+        for (e, enc), b in gpu_blobs(sh, l, range(sh.n_experts), [fm.F16, fm.Q4]).items():
+            ctx.register_expert(l, e, enc, b.cpu().numpy())
+    ctx.token_begin()
+    x = torch.from_numpy(sg.hidden_states(sh, 5, 0)).cuda()
+    y = torch.empty(1, sh.hidden, dtype=torch.float32, device="cuda")
+    with pytest.raises(H.HobbitError) as ei:
+        ctx.forward(0, x, y)
+        torch.cuda.synchronize()
+        ctx.events()                                   # device manager: reported here
+    assert "HB_ECAPACITY" in str(ei.value)

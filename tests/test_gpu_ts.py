@@ -126,3 +126,30 @@ def test_ts_two_processes_staged(world, tmp_path):
                     got = [(int(m[0]), int(m[1]), int(m[2] & 0xff)) for m in meta[q] if m[0] >= 0]
                     assert got == [(b, e, d) for b, e, d, _ in sent[q]], (B, l, r, q)
                     assert all(m[0] == -1 for m in meta[q][len(sent[q]):])
+
+
+def test_ts_nonfinite_row_and_all_skip_second_selection():
+    """R28 on the token-sharded path: a token whose x has an inf gets a NaN
+    row (nothing dispatched for it), the others equal the oracle; and with
+    T1 = T2 = 0 every second selection is Skip -- one row per token
+    travels."""
+    sh = sg.TINY
+    B = 6
+    ctx = _resident(sh, [0], fm.F16, fm.Q4, max_batch=B, batched_min=4, token_sharded=1)
+    x16 = sg.hidden_states(sh, 77, 0, batch=B)
+    x16[2, 5] = np.float16(np.inf)
+    y = _run(ctx, 0, x16)
+    assert np.isnan(y[2]).all()
+    store = OracleStore(sh)
+    ok = [b for b in range(B) if b != 2]
+    ref, _ = om.moe_layer(x16[ok], sg.router_weights(sh, 0), store, 0, 2, 0.6, 0.9, fm.F16, fm.Q4)
+    for i, b in enumerate(ok):
+        assert rel_err(y[b], ref[i])[0] <= TOL
+    ctx2 = _resident(sh, [0], fm.F16, fm.Q4, max_batch=B, batched_min=0, token_sharded=1,
+                     t1=0.0, t2=0.0)
+    x16 = sg.hidden_states(sh, 78, 0, batch=B)
+    y = _run(ctx2, 0, x16)
+    ref, routes = om.moe_layer(x16, sg.router_weights(sh, 0), store, 0, 2, 0.0, 0.0, fm.F16, fm.Q4)
+    assert all(r.decisions[1] == rt.SKIP for r in routes)
+    for b in range(B):
+        assert rel_err(y[b], ref[b])[0] <= TOL
