@@ -169,6 +169,7 @@ struct hb_ctx {
   int k3_min_batch = 4;                   // HB_K3_MIN_BATCH / hb_set_batched_min (K3 wins from B = 4, profiles/r01_batched.md)
   bool k3_ok = false;
   int k3_ks = 1;
+  int k3_ts = 1;                          // quantised K3 items: A dequantised into TMEM (HB_K3_TS=0: smem)
   __half* k3_xg = nullptr;
   __half* k3_hB = nullptr;
   K3Table* k3_tab = nullptr;
@@ -465,6 +466,8 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
       c->k3_ks = (F / 2) % 256 == 0 && !k.deterministic ? 2 : 1;   // deterministic: no K split
       cudaMemset(c->k3_tab, 0, sizeof(K3Table));
     }
+    const char* kt = std::getenv("HB_K3_TS");
+    if (kt) c->k3_ts = kt[0] == '1';
     const char* km = std::getenv("HB_K3_MIN_BATCH");
     if (km) c->k3_min_batch = std::atoi(km);
   }
@@ -947,6 +950,7 @@ static void launch_batched(hb_ctx* c, int layer, const void* x, void* y, cudaStr
   kp.tmap = c->k3_tmap + (size_t)layer * c->cfg.n_experts * 24;
   kp.has_f16 = c->cfg.hi_enc == HB_F16 || c->cfg.lo_enc == HB_F16;
   kp.has_q = c->cfg.hi_enc != HB_F16 || c->cfg.lo_enc != HB_F16;
+  kp.ts = c->k3_ts;
   cudaEvent_t* ev = nullptr;
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
   launch_k3_prep(kp, (const __half*)x, s);

@@ -44,7 +44,7 @@ constexpr int kRows = 128;                 // weight rows per tile = MMA M
 constexpr int kBK = 64;                    // K elements per canonical stage
 constexpr int kRawSlots = 4;
 constexpr int kCanSlots = 3;
-constexpr int kMaxBSlots = 8;
+constexpr int kMaxBSlots = 12;
 constexpr int kConvWarps = 16;             // warps 0..15 dequantise (all on one step)
 constexpr int kConvThreads = kConvWarps * 32;
 constexpr int kEpiWarp0 = kConvWarps;      // 4 epilogue warps (warp % 4 = TMEM lane quarter)
@@ -61,6 +61,16 @@ constexpr int kBBytes = kK3MaxN * kBK * 2; // 16 KB: largest B tile (np = 128)
 constexpr int kBRing = 32768;
 constexpr int kBarOff = kRawSlots * kRawBytes + kCanSlots * kABytes + kBRing;
 constexpr int kSmem = kBarOff + 512 + 1024;   // + alignment slack (swizzle atoms: 1 KB)
+// TS variant (K3Params::ts): no fp16 A stages in shared memory -- the
+// converters dequantise into TMEM (columns 256..511: 4 two-matrix or 8
+// one-matrix stages of 64 K) and the MMA reads A from there, so the raw ring
+// gets the shared memory the A stages held
+// (measured: 5/6/7 raw slots, 32-80 KB of B tiles, 4-6 A stages and one or
+// two accumulator buffers all within 1 %; the A stage in TMEM is the gain)
+constexpr int kRawSlotsTS = 7;
+constexpr int kBRingTS = 56 * 1024;            // B tiles in flight (np = 64: 7 slots)
+constexpr int kBarOffTS = kRawSlotsTS * kRawBytes + kBRingTS;
+constexpr int kSmemTS = kBarOffTS + 1024 + 1024;   // barriers: up to 66 x 8 B
 
 #ifdef HB_K3_TRACE
 // diagnostic timeline (tools/k3_trace.py): CTA 0 stamps %globaltimer per event
@@ -151,6 +161,18 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t ad, uint64_t bd, 
       "{ .reg .pred p; setp.ne.b32 p, %4, 0; "
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
       :: "r"(tmem_d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+}
+// A from TMEM (K-major: lane = row, column c holds K elements 2c, 2c + 1)
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bd, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; "
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }"
+      :: "r"(tmem_d), "r"(tmem_a), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint4 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+               :: "r"(taddr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -346,14 +368,14 @@ __device__ __forceinline__ Item item_of(const K3Params& p, int it, int v0) {
 // K3b: y[token] += g * o (Eq. 1) with fp32 reductions.
 template <int NMAT>
 __device__ __forceinline__ void epilogue_item(const K3Params& p, const Item& I, uint32_t tacc,
-                                              int q4, int lane) {
+                                              int q4, int lane, int ms = 128) {
   const int np = I.v->np, n_real = I.v->n;
   const int row = I.tile * kRows + q4 * 32 + lane;   // weight row of this thread
   for (int n0 = 0; n0 < np; n0 += 16) {
     if (NMAT == 2) {
       float a[16], uu[16];
       tmem_ld16(tacc + n0, a);
-      tmem_ld16(tacc + 128 + n0, uu);
+      tmem_ld16(tacc + ms + n0, uu);
       // h (fp16) into hB in K3b's canonical B layout: K index = row (of F)
       __half* hb = p.hB + I.v->hoff + (size_t)(row >> 6) * np * kBK +
                    ((row & 63) >> 3) * 64 + (row & 7);
@@ -383,16 +405,22 @@ __device__ __forceinline__ void epilogue_item(const K3Params& p, const Item& I, 
 
 // Quantised items (Q8/Q4/Q2): persistent tcgen05 GEMM.  NMAT = 2: K3a (W1, W3
 // over K = H; SwiGLU epilogue); NMAT = 1: K3b (W2 over K = F / ks; Eq. 1).
-// Rings: raw codes + scales (bulk copies, 4 x 24 KB) -> 16 converter warps ->
-// fp16 A tiles (2 x 32 KB); B tiles (X or h, np x 64) in their own ring of up
-// to 8 stages fed by a second producer, so their L2 latency is hidden.
-template <int NMAT>
+// Rings: raw codes + scales (bulk copies) -> 16 converter warps -> fp16 A
+// stages; B tiles (X or h, np x 64) in their own ring fed by a second
+// producer, so their L2 latency is hidden.  TS = true (default, K3Params::ts):
+// the converters write A into TMEM with tcgen05.st (warp w: lanes 32 (w % 4)..,
+// K chunks w / 4) and the MMA reads A from TMEM (kind::f16, A-from-TMEM form),
+// so no fp16 A tile goes through shared memory and the raw ring gets 7 x 24 KB
+// (K3a Q4 at B = 256: 338 -> 308 us; profiles/r02_k3_ts.md).  TS = false: A
+// stages in shared memory (4 raw slots, 3 x 32 KB SW64 A stages).
+template <int NMAT, bool TS>
 __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t sbase = (su32(sm) + 1023) & ~1023u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t bars = sbase + kBarOff;
-  constexpr int R = kRawSlots, CS = kCanSlots, BS = kMaxBSlots;
+  const uint32_t bars = sbase + (TS ? kBarOffTS : kBarOff);
+  constexpr int R = TS ? kRawSlotsTS : kRawSlots, BS = kMaxBSlots;
+  constexpr int CS = TS ? 12 : kCanSlots;        // barriers for up to CS A stages
   auto raw_full = [&](int i) { return bars + 8 * i; };
   auto raw_empty = [&](int i) { return bars + 8 * (R + i); };
   auto can_full = [&](int i) { return bars + 8 * (2 * R + i); };
@@ -443,8 +471,17 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
   int npmax = 16;
   for (int v = v0; v < p.tab->n; ++v) npmax = max(npmax, p.tab->v[v].np);
   const int bslot = npmax * kBK * 2;
-  const int nb = min(BS, kBRing / bslot);
-  const uint32_t bring = sbase + kRawSlots * kRawBytes + kCanSlots * kABytes;
+  const int nb = min(BS, (TS ? kBRingTS : kBRing) / bslot);
+  const uint32_t bring = sbase + R * kRawBytes + (TS ? 0 : kCanSlots * kABytes);
+  // TMEM accumulators: TS keeps columns 0..255 for them (per matrix MS columns,
+  // two buffers when they fit, else one); the smem variant uses 2 x 256
+  // TS: accumulators first (MS columns per matrix, two buffers when they fit
+  // in 256 columns), the A stages of NMAT x 32 columns after them
+  const int MS = TS ? (npmax <= 64 ? 64 : 128) : 128;
+  const int nbuf = TS ? (NMAT * MS * 2 > 256 ? 1 : 2) : 2;
+  const uint32_t bufc = TS ? (uint32_t)(NMAT * MS) : 256u;
+  const uint32_t abase = TS ? (uint32_t)(nbuf * NMAT * MS) : 0u;
+  const int nst = TS ? min(CS, (int)((512u - abase) / (NMAT * 32))) : CS;
 
   if (warp == kProdWarp) {
     if (lane == 0) {                               // raw codes + scales
@@ -505,7 +542,9 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
     // thread = (row, t): its share of the row's raw piece for one 64-K step
     // -> K chunks kc = t and 4 + t (blocks j0, j0 + 1).  Quarter-warps store
     // 8 rows of one chunk: conflict-free 16-byte stores.
-    const int t = (tid >> 3) & 3, row = (tid & 7) + 8 * (tid >> 5);
+    // TS: warp w writes TMEM lanes 32 (w % 4) .. +31 (its rows), K chunks t = w / 4
+    const int t = TS ? warp >> 2 : (tid >> 3) & 3;
+    const int row = TS ? 32 * (warp & 3) + lane : (tid & 7) + 8 * (tid >> 5);
     const int tl = row >> 4, rr = row & 15;
     int rs = 0, cs = 0, ntc = 0, ntr = 0;
     uint32_t rph = 0, cph = 0;
@@ -537,22 +576,36 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
           }
           if (lane == 0) bar_wait(can_empty(cs), cph ^ 1);
           __syncwarp();
-          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
+          if constexpr (TS) {
+            tc_fence_after();
+            // chunk kc (8 fp16) of the row -> columns 4 kc .. 4 kc + 3 of the stage
 #pragma unroll
-          for (int m = 0; m < NMAT; ++m) {
-            // UMMA K-major SWIZZLE_64B (as the TMA path): K chunk kc of a row in
-            // block kc / 4 (8 KB = 128 rows x 64 B), 16-byte slot (kc % 4) ^ ((row / 2) % 4)
-            const uint32_t dst = can + m * kAMat + row * 64 + ((t ^ ((row >> 1) & 3)) << 4);
-            sts128(dst, w[m][0]);
-            sts128(dst + 8192, w[m][1]);
-          }
+            for (int m = 0; m < NMAT; ++m) {
+              const uint32_t ta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + abase +
+                                  (uint32_t)(cs * NMAT * 32 + m * 32);
+              tmem_st4(ta + 4 * t, w[m][0]);
+              tmem_st4(ta + 16 + 4 * t, w[m][1]);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+          } else {
+            const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) {
+              // UMMA K-major SWIZZLE_64B (as the TMA path): K chunk kc of a row in
+              // block kc / 4 (8 KB = 128 rows x 64 B), 16-byte slot (kc % 4) ^ ((row / 2) % 4)
+              const uint32_t dst = can + m * kAMat + row * 64 + ((t ^ ((row >> 1) & 3)) << 4);
+              sts128(dst, w[m][0]);
+              sts128(dst + 8192, w[m][1]);
+            }
 #ifndef HB_K3_NOFENCE
-          fence_async_smem();
+            fence_async_smem();
 #endif
+          }
           __syncwarp();
           if (lane == 0) bar_arrive(can_full(cs));
           if (NMAT == 2 && tid == 0) K3_STAMP(2, ntc++);
-          if (++cs == CS) { cs = 0; cph ^= 1; }
+          if (++cs == nst) { cs = 0; cph ^= 1; }
         }
         __syncwarp();
         if (lane == 0) bar_arrive(raw_empty(rs));
@@ -568,27 +621,36 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
         const uint32_t idesc = idesc_f16(I.v->np);
         bar_wait(tm_empty(ab), abph ^ 1);
         tc_fence_after();
-        const uint32_t tacc = tbase + ab * 256;
+        const uint32_t tacc = tbase + ab * bufc;
         for (int s = 0; s < nsteps; ++s) {
           bar_wait(can_full(cs), cph);
           bar_wait(b_full(bs), bph);
           if (NMAT == 2) K3_STAMP(3, ntm++);
           tc_fence_after();
-          const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
           const uint32_t bt = bring + bs * bslot;
+          if constexpr (TS) {
 #pragma unroll
-          for (int m = 0; m < NMAT; ++m)
+            for (int m = 0; m < NMAT; ++m)
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk)
-              umma(tacc + m * 128, sdesc_sw64(can + m * kAMat + (kk >> 1) * 8192 + (kk & 1) * 32),
-                   sdesc(bt + kk * 256), idesc, (s | kk) ? 1u : 0u);
+              for (int kk = 0; kk < kBK / 16; ++kk)
+                umma_ts(tacc + m * MS, tbase + abase + (uint32_t)(cs * NMAT * 32 + m * 32 + kk * 8),
+                        sdesc(bt + kk * 256), idesc, (s | kk) ? 1u : 0u);
+          } else {
+            const uint32_t can = sbase + kRawSlots * kRawBytes + cs * kABytes;
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk)
+                umma(tacc + m * 128, sdesc_sw64(can + m * kAMat + (kk >> 1) * 8192 + (kk & 1) * 32),
+                     sdesc(bt + kk * 256), idesc, (s | kk) ? 1u : 0u);
+          }
           umma_commit(can_empty(cs));
           umma_commit(b_empty(bs));
-          if (++cs == CS) { cs = 0; cph ^= 1; }
+          if (++cs == nst) { cs = 0; cph ^= 1; }
           if (++bs == nb) { bs = 0; bph ^= 1; }
         }
         umma_commit(tm_full(ab));
-        if (++ab == 2) { ab = 0; abph ^= 1; }
+        if (++ab == nbuf) { ab = 0; abph ^= 1; }
       }
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
@@ -599,11 +661,11 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
       const Item I = item_of<NMAT>(p, it, v0);
       bar_wait(tm_full(ab), abph);
       tc_fence_after();
-      epilogue_item<NMAT>(p, I, tbase + ((uint32_t)(q4 * 32) << 16) + ab * 256, q4, lane);
+      epilogue_item<NMAT>(p, I, tbase + ((uint32_t)(q4 * 32) << 16) + ab * bufc, q4, lane, MS);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(tm_empty(ab));
-      if (++ab == 2) { ab = 0; abph ^= 1; }
+      if (++ab == nbuf) { ab = 0; abph ^= 1; }
     }
   }
   tc_fence_before();
@@ -875,17 +937,25 @@ namespace hb {
 void launch_k3_prep(const K3Params& p, const __half* x, cudaStream_t s) {
   k3_prep_kernel<<<2 * kNumSM, 256, 0, s>>>(p, x);
 }
+template <int NMAT>
+static void launch_q(const K3Params& p, cudaStream_t s) {
+  if (p.ts) {
+    set_max_dyn_smem(k3_kernel<NMAT, true>, kSmemTS);
+    k3_kernel<NMAT, true><<<kNumSM, kThreads, kSmemTS, s>>>(p);
+  } else {
+    set_max_dyn_smem(k3_kernel<NMAT, false>, kSmem);
+    k3_kernel<NMAT, false><<<kNumSM, kThreads, kSmem, s>>>(p);
+  }
+}
 void launch_k3a(const K3Params& p, cudaStream_t s) {
-  set_max_dyn_smem(k3_kernel<2>, kSmem);
   set_max_dyn_smem(k3d_kernel<2>, d_smem<2>());
   if (p.has_f16) k3d_kernel<2><<<kNumSM, kDThreads, d_smem<2>(), s>>>(p);
-  if (p.has_q) k3_kernel<2><<<kNumSM, kThreads, kSmem, s>>>(p);
+  if (p.has_q) launch_q<2>(p, s);
 }
 void launch_k3b(const K3Params& p, cudaStream_t s) {
-  set_max_dyn_smem(k3_kernel<1>, kSmem);
   set_max_dyn_smem(k3d_kernel<1>, d_smem<1>());
   if (p.has_f16) k3d_kernel<1><<<kNumSM, kDThreads, d_smem<1>(), s>>>(p);
-  if (p.has_q) k3_kernel<1><<<kNumSM, kThreads, kSmem, s>>>(p);
+  if (p.has_q) launch_q<1>(p, s);
 }
 
 }  // namespace hb
