@@ -15,6 +15,14 @@ Encodings (block = 32 consecutive elements along K of one row):
     Q2   w = d * q + m      q in [0, 3]                    (3.0 bits/weight)
 d, m fp16, one per block.  Every value is an exact dyadic rational in fp64.
 
+    Q2K  llama.cpp's Q2_K arithmetic (HOBBIT runs on Llama.cpp,
+         whose "int2" version of an int8 model is a k-quant): super-block of
+         256 elements of a row = 16 sub-blocks of 16, per sub-block j a byte
+         sc_j (low nibble scale, high nibble min), per super-block fp16 d, dmin:
+             w = d * (sc_j & 15) * q - dmin * (sc_j >> 4),  q in [0, 3]
+         (2.625 bits/weight).  Packed with OUR canonical conventions (LSB-first,
+         row-major) rather than llama.cpp's interleaved qs order (R32).
+
 CANONICAL blob (the interchange format the oracle reads and
 writes; the library converts it into its own device layout with
 hb_repack_canonical, which the oracle knows nothing about):
@@ -32,10 +40,11 @@ from __future__ import annotations
 
 import numpy as np
 
-F16, Q8, Q4, Q2 = 0, 1, 2, 3
-ENC_NAMES = {F16: "F16", Q8: "Q8", Q4: "Q4", Q2: "Q2"}
-QBITS = {F16: 16, Q8: 8, Q4: 4, Q2: 2}
+F16, Q8, Q4, Q2, Q2K = 0, 1, 2, 3, 4
+ENC_NAMES = {F16: "F16", Q8: "Q8", Q4: "Q4", Q2: "Q2", Q2K: "Q2K"}
+QBITS = {F16: 16, Q8: 8, Q4: 4, Q2: 2, Q2K: 2}
 BLOCK = 32
+SUPER, SUB = 256, 16           # Q2K super-block and sub-block
 SECTION_ALIGN = 256
 
 
@@ -47,6 +56,9 @@ def matrix_sections(enc: int, n: int, k: int):
     """[(name, nbytes)] of one [n,k] matrix in encoding enc."""
     if enc == F16:
         return [("w", n * k * 2)]
+    if enc == Q2K:             # codes, sc [n][k/16] bytes, d and dmin [n][k/256] fp16
+        return [("q", n * k // 4), ("sc", n * (k // SUB)), ("d", n * (k // SUPER) * 2),
+                ("dm", n * (k // SUPER) * 2)]
     secs = [("q", n * k * QBITS[enc] // 8), ("d", n * (k // BLOCK) * 2)]
     if enc == Q2:
         secs.append(("m", n * (k // BLOCK) * 2))
@@ -59,7 +71,8 @@ def expert_matrix_shapes(hidden: int, ffn: int):
 
 
 def blob_layout(enc: int, hidden: int, ffn: int):
-    """({mat: {section: (offset, nbytes)}}, total bytes) of one expert blob."""
+    """({mat: {section: (offset, nbytes)}}, total bytes) of one expert blob.
+    Q2K blobs are padded to the Q2 total (the same container size, R32)."""
     off = 0
     lay = {}
     for mat, (n, k) in enumerate(expert_matrix_shapes(hidden, ffn)):
@@ -67,6 +80,8 @@ def blob_layout(enc: int, hidden: int, ffn: int):
         for name, nbytes in matrix_sections(enc, n, k):
             lay[mat][name] = (off, nbytes)
             off = _align(off + nbytes)
+    if enc == Q2K:
+        off = max(off, blob_layout(Q2, hidden, ffn)[1])
     return lay, off
 
 
@@ -91,6 +106,12 @@ def decode_matrix(enc: int, blob: np.ndarray, sections: dict, n: int, k: int) ->
     rows = blob[off:off + nb].reshape(n, k * b // 8)
     kk = np.arange(k)
     raw = (rows[:, kk * b // 8].astype(np.int64) >> ((kk * b) % 8)) & ((1 << b) - 1)
+    if enc == Q2K:             # w = d * (sc & 15) * q - dmin * (sc >> 4)
+        off, nb = sections["sc"]
+        sc = np.repeat(blob[off:off + nb].reshape(n, k // SUB).astype(np.int64), SUB, axis=1)
+        d = np.repeat(_f16_section(blob, sections["d"], n, k // SUPER), SUPER, axis=1)
+        dm = np.repeat(_f16_section(blob, sections["dm"], n, k // SUPER), SUPER, axis=1)
+        return d * (sc & 15) * raw - dm * (sc >> 4)
     d = np.repeat(_f16_section(blob, sections["d"], n, k // BLOCK), BLOCK, axis=1)
     if enc == Q8:
         return d * np.where(raw >= 128, raw - 256, raw)       # two's complement int8
@@ -156,6 +177,37 @@ def quantize_codes(enc: int, w16: np.ndarray):
     raise ValueError(enc)
 
 
+def quantize_q2k(w16: np.ndarray):
+    """R33: the Q2K quantiser (ours, not llama.cpp's iterative make_qkx2_quants),
+    IEEE fp32 in exactly this order (the CUDA quantiser does the same):
+      per sub-block j of 16: mn_j = min(0, min x), mx_j = max x,
+        s_j = (mx_j - mn_j) / 3,  mm_j = -mn_j
+      per super-block: d = f16(max_j s_j / 15), dmin = f16(max_j mm_j / 15)
+      sc_lo_j = clamp(rint(s_j / d), 0, 15)   (0 if d == 0)
+      sc_hi_j = clamp(rint(mm_j / dmin), 0, 15)  (0 if dmin == 0)
+      dl_j = d * sc_lo_j, ml_j = dmin * sc_hi_j
+      q = clamp(rint((x + ml_j) / dl_j), 0, 3)  (0 if dl_j == 0)
+    Returns (codes int64 [n,k], sc uint8 [n,k/16], d fp16 [n,k/256], dmin fp16 [n,k/256])."""
+    n, k = w16.shape
+    x = w16.astype(np.float32).reshape(n, k // SUPER, SUPER // SUB, SUB)
+    mn = np.minimum(np.float32(0.0), x.min(axis=3))
+    mx = x.max(axis=3)
+    s_j = (mx - mn) / np.float32(3.0)
+    mm_j = -mn
+    d16 = (s_j.max(axis=2) / np.float32(15.0)).astype(np.float16)
+    dm16 = (mm_j.max(axis=2) / np.float32(15.0)).astype(np.float16)
+    d = d16.astype(np.float32)[..., None]
+    dm = dm16.astype(np.float32)[..., None]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lo = np.where(d == 0, 0, np.clip(np.rint(s_j / d), 0, 15))
+        hi = np.where(dm == 0, 0, np.clip(np.rint(mm_j / dm), 0, 15))
+        dl = (d * lo.astype(np.float32))[..., None]
+        ml = (dm * hi.astype(np.float32))[..., None]
+        q = np.where(dl == 0, 0, np.clip(np.rint((x + ml) / dl), 0, 3))
+    sc = (lo.astype(np.int64) | (hi.astype(np.int64) << 4)).astype(np.uint8)
+    return (q.astype(np.int64).reshape(n, k), sc.reshape(n, k // SUB), d16, dm16)
+
+
 def pack_codes(enc: int, codes: np.ndarray) -> np.ndarray:
     """The "q" section (uint8): codes [n,k] row-major, LSB first."""
     n, k = codes.shape
@@ -184,6 +236,13 @@ def quantize_blob(enc: int, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray) -> n
         sec = lay[mat]
         if enc == F16:
             put(sec["w"], np.ascontiguousarray(w, dtype=np.float16))
+            continue
+        if enc == Q2K:
+            codes, sc, d16, dm16 = quantize_q2k(w)
+            put(sec["q"], pack_codes(enc, codes))
+            put(sec["sc"], sc)
+            put(sec["d"], d16)
+            put(sec["dm"], dm16)
             continue
         codes, d16, m16 = quantize_codes(enc, w)
         put(sec["q"], pack_codes(enc, codes))

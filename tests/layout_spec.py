@@ -27,6 +27,10 @@ of the group, fp16) and, for Q2, another 2*BPG bytes of m:
     scale record of (n, grp) at 16*SB*(G*tile + grp) + SB*r
         d of block j at +2*j,  m of block j at +2*BPG + 2*j   (Q2)
 
+Q2K (R32): the codes as Q2; the 32-byte record of (n, grp) (one
+super-block of 256) holds d (fp16) at +0, dmin (fp16) at +2 and the 16
+sub-block bytes sc_j at +4 + j, bytes +20..+31 zero.
+
 Per matrix (W1, W3, W2): a code section then (quantised) one scale section,
 each 256-byte aligned.  The total size equals the canonical blob's.
 """
@@ -34,9 +38,9 @@ from __future__ import annotations
 
 import numpy as np
 
-F16, Q8, Q4, Q2 = 0, 1, 2, 3
-QBITS = {F16: 16, Q8: 8, Q4: 4, Q2: 2}
-EPG = {F16: 32, Q8: 64, Q4: 128, Q2: 256}
+F16, Q8, Q4, Q2, Q2K = 0, 1, 2, 3, 4
+QBITS = {F16: 16, Q8: 8, Q4: 4, Q2: 2, Q2K: 2}
+EPG = {F16: 32, Q8: 64, Q4: 128, Q2: 256, Q2K: 256}
 TILE = 16
 
 
@@ -49,7 +53,7 @@ def bpg(enc):
 
 
 def scale_record_bytes(enc):
-    return 0 if enc == F16 else 2 * bpg(enc) * (2 if enc == Q2 else 1)
+    return 0 if enc == F16 else 2 * bpg(enc) * (2 if enc in (Q2, Q2K) else 1)
 
 
 def sections(enc, hidden, ffn):
@@ -61,7 +65,7 @@ def sections(enc, hidden, ffn):
         s = None
         if enc != F16:
             s = off
-            off = _align(off + n * (k // 32) * 2 * (2 if enc == Q2 else 1))
+            off = _align(off + n * (k // 32) * 2 * (2 if enc in (Q2, Q2K) else 1))
         out.append((q, s))
     return out, off
 
@@ -112,6 +116,18 @@ def device_matrix(enc, codes_or_f16, d16, m16, n, k):
         sel = shift[0] == s
         out[pos[:, sel].ravel()] |= ((codes[:, sel] & mask) << s).astype(np.uint8).ravel()
     sc = np.zeros(n * (k // EPG[enc]) * scale_record_bytes(enc), dtype=np.uint8)
+    if enc == Q2K:                    # d16 = (sc bytes [n][k/16], d [n][k/256], dmin [n][k/256])
+        scb, dd, dm = d16
+        G = k // 256
+        grp = np.arange(G)[None, :]
+        rec = 16 * 32 * (G * (N // TILE) + grp) + 32 * (N % TILE)
+        for arr, o in ((dd, 0), (dm, 2)):
+            bits = np.ascontiguousarray(arr, dtype=np.float16).view(np.uint16)
+            sc[(rec + o).ravel()] = (bits & 0xFF).astype(np.uint8).ravel()
+            sc[(rec + o + 1).ravel()] = (bits >> 8).astype(np.uint8).ravel()
+        for j in range(16):
+            sc[(rec + 4 + j).ravel()] = scb[:, j::16].ravel()
+        return out, sc
     Bk = np.arange(k // 32)[None, :]
     for arr, which in ((d16, "d"), (m16, "m")):
         if arr is None:
@@ -138,6 +154,15 @@ def canonical_fields(enc, blob, hidden, ffn):
         off = _align(off + n * k * b // 8)
         kk = np.arange(k)
         codes = (rows[:, kk * b // 8].astype(np.int64) >> ((kk * b) % 8)) & ((1 << b) - 1)
+        if enc == Q2K:                # sc [n][k/16] bytes, d and dmin [n][k/256] fp16
+            scb = blob[off:off + n * k // 16].reshape(n, k // 16)
+            off = _align(off + n * k // 16)
+            dd = blob[off:off + n * k // 128].view(np.float16).reshape(n, k // 256)
+            off = _align(off + n * k // 128)
+            dm = blob[off:off + n * k // 128].view(np.float16).reshape(n, k // 256)
+            off = _align(off + n * k // 128)
+            out.append((codes, (scb, dd, dm), None))
+            continue
         d = blob[off:off + n * k // 16].view(np.float16).reshape(n, k // 32)
         off = _align(off + n * k // 16)
         m = None

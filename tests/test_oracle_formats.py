@@ -216,3 +216,69 @@ def test_f16_blob_roundtrip():
     out = fm.decode_blob(fm.F16, fm.quantize_blob(fm.F16, w1, w3, w2), 32, 64)
     for a, b in zip(out, (w1, w3, w2)):
         assert np.array_equal(a, b.astype(np.float64))
+
+
+# ---------------------------------------------------------------- Q2K (R32/R33)
+def _q2k_blob(codes, sc, d16, dm16):
+    """One [1, 256] Q2K matrix laid out by hand: codes LSB first (4 per byte),
+    then the 16 sub-block bytes, then d, then dmin."""
+    q = np.zeros(64, dtype=np.uint8)
+    for k, c in enumerate(codes):
+        q[k // 4] |= (c & 3) << (2 * (k % 4))
+    parts = [q, np.asarray(sc, dtype=np.uint8), np.array([d16], dtype=np.float16).view(np.uint8),
+             np.array([dm16], dtype=np.float16).view(np.uint8)]
+    sec, off = {}, 0
+    for name, part in zip(("q", "sc", "d", "dm"), parts):
+        sec[name] = (off, part.size)
+        off += part.size
+    return np.concatenate(parts), sec
+
+
+def test_q2k_decode_hand_worked():
+    """Q2K (llama.cpp's Q2_K arithmetic): element k of a super-block lies in
+    sub-block j = k // 16; sc_j = j | (15 - j) << 4, q = k % 4, d = 0.5,
+    dmin = 0.25.  Values worked out by hand:
+      k = 0   (j = 0, q = 0):  0.5*0*0  - 0.25*15 = -3.75
+      k = 17  (j = 1, q = 1):  0.5*1*1  - 0.25*14 = -3.0
+      k = 130 (j = 8, q = 2):  0.5*8*2  - 0.25*7  =  6.25
+      k = 255 (j = 15, q = 3): 0.5*15*3 - 0.25*0  = 22.5"""
+    codes = [k % 4 for k in range(256)]
+    sc = [j | ((15 - j) << 4) for j in range(16)]
+    blob, sec = _q2k_blob(codes, sc, 0.5, 0.25)
+    w = fm.decode_matrix(fm.Q2K, blob, sec, 1, 256)
+    assert w[0, 0] == -3.75 and w[0, 17] == -3.0 and w[0, 130] == 6.25 and w[0, 255] == 22.5
+
+
+def test_q2k_quantiser_exact_when_representable():
+    """Values on the Q2K grid of d = 0.5, sc_lo = 15 (dl = 7.5), no negative
+    part (dmin = 0): every sub-block holds 0, 7.5, 15, 22.5 and round-trips
+    exactly (the quantiser picks d = max s_j / 15 = 7.5 / 15 = 0.5)."""
+    row = np.array([7.5 * (k % 4) for k in range(512)], dtype=np.float16)[None, :]
+    codes, sc, d16, dm16 = fm.quantize_q2k(row)
+    assert np.all(d16 == 0.5) and np.all(dm16 == 0) and np.all(sc == 15)
+    assert np.array_equal(codes[0], np.arange(512) % 4)
+
+
+def test_q2k_quantiser_roundtrip_bound_and_container():
+    """|x - deq| <= dl_j / 2 + the scale roundings, on random rows; a Q2K blob
+    has the Q2 container size (R32)."""
+    rng = np.random.default_rng(11)
+    w = (rng.standard_normal((32, 512)) * 0.02).astype(np.float16)
+    codes, sc, d16, dm16 = fm.quantize_q2k(w)
+    parts = [fm.pack_codes(fm.Q2K, codes), sc.ravel(), d16.view(np.uint8).ravel(),
+             dm16.view(np.uint8).ravel()]
+    sec, off = {}, 0
+    for name, part in zip(("q", "sc", "d", "dm"), parts):
+        sec[name] = (off, part.size)
+        off += part.size
+    deq = fm.decode_matrix(fm.Q2K, np.concatenate(parts), sec, 32, 512)
+    dl = np.repeat(np.repeat(d16.astype(np.float64), 16, axis=1) * (sc & 15), 16, axis=1)
+    x = w.astype(np.float64)
+    ml = np.repeat(np.repeat(dm16.astype(np.float64), 16, axis=1) * (sc >> 4), 16, axis=1)
+    inside = (x >= -ml) & (x <= 3 * dl - ml)
+    err = np.abs(deq - x)
+    # a 4-bit scale step can leave the sub-block range up to 1/30 of the super-block max outside
+    slack = np.repeat(np.repeat(np.maximum(d16, dm16).astype(np.float64), 256, axis=1), 1, axis=0)
+    assert np.all(err[inside] <= 0.5 * dl[inside] + 1e-12)
+    assert np.all(err <= 0.5 * dl + 3 * slack + 1e-12)
+    assert fm.blob_bytes(fm.Q2K, 4096, 14336) == fm.blob_bytes(fm.Q2, 4096, 14336)
