@@ -38,7 +38,8 @@ UNIT = "tokens/s"
 WORKLOAD = "mixtral-8x7b-shapes batch-1 decode, 32 layers, fp16/int4 strict (T1=0.6,T2=0.9), all experts resident"
 
 
-PAIRS = {"f16q4": (0, 2), "f16q2": (0, 3), "q8q2": (1, 3), "q8q4": (1, 2)}
+PAIRS = {"f16q4": (0, 2), "f16q2": (0, 3), "q8q2": (1, 3), "q8q4": (1, 2),
+         "f16q2k": (0, 4), "q8q2k": (1, 4)}     # 4 = HB_Q2K (llama.cpp Q2_K arithmetic, R32)
 
 
 def peaks():

@@ -69,7 +69,18 @@ extern "C" {
  *    contiguous 1 KB "unit" -- and one scale section of per-(unit,row) d/m
  *    records (hb_blob_section()).  hb_repack_canonical converts; the
  *    quantiser writes it directly. */
-enum { HB_F16 = 0, HB_Q8 = 1, HB_Q4 = 2, HB_Q2 = 3 };
+enum { HB_F16 = 0, HB_Q8 = 1, HB_Q4 = 2, HB_Q2 = 3, HB_Q2K = 4 };
+/* HB_Q2K: llama.cpp's Q2_K arithmetic (R32/R33): super-block of 256
+ * elements of a row = 16 sub-blocks of 16; per sub-block j a byte sc_j (low
+ * nibble scale, high nibble min), per super-block fp16 d and dmin:
+ *   w = d * (sc_j & 15) * q - dmin * (sc_j >> 4),  q in [0, 3]   (2.625 bits/weight)
+ * CANONICAL: per matrix q (as Q2), sc [N][K/16] bytes, d [N][K/256] fp16,
+ * dmin [N][K/256] fp16 (hb_canonical_section sec 0..3), blob padded to the Q2
+ * size.  DEVICE: the Q2 code layout; the 32-byte record of (unit, row) holds
+ * d, dmin, sc[16].  The decode kernels form each weight in fp16 (two
+ * roundings) before the MMA; the batched tcgen05 path is not built for it (a
+ * context with HB_Q2K runs every batch on the dequant-GEMV path).  A pair may
+ * use HB_Q2K or HB_Q2, not both. */
 /* Precision decision of one selected expert. */
 enum { HB_HIGH = 0, HB_LOW = 1, HB_SKIP = 2 };
 #define HB_ENC_NONE 255
@@ -170,7 +181,8 @@ size_t      hb_blob_bytes(int enc, int hidden, int ffn);
  * does not exist (F16 has no scale section). */
 int         hb_blob_section(int enc, int hidden, int ffn, int mat, int sec,
                             size_t* offset, size_t* nbytes);
-/* Same for a CANONICAL blob: sec 0 codes / fp16 values, 1 d, 2 m (Q2 only). */
+/* Same for a CANONICAL blob: sec 0 codes / fp16 values, 1 d, 2 m (Q2 only);
+ * HB_Q2K: 1 sc, 2 d, 3 dmin. */
 int         hb_canonical_section(int enc, int hidden, int ffn, int mat, int sec,
                                  size_t* offset, size_t* nbytes);
 /* Convert a canonical blob into the device layout: src and dst are device

@@ -40,8 +40,9 @@ cudaError_t set_max_dyn_smem_impl(const void* kernel, int bytes) {
 }
 
 int blob_layout(int enc, int hidden, int ffn, BlobLayout* out) {
-  if (enc < HB_F16 || enc > HB_Q2 || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
+  if (enc < HB_F16 || enc > HB_Q2K || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
     return HB_EINVAL;
+  if (enc == HB_Q2K) enc = HB_Q2;            // same codes, same 32-byte records (R32)
   // code section + one scale section per matrix (tile-major units, DESIGN.md
   // "Blob layout"); every section 256-byte aligned
   const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
@@ -112,6 +113,7 @@ struct hb_ctx {
   int dc_fg_ctas = 32, dc_bg_ctas = 16;   // HB_DC_FG_CTAS / HB_DC_BG_CTAS
   size_t dc_chunk = 256u << 10;           // HB_DC_CHUNK_KB
   uint64_t copied[2] = {0, 0};            // host path: bytes issued on demand / prefetch+explicit
+  bool kq = false;                        // the Q2 slot holds HB_Q2K blobs (R32)
   // token-sharded EP (hb_config.token_sharded)
   bool ts = false;
   int ts_C = 0;                           // rows per (source, destination) = max_batch * top_k
@@ -292,20 +294,27 @@ int hb_blob_section(int enc, int hidden, int ffn, int mat, int sec, size_t* offs
   if (sec == 0) { *offset = L.mat[mat].q; *nbytes = (size_t)N * K * bits / 8; return HB_OK; }
   if (enc == HB_F16 || sec == 2) return fail(nullptr, HB_EINVAL, "section does not exist");
   *offset = L.mat[mat].s;
-  *nbytes = (size_t)N * (K / 32) * 2 * (enc == HB_Q2 ? 2 : 1);
+  *nbytes = (size_t)N * (K / 32) * 2 * (enc == HB_Q2 || enc == HB_Q2K ? 2 : 1);
   return HB_OK;
 }
 
 int hb_canonical_section(int enc, int hidden, int ffn, int mat, int sec, size_t* offset,
                          size_t* nbytes) {
   CanonLayout C;
-  if (canonical_layout(enc, hidden, ffn, &C) || mat < 0 || mat > 2 || sec < 0 || sec > 2 ||
+  if (canonical_layout(enc, hidden, ffn, &C) || mat < 0 || mat > 2 || sec < 0 || sec > 3 ||
       !offset || !nbytes)
     return fail(nullptr, HB_EINVAL, "bad canonical section query");
   const int N = mat < 2 ? ffn : hidden, K = mat < 2 ? hidden : ffn;
   const int bits = enc == HB_F16 ? 16 : enc == HB_Q8 ? 8 : enc == HB_Q4 ? 4 : 2;
   if (sec == 0) { *offset = C.q[mat]; *nbytes = (size_t)N * K * bits / 8; return HB_OK; }
-  if (enc == HB_F16 || (sec == 2 && enc != HB_Q2)) return fail(nullptr, HB_EINVAL, "section does not exist");
+  if (enc == HB_Q2K) {
+    if (sec == 1) { *offset = C.sc[mat]; *nbytes = (size_t)N * (K / 16); return HB_OK; }
+    *offset = sec == 2 ? C.d[mat] : C.m[mat];
+    *nbytes = (size_t)N * (K / 256) * 2;
+    return HB_OK;
+  }
+  if (sec == 3 || enc == HB_F16 || (sec == 2 && enc != HB_Q2))
+    return fail(nullptr, HB_EINVAL, "section does not exist");
   *offset = sec == 1 ? C.d[mat] : C.m[mat];
   *nbytes = (size_t)N * (K / 32) * 2;
   return HB_OK;
@@ -371,7 +380,16 @@ static void free_ctx(hb_ctx* c) {
 
 int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   if (!cfg || !out) return fail(nullptr, HB_EINVAL, "null argument");
-  const hb_config& k = *cfg;
+  // HB_Q2K lives in the Q2 slot of every per-encoding table (same device
+  // layout size); the context remembers the format (hb_ctx::kq) and maps the
+  // encoding at the boundary (registration, loads, events, decisions)
+  hb_config kin = *cfg;
+  const bool kq = kin.hi_enc == HB_Q2K || kin.lo_enc == HB_Q2K;
+  if (kq && (kin.hi_enc == HB_Q2 || kin.lo_enc == HB_Q2))
+    return fail(nullptr, HB_EINVAL, "a pair may use HB_Q2K or HB_Q2, not both");
+  if (kin.hi_enc == HB_Q2K) kin.hi_enc = HB_Q2;
+  if (kin.lo_enc == HB_Q2K) kin.lo_enc = HB_Q2;
+  const hb_config& k = kin;
   if (k.n_layers <= 0 || k.n_experts <= 0 || k.n_experts > 64 || k.top_k <= 0 ||
       k.top_k > k.n_experts || k.top_k > kMaxTopK)
     return fail(nullptr, HB_EINVAL, "bad n_layers / n_experts (<=64) / top_k (<=8)");
@@ -393,6 +411,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   hb_ctx* c = new (std::nothrow) hb_ctx;
   if (!c) return fail(nullptr, HB_ENOMEM, "out of host memory");
   c->cfg = k;
+  c->kq = kq;
   c->device = device;
   c->resident = resident;
   for (int e = 0; e < 4; ++e) {
@@ -457,7 +476,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     // K3 scratch: X and h of every vjob3 in canonical blocks (rows padded to 16)
     const int max_v3 = c->max_jobs + (c->max_slots + kK3MaxN - 1) / kK3MaxN;
     const size_t rows = (size_t)c->max_slots + 16 * (size_t)max_v3;
-    if (B > 1 && max_v3 <= kK3MaxV3) {
+    if (B > 1 && max_v3 <= kK3MaxV3 && !kq) {       // no tcgen05 path for Q2K
       if (!dm((void**)&c->k3_xg, rows * H * 2) || !dm((void**)&c->k3_hB, rows * F * 2) ||
           !dm((void**)&c->k3_tab, sizeof(K3Table)) ||
           (resident && !dm((void**)&c->k3_tmap, sizeof(CUtensorMap) * (size_t)L * E * 24)))
@@ -482,7 +501,8 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     // (one-CTA filtered router kernel, K2a, hfin, K2b)
     const char* dm_ = std::getenv("HB_DECODE");
     const std::string mode = dm_ ? dm_ : "legacy";
-    c->fused_ok = resident && K == 2 && mode != "legacy" && fused_fits(E, H, F, k.hi_enc, k.lo_enc);
+    c->fused_ok = resident && K == 2 && mode != "legacy" && !kq &&
+                  fused_fits(E, H, F, k.hi_enc, k.lo_enc);
     c->fused_split = mode == "split";
     c->fused_router = mode == "router";
     // measured slower (K2a CTAs held at the barrier: K2b's prologue cannot
@@ -645,6 +665,13 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
                        size_t nbytes, int flags) {
   if (!c || !blob) return fail(c, HB_EINVAL, "null argument");
   const hb_config& k = c->cfg;
+  const int enc_ext = enc;                      // the caller's encoding (repack format)
+  if (enc == HB_Q2K) {
+    if (!c->kq) return fail(c, HB_EINVAL, "HB_Q2K blob for a context without HB_Q2K");
+    enc = HB_Q2;
+  } else if (enc == HB_Q2 && c->kq) {
+    return fail(c, HB_EINVAL, "this context's low-bit encoding is HB_Q2K");
+  }
   if (layer < 0 || layer >= k.n_layers || expert < 0 || expert >= k.n_experts)
     return fail(c, HB_EINVAL, "bad layer / expert");
   if (enc != k.hi_enc && enc != k.lo_enc) return fail(c, HB_EINVAL, "encoding is neither hi_enc nor lo_enc");
@@ -660,7 +687,7 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
       if (canonical) return fail(c, HB_EINVAL, "a borrowed blob must be in the device layout");
     } else if (mode == HB_REG_DEVICE_COPY || mode == HB_REG_HOST_COPY) {
       uint8_t* owned = nullptr;
-      if (int rc = copy_to_device(c, blob, mode == HB_REG_HOST_COPY, canonical, nbytes, enc, &owned))
+      if (int rc = copy_to_device(c, blob, mode == HB_REG_HOST_COPY, canonical, nbytes, enc_ext, &owned))
         return rc;
       c->dev_owned.push_back(owned);
       dblob = owned;
@@ -695,7 +722,7 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
       return fail(c, HB_ENOMEM, "pinned arena allocation failed");
     if (canonical) {                            // convert on the device, back into the arena
       uint8_t* dev = nullptr;
-      if (int rc = copy_to_device(c, blob, true, true, nbytes, enc, &dev)) {
+      if (int rc = copy_to_device(c, blob, true, true, nbytes, enc_ext, &dev)) {
         cudaFreeHost(p);
         return rc;
       }
@@ -816,6 +843,7 @@ static GemvParams gemv_params(hb_ctx* c, int batch, void* y, float* au) {
   g.y = (float*)y;
   g.rowbad = c->rowbad;
   g.hfin_tail = c->hfin_tail;
+  g.kq = c->kq;
   g.ctas = kGemvCTAs;
   g.clean = !c->hfin_tail;                   // hfin leaves the K2a sums clean, zeroes y
   g.gbar = c->gbar;
@@ -1499,6 +1527,9 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
 
 int expert_cache_load(hb_ctx* c, int layer, int expert, int enc, void* stream) {
   if (!c) return fail(nullptr, HB_EINVAL, "null ctx");
+  if (enc == HB_Q2K && c->kq) enc = HB_Q2;
+  else if ((enc == HB_Q2 && c->kq) || enc == HB_Q2K)
+    return fail(c, HB_EINVAL, "encoding is neither hi_enc nor lo_enc");
   if (c->resident) return fail(c, HB_ESTATE, "expert_cache_load needs a constrained cache");
   const hb_config& k = c->cfg;
   if (layer < 0 || layer >= k.n_layers || expert < 0 || expert >= k.n_experts)
@@ -1602,6 +1633,9 @@ int hb_get_decisions(hb_ctx* c, hb_decision* out, int cap) {
     CUDA_TRY(c, cudaDeviceSynchronize());
     CUDA_TRY(c, cudaMemcpy(out, c->dec, sizeof(hb_decision) * n, cudaMemcpyDeviceToHost));
   }
+  if (c->kq)                                    // the Q2 slot holds HB_Q2K
+    for (int i = 0; i < n; ++i)
+      if (out[i].served_enc == HB_Q2) out[i].served_enc = HB_Q2K;
   return n;
 }
 
@@ -1629,10 +1663,18 @@ int hb_get_logits(hb_ctx* c, int64_t* out, int cap_pairs) {
 
 int hb_get_events(hb_ctx* c, hb_event* out, int cap) {
   if (!c || (cap > 0 && !out)) return fail(c, HB_EINVAL, "null argument");
-  if (c->dc) return dc_events(c, out, cap);
-  const int n = std::min<int>(cap, (int)c->log.size());
-  for (int i = 0; i < n; ++i) out[i] = c->log[i];
-  c->log.erase(c->log.begin(), c->log.begin() + n);
+  int n;
+  if (c->dc) {
+    n = dc_events(c, out, cap);
+    if (n < 0) return n;
+  } else {
+    n = std::min<int>(cap, (int)c->log.size());
+    for (int i = 0; i < n; ++i) out[i] = c->log[i];
+    c->log.erase(c->log.begin(), c->log.begin() + n);
+  }
+  if (c->kq)
+    for (int i = 0; i < n; ++i)
+      if (out[i].enc == HB_Q2) out[i].enc = HB_Q2K;
   return n;
 }
 
@@ -1710,10 +1752,11 @@ int hb_last_expert_bytes(hb_ctx* c, uint64_t* out) {
   uint64_t tot = 0;
   for (int i = 0; i < n; ++i) {
     if (d[i].served_enc == HB_ENC_NONE) continue;
-    const size_t key = (size_t)d[i].expert * 4 + d[i].served_enc;
+    const int se = d[i].served_enc == HB_Q2K ? HB_Q2 : d[i].served_enc;
+    const size_t key = (size_t)d[i].expert * 4 + se;
     if (seen[key]) continue;
     seen[key] = 1;
-    tot += c->bbytes[d[i].served_enc];
+    tot += c->bbytes[se];
   }
   *out = tot;
   return HB_OK;

@@ -113,6 +113,15 @@ __device__ __forceinline__ float lds_half(uint32_t a) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
   return __half2float(__ushort_as_half(v));
 }
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t f2h2u(float v) {     // (rn(v), rn(v)) as a packed pair
+  __half2 h = __float2half2_rn(v);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
 __device__ __forceinline__ float lds_f32(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -183,6 +192,10 @@ template <> struct Enc<HB_F16> { static constexpr int BPG = 1, EPG = 32,  SB = 0
 template <> struct Enc<HB_Q8>  { static constexpr int BPG = 2, EPG = 64,  SB = 4;  };
 template <> struct Enc<HB_Q4>  { static constexpr int BPG = 4, EPG = 128, SB = 8;  };
 template <> struct Enc<HB_Q2>  { static constexpr int BPG = 8, EPG = 256, SB = 32; };
+// HB_Q2K (R32), kernel-internal template value (the context stores it in the
+// Q2 slot): Q2's code layout, 32-byte records [d, dmin, sc[16], pad]
+constexpr int kEncQ2K = 4;
+template <> struct Enc<kEncQ2K> { static constexpr int BPG = 8, EPG = 256, SB = 32; };
 
 __host__ __device__ constexpr int epg_of(int enc) {
   return enc == HB_F16 ? 32 : enc == HB_Q8 ? 64 : enc == HB_Q4 ? 128 : 256;
@@ -682,7 +695,7 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
     const size_t u = (size_t)ptile * G + goff + pgrp;      // unit in the blob
 #pragma unroll
     for (int m = 0; m < NMAT; ++m) {
-      const MatLayout& L = p.lay[ENC].mat[W13 ? m : 2];
+      const MatLayout& L = p.lay[ENC == kEncQ2K ? HB_Q2 : ENC].mat[W13 ? m : 2];
       qp[m] = vj.blob + L.q + u * 1024 + 16 * lane;
       sp_[m] = vj.blob + L.s + u * 16 * SB + 16 * lane;
     }
@@ -740,7 +753,7 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
       if (lane < n && l < Uv) {
         const int tl = l / Gs, gr = l - tl * Gs;
         const size_t u = (size_t)tl * G + goff + gr;
-        const MatLayout& L = p.lay[ENC].mat[2];
+        const MatLayout& L = p.lay[ENC == kEncQ2K ? HB_Q2 : ENC].mat[2];
         const char* q = reinterpret_cast<const char*>(vj.blob + L.q + u * 1024);
 #pragma unroll
         for (int i = 0; i < 8; ++i) asm volatile("prefetch.global.L2 [%0];" :: "l"(q + 128 * i));
@@ -861,6 +874,30 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
           if constexpr (SPLIT && !kDbgNoLo) {
             mma16816(r[m], Pg[0], Ph[0], Pg[1], Ph[1], xl.x, xl.y);
             mma16816(r[m], Pg[2], Ph[2], Pg[3], Ph[3], xl.z, xl.w);
+          }
+        } else if constexpr (ENC == kEncQ2K) {
+          // Q2K (R32): lane t's pairs lie in sub-block 2 blk + t / 2 of rows g,
+          // g + 8; w = d (sc & 15) q - dmin (sc >> 4) is formed in fp16 (scale
+          // products rounded once, then one fma) and fed to the MMA directly
+          const uint32_t sd = sst + m * NU * 16 * SB;
+          const uint32_t rg = sd + g * SB, rh = sd + (g + 8) * SB;
+          const int sub = 2 * blk + (t >> 1);
+          const uint32_t cg = lds_u8(rg + 4 + sub), ch = lds_u8(rh + 4 + sub);
+          const uint32_t Dg = f2h2u(lds_half(rg) * (float)(cg & 15u));
+          const uint32_t Mg = f2h2u(-lds_half(rg + 2) * (float)(cg >> 4));
+          const uint32_t Dh = f2h2u(lds_half(rh) * (float)(ch & 15u));
+          const uint32_t Mh = f2h2u(-lds_half(rh + 2) * (float)(ch >> 4));
+          uint32_t Ag[4], Ah[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            Ag[c] = hfma2u(Pg[c], Dg, Mg);
+            Ah[c] = hfma2u(Ph[c], Dh, Mh);
+          }
+          mma16816(r[m], Ag[0], Ah[0], Ag[1], Ah[1], xb.x, xb.y);
+          mma16816(r[m], Ag[2], Ah[2], Ag[3], Ah[3], xb.z, xb.w);
+          if constexpr (SPLIT && !kDbgNoLo) {
+            mma16816(r[m], Ag[0], Ah[0], Ag[1], Ah[1], xl.x, xl.y);
+            mma16816(r[m], Ag[2], Ah[2], Ag[3], Ah[3], xl.z, xl.w);
           }
         } else {
           const uint32_t sd = sst + m * NU * 16 * SB;
@@ -1059,7 +1096,7 @@ __device__ HB_PHASE_ATTR void phase_setup(const GemvParams& p, const int* s_cum,
 
 // Every warp streams its static range, then dynamic chunks, through its ring
 // (no CTA-wide synchronisation: warps leave at different times).
-template <bool W13, bool FUSED>
+template <bool W13, bool FUSED, bool KQ = false>
 __device__ HB_PHASE_ATTR void phase_run(const GemvParams& p, const int* s_cum, const FeedConst* s_fk,
                           const int* s_subvh, const PhaseCtx& pc, const Stage& S, uint2* meta) {
   const int warp = threadIdx.x >> 5;
@@ -1113,8 +1150,14 @@ __device__ HB_PHASE_ATTR void phase_run(const GemvParams& p, const int* s_cum, c
       case 2 * HB_Q8 + 0: HB_RUN(HB_Q8, false); break;
       case 2 * HB_Q4 + 1: HB_RUN(HB_Q4, true); break;
       case 2 * HB_Q4 + 0: HB_RUN(HB_Q4, false); break;
-      case 2 * HB_Q2 + 1: HB_RUN(HB_Q2, true); break;
-      default: HB_RUN(HB_Q2, false); break;
+      // the Q2 slot: HB_Q2K in the KQ kernels (their own instantiation, so the
+      // default kernels' register allocation is not touched)
+      case 2 * HB_Q2 + 1:
+        if constexpr (KQ) HB_RUN(kEncQ2K, true); else HB_RUN(HB_Q2, true);
+        break;
+      default:
+        if constexpr (KQ) HB_RUN(kEncQ2K, false); else HB_RUN(HB_Q2, false);
+        break;
     }
 #undef HB_RUN
     first = false;
@@ -1227,8 +1270,9 @@ __device__ __noinline__ void k2a_hfin_tail(const GemvParams& p, bool any) {
 }
 
 // Legacy chain (router kernel -> K2a -> hfin -> K2b): batches, the offload
-// path and configurations the fused kernel does not cover.
-template <bool W13>
+// path and configurations the fused kernel does not cover.  KQ: the Q2 slot
+// holds HB_Q2K blobs (a separate instantiation).
+template <bool W13, bool KQ>
 __global__ void __launch_bounds__(kGemvWarps * 32, 1)
 gemv_kernel(const __grid_constant__ GemvParams p) {
   __shared__ __align__(8) uint64_t s_bar;
@@ -1275,7 +1319,7 @@ gemv_kernel(const __grid_constant__ GemvParams p) {
   PhaseCtx pc;
   phase_setup<W13, false>(p, s_cum, &s_fk, s_subb, s_subc, s_subvh, &s_nsub, smem_u32(&s_bar),
                           p.h_global, S, pc);
-  phase_run<W13, false>(p, s_cum, &s_fk, s_subvh, pc, S, s_meta[warp]);
+  phase_run<W13, false, KQ>(p, s_cum, &s_fk, s_subvh, pc, S, s_meta[warp]);
   HB_TL(W13, warp * gridDim.x + blockIdx.x, 3);
   if (W13 && p.hfin_tail) k2a_hfin_tail(p, true);
 #if HB_LEGACY_TL == 1
@@ -1895,8 +1939,13 @@ __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvP
 
 void launch_w13(const GemvParams& p, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<true>();
-  set_max_dyn_smem(gemv_kernel<true>, smem);
-  launch_pdl(gemv_kernel<true>, p.ctas, kGemvWarps * 32, smem, s, p);
+  if (p.kq) {
+    set_max_dyn_smem(gemv_kernel<true, true>, smem);
+    launch_pdl(gemv_kernel<true, true>, p.ctas, kGemvWarps * 32, smem, s, p);
+    return;
+  }
+  set_max_dyn_smem(gemv_kernel<true, false>, smem);
+  launch_pdl(gemv_kernel<true, false>, p.ctas, kGemvWarps * 32, smem, s, p);
 }
 void launch_fused(const FusedParams& p, bool split, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<false>() > gemv_smem_bytes<true>() ? gemv_smem_bytes<false>()
@@ -1935,8 +1984,13 @@ void launch_hfin(const GemvParams& p, int max_slots, cudaStream_t s) {
 }
 void launch_w2(const GemvParams& p, cudaStream_t s) {
   constexpr int smem = gemv_smem_bytes<false>();
-  set_max_dyn_smem(gemv_kernel<false>, smem);
-  launch_pdl(gemv_kernel<false>, p.ctas, kGemvWarps * 32, smem, s, p);
+  if (p.kq) {
+    set_max_dyn_smem(gemv_kernel<false, true>, smem);
+    launch_pdl(gemv_kernel<false, true>, p.ctas, kGemvWarps * 32, smem, s, p);
+    return;
+  }
+  set_max_dyn_smem(gemv_kernel<false, false>, smem);
+  launch_pdl(gemv_kernel<false, false>, p.ctas, kGemvWarps * 32, smem, s, p);
 }
 int w2_stage_capacity() { return KCfg<false>::XSTAGE; }
 

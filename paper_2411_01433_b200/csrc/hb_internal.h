@@ -37,7 +37,8 @@ int blob_layout(int enc, int hidden, int ffn, BlobLayout* out);   // host
 // Canonical blob (include/hobbit.h): per matrix the code
 // section q (row-major, LSB first), d [N][K/32] and (Q2) m, 256-byte aligned.
 struct CanonLayout {
-  uint64_t q[3], d[3], m[3];   // section offsets per matrix (0 when absent)
+  uint64_t q[3], d[3], m[3];   // section offsets per matrix (0 when absent); Q2K: m = dmin
+  uint64_t sc[3];              // Q2K: the sub-block bytes [N][K/16]
   uint64_t total;
 };
 int canonical_layout(int enc, int hidden, int ffn, CanonLayout* out);   // host
@@ -163,6 +164,7 @@ struct GemvParams {
   float* y;                            // [B][H] (zeroed by router)
   const int* rowbad;                   // [B] router's non-finite x flags: NaN rows (R28)
   int hfin_tail;                       // K2a ends with a grid barrier + h (no hfin kernel)
+  int kq;                              // the Q2 slot holds HB_Q2K blobs (R32)
   int det;                             // hb_config.deterministic: whole row tiles dealt statically
   int ctas;                            // K2a / K2b grid (<= kGemvCTAs)
   int clean;                           // hfin zeroes the K2a sums it read and the y rows (the

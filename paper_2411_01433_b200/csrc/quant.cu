@@ -126,6 +126,62 @@ __global__ void quant_kernel(const __half* __restrict__ w, int n, int k, uint8_t
     dst[i] = make_uint4(words[4 * i], words[4 * i + 1], words[4 * i + 2], words[4 * i + 3]);
 }
 
+// Q2K (R33; oracle/formats.quantize_q2k): one thread per (row,
+// super-block of 256); the codes go where Q2's go, the record holds d, dmin
+// and the 16 sub-block bytes.  IEEE fp32 in the oracle's order.
+__global__ void quant_q2k_kernel(const __half* __restrict__ w, int n, int k, uint8_t* __restrict__ q,
+                                 uint8_t* __restrict__ ssec) {
+  const int groups = k / 256;
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)n * groups) return;
+  const int row = (int)(gid / groups), grp = (int)(gid % groups);
+  const size_t unit = (size_t)(row / 16) * groups + grp;
+  const __half* src = w + (size_t)row * k + (size_t)grp * 256;
+  float s_j[16], mm_j[16];
+  float smax = 0.f, mmax = 0.f;
+  for (int j = 0; j < 16; ++j) {
+    float mn = 0.f, mx = f16(src, 16 * j);
+    for (int l = 0; l < 16; ++l) {
+      const float v = f16(src, 16 * j + l);
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+    s_j[j] = __fdiv_rn(__fsub_rn(mx, mn), 3.0f);
+    mm_j[j] = -mn;
+    smax = fmaxf(smax, s_j[j]);
+    mmax = fmaxf(mmax, mm_j[j]);
+  }
+  const __half d16 = __float2half_rn(__fdiv_rn(smax, 15.0f));
+  const __half dm16 = __float2half_rn(__fdiv_rn(mmax, 15.0f));
+  const float d = __half2float(d16), dm = __half2float(dm16);
+  uint8_t* rec = ssec + (unit * 16 + row % 16) * 32;
+  reinterpret_cast<__half*>(rec)[0] = d16;
+  reinterpret_cast<__half*>(rec)[1] = dm16;
+  uint32_t words[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) words[i] = 0u;
+  for (int j = 0; j < 16; ++j) {
+    const float lo = d == 0.f ? 0.f : fminf(fmaxf(rintf(__fdiv_rn(s_j[j], d)), 0.f), 15.f);
+    const float hi = dm == 0.f ? 0.f : fminf(fmaxf(rintf(__fdiv_rn(mm_j[j], dm)), 0.f), 15.f);
+    rec[4 + j] = (uint8_t)((int)lo | ((int)hi << 4));
+    const float dl = __fmul_rn(d, lo), ml = __fmul_rn(dm, hi);
+    for (int l = 0; l < 16; ++l) {
+      const int e = 16 * j + l;                      // element of the super-block
+      uint32_t c = 0;
+      if (dl != 0.f) c = (uint32_t)fminf(fmaxf(rintf(__fdiv_rn(__fadd_rn(f16(src, e), ml), dl)), 0.f), 3.f);
+      // Q2 placement: element 32 jb + 8 t + r -> byte 16t + 4(jb/2) + 2(r/4) + jb%2, bits 2(r%4)
+      const int jb = e >> 5, t = (e & 31) >> 3, r = e & 7;
+      const int byte = 16 * t + 4 * (jb >> 1) + 2 * (r >> 2) + (jb & 1);
+      words[byte >> 2] |= c << (8 * (byte & 3) + 2 * (r & 3));
+    }
+  }
+  for (int z = 20; z < 32; ++z) rec[z] = 0;
+  uint4* dst = reinterpret_cast<uint4*>(q + unit * 1024 + (row % 16) * 64);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    dst[i] = make_uint4(words[4 * i], words[4 * i + 1], words[4 * i + 2], words[4 * i + 3]);
+}
+
 int launch_quantize_expert(int enc, int hidden, int ffn, const __half* w1, const __half* w3,
                            const __half* w2, uint8_t* blob, cudaStream_t s) {
   BlobLayout L;
@@ -145,7 +201,8 @@ int launch_quantize_expert(int enc, int hidden, int ffn, const __half* w1, const
     const int grid = (int)((threads + 127) / 128);
     uint8_t* q = blob + L.mat[m].q;
     uint8_t* sc = blob + L.mat[m].s;
-    if (enc == HB_Q8) quant_kernel<HB_Q8><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, sc);
+    if (enc == HB_Q2K) quant_q2k_kernel<<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, sc);
+    else if (enc == HB_Q8) quant_kernel<HB_Q8><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, sc);
     else if (enc == HB_Q4) quant_kernel<HB_Q4><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, sc);
     else quant_kernel<HB_Q2><<<grid, 128, 0, s>>>(src[m], N[m], K[m], q, sc);
   }

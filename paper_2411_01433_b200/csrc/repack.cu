@@ -23,6 +23,7 @@
 namespace hb {
 
 struct RepackMat {
+  const uint8_t* sc;    // Q2K: canonical sub-block bytes [N][K/16]
   const uint8_t* q;     // canonical code section (fp16 values for F16)
   const uint16_t* d;    // canonical d [N][K/32] (quantised)
   const uint16_t* m;    // canonical m [N][K/32] (Q2)
@@ -42,7 +43,7 @@ __global__ void repack_kernel(const __grid_constant__ RepackParams p) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)M.N * nblk) return;
   const int n = (int)(i / nblk), blk = (int)(i - (long long)n * nblk);
-  const int enc = p.enc;
+  const int enc = p.enc == HB_Q2K ? HB_Q2 : p.enc;   // Q2K codes are Q2's
   const int epg = epg_of_enc(enc), bpg = epg / 32;
   const int G = M.K / epg, tile = n / 16, r = n % 16, grp = blk / bpg, j = blk % bpg;
   uint8_t* base = M.dq + 1024ull * ((size_t)G * tile + grp) + 64 * r;
@@ -70,13 +71,44 @@ __global__ void repack_kernel(const __grid_constant__ RepackParams p) {
   }
   const int sb = 2 * bpg * (enc == HB_Q2 ? 2 : 1);
   uint16_t* rec = reinterpret_cast<uint16_t*>(M.ds + 16ull * sb * ((size_t)G * tile + grp) + sb * r);
+  if (p.enc == HB_Q2K) {            // record: d, dmin, sc[16] of the super-block (R32)
+    uint8_t* rb = reinterpret_cast<uint8_t*>(rec);
+    rb[4 + 2 * j] = M.sc[(size_t)n * (M.K / 16) + 2 * blk];
+    rb[4 + 2 * j + 1] = M.sc[(size_t)n * (M.K / 16) + 2 * blk + 1];
+    if (j == 0) {
+      rec[0] = M.d[(size_t)n * G + grp];
+      rec[1] = M.m[(size_t)n * G + grp];
+      for (int z = 20; z < 32; ++z) rb[z] = 0;
+    }
+    return;
+  }
   rec[j] = M.d[(size_t)n * nblk + blk];
   if (enc == HB_Q2) rec[bpg + j] = M.m[(size_t)n * nblk + blk];
 }
 
 int canonical_layout(int enc, int hidden, int ffn, CanonLayout* out) {
-  if (enc < HB_F16 || enc > HB_Q2 || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
+  if (enc < HB_F16 || enc > HB_Q2K || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
     return HB_EINVAL;
+  if (enc == HB_Q2K) {              // q, sc [N][K/16], d [N][K/256], dmin [N][K/256]; Q2 total
+    const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
+    auto align = [](uint64_t v) { return (v + 255) / 256 * 256; };
+    uint64_t off = 0;
+    for (int m = 0; m < 3; ++m) {
+      out->q[m] = off;
+      off = align(off + (uint64_t)N[m] * K[m] / 4);
+      out->sc[m] = off;
+      off = align(off + (uint64_t)N[m] * (K[m] / 16));
+      out->d[m] = off;
+      off = align(off + (uint64_t)N[m] * (K[m] / 256) * 2);
+      out->m[m] = off;
+      off = align(off + (uint64_t)N[m] * (K[m] / 256) * 2);
+    }
+    CanonLayout q2;
+    canonical_layout(HB_Q2, hidden, ffn, &q2);
+    out->total = std::max(off, q2.total);
+    return HB_OK;
+  }
+  for (int m = 0; m < 3; ++m) out->sc[m] = 0;
   const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
   const int bits = enc == HB_F16 ? 16 : enc == HB_Q8 ? 8 : enc == HB_Q4 ? 4 : 2;
   auto align = [](uint64_t v) { return (v + 255) / 256 * 256; };
@@ -109,6 +141,7 @@ int launch_repack_canonical(int enc, int hidden, int ffn, const uint8_t* src, ui
   long long most = 0;
   for (int m = 0; m < 3; ++m) {
     p.mat[m].q = src + C.q[m];
+    p.mat[m].sc = src + C.sc[m];
     p.mat[m].d = reinterpret_cast<const uint16_t*>(src + C.d[m]);
     p.mat[m].m = reinterpret_cast<const uint16_t*>(src + C.m[m]);
     p.mat[m].dq = dst + D.mat[m].q;
