@@ -75,9 +75,9 @@ enum { HB_F16 = 0, HB_Q8 = 1, HB_Q4 = 2, HB_Q2 = 3, HB_Q2K = 4 };
  * nibble scale, high nibble min), per super-block fp16 d and dmin:
  *   w = d * (sc_j & 15) * q - dmin * (sc_j >> 4),  q in [0, 3]   (2.625 bits/weight)
  * CANONICAL: per matrix q (as Q2), sc [N][K/16] bytes, d [N][K/256] fp16,
- * dmin [N][K/256] fp16 (hb_canonical_section sec 0..3), blob padded to the Q2
- * size.  DEVICE: the Q2 code layout; the 32-byte record of (unit, row) holds
- * d, dmin, sc[16].  The decode kernels form each weight in fp16 (two
+ * dmin [N][K/256] fp16 (hb_canonical_section sec 0..3).  DEVICE: the Q2 code
+ * layout; the 20-byte record of (unit, row) holds d, dmin, sc[16]; the blob is
+ * padded to the canonical size.  The decode kernels form each weight in fp16 (two
  * roundings) before the MMA; the batched tcgen05 path is not built for it (a
  * context with HB_Q2K runs every batch on the dequant-GEMV path).  A pair may
  * use HB_Q2K or HB_Q2, not both. */

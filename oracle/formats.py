@@ -21,7 +21,8 @@ d, m fp16, one per block.  Every value is an exact dyadic rational in fp64.
          sc_j (low nibble scale, high nibble min), per super-block fp16 d, dmin:
              w = d * (sc_j & 15) * q - dmin * (sc_j >> 4),  q in [0, 3]
          (2.625 bits/weight).  Packed with OUR canonical conventions (LSB-first,
-         row-major) rather than llama.cpp's interleaved qs order (R32).
+         row-major) rather than llama.cpp's interleaved qs order (DESIGN.md R32);
+         sections q, sc [n][k/16] bytes, d [n][k/256], dmin [n][k/256].
 
 CANONICAL blob (the interchange format the oracle reads and
 writes; the library converts it into its own device layout with
@@ -71,8 +72,7 @@ def expert_matrix_shapes(hidden: int, ffn: int):
 
 
 def blob_layout(enc: int, hidden: int, ffn: int):
-    """({mat: {section: (offset, nbytes)}}, total bytes) of one expert blob.
-    Q2K blobs are padded to the Q2 total (the same container size, R32)."""
+    """({mat: {section: (offset, nbytes)}}, total bytes) of one expert blob."""
     off = 0
     lay = {}
     for mat, (n, k) in enumerate(expert_matrix_shapes(hidden, ffn)):
@@ -80,8 +80,6 @@ def blob_layout(enc: int, hidden: int, ffn: int):
         for name, nbytes in matrix_sections(enc, n, k):
             lay[mat][name] = (off, nbytes)
             off = _align(off + nbytes)
-    if enc == Q2K:
-        off = max(off, blob_layout(Q2, hidden, ffn)[1])
     return lay, off
 
 

@@ -42,7 +42,21 @@ cudaError_t set_max_dyn_smem_impl(const void* kernel, int bytes) {
 int blob_layout(int enc, int hidden, int ffn, BlobLayout* out) {
   if (enc < HB_F16 || enc > HB_Q2K || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
     return HB_EINVAL;
-  if (enc == HB_Q2K) enc = HB_Q2;            // same codes, same 32-byte records (R32)
+  if (enc == HB_Q2K) {                       // Q2's codes, 20-byte records [d, dmin, sc16] (R32)
+    const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
+    auto align = [](uint64_t v) { return (v + 255) / 256 * 256; };
+    uint64_t off = 0;
+    for (int m = 0; m < 3; ++m) {
+      out->mat[m].q = off;
+      off = align(off + (uint64_t)N[m] * K[m] / 4);
+      out->mat[m].s = off;
+      off = align(off + (uint64_t)N[m] * (K[m] / 256) * 20);
+    }
+    CanonLayout C;
+    canonical_layout(HB_Q2K, hidden, ffn, &C);
+    out->total = std::max(off, C.total);       // the canonical blob's size
+    return HB_OK;
+  }
   // code section + one scale section per matrix (tile-major units, DESIGN.md
   // "Blob layout"); every section 256-byte aligned
   const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
@@ -294,7 +308,7 @@ int hb_blob_section(int enc, int hidden, int ffn, int mat, int sec, size_t* offs
   if (sec == 0) { *offset = L.mat[mat].q; *nbytes = (size_t)N * K * bits / 8; return HB_OK; }
   if (enc == HB_F16 || sec == 2) return fail(nullptr, HB_EINVAL, "section does not exist");
   *offset = L.mat[mat].s;
-  *nbytes = (size_t)N * (K / 32) * 2 * (enc == HB_Q2 || enc == HB_Q2K ? 2 : 1);
+  *nbytes = enc == HB_Q2K ? (size_t)N * (K / 256) * 20 : (size_t)N * (K / 32) * 2 * (enc == HB_Q2 ? 2 : 1);
   return HB_OK;
 }
 
@@ -415,7 +429,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   c->device = device;
   c->resident = resident;
   for (int e = 0; e < 4; ++e) {
-    blob_layout(e, k.hidden, k.ffn, &c->lay[e]);
+    blob_layout(kq && e == HB_Q2 ? HB_Q2K : e, k.hidden, k.ffn, &c->lay[e]);   // the Q2 slot
     c->bbytes[e] = c->lay[e].total;
   }
   auto bail = [&](int code, const std::string& m) {

@@ -193,9 +193,9 @@ template <> struct Enc<HB_Q8>  { static constexpr int BPG = 2, EPG = 64,  SB = 4
 template <> struct Enc<HB_Q4>  { static constexpr int BPG = 4, EPG = 128, SB = 8;  };
 template <> struct Enc<HB_Q2>  { static constexpr int BPG = 8, EPG = 256, SB = 32; };
 // HB_Q2K (R32), kernel-internal template value (the context stores it in the
-// Q2 slot): Q2's code layout, 32-byte records [d, dmin, sc[16], pad]
+// Q2 slot): Q2's code layout, 20-byte records [d, dmin, sc[16]] (2.625 bpw)
 constexpr int kEncQ2K = 4;
-template <> struct Enc<kEncQ2K> { static constexpr int BPG = 8, EPG = 256, SB = 32; };
+template <> struct Enc<kEncQ2K> { static constexpr int BPG = 8, EPG = 256, SB = 20; };
 
 __host__ __device__ constexpr int epg_of(int enc) {
   return enc == HB_F16 ? 32 : enc == HB_Q8 ? 64 : enc == HB_Q4 ? 128 : 256;

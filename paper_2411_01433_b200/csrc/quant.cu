@@ -154,7 +154,7 @@ __global__ void quant_q2k_kernel(const __half* __restrict__ w, int n, int k, uin
   const __half d16 = __float2half_rn(__fdiv_rn(smax, 15.0f));
   const __half dm16 = __float2half_rn(__fdiv_rn(mmax, 15.0f));
   const float d = __half2float(d16), dm = __half2float(dm16);
-  uint8_t* rec = ssec + (unit * 16 + row % 16) * 32;
+  uint8_t* rec = ssec + (unit * 16 + row % 16) * 20;        // 20-byte record
   reinterpret_cast<__half*>(rec)[0] = d16;
   reinterpret_cast<__half*>(rec)[1] = dm16;
   uint32_t words[16];
@@ -175,7 +175,6 @@ __global__ void quant_q2k_kernel(const __half* __restrict__ w, int n, int k, uin
       words[byte >> 2] |= c << (8 * (byte & 3) + 2 * (r & 3));
     }
   }
-  for (int z = 20; z < 32; ++z) rec[z] = 0;
   uint4* dst = reinterpret_cast<uint4*>(q + unit * 1024 + (row % 16) * 64);
 #pragma unroll
   for (int i = 0; i < 4; ++i)

@@ -69,16 +69,15 @@ __global__ void repack_kernel(const __grid_constant__ RepackParams p) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) base[16 * t + 4 * (j / 2) + 2 * h + (j % 2)] = src[2 * t + h];
   }
-  const int sb = 2 * bpg * (enc == HB_Q2 ? 2 : 1);
+  const int sb = p.enc == HB_Q2K ? 20 : 2 * bpg * (enc == HB_Q2 ? 2 : 1);
   uint16_t* rec = reinterpret_cast<uint16_t*>(M.ds + 16ull * sb * ((size_t)G * tile + grp) + sb * r);
-  if (p.enc == HB_Q2K) {            // record: d, dmin, sc[16] of the super-block (R32)
+  if (p.enc == HB_Q2K) {            // 20-byte record: d, dmin, sc[16] of the super-block (R32)
     uint8_t* rb = reinterpret_cast<uint8_t*>(rec);
     rb[4 + 2 * j] = M.sc[(size_t)n * (M.K / 16) + 2 * blk];
     rb[4 + 2 * j + 1] = M.sc[(size_t)n * (M.K / 16) + 2 * blk + 1];
     if (j == 0) {
       rec[0] = M.d[(size_t)n * G + grp];
       rec[1] = M.m[(size_t)n * G + grp];
-      for (int z = 20; z < 32; ++z) rb[z] = 0;
     }
     return;
   }
@@ -89,7 +88,7 @@ __global__ void repack_kernel(const __grid_constant__ RepackParams p) {
 int canonical_layout(int enc, int hidden, int ffn, CanonLayout* out) {
   if (enc < HB_F16 || enc > HB_Q2K || hidden <= 0 || ffn <= 0 || hidden % 256 || ffn % 256)
     return HB_EINVAL;
-  if (enc == HB_Q2K) {              // q, sc [N][K/16], d [N][K/256], dmin [N][K/256]; Q2 total
+  if (enc == HB_Q2K) {              // q, sc [N][K/16], d [N][K/256], dmin [N][K/256]
     const int N[3] = {ffn, ffn, hidden}, K[3] = {hidden, hidden, ffn};
     auto align = [](uint64_t v) { return (v + 255) / 256 * 256; };
     uint64_t off = 0;
@@ -103,9 +102,7 @@ int canonical_layout(int enc, int hidden, int ffn, CanonLayout* out) {
       out->m[m] = off;
       off = align(off + (uint64_t)N[m] * (K[m] / 256) * 2);
     }
-    CanonLayout q2;
-    canonical_layout(HB_Q2, hidden, ffn, &q2);
-    out->total = std::max(off, q2.total);
+    out->total = off;
     return HB_OK;
   }
   for (int m = 0; m < 3; ++m) out->sc[m] = 0;

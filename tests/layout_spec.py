@@ -27,9 +27,9 @@ of the group, fp16) and, for Q2, another 2*BPG bytes of m:
     scale record of (n, grp) at 16*SB*(G*tile + grp) + SB*r
         d of block j at +2*j,  m of block j at +2*BPG + 2*j   (Q2)
 
-Q2K (R32): the codes as Q2; the 32-byte record of (n, grp) (one
+Q2K (R32): the codes as Q2; the 20-byte record of (n, grp) (one
 super-block of 256) holds d (fp16) at +0, dmin (fp16) at +2 and the 16
-sub-block bytes sc_j at +4 + j, bytes +20..+31 zero.
+sub-block bytes sc_j at +4 + j; the blob is padded to the canonical size.
 
 Per matrix (W1, W3, W2): a code section then (quantised) one scale section,
 each 256-byte aligned.  The total size equals the canonical blob's.
@@ -53,7 +53,9 @@ def bpg(enc):
 
 
 def scale_record_bytes(enc):
-    return 0 if enc == F16 else 2 * bpg(enc) * (2 if enc in (Q2, Q2K) else 1)
+    if enc == Q2K:
+        return 20
+    return 0 if enc == F16 else 2 * bpg(enc) * (2 if enc == Q2 else 1)
 
 
 def sections(enc, hidden, ffn):
@@ -65,8 +67,12 @@ def sections(enc, hidden, ffn):
         s = None
         if enc != F16:
             s = off
-            off = _align(off + n * (k // 32) * 2 * (2 if enc in (Q2, Q2K) else 1))
+            off = _align(off + n * (k // EPG[enc]) * scale_record_bytes(enc))
         out.append((q, s))
+    if enc == Q2K:                    # padded to the canonical blob's size
+        canon = sum(_align(n * k // 4) + _align(n * k // 16) + 2 * _align(n * k // 128)
+                    for n, k in ((ffn, hidden), (ffn, hidden), (hidden, ffn)))
+        off = max(off, canon)
     return out, off
 
 
@@ -120,7 +126,7 @@ def device_matrix(enc, codes_or_f16, d16, m16, n, k):
         scb, dd, dm = d16
         G = k // 256
         grp = np.arange(G)[None, :]
-        rec = 16 * 32 * (G * (N // TILE) + grp) + 32 * (N % TILE)
+        rec = 16 * 20 * (G * (N // TILE) + grp) + 20 * (N % TILE)
         for arr, o in ((dd, 0), (dm, 2)):
             bits = np.ascontiguousarray(arr, dtype=np.float16).view(np.uint16)
             sc[(rec + o).ravel()] = (bits & 0xFF).astype(np.uint8).ravel()

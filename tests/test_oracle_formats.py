@@ -260,8 +260,8 @@ def test_q2k_quantiser_exact_when_representable():
 
 
 def test_q2k_quantiser_roundtrip_bound_and_container():
-    """|x - deq| <= dl_j / 2 + the scale roundings, on random rows; a Q2K blob
-    has the Q2 container size (R32)."""
+    """|x - deq| <= dl_j / 2 + the scale roundings, on random rows; the blob
+    size is the closed form of its four sections."""
     rng = np.random.default_rng(11)
     w = (rng.standard_normal((32, 512)) * 0.02).astype(np.float16)
     codes, sc, d16, dm16 = fm.quantize_q2k(w)
@@ -281,4 +281,7 @@ def test_q2k_quantiser_roundtrip_bound_and_container():
     slack = np.repeat(np.repeat(np.maximum(d16, dm16).astype(np.float64), 256, axis=1), 1, axis=0)
     assert np.all(err[inside] <= 0.5 * dl[inside] + 1e-12)
     assert np.all(err <= 0.5 * dl + 3 * slack + 1e-12)
-    assert fm.blob_bytes(fm.Q2K, 4096, 14336) == fm.blob_bytes(fm.Q2, 4096, 14336)
+    # 2.625 bits per weight: q + sc + d + dmin, each section 256-aligned
+    n_k = [(14336, 4096), (14336, 4096), (4096, 14336)]
+    assert fm.blob_bytes(fm.Q2K, 4096, 14336) == sum(n * k // 4 + n * k // 16 + 2 * (n * k // 128)
+                                                      for n, k in n_k)
