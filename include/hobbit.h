@@ -77,10 +77,9 @@ enum { HB_F16 = 0, HB_Q8 = 1, HB_Q4 = 2, HB_Q2 = 3, HB_Q2K = 4 };
  * CANONICAL: per matrix q (as Q2), sc [N][K/16] bytes, d [N][K/256] fp16,
  * dmin [N][K/256] fp16 (hb_canonical_section sec 0..3).  DEVICE: the Q2 code
  * layout; the 20-byte record of (unit, row) holds d, dmin, sc[16]; the blob is
- * padded to the canonical size.  The decode kernels form each weight in fp16 (two
- * roundings) before the MMA; the batched tcgen05 path is not built for it (a
- * context with HB_Q2K runs every batch on the dequant-GEMV path).  A pair may
- * use HB_Q2K or HB_Q2, not both. */
+ * padded to the canonical size.  The kernels (GEMV and tcgen05) form each
+ * weight in fp16 (two roundings) before the MMA.  A pair may use HB_Q2K or
+ * HB_Q2, not both. */
 /* Precision decision of one selected expert. */
 enum { HB_HIGH = 0, HB_LOW = 1, HB_SKIP = 2 };
 #define HB_ENC_NONE 255

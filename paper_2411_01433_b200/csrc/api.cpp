@@ -490,7 +490,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
     // K3 scratch: X and h of every vjob3 in canonical blocks (rows padded to 16)
     const int max_v3 = c->max_jobs + (c->max_slots + kK3MaxN - 1) / kK3MaxN;
     const size_t rows = (size_t)c->max_slots + 16 * (size_t)max_v3;
-    if (B > 1 && max_v3 <= kK3MaxV3 && !kq) {       // no tcgen05 path for Q2K
+    if (B > 1 && max_v3 <= kK3MaxV3) {
       if (!dm((void**)&c->k3_xg, rows * H * 2) || !dm((void**)&c->k3_hB, rows * F * 2) ||
           !dm((void**)&c->k3_tab, sizeof(K3Table)) ||
           (resident && !dm((void**)&c->k3_tmap, sizeof(CUtensorMap) * (size_t)L * E * 24)))
@@ -716,8 +716,8 @@ int hb_register_expert(hb_ctx* c, int layer, int expert, int enc, const void* bl
       for (int i = 0; i < 3; ++i) {
         const MatLayout& ML = c->lay[enc].mat[i];
         const int rc = enc == HB_F16 ? k3_encode_f16_map(&m[i], dblob + ML.q, rows[i], cols[i])
-                                     : k3_encode_q_maps(&m[i], &m[3 + i], enc, dblob + ML.q, dblob + ML.s,
-                                                        rows[i], cols[i]);
+                                     : k3_encode_q_maps(&m[i], &m[3 + i], enc_ext, dblob + ML.q,
+                                                        dblob + ML.s, rows[i], cols[i]);
         if (rc) return fail(c, HB_ECUDA, "cuTensorMapEncodeTiled failed");
       }
       CUDA_TRY(c, cudaMemcpy(c->k3_tmap + (((size_t)layer * k.n_experts + expert) * 4 + enc) * 6, m,
@@ -993,6 +993,7 @@ static void launch_batched(hb_ctx* c, int layer, const void* x, void* y, cudaStr
   kp.has_f16 = c->cfg.hi_enc == HB_F16 || c->cfg.lo_enc == HB_F16;
   kp.has_q = c->cfg.hi_enc != HB_F16 || c->cfg.lo_enc != HB_F16;
   kp.ts = c->k3_ts;
+  kp.kq = c->kq;
   cudaEvent_t* ev = nullptr;
   if (c->prof_n < c->prof_max) ev = &c->prof_ev[3 * c->prof_n++];
   launch_k3_prep(kp, (const __half*)x, s);

@@ -113,6 +113,11 @@ __device__ __forceinline__ float lds_half(uint32_t a) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
   return __half2float(__ushort_as_half(v));
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
@@ -840,6 +845,21 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
     r[0][0] += __uint_as_float((w[0][0].x ^ w[0][1].y) & 0x3F800000u);
     return;
 #endif
+    // Q2K: the records of rows g and g + 8 once per unit (d, dmin, 16 sub-block bytes)
+    float q2d[NMAT][2], q2m[NMAT][2];
+    uint32_t q2s[NMAT][2][4];
+    if constexpr (ENC == kEncQ2K) {
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const uint32_t rec = sst + m * NU * 16 * SB + (g + 8 * h2) * SB;
+          q2d[m][h2] = lds_half(rec);
+          q2m[m][h2] = lds_half(rec + 2);
+#pragma unroll
+          for (int wv = 0; wv < 4; ++wv) q2s[m][h2][wv] = lds_u32(rec + 4 + 4 * wv);
+        }
+    }
 #pragma unroll
     for (int blk = 0; blk < BPG; ++blk) {
       uint4 xb, xl;
@@ -879,14 +899,14 @@ __device__ HB_RUN_ATTR void run(const GemvParams& p, const VJob& vj, int cum, in
           // Q2K (R32): lane t's pairs lie in sub-block 2 blk + t / 2 of rows g,
           // g + 8; w = d (sc & 15) q - dmin (sc >> 4) is formed in fp16 (scale
           // products rounded once, then one fma) and fed to the MMA directly
-          const uint32_t sd = sst + m * NU * 16 * SB;
-          const uint32_t rg = sd + g * SB, rh = sd + (g + 8) * SB;
-          const int sub = 2 * blk + (t >> 1);
-          const uint32_t cg = lds_u8(rg + 4 + sub), ch = lds_u8(rh + 4 + sub);
-          const uint32_t Dg = f2h2u(lds_half(rg) * (float)(cg & 15u));
-          const uint32_t Mg = f2h2u(-lds_half(rg + 2) * (float)(cg >> 4));
-          const uint32_t Dh = f2h2u(lds_half(rh) * (float)(ch & 15u));
-          const uint32_t Mh = f2h2u(-lds_half(rh + 2) * (float)(ch >> 4));
+          // sub-block 2 blk + t / 2: byte 2 (blk % 2) + t / 2 of word blk / 2
+          const int sh = 8 * (2 * (blk & 1) + (t >> 1));
+          const uint32_t cg = (q2s[m][0][blk >> 1] >> sh) & 0xFFu;
+          const uint32_t ch = (q2s[m][1][blk >> 1] >> sh) & 0xFFu;
+          const uint32_t Dg = f2h2u(q2d[m][0] * (float)(cg & 15u));
+          const uint32_t Mg = f2h2u(-q2m[m][0] * (float)(cg >> 4));
+          const uint32_t Dh = f2h2u(q2d[m][1] * (float)(ch & 15u));
+          const uint32_t Mh = f2h2u(-q2m[m][1] * (float)(ch >> 4));
           uint32_t Ag[4], Ah[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {

@@ -208,6 +208,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ uint16_t lds16(uint32_t a) {
   uint16_t v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
@@ -333,6 +338,22 @@ __device__ __forceinline__ void dequant16(int enc, uint32_t code, uint32_t sc, u
 
 __device__ __forceinline__ int scale_rec(int enc) {   // SB, bytes per (unit, row)
   return enc == HB_Q8 ? 4 : enc == HB_Q4 ? 8 : enc == HB_Q2 ? 32 : 0;
+}
+// HB_Q2K (R32) in the Q2 slot: Q2's codes, 20-byte records
+// [d, dmin, sc16]; chunk t of blocks j0, j0 + 1 lies in sub-blocks
+// 2 j + t / 2.  w = q (d sc_lo) - dmin sc_hi with both scales rounded once
+// to fp16 (R34), then the one fp16 fma of q2_chunk.
+__device__ __forceinline__ void dequant16_q2k(uint32_t code, uint32_t rec, int j0, int t, uint4& w0,
+                                              uint4& w1) {
+  const float d = __half2float(__ushort_as_half(lds16(rec)));
+  const float dm = __half2float(__ushort_as_half(lds16(rec + 2)));
+  const uint32_t c0 = lds8(rec + 4 + 2 * j0 + (t >> 1));
+  const uint32_t c1 = lds8(rec + 4 + 2 * j0 + 2 + (t >> 1));
+  const __half2 d0 = __float2half2_rn(d * (float)(c0 & 15u)), m0 = __float2half2_rn(-dm * (float)(c0 >> 4));
+  const __half2 d1 = __float2half2_rn(d * (float)(c1 & 15u)), m1 = __float2half2_rn(-dm * (float)(c1 >> 4));
+  const uint32_t v = lds32(code);
+  w0 = q2_chunk(prmt(v, 0, 0x4040), prmt(v, 0, 0x4242), d0, m0);
+  w1 = q2_chunk(prmt(v, 0, 0x4141), prmt(v, 0, 0x4343), d1, m1);
 }
 // raw units per (matrix, 16-row tile) in one raw slot: 16 KB of codes per slot
 template <int NMAT>
@@ -490,7 +511,8 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const Item I = item_of<NMAT>(p, it, v0);
         const int enc = I.v->enc;
-        const int epg = epg_of_enc(enc), ru = raw_units<NMAT>(enc, Kitem), sb = scale_rec(enc);
+        const int epg = epg_of_enc(enc), ru = raw_units<NMAT>(enc, Kitem);
+        const int sb = (p.kq && enc == HB_Q2) ? 20 : scale_rec(enc);
         const int G = Kdim / epg;
         const int nraw = Kitem / (ru * epg);
         const int g0 = I.ks * (Kitem / epg);
@@ -551,7 +573,9 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const Item I = item_of<NMAT>(p, it, v0);
       const int enc = I.v->enc;
-      const int epg = epg_of_enc(enc), ru = raw_units<NMAT>(enc, Kitem), sb = scale_rec(enc);
+      const int epg = epg_of_enc(enc), ru = raw_units<NMAT>(enc, Kitem);
+      const bool q2k = p.kq && enc == HB_Q2;
+      const int sb = q2k ? 20 : scale_rec(enc);
       const int nraw = Kitem / (ru * epg);
       const int cpr = ru * epg / kBK;               // canonical stages per raw slot
       for (int r = 0; r < nraw; ++r) {
@@ -571,8 +595,9 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
           for (int m = 0; m < NMAT; ++m) {
             const int su = u * 8 + tl;                // raw slot [m][u][tile]
             const uint32_t code = raw + m * (8 * ru * 1024) + su * 1024 + rr * 64 + 16 * t + coff;
-            const uint32_t sc = raw + kRawCode + m * (8 * ru * 16 * sb) + su * 16 * sb + rr * sb + soff;
-            dequant16(enc, code, sc, w[m][0], w[m][1]);
+            const uint32_t sc = raw + kRawCode + m * (8 * ru * 16 * sb) + su * 16 * sb + rr * sb;
+            if (q2k) dequant16_q2k(code, sc, 2 * (c & 3), t, w[m][0], w[m][1]);
+            else dequant16(enc, code, sc + soff, w[m][0], w[m][1]);
           }
           if (lane == 0) bar_wait(can_empty(cs), cph ^ 1);
           __syncwarp();
@@ -890,8 +915,10 @@ int k3_encode_f16_map(CUtensorMap* out, const void* q, int n, int k) {
 // tile | group), box = 8 tiles x 1 unit.
 int k3_encode_q_maps(CUtensorMap* code, CUtensorMap* scale, int enc, const void* q, const void* s,
                      int n, int k) {
+  const bool q2k = enc == HB_Q2K;
+  if (q2k) enc = HB_Q2;                       // Q2's codes, 20-byte records
   const cuuint64_t G = (cuuint64_t)k / epg_of_enc(enc);
-  const cuuint64_t sb = enc == HB_Q8 ? 4 : enc == HB_Q4 ? 8 : 32;
+  const cuuint64_t sb = q2k ? 20 : enc == HB_Q8 ? 4 : enc == HB_Q4 ? 8 : 32;
   const cuuint64_t cd[4] = {64, 16, (cuuint64_t)n / 16, G};
   const cuuint64_t cs[3] = {64, G * 1024, 1024};
   const cuuint32_t cb[4] = {64, 16, 8, 1};

@@ -43,6 +43,7 @@ struct K3Params {
   const CUtensorMap* tmap;       // [E][4 enc][6] tensor maps of this layer's blobs:
                                  //   F16: [0..2] W1, W3, W2; Q: [0..2] codes, [3..5] scales
   int has_f16, has_q;            // encodings in the pair (launch k3d_kernel / k3_kernel)
+  int kq;                        // the Q2 slot holds HB_Q2K blobs (20-byte records, R32)
   int ts;                        // quantised items: A operand dequantised into TMEM (tcgen05.st,
                                  // A-from-TMEM MMA) instead of shared memory (HB_K3_TS)
 };

@@ -4,10 +4,10 @@ DESIGN.md R32/R33) through the C-ABI against the oracle.
   * quantiser bytes three ways (library quantiser; hb_repack_canonical of the
     oracle's canonical blob; tests/layout_spec.py on the CPU);
   * decode-layer parity for the pairs F16/Q2K and Q8/Q2K at the tiny shape
-    (B = 1, 5, 16; the GEMV path takes every batch, no tcgen05 path for Q2K)
-    and at the full Mixtral shape; bar 1e-3 normwise: the kernels form each
-    Q2K weight in fp16 (the scale products and the fma each round once) where
-    the other encodings keep exact integer codes (R34);
+    (B = 1, 5, 16 on the GEMV path; B = 4, 16, 40 on the tcgen05 path) and at
+    the full Mixtral shape; bar 1e-3 normwise: the kernels form each Q2K
+    weight in fp16 (the scale products and the fma each round once) where the
+    other encodings keep exact integer codes (R34);
   * the offload path: cache events reported with HB_Q2K, bit-exact with O9/O10.
 """
 import numpy as np
@@ -58,6 +58,23 @@ def test_q2k_layer_parity_tiny(hi, B):
                 want = 255 if dec == rt.SKIP else (hi if dec == rt.HIGH else fm.Q2K)
                 assert served[b][i] == want
             assert rel_err(y[b], ref[b])[0] <= TOL_Q2K, b
+
+
+@pytest.mark.parametrize("hi", [fm.F16, fm.Q8], ids=["F16-Q2K", "Q8-Q2K"])
+@pytest.mark.parametrize("B", [4, 16, 40])
+def test_q2k_batched_tcgen05_parity(hi, B):
+    """The tcgen05 grouped GEMM (K3) with Q2K items: the converters dequantise
+    the 20-byte records (R34) into the A operand."""
+    sh = sg.TINY
+    ctx = _resident(sh, [0], hi, fm.Q2K, max_batch=40, batched_min=4)
+    store = OracleStore(sh)
+    x16 = sg.hidden_states(sh, 50 + B, 0, batch=B)
+    y = _run(ctx, 0, x16)
+    ref, routes = om.moe_layer(x16, sg.router_weights(sh, 0), store, 0, 2, 0.6, 0.9, hi, fm.Q2K)
+    _check_routes(ctx, routes, B, 2)
+    assert sum(d == rt.LOW for r in routes for d in r.decisions) >= 1
+    for b in range(B):
+        assert rel_err(y[b], ref[b])[0] <= TOL_Q2K, b
 
 
 def test_q2k_layer_parity_full_size():

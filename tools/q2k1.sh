@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests/test_gpu_q2k.py -x -q 2>&1 | tail -5
-MODELS="mixtral:f16q2k mixtral:f16q2 mixtral:q8q2k mixtral:q8q2" bash tools/cmp.sh
+MODELS="mixtral:f16q2k mixtral:q8q2k" bash tools/cmp.sh
