@@ -129,7 +129,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------ our arm
 def build_model(h, sg, fm, shape, hi, lo, rank, world, dev, t1=0.6, t2=0.9, max_batch=1, layers=None,
-                tp_rank=0, tp_world=1):
+                tp_rank=0, tp_world=1, cfg_extra=None):
     """Random-init weights of the shape (seeded generator), quantised on the
     GPU and registered resident.  EP (world > 1): this rank's experts
     (e % world == rank).  TP-within-expert (tp_world > 1): every expert, rows
@@ -139,7 +139,8 @@ def build_model(h, sg, fm, shape, hi, lo, rank, world, dev, t1=0.6, t2=0.9, max_
     Fs = F // tp_world
     cfg = h.default_config(n_layers=shape.n_layers, n_experts=shape.n_experts, top_k=shape.top_k,
                            hidden=H, ffn=Fs, hi_enc=hi, lo_enc=lo, t1=t1,
-                           t2=t2, max_batch=max_batch, rank=rank, world=world)
+                           t2=t2, max_batch=max_batch, rank=rank, world=world,
+                           **(cfg_extra or {}))
     ctx = h.Context(cfg, dev)
     tmp = [torch.empty(n * k, dtype=torch.float16, device="cuda")
            for n, k in ((F, H), (F, H), (H, F))]

@@ -36,7 +36,8 @@ def main():
     ap.add_argument("--model", default="mixtral")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--paths", default="k2,k3")
+    ap.add_argument("--paths", default="k2,k3",
+                    help="k2 (GEMV), k3 (tcgen05 GEMM), ts (token-sharded EP at world 1)")
     args = ap.parse_args()
     batches = [int(b) for b in args.batches.split(",")]
     shape = {"mixtral": sg.MIXTRAL, "phi": sg.PHI}[args.model]
@@ -45,6 +46,15 @@ def main():
     torch.cuda.set_device(0)
     ctx, blobs = bench.build_model(h, sg, None, shape, hi, lo, 0, 1, 0, max_batch=max(batches),
                                    layers=L)
+    ctx_ts = None
+    if "ts" in args.paths.split(","):
+        # token-sharded EP context at world 1: dispatch into the
+        # local block, the owner batch through K3, combine -- the overhead of
+        # the token-sharded path against the plain batched forward
+        ctx_ts, blobs_ts = bench.build_model(h, sg, None, shape, hi, lo, 0, 1, 0,
+                                             max_batch=max(batches), layers=L,
+                                             cfg_extra={"token_sharded": 1})
+        ctx_ts.set_batched_min(1)
     peak, peak_kind = bench.peaks()
     mats = {}
     for enc in (hi, lo):
@@ -66,12 +76,14 @@ def main():
                                        for l in range(L)])).cuda()
         Y = torch.empty(L, B, Hd, dtype=torch.float32, device="cuda")
         for path in args.paths.split(","):
-            if path == "k3" and B > 1:
-                ctx.set_batched_min(1)
-            elif path == "k3":
+            if path in ("k3", "ts") and B == 1:
                 continue
-            else:
+            if path == "k3":
+                ctx.set_batched_min(1)
+            elif path == "k2":
                 ctx.set_batched_min(0)
+            else:
+                ctx.set_batched_min(1)         # bytes from the plain K3 forward's decisions
             # decisions -> algorithmic bytes / flops of one step
             a_bytes = b_bytes = 0
             flops = 0
@@ -87,11 +99,14 @@ def main():
                     a_bytes += sum(mats[e][0] for _, e in jobs) + 2 * B * Hd + 2 * nsel * F
                     b_bytes += sum(mats[e][1] for _, e in jobs) + 2 * nsel * F + 4 * B * Hd
                     flops += 2 * 3 * Hd * F * nsel
+            cx = ctx_ts if path == "ts" else ctx
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(stream):
+                for l in range(L):                 # warm (allocations) outside the capture
+                    cx.forward(l, X[l], Y[l], stream=stream)
                 with torch.cuda.graph(g, stream=stream):
                     for l in range(L):
-                        ctx.forward(l, X[l], Y[l], stream=stream)
+                        cx.forward(l, X[l], Y[l], stream=stream)
                 for _ in range(args.warmup):
                     g.replay()
                 torch.cuda.synchronize()
@@ -102,11 +117,11 @@ def main():
                 e1.record(stream)
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / args.steps
-                ctx.profile(L)
+                cx.profile(L)
                 for l in range(L):
-                    ctx.forward(l, X[l], Y[l], stream=stream)
-                prof = ctx.profile_read()
-                ctx.profile(0)
+                    cx.forward(l, X[l], Y[l], stream=stream)
+                prof = cx.profile_read()
+                cx.profile(0)
             ka = sum(p[0] for p in prof)
             kb = sum(p[1] for p in prof)
             out = {"B": B, "path": path, "layers": L, "pair": args.pair, "model": args.model,
