@@ -119,11 +119,12 @@ typedef struct {
   int token_sharded;                /* resident mode, strict.  1: token-sharded expert
                                        parallelism: each rank passes ITS OWN
                                        max_batch tokens; the router runs on them, every
-                                       non-skipped selection is sent (x row + hb_ts_meta) to the
-                                       rank owning the expert (e % world) in a fixed-capacity slot
-                                       (C = max_batch * top_k rows per peer), the owner computes
-                                       its received rows as one batch and sends the gate-weighted
-                                       outputs back, and y[b] = the sum of the token's k rows.
+                                       token's non-skipped selections go to the ranks owning their
+                                       experts (e % world): one row (x + hb_ts_meta) per (token,
+                                       owner) in a fixed-capacity block (C = max_batch rows per
+                                       peer); the owner computes its received rows as one batch and
+                                       sends each row's gate-weighted expert sum back; y[b] = the
+                                       sum of the token's returned rows.
                                        moe_layer_forward does the two exchanges with NCCL
                                        (hb_nccl_init) -- for world 1 without NCCL, locally; the
                                        staged calls hb_ts_dispatch / hb_ts_compute / hb_ts_combine
@@ -160,14 +161,15 @@ typedef struct {
   int32_t victim;                   /* evicted key layer*E+expert, or -1 */
 } hb_event;
 
-/* Token-sharded EP (hb_config.token_sharded): the record that travels with
- * each dispatched selection (the x row travels in a parallel rows buffer). */
+/* Token-sharded EP (hb_config.token_sharded): one dispatched ROW = one source
+ * token's selections owned by one rank (the token's x row travels once per
+ * owner in a parallel rows buffer). */
 typedef struct {
-  int32_t token;                    /* source token index, -1 = empty slot */
-  int32_t expert;                   /* e_i (owned by the receiving rank) */
-  uint8_t prec;                     /* HB_HIGH / HB_LOW */
-  uint8_t pad[3];
-  float gate;                       /* G(x)_{e_i} computed by the source's router */
+  int32_t token;                    /* source token index, -1 = empty row */
+  int32_t n;                        /* selections of the token this rank owns (1..top_k) */
+  int32_t expert[8];                /* their experts e_i, in rank order */
+  uint8_t prec[8];                  /* HB_HIGH / HB_LOW */
+  float gate[8];                    /* G(x)_{e_i} computed by the source's router */
 } hb_ts_meta;
 
 typedef struct hb_ctx hb_ctx;
@@ -309,16 +311,17 @@ int hb_get_events(hb_ctx* ctx, hb_event* out, int cap);
 /* Token-sharded EP, staged (hb_config.token_sharded = 1).
  * Buffers are device memory owned by the caller, laid out per peer rank r:
  * meta [world][C] hb_ts_meta, rows [world][C][hidden] fp16, ret [world][C][hidden]
- * fp32, C = max_batch * top_k; hb_ts_buffer_bytes gives the sizes.
+ * fp32, C = max_batch; hb_ts_buffer_bytes gives the sizes.
  *  hb_ts_dispatch: routes x [batch, hidden] (this rank's tokens, exact decisions)
- *    and writes block r of meta_send / rows_send with the selections owned by
- *    rank r (empty slots: token = -1).  The caller then sends block r to rank r
+ *    and writes block r of meta_send / rows_send: one row per token with
+ *    selections owned by rank r, tokens in order (empty rows: token = -1).  The caller then sends block r to rank r
  *    (all-to-all) and receives block r from rank r into meta_recv / rows_recv.
- *  hb_ts_compute: the received rows as one batch (each row's selection, Eq. 1
- *    terms g * E_e(x) of the source token) -> ret_send block r = the rows that
- *    came from rank r.  The caller returns block r to rank r (all-to-all).
+ *  hb_ts_compute: the received rows as one batch (each row's selections: the
+ *    Eq. 1 terms sum_i g_i E_{e_i}(x) this rank owns) -> ret_send block r = the
+ *    rows that came from rank r.  The caller returns block r to rank r (all-to-all).
  *  hb_ts_combine: y [batch, hidden] fp32 <- per token the sum of its returned
- *    rows (rank order), NaN rows for non-finite x (R28).  Needs the dispatch of
+ *    rows (owners in the order of the token's selections), NaN rows for
+ *    non-finite x (R28).  Needs the dispatch of
  *    the same batch on this context just before.
  * Errors: HB_ESTATE if the context is not token-sharded; HB_EINVAL on bad
  * sizes / pointers. */

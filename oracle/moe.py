@@ -99,44 +99,50 @@ def tp_slice(w1: np.ndarray, w3: np.ndarray, w2: np.ndarray, tp_rank: int, tp_wo
 
 
 def ts_dispatch_plan(routes, world: int, capacity: int):
-    """Token-sharded EP, dispatch side: every non-skipped
-    selection (token b, rank i) goes to the owner of its expert, owner(e) =
-    e mod world, at the next free slot of that destination, selections taken
-    in (token, rank) order.  Returns pos[b][i] = dest * capacity + slot or -1,
-    and per destination the list of (token, expert, decision, gate)."""
+    """Token-sharded EP, dispatch side: a token's non-skipped
+    selections go to the owners of their experts, owner(e) = e mod world;
+    one ROW per (token, owner) holds the token's selections that owner has
+    (rank order); the rows of an owner are in token order.  Returns pos[b][i]
+    = dest * capacity + row of selection i's owner (-1 for Skip) and per
+    destination the list of rows (token, [(expert, decision, gate), ...])."""
     pos = [[-1] * len(r.experts) for r in routes]
     sent = [[] for _ in range(world)]
     for b, r in enumerate(routes):
+        rows = {}
         for i, (e, g, d) in enumerate(zip(r.experts, r.gates, r.decisions)):
             if d == SKIP:
                 continue
             q = owner(e, world)
-            if len(sent[q]) >= capacity:
-                raise ValueError("token-sharded capacity exceeded")
-            pos[b][i] = q * capacity + len(sent[q])
-            sent[q].append((b, e, d, g))
+            if q not in rows:
+                if len(sent[q]) >= capacity:
+                    raise ValueError("token-sharded capacity exceeded")
+                rows[q] = len(sent[q])
+                sent[q].append((b, []))
+            sent[q][rows[q]][1].append((e, d, g))
+            pos[b][i] = q * capacity + rows[q]
     return pos, sent
 
 
 def ts_owner_rows(x_rows: np.ndarray, records, store: ExpertStore, layer: int, hi_enc: int,
                   lo_enc: int) -> np.ndarray:
-    """Token-sharded EP, owner side: each received row is one term of Eq. 1,
-    g * E_e(x) with the source's gate and the strict served encoding."""
+    """Token-sharded EP, owner side: each received row is the sum of the Eq. 1
+    terms g * E_e(x) of its selections (the source's gates, strict encodings)."""
     out = np.zeros((len(records), x_rows.shape[1]), dtype=np.float64)
-    for j, (_, e, d, g) in enumerate(records):
-        w1, w3, w2 = store.get(layer, e, served_encoding_strict(d, hi_enc, lo_enc))
-        out[j] = g * expert_ffn(w1, w3, w2, x_rows[j].astype(np.float64))
+    for j, (_, sels) in enumerate(records):
+        x = x_rows[j].astype(np.float64)
+        for e, d, g in sels:
+            w1, w3, w2 = store.get(layer, e, served_encoding_strict(d, hi_enc, lo_enc))
+            out[j] += g * expert_ffn(w1, w3, w2, x)
     return out
 
 
 def ts_combine(pos, returned: np.ndarray, H: int) -> np.ndarray:
-    """Token-sharded EP, source side: y[b] = sum over the token's selections
-    (rank order) of its returned rows (returned[dest * capacity + slot])."""
+    """Token-sharded EP, source side: y[b] = the sum of the token's returned
+    rows, each owner's row once (returned[dest * capacity + row])."""
     y = np.zeros((len(pos), H), dtype=np.float64)
     for b, row in enumerate(pos):
-        for p_ in row:
-            if p_ >= 0:
-                y[b] += returned[p_]
+        for p_ in dict.fromkeys(p for p in row if p >= 0):
+            y[b] += returned[p_]
     return y
 
 

@@ -130,7 +130,7 @@ struct hb_ctx {
   bool kq = false;                        // the Q2 slot holds HB_Q2K blobs (R32)
   // token-sharded EP (hb_config.token_sharded)
   bool ts = false;
-  int ts_C = 0;                           // rows per (source, destination) = max_batch * top_k
+  int ts_C = 0;                           // rows per (source, destination) = max_batch
   hb_decision* ts_dec = nullptr;          // local decisions [max_batch][k]
   int* ts_pos = nullptr;                  // [max_batch][k] dest * C + position or -1
   int* ts_rowbad = nullptr;               // [max_batch]
@@ -595,7 +595,7 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   }
   if (k.token_sharded) {
     c->ts = true;
-    c->ts_C = k.max_batch * K;
+    c->ts_C = k.max_batch;
     const size_t nr = (size_t)k.world * c->ts_C;
     bool tok = dm((void**)&c->ts_dec, sizeof(hb_decision) * k.max_batch * K) &&
                dm((void**)&c->ts_pos, sizeof(int) * k.max_batch * K) &&

@@ -214,16 +214,16 @@ void launch_router(const RouterParams& p, cudaStream_t s);
 
 // Token-sharded expert parallelism (router.cu): the tokens of
 // a layer are split over the ranks; each rank routes its own tokens, sends
-// every non-skipped selection (x row + this record) to the rank owning the
-// expert (e % R), computes the selections it received as a batch of rows with
-// one selection each, and sends the gate-weighted outputs back, where each
-// token sums its k contributions.  Fixed capacity C rows per (source, dest):
-// no counts exchange, no host sync.
+// one row per (token, owner rank) -- x and the token's selections that rank
+// owns -- computes the rows it received as one batch, and sends each row's
+// gate-weighted expert sum back, where each token sums its rows.  Fixed
+// capacity C = max_batch rows per (source, dest): no counts exchange, no host
+// sync.
 struct TsParams {
   const hb_decision* dec;      // local decisions [B][k] (the router's)
   const __half* x;             // local x [B][H]
   int B, k, H, R, C;
-  int* pos;                    // [B][k] dest * C + position, or -1 (Skip)
+  int* pos;                    // [B][k] row dest * C + position of the selection's owner, or -1
   hb_ts_meta* meta_send;       // [R][C]
   __half* rows_send;           // [R][C][H]
   const float* ret;            // [R][C][H] gate-weighted expert outputs of this rank's rows

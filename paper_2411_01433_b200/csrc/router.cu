@@ -1589,50 +1589,84 @@ void launch_router(const RouterParams& p, cudaStream_t s) {
 }
 
 // ------------------------------------------------ token-sharded EP (f3)
-// One CTA per local selection j = b*k + i: its slot in the send buffer of the
-// owner rank (selections in (token, rank) order per destination: a prefix
-// count over the decisions, deterministic), the record and the x row.
+// One CTA per local token b: one row per owner rank of its non-skipped
+// selections (owners in the order of the token's selections).  The row of
+// (b, owner d) is d * C + (number of tokens before b with a selection owned by
+// d): a prefix count over the decisions, deterministic.  The row carries the
+// token's selections owned by d (rank order) and its x.
 __global__ void __launch_bounds__(128) ts_pack_kernel(const __grid_constant__ TsParams p) {
-  const int j = blockIdx.x, tid = threadIdx.x;
-  __shared__ int s_pos;
-  const hb_decision d = p.dec[j];
-  const bool live = d.prec != HB_SKIP && d.expert >= 0;
-  if (tid == 0) {
-    int pos = -1;
-    if (live) {
+  const int b = blockIdx.x, tid = threadIdx.x;
+  __shared__ int s_dest[kMaxTopK], s_cnt[kMaxTopK], s_row[kMaxTopK];
+  __shared__ int s_nd;
+  if (tid == 0) {                                // the token's owners, in selection order
+    int nd = 0;
+    for (int i = 0; i < p.k; ++i) {
+      const hb_decision d = p.dec[b * p.k + i];
+      if (d.prec == HB_SKIP || d.expert < 0) continue;
       const int dest = d.expert % p.R;
-      int n = 0;
-      for (int q = 0; q < j; ++q) {
-        const hb_decision o = p.dec[q];
-        n += (o.prec != HB_SKIP && o.expert >= 0 && o.expert % p.R == dest);
-      }
-      pos = dest * p.C + n;
-      hb_ts_meta m;
-      m.token = j / p.k;
-      m.expert = d.expert;
-      m.prec = d.prec;
-      m.pad[0] = m.pad[1] = m.pad[2] = 0;
-      m.gate = d.gate;
-      p.meta_send[pos] = m;
+      bool seen = false;
+      for (int q = 0; q < nd; ++q) seen |= s_dest[q] == dest;
+      if (!seen) { s_cnt[nd] = 0; s_dest[nd++] = dest; }
     }
-    p.pos[j] = pos;
-    s_pos = pos;
+    s_nd = nd;
   }
   __syncthreads();
-  const int pos = s_pos;
-  if (pos < 0) return;
-  const uint4* src = reinterpret_cast<const uint4*>(p.x + (size_t)(j / p.k) * p.H);
-  uint4* dst = reinterpret_cast<uint4*>(p.rows_send + (size_t)pos * p.H);
-  for (int i = tid; i < p.H / 8; i += blockDim.x) dst[i] = src[i];
+  const int nd = s_nd;
+  // rows already taken in each owner's block: tokens before b with a selection it owns
+  for (int bb = tid; bb < b; bb += blockDim.x) {
+    unsigned mask = 0u;
+    for (int i = 0; i < p.k; ++i) {
+      const hb_decision o = p.dec[bb * p.k + i];
+      if (o.prec == HB_SKIP || o.expert < 0) continue;
+      for (int q = 0; q < nd; ++q) if (o.expert % p.R == s_dest[q]) mask |= 1u << q;
+    }
+    for (int q = 0; q < nd; ++q) if (mask >> q & 1u) atomicAdd(&s_cnt[q], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int q = 0; q < nd; ++q) {
+      s_row[q] = s_dest[q] * p.C + s_cnt[q];
+      hb_ts_meta m;
+      m.token = b;
+      m.n = 0;
+      for (int z = 0; z < kMaxTopK; ++z) { m.expert[z] = -1; m.prec[z] = HB_SKIP; m.gate[z] = 0.f; }
+      for (int i = 0; i < p.k; ++i) {
+        const hb_decision d = p.dec[b * p.k + i];
+        if (d.prec == HB_SKIP || d.expert < 0 || d.expert % p.R != s_dest[q]) continue;
+        m.expert[m.n] = d.expert;
+        m.prec[m.n] = d.prec;
+        m.gate[m.n] = d.gate;
+        m.n += 1;
+      }
+      p.meta_send[s_row[q]] = m;
+    }
+    for (int i = 0; i < p.k; ++i) {
+      const hb_decision d = p.dec[b * p.k + i];
+      int pos = -1;
+      if (d.prec != HB_SKIP && d.expert >= 0)
+        for (int q = 0; q < nd; ++q) if (d.expert % p.R == s_dest[q]) pos = s_row[q];
+      p.pos[b * p.k + i] = pos;
+    }
+  }
+  __syncthreads();
+  const uint4* src = reinterpret_cast<const uint4*>(p.x + (size_t)b * p.H);
+  for (int r = 0; r < nd; ++r) {
+    uint4* dst = reinterpret_cast<uint4*>(p.rows_send + (size_t)s_row[r] * p.H);
+    for (int i = tid; i < p.H / 8; i += blockDim.x) dst[i] = src[i];
+  }
 }
 
-// y[b] = sum over the token's selections (rank order) of the returned rows;
-// NaN for a token whose x was non-finite (R28)
+// y[b] = sum of the token's returned rows (one per owner, in the order of the
+// token's selections); NaN for a token whose x was non-finite (R28)
 __global__ void __launch_bounds__(256) ts_combine_kernel(const __grid_constant__ TsParams p) {
   const int b = blockIdx.x;
   const bool bad = p.rowbad && p.rowbad[b];
   int pos[kMaxTopK];
-  for (int i = 0; i < p.k; ++i) pos[i] = p.pos[b * p.k + i];
+  for (int i = 0; i < p.k; ++i) {
+    pos[i] = p.pos[b * p.k + i];
+    for (int q = 0; q < i; ++q)
+      if (pos[q] == pos[i]) pos[i] = -1;        // the owner's row counted once
+  }
   for (int c = threadIdx.x * 4; c < p.H; c += blockDim.x * 4) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = 0; i < p.k; ++i) {
@@ -1647,24 +1681,24 @@ __global__ void __launch_bounds__(256) ts_combine_kernel(const __grid_constant__
 }
 
 // Received rows -> the owner's batch: one CTA per row writes the row's k
-// decision records (its selection at rank 0, Skip after), its pair-permuted x
-// and block sums, zero rowbad and zero y; the last CTA builds the job table.
+// decision records (its n selections, then Skip), its pair-permuted x and
+// block sums, zero rowbad and zero y; the last CTA builds the job table.
 __global__ void __launch_bounds__(kRouterThreads)
 ts_jobs_kernel(const __grid_constant__ RouterParams p, const hb_ts_meta* meta, const __half* rows,
                float* y) {
   __shared__ BatchSmem sm;
   const int j = blockIdx.x, tid = threadIdx.x;
   if (tid < p.k) {
-    const hb_ts_meta m = meta[j];
+    const hb_ts_meta& m = meta[j];
     hb_decision d;
     d.token = j;
     d.sel_rank = (uint8_t)tid;
     d.served_enc = HB_ENC_NONE;
     d.hit = 0;
-    if (tid == 0 && m.token >= 0) {
-      d.expert = m.expert;
-      d.prec = m.prec;
-      d.gate = m.gate;
+    if (m.token >= 0 && tid < m.n) {             // the row's selections, then Skip
+      d.expert = m.expert[tid];
+      d.prec = m.prec[tid];
+      d.gate = m.gate[tid];
     } else {
       d.expert = -1;
       d.prec = HB_SKIP;
@@ -1690,7 +1724,7 @@ ts_jobs_kernel(const __grid_constant__ RouterParams p, const hb_ts_meta* meta, c
 }
 
 void launch_ts_pack(const TsParams& p, cudaStream_t s) {
-  if (p.B * p.k > 0) ts_pack_kernel<<<p.B * p.k, 128, 0, s>>>(p);
+  if (p.B > 0) ts_pack_kernel<<<p.B, 128, 0, s>>>(p);
 }
 void launch_ts_combine(const TsParams& p, cudaStream_t s) {
   if (p.B > 0) ts_combine_kernel<<<p.B, 256, 0, s>>>(p);

@@ -125,34 +125,43 @@ def test_tp_slice_is_a_restriction():
 
 # ------------------------------------------------------- token-sharded EP (f3)
 TS_B = 5          # tokens per rank
+NSEL = 2          # top_k of the tiny shape
 
 
 def _ts_worker(rank, world, port, out_dir):
-    """Each rank routes ITS tokens, sends every selection to the expert's owner
-    (all_to_all of fixed-capacity blocks), computes what it received, sends
-    the gate-weighted rows back and sums them per token."""
+    """Each rank routes ITS tokens, sends one row per (token, owner) with the
+    token's selections that owner holds (all_to_all of fixed-capacity blocks),
+    computes the rows it received, sends them back and sums them per token."""
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        H, k = SH.hidden, SH.top_k
-        C = TS_B * k
+        H = SH.hidden
+        C = TS_B
         x16 = sg.hidden_states(SH, 40 + rank, LAYER, batch=TS_B)
-        routes = rt.route(x16, sg.router_weights(SH, LAYER), k, 0.6, 0.9)
+        routes = rt.route(x16, sg.router_weights(SH, LAYER), SH.top_k, 0.6, 0.9)
         pos, sent = om.ts_dispatch_plan(routes, world, C)
         rows = np.zeros((world, C, H), dtype=np.float64)
-        meta = np.full((world, C, 4), -1.0)
+        meta = np.full((world, C, 2 + 3 * NSEL), -1.0)      # token, n, (e, d, g) x NSEL
         for q in range(world):
-            for j, (b, e, d, g) in enumerate(sent[q]):
+            for j, (b, sels) in enumerate(sent[q]):
                 rows[q, j] = x16[b].astype(np.float64)
-                meta[q, j] = (b, e, d, g)
-        rrows, rmeta = torch.empty(world * C * H, dtype=torch.float64), torch.empty(world * C * 4, dtype=torch.float64)
+                meta[q, j, :2] = (b, len(sels))
+                for i, (e, d, g) in enumerate(sels):
+                    meta[q, j, 2 + 3 * i:5 + 3 * i] = (e, d, g)
+        rrows = torch.empty(world * C * H, dtype=torch.float64)
+        rmeta = torch.empty(meta.size, dtype=torch.float64)
         dist.all_to_all_single(rrows, torch.from_numpy(rows.ravel()))
         dist.all_to_all_single(rmeta, torch.from_numpy(meta.ravel()))
         rrows = rrows.numpy().reshape(world * C, H)
-        rmeta = rmeta.numpy().reshape(world * C, 4)
+        rmeta = rmeta.numpy().reshape(world * C, 2 + 3 * NSEL)
         live = [j for j in range(world * C) if rmeta[j, 0] >= 0]
-        assert all(om.owner(int(rmeta[j, 1]), world) == rank for j in live)
-        recs = [(int(rmeta[j, 0]), int(rmeta[j, 1]), int(rmeta[j, 2]), rmeta[j, 3]) for j in live]
+        recs = []
+        for j in live:
+            n = int(rmeta[j, 1])
+            sels = [(int(rmeta[j, 2 + 3 * i]), int(rmeta[j, 3 + 3 * i]), rmeta[j, 4 + 3 * i])
+                    for i in range(n)]
+            assert all(om.owner(e, world) == rank for e, _, _ in sels)
+            recs.append((int(rmeta[j, 0]), sels))
         out = np.zeros((world * C, H))
         out[live] = om.ts_owner_rows(rrows[live].astype(np.float16), recs, _store(), LAYER,
                                      fm.F16, fm.Q4)
@@ -180,15 +189,16 @@ def test_token_sharded_gloo_equals_single_process(world):
 
 
 def test_ts_dispatch_plan_order_and_capacity():
-    """Slots per destination follow (token, rank) order; Skip sends nothing;
-    overflow raises."""
+    """One row per (token, owner), rows in token order per owner, selections in
+    rank order inside a row; Skip sends nothing; overflow raises."""
     R = rt.Route
     routes = [R(experts=[3, 0], gates=[0.7, 0.3], decisions=[rt.HIGH, rt.LOW], logits=None),
               R(experts=[1, 2], gates=[0.9, 0.1], decisions=[rt.HIGH, rt.SKIP], logits=None),
-              R(experts=[2, 1], gates=[0.6, 0.4], decisions=[rt.HIGH, rt.HIGH], logits=None)]
+              R(experts=[2, 0], gates=[0.6, 0.4], decisions=[rt.HIGH, rt.HIGH], logits=None)]
     pos, sent = om.ts_dispatch_plan(routes, 2, 4)
-    assert pos == [[4, 0], [5, -1], [1, 6]]
-    assert [s[:2] for s in sent[0]] == [(0, 0), (2, 2)]
-    assert [s[:2] for s in sent[1]] == [(0, 3), (1, 1), (2, 1)]
+    # owner 0 (even experts): token 0 (e0), token 2 (e2, e0); owner 1: token 0 (e3), token 1 (e1)
+    assert pos == [[4, 0], [5, -1], [1, 1]]
+    assert [(b, [e for e, _, _ in sels]) for b, sels in sent[0]] == [(0, [0]), (2, [2, 0])]
+    assert [(b, [e for e, _, _ in sels]) for b, sels in sent[1]] == [(0, [3]), (1, [1])]
     with pytest.raises(ValueError):
-        om.ts_dispatch_plan(routes, 1, 3)
+        om.ts_dispatch_plan(routes, 1, 2)

@@ -1,10 +1,11 @@
 """GPU parity of token-sharded expert parallelism (
 hb_config.token_sharded) through the C-ABI against the oracle.
 
-Each rank routes its own tokens (exact decisions), packs every non-skipped
-selection into the block of the expert's owner (e mod world), the owner runs
-its received rows as one batch through the K2 (GEMV) or K3 (tcgen05 GEMM)
-path, and the gate-weighted rows come back to be summed per token
+Each rank routes its own tokens (exact decisions), packs one row per (token,
+owner) -- x and the token's selections that owner holds -- into the owner's
+block (e mod world), the owner runs its received rows as one batch through the
+K2 (GEMV) or K3 (tcgen05 GEMM) path, and the gate-weighted rows come back to
+be summed per token
 (oracle: ts_dispatch_plan / ts_owner_rows / ts_combine, pinned by
 tests/test_ep_gloo.py against the single-process layer).
 
@@ -112,20 +113,25 @@ def test_ts_two_processes_staged(world, tmp_path):
                        start_method="spawn")
     sh = sg.TINY
     for B in (3, 24):
-        C = 2 * B
+        C = B                                   # one row per (token, owner)
         for l in range(2):
             for r in range(world):
                 x16 = sg.hidden_states(sh, 70 + r, l, batch=B)
                 y = np.load(tmp_path / f"y_{B}_{l}_{r}.npy")
                 _check_layer(y, x16, sh, l)
-                # the dispatched records = the oracle's plan
+                # the dispatched rows = the oracle's plan (hb_ts_meta: token, n,
+                # expert[8], prec[8] bytes, gate[8] = 20 words)
                 routes = rt.route(x16, sg.router_weights(sh, l), 2, 0.6, 0.9)
                 _, sent = om.ts_dispatch_plan(routes, world, C)
-                meta = np.load(tmp_path / f"meta_{B}_{l}_{r}.npy").view(np.int32).reshape(world, C, 4)
+                raw = np.load(tmp_path / f"meta_{B}_{l}_{r}.npy")
+                words = raw.view(np.int32).reshape(world, C, 20)
+                precs = raw.reshape(world, C, 80)[:, :, 40:48]
                 for q in range(world):
-                    got = [(int(m[0]), int(m[1]), int(m[2] & 0xff)) for m in meta[q] if m[0] >= 0]
-                    assert got == [(b, e, d) for b, e, d, _ in sent[q]], (B, l, r, q)
-                    assert all(m[0] == -1 for m in meta[q][len(sent[q]):])
+                    got = [(int(m[0]), [int(e) for e in m[2:2 + m[1]]], [int(d) for d in pp[:m[1]]])
+                           for m, pp in zip(words[q], precs[q]) if m[0] >= 0]
+                    want = [(b, [e for e, _, _ in sels], [d for _, d, _ in sels]) for b, sels in sent[q]]
+                    assert got == want, (B, l, r, q)
+                    assert all(m[0] == -1 for m in words[q][len(sent[q]):])
 
 
 def test_ts_nonfinite_row_and_all_skip_second_selection():
