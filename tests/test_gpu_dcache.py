@@ -229,3 +229,37 @@ def test_offload_capacity_error_is_loud(dc):
         torch.cuda.synchronize()
         ctx.events()                                   # device manager: reported here
     assert "HB_ECAPACITY" in str(ei.value)
+
+
+def test_dcache_expert_parallel_rank():
+    """The device cache manager on EP rank 1 of 2 (owns the odd experts):
+    events bit-exact with the oracle's cache of the same rank."""
+    sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
+    ch, cl, p = 3, 3, 1
+    ctx = _ctx(sh, fm.F16, fm.Q4, max_batch=1, cap_high=ch, cap_low=cl, lookahead_p=p,
+               device_cache=1, rank=1, world=2)
+    for l in range(sh.n_layers):
+        ctx.set_router(l, sg.router_weights(sh, l))
+        for (e, enc), b in gpu_blobs(sh, l, range(1, 8, 2), [fm.F16, fm.Q4]).items():
+            ctx.register_expert(l, e, enc, b.cpu().numpy())
+    store = OracleStore(sh)
+    ref = oc.ExpertCache(sh.n_layers, sh.n_experts, ch, cl, (1, 1, 1, 1), fm.F16, fm.Q4,
+                         rank=1, world=2)
+    xs = sg.correlated_states(sh, 6, 0.999, 0.5)
+    for t in range(6):
+        ctx.token_begin()
+        ref.token_begin()
+        for l in range(sh.n_layers):
+            x16 = xs[t, l][None, :]
+            x = torch.from_numpy(x16).cuda()
+            y = torch.empty(1, sh.hidden, dtype=torch.float32, device="cuda")
+            ctx.forward(l, x, y)
+            served = ref.forward(l, rt.route(x16, sg.router_weights(sh, l), 2, 0.6, 0.9)[0])
+            r, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9, fm.F16,
+                                fm.Q4, rank=1, world=2, served=[served])
+            torch.cuda.synchronize()
+            assert rel_err(y.cpu().numpy()[0], r[0])[0] <= TOL
+            ctx.prefetch(l, x)
+            ref.prefetch(l, _predict(sh, x16, l, p))
+    torch.cuda.synchronize()
+    assert ctx.events() == ref.events

@@ -125,3 +125,21 @@ def test_q2k_offload_events(dc):
     ev = ctx.events()
     assert ev == ref.events
     assert any(e[4] == fm.Q2K for e in ev)
+
+
+def test_q2k_phi_full_size():
+    """Phi shapes (F = 6400: W2 has 25 Q2K groups per row, K2b's unstaged-h path)."""
+    sh1 = sg.MoEShape("phi", 32, 16, 2, 4096, 6400, 1.8)
+    layer = 3
+    ctx = _resident(sh1, [layer], fm.F16, fm.Q2K)
+    store = OracleStore(sh1)
+    wg = sg.router_weights(sh1, layer)
+    lows = 0
+    for t in range(4):
+        x16 = sg.hidden_states(sh1, 300 + t, layer)
+        y = _run(ctx, layer, x16)
+        ref, routes = om.moe_layer(x16, wg, store, layer, 2, 0.6, 0.9, fm.F16, fm.Q2K)
+        _check_routes(ctx, routes, 1, 2)
+        lows += sum(d == rt.LOW for d in routes[0].decisions)
+        assert rel_err(y[0], ref[0])[0] <= TOL_Q2K
+    assert lows >= 1
