@@ -248,14 +248,16 @@ __device__ __forceinline__ void dequant(const uint4& v, int blk, uint32_t (&P)[4
     P[2] = prmt(v.y, v.w, 0x5410);
     P[3] = prmt(v.y, v.w, 0x7632);
   } else if constexpr (ENC == HB_Q8) {
-    // block j holds r0..3 in word 2j, r4..7 in word 2j+1; q+128 via xor
+    // block j holds r0..3 in word 2j, r4..7 in word 2j+1; q+128 via xor.
+    // Interleave once (u = r0 r4 r1 r5, w = r2 r6 r3 r7), then one PRMT with
+    // the 0x64 exponent bytes per pair: (1024 + q + 128) - 1152 = q exactly
     const uint32_t a = u4get(v, 2 * blk) ^ 0x80808080u;
     const uint32_t b = u4get(v, 2 * blk + 1) ^ 0x80808080u;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint32_t t = prmt(a, b, (uint32_t)(c | ((4 + c) << 8)));
-      P[c] = hsub2u(lop_magic<0x00FF00FFu>(t), kH1152);
-    }
+    const uint32_t u = prmt(a, b, 0x5140u), w = prmt(a, b, 0x7362u);
+    P[0] = hsub2u(prmt(u, 0x64646464u, 0x4140u), kH1152);
+    P[1] = hsub2u(prmt(u, 0x64646464u, 0x4342u), kH1152);
+    P[2] = hsub2u(prmt(w, 0x64646464u, 0x4140u), kH1152);
+    P[3] = hsub2u(prmt(w, 0x64646464u, 0x4342u), kH1152);
   } else if constexpr (ENC == HB_Q4) {
     const uint32_t w = u4get(v, blk);                     // nibble r = element 8t+r
     const uint32_t w8 = w >> 8;
