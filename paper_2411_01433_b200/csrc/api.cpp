@@ -174,6 +174,12 @@ struct hb_ctx {
   JobTable jt{};
   void* jt_dev = nullptr;
   void* jt_host = nullptr;                // pinned staging
+  // offload path, hits first: the misses' job table (same layout as jt)
+  JobTable jt2{};
+  void* jt2_dev = nullptr;
+  void* jt2_host = nullptr;
+  bool hit_first = true;                  // HB_HIT_FIRST=0: one K2 chain after every load
+  uint64_t split_fwds = 0;
   size_t jt_bytes = 0;
   int max_jobs = 0, max_slots = 0, max_vjobs = 0;
   float static_frac = 0.8f;               // GEMV work feed K2a (HB_STATIC_FRAC, HB_CHUNK)
@@ -361,7 +367,7 @@ static void free_ctx(hb_ctx* c) {
   cudaDeviceSynchronize();
   void* dptrs[] = {c->wg, c->dev_blob_table, c->pool_mem[0], c->pool_mem[1], c->dec, c->dec_pred,
                    c->logits, c->lbuf, c->x_perm, c->xsum, c->au, c->h_hi, c->h_lo,
-                   c->hsum, c->done, c->gctr, c->jt_dev, c->k3_xg, c->k3_hB, c->k3_tab, c->k3_tmap,
+                   c->hsum, c->done, c->gctr, c->jt_dev, c->jt2_dev, c->k3_xg, c->k3_hB, c->k3_tab, c->k3_tmap,
                    c->gbar, c->fwd_idx, c->stamps, c->x_save, c->wnorm, c->rowbad,
                    c->dc, c->host_blob_dev, c->dc_h.pool[0], c->dc_h.pool[1], c->dc_h.where[0],
                    c->dc_h.where[1], c->dc_h.R, c->dc_h.F, c->dc_h.H, c->dc_h.mask_exp,
@@ -376,6 +382,7 @@ static void free_ctx(hb_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_side) cudaEventDestroy(c->ev_side);
   if (c->jt_host) cudaFreeHost(c->jt_host);
+  if (c->jt2_host) cudaFreeHost(c->jt2_host);
   for (void* p : c->arena) cudaFreeHost(p);
   for (void* p : c->dev_owned) cudaFree(p);
   for (int i = 0; i < 2; ++i) {
@@ -556,6 +563,22 @@ int hb_create(const hb_config* cfg, int device, hb_ctx** out) {
   c->jt.vjobs = (VJobD*)(jb + o_vj);
   c->jt.vcum13 = (long long*)(jb + o_c13);
   c->jt.vcum2 = (long long*)(jb + o_c2);
+  if (!resident) {                           // the misses' table of a split offload forward
+    if (!dm(&c->jt2_dev, total) || cudaHostAlloc(&c->jt2_host, total, cudaHostAllocDefault) != cudaSuccess)
+      return bail(HB_ENOMEM, "job table allocation failed");
+    cudaMemset(c->jt2_dev, 0, total);
+    uint8_t* j2 = (uint8_t*)c->jt2_dev;
+    c->jt2.hdr = (int32_t*)j2;
+    c->jt2.jobs = (Job*)(j2 + o_jobs);
+    c->jt2.slot_token = (int32_t*)(j2 + o_tok);
+    c->jt2.slot_gate = (float*)(j2 + o_gate);
+    c->jt2.tok_slots = (int32_t*)(j2 + o_ts);
+    c->jt2.vjobs = (VJobD*)(j2 + o_vj);
+    c->jt2.vcum13 = (long long*)(j2 + o_c13);
+    c->jt2.vcum2 = (long long*)(j2 + o_c2);
+    const char* hf = std::getenv("HB_HIT_FIRST");
+    c->hit_first = !(hf && hf[0] == '0');
+  }
   if (cudaHostAlloc((void**)&c->dec_host, sizeof(hb_decision) * (1 + P) * B * K,
                     cudaHostAllocDefault) != cudaSuccess)
     return bail(HB_ENOMEM, "pinned decision buffer allocation failed");
@@ -1495,46 +1518,64 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
     if (served[i] != HB_ENC_NONE)
       if (int r2 = pf_settle(c, pool[i], slot[i], true)) return r2;
   if (int r2 = pf_top_up(c)) return r2;
-  // job table on the host: one job per non-skipped owned selection
-  uint8_t* jh = (uint8_t*)c->jt_host;
-  int32_t* hdr = (int32_t*)jh;
-  Job* jobs = (Job*)(jh + ((uint8_t*)c->jt.jobs - (uint8_t*)c->jt_dev));
-  int32_t* stok = (int32_t*)(jh + ((uint8_t*)c->jt.slot_token - (uint8_t*)c->jt_dev));
-  float* sgate = (float*)(jh + ((uint8_t*)c->jt.slot_gate - (uint8_t*)c->jt_dev));
-  int32_t* tslots = (int32_t*)(jh + ((uint8_t*)c->jt.tok_slots - (uint8_t*)c->jt_dev));
-  int nj = 0;
   for (int i = 0; i < K; ++i) {
     c->dec_host[i].served_enc = served[i];
     c->dec_host[i].hit = hit[i];
-    tslots[i] = served[i] == HB_ENC_NONE ? -1 : nj;
-    if (served[i] == HB_ENC_NONE) continue;
-    Job j;
-    j.blob = c->pool_mem[pool[i]] + (size_t)slot[i] * c->slot_bytes[pool[i]];
-    j.enc = served[i];
-    j.expert = ex[i];
-    j.n_tok = 1;
-    j.slot_off = nj;
-    jobs[nj] = j;
-    stok[nj] = 0;
-    sgate[nj] = c->dec_host[i].gate;
-    ++nj;
   }
-  hdr[0] = nj;
-  hdr[1] = nj;
-  hdr[2] = build_vjobs(jobs, nj, k.hidden, k.ffn,
-                       (VJobD*)(jh + ((uint8_t*)c->jt.vjobs - (uint8_t*)c->jt_dev)),
-                       (long long*)(jh + ((uint8_t*)c->jt.vcum13 - (uint8_t*)c->jt_dev)),
-                       (long long*)(jh + ((uint8_t*)c->jt.vcum2 - (uint8_t*)c->jt_dev)));
-  CUDA_TRY(c, cudaMemcpyAsync(c->jt_dev, c->jt_host, c->jt_bytes, cudaMemcpyHostToDevice, s));
+  // Hits compute while the misses load (improving on P:349's
+  // "waits for all"): when the layer has both, the hits' K2 chain runs
+  // first, waiting only on the hit slots; the misses' chain follows on their
+  // ready events and adds into the same y (its hfin leaves y alone).
+  bool any_hit = false, any_miss = false;
   for (int i = 0; i < K; ++i)
-    if (served[i] != HB_ENC_NONE)
-      CUDA_TRY(c, cudaStreamWaitEvent(s, c->slot_ready[pool[i]][slot[i]], 0));
-  GemvParams gp = gemv_params(c, batch, y, au_buf(c, cn));
-  launch_gemv(c, gp, s);
-  if (gp.clean) c->au_dirty[cn] = 0;
-  for (int i = 0; i < K; ++i)
-    if (served[i] != HB_ENC_NONE)
-      CUDA_TRY(c, cudaEventRecord(c->slot_free[pool[i]][slot[i]], s));
+    if (served[i] != HB_ENC_NONE) (hit[i] ? any_hit : any_miss) = true;
+  const bool split = c->hit_first && any_hit && any_miss;
+  c->split_fwds += split;
+  for (int part = 0; part < (split ? 2 : 1); ++part) {
+    auto in_part = [&](int i) {
+      return served[i] != HB_ENC_NONE && (!split || (part == 0) == (hit[i] != 0));
+    };
+    // job table on the host: one job per non-skipped selection of this part
+    void* tdev = part ? c->jt2_dev : c->jt_dev;
+    uint8_t* jh = (uint8_t*)(part ? c->jt2_host : c->jt_host);
+    auto at = [&](const void* p) { return jh + ((const uint8_t*)p - (const uint8_t*)c->jt_dev); };
+    int32_t* hdr = (int32_t*)jh;
+    Job* jobs = (Job*)at(c->jt.jobs);
+    int32_t* stok = (int32_t*)at(c->jt.slot_token);
+    float* sgate = (float*)at(c->jt.slot_gate);
+    int32_t* tslots = (int32_t*)at(c->jt.tok_slots);
+    int nj = 0;
+    for (int i = 0; i < K; ++i) {
+      tslots[i] = in_part(i) ? nj : -1;
+      if (!in_part(i)) continue;
+      Job j;
+      j.blob = c->pool_mem[pool[i]] + (size_t)slot[i] * c->slot_bytes[pool[i]];
+      j.enc = served[i];
+      j.expert = ex[i];
+      j.n_tok = 1;
+      j.slot_off = nj;
+      jobs[nj] = j;
+      stok[nj] = 0;
+      sgate[nj] = c->dec_host[i].gate;
+      ++nj;
+    }
+    hdr[0] = nj;
+    hdr[1] = nj;
+    hdr[2] = build_vjobs(jobs, nj, k.hidden, k.ffn, (VJobD*)at(c->jt.vjobs),
+                         (long long*)at(c->jt.vcum13), (long long*)at(c->jt.vcum2));
+    CUDA_TRY(c, cudaMemcpyAsync(tdev, jh, c->jt_bytes, cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < K; ++i)
+      if (in_part(i)) CUDA_TRY(c, cudaStreamWaitEvent(s, c->slot_ready[pool[i]][slot[i]], 0));
+    GemvParams gp = gemv_params(c, batch, y, au_buf(c, cn));
+    if (part) {
+      gp.jt = c->jt2;
+      gp.keep_y = 1;
+    }
+    launch_gemv(c, gp, s);
+    if (gp.clean) c->au_dirty[cn] = 0;
+    for (int i = 0; i < K; ++i)
+      if (in_part(i)) CUDA_TRY(c, cudaEventRecord(c->slot_free[pool[i]][slot[i]], s));
+  }
   c->last_host_decisions = true;
   CUDA_TRY(c, cudaGetLastError());
   return ep_reduce(c, y, batch, s);

@@ -1905,7 +1905,7 @@ __global__ void __launch_bounds__(256) hfin_kernel(const __grid_constant__ GemvP
   const int nb = p.F / 32;
   const int n = __ldcg(p.jt.hdr + 1) * nb * 4;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (rowbad || (p.clean && (int)blockIdx.x < p.B)) {
+  if (rowbad || (p.clean && !p.keep_y && (int)blockIdx.x < p.B)) {
     const float v = rowbad ? __int_as_float(0x7fc00000) : 0.f;
     for (int c = threadIdx.x; c < p.H; c += blockDim.x) p.y[(size_t)blockIdx.x * p.H + c] = v;
   }

@@ -169,6 +169,7 @@ struct GemvParams {
   int ctas;                            // K2a / K2b grid (<= kGemvCTAs)
   int clean;                           // hfin zeroes the K2a sums it read and the y rows (the
                                        // solo router zeroes nothing)
+  int keep_y;                          // hfin leaves y alone (second chain of a split forward)
   unsigned* gbar;                      // that grid barrier [count, generation] (self-resetting)
   // work feed: a static share of the units, then dynamic chunks (K2)
   unsigned* ctr;                       // chunk counters: [0] K2a, [1] K2b, [2 + q] K2a group q, [2 + 148 + q] K2b group q

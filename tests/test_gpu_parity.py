@@ -300,6 +300,43 @@ def test_offload_cache_events_and_outputs(p, dc):
     assert ctx.events() == ref_cache.events
 
 
+@pytest.mark.parametrize("hit_first", ["1", "0"])
+def test_offload_hits_compute_first(hit_first, monkeypatch):
+    """Host offload path, a layer with both hits and misses: the hits' K2
+    chain (K2a, hfin, K2b) runs first and the misses' chain adds into the same
+    y (3 more launches); y still equals the oracle with the served encodings,
+    events stay bit-exact.  HB_HIT_FIRST=0: one chain after every load."""
+    monkeypatch.setenv("HB_HIT_FIRST", hit_first)
+    sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
+    ch, cl = 6, 6
+    ctx, store = _offload_ctx(sh, ch, cl, 0)
+    ref_cache = oc.ExpertCache(sh.n_layers, sh.n_experts, ch, cl, (1, 1, 1, 1), fm.F16, fm.Q4)
+    xs = sg.correlated_states(sh, 10, 0.999, 0.5)
+    deltas = {False: set(), True: set()}
+    for t in range(10):
+        ctx.token_begin()
+        ref_cache.token_begin()
+        for l in range(sh.n_layers):
+            x16 = xs[t, l][None, :]
+            n0 = ctx.launch_count()
+            y = _run(ctx, l, x16)
+            n1 = ctx.launch_count()
+            route = rt.route(x16, sg.router_weights(sh, l), 2, 0.6, 0.9)[0]
+            served = ref_cache.forward(l, route)
+            ref, _ = om.moe_layer(x16, sg.router_weights(sh, l), store, l, 2, 0.6, 0.9,
+                                  fm.F16, fm.Q4, served=[served])
+            assert rel_err(y[0], ref[0])[0] <= TOL
+            d = [v for v in ctx.decisions(1) if v.served_enc != 255]
+            mixed = any(v.hit for v in d) and any(not v.hit for v in d)
+            deltas[mixed].add(n1 - n0)
+    torch.cuda.synchronize()
+    assert ctx.events() == ref_cache.events
+    assert deltas[True], "the trace must have a layer with both a hit and a miss"
+    assert len(deltas[False]) == 1 and len(deltas[True]) == 1
+    extra = next(iter(deltas[True])) - next(iter(deltas[False]))
+    assert extra == (3 if hit_first == "1" else 0)
+
+
 @pytest.mark.parametrize("dc", [0, 1])
 def test_offload_explicit_load_and_reset(dc):
     sh = sg.MoEShape("tiny4", 4, 8, 2, 256, 512, 1.5)
