@@ -64,6 +64,6 @@ def rel_err(y, ref):
     ref = np.asarray(ref, dtype=np.float64)
     nw = np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-300)
     rms = np.sqrt((ref ** 2).mean()) if ref.size else 0.0
-    sel = np.abs(ref) >= 0.1 * rms
+    sel = (np.abs(ref) >= 0.1 * rms) & (np.abs(ref) > 0)      # an all-zero row has no relative error
     el = (np.abs(y - ref)[sel] / np.abs(ref)[sel]).max() if sel.any() else 0.0
     return nw, el
