@@ -33,6 +33,8 @@
 //  * Weights are dequantised to fp16 (one rounding of d*q, d*q+m) because the
 //    tensor core accumulates across blocks; h is rounded to fp16 for K3b
 //    (R26).  Accumulation is fp32 in TMEM.
+#include <type_traits>
+
 #include "hb_internal.h"
 #include "k3.h"
 
@@ -570,12 +572,13 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
     const int tl = row >> 4, rr = row & 15;
     int rs = 0, cs = 0, ntc = 0, ntr = 0;
     uint32_t rph = 0, cph = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const Item I = item_of<NMAT>(p, it, v0);
-      const int enc = I.v->enc;
-      const int epg = epg_of_enc(enc), ru = raw_units<NMAT>(enc, Kitem);
-      const bool q2k = p.kq && enc == HB_Q2;
-      const int sb = q2k ? 20 : scale_rec(enc);
+    // one item's raw slots, the encoding a compile-time constant (EK: 4 = Q2K)
+    auto conv_item = [&](auto ek) {
+      constexpr int EK = decltype(ek)::value;
+      constexpr int ENC = EK == 4 ? HB_Q2 : EK;
+      constexpr int epg = ENC == HB_Q8 ? 64 : ENC == HB_Q4 ? 128 : 256;
+      constexpr int sb = EK == 4 ? 20 : ENC == HB_Q8 ? 4 : ENC == HB_Q4 ? 8 : 32;
+      const int ru = raw_units<NMAT>(ENC, Kitem);
       const int nraw = Kitem / (ru * epg);
       const int cpr = ru * epg / kBK;               // canonical stages per raw slot
       for (int r = 0; r < nraw; ++r) {
@@ -585,9 +588,9 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
         const uint32_t raw = sbase + rs * kRawBytes;
         for (int c = 0; c < cpr; ++c) {
           // step-uniform offsets inside the raw slot (oracle/formats.py layout)
-          const int u = enc == HB_Q8 ? c : enc == HB_Q4 ? (c >> 1) : (c >> 2);
-          const int coff = enc == HB_Q8 ? 0 : enc == HB_Q4 ? 8 * (c & 1) : 4 * (c & 3);
-          const int soff = enc == HB_Q8 ? 0 : enc == HB_Q4 ? 4 * (c & 1) : 4 * (c & 3);
+          const int u = ENC == HB_Q8 ? c : ENC == HB_Q4 ? (c >> 1) : (c >> 2);
+          const int coff = ENC == HB_Q8 ? 0 : ENC == HB_Q4 ? 8 * (c & 1) : 4 * (c & 3);
+          const int soff = ENC == HB_Q8 ? 0 : ENC == HB_Q4 ? 4 * (c & 1) : 4 * (c & 3);
           // dequantise into registers first (the raw slot is ready), then wait
           // for the A stage: the ALU chain overlaps the MMA of older stages
           uint4 w[NMAT][2];
@@ -596,8 +599,8 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
             const int su = u * 8 + tl;                // raw slot [m][u][tile]
             const uint32_t code = raw + m * (8 * ru * 1024) + su * 1024 + rr * 64 + 16 * t + coff;
             const uint32_t sc = raw + kRawCode + m * (8 * ru * 16 * sb) + su * 16 * sb + rr * sb;
-            if (q2k) dequant16_q2k(code, sc, 2 * (c & 3), t, w[m][0], w[m][1]);
-            else dequant16(enc, code, sc + soff, w[m][0], w[m][1]);
+            if constexpr (EK == 4) dequant16_q2k(code, sc, 2 * (c & 3), t, w[m][0], w[m][1]);
+            else dequant16(ENC, code, sc + soff, w[m][0], w[m][1]);
           }
           if (lane == 0) bar_wait(can_empty(cs), cph ^ 1);
           __syncwarp();
@@ -636,6 +639,14 @@ __global__ void __launch_bounds__(kThreads, 1) k3_kernel(K3Params p) {
         if (lane == 0) bar_arrive(raw_empty(rs));
         if (++rs == R) { rs = 0; rph ^= 1; }
       }
+    };
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item I = item_of<NMAT>(p, it, v0);
+      const int enc = I.v->enc;
+      if (enc == HB_Q4) conv_item(std::integral_constant<int, HB_Q4>{});
+      else if (enc == HB_Q8) conv_item(std::integral_constant<int, HB_Q8>{});
+      else if (p.kq) conv_item(std::integral_constant<int, 4>{});
+      else conv_item(std::integral_constant<int, HB_Q2>{});
     }
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
