@@ -234,60 +234,24 @@ __device__ __forceinline__ __half2 bcast(uint16_t h) {
   return u2h((uint32_t)h | ((uint32_t)h << 16));
 }
 
-// 8 consecutive K elements of one row, dequantised to fp16 (element order).
-// code: shared address of the row's 64-byte piece of the unit; sc: its scale
-// record; e: K offset inside the group (multiple of 8).  Layout formulas:
-// oracle/formats.py docstring (the definition; tests/golden pins it).
-__device__ __forceinline__ uint4 dequant8(int enc, uint32_t code, uint32_t sc, int e) {
-  const int j = e >> 5, t = (e & 31) >> 3;
-  if (enc == HB_F16) return lds128(code + 2 * e);
-  const __half2 d = bcast(lds16(sc + 2 * j));
-  uint4 o;
-  if (enc == HB_Q4) {
-    // nibble i = element i; (1024 + q) via the 0x6400 exponent, - 1032 exact
-    const uint32_t v = lds32(code + 16 * t + 4 * j);
-    const uint32_t A = v & 0x0F0F0F0Fu, B = (v >> 4) & 0x0F0F0F0Fu;
-    const __half2 off = u2h(0x64086408u);                  // (1032, 1032)
-    o.x = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0400), 0x00FF00FFu, 0x64006400u)), off), d));
-    o.y = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0501), 0x00FF00FFu, 0x64006400u)), off), d));
-    o.z = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0602), 0x00FF00FFu, 0x64006400u)), off), d));
-    o.w = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0703), 0x00FF00FFu, 0x64006400u)), off), d));
-  } else if (enc == HB_Q8) {
-    // int8 ^ 0x80 = q + 128 in [1, 255]: (1024 + q + 128) - 1152 exact
-    const uint32_t a = lds32(code + 16 * t + 8 * j) ^ 0x80808080u;
-    const uint32_t b = lds32(code + 16 * t + 8 * j + 4) ^ 0x80808080u;
-    const uint32_t M = 0x64646464u;
-    const __half2 off = u2h(0x64806480u);                  // (1152, 1152)
-    o.x = h2u(__hmul2(__hsub2(u2h(prmt(a, M, 0x5150)), off), d));
-    o.y = h2u(__hmul2(__hsub2(u2h(prmt(a, M, 0x5352)), off), d));
-    o.z = h2u(__hmul2(__hsub2(u2h(prmt(b, M, 0x5150)), off), d));
-    o.w = h2u(__hmul2(__hsub2(u2h(prmt(b, M, 0x5352)), off), d));
-  } else {  // HB_Q2: w = d*q + m; elements 0-3 in byte c0, 4-7 in byte c0 + 2
-    const __half2 m = bcast(lds16(sc + 16 + 2 * j));
-    const uint32_t v = lds32(code + 16 * t + 4 * (j >> 1));
-    const uint32_t s0 = (j & 1) ? 0x0101u : 0u;             // byte (j%2) into bytes 0 and 2
-    const uint32_t c0 = prmt(v, 0, 0x4040u + s0), c1 = prmt(v, 0, 0x4242u + s0);
-    // (q0 bits 0-1 | q1 bits 18-19) and (q2 bits 4-5 | q3 bits 22-23), magic 0x6400
-    const __half2 n01 = u2h(0x34003C00u), b01 = u2h(0xDC00E400u);  // (1, 1/4), (-1024, -256)
-    const __half2 n23 = u2h(0x24002C00u), b23 = u2h(0xCC00D400u);  // (1/16, 1/64), (-64, -16)
-    o.x = h2u(__hfma2(__hfma2(u2h(and_or(c0, 0x000C0003u, 0x64006400u)), n01, b01), d, m));
-    o.y = h2u(__hfma2(__hfma2(u2h(and_or(c0, 0x00C00030u, 0x64006400u)), n23, b23), d, m));
-    o.z = h2u(__hfma2(__hfma2(u2h(and_or(c1, 0x000C0003u, 0x64006400u)), n01, b01), d, m));
-    o.w = h2u(__hfma2(__hfma2(u2h(and_or(c1, 0x00C00030u, 0x64006400u)), n23, b23), d, m));
-  }
-  return o;
-}
 
-__device__ __forceinline__ uint4 q4_chunk(uint32_t v, __half2 d) {
-  const uint32_t A = v & 0x0F0F0F0Fu, B = (v >> 4) & 0x0F0F0F0Fu;
-  const __half2 off = u2h(0x64086408u);                    // (1032, 1032)
+// Q4 K chunks are consumed in the pair-permuted K order (0 4 1 5 2 6 3 7)
+// within each 8-element chunk; the B operand of Q4 vjob3 (X gather, K3a's h
+// epilogue) is stored in the same order, so the dot products are unchanged.
+// Nibble r = element r: (e0, e4) and (e2, e6) are the low nibbles of the
+// half-words of v and v >> 8, (e1, e5) and (e3, e7) the high ones (x16).
+__device__ __forceinline__ uint4 q4_chunk_perm(uint32_t v, __half2 d) {
+  const uint32_t v8 = v >> 8;
+  const __half2 off = u2h(0x64086408u), inv16 = u2h(0x2C002C00u), m72 = u2h(0xD480D480u);
   uint4 o;
-  o.x = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0400), 0x00FF00FFu, 0x64006400u)), off), d));
-  o.y = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0501), 0x00FF00FFu, 0x64006400u)), off), d));
-  o.z = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0602), 0x00FF00FFu, 0x64006400u)), off), d));
-  o.w = h2u(__hmul2(__hsub2(u2h(and_or(prmt(A, B, 0x0703), 0x00FF00FFu, 0x64006400u)), off), d));
+  o.x = h2u(__hmul2(__hsub2(u2h(and_or(v, 0x000F000Fu, 0x64006400u)), off), d));
+  o.y = h2u(__hmul2(__hfma2(u2h(and_or(v, 0x00F000F0u, 0x64006400u)), inv16, m72), d));
+  o.z = h2u(__hmul2(__hsub2(u2h(and_or(v8, 0x000F000Fu, 0x64006400u)), off), d));
+  o.w = h2u(__hmul2(__hfma2(u2h(and_or(v8, 0x00F000F0u, 0x64006400u)), inv16, m72), d));
   return o;
 }
+// position of element j (0..7) of a chunk in that order
+__device__ __forceinline__ int q4_perm_pos(int j) { return ((j & 3) << 1) | (j >> 2); }
 __device__ __forceinline__ uint4 q8_chunk(uint32_t a, uint32_t b, __half2 d) {
   a ^= 0x80808080u;
   b ^= 0x80808080u;
@@ -323,8 +287,8 @@ __device__ __forceinline__ void dequant16(int enc, uint32_t code, uint32_t sc, u
   const __half2 d0 = u2h(prmt(dd, 0, 0x1010)), d1 = u2h(prmt(dd, 0, 0x3232));
   if (enc == HB_Q4) {
     const uint2 v = lds64(code);
-    w0 = q4_chunk(v.x, d0);
-    w1 = q4_chunk(v.y, d1);
+    w0 = q4_chunk_perm(v.x, d0);
+    w1 = q4_chunk_perm(v.y, d1);
   } else if (enc == HB_Q8) {
     const uint4 v = lds128(code);
     w0 = q8_chunk(v.x, v.y, d0);
@@ -400,8 +364,9 @@ __device__ __forceinline__ void epilogue_item(const K3Params& p, const Item& I, 
       tmem_ld16(tacc + n0, a);
       tmem_ld16(tacc + ms + n0, uu);
       // h (fp16) into hB in K3b's canonical B layout: K index = row (of F)
+      const int j = I.v->enc == HB_Q4 ? q4_perm_pos(row & 7) : (row & 7);
       __half* hb = p.hB + I.v->hoff + (size_t)(row >> 6) * np * kBK +
-                   ((row & 63) >> 3) * 64 + (row & 7);
+                   ((row & 63) >> 3) * 64 + j;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int n = n0 + i;
@@ -898,6 +863,9 @@ __global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* 
       if (n < v.n) {
         const int tok = p.jt.slot_token[v.slot0 + n];
         val = *reinterpret_cast<const uint4*>(x + (size_t)tok * p.H + ks * kBK + kc * 8);
+        if (v.enc == HB_Q4)                          // the Q4 converters' K order
+          val = make_uint4(prmt(val.x, val.z, 0x5410), prmt(val.x, val.z, 0x7632),
+                           prmt(val.y, val.w, 0x5410), prmt(val.y, val.w, 0x7632));
       }
       dst[c] = val;
     }
