@@ -10,7 +10,7 @@
 // M_e = B*k/E makes these real dense contractions.
 //
 // Design ("K3"):
-//  * vjob3 = <= 128 tokens of one job (MMA N = np = round-up-16 of the count).
+//  * vjob3 = <= 128 tokens of one job (F16: <= 256; MMA N = np = round-up-16 of the count).
 //    k3_prep (one launch) builds the vjob3 table from the router's job table
 //    and gathers X of every vjob3 into xg in the UMMA canonical K-major layout
 //    (8x8 core matrices, 16-byte rows), so each K3a stage gets X with ONE bulk
@@ -694,17 +694,28 @@ constexpr int d_smem() { return d_slots<NMAT>() * d_slot_bytes<NMAT>() + 1024 + 
 
 template <int NMAT>
 __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
-  constexpr int S = d_slots<NMAT>(), SB = d_slot_bytes<NMAT>();
+  constexpr int SMAX = d_slots<NMAT>(), RING = SMAX * d_slot_bytes<NMAT>();
   extern __shared__ uint8_t smd[];
   const uint32_t raw0 = su32(smd);
   const uint32_t sbase = (raw0 + 1023) & ~1023u;            // swizzle atoms: 1 KB aligned
-  const uint32_t bars = sbase + S * SB;
+  const uint32_t bars = sbase + RING;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto full = [&](int i) { return bars + 8 * i; };
-  auto empty = [&](int i) { return bars + 8 * (S + i); };
-  auto tm_full = [&](int i) { return bars + 8 * (2 * S + i); };
-  auto tm_empty = [&](int i) { return bars + 8 * (2 * S + 2 + i); };
-  const uint32_t tslot = bars + 8 * (2 * S + 4);
+  auto empty = [&](int i) { return bars + 8 * (SMAX + i); };
+  auto tm_full = [&](int i) { return bars + 8 * (2 * SMAX + i); };
+  auto tm_empty = [&](int i) { return bars + 8 * (2 * SMAX + 2 + i); };
+  const uint32_t tslot = bars + 8 * (2 * SMAX + 4);
+  // geometry from the largest F16 vjob3 of this launch (np <= 256): stage =
+  // A tiles + that B tile; accumulators of MSd columns per matrix, two
+  // buffers when they fit in TMEM (np > 128 at NMAT = 2: one buffer)
+  const int nv = p.tab->n16;
+  int npmax = 16;
+  for (int v = 0; v < nv; ++v) npmax = max(npmax, p.tab->v[v].np);
+  const int MSd = npmax <= 128 ? 128 : 256;
+  const uint32_t bufc = (uint32_t)(NMAT * MSd);
+  const int nbuf = 2 * bufc <= 512 ? 2 : 1;
+  const int SB = NMAT * kAMat + npmax * kBK * 2;
+  const int S = min(SMAX, RING / SB);
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       bar_init(full(i), 1);
@@ -727,7 +738,6 @@ __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
   uint32_t tbase;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tbase) : "r"(tslot));
 
-  const int nv = p.tab->n16;
   const int per_v = NMAT == 2 ? p.F / kRows : (p.H / kRows) * p.ks;
   const int n_items = nv * per_v;
   const int Kitem = NMAT == 2 ? p.H : p.F / p.ks;
@@ -765,7 +775,7 @@ __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
         const uint32_t idesc = idesc_f16(I.v->np);
         bar_wait(tm_empty(ab), abph ^ 1);
         tc_fence_after();
-        const uint32_t tacc = tbase + ab * 256;
+        const uint32_t tacc = tbase + ab * bufc;
         for (int s = 0; s < nsteps; ++s) {
           bar_wait(full(cs), cph);
           tc_fence_after();
@@ -774,13 +784,13 @@ __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
           for (int m = 0; m < NMAT; ++m)
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
-              umma(tacc + m * 128, sdesc_sw64(st + m * kAMat + (kk >> 1) * 8192 + (kk & 1) * 32),
+              umma(tacc + m * MSd, sdesc_sw64(st + m * kAMat + (kk >> 1) * 8192 + (kk & 1) * 32),
                    sdesc(st + NMAT * kAMat + kk * 256), idesc, (s | kk) ? 1u : 0u);
           umma_commit(empty(cs));
           if (++cs == S) { cs = 0; cph ^= 1; }
         }
         umma_commit(tm_full(ab));
-        if (++ab == 2) { ab = 0; abph ^= 1; }
+        if (++ab == nbuf) { ab = 0; abph ^= 1; }
       }
     }
   } else if (warp >= 4) {
@@ -791,11 +801,11 @@ __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
       const Item I = item_of<NMAT>(p, it, 0);
       bar_wait(tm_full(ab), abph);
       tc_fence_after();
-      epilogue_item<NMAT>(p, I, tbase + ((uint32_t)(q4 * 32) << 16) + ab * 256, q4, lane);
+      epilogue_item<NMAT>(p, I, tbase + ((uint32_t)(q4 * 32) << 16) + ab * bufc, q4, lane, MSd);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(tm_empty(ab));
-      if (++ab == 2) { ab = 0; abph ^= 1; }
+      if (++ab == nbuf) { ab = 0; abph ^= 1; }
     }
   }
   tc_fence_before();
@@ -824,14 +834,15 @@ __global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* 
     for (int j = 0; j < nj; ++j) {
       const Job J = p.jt.jobs[j];
       if ((J.enc == HB_F16) != (pass == 0)) continue;
-      for (int s = 0; s < J.n_tok && n < kK3MaxV3; s += kK3MaxN) {
+      const int cap = J.enc == HB_F16 ? kK3MaxNF16 : kK3MaxN;
+      for (int s = 0; s < J.n_tok && n < kK3MaxV3; s += cap) {
         V3 v;
         v.blob = J.blob;
         v.enc = J.enc;
         v.expert = J.expert;
         n16 += pass == 0;
         v.slot0 = J.slot_off + s;
-        v.n = J.n_tok - s < kK3MaxN ? J.n_tok - s : kK3MaxN;
+        v.n = J.n_tok - s < cap ? J.n_tok - s : cap;
         v.np = (v.n + 15) & ~15;
         v.xoff = xo;
         v.hoff = ho;

@@ -8,6 +8,8 @@
 namespace hb {
 
 constexpr int kK3MaxN = 128;    // tokens per vjob3 (MMA N, two TMEM accumulators per buffer)
+constexpr int kK3MaxNF16 = 256; // F16 vjob3 (k3d_kernel): up to MMA N = 256, so an expert's weights
+                                // stream once for up to 256 tokens
 constexpr int kK3MaxV3 = 64;    // vjob3 entries per forward
 
 // <= 128 token slots of one job; np = count rounded up to 16 (MMA N)

@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--model", default="mixtral")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--strict", type=int, default=1,
+                    help="0: SURVEY C5's rule (R27, allow the F16 copy for Low requests)")
     ap.add_argument("--paths", default="k2,k3",
                     help="k2 (GEMV), k3 (tcgen05 GEMM), ts (token-sharded EP at world 1)")
     args = ap.parse_args()
@@ -45,7 +47,7 @@ def main():
     L, Hd, F = args.layers, shape.hidden, shape.ffn
     torch.cuda.set_device(0)
     ctx, blobs = bench.build_model(h, sg, None, shape, hi, lo, 0, 1, 0, max_batch=max(batches),
-                                   layers=L)
+                                   layers=L, cfg_extra=None if args.strict else {"strict": 0})
     ctx_ts = None
     if "ts" in args.paths.split(","):
         # token-sharded EP context at world 1: dispatch into the
