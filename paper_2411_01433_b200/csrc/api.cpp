@@ -1462,6 +1462,7 @@ int moe_layer_forward(hb_ctx* c, int layer, const void* x, int batch, void* y, v
       return ep_reduce(c, y, batch, s);
     }
     if (k3) rp.zero_n[0] = 0;                          // K3 does not use the K2a sums
+    rp.no_vjobs = k3;                                  // ... nor the GEMV vjob table
     const int cn = k3 ? 0 : legacy_au(c, rp, batch);
     launch_router(rp, s);
     c->launches += 1;

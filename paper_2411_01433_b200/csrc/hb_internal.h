@@ -126,6 +126,7 @@ struct RouterParams {
   double t1, t2;                       // k > 2 fp64 test
   int rank, world;
   int strict;                          // 0: Low served by hi_enc when the expert is touched High (R27)
+  int no_vjobs;                        // the forward runs K3 (own vjob3 table): skip the GEMV vjob table
   hb_decision* dec;                    // [n_route][B][k]
   long long* lbuf;                     // [n_route][B][E][2] exact logits (scratch)
   int* rowbad;                         // [n_route][B] non-finite x flags (scratch)

@@ -324,7 +324,7 @@ __device__ void build_jobs(const RouterParams& p, RouterSmem& sm, const hb_decis
   }
   p.jt.hdr[0] = nj;
   p.jt.hdr[1] = off;
-  p.jt.hdr[2] = build_vjobs(sm.jobs, nj, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
+  p.jt.hdr[2] = p.no_vjobs ? 0 : build_vjobs(sm.jobs, nj, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
 }
 
 // build_jobs for batches, by the whole (last) CTA: per-key counts with shared
@@ -401,7 +401,8 @@ __device__ void build_jobs_cta(const RouterParams& p, SmemT& sm, const hb_decisi
       __syncwarp();
     }
     if (lane == 0)
-      p.jt.hdr[2] = build_vjobs(sm.jobs, sm.last, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
+      p.jt.hdr[2] = p.no_vjobs ? 0
+                                : build_vjobs(sm.jobs, sm.last, p.H, p.F, p.jt.vjobs, p.jt.vcum13, p.jt.vcum2);
   }
 }
 
