@@ -820,19 +820,24 @@ __global__ void __launch_bounds__(kDThreads, 1) k3d_kernel(K3Params p) {
 // memory; CTA 0 publishes it) + gather of X into xg (canonical B layout).
 __global__ void __launch_bounds__(256) k3_prep_kernel(K3Params p, const __half* __restrict__ x) {
   __shared__ V3 tab[kK3MaxV3];
+  __shared__ Job sjobs[2 * 64 + 1];
   __shared__ int s_n;
   // R28: NaN rows of y for tokens whose x had a non-finite element
   for (int b = blockIdx.x; b < p.B; b += gridDim.x)
     if (__ldcg(p.rowbad + b))
       for (int i = threadIdx.x; i < p.H; i += blockDim.x) p.y[(size_t)b * p.H + i] = __int_as_float(0x7fc00000);
+  // the router's jobs into shared memory once (the serial table walk below
+  // then reads no global memory)
+  const int nj = min(__ldcg(p.jt.hdr), 2 * 64 + 1);
+  for (int j = threadIdx.x; j < nj; j += blockDim.x) sjobs[j] = p.jt.jobs[j];
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const int nj = p.jt.hdr[0];
     int n = 0, n16 = 0;
     long long xo = 0, ho = 0;
     // F16 jobs first (k3d_kernel: TMA straight into the MMA layout), then the rest
     for (int pass = 0; pass < 2; ++pass)
     for (int j = 0; j < nj; ++j) {
-      const Job J = p.jt.jobs[j];
+      const Job J = sjobs[j];
       if ((J.enc == HB_F16) != (pass == 0)) continue;
       const int cap = J.enc == HB_F16 ? kK3MaxNF16 : kK3MaxN;
       for (int s = 0; s < J.n_tok && n < kK3MaxV3; s += cap) {

@@ -6,4 +6,4 @@ import json,sys
 for l in sys.stdin:
     d=json.loads(l); print('strict=$st', {k: d.get(k) for k in ('B','tok_s','ms_per_step','step_gbs')})"
 done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"router|prep" -c 40 --csv --log-file gpurun_out/rtr2_512.csv python tools/bench_batched.py --batches 512 --paths k3 --layers 1 --steps 2 --warmup 1 --strict 0 > gpurun_out/rtr2_512.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"router|prep" -c 40 --csv --log-file gpurun_out/rtr3_512.csv python tools/bench_batched.py --batches 512 --paths k3 --layers 1 --steps 2 --warmup 1 --strict 0 > gpurun_out/rtr3_512.log 2>&1
